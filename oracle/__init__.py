@@ -1,0 +1,179 @@
+"""Plain CPU oracle for the sliding-window-sum hot path (arXiv 2305.16513).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  The product package ``paper_2305_16513_b200`` never imports it and
+shares no code with it.
+
+This module is argument marshalling (numpy <-> ctypes) around ``oracle.c``;
+all arithmetic is in ``oracle.c``, each routine citing the PAPER.md passage it
+writes out (Eq. 3, Sec. 2.3, Eq. 4-9, Sec. 2.5, Conclusion).  Pins that tie
+the oracle to the paper and to mathematics, not to itself, live in
+``tests/test_oracle_pins.py``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_SO = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+POOL2D_MAX = 0
+POOL2D_AVG = 1
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c with gcc (-O2, IEEE, no fast-math) into liboracle.so."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
+        os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))
+    ):
+        tmp = _SO + f".tmp{os.getpid()}"
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fno-fast-math",
+             "-ffp-contract=off", "-o", tmp, _SRC, "-lm"]
+        )
+        os.replace(tmp, _SO)
+    return _SO
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = ctypes.CDLL(_SO)
+            i64, vp, dp = ctypes.c_int64, ctypes.c_void_p, ctypes.c_double
+            L.oracle_out_len.argtypes = [i64, i64, i64]
+            L.oracle_out_len.restype = i64
+            for name in ("oracle_pool_sum_i32", "oracle_pool_max_i32", "oracle_pool_max_f32"):
+                getattr(L, name).argtypes = [vp, i64, i64, i64, i64, vp]
+                getattr(L, name).restype = ctypes.c_int
+            L.oracle_pool_sum_f32.argtypes = [vp, i64, i64, i64, i64, vp, vp]
+            L.oracle_pool_sum_f32.restype = ctypes.c_int
+            L.oracle_conv1d_f32.argtypes = [vp, i64, i64, vp, i64, i64, vp, vp]
+            L.oracle_conv1d_f32.restype = ctypes.c_int
+            L.oracle_pool2d_f32.argtypes = [vp, i64, i64, i64, i64, i64, i64, i64,
+                                            ctypes.c_int, vp, vp]
+            L.oracle_pool2d_f32.restype = ctypes.c_int
+            L.oracle_gamma_combine.argtypes = [dp, dp, dp, dp, vp, vp]
+            L.oracle_gamma_combine.restype = None
+            L.oracle_gamma_sequence.argtypes = [vp, vp, i64, vp, vp]
+            L.oracle_gamma_sequence.restype = ctypes.c_int
+            L.oracle_gamma_dot.argtypes = [vp, vp, i64, vp]
+            L.oracle_gamma_dot.restype = dp
+            _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _rows(x: np.ndarray):
+    x = np.ascontiguousarray(x)
+    if x.ndim == 1:
+        return x, x.shape[0], 1
+    assert x.ndim == 2
+    return x, x.shape[1], x.shape[0]
+
+
+def out_len(N: int, w: int, s: int = 1) -> int:
+    return int(lib().oracle_out_len(N, w, s))
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise ValueError("oracle rejected its arguments")
+
+
+def pool_sum(x: np.ndarray, w: int, s: int = 1):
+    """Eq. 3 with + .  int32 -> exact int64 sums; float32 -> (double sums, absmag)."""
+    x, N, B = _rows(x)
+    L = out_len(N, w, s)
+    if L < 0:
+        raise ValueError("window exceeds input")
+    if x.dtype == np.int32:
+        y = np.empty((B, L), np.int64)
+        _check(lib().oracle_pool_sum_i32(_p(x), N, B, w, s, _p(y)))
+        return y if x.ndim == 2 else y[0]
+    assert x.dtype == np.float32
+    y = np.empty((B, L), np.float64)
+    m = np.empty((B, L), np.float64)
+    _check(lib().oracle_pool_sum_f32(_p(x), N, B, w, s, _p(y), _p(m)))
+    return (y, m) if x.ndim == 2 else (y[0], m[0])
+
+
+def pool_max(x: np.ndarray, w: int, s: int = 1) -> np.ndarray:
+    """Eq. 3 with max (Sec. 2.3); exact, same dtype as x."""
+    x, N, B = _rows(x)
+    L = out_len(N, w, s)
+    if L < 0:
+        raise ValueError("window exceeds input")
+    y = np.empty((B, L), x.dtype)
+    fn = {np.dtype(np.int32): lib().oracle_pool_max_i32,
+          np.dtype(np.float32): lib().oracle_pool_max_f32}[x.dtype]
+    _check(fn(_p(x), N, B, w, s, _p(y)))
+    return y if x.ndim == 2 else y[0]
+
+
+def conv1d(x: np.ndarray, f: np.ndarray, s: int = 1):
+    """Sec. 2.5 sliding dot product (cross-correlation); returns (y double, absmag)."""
+    x, N, B = _rows(x)
+    f = np.ascontiguousarray(f, np.float32)
+    k = f.shape[0]
+    L = out_len(N, k, s)
+    if L < 0:
+        raise ValueError("window exceeds input")
+    y = np.empty((B, L), np.float64)
+    m = np.empty((B, L), np.float64)
+    _check(lib().oracle_conv1d_f32(_p(x), N, B, _p(f), k, s, _p(y), _p(m)))
+    return (y, m) if x.ndim == 2 else (y[0], m[0])
+
+
+def pool2d(x: np.ndarray, kh: int, kw: int, sh: int, sw: int, mode: int):
+    """Direct 2-D window pooling on [planes, H, W]; returns (y double, absmag)."""
+    x = np.ascontiguousarray(x, np.float32)
+    P, H, W = x.shape
+    OH, OW = out_len(H, kh, sh), out_len(W, kw, sw)
+    if OH < 0 or OW < 0:
+        raise ValueError("window exceeds input")
+    y = np.empty((P, OH, OW), np.float64)
+    m = np.empty((P, OH, OW), np.float64)
+    _check(lib().oracle_pool2d_f32(_p(x), P, H, W, kh, kw, sh, sw, mode, _p(y), _p(m)))
+    return y, m
+
+
+def gamma_combine(gi, gj):
+    """Eq. 8."""
+    u = ctypes.c_double()
+    v = ctypes.c_double()
+    lib().oracle_gamma_combine(gi[0], gi[1], gj[0], gj[1], ctypes.byref(u), ctypes.byref(v))
+    return (u.value, v.value)
+
+
+def gamma_sequence(a: np.ndarray, b: np.ndarray):
+    """Eq. 5 + Eq. 7: the M+1 pairs (u, v)."""
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    M = a.shape[0]
+    u = np.empty(M + 1)
+    v = np.empty(M + 1)
+    _check(lib().oracle_gamma_sequence(_p(a), _p(b), M, _p(u), _p(v)))
+    return u, v
+
+
+def gamma_dot(a: np.ndarray, b: np.ndarray):
+    """Eq. 9: returns (v(delta_M) = dot product, u(delta_M))."""
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    u = ctypes.c_double()
+    v = lib().oracle_gamma_dot(_p(a), _p(b), a.shape[0], ctypes.byref(u))
+    return v, u.value

@@ -1,0 +1,220 @@
+/*
+ * oracle.c -- plain CPU oracle (TEST INFRASTRUCTURE ONLY; see oracle.h).
+ *
+ * Each function is the definition it cites, written as the obvious loop.
+ * Compiled with -O2 and no fast-math (IEEE double).  Single-threaded.
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stddef.h>
+
+/* Output length of a valid-padding window of w addends at stride s
+ * (Eq. 3 gives N-w+1 at s=1; stride reading R4 in DESIGN.md). */
+int64_t oracle_out_len(int64_t N, int64_t w, int64_t s) {
+  if (N < 1 || w < 1 || s < 1 || w > N) return -1;
+  return (N - w) / s + 1;
+}
+
+static int bad_1d(const void* x, const void* y, int64_t N, int64_t batch,
+                  int64_t w, int64_t s) {
+  return x == NULL || y == NULL || batch < 1 || oracle_out_len(N, w, s) < 0;
+}
+
+/* Eq. 3, (+) = +: y_i = x_{is} + ... + x_{is+w-1}, left to right, in int64. */
+int oracle_pool_sum_i32(const int32_t* x, int64_t N, int64_t batch, int64_t w,
+                        int64_t s, int64_t* y) {
+  if (bad_1d(x, y, N, batch, w, s)) return -1;
+  int64_t L = oracle_out_len(N, w, s);
+  for (int64_t b = 0; b < batch; ++b) {
+    const int32_t* xr = x + b * N;
+    for (int64_t i = 0; i < L; ++i) {
+      int64_t acc = 0;
+      for (int64_t j = 0; j < w; ++j) acc += (int64_t)xr[i * s + j];
+      y[b * L + i] = acc;
+    }
+  }
+  return 0;
+}
+
+/* Eq. 3, (+) = +, fp32 input summed in double. */
+int oracle_pool_sum_f32(const float* x, int64_t N, int64_t batch, int64_t w,
+                        int64_t s, double* y, double* absmag) {
+  if (bad_1d(x, y, N, batch, w, s)) return -1;
+  int64_t L = oracle_out_len(N, w, s);
+  for (int64_t b = 0; b < batch; ++b) {
+    const float* xr = x + b * N;
+    for (int64_t i = 0; i < L; ++i) {
+      double acc = 0.0, mag = 0.0;
+      for (int64_t j = 0; j < w; ++j) {
+        double v = (double)xr[i * s + j];
+        acc += v;
+        mag += fabs(v);
+      }
+      y[b * L + i] = acc;
+      if (absmag) absmag[b * L + i] = mag;
+    }
+  }
+  return 0;
+}
+
+/* Eq. 3, (+) = max (Sec. 2.3): m = x_{is}; m = (v > m ? v : m) left to right. */
+int oracle_pool_max_i32(const int32_t* x, int64_t N, int64_t batch, int64_t w,
+                        int64_t s, int32_t* y) {
+  if (bad_1d(x, y, N, batch, w, s)) return -1;
+  int64_t L = oracle_out_len(N, w, s);
+  for (int64_t b = 0; b < batch; ++b) {
+    const int32_t* xr = x + b * N;
+    for (int64_t i = 0; i < L; ++i) {
+      int32_t m = xr[i * s];
+      for (int64_t j = 1; j < w; ++j) {
+        int32_t v = xr[i * s + j];
+        m = v > m ? v : m;
+      }
+      y[b * L + i] = m;
+    }
+  }
+  return 0;
+}
+
+int oracle_pool_max_f32(const float* x, int64_t N, int64_t batch, int64_t w,
+                        int64_t s, float* y) {
+  if (bad_1d(x, y, N, batch, w, s)) return -1;
+  int64_t L = oracle_out_len(N, w, s);
+  for (int64_t b = 0; b < batch; ++b) {
+    const float* xr = x + b * N;
+    for (int64_t i = 0; i < L; ++i) {
+      float m = xr[i * s];
+      for (int64_t j = 1; j < w; ++j) {
+        float v = xr[i * s + j];
+        m = v > m ? v : m;
+      }
+      y[b * L + i] = m;
+    }
+  }
+  return 0;
+}
+
+/* Sec. 2.4-2.5: convolution = sliding dot product (Eq. 4 per window),
+ * cross-correlation orientation (reading R2): y_i = sum_j f_j * x_{is+j}. */
+int oracle_conv1d_f32(const float* x, int64_t N, int64_t batch, const float* f,
+                      int64_t k, int64_t s, double* y, double* absmag) {
+  if (bad_1d(x, y, N, batch, k, s) || f == NULL) return -1;
+  int64_t L = oracle_out_len(N, k, s);
+  for (int64_t b = 0; b < batch; ++b) {
+    const float* xr = x + b * N;
+    for (int64_t i = 0; i < L; ++i) {
+      double acc = 0.0, mag = 0.0;
+      for (int64_t j = 0; j < k; ++j) {
+        double p = (double)f[j] * (double)xr[i * s + j];
+        acc += p;
+        mag += fabs(p);
+      }
+      y[b * L + i] = acc;
+      if (absmag) absmag[b * L + i] = mag;
+    }
+  }
+  return 0;
+}
+
+/* 2-D pooling (Sec. 2.3 operators over the multi-dimensional window of the
+ * Conclusion): out[p][r][c] = (+)_{dr<kh, dc<kw} x[p][r*sh+dr][c*sw+dc].
+ * mode 0: max; mode 1: average = (double sum) / (kh*kw). */
+int oracle_pool2d_f32(const float* x, int64_t planes, int64_t H, int64_t W,
+                      int64_t kh, int64_t kw, int64_t sh, int64_t sw, int mode,
+                      double* y, double* absmag) {
+  if (x == NULL || y == NULL || planes < 1 || (mode != 0 && mode != 1)) return -1;
+  int64_t OH = oracle_out_len(H, kh, sh), OW = oracle_out_len(W, kw, sw);
+  if (OH < 0 || OW < 0) return -1;
+  double cnt = (double)(kh * kw);
+  for (int64_t p = 0; p < planes; ++p) {
+    const float* xp = x + p * H * W;
+    for (int64_t r = 0; r < OH; ++r) {
+      for (int64_t c = 0; c < OW; ++c) {
+        double acc = 0.0, mag = 0.0;
+        float m = xp[(r * sh) * W + c * sw];
+        for (int64_t dr = 0; dr < kh; ++dr) {
+          for (int64_t dc = 0; dc < kw; ++dc) {
+            float v = xp[(r * sh + dr) * W + (c * sw + dc)];
+            acc += (double)v;
+            mag += fabs((double)v);
+            m = v > m ? v : m;
+          }
+        }
+        int64_t o = (p * OH + r) * OW + c;
+        if (mode == 0) {
+          y[o] = (double)m;
+          if (absmag) absmag[o] = 0.0;
+        } else {
+          y[o] = acc / cnt;
+          if (absmag) absmag[o] = mag / cnt;
+        }
+      }
+    }
+  }
+  return 0;
+}
+
+/* Eq. 8. */
+void oracle_gamma_combine(double ui, double vi, double uj, double vj,
+                          double* u_out, double* v_out) {
+  *u_out = ui * uj;
+  *v_out = uj * vi + vj;
+}
+
+/* Eq. 5 (masking) then Eq. 7:
+ *   alpha_i = 1 if a_i == 0 else a_i;   beta_i = 0 if a_i == 0 else b_i
+ *   u_0 = 1;  u_i = alpha_{i-1} / alpha_i (0 < i < M);  u_M = alpha_{M-1}
+ *   v_i = beta_i (i < M);  v_M = 0.                                          */
+int oracle_gamma_sequence(const double* a, const double* b, int64_t M,
+                          double* u, double* v) {
+  if (a == NULL || b == NULL || u == NULL || v == NULL || M < 1) return -1;
+  for (int64_t i = 0; i <= M; ++i) {
+    if (i == 0) {
+      u[i] = 1.0;
+    } else if (i < M) {
+      double alpha_prev = a[i - 1] == 0.0 ? 1.0 : a[i - 1];
+      double alpha_i = a[i] == 0.0 ? 1.0 : a[i];
+      u[i] = alpha_prev / alpha_i;
+    } else {
+      u[i] = a[M - 1] == 0.0 ? 1.0 : a[M - 1];
+    }
+    if (i < M) {
+      v[i] = a[i] == 0.0 ? 0.0 : b[i];
+    } else {
+      v[i] = 0.0;
+    }
+  }
+  return 0;
+}
+
+/* Eq. 9: delta_0 = gamma_0, delta_i = delta_{i-1} (+) gamma_i;
+ * the bottom element of delta_M is the dot product. */
+double oracle_gamma_dot(const double* a, const double* b, int64_t M, double* u_out) {
+  if (a == NULL || b == NULL || M < 1) return NAN;
+  double du = 1.0, dv = 0.0;
+  for (int64_t i = 0; i <= M; ++i) {
+    double ui, vi;
+    if (i == 0) {
+      ui = 1.0;
+    } else if (i < M) {
+      double alpha_prev = a[i - 1] == 0.0 ? 1.0 : a[i - 1];
+      double alpha_i = a[i] == 0.0 ? 1.0 : a[i];
+      ui = alpha_prev / alpha_i;
+    } else {
+      ui = a[M - 1] == 0.0 ? 1.0 : a[M - 1];
+    }
+    vi = (i < M) ? (a[i] == 0.0 ? 0.0 : b[i]) : 0.0;
+    if (i == 0) {
+      du = ui;
+      dv = vi;
+    } else {
+      double nu, nv;
+      oracle_gamma_combine(du, dv, ui, vi, &nu, &nv);
+      du = nu;
+      dv = nv;
+    }
+  }
+  if (u_out) *u_out = du;
+  return dv;
+}

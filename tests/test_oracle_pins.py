@@ -1,0 +1,316 @@
+"""Pins for the CPU oracle (oracle/): each check ties an oracle routine to
+something other than itself -- values printed in the spec written from the
+paper (tests/golden/spec_examples.json), closed forms, invariants, brute force
+on tiny inputs, and independent library routines (numpy cumsum, torch float64
+pooling/conv) -- so that a dropped term, a wrong sign or index, or a transposed
+operand in oracle.c fails at least one of them.
+
+CPU only (no GPU marker)."""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+import oracle
+import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+# ---------------------------------------------------------------- golden values
+@pytest.mark.parametrize("case", GOLD["sliding_sum"], ids=lambda c: c["cite"])
+def test_golden_sliding_sum(case):
+    x = np.array(case["x"], np.int32)
+    if case["op"] == "add":
+        y = oracle.pool_sum(x, case["w"])
+        np.testing.assert_array_equal(y, np.array(case["y"], np.int64))
+        yf, _ = oracle.pool_sum(x.astype(np.float32), case["w"])
+        np.testing.assert_array_equal(yf, np.array(case["y"], np.float64))
+    else:
+        np.testing.assert_array_equal(oracle.pool_max(x, case["w"]), np.array(case["y"], np.int32))
+        np.testing.assert_array_equal(oracle.pool_max(x.astype(np.float32), case["w"]),
+                                      np.array(case["y"], np.float32))
+
+
+@pytest.mark.parametrize("case", GOLD["avg_pool"], ids=lambda c: c["cite"])
+def test_golden_avg_pool(case):
+    # SPEC avg_pool = sliding + divided by w (reading R5: ss_pool_sum is the raw sum;
+    # the 1-D average is modelled here as a 1 x w 2-D average pool).
+    x = np.array(case["x"], np.float32)
+    y, _ = oracle.pool_sum(x, case["w"], case["stride"])
+    np.testing.assert_array_equal(y / case["w"], np.array(case["y"]))
+    y2, _ = oracle.pool2d(x.reshape(1, 1, -1), 1, case["w"], 1, case["stride"], oracle.POOL2D_AVG)
+    np.testing.assert_array_equal(y2.reshape(-1), np.array(case["y"]))
+
+
+@pytest.mark.parametrize("case", GOLD["conv1d"], ids=lambda c: c["cite"])
+def test_golden_conv1d(case):
+    y, _ = oracle.conv1d(np.array(case["x"], np.float32), np.array(case["f"], np.float32))
+    np.testing.assert_array_equal(y, np.array(case["y"], np.float64))
+
+
+@pytest.mark.parametrize("case", GOLD["gamma_combine"], ids=lambda c: c["cite"])
+def test_golden_gamma_combine(case):
+    assert oracle.gamma_combine(case["gi"], case["gj"]) == tuple(case["out"])
+
+
+def test_gamma_combine_noncommutative_and_associative():
+    # Eq. 8 is associative but not commutative.
+    a, b, c = (2.0, 3.0), (0.5, -1.0), (4.0, 0.25)
+    assert oracle.gamma_combine(a, b) != oracle.gamma_combine(b, a)
+    lhs = oracle.gamma_combine(oracle.gamma_combine(a, b), c)
+    rhs = oracle.gamma_combine(a, oracle.gamma_combine(b, c))
+    assert lhs == rhs  # dyadic values: exact
+
+
+@pytest.mark.parametrize("case", GOLD["gamma_sequence"], ids=lambda c: c["cite"])
+def test_golden_gamma_sequence(case):
+    u, v = oracle.gamma_sequence(np.array(case["a"]), np.array(case["b"]))
+    np.testing.assert_array_equal(u, case["u"])
+    np.testing.assert_array_equal(v, case["v"])
+
+
+@pytest.mark.parametrize("case", GOLD["gamma_dot"], ids=lambda c: c["cite"])
+def test_golden_gamma_dot(case):
+    v, _ = oracle.gamma_dot(np.array(case["a"], float), np.array(case["b"], float))
+    assert v == case["dot"]
+
+
+def test_golden_splitmix64():
+    case = GOLD["splitmix64"][0]
+    z = synth.splitmix64(case["seed"], np.array([case["counter"]], np.uint64))[0]
+    assert int(z) == int(case["z"], 16)
+
+
+# ------------------------------------------- P5: dot product is a prefix sum (Eq. 9)
+def test_gamma_dot_equals_direct_dot_product():
+    rng = np.random.default_rng(11)
+    for trial in range(300):
+        M = int(rng.integers(1, 257))
+        a = rng.uniform(0.25, 2.0, M) * rng.choice([-1.0, 1.0], M)
+        a[rng.random(M) < 0.25] = 0.0  # Eq. 5 masking exercised
+        b = rng.normal(size=M)
+        v, u = oracle.gamma_dot(a, b)
+        direct = float(np.dot(a, b))
+        scale = float(np.abs(a * b).sum()) + 1e-300
+        assert abs(v - direct) <= 1e-10 * scale, (M, v, direct)
+        # u(delta_M) = prod u_i telescopes to alpha_0 (Eq. 7)
+        alpha0 = 1.0 if a[0] == 0.0 else a[0]
+        assert abs(u - alpha0) <= 1e-12 * abs(alpha0)
+
+
+def test_gamma_masking_identity_eq6():
+    # Eq. 6: sum alpha_i beta_i = sum a_i b_i (same order -> exact)
+    rng = np.random.default_rng(5)
+    a = rng.normal(size=64)
+    a[rng.random(64) < 0.3] = 0.0
+    b = rng.normal(size=64)
+    u, v = oracle.gamma_sequence(a, b)
+    alpha = np.where(a == 0.0, 1.0, a)
+    beta = v[:-1]
+    s1 = 0.0
+    s2 = 0.0
+    for i in range(64):
+        s1 += alpha[i] * beta[i]
+        s2 += a[i] * b[i]
+    assert s1 == s2
+
+
+# ------------------------------------------- P1: prefix-sum definition (Eq. 1, 2)
+@pytest.mark.parametrize("w,s", [(1, 1), (2, 1), (3, 1), (16, 1), (64, 1), (256, 1), (5, 2), (7, 3), (3, 5)])
+def test_pool_sum_i32_equals_prefix_difference(w, s):
+    # Sliding sum (Eq. 3) = P_{is+w} - P_{is} with P the prefix sums of Eq. 1,
+    # built here by numpy's cumsum (an independent library routine).
+    x = synth.randint(2, 5000, -1000, 1000)
+    P = np.concatenate([[0], np.cumsum(x.astype(np.int64))])
+    L = (5000 - w) // s + 1
+    i = np.arange(L) * s
+    np.testing.assert_array_equal(oracle.pool_sum(x, w, s), P[i + w] - P[i])
+
+
+def test_prefix_recurrence_eq2():
+    # Eq. 2: the window starting at 0 with w = i+1 is the prefix y_i, and
+    # y_{i+1} = y_i + x_{i+1}.
+    x = synth.randint(9, 50, -1000, 1000)
+    ys = [int(oracle.pool_sum(x[: i + 1], i + 1)[0]) for i in range(50)]
+    for i in range(49):
+        assert ys[i + 1] == ys[i] + int(x[i + 1])
+    assert ys[0] == int(x[0])
+
+
+# ------------------------------------------- P2: closed forms
+@pytest.mark.parametrize("w,s", [(1, 1), (3, 1), (8, 1), (64, 1), (4, 3), (9, 2)])
+def test_closed_forms_ramp_and_constant(w, s):
+    N = 300
+    L = (N - w) // s + 1
+    i = np.arange(L, dtype=np.int64)
+    ramp = np.arange(N, dtype=np.int32)
+    np.testing.assert_array_equal(oracle.pool_sum(ramp, w, s), w * (i * s) + w * (w - 1) // 2)
+    np.testing.assert_array_equal(oracle.pool_max(ramp, w, s), i * s + w - 1)
+    np.testing.assert_array_equal(oracle.pool_max(-ramp, w, s), -(i * s))
+    yf, mag = oracle.pool_sum(ramp.astype(np.float32), w, s)
+    np.testing.assert_array_equal(yf, (w * (i * s) + w * (w - 1) // 2).astype(np.float64))
+    np.testing.assert_array_equal(mag, yf)  # non-negative input: absmag = sum
+    np.testing.assert_array_equal(oracle.pool_max(ramp.astype(np.float32), w, s), (i * s + w - 1).astype(np.float32))
+    c = np.full(N, 7, np.int32)
+    np.testing.assert_array_equal(oracle.pool_sum(c, w, s), np.full(L, 7 * w))
+    np.testing.assert_array_equal(oracle.pool_max(c, w, s), np.full(L, 7))
+
+
+def test_closed_forms_2d():
+    P, H, W = 3, 17, 13
+    r = np.arange(H)[:, None]
+    c = np.arange(W)[None, :]
+    x = np.broadcast_to((r * W + c).astype(np.float32), (P, H, W)).copy()
+    for kh, kw, sh, sw in [(3, 3, 1, 1), (2, 2, 2, 2), (3, 2, 2, 3), (1, 1, 1, 1), (17, 13, 1, 1)]:
+        OH, OW = (H - kh) // sh + 1, (W - kw) // sw + 1
+        orr = np.arange(OH)[:, None]
+        occ = np.arange(OW)[None, :]
+        ymax, _ = oracle.pool2d(x, kh, kw, sh, sw, oracle.POOL2D_MAX)
+        exp_max = (orr * sh + kh - 1) * W + occ * sw + kw - 1
+        np.testing.assert_array_equal(ymax, np.broadcast_to(exp_max, (P, OH, OW)))
+        yavg, mag = oracle.pool2d(x, kh, kw, sh, sw, oracle.POOL2D_AVG)
+        exp_avg = (orr * sh + (kh - 1) / 2) * W + occ * sw + (kw - 1) / 2
+        np.testing.assert_allclose(yavg, np.broadcast_to(exp_avg, (P, OH, OW)), rtol=1e-15, atol=1e-12)
+        np.testing.assert_array_equal(mag, yavg)
+
+
+# ------------------------------------------- P3: delta and box filters
+@pytest.mark.parametrize("k,m,s", [(1, 0, 1), (3, 0, 1), (3, 2, 1), (8, 5, 1), (31, 17, 1), (63, 62, 1), (5, 3, 2)])
+def test_conv_delta_filter_is_shift(k, m, s):
+    x = synth.normal(3, 1000)
+    f = np.zeros(k, np.float32)
+    f[m] = 1.0
+    y, mag = oracle.conv1d(x, f, s)
+    L = (1000 - k) // s + 1
+    exp = x[np.arange(L) * s + m].astype(np.float64)
+    np.testing.assert_array_equal(y, exp)  # orientation: cross-correlation, no flip
+    np.testing.assert_array_equal(mag, np.abs(exp))
+
+
+def test_conv_box_filter_is_sliding_sum():
+    x = synth.uniform_pm1(0, 777)
+    for k in (1, 2, 8, 33):
+        y, mag = oracle.conv1d(x, np.ones(k, np.float32))
+        ys, mags = oracle.pool_sum(x, k)
+        np.testing.assert_array_equal(y, ys)
+        np.testing.assert_array_equal(mag, mags)
+
+
+def test_conv_asymmetric_filter_orientation():
+    # [1,2,3,4] with f=[1,10]: cross-correlation gives x_i + 10 x_{i+1}
+    y, _ = oracle.conv1d(np.array([1, 2, 3, 4], np.float32), np.array([1, 10], np.float32))
+    np.testing.assert_array_equal(y, [21, 32, 43])
+
+
+# ------------------------------------------- P4: brute force on tiny inputs
+def test_brute_force_tiny_exhaustive():
+    vals = [-2, -1, 0, 1, 2]
+    for N in range(1, 6):
+        for xs in itertools.product(vals, repeat=N):
+            x = np.array(xs, np.int32)
+            for w in range(1, N + 1):
+                for s in (1, 2, 3):
+                    L = (N - w) // s + 1
+                    exp_sum = [sum(xs[i * s:i * s + w]) for i in range(L)]
+                    exp_max = [max(xs[i * s:i * s + w]) for i in range(L)]
+                    assert oracle.pool_sum(x, w, s).tolist() == exp_sum
+                    assert oracle.pool_max(x, w, s).tolist() == exp_max
+                    if s == 1 and L > 1:
+                        y = oracle.pool_sum(x, w, 1)
+                        # Eq. 3 identity: y_{i+1} - y_i = x_{i+w} - x_i
+                        assert all(y[i + 1] - y[i] == xs[i + w] - xs[i] for i in range(L - 1))
+
+
+# ------------------------------------------- P7: independent library routines (float64)
+@pytest.mark.parametrize("w,s", [(1, 1), (3, 1), (8, 1), (16, 2), (64, 1), (5, 5)])
+def test_pool_vs_torch(w, s):
+    x = synth.normal(1, 3 * 1000).reshape(3, 1000)
+    xt = torch.from_numpy(x.astype(np.float64)).unsqueeze(1)
+    y, mag = oracle.pool_sum(x, w, s)
+    ref = F.avg_pool1d(xt, w, s).squeeze(1).numpy() * w
+    np.testing.assert_allclose(y, ref, rtol=1e-12, atol=1e-12)
+    ref_mag = F.avg_pool1d(xt.abs(), w, s).squeeze(1).numpy() * w
+    np.testing.assert_allclose(mag, ref_mag, rtol=1e-12, atol=1e-12)
+    np.testing.assert_array_equal(oracle.pool_max(x, w, s),
+                                  F.max_pool1d(torch.from_numpy(x).unsqueeze(1), w, s).squeeze(1).numpy())
+    xi = synth.randint(2, 3000, -1000, 1000).reshape(3, 1000)
+    ref_i = F.max_pool1d(torch.from_numpy(xi.astype(np.float64)).unsqueeze(1), w, s).squeeze(1).numpy()
+    np.testing.assert_array_equal(oracle.pool_max(xi, w, s), ref_i.astype(np.int32))
+
+
+@pytest.mark.parametrize("k,s", [(1, 1), (3, 1), (5, 2), (8, 1), (31, 1), (63, 1), (7, 3)])
+def test_conv_vs_torch(k, s):
+    x = synth.normal(3, 2 * 2000).reshape(2, 2000)
+    f = synth.normal(4, k, sigma=synth.cfg_sigma_filter(k))
+    y, mag = oracle.conv1d(x, f, s)
+    xt = torch.from_numpy(x.astype(np.float64)).unsqueeze(1)
+    ft = torch.from_numpy(f.astype(np.float64)).view(1, 1, k)
+    ref = F.conv1d(xt, ft, stride=s).squeeze(1).numpy()
+    np.testing.assert_allclose(y, ref, rtol=1e-12, atol=1e-12)
+    ref_mag = F.conv1d(xt.abs(), ft.abs(), stride=s).squeeze(1).numpy()
+    np.testing.assert_allclose(mag, ref_mag, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("kh,kw,sh,sw", [(3, 3, 1, 1), (2, 2, 2, 2), (3, 5, 2, 1), (1, 1, 1, 1), (4, 3, 3, 2)])
+def test_pool2d_vs_torch(kh, kw, sh, sw):
+    x = synth.uniform01(5, 4 * 23 * 19).reshape(4, 23, 19)
+    xt = torch.from_numpy(x.astype(np.float64)).unsqueeze(1)
+    ymax, _ = oracle.pool2d(x, kh, kw, sh, sw, oracle.POOL2D_MAX)
+    np.testing.assert_array_equal(ymax, F.max_pool2d(xt, (kh, kw), (sh, sw)).squeeze(1).numpy())
+    yavg, mag = oracle.pool2d(x, kh, kw, sh, sw, oracle.POOL2D_AVG)
+    ref = F.avg_pool2d(xt, (kh, kw), (sh, sw)).squeeze(1).numpy()
+    np.testing.assert_allclose(yavg, ref, rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(mag, ref, rtol=1e-13, atol=1e-15)  # x >= 0
+
+
+# ------------------------------------------- P9: linearity, separability
+def test_conv_linearity():
+    x1 = synth.normal(21, 4000)
+    x2 = synth.normal(22, 4000)
+    f = synth.normal(4, 31, sigma=synth.cfg_sigma_filter(31))
+    a = np.float32(0.5)  # exact scaling
+    y1, m1 = oracle.conv1d(x1, f)
+    y2, m2 = oracle.conv1d(x2, f)
+    y12, _ = oracle.conv1d((a * x1 + x2).astype(np.float32), f)
+    # inputs of (a x1 + x2) are rounded to fp32 once: allow that rounding
+    bound = 1e-6 * (a * m1 + m2) + 1e-12
+    assert np.all(np.abs(y12 - (a * y1 + y2)) <= bound)
+
+
+def test_pool2d_max_separable_equals_direct():
+    x = synth.normal(8, 5 * 31 * 29).reshape(5, 31, 29)
+    for kh, kw, sh, sw in [(3, 3, 1, 1), (2, 2, 2, 2), (5, 3, 2, 3)]:
+        ymax, _ = oracle.pool2d(x, kh, kw, sh, sw, oracle.POOL2D_MAX)
+        rows = np.lib.stride_tricks.sliding_window_view(x, kw, axis=2)[:, :, ::sw].max(-1)
+        cols = np.lib.stride_tricks.sliding_window_view(rows, kh, axis=1)[:, ::sh].max(-1)
+        np.testing.assert_array_equal(ymax, cols.astype(np.float64))
+
+
+# ------------------------------------------- argument checks
+def test_oracle_rejects_window_exceeding_input():
+    with pytest.raises(ValueError):
+        oracle.pool_sum(np.zeros(3, np.int32), 4)
+    with pytest.raises(ValueError):
+        oracle.conv1d(np.zeros(3, np.float32), np.ones(5, np.float32))
+    assert oracle.out_len(3, 4, 1) == -1
+    assert oracle.out_len(10, 3, 4) == 2
+    assert oracle.out_len(2 ** 32, 31, 1) == 2 ** 32 - 30
+
+
+# ------------------------------------------- generator sanity (shared inputs)
+def test_generator_counter_based_and_distributions():
+    a = synth.normal(6, 1000, start=5000)
+    b = synth.normal(6, 6000)[5000:]
+    np.testing.assert_array_equal(a, b)
+    z = synth.normal(3, 200000)
+    assert abs(float(z.mean())) < 0.01 and abs(float(z.var()) - 1.0) < 0.02
+    i = synth.randint(2, 200000, -1000, 1000)
+    assert i.min() == -1000 and i.max() == 1000
+    u = synth.uniform_pm1(0, 100000)
+    assert u.min() >= -1.0 and u.max() < 1.0
+    assert np.all((u * 2 ** 23) == np.round(u * 2 ** 23))
