@@ -1,0 +1,130 @@
+/*
+ * ss.h -- C ABI of the B200 (sm_100a) sliding-window-sum library `libss.so`,
+ * the data-parallel hot path of arXiv 2305.16513 ("sliding window sums" for
+ * DNN pooling and convolution).  Implementation: paper_2305_16513_b200/csrc/.
+ *
+ * The operation (Sec. 2.2, Eq. 3):
+ *     y_i = x_i (+) x_{i+1} (+) ... (+) x_{i+w-1}      ("exactly w addends")
+ * for (+) in {+, max} (Sec. 2.3: average / max pooling) and
+ * the sliding dot product (Sec. 2.4-2.5: convolution with a
+ * length-k filter), evaluated directly on the unmodified input (no im2col,
+ * PAPER.md l.17-19).  2-D pooling is the multi-dimensional extension named in
+ * the Conclusion, computed separably (row pass, then column
+ * pass).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  Pointers   x, y are DEVICE pointers (cudaMalloc / torch CUDA memory) on the
+ *             current CUDA device; `filter_host` is a HOST pointer.  The
+ *             caller owns all memory.  x and y must not overlap.  Any
+ *             element-aligned pointer is accepted (16-byte-aligned buffers
+ *             take the fastest path).  Reads may touch the bytes of the
+ *             16-byte granules that contain x's first and last element; they
+ *             are never written.
+ *  Layout     1-D: x is [batch][N] row-major contiguous (row pitch N);
+ *             y is [batch][out_len] contiguous, out_len = ss_out_len(N,w,s).
+ *             2-D: x is [planes][H][W], y is [planes][OH][OW], contiguous.
+ *             Valid padding only: output i covers x[i*s .. i*s+w-1]
+ *             (readings R1-R4).
+ *  Sizes      int64_t throughout (N = 2^32 is supported).
+ *  Stream     `stream` is a cudaStream_t passed as void* (NULL = the legacy
+ *             default stream).  Every call only ENQUEUES work on `stream`
+ *             and returns; there is no implicit synchronisation.  Calls on
+ *             different streams may run concurrently (no global mutable
+ *             device state; no __constant__ writes).
+ *  Errors     A non-OK status means NOTHING was enqueued: all arguments are
+ *             validated before any launch.  SS_ERR_CUDA reports a launch
+ *             failure (detail in ss_last_error()).  Asynchronous faults
+ *             surface at the caller's next synchronisation.  The library
+ *             never aborts, throws or prints.
+ *  Memory     The library allocates no device memory and keeps no per-call
+ *             state; it caches per-device attributes (SM count) only.
+ *  Numerics   int32 + wraps modulo 2^32.  fp32 uses IEEE round-to-nearest
+ *             FMA/adds (no fast-math, no flush-to-zero).  max uses
+ *             `a > b ? a : b` (inputs are finite; NaN unsupported).  Results
+ *             are bitwise deterministic run to run; conv1d and max results
+ *             are also independent of tiling and of sharding.  fp32 results
+ *             satisfy |y - y_exact| <= 1e-5 * sum_j |x_j f_j| + 1e-6
+ *             (BASELINE.json north_star; f = 1 for sums, 1/(kh*kw) for avg).
+ */
+#ifndef SS_H
+#define SS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SS_ABI_VERSION 1
+
+typedef enum { SS_F32 = 0, SS_I32 = 1 } ss_dtype_t;
+typedef enum { SS_POOL_MAX = 0, SS_POOL_AVG = 1 } ss_pool_mode_t;
+
+typedef enum {
+  SS_OK = 0,
+  SS_ERR_NULL = 1,                  /* a required pointer is NULL              */
+  SS_ERR_BAD_SIZE = 2,              /* N/batch/w/k/stride/planes/H/W < 1, or a  */
+                                    /* size whose byte count overflows int64    */
+  SS_ERR_WINDOW_EXCEEDS_INPUT = 3,  /* w > N ("window exceeds")  */
+  SS_ERR_UNSUPPORTED = 4,           /* dtype/op combination not provided,      */
+                                    /* or k > SS_K_MAX                          */
+  SS_ERR_CUDA = 5,                  /* CUDA launch/attribute failure           */
+  SS_ERR_OVERLAP = 6                /* x and y byte ranges overlap             */
+} ss_status_t;
+
+/* Largest conv1d filter length accepted. */
+#define SS_K_MAX 1024
+
+/* ABI version of the loaded library (== SS_ABI_VERSION it was built with). */
+int ss_abi_version(void);
+
+/* Valid-padding output length (N - w) / stride + 1 (Eq. 3 at stride 1 gives
+ * N - w + 1); -1 if N < 1, w < 1, stride < 1 or w > N.  Pure host function. */
+int64_t ss_out_len(int64_t N, int64_t w, int64_t stride);
+
+/* Eq. 3 with (+) = + (average pooling is the sliding sum with
+ * +).  Returns the RAW window sum (divide by w for the average; reading R5).
+ * y[b][i] = sum_{j<w} x[b][i*stride + j].  dtype SS_I32 (wrapping) or SS_F32. */
+ss_status_t ss_pool_sum(const void* x, void* y, int64_t N, int64_t batch,
+                        int64_t w, int64_t stride, ss_dtype_t dtype, void* stream);
+
+/* Eq. 3 with (+) = max (max pooling).
+ * y[b][i] = max_{j<w} x[b][i*stride + j].  dtype SS_I32 or SS_F32. */
+ss_status_t ss_pool_max(const void* x, void* y, int64_t N, int64_t batch,
+                        int64_t w, int64_t stride, ss_dtype_t dtype, void* stream);
+
+/* Sliding dot product = 1-D convolution with a length-k filter (PAPER.md
+ * l.86-87, Sec. 2.5; Eq. 4 per window), cross-correlation orientation
+ * (reading R2): y[b][i] = sum_{j<k} filter[j] * x[b][i*stride + j],
+ * accumulated in fp32 FMA in the fixed order j = 0..k-1.  One filter shared
+ * by all rows.  `filter_host` (k floats, HOST memory) is read before the call
+ * returns and may be freed immediately.  dtype must be SS_F32; 1 <= k <= SS_K_MAX. */
+ss_status_t ss_conv1d(const void* x, void* y, int64_t N, int64_t batch,
+                      const float* filter_host, int64_t k, int64_t stride,
+                      ss_dtype_t dtype, void* stream);
+
+/* 2-D pooling, computed separably: a row sliding (+) over kw at stride sw,
+ * then a column sliding (+) over kh at stride sh (PAPER.md l.53 operators,
+ * l.226 multi-dimensional extension).  mode SS_POOL_MAX: max; SS_POOL_AVG:
+ * window sum times 1/(kh*kw) (no padding, so every window has kh*kw terms).
+ * x is [planes][H][W] (planes = N*C of an NCHW tensor), y is
+ * [planes][(H-kh)/sh+1][(W-kw)/sw+1].  dtype must be SS_F32. */
+ss_status_t ss_pool2d(const void* x, void* y, int64_t planes, int64_t H, int64_t W,
+                      int64_t kh, int64_t kw, int64_t sh, int64_t sw,
+                      ss_pool_mode_t mode, ss_dtype_t dtype, void* stream);
+
+/* Static description of a status code. */
+const char* ss_status_string(ss_status_t s);
+/* Thread-local detail for the last non-OK status returned on this thread
+ * ("" if none).  Valid until the next ss_* call on the same thread. */
+const char* ss_last_error(void);
+
+/* Number of kernel launches the library has enqueued in this process (all
+ * threads).  Used by bench.py to report `gpu_launches`. */
+uint64_t ss_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SS_H */

@@ -1,0 +1,221 @@
+"""B200-native sliding-window-sum library (hot path of arXiv 2305.16513).
+
+Thin Python binding over the C ABI in ``include/ss.h`` (``libss.so``, built
+in-tree from ``csrc/`` for sm_100a).  This module only marshals arguments:
+every step of the computation runs in the CUDA kernels.  There is no CPU
+fallback -- importing this package without the built library raises.
+
+Low-level names mirror the ABI (``ss_pool_sum``, ``ss_pool_max``,
+``ss_conv1d``, ``ss_pool2d``, ``ss_out_len``...) and take raw device pointers;
+the tensor helpers (``pool_sum``, ``pool_max``, ``conv1d``, ``pool2d``) take
+CUDA torch tensors, allocate the output with torch, and launch on the current
+torch stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libss.so")
+
+SS_F32 = 0
+SS_I32 = 1
+SS_POOL_MAX = 0
+SS_POOL_AVG = 1
+SS_OK = 0
+SS_ERR_NULL = 1
+SS_ERR_BAD_SIZE = 2
+SS_ERR_WINDOW_EXCEEDS_INPUT = 3
+SS_ERR_UNSUPPORTED = 4
+SS_ERR_CUDA = 5
+SS_ERR_OVERLAP = 6
+SS_K_MAX = 1024
+
+EXPORTED = ("ss_abi_version", "ss_out_len", "ss_pool_sum", "ss_pool_max", "ss_conv1d",
+            "ss_pool2d", "ss_status_string", "ss_last_error", "ss_launch_count")
+
+
+class SSError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        super().__init__(f"{ss_status_string(status)} -- {detail}")
+        self.status = status
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    i64, vp, i32 = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
+    L.ss_abi_version.argtypes = []
+    L.ss_abi_version.restype = i32
+    L.ss_out_len.argtypes = [i64, i64, i64]
+    L.ss_out_len.restype = i64
+    for n in ("ss_pool_sum", "ss_pool_max"):
+        getattr(L, n).argtypes = [vp, vp, i64, i64, i64, i64, i32, vp]
+        getattr(L, n).restype = i32
+    L.ss_conv1d.argtypes = [vp, vp, i64, i64, ctypes.POINTER(ctypes.c_float), i64, i64, i32, vp]
+    L.ss_conv1d.restype = i32
+    L.ss_pool2d.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, i32, i32, vp]
+    L.ss_pool2d.restype = i32
+    L.ss_status_string.argtypes = [i32]
+    L.ss_status_string.restype = ctypes.c_char_p
+    L.ss_last_error.argtypes = []
+    L.ss_last_error.restype = ctypes.c_char_p
+    L.ss_launch_count.argtypes = []
+    L.ss_launch_count.restype = ctypes.c_uint64
+    return L
+
+
+_lib = _load()
+lib = _lib
+
+
+# ------------------------------------------------------------ raw C-ABI names
+def ss_abi_version() -> int:
+    return _lib.ss_abi_version()
+
+
+def ss_out_len(N: int, w: int, stride: int = 1) -> int:
+    return int(_lib.ss_out_len(N, w, stride))
+
+
+def ss_status_string(s: int) -> str:
+    return _lib.ss_status_string(s).decode()
+
+
+def ss_last_error() -> str:
+    return _lib.ss_last_error().decode()
+
+
+def ss_launch_count() -> int:
+    return int(_lib.ss_launch_count())
+
+
+def ss_pool_sum(x_ptr: int, y_ptr: int, N: int, batch: int, w: int, stride: int, dtype: int,
+                stream: int = 0) -> int:
+    return _lib.ss_pool_sum(x_ptr, y_ptr, N, batch, w, stride, dtype, stream)
+
+
+def ss_pool_max(x_ptr: int, y_ptr: int, N: int, batch: int, w: int, stride: int, dtype: int,
+                stream: int = 0) -> int:
+    return _lib.ss_pool_max(x_ptr, y_ptr, N, batch, w, stride, dtype, stream)
+
+
+def ss_conv1d(x_ptr: int, y_ptr: int, N: int, batch: int, filter_host, k: int, stride: int,
+              dtype: int = SS_F32, stream: int = 0) -> int:
+    if filter_host is None:
+        fp = None
+    else:
+        fp = (ctypes.c_float * len(filter_host))(*[float(v) for v in filter_host])
+    return _lib.ss_conv1d(x_ptr, y_ptr, N, batch, fp, k, stride, dtype, stream)
+
+
+def ss_pool2d(x_ptr: int, y_ptr: int, planes: int, H: int, W: int, kh: int, kw: int, sh: int,
+              sw: int, mode: int, dtype: int = SS_F32, stream: int = 0) -> int:
+    return _lib.ss_pool2d(x_ptr, y_ptr, planes, H, W, kh, kw, sh, sw, mode, dtype, stream)
+
+
+def check(status: int) -> None:
+    if status != SS_OK:
+        raise SSError(status, ss_last_error())
+
+
+# ------------------------------------------------------------ tensor helpers
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.float32:
+        return SS_F32
+    if t.dtype == torch.int32:
+        return SS_I32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def _stream(stream) -> int:
+    torch = _torch()
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _rows(x):
+    if not x.is_cuda:
+        raise ValueError("x must be a CUDA tensor (there is no CPU path)")
+    if not x.is_contiguous():
+        raise ValueError("x must be contiguous")
+    if x.dim() == 1:
+        return x.shape[0], 1
+    if x.dim() == 2:
+        return x.shape[1], x.shape[0]
+    raise ValueError("x must be [N] or [batch, N]")
+
+
+def _out(x, L, out):
+    torch = _torch()
+    shape = (L,) if x.dim() == 1 else (x.shape[0], L)
+    if out is None:
+        return torch.empty(shape, dtype=x.dtype, device=x.device)
+    assert tuple(out.shape) == shape and out.dtype == x.dtype and out.is_contiguous()
+    return out
+
+
+def pool_sum(x, w: int, stride: int = 1, out=None, stream=None):
+    """Eq. 3 with + (raw window sums) over the last dim of a CUDA [N] / [B, N] tensor."""
+    N, B = _rows(x)
+    L = ss_out_len(N, w, stride)
+    if L < 0:
+        check(ss_pool_sum(x.data_ptr(), 0, N, B, w, stride, _dtype_code(x), _stream(stream)) or SS_ERR_BAD_SIZE)
+    y = _out(x, L, out)
+    check(ss_pool_sum(x.data_ptr(), y.data_ptr(), N, B, w, stride, _dtype_code(x), _stream(stream)))
+    return y
+
+
+def pool_max(x, w: int, stride: int = 1, out=None, stream=None):
+    """Eq. 3 with max over the last dim of a CUDA [N] / [B, N] tensor."""
+    N, B = _rows(x)
+    L = ss_out_len(N, w, stride)
+    if L < 0:
+        check(ss_pool_max(x.data_ptr(), 0, N, B, w, stride, _dtype_code(x), _stream(stream)) or SS_ERR_BAD_SIZE)
+    y = _out(x, L, out)
+    check(ss_pool_max(x.data_ptr(), y.data_ptr(), N, B, w, stride, _dtype_code(x), _stream(stream)))
+    return y
+
+
+def conv1d(x, filt, stride: int = 1, out=None, stream=None):
+    """Sliding dot product (cross-correlation) of a CUDA fp32 [N]/[B, N] tensor with
+    a host filter (sequence of floats, numpy array or CPU tensor)."""
+    N, B = _rows(x)
+    f = [float(v) for v in (filt.tolist() if hasattr(filt, "tolist") else filt)]
+    k = len(f)
+    L = ss_out_len(N, k, stride)
+    if L < 0:
+        check(ss_conv1d(x.data_ptr(), 0, N, B, f, k, stride, _dtype_code(x), _stream(stream)) or SS_ERR_BAD_SIZE)
+    y = _out(x, L, out)
+    check(ss_conv1d(x.data_ptr(), y.data_ptr(), N, B, f, k, stride, _dtype_code(x), _stream(stream)))
+    return y
+
+
+def pool2d(x, kernel, stride, mode: str = "max", out=None, stream=None):
+    """Separable 2-D max/avg pooling of a CUDA fp32 tensor [..., H, W] (e.g. NCHW)."""
+    torch = _torch()
+    if not x.is_cuda or not x.is_contiguous():
+        raise ValueError("x must be a contiguous CUDA tensor")
+    kh, kw = kernel
+    sh, sw = stride
+    H, W = x.shape[-2], x.shape[-1]
+    planes = x.numel() // (H * W)
+    OH, OW = ss_out_len(H, kh, sh), ss_out_len(W, kw, sw)
+    m = SS_POOL_MAX if mode == "max" else SS_POOL_AVG
+    if OH < 0 or OW < 0:
+        check(ss_pool2d(x.data_ptr(), 0, planes, H, W, kh, kw, sh, sw, m, _dtype_code(x), _stream(stream)) or SS_ERR_BAD_SIZE)
+    shape = tuple(x.shape[:-2]) + (OH, OW)
+    y = torch.empty(shape, dtype=x.dtype, device=x.device) if out is None else out
+    check(ss_pool2d(x.data_ptr(), y.data_ptr(), planes, H, W, kh, kw, sh, sw, m, _dtype_code(x), _stream(stream)))
+    return y

@@ -1,0 +1,188 @@
+// pool2d.cu -- separable 2-D pooling (PAPER.md l.53 operators, l.226
+// multi-dimensional extension): a row sliding (+) over kw at stride sw, then a
+// column sliding (+) over kh at stride sh, fused on chip (the row results of a
+// column never leave registers).
+//
+// Skeleton: persistent CTAs walk tiles = (plane, band of output rows).  The
+// band's input rows are one contiguous byte range of the NCHW tensor, staged
+// HBM -> smem with one cp.async.bulk (1-D TMA) per tile into a ring of stages
+// (mbarrier completion).  Threads own output columns; each thread walks its
+// rows down the band keeping the last KH row results in a register ring
+// (stride-1 columns) so each input element is read from smem once per window
+// column it belongs to.  Outputs are written with coalesced stores.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ss_device.cuh"
+#include "ss_internal.h"
+
+namespace ss {
+
+constexpr int kP2Threads = 256;
+
+struct AvgOp {  // window sum, scaled at the end
+  using T = float;
+  static __device__ __forceinline__ float identity() { return 0.0f; }
+  static __device__ __forceinline__ float combine(float a, float b) { return __fadd_rn(a, b); }
+};
+
+template <class Op, int KW>
+__device__ __forceinline__ float row_result(const float* __restrict__ xs, int64_t c0, int kw) {
+  if constexpr (KW > 0) {
+    float r = xs[c0];
+#pragma unroll
+    for (int dc = 1; dc < KW; ++dc) r = Op::combine(r, xs[c0 + dc]);
+    return r;
+  } else {
+    float r = xs[c0];
+    for (int dc = 1; dc < kw; ++dc) r = Op::combine(r, xs[c0 + dc]);
+    return r;
+  }
+}
+
+template <class Op, int KH, int KW>
+__global__ void __launch_bounds__(kP2Threads)
+pool2d_kernel(const __grid_constant__ Pool2DParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
+                                             ~uintptr_t(127));
+  const int S = p.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int kh = KH > 0 ? KH : (int)p.kh;
+  const int kw = KW > 0 ? KW : (int)p.kw;
+  const int64_t W = p.W, OW = p.OW;
+  // thread -> (column lane, row group)
+  const int ncol = OW >= kP2Threads ? kP2Threads : (int)((OW + 31) / 32) * 32;
+  const int groups = kP2Threads / ncol;
+  const int col_lane = tid % ncol, grp = tid / ncol;
+
+  auto tile_rows = [&](int64_t tau, int64_t& plane, int64_t& r0, int64_t& r1, int64_t& in0,
+                       int64_t& nin) {
+    plane = tau / p.bands;
+    const int64_t band = tau - plane * p.bands;
+    r0 = band * p.band_rows;
+    r1 = r0 + p.band_rows < p.OH ? r0 + p.band_rows : p.OH;
+    in0 = r0 * p.sh;
+    nin = (r1 - 1) * p.sh + kh - in0;
+  };
+  auto issue = [&](int64_t tau, int s) {
+    int64_t plane, r0, r1, in0, nin;
+    tile_rows(tau, plane, r0, r1, in0, nin);
+    const float* src = p.x + (plane * p.H + in0) * W;
+    const uint32_t bytes = (uint32_t)(nin * W * 4);
+    mbar_arrive_expect_tx(&full[s], bytes);
+    bulk_load_1d(smem + (size_t)s * p.stage_bytes, src, bytes, &full[s]);
+  };
+
+  // prologue
+  if (p.bulk && tid == 0) {
+    int k = 0;
+    for (int64_t tau = blockIdx.x; tau < p.ntiles && k < S - 1; tau += gridDim.x, ++k) issue(tau, k);
+  }
+  int it = 0;
+  for (int64_t tau = blockIdx.x; tau < p.ntiles; tau += gridDim.x, ++it) {
+    const int s = it % S;
+    float* xs = reinterpret_cast<float*>(smem + (size_t)s * p.stage_bytes);
+    int64_t plane, r0, r1, in0, nin;
+    tile_rows(tau, plane, r0, r1, in0, nin);
+    if (p.bulk) {
+      if (tid == 0) {  // keep S-1 tiles in flight: refill the stage freed last iteration
+        const int64_t nxt = tau + (int64_t)(S - 1) * gridDim.x;
+        if (nxt < p.ntiles) issue(nxt, (it + S - 1) % S);
+      }
+      mbar_wait(&full[s], (uint32_t)(it / S) & 1u);
+    } else {
+      const float* src = p.x + (plane * p.H + in0) * W;
+      for (int64_t e = tid; e < nin * W; e += kP2Threads) xs[e] = __ldg(src + e);
+      __syncthreads();
+    }
+    // rows of this band handled by my group
+    const int64_t nr = r1 - r0;
+    const int64_t per = (nr + groups - 1) / groups;
+    const int64_t ra = r0 + grp * per;
+    const int64_t rb = ra + per < r1 ? ra + per : r1;
+    float* yp = p.y + plane * p.OH * OW;
+    for (int64_t c = col_lane; c < OW; c += ncol) {
+      const int64_t xc = c * p.sw;
+      bool done = false;
+      if constexpr (KH > 0) {
+        if (p.sh == 1) {  // overlapping row windows: register ring of row results
+          float ring[KH];
+          int64_t r = ra;
+          if (r < rb) {
+#pragma unroll
+            for (int i = 0; i < KH - 1; ++i) ring[i] = row_result<Op, KW>(xs + (r + i - in0) * W, xc, kw);
+          }
+          for (; r < rb; ++r) {
+            ring[KH - 1] = row_result<Op, KW>(xs + (r + KH - 1 - in0) * W, xc, kw);
+            float acc = ring[0];
+#pragma unroll
+            for (int i = 1; i < KH; ++i) acc = Op::combine(acc, ring[i]);
+            if (p.mode == 1) acc = __fmul_rn(acc, p.inv_area);
+            yp[r * OW + c] = acc;
+#pragma unroll
+            for (int i = 0; i < KH - 1; ++i) ring[i] = ring[i + 1];
+          }
+          done = true;
+        }
+      }
+      if (!done) {
+        for (int64_t r = ra; r < rb; ++r) {
+          const float* xr = xs + (r * p.sh - in0) * W;
+          float acc = row_result<Op, KW>(xr, xc, kw);
+          for (int dr = 1; dr < kh; ++dr) acc = Op::combine(acc, row_result<Op, KW>(xr + dr * W, xc, kw));
+          if (p.mode == 1) acc = __fmul_rn(acc, p.inv_area);
+          yp[r * OW + c] = acc;
+        }
+      }
+    }
+    __syncthreads();  // stage s is free for the refill issued next iteration
+  }
+}
+
+template <class Op>
+static cudaError_t launch_op(Pool2DParams& p, cudaStream_t stream, int grid, size_t smem) {
+  auto go = [&](auto kfn) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int64_t g = p.ntiles < grid ? p.ntiles : grid;
+    kfn<<<(unsigned)(g < 1 ? 1 : g), kP2Threads, smem, stream>>>(p);
+    note_launch();
+    return cudaGetLastError();
+  };
+  if (p.kh == 3 && p.kw == 3) return go(pool2d_kernel<Op, 3, 3>);
+  if (p.kh == 2 && p.kw == 2) return go(pool2d_kernel<Op, 2, 2>);
+  return go(pool2d_kernel<Op, 0, 0>);
+}
+
+cudaError_t launch_pool2d(Pool2DParams& p, cudaStream_t stream, int grid) {
+  // band size: keep a stage <= 64 KB
+  const int64_t row_bytes = p.W * 4;
+  int64_t max_in_rows = (64 * 1024) / row_bytes;
+  if (max_in_rows < p.kh) max_in_rows = p.kh;
+  int64_t band_rows = (max_in_rows - p.kh) / p.sh + 1;
+  if (band_rows > p.OH) band_rows = p.OH;
+  if (band_rows < 1) band_rows = 1;
+  p.band_rows = band_rows;
+  p.bands = (p.OH + band_rows - 1) / band_rows;
+  p.ntiles = p.planes * p.bands;
+  const int64_t in_rows = (band_rows - 1) * p.sh + p.kh;
+  p.stage_bytes = (uint32_t)(((in_rows * row_bytes) + 127) / 128 * 128);
+  int S = 4;
+  while (S > 1 && (size_t)S * p.stage_bytes + 256 > (size_t)kSmemBudget) --S;
+  if ((size_t)S * p.stage_bytes + 256 > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
+  if (!p.bulk) S = 1;
+  p.stages = S;
+  const size_t smem = (size_t)S * p.stage_bytes + 256;
+  if (p.mode == 0) return launch_op<OpMaxF32>(p, stream, grid, smem);
+  return launch_op<AvgOp>(p, stream, grid, smem);
+}
+
+}  // namespace ss

@@ -1,0 +1,73 @@
+// ss_internal.h -- host/device shared declarations of libss (not part of the ABI).
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace ss {
+
+constexpr int kOpSum = 0;
+constexpr int kOpMax = 1;
+constexpr int kSmemBudget = 227 * 1024;  // max dynamic smem per CTA on sm_100a
+constexpr int kConvTmaMaxK = 64;          // largest k served by the TMA conv kernel
+constexpr int kPoolTmaMaxW = 1024;        // largest w served by the TMA pool kernel
+
+// Parameters of the TMA tile kernel (slide1d.cu).  x and y are viewed as 2-D
+// arrays of 128-B rows starting at x_view / y_view (16-B aligned-down copies
+// of the caller's pointers); shift_x / shift_y are the element offsets of the
+// caller's x / y inside those views.
+struct alignas(64) Slide1DParams {
+  CUtensorMap tm_x_main;  // box {32, 256}, SWIZZLE_128B
+  CUtensorMap tm_x_halo;  // box {32, 8},   SWIZZLE_128B
+  CUtensorMap tm_y;       // box {32, 32},  SWIZZLE_128B (valid iff has_y_map)
+  const void* x_view;
+  void* y_view;
+  int64_t N, L, batch;
+  int64_t shift_x, shift_y;
+  int64_t x_full_elems;   // elements covered by tm_x_* (32 * full rows)
+  int64_t x_total_elems;  // shift_x + batch * N
+  int64_t tiles_per_row, ntiles;
+  int64_t w;              // window (pool)
+  uint32_t stage_bytes;
+  int stages;
+  int span;
+  int has_y_map;
+  float taps[kConvTmaMaxK];  // conv taps, zero-padded to the kernel's KT
+};
+
+// Parameters of the generic (any stride / alignment / size) kernels.
+struct GenericParams {
+  const void* x;
+  void* y;
+  int64_t N, L, batch, w, stride;
+  float taps[1024];  // SS_K_MAX
+};
+
+struct Pool2DParams {
+  const float* x;
+  float* y;
+  int64_t planes, H, W, OH, OW, kh, kw, sh, sw;
+  int64_t bands;        // output-row bands per plane
+  int64_t band_rows;    // output rows per band (last band may be shorter)
+  int64_t ntiles;       // planes * bands
+  uint32_t stage_bytes;
+  int stages;
+  int bulk;             // 1: rows are 16-B aligned -> cp.async.bulk staging
+  int mode;             // 0 max, 1 avg
+  float inv_area;       // 1 / (kh * kw) for avg
+};
+
+void note_launch();
+int num_sms(int device);
+
+cudaError_t launch_conv_tma(Slide1DParams& p, int KT, cudaStream_t stream, int grid);
+cudaError_t launch_pool_tma(Slide1DParams& p, int op, int dtype, int P, cudaStream_t stream,
+                            int grid);
+cudaError_t launch_pool_generic(const GenericParams& p, int op, int dtype, cudaStream_t stream,
+                                int grid);
+cudaError_t launch_conv_generic(const GenericParams& p, cudaStream_t stream, int grid);
+cudaError_t launch_pool2d(Pool2DParams& p, cudaStream_t stream, int grid);
+cudaError_t launch_pool2d_direct(const Pool2DParams& p, cudaStream_t stream, int grid);
+
+}  // namespace ss

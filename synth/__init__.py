@@ -97,3 +97,58 @@ def generate(dist: str, seed: int, n: int, start: int = 0, **kw) -> np.ndarray:
     if dist == "normal":
         return normal(seed, n, kw.get("sigma", 1.0), start)
     raise ValueError(dist)
+
+
+# ---- device twin (synth.cu -> libsynth.so) -----------------------------------
+import ctypes as _ct
+import os as _os
+import subprocess as _sp
+
+_SYN_DIR = _os.path.dirname(_os.path.abspath(__file__))
+_SYN_SO = _os.path.join(_SYN_DIR, "libsynth.so")
+_syn = None
+
+
+def build_device(force: bool = False) -> str:
+    src = _os.path.join(_SYN_DIR, "synth.cu")
+    if force or not _os.path.exists(_SYN_SO) or _os.path.getmtime(_SYN_SO) < _os.path.getmtime(src):
+        tmp = _SYN_SO + f".tmp{_os.getpid()}"
+        _sp.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a",
+                        "-O3", "--fmad=false", "-Xcompiler", "-fPIC", "-shared", "-o", tmp, src])
+        _os.replace(tmp, _SYN_SO)
+    return _SYN_SO
+
+
+def _dev():
+    global _syn
+    if _syn is None:
+        build_device()
+        L = _ct.CDLL(_SYN_SO)
+        i64, u64, vp = _ct.c_int64, _ct.c_uint64, _ct.c_void_p
+        L.synth_uniform01.argtypes = [vp, i64, u64, i64, vp]
+        L.synth_uniform_pm1.argtypes = [vp, i64, u64, i64, vp]
+        L.synth_randint.argtypes = [vp, i64, u64, i64, i64, i64, vp]
+        L.synth_normal.argtypes = [vp, i64, u64, _ct.c_double, i64, vp]
+        _syn = L
+    return _syn
+
+
+def fill_device(t, dist: str, seed: int, start: int = 0, stream=None, **kw):
+    """Fill the contiguous CUDA tensor `t` with elements [start, start+numel) of a stream."""
+    import torch
+    s = torch.cuda.current_stream().cuda_stream if stream is None else stream.cuda_stream
+    n = t.numel()
+    L = _dev()
+    if dist == "u01":
+        rc = L.synth_uniform01(t.data_ptr(), n, seed, start, s)
+    elif dist == "upm1":
+        rc = L.synth_uniform_pm1(t.data_ptr(), n, seed, start, s)
+    elif dist == "int":
+        rc = L.synth_randint(t.data_ptr(), n, seed, kw["lo"], kw["hi"], start, s)
+    elif dist == "normal":
+        rc = L.synth_normal(t.data_ptr(), n, seed, float(kw.get("sigma", 1.0)), start, s)
+    else:
+        raise ValueError(dist)
+    if rc != 0:
+        raise RuntimeError(f"synth kernel launch failed: cuda error {rc}")
+    return t
