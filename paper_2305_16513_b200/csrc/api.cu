@@ -104,10 +104,10 @@ static bool make_slide_params(Slide1DParams& p, const void* x, void* y, int64_t 
   p.x_full_elems = 32 * x_rows;
   const int64_t y_rows = (p.shift_y + batch * L) / 32;
   if (y_rows >= (int64_t(1) << 31) - 1024) return false;
-  if (!make_map(&p.tm_x_main, p.x_view, x_rows, 256)) return false;
+  if (!make_map(&p.tm_x_main, p.x_view, x_rows, kSlideTileRows)) return false;
   if (!make_map(&p.tm_x_halo, p.x_view, x_rows, 8)) return false;
-  p.has_y_map = y_rows >= 1 && make_map(&p.tm_y, p.y_view, y_rows, 32);
-  p.tiles_per_row = (L / 32 + 2 + 255) / 256;
+  p.has_y_map = y_rows >= 1 && make_map(&p.tm_y, p.y_view, y_rows, 16);
+  p.tiles_per_row = (L / 32 + 2 + kSlideTileRows - 1) / kSlideTileRows;
   p.ntiles = batch * p.tiles_per_row;
   return true;
 }

@@ -1,9 +1,9 @@
 // generic.cu -- direct-window kernels for the cases the TMA tile kernel does
 // not take (stride > 1, tiny or misaligned inputs, very long windows, k > 64).
 // One output per thread, window loop over the read-only path (Eq. 3 as
-// written; conv as Sec. 2.5, l.86-87).  Conv accumulates
-// with the same FMA sequence (j = 0..k-1, starting from 0) as the tile kernel,
-// so both produce bitwise-identical outputs.
+// written; conv as Sec. 2.5, l.86-87).  Conv uses the tile
+// kernel's association (even-tap and odd-tap FMA chains, then one add), so
+// both produce bitwise-identical outputs.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -36,9 +36,12 @@ __global__ void __launch_bounds__(256) conv_generic_kernel(const __grid_constant
        o += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = o / p.L, i = o - b * p.L;
     const float* xr = x + b * p.N + i * p.stride;
-    float acc = 0.0f;
-    for (int64_t j = 0; j < p.w; ++j) acc = __fmaf_rn(p.taps[j], __ldg(xr + j), acc);
-    y[o] = acc;
+    // even-tap and odd-tap partial sums, each in increasing j, then added:
+    // the association of the tile kernel (slide1d.cu ConvKind)
+    float s0 = 0.0f, s1 = 0.0f;
+    for (int64_t j = 0; j < p.w; j += 2) s0 = __fmaf_rn(p.taps[j], __ldg(xr + j), s0);
+    for (int64_t j = 1; j < p.w; j += 2) s1 = __fmaf_rn(p.taps[j], __ldg(xr + j), s1);
+    y[o] = __fadd_rn(s0, s1);
   }
 }
 

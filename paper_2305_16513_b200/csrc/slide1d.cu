@@ -3,27 +3,36 @@
 // product / 1-D convolution (Sec. 2.5, l.86-87).
 //
 // Tile skeleton:
-//   * Both x and y are viewed as 2-D arrays of 128-byte rows (32 elements).
-//   * A persistent CTA (one per SM) walks CTA tiles of 256 output rows
-//     (8192 outputs) of one batch row.  A producer warp stages the tile's
+//   * x and y are viewed as 2-D arrays of 128-byte rows (32 elements).
+//   * A persistent CTA (one per SM) walks CTA tiles of 240 output rows
+//     (7680 outputs) of one batch row.  A producer warp stages the tile's
 //     input rows plus the (w-1)-element halo rows HBM -> smem with TMA
 //     (cp.async.bulk.tensor.2d, SWIZZLE_128B) into a ring of stages guarded
 //     by full/empty mbarriers.
-//   * 8 consumer warps; lane t of warp i owns the 32 consecutive outputs of
-//     output row 32*i + t.  It reads its input run from the swizzled stage with
-//     conflict-free 128-bit LDS, evaluates its 32 windows in registers, and
-//     writes the row into a swizzled staging buffer that one lane stores with
-//     a TMA tensor store (rows crossing a batch-row edge use masked stores).
-//   * Window evaluation (the "P-block pivot" form of Alg. 2's prefix/suffix
-//     split): the 32 outputs are cut into blocks of
-//     P = 2^floor(log2 min(w,32)) outputs; for the block [g, g+P) every window
-//     contains the block's last element, so
-//         y_{g+r} = suffix_{g+r..g+P-1} (+) middle_{g+P..g+w-1} (+) prefix_{g+w..g+w+r-1}
-//     costing ~3 (+) per output whatever w is (order-preserving, so only
-//     associativity is used).
-//   * Conv: each thread keeps its 32+k-1 inputs in registers and runs
-//     32*k FMAs with the taps in the kernel-parameter constant bank, in the
-//     fixed tap order j = 0..k-1 (bitwise independent of tiling/sharding).
+//   * 15 consumer warps (+1 producer = 4 warps per SM sub-partition); lane t
+//     of warp i owns the 16 consecutive outputs [16*(t>>4), +16) of output row
+//     16*i + (t&15).  It reads its input run from the swizzled stage with
+//     128-bit ld.shared (the swizzle makes the 8 lanes of every LDS.128 phase
+//     hit 8 distinct bank groups), evaluates its 16 windows in registers and
+//     writes them into a swizzled staging buffer that one lane stores with a
+//     TMA tensor store (warps straddling a batch-row edge use masked stores).
+//   * The tile's misalignment SH = (first input element) mod 4 is uniform per
+//     tile, so each kind is instantiated for SH = 0..3 and the realignment of
+//     the input run is pure register renaming.
+//   * Pool (+, max): the "P-block pivot" form of Alg. 2's prefix/suffix split
+//     (PAPER.md l.113-134): the 16 outputs are cut into blocks of
+//     P = 2^floor(log2 min(w,16)) outputs; every window starting in the block
+//     [g, g+P) contains the block's last element, so
+//        y_{g+r} = suffix_{g+r..g+P-1} (+) middle_{g+P..g+w-1} (+) prefix_{g+w..g+w+r-1}
+//     ~3 (+) per output whatever w is; order-preserving (associativity only).
+//   * Conv: output pairs accumulated with FFMA2 (fma.rn.f32x2, two IEEE fp32
+//     FMAs per instruction): an even-tap and an odd-tap partial sum per
+//     output, each in increasing tap order from 0, added at the end -- an
+//     association fixed by the tap index alone, so outputs are bitwise
+//     independent of tiling and identical to the generic kernel.  Taps are
+//     processed in passes of 32 to bound register use.
+//   * Tiles that read past the last full 128-B row of x (the very end of the
+//     array) take a compact direct-window path from global memory.
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -33,231 +42,306 @@
 
 namespace ss {
 
-constexpr int kWarps = 8;                    // consumer warps per CTA
+constexpr int kWarps = kSlideWarps;          // consumer warps per CTA
 constexpr int kThreads = (kWarps + 1) * 32;  // + 1 producer warp
-constexpr int kTileRows = kWarps * 32;       // 256 output rows = 8192 outputs
+constexpr int kR = 16;                       // outputs per thread
+constexpr int kTileRows = kSlideTileRows;    // 240 output rows = 7680 outputs
+constexpr int kWarpRows = 16;                // output rows per warp
 constexpr int kHaloBoxRows = 8;
 constexpr int kStageAlign = 1024;
+constexpr int kStagingBytes = kWarpRows * 128;  // 2 KB per warp buffer
+constexpr int kConvPass = 32;                   // taps per register pass
 
-struct TileGeom {
-  int64_t b;        // batch row
-  int64_t yrow0;    // first y-view row of the CTA tile
-  int64_t e_y;      // y-view element index of output 0 of batch row b
-  int64_t L;        // outputs per batch row
-  int64_t xrow0;    // first x-view row loaded (may be -1)
-  int m;            // element offset of the tile's first input inside row xrow0
-  int halo_boxes;   // 8-row halo boxes loaded after the 256 main rows
-  bool empty;
-};
-
-__device__ __forceinline__ int64_t floor_div32(int64_t a) { return a >= 0 ? a / 32 : -((31 - a) / 32); }
-
-__device__ __forceinline__ TileGeom tile_geom(const Slide1DParams& p, int64_t tau) {
-  TileGeom g;
-  g.b = tau / p.tiles_per_row;
-  int64_t j = tau - g.b * p.tiles_per_row;
-  g.L = p.L;
-  g.e_y = p.shift_y + g.b * p.L;
-  g.yrow0 = g.e_y / 32 + (int64_t)kTileRows * j;
-  g.empty = 32 * g.yrow0 >= g.e_y + p.L;
-  int64_t ix0 = p.shift_x + g.b * p.N + (32 * g.yrow0 - g.e_y);
-  g.xrow0 = floor_div32(ix0);
-  g.m = (int)(ix0 - 32 * g.xrow0);
-  int64_t last_local = 32 * (kTileRows - 1) + g.m + 31 + p.span;
-  int nrows = (int)(last_local / 32) + 1;
-  int halo = nrows - kTileRows;
-  g.halo_boxes = halo > 0 ? (halo + kHaloBoxRows - 1) / kHaloBoxRows : 0;
-  return g;
+// ------------------------------------------------------------- smem access
+__device__ __forceinline__ uint32_t chunk_addr(uint32_t st_s, int c) {
+  return st_s + swz128(16u * (uint32_t)c);
+}
+__device__ __forceinline__ void lds_v4(uint32_t a, uint32_t& x0, uint32_t& x1, uint32_t& x2,
+                                       uint32_t& x3) {
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+               : "r"(a));
+}
+__device__ __forceinline__ void lds_v2x64(uint32_t a, uint64_t& lo, uint64_t& hi) {
+  asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "r"(a));
+}
+__device__ __forceinline__ uint64_t pack2(uint32_t lo, uint32_t hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+__device__ __forceinline__ void unpack2(uint64_t v, uint32_t& lo, uint32_t& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+}
+// two IEEE fp32 FMAs: d.{lo,hi} = a.{lo,hi} * b.{lo,hi} + c.{lo,hi}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
 }
 
-// ------------------------------------------------------------- input loading
-// Element e of a stage lives at byte swz128(4e) from the stage base.
-template <typename T>
-struct StageReader {
-  const uint8_t* stage;   // generic pointer to the stage (1024-B aligned)
-  bool slow;              // tile touches x-view elements past the TMA-covered rows
-  int64_t gbase;          // x-view element index of stage element 0
-  int64_t full_elems;     // x-view elements covered by the tensor map
-  int64_t total_elems;    // x-view elements that exist
-  const T* xg;            // x-view element 0 in global memory
+// v[i] = stage element (4*c0 + SH + i), i < NV  (SH compile-time: no shuffling)
+template <typename T, int SH, int NV>
+__device__ __forceinline__ void load_run(uint32_t st_s, int c0, T (&v)[NV]) {
+  constexpr int NC = (SH + NV + 3) / 4;
+  uint32_t raw[4 * NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+    lds_v4(chunk_addr(st_s, c0 + c), raw[4 * c], raw[4 * c + 1], raw[4 * c + 2], raw[4 * c + 3]);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = bitcast<T>(raw[SH + i]);
+}
 
-  __device__ __forceinline__ T elem(int e) const {
-    if (!slow) return *reinterpret_cast<const T*>(stage + swz128(4u * (uint32_t)e));
-    int64_t g = gbase + e;
-    if (g >= 0 && g < full_elems) return *reinterpret_cast<const T*>(stage + swz128(4u * (uint32_t)e));
-    if (g >= full_elems && g < total_elems) return __ldg(xg + g);
-    return T(0);
-  }
-  // 4 elements of chunk c (elements 4c..4c+3)
-  __device__ __forceinline__ void chunk(int c, T (&q)[4]) const {
-    int64_t g = gbase + 4 * (int64_t)c;
-    if (!slow || (g >= 0 && g + 3 < full_elems)) {
-      const uint4 v = *reinterpret_cast<const uint4*>(stage + swz128(16u * (uint32_t)c));
-      q[0] = bitcast<T>(v.x); q[1] = bitcast<T>(v.y); q[2] = bitcast<T>(v.z); q[3] = bitcast<T>(v.w);
-    } else {
+// v[i] = stage element (e0 + i), i < NV, with a runtime misalignment e0 & 3
+// (2-stage select network).
+template <typename T, int NV>
+__device__ __forceinline__ void load_run_rt(uint32_t st_s, int e0, T (&v)[NV]) {
+  constexpr int NC = (NV + 3 + 3) / 4;
+  uint32_t raw[4 * NC];
+  const int c0 = e0 >> 2;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) q[e] = elem(4 * c + e);
-    }
-  }
-  // v[i] = element (p0 + i), i < NV; 128-bit loads plus a 2-stage select
-  // network for the runtime misalignment p0 & 3.
-  template <int NV>
-  __device__ __forceinline__ void run(int p0, T (&v)[NV]) const {
-    constexpr int NC = (NV + 3 + 3) / 4;
-    T raw[4 * NC];
-    const int c0 = p0 >> 2;
+  for (int c = 0; c < NC; ++c)
+    lds_v4(chunk_addr(st_s, c0 + c), raw[4 * c], raw[4 * c + 1], raw[4 * c + 2], raw[4 * c + 3]);
+  const int sh = e0 & 3;
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      T q[4];
-      chunk(c0 + c, q);
-      raw[4 * c + 0] = q[0]; raw[4 * c + 1] = q[1]; raw[4 * c + 2] = q[2]; raw[4 * c + 3] = q[3];
-    }
-    const int sh = p0 & 3;
-    if (sh & 1) {
+  for (int i = 0; i < 4 * NC - 1; ++i) raw[i] = (sh & 1) ? raw[i + 1] : raw[i];
 #pragma unroll
-      for (int i = 0; i < 4 * NC - 1; ++i) raw[i] = raw[i + 1];
-    }
-    if (sh & 2) {
+  for (int i = 0; i < 4 * NC - 3; ++i) raw[i] = (sh & 2) ? raw[i + 2] : raw[i];
 #pragma unroll
-      for (int i = 0; i < 4 * NC - 3; ++i) raw[i] = raw[i + 2];
-    }
-#pragma unroll
-    for (int i = 0; i < NV; ++i) v[i] = raw[i];
-  }
-};
+  for (int i = 0; i < NV; ++i) v[i] = bitcast<T>(raw[i]);
+}
 
 // ------------------------------------------------------------- the kinds
-// Conv: y_r = sum_{j<KT} taps[j] * x_{p0+r+j}; taps beyond k are zero.
+// Conv: y_r = sum_{j<KT} taps[j] * x_{p0+r+j} (taps beyond k are zero),
+// evaluated as two partial sums, over the even taps and over the odd taps,
+// each accumulated with fp32 FMA in increasing j from 0, then added:
+//     y_r = fl( S_even(r) + S_odd(r) ).
+// The association depends only on the tap index, so every output is bitwise
+// independent of tiling/sharding and equal to the generic kernel's.  It lets
+// FFMA2 (two FMAs per instruction) read every input pair as an aligned
+// register pair: for tap parity c the output pairs start at r0 with
+// (SH + r0 + c) even, so x_{p0+r0+j}, x_{p0+r0+j+1} is (raw[2m], raw[2m+1]).
 template <int KT>
 struct ConvKind {
   using T = float;
-  static constexpr int kSpan = (32 + KT - 1) - 26;  // max elements read past the own 32 (see StageReader::run)
-  template <class R>
-  static __device__ __forceinline__ void compute(const Slide1DParams& p, const R& rd, int p0,
-                                                 float (&y)[32]) {
-    constexpr int NV = 32 + KT - 1;
-    float v[NV];
-    rd.template run<NV>(p0, v);
-#pragma unroll
-    for (int r = 0; r < 32; ++r) y[r] = 0.0f;
-#pragma unroll
-    for (int j = 0; j < KT; ++j) {
-      const float f = p.taps[j];
-#pragma unroll
-      for (int r = 0; r < 32; ++r) y[r] = __fmaf_rn(f, v[r + j], y[r]);
-    }
-  }
-};
+  // elements read past the thread's first input (max over SH): chunks cover
+  // [0, SH + 16 + KT) rounded up to a chunk
+  static constexpr int kSpan = 4 * ((3 + kR + KT + 3) / 4) - kR;
 
-// Pool with P-block pivots, P <= w < 2P (P < 32), all in registers.
-template <class Op, int P>
-struct PoolKind {
-  using T = typename Op::T;
-  static constexpr int kSpan = (32 + 2 * P - 2) - 26;
-  template <class R>
-  static __device__ __forceinline__ void compute(const Slide1DParams& p, const R& rd, int p0,
-                                                 T (&y)[32]) {
-    constexpr int NV = 32 + 2 * P - 2;
-    T v[NV];
-    rd.template run<NV>(p0, v);
-    const int w = (int)p.w;
-    const int s = w - P;  // in [0, P)
-    // u[i] = v[i + s] for i in [P, 32 + P - 1): barrel shift by s
-    T u[NV];
+  template <int SH>
+  static __device__ __forceinline__ void compute(const Slide1DParams& p, uint32_t st_s, int c0,
+                                                 float (&y)[kR]) {
+    constexpr int PI0 = SH & 1;        // first output of the pairs of even taps is -PI0 (mod 2)
+    constexpr int PI1 = (SH + 1) & 1;  // ... of odd taps
+    constexpr int N0 = kR / 2 + PI0, N1 = kR / 2 + PI1;
+    float2 A0[N0], A1[N1];  // A_c[i]: outputs (2i - PI_c, 2i - PI_c + 1)
 #pragma unroll
-    for (int i = 0; i < NV; ++i) u[i] = v[i];
+    for (int i = 0; i < N0; ++i) A0[i] = make_float2(0.0f, 0.0f);
 #pragma unroll
-    for (int k = 1; k < P; k <<= 1) {
-      if (s & k) {
+    for (int i = 0; i < N1; ++i) A1[i] = make_float2(0.0f, 0.0f);
 #pragma unroll
-        for (int i = 0; i + k < NV; ++i) u[i] = u[i + k];
-      }
-    }
+    for (int j0 = 0; j0 < KT; j0 += kConvPass) {
+      constexpr int JMAX = KT < kConvPass ? KT : kConvPass;
+      const int J = KT - j0 < JMAX ? KT - j0 : JMAX;  // compile-time after unrolling
+      // raw elements [0, SH + 16 + J) relative to chunk c0 + j0/4 (j0 % 4 == 0)
+      constexpr int NC = (SH + kR + JMAX + 3) / 4;
+      float2 E[2 * NC];  // E[m] = (raw[2m], raw[2m+1])
 #pragma unroll
-    for (int g = 0; g < 32; g += P) {
-      T a[P];
-      a[P - 1] = v[g + P - 1];
-#pragma unroll
-      for (int i = P - 2; i >= 0; --i) a[i] = Op::combine(v[g + i], a[i + 1]);
-      T m = Op::identity();
-#pragma unroll
-      for (int i = 0; i < P - 1; ++i)
-        if (i < s) m = Op::combine(m, v[g + P + i]);
-      y[g] = Op::combine(a[0], m);
-      T pre = m;
-#pragma unroll
-      for (int r = 1; r < P; ++r) {
-        pre = Op::combine(pre, u[g + P + r - 1]);
-        y[g + r] = Op::combine(a[r], pre);
-      }
-    }
-  }
-};
-
-// Pool with one pivot per thread (P = 32, w >= 32): the middle is streamed.
-template <class Op>
-struct PoolKind<Op, 32> {
-  using T = typename Op::T;
-  static constexpr int kSpan = -1;  // runtime: w + 5
-  template <class R>
-  static __device__ __forceinline__ void compute(const Slide1DParams& p, const R& rd, int p0,
-                                                 T (&y)[32]) {
-    const int w = (int)p.w;
-    T a[32];
-    rd.template run<32>(p0, a);
-#pragma unroll
-    for (int i = 30; i >= 0; --i) a[i] = Op::combine(a[i], a[i + 1]);
-    // middle: elements [p0+32, p0+w)
-    T m0 = Op::identity(), m1 = Op::identity(), m2 = Op::identity(), m3 = Op::identity();
-    const int s0 = p0 + 32, e0 = p0 + w;
-    if (e0 > s0) {
-      const int cs = s0 >> 2, ce = (e0 - 1) >> 2;
-      {  // first chunk (partial)
-        T q[4];
-        rd.chunk(cs, q);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int idx = 4 * cs + e;
-          if (idx >= s0 && idx < e0) m0 = Op::combine(m0, q[e]);
+      for (int c = 0; c < NC; ++c) {
+        if (4 * c < SH + kR + J) {
+          uint32_t a0, a1, a2, a3;
+          lds_v4(chunk_addr(st_s, c0 + j0 / 4 + c), a0, a1, a2, a3);
+          E[2 * c] = make_float2(__uint_as_float(a0), __uint_as_float(a1));
+          E[2 * c + 1] = make_float2(__uint_as_float(a2), __uint_as_float(a3));
+        } else {
+          E[2 * c] = E[2 * c + 1] = make_float2(0.0f, 0.0f);
         }
       }
-      int c = cs + 1;
-      for (; c + 1 < ce; c += 2) {  // full chunks
-        T q[4], q2[4];
-        rd.chunk(c, q);
-        rd.chunk(c + 1, q2);
-        m0 = Op::combine(m0, Op::combine(q[0], q2[0]));
-        m1 = Op::combine(m1, Op::combine(q[1], q2[1]));
-        m2 = Op::combine(m2, Op::combine(q[2], q2[2]));
-        m3 = Op::combine(m3, Op::combine(q[3], q2[3]));
-      }
-      for (; c <= ce; ++c) {  // remaining (last may be partial)
-        T q[4];
-        rd.chunk(c, q);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int idx = 4 * c + e;
-          if (idx < e0) {
-            if (e == 0) m0 = Op::combine(m0, q[e]);
-            if (e == 1) m1 = Op::combine(m1, q[e]);
-            if (e == 2) m2 = Op::combine(m2, q[e]);
-            if (e == 3) m3 = Op::combine(m3, q[e]);
+      for (int jj = 0; jj < JMAX; ++jj) {
+        if (jj < J) {
+          const float f = p.taps[j0 + jj];
+          const float2 f2 = make_float2(f, f);
+          if ((jj & 1) == 0) {
+#pragma unroll
+            for (int i = 0; i < N0; ++i) {
+              const int idx = SH + 2 * i - PI0 + jj;  // even by construction
+              A0[i] = __ffma2_rn(E[idx >> 1], f2, A0[i]);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < N1; ++i) {
+              const int idx = SH + 2 * i - PI1 + jj;
+              A1[i] = __ffma2_rn(E[idx >> 1], f2, A1[i]);
+            }
           }
         }
       }
     }
-    const T m = Op::combine(Op::combine(m0, m1), Op::combine(m2, m3));
-    T b[31];
-    rd.template run<31>(p0 + w, b);
-    y[0] = Op::combine(a[0], m);
-    T pre = m;
 #pragma unroll
-    for (int r = 1; r < 32; ++r) {
-      pre = Op::combine(pre, b[r - 1]);
-      y[r] = Op::combine(a[r], pre);
+    for (int r = 0; r < kR; ++r) {
+      const int i0 = (r + PI0) >> 1, i1 = (r + PI1) >> 1;
+      const float s0 = ((r + PI0) & 1) ? A0[i0].y : A0[i0].x;
+      const float s1 = ((r + PI1) & 1) ? A1[i1].y : A1[i1].x;
+      y[r] = __fadd_rn(s0, s1);
     }
   }
 };
+
+// Pool with P-block pivots.  P < 16: P <= w < 2P, own run and middle in
+// registers.  P = 16: w >= 16, the middle x[p0+16, p0+w) is streamed.
+template <class Op, int P>
+struct PoolKind {
+  using T = typename Op::T;
+  static constexpr int kOwn = P < 16 ? kR + P - 1 : kR;  // own run length
+  static constexpr int kSpan = -1;                        // runtime: w + 20
+
+  template <int SH>
+  static __device__ __forceinline__ void compute(const Slide1DParams& p, uint32_t st_s, int c0,
+                                                 T (&y)[kR]) {
+    const int w = (int)p.w;
+    T v[kOwn];
+    load_run<T, SH, kOwn>(st_s, c0, v);
+    // tail run: tl[i] = x[p0 + w + i], i < 15 (runtime misalignment)
+    T tl[kR - 1];
+    load_run_rt<T, kR - 1>(st_s, 4 * c0 + SH + w, tl);
+    if constexpr (P < 16) {
+      const int s = w - P;  // middle length per block, in [0, P)
+#pragma unroll
+      for (int g = 0; g < kR; g += P) {
+        T a[P];
+        a[P - 1] = v[g + P - 1];
+#pragma unroll
+        for (int i = P - 2; i >= 0; --i) a[i] = Op::combine(v[g + i], a[i + 1]);
+        T m = Op::identity();
+#pragma unroll
+        for (int i = 0; i < P - 1; ++i)
+          if (i < s) m = Op::combine(m, v[g + P + i]);
+        y[g] = Op::combine(a[0], m);
+        T pre = m;
+#pragma unroll
+        for (int r = 1; r < P; ++r) {
+          pre = Op::combine(pre, tl[g + r - 1]);
+          y[g + r] = Op::combine(a[r], pre);
+        }
+      }
+    } else {
+      T a[kR];
+      a[kR - 1] = v[kR - 1];
+#pragma unroll
+      for (int i = kR - 2; i >= 0; --i) a[i] = Op::combine(v[i], a[i + 1]);
+      // middle: stage elements [p0 + 16, p0 + w) with p0 = 4*c0 + SH
+      T m0 = Op::identity(), m1 = Op::identity(), m2 = Op::identity(), m3 = Op::identity();
+      const int e0 = 4 * c0 + SH + w;  // one past the middle
+      if (w > kR) {
+        const int cs = c0 + 4, ce = (e0 - 1) >> 2;  // chunk cs starts at element p0 + 16 - SH
+        {
+          uint32_t q0, q1, q2, q3;
+          lds_v4(chunk_addr(st_s, cs), q0, q1, q2, q3);
+          const int n = e0 - 4 * cs;  // elements of this chunk before e0
+          if (SH <= 0 && 0 < n) m0 = Op::combine(m0, bitcast<T>(q0));
+          if (SH <= 1 && 1 < n) m1 = Op::combine(m1, bitcast<T>(q1));
+          if (SH <= 2 && 2 < n) m2 = Op::combine(m2, bitcast<T>(q2));
+          if (3 < n) m3 = Op::combine(m3, bitcast<T>(q3));
+        }
+        int c = cs + 1;
+#pragma unroll 2
+        for (; c < ce; ++c) {
+          uint32_t q0, q1, q2, q3;
+          lds_v4(chunk_addr(st_s, c), q0, q1, q2, q3);
+          m0 = Op::combine(m0, bitcast<T>(q0));
+          m1 = Op::combine(m1, bitcast<T>(q1));
+          m2 = Op::combine(m2, bitcast<T>(q2));
+          m3 = Op::combine(m3, bitcast<T>(q3));
+        }
+        if (c == ce) {
+          uint32_t q0, q1, q2, q3;
+          lds_v4(chunk_addr(st_s, c), q0, q1, q2, q3);
+          const int n = e0 - 4 * c;
+          m0 = Op::combine(m0, bitcast<T>(q0));
+          if (1 < n) m1 = Op::combine(m1, bitcast<T>(q1));
+          if (2 < n) m2 = Op::combine(m2, bitcast<T>(q2));
+          if (3 < n) m3 = Op::combine(m3, bitcast<T>(q3));
+        }
+      }
+      const T m = Op::combine(Op::combine(m0, m1), Op::combine(m2, m3));
+      y[0] = Op::combine(a[0], m);
+      T pre = m;
+#pragma unroll
+      for (int r = 1; r < kR; ++r) {
+        pre = Op::combine(pre, tl[r - 1]);
+        y[r] = Op::combine(a[r], pre);
+      }
+    }
+  }
+};
+
+template <class Kind>
+struct SlowPath;  // direct windows from global memory (array-end tiles)
+
+template <int KT>
+struct SlowPath<ConvKind<KT>> {
+  static __device__ __forceinline__ float eval(const Slide1DParams& p, const float* x) {
+    float s0 = 0.0f, s1 = 0.0f;  // even taps, odd taps (same association as compute())
+    for (int j = 0; j < (int)p.w; j += 2) s0 = __fmaf_rn(p.taps[j], __ldg(x + j), s0);
+    for (int j = 1; j < (int)p.w; j += 2) s1 = __fmaf_rn(p.taps[j], __ldg(x + j), s1);
+    return __fadd_rn(s0, s1);
+  }
+};
+template <class Op, int P>
+struct SlowPath<PoolKind<Op, P>> {
+  static __device__ __forceinline__ typename Op::T eval(const Slide1DParams& p,
+                                                        const typename Op::T* x) {
+    typename Op::T acc = __ldg(x);
+    for (int j = 1; j < (int)p.w; ++j) acc = Op::combine(acc, __ldg(x + j));
+    return acc;
+  }
+};
+
+// ------------------------------------------------------------- tile walk
+struct TileCursor {
+  int64_t b, j;  // batch row, tile within the row
+  __device__ __forceinline__ void init(int64_t tau, int64_t tpr) {
+    b = tau / tpr;
+    j = tau - b * tpr;
+  }
+  __device__ __forceinline__ void advance(int64_t step, int64_t tpr) {
+    j += step;
+    while (j >= tpr) {
+      j -= tpr;
+      ++b;
+    }
+  }
+};
+
+struct TileGeom {
+  int64_t yrow0;  // first y-view row of the CTA tile
+  int64_t e_y;    // y-view element index of output 0 of batch row b
+  int64_t xrow0;  // first x-view row loaded (may be -1: TMA zero-fills)
+  int m;          // element offset of the tile's first input inside row xrow0
+  int halo_boxes; // 8-row halo boxes loaded after the main rows
+  bool empty;
+  bool slow;      // reads past the TMA-covered part of x
+};
+
+__device__ __forceinline__ int64_t floor_div32(int64_t a) {
+  return a >= 0 ? (a >> 5) : -((31 - a) >> 5);
+}
+
+__device__ __forceinline__ TileGeom tile_geom(const Slide1DParams& p, const TileCursor& tc) {
+  TileGeom g;
+  g.e_y = p.shift_y + tc.b * p.L;
+  g.yrow0 = (g.e_y >> 5) + (int64_t)kTileRows * tc.j;
+  g.empty = 32 * g.yrow0 >= g.e_y + p.L;
+  const int64_t ix0 = p.shift_x + tc.b * p.N + (32 * g.yrow0 - g.e_y);
+  g.xrow0 = floor_div32(ix0);
+  g.m = (int)(ix0 - 32 * g.xrow0);
+  const int last_local = 32 * (kTileRows - 1) + g.m + 31 + p.span;
+  const int halo = (last_local >> 5) + 1 - kTileRows;
+  g.halo_boxes = halo > 0 ? (halo + kHaloBoxRows - 1) / kHaloBoxRows : 0;
+  g.slow = 32 * g.xrow0 + last_local >= p.x_full_elems;
+  return g;
+}
 
 // ------------------------------------------------------------- the kernel
 template <class Kind>
@@ -269,9 +353,10 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
       (reinterpret_cast<uintptr_t>(smem_raw) + kStageAlign - 1) & ~uintptr_t(kStageAlign - 1));
   const int S = p.stages;
   const uint32_t stage_bytes = p.stage_bytes;
-  uint8_t* staging = smem + (size_t)S * stage_bytes;                  // kWarps * 2 * 4 KB
-  uint64_t* full = reinterpret_cast<uint64_t*>(staging + kWarps * 2 * 4096);
+  uint8_t* staging = smem + (size_t)S * stage_bytes;  // kWarps * 2 * 2 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + kWarps * 2 * kStagingBytes);
   uint64_t* empty = full + S;
+  const uint32_t smem_s = smem_u32(smem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -287,24 +372,31 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
     if (p.has_y_map) prefetch_tmap(&p.tm_y);
   }
   __syncthreads();
+  const int64_t tpr = p.tiles_per_row;
 
   if (warp == kWarps) {
-    // ---------------- producer: one elected lane issues the TMA loads
+    // ---------------- producer: one lane issues the TMA loads
     if (lane == 0) {
       int it = 0;
-      for (int64_t tau = blockIdx.x; tau < p.ntiles; tau += gridDim.x) {
-        const TileGeom g = tile_geom(p, tau);
+      TileCursor tc;
+      tc.init(blockIdx.x, tpr);
+      for (int64_t tau = blockIdx.x; tau < p.ntiles; tau += gridDim.x, tc.advance(gridDim.x, tpr)) {
+        const TileGeom g = tile_geom(p, tc);
         if (g.empty) continue;
         const int s = it % S;
         const uint32_t ph = (uint32_t)(it / S) & 1u;
         mbar_wait(&empty[s], ph ^ 1u);
         uint8_t* dst = smem + (size_t)s * stage_bytes;
-        const uint32_t bytes = (uint32_t)(kTileRows + kHaloBoxRows * g.halo_boxes) * 128u;
-        mbar_arrive_expect_tx(&full[s], bytes);
-        tma_load_2d(dst, &p.tm_x_main, 0, (int32_t)g.xrow0, &full[s]);
-        for (int h = 0; h < g.halo_boxes; ++h)
-          tma_load_2d(dst + (size_t)(kTileRows + kHaloBoxRows * h) * 128, &p.tm_x_halo, 0,
-                      (int32_t)(g.xrow0 + kTileRows + kHaloBoxRows * h), &full[s]);
+        if (g.slow) {  // consumers read global memory directly for this tile
+          mbar_arrive(&full[s]);
+        } else {
+          const uint32_t bytes = (uint32_t)(kTileRows + kHaloBoxRows * g.halo_boxes) * 128u;
+          mbar_arrive_expect_tx(&full[s], bytes);
+          tma_load_2d(dst, &p.tm_x_main, 0, (int32_t)g.xrow0, &full[s]);
+          for (int h = 0; h < g.halo_boxes; ++h)
+            tma_load_2d(dst + (size_t)(kTileRows + kHaloBoxRows * h) * 128, &p.tm_x_halo, 0,
+                        (int32_t)(g.xrow0 + kTileRows + kHaloBoxRows * h), &full[s]);
+        }
         ++it;
       }
     }
@@ -312,47 +404,59 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
   }
 
   // ---------------- consumers
-  int it = 0;
-  uint8_t* my_staging = staging + warp * 2 * 4096;
+  const int row_in_warp = lane & 15, half = lane >> 4;
+  const int row = kWarpRows * warp + row_in_warp;  // output row within the tile
+  uint8_t* my_staging = staging + warp * 2 * kStagingBytes;
   const uint32_t my_staging_s = smem_u32(my_staging);
-  for (int64_t tau = blockIdx.x; tau < p.ntiles; tau += gridDim.x) {
-    const TileGeom g = tile_geom(p, tau);
+  int it = 0;
+  TileCursor tc;
+  tc.init(blockIdx.x, tpr);
+  for (int64_t tau = blockIdx.x; tau < p.ntiles; tau += gridDim.x, tc.advance(gridDim.x, tpr)) {
+    const TileGeom g = tile_geom(p, tc);
     if (g.empty) continue;
     const int s = it % S;
     const uint32_t ph = (uint32_t)(it / S) & 1u;
-    const uint8_t* st = smem + (size_t)s * stage_bytes;
+    const uint32_t st_s = smem_s + (uint32_t)s * stage_bytes;
 
-    const int64_t wrow0 = g.yrow0 + 32 * warp;  // first y-view row of this warp
-    const int64_t o_first = 32 * wrow0, o_end = 32 * (wrow0 + 32);
-    const bool warp_active = o_first < g.e_y + g.L && o_end > g.e_y;
-    const bool warp_full = o_first >= g.e_y && o_end <= g.e_y + g.L;
+    const int64_t wrow0 = g.yrow0 + kWarpRows * warp;  // first y-view row of this warp
+    const int64_t y_lo = g.e_y, y_hi = g.e_y + p.L;     // valid outputs [y_lo, y_hi)
+    const bool warp_active = 32 * wrow0 < y_hi && 32 * (wrow0 + kWarpRows) > y_lo;
+    const bool warp_full = 32 * wrow0 >= y_lo && 32 * (wrow0 + kWarpRows) <= y_hi;
+    const int64_t o0 = 32 * (wrow0 + row_in_warp) + kR * half;  // my first output (y view)
 
     mbar_wait(&full[s], ph);
-    T y[32];
-    if (warp_active) {
-      StageReader<T> rd;
-      rd.stage = st;
-      rd.gbase = 32 * g.xrow0;
-      rd.full_elems = p.x_full_elems;
-      rd.total_elems = p.x_total_elems;
-      rd.xg = reinterpret_cast<const T*>(p.x_view);
-      const int64_t last_read = rd.gbase + 32 * (kTileRows - 1) + g.m + 31 + p.span;
-      rd.slow = (rd.gbase < 0) || (last_read >= p.x_full_elems);
-      const int p0 = 32 * (32 * warp + lane) + g.m;
-      Kind::compute(p, rd, p0, y);
+    T y[kR];
+    if (warp_active && !g.slow) {
+      const int p0 = 32 * row + kR * half + g.m;  // stage element of my first input
+      const int c0 = p0 >> 2;
+      switch (g.m & 3) {
+        case 0: Kind::template compute<0>(p, st_s, c0, y); break;
+        case 1: Kind::template compute<1>(p, st_s, c0, y); break;
+        case 2: Kind::template compute<2>(p, st_s, c0, y); break;
+        default: Kind::template compute<3>(p, st_s, c0, y); break;
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 
     if (warp_active) {
-      if (warp_full && p.has_y_map) {
+      if (g.slow) {
+        // array-end tile: direct windows from global memory (valid outputs only)
+        const T* xg = reinterpret_cast<const T*>(p.x_view);
+        T* yv = reinterpret_cast<T*>(p.y_view);
+        const int64_t dxy = p.shift_x + tc.b * p.N - g.e_y;  // x-view index = o + dxy
+        for (int r = 0; r < kR; ++r) {
+          const int64_t o = o0 + r;
+          if (o >= y_lo && o < y_hi) yv[o] = SlowPath<Kind>::eval(p, xg + o + dxy);
+        }
+      } else if (warp_full && p.has_y_map) {
         const int buf = it & 1;
         if (lane == 0) bulk_wait_read<1>();
         __syncwarp();
-        const uint32_t base = my_staging_s + buf * 4096;
+        const uint32_t base = my_staging_s + buf * kStagingBytes;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t off = swz128((uint32_t)lane * 128u + 16u * c);
+        for (int c = 0; c < kR / 4; ++c) {
+          const uint32_t off = swz128((uint32_t)row_in_warp * 128u + 64u * half + 16u * c);
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(base + off),
                        "r"(bitcast<uint32_t>(y[4 * c + 0])), "r"(bitcast<uint32_t>(y[4 * c + 1])),
                        "r"(bitcast<uint32_t>(y[4 * c + 2])), "r"(bitcast<uint32_t>(y[4 * c + 3]))
@@ -361,16 +465,15 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&p.tm_y, 0, (int32_t)wrow0, my_staging + buf * 4096);
+          tma_store_2d(&p.tm_y, 0, (int32_t)wrow0, my_staging + buf * kStagingBytes);
           bulk_commit();
         }
       } else {
         T* yv = reinterpret_cast<T*>(p.y_view);
-        const int64_t orow = 32 * (wrow0 + lane);
 #pragma unroll
-        for (int r = 0; r < 32; ++r) {
-          const int64_t o = orow + r;
-          if (o >= g.e_y && o < g.e_y + g.L) yv[o] = y[r];
+        for (int r = 0; r < kR; ++r) {
+          const int64_t o = o0 + r;
+          if (o >= y_lo && o < y_hi) yv[o] = y[r];
         }
       }
     }
@@ -382,12 +485,13 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
 // ------------------------------------------------------------- host launch
 template <class Kind>
 static cudaError_t launch_kind(Slide1DParams& p, cudaStream_t stream, int grid) {
-  int span = Kind::kSpan >= 0 ? Kind::kSpan : (int)p.w + 5;
+  const int span = Kind::kSpan >= 0 ? Kind::kSpan : (int)p.w + 20;
   p.span = span;
-  const int max_halo_rows = (int)((32 * (kTileRows - 1) + 31 + 31 + span) / 32) + 1 - kTileRows;
-  const int halo_cap = ((max_halo_rows + kHaloBoxRows - 1) / kHaloBoxRows) * kHaloBoxRows;
-  p.stage_bytes = (uint32_t)(kTileRows + (halo_cap > 0 ? halo_cap : 0)) * 128u;
-  const size_t fixed = kWarps * 2 * 4096 + kStageAlign + 256;
+  const int max_halo_rows = (32 * (kTileRows - 1) + 31 + 31 + span) / 32 + 1 - kTileRows;
+  const int halo_cap =
+      max_halo_rows > 0 ? ((max_halo_rows + kHaloBoxRows - 1) / kHaloBoxRows) * kHaloBoxRows : 0;
+  p.stage_bytes = (uint32_t)(kTileRows + halo_cap) * 128u;
+  const size_t fixed = (size_t)kWarps * 2 * kStagingBytes + kStageAlign + 256;
   int S = 4;
   while (S > 2 && (size_t)S * p.stage_bytes + fixed > (size_t)kSmemBudget) --S;
   if ((size_t)S * p.stage_bytes + fixed > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
@@ -432,13 +536,13 @@ static cudaError_t launch_pool_op(Slide1DParams& p, int P, cudaStream_t stream, 
     case 4: return launch_kind<PoolKind<Op, 4>>(p, stream, grid);
     case 8: return launch_kind<PoolKind<Op, 8>>(p, stream, grid);
     case 16: return launch_kind<PoolKind<Op, 16>>(p, stream, grid);
-    case 32: return launch_kind<PoolKind<Op, 32>>(p, stream, grid);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_pool_tma(Slide1DParams& p, int op, int dtype, int P, cudaStream_t stream,
                             int grid) {
+  if (P > 16) P = 16;
   if (op == kOpSum && dtype == 1) return launch_pool_op<OpSumI32>(p, P, stream, grid);
   if (op == kOpSum && dtype == 0) return launch_pool_op<OpSumF32>(p, P, stream, grid);
   if (op == kOpMax && dtype == 1) return launch_pool_op<OpMaxI32>(p, P, stream, grid);

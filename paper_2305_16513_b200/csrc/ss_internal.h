@@ -12,15 +12,17 @@ constexpr int kOpMax = 1;
 constexpr int kSmemBudget = 227 * 1024;  // max dynamic smem per CTA on sm_100a
 constexpr int kConvTmaMaxK = 64;          // largest k served by the TMA conv kernel
 constexpr int kPoolTmaMaxW = 1024;        // largest w served by the TMA pool kernel
+constexpr int kSlideWarps = 15;           // consumer warps of the 1-D tile kernel
+constexpr int kSlideTileRows = kSlideWarps * 16;  // output rows (of 32) per CTA tile
 
 // Parameters of the TMA tile kernel (slide1d.cu).  x and y are viewed as 2-D
 // arrays of 128-B rows starting at x_view / y_view (16-B aligned-down copies
 // of the caller's pointers); shift_x / shift_y are the element offsets of the
 // caller's x / y inside those views.
 struct alignas(64) Slide1DParams {
-  CUtensorMap tm_x_main;  // box {32, 256}, SWIZZLE_128B
+  CUtensorMap tm_x_main;  // box {32, kSlideTileRows}, SWIZZLE_128B
   CUtensorMap tm_x_halo;  // box {32, 8},   SWIZZLE_128B
-  CUtensorMap tm_y;       // box {32, 32},  SWIZZLE_128B (valid iff has_y_map)
+  CUtensorMap tm_y;       // box {32, 16},  SWIZZLE_128B (valid iff has_y_map)
   const void* x_view;
   void* y_view;
   int64_t N, L, batch;
