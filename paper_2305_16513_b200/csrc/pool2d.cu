@@ -147,6 +147,132 @@ pool2d_kernel(const __grid_constant__ Pool2DParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Vectorised separable kernel for small compile-time windows (KH x KW, stride
+// SH x SW with SW in {1,2,4} and KW - SW <= 4; BASELINE config 4 uses 3x3/1
+// and 2x2/2).  Warp-specialised: warp kP2VWarps issues one cp.async.bulk per
+// plane into a 3-stage ring (full/empty mbarriers); each consumer warp owns a
+// band of output rows of the plane; lane t owns VO = 4/SW consecutive output
+// columns [VO*t, VO*t+VO) of a 128-column strip, reads the 4 + (KW-SW) input
+// columns it needs with one LDS.128 (+ one LDS.64), forms the VO row results,
+// and keeps the last KH row results per column in a register ring: the
+// column pass costs KH-1 (+) per output and nothing goes back to HBM but y.
+constexpr int kP2VWarps = 15;
+constexpr int kP2VThreads = (kP2VWarps + 1) * 32;
+
+template <class Op, int KH, int KW, int SH, int SW>
+__global__ void __launch_bounds__(kP2VThreads, 1)
+pool2d_vec_kernel(const __grid_constant__ Pool2DParams p) {
+  constexpr int VO = 4 / SW;        // output columns per lane
+  constexpr int XE = KW - SW;       // extra input columns past the lane's 4
+  static_assert(XE >= 0 && XE <= 4, "window shape");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
+                                             ~uintptr_t(127));
+  const int S = p.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
+  uint64_t* empty = full + S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kP2VWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t W = p.W, OW = p.OW, OH = p.OH, plane_elems = p.H * p.W;
+  const uint32_t plane_bytes = (uint32_t)(plane_elems * 4);
+
+  if (warp == kP2VWarps) {  // producer
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t pl = blockIdx.x; pl < p.planes; pl += gridDim.x, ++it) {
+        const int s = it % S;
+        mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&full[s], plane_bytes);
+        bulk_load_1d(smem + (size_t)s * p.stage_bytes, p.x + pl * plane_elems, plane_bytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // consumers: warp -> band of output rows
+  const int64_t rows_per = (OH + kP2VWarps - 1) / kP2VWarps;
+  const int64_t ra = warp * rows_per;
+  const int64_t rb = ra + rows_per < OH ? ra + rows_per : OH;
+  const uint32_t smem_s = smem_u32(smem);
+  int it = 0;
+  for (int64_t pl = blockIdx.x; pl < p.planes; pl += gridDim.x, ++it) {
+    const int s = it % S;
+    mbar_wait(&full[s], (uint32_t)(it / S) & 1u);
+    const uint32_t xs = smem_s + (uint32_t)s * p.stage_bytes;
+    float* yp = p.y + pl * OH * OW;
+    for (int64_t c0 = (int64_t)VO * lane; c0 < OW; c0 += 32 * VO) {  // 128-input-column strips
+      const uint32_t colb = (uint32_t)(c0 * SW) * 4u;  // byte offset of the lane's first input column
+      auto row_res = [&](int64_t ri, float (&rr)[VO]) {
+        float x[4 + XE];
+        const uint32_t a = xs + (uint32_t)(ri * W) * 4u + colb;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]) : "r"(a));
+        if constexpr (XE > 0) {
+          float e[4];
+          if constexpr (XE <= 2) {
+            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(e[0]), "=f"(e[1]) : "r"(a + 16));
+          } else {
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(e[0]), "=f"(e[1]), "=f"(e[2]), "=f"(e[3]) : "r"(a + 16));
+          }
+#pragma unroll
+          for (int i = 0; i < XE; ++i) x[4 + i] = e[i];
+        }
+#pragma unroll
+        for (int o = 0; o < VO; ++o) {
+          float r = x[o * SW];
+#pragma unroll
+          for (int d = 1; d < KW; ++d) r = Op::combine(r, x[o * SW + d]);
+          rr[o] = r;
+        }
+      };
+      float ring[KH][VO];
+      int64_t r = ra;
+      if (r < rb) {
+#pragma unroll
+        for (int i = 0; i < KH - SH; ++i) row_res(r * SH + i, ring[i + SH]);
+      }
+      for (; r < rb; ++r) {
+#pragma unroll
+        for (int i = 0; i < KH - SH; ++i)  // slide the ring by SH rows
+#pragma unroll
+          for (int o = 0; o < VO; ++o) ring[i][o] = ring[i + SH][o];
+#pragma unroll
+        for (int i = (KH - SH > 0 ? KH - SH : 0); i < KH; ++i) row_res(r * SH + i, ring[i]);
+        float out[VO];
+#pragma unroll
+        for (int o = 0; o < VO; ++o) {
+          float acc = ring[0][o];
+#pragma unroll
+          for (int i = 1; i < KH; ++i) acc = Op::combine(acc, ring[i][o]);
+          out[o] = p.mode == 1 ? __fmul_rn(acc, p.inv_area) : acc;
+        }
+        float* yr = yp + r * OW + c0;
+        if (c0 + VO <= OW && ((reinterpret_cast<uintptr_t>(yr) & 7) == 0)) {
+#pragma unroll
+          for (int o = 0; o < VO; o += 2)
+            asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(yr + o), "f"(out[o]), "f"(out[o + 1])
+                         : "memory");
+        } else {
+#pragma unroll
+          for (int o = 0; o < VO; ++o)
+            if (c0 + o < OW) yr[o] = out[o];
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
 template <class Op>
 static cudaError_t launch_op(Pool2DParams& p, cudaStream_t stream, int grid, size_t smem) {
   auto go = [&](auto kfn) -> cudaError_t {
@@ -162,7 +288,34 @@ static cudaError_t launch_op(Pool2DParams& p, cudaStream_t stream, int grid, siz
   return go(pool2d_kernel<Op, 0, 0>);
 }
 
+template <class Op, int KH, int KW, int SH, int SW>
+static cudaError_t launch_vec(Pool2DParams& p, cudaStream_t stream, int grid) {
+  p.stage_bytes = (uint32_t)((p.H * p.W * 4 + 16 + 127) / 128 * 128);  // +16: last-lane over-read
+  int S = 3;
+  while (S > 2 && (size_t)S * p.stage_bytes + 256 > (size_t)kSmemBudget) --S;
+  if ((size_t)S * p.stage_bytes + 256 > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
+  p.stages = S;
+  const size_t smem = (size_t)S * p.stage_bytes + 256;
+  auto kfn = pool2d_vec_kernel<Op, KH, KW, SH, SW>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int64_t g = p.planes < grid ? p.planes : grid;
+  kfn<<<(unsigned)(g < 1 ? 1 : g), kP2VThreads, smem, stream>>>(p);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pool2d(Pool2DParams& p, cudaStream_t stream, int grid) {
+  // fast vectorised path: whole plane per stage, 16-B aligned rows, known window
+  if (p.bulk && (p.H * p.W * 4) % 16 == 0 && p.H * p.W * 4 + 16 <= 100 * 1024) {
+    cudaError_t e = cudaErrorInvalidValue;
+    const bool avg = p.mode == 1;
+    if (p.kh == 3 && p.kw == 3 && p.sh == 1 && p.sw == 1)
+      e = avg ? launch_vec<AvgOp, 3, 3, 1, 1>(p, stream, grid) : launch_vec<OpMaxF32, 3, 3, 1, 1>(p, stream, grid);
+    else if (p.kh == 2 && p.kw == 2 && p.sh == 2 && p.sw == 2)
+      e = avg ? launch_vec<AvgOp, 2, 2, 2, 2>(p, stream, grid) : launch_vec<OpMaxF32, 2, 2, 2, 2>(p, stream, grid);
+    if (e != cudaErrorInvalidValue) return e;
+  }
   // band size: keep a stage <= 64 KB
   const int64_t row_bytes = p.W * 4;
   int64_t max_in_rows = (64 * 1024) / row_bytes;

@@ -51,6 +51,8 @@ constexpr int kHaloBoxRows = 8;
 constexpr int kStageAlign = 1024;
 constexpr int kStagingBytes = kWarpRows * 128;  // 2 KB per warp buffer
 constexpr int kConvPass = 32;                   // taps per register pass
+constexpr int kBSWarpBytes = 4 * (32 + 64 + 8);  // per-warp block totals (+64 following, +8 over-read)
+constexpr int kBSBytes = kSlideWarps * kBSWarpBytes / 2;  // (2 * kBSBytes reserved in smem)
 
 // ------------------------------------------------------------- smem access
 __device__ __forceinline__ uint32_t chunk_addr(uint32_t st_s, int c) {
@@ -124,6 +126,7 @@ __device__ __forceinline__ void load_run_rt(uint32_t st_s, int e0, T (&v)[NV]) {
 template <int KT>
 struct ConvKind {
   using T = float;
+  static constexpr bool kTwoPhase = false;
   // elements read past the thread's first input (max over SH): chunks cover
   // [0, SH + 16 + KT) rounded up to a chunk
   static constexpr int kSpan = 4 * ((3 + kR + KT + 3) / 4) - kR;
@@ -193,6 +196,7 @@ struct ConvKind {
 template <class Op, int P>
 struct PoolKind {
   using T = typename Op::T;
+  static constexpr bool kTwoPhase = false;
   static constexpr int kOwn = P < 16 ? kR + P - 1 : kR;  // own run length
   static constexpr int kSpan = -1;                        // runtime: w + 20
 
@@ -276,6 +280,88 @@ struct PoolKind {
   }
 };
 
+// Pool for long windows (w >= 48): the middle x[p0+16, p0+w) is assembled
+// from 16-element block totals instead of being re-read element by element.
+// Within a warp the 32 threads own 32 consecutive blocks (block beta =
+// 2*row + half); each publishes B[beta] = its suffix a[0] to a per-warp
+// shared array, and lanes 0..q-1 also total the q blocks that follow the
+// warp's range.  After __syncwarp:
+//   middle = B[beta+1] (+) ... (+) B[beta+q] (+) head(block beta+q+1, rr elements),
+//   q = (w-16) div 16, rr = (w-16) mod 16.
+template <class Op>
+struct PoolBlockKind {
+  using T = typename Op::T;
+  static constexpr bool kTwoPhase = true;
+  static constexpr int kSpan = -1;  // runtime: w + 20
+
+  template <int SH>
+  static __device__ __forceinline__ T block_total(uint32_t st_s, int c0) {
+    T v[kR];
+    load_run<T, SH, kR>(st_s, c0, v);
+#pragma unroll
+    for (int s = 1; s < kR; s <<= 1)
+#pragma unroll
+      for (int i = 0; i + s < kR; i += 2 * s) v[i] = Op::combine(v[i], v[i + s]);
+    return v[0];
+  }
+
+  // Called by every lane of an active warp.  bs_s: this warp's block-total
+  // array; lb: my block index within the warp (0..31).
+  template <int SH>
+  static __device__ __forceinline__ void run(const Slide1DParams& p, uint32_t st_s, int c0,
+                                             uint32_t bs_s, int lb, int lane, T (&y)[kR]) {
+    const int w = (int)p.w;
+    const int q = (w - kR) >> 4, rr = (w - kR) & 15;
+    T a[kR];
+    load_run<T, SH, kR>(st_s, c0, a);
+#pragma unroll
+    for (int i = kR - 2; i >= 0; --i) a[i] = Op::combine(a[i], a[i + 1]);
+    __syncwarp();  // previous tile's readers of bs are done
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(bs_s + 4u * lb), "r"(bitcast<uint32_t>(a[0]))
+                 : "memory");
+    // blocks 32..31+q of the warp's block sequence: the 16 rows after the warp
+    // (block 32 + e starts 16*(32 + e - lb) elements after my block)
+    for (int e = lane; e < q; e += 32) {
+      const T t = block_total<SH>(st_s, c0 + 4 * (32 + e - lb));
+      asm volatile("st.shared.b32 [%0], %1;" ::"r"(bs_s + 4u * (32 + e)), "r"(bitcast<uint32_t>(t))
+                   : "memory");
+    }
+    __syncwarp();
+    // fold B[lb+1 .. lb+q]: loads issued 8 at a time ahead of their folds
+    T m0 = Op::identity(), m1 = Op::identity();
+    for (int i = 1; i <= q; i += 8) {
+      uint32_t b[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(b[k]) : "r"(bs_s + 4u * (lb + i + k)));
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        if (i + k <= q) m0 = Op::combine(m0, bitcast<T>(b[k]));
+        if (i + k + 1 <= q) m1 = Op::combine(m1, bitcast<T>(b[k + 1]));
+      }
+    }
+    T m = Op::combine(m0, m1);
+    if (rr > 0) {  // head: first rr elements of block lb+q+1
+      T hb[kR - 1];
+      load_run<T, SH, kR - 1>(st_s, c0 + 4 * (q + 1), hb);
+      T h = hb[0];
+#pragma unroll
+      for (int k = 1; k < kR - 1; ++k)
+        if (k < rr) h = Op::combine(h, hb[k]);
+      m = Op::combine(m, h);
+    }
+    T tl[kR - 1];
+    load_run_rt<T, kR - 1>(st_s, 4 * c0 + SH + w, tl);
+    y[0] = Op::combine(a[0], m);
+    T pre = m;
+#pragma unroll
+    for (int r = 1; r < kR; ++r) {
+      pre = Op::combine(pre, tl[r - 1]);
+      y[r] = Op::combine(a[r], pre);
+    }
+  }
+};
+
 template <class Kind>
 struct SlowPath;  // direct windows from global memory (array-end tiles)
 
@@ -297,6 +383,9 @@ struct SlowPath<PoolKind<Op, P>> {
     return acc;
   }
 };
+
+template <class Op>
+struct SlowPath<PoolBlockKind<Op>> : SlowPath<PoolKind<Op, 16>> {};
 
 // ------------------------------------------------------------- tile walk
 struct TileCursor {
@@ -339,7 +428,16 @@ __device__ __forceinline__ TileGeom tile_geom(const Slide1DParams& p, const Tile
   const int last_local = 32 * (kTileRows - 1) + g.m + 31 + p.span;
   const int halo = (last_local >> 5) + 1 - kTileRows;
   g.halo_boxes = halo > 0 ? (halo + kHaloBoxRows - 1) / kHaloBoxRows : 0;
-  g.slow = 32 * g.xrow0 + last_local >= p.x_full_elems;
+  // Rows past the tensor map read as zeros and only feed masked outputs; a
+  // tile is "slow" only if a window of a valid output needs an element of
+  // x's partial last 128-B row (not covered by the tensor map).
+  if (p.x_total_elems > p.x_full_elems) {
+    const int64_t o_end = min(32 * (g.yrow0 + kTileRows), g.e_y + p.L);  // one past last valid output
+    const int64_t x_last = (o_end - 1 - g.e_y) + p.shift_x + tc.b * p.N + p.w - 1;
+    g.slow = x_last >= p.x_full_elems;
+  } else {
+    g.slow = false;
+  }
   return g;
 }
 
@@ -354,7 +452,8 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
   const int S = p.stages;
   const uint32_t stage_bytes = p.stage_bytes;
   uint8_t* staging = smem + (size_t)S * stage_bytes;  // kWarps * 2 * 2 KB
-  uint64_t* full = reinterpret_cast<uint64_t*>(staging + kWarps * 2 * kStagingBytes);
+  uint8_t* bsbuf = staging + kWarps * 2 * kStagingBytes;  // 2 x kBSBytes block totals
+  uint64_t* full = reinterpret_cast<uint64_t*>(bsbuf + 2 * kBSBytes);
   uint64_t* empty = full + S;
   const uint32_t smem_s = smem_u32(smem);
 
@@ -426,7 +525,21 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
 
     mbar_wait(&full[s], ph);
     T y[kR];
-    if (warp_active && !g.slow) {
+    if constexpr (Kind::kTwoPhase) {
+      if (warp_active && !g.slow) {
+        const int p0 = 32 * row + kR * half + g.m;
+        const int c0 = p0 >> 2;
+        // block order inside the warp: lb = 2*row_in_warp + half (consecutive blocks)
+        const int lb = 2 * row_in_warp + half;
+        const uint32_t bs_s = smem_u32(bsbuf) + (uint32_t)warp * kBSWarpBytes;
+        switch (g.m & 3) {
+          case 0: Kind::template run<0>(p, st_s, c0, bs_s, lb, lane, y); break;
+          case 1: Kind::template run<1>(p, st_s, c0, bs_s, lb, lane, y); break;
+          case 2: Kind::template run<2>(p, st_s, c0, bs_s, lb, lane, y); break;
+          default: Kind::template run<3>(p, st_s, c0, bs_s, lb, lane, y); break;
+        }
+      }
+    } else if (warp_active && !g.slow) {
       const int p0 = 32 * row + kR * half + g.m;  // stage element of my first input
       const int c0 = p0 >> 2;
       switch (g.m & 3) {
@@ -491,7 +604,7 @@ static cudaError_t launch_kind(Slide1DParams& p, cudaStream_t stream, int grid) 
   const int halo_cap =
       max_halo_rows > 0 ? ((max_halo_rows + kHaloBoxRows - 1) / kHaloBoxRows) * kHaloBoxRows : 0;
   p.stage_bytes = (uint32_t)(kTileRows + halo_cap) * 128u;
-  const size_t fixed = (size_t)kWarps * 2 * kStagingBytes + kStageAlign + 256;
+  const size_t fixed = (size_t)kWarps * 2 * kStagingBytes + 2 * kBSBytes + kStageAlign + 256;
   int S = 4;
   while (S > 2 && (size_t)S * p.stage_bytes + fixed > (size_t)kSmemBudget) --S;
   if ((size_t)S * p.stage_bytes + fixed > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
@@ -530,6 +643,7 @@ cudaError_t launch_conv_tma(Slide1DParams& p, int KT, cudaStream_t stream, int g
 
 template <class Op>
 static cudaError_t launch_pool_op(Slide1DParams& p, int P, cudaStream_t stream, int grid) {
+  if (p.w >= 48 && p.w <= 16 + 16 * 64) return launch_kind<PoolBlockKind<Op>>(p, stream, grid);
   switch (P) {
     case 1: return launch_kind<PoolKind<Op, 1>>(p, stream, grid);
     case 2: return launch_kind<PoolKind<Op, 2>>(p, stream, grid);
