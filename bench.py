@@ -109,68 +109,65 @@ def cfg_cells(workload: str):
 
 # ============================================================== clocks (NVML)
 class ClockSampler:
-    """Samples SM clock and throttle reasons with NVML during the timed region."""
+    """Samples SM clock and throttle reasons DURING the timed region with
+    `nvidia-smi -lms 20` in a subprocess (the GPU selected by UUID, so
+    CUDA_VISIBLE_DEVICES remapping is respected); falls back to NVML polling."""
 
-    def __init__(self, device_index: int, period: float = 0.01):
-        self.dev, self.period = device_index, period
-        self.samples, self.reasons = [], set()
-        self.max_mhz = None
-        self._stop = threading.Event()
-        self._t = None
-        self.ok = False
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
 
     def __enter__(self):
         try:
-            import pynvml as nv
-            nv.nvmlInit()
-            self.nv = nv
-            self.h = None
-            try:  # map the torch device to NVML by UUID (CUDA_VISIBLE_DEVICES may remap indices)
-                import torch
-                u = str(torch.cuda.get_device_properties(self.dev).uuid)
-                self.h = nv.nvmlDeviceGetHandleByUUID(u if u.startswith("GPU-") else "GPU-" + u)
-            except Exception:  # noqa: BLE001
-                self.h = nv.nvmlDeviceGetHandleByIndex(self.dev)
-            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
-            self.ok = True
+            import torch
+            u = str(torch.cuda.get_device_properties(self.dev).uuid)
+            uid = u if u.startswith("GPU-") else "GPU-" + u
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                                          "-lms", "20", "-i", uid], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # let the sampler start before the timed region
         except Exception as e:  # noqa: BLE001
             self.err = str(e)
-            return self
-        names = {
-            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
-            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
-            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
-        }
-
-        def run():
-            while not self._stop.is_set():
-                try:
-                    self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                    try:
-                        r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                    except AttributeError:
-                        r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
-                    for n, bit in names.items():
-                        if r & bit and n != "gpu_idle":
-                            self.reasons.add(n)
-                except Exception:  # noqa: BLE001
-                    pass
-                time.sleep(self.period)
-
-        self._t = threading.Thread(target=run, daemon=True)
-        self._t.start()
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join()
+        if self.proc is not None:
+            time.sleep(0.05)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
 
     def summary(self):
-        if not self.ok:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": getattr(self, "err", "")}
-        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons, pw = [], None, set(), []
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+                pw.append(float(f[6]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "note": getattr(self, "err", "no nvidia-smi samples")}
+        busy = [c for c, p in zip(sm, pw) if p > 200] or sm  # samples under load
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(pw) if pw else None}
 
 
 # ============================================================== helpers
@@ -314,14 +311,20 @@ class Runner:
         e.record(self.stream)
         events.append((c, ev0, e))
 
-    def step(self, events=None):
-        """One pass of the hot path over the workload (this rank's share)."""
+    def step(self, events=None, before=None, after=None):
+        """One pass of the hot path over the workload (this rank's share).
+        before(c)/after(c): optional hooks around each cell's launches (the
+        end-to-end loop uses them to chain copies on other streams)."""
         works = {}
         for key, (kind, geo) in self.meta.items():  # post halo exchanges first
             if kind == "seq" and self.world > 1:
                 works[key] = self.ssd.halo_start(self.x[key], geo)
         for c in self.cells:  # interiors / whole cells
+            if before:
+                before(c)
             self._launch_cell(c, events)
+            if after and not (self.meta[c.inp][0] == "seq" and works):
+                after(c)
         for key, wk in works.items():
             self.ssd.wait_all(wk)
         if works:
@@ -330,9 +333,13 @@ class Runner:
                 if kind == "seq":
                     self.ssd.run_tail(self.x[c.inp], geo, c.w,
                                       lambda xv, yv, c=c: self._launch_1d(c, xv, yv), self.y[c.name])
+                    if after:
+                        after(c)
 
     # ---- end to end: pinned host buffers -> device -> kernels -> host
     def setup_e2e(self):
+        """Pinned host buffers for every input and output, and the streams /
+        events of the overlapped end-to-end loop."""
         torch = self.torch
         self.hx = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in self.x.items()}
         for k, v in self.x.items():
@@ -344,13 +351,53 @@ class Runner:
         torch.cuda.synchronize()
         self.h2d_bytes = sum(v.numel() * v.element_size() for v in self.hx.values())
         self.d2h_bytes = sum(v.numel() * v.element_size() for v in self.hy.values())
+        self.s_h2d = torch.cuda.Stream(device=self.device)
+        self.s_d2h = torch.cuda.Stream(device=self.device)
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+        self.ev_in_ready = {k: ev() for k in self.x}
+        self.ev_in_free = {k: ev() for k in self.x}
+        self.ev_out_ready = {c.name: ev() for c in self.cells}
+        self.ev_out_free = {c.name: ev() for c in self.cells}
+        for e in list(self.ev_in_free.values()) + list(self.ev_out_free.values()):
+            e.record(self.stream)
+        self.last_reader = {c.inp: c.name for c in self.cells}  # last cell reading each input
 
     def step_e2e(self):
+        """One end-to-end step through the public C ABI: H2D of every input from
+        pinned memory (copy stream), the kernels (compute stream), D2H of every
+        output to pinned memory (second copy stream).  Copies of one cell overlap
+        kernels of the next; an input is overwritten only after its last reader
+        of the previous step, an output only after its previous D2H."""
+        torch = self.torch
         for k in self.x:
-            self.x[k].copy_(self.hx[k], non_blocking=True)
-        self.step()
-        for c in self.cells:
-            self.hy[c.name].copy_(self.y[c.name], non_blocking=True)
+            self.s_h2d.wait_event(self.ev_in_free[k])
+            with torch.cuda.stream(self.s_h2d):
+                self.x[k].copy_(self.hx[k], non_blocking=True)
+            self.ev_in_ready[k].record(self.s_h2d)
+
+        def before(c):
+            self.stream.wait_event(self.ev_in_ready[c.inp])
+            self.stream.wait_event(self.ev_out_free[c.name])
+
+        def after(c):
+            self.ev_out_ready[c.name].record(self.stream)
+            if self.last_reader[c.inp] == c.name:
+                self.ev_in_free[c.inp].record(self.stream)
+            self.s_d2h.wait_event(self.ev_out_ready[c.name])
+            with torch.cuda.stream(self.s_d2h):
+                self.hy[c.name].copy_(self.y[c.name], non_blocking=True)
+            self.ev_out_free[c.name].record(self.s_d2h)
+
+        self.step(before=before, after=after)
+
+    def e2e_fence(self):
+        """Make the compute stream wait for every outstanding copy."""
+        done = self.torch.cuda.Event()
+        done.record(self.s_d2h)
+        self.stream.wait_event(done)
+        done2 = self.torch.cuda.Event()
+        done2.record(self.s_h2d)
+        self.stream.wait_event(done2)
 
 
 def run_ours(args):
@@ -456,9 +503,12 @@ def run_ours(args):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         n_e2e = max(2, min(args.steps, args.e2e_steps))
+        R.e2e_fence()
         e0.record(R.stream)
+        R.s_h2d.wait_stream(R.stream)
         for _ in range(n_e2e):
             R.step_e2e()
+        R.e2e_fence()
         e1.record(R.stream)
         torch.cuda.synchronize()
         barrier()
@@ -466,7 +516,8 @@ def run_ours(args):
         e2e = {"value": round(out_total / args.steps * n_e2e / (ems * 1e-3) / 1e9, 3), "unit": "GElem/s",
                "h2d_bytes_per_step": int(R.h2d_bytes), "d2h_bytes_per_step": int(R.d2h_bytes),
                "ms_per_step": round(ems / n_e2e, 3), "steps": n_e2e,
-               "path": "pinned host -> cudaMemcpyAsync -> ss_* C ABI -> cudaMemcpyAsync -> pinned host"}
+               "path": "pinned host -> cudaMemcpyAsync (copy stream) -> ss_* C ABI (compute stream) -> "
+                       "cudaMemcpyAsync (2nd copy stream) -> pinned host, overlapped across cells"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -595,7 +646,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="suite", choices=["suite", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -50,6 +50,8 @@ constexpr int kWarpRows = 16;                // output rows per warp
 constexpr int kHaloBoxRows = 8;
 constexpr int kStageAlign = 1024;
 constexpr int kStagingBytes = kWarpRows * 128;  // 2 KB per warp buffer
+constexpr int kStagingBufs = 1;                 // output staging buffers per warp
+constexpr int kMaxStages = 5;
 constexpr int kConvPass = 32;                   // taps per register pass
 constexpr int kBSWarpBytes = 4 * (32 + 64 + 8);  // per-warp block totals (+64 following, +8 over-read)
 constexpr int kBSBytes = kSlideWarps * kBSWarpBytes / 2;  // (2 * kBSBytes reserved in smem)
@@ -451,8 +453,8 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
       (reinterpret_cast<uintptr_t>(smem_raw) + kStageAlign - 1) & ~uintptr_t(kStageAlign - 1));
   const int S = p.stages;
   const uint32_t stage_bytes = p.stage_bytes;
-  uint8_t* staging = smem + (size_t)S * stage_bytes;  // kWarps * 2 * 2 KB
-  uint8_t* bsbuf = staging + kWarps * 2 * kStagingBytes;  // 2 x kBSBytes block totals
+  uint8_t* staging = smem + (size_t)S * stage_bytes;  // kWarps * kStagingBufs * 2 KB
+  uint8_t* bsbuf = staging + kWarps * kStagingBufs * kStagingBytes;  // block totals
   uint64_t* full = reinterpret_cast<uint64_t*>(bsbuf + 2 * kBSBytes);
   uint64_t* empty = full + S;
   const uint32_t smem_s = smem_u32(smem);
@@ -505,7 +507,7 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
   // ---------------- consumers
   const int row_in_warp = lane & 15, half = lane >> 4;
   const int row = kWarpRows * warp + row_in_warp;  // output row within the tile
-  uint8_t* my_staging = staging + warp * 2 * kStagingBytes;
+  uint8_t* my_staging = staging + warp * kStagingBufs * kStagingBytes;
   const uint32_t my_staging_s = smem_u32(my_staging);
   int it = 0;
   TileCursor tc;
@@ -563,8 +565,8 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
           if (o >= y_lo && o < y_hi) yv[o] = SlowPath<Kind>::eval(p, xg + o + dxy);
         }
       } else if (warp_full && p.has_y_map) {
-        const int buf = it & 1;
-        if (lane == 0) bulk_wait_read<1>();
+        const int buf = kStagingBufs == 1 ? 0 : (it & 1);
+        if (lane == 0) bulk_wait_read<kStagingBufs - 1>();
         __syncwarp();
         const uint32_t base = my_staging_s + buf * kStagingBytes;
 #pragma unroll
@@ -604,8 +606,8 @@ static cudaError_t launch_kind(Slide1DParams& p, cudaStream_t stream, int grid) 
   const int halo_cap =
       max_halo_rows > 0 ? ((max_halo_rows + kHaloBoxRows - 1) / kHaloBoxRows) * kHaloBoxRows : 0;
   p.stage_bytes = (uint32_t)(kTileRows + halo_cap) * 128u;
-  const size_t fixed = (size_t)kWarps * 2 * kStagingBytes + 2 * kBSBytes + kStageAlign + 256;
-  int S = 4;
+  const size_t fixed = (size_t)kWarps * kStagingBufs * kStagingBytes + 2 * kBSBytes + kStageAlign + 256;
+  int S = kMaxStages;
   while (S > 2 && (size_t)S * p.stage_bytes + fixed > (size_t)kSmemBudget) --S;
   if ((size_t)S * p.stage_bytes + fixed > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
   p.stages = S;
