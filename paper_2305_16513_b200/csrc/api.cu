@@ -8,6 +8,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -22,6 +24,19 @@ static std::atomic<uint64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static thread_local std::string g_last_error;
+
+cudaError_t ensure_smem_attr(const void* kfn) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, cudaError_t>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& d : done)
+    if (d.first.first == kfn && d.first.second == dev) return d.second;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
+  done.push_back({{kfn, dev}, e});
+  return e;
+}
 
 static ss_status_t fail(ss_status_t st, const char* fmt, ...) {
   char buf[512];

@@ -276,7 +276,7 @@ pool2d_vec_kernel(const __grid_constant__ Pool2DParams p) {
 template <class Op>
 static cudaError_t launch_op(Pool2DParams& p, cudaStream_t stream, int grid, size_t smem) {
   auto go = [&](auto kfn) -> cudaError_t {
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
     if (e != cudaSuccess) return e;
     int64_t g = p.ntiles < grid ? p.ntiles : grid;
     kfn<<<(unsigned)(g < 1 ? 1 : g), kP2Threads, smem, stream>>>(p);
@@ -297,7 +297,7 @@ static cudaError_t launch_vec(Pool2DParams& p, cudaStream_t stream, int grid) {
   p.stages = S;
   const size_t smem = (size_t)S * p.stage_bytes + 256;
   auto kfn = pool2d_vec_kernel<Op, KH, KW, SH, SW>;
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
   if (e != cudaSuccess) return e;
   int64_t g = p.planes < grid ? p.planes : grid;
   kfn<<<(unsigned)(g < 1 ? 1 : g), kP2VThreads, smem, stream>>>(p);

@@ -613,7 +613,7 @@ static cudaError_t launch_kind(Slide1DParams& p, cudaStream_t stream, int grid) 
   p.stages = S;
   const size_t smem = (size_t)S * p.stage_bytes + fixed;
   auto kfn = slide1d_tma_kernel<Kind>;
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
   if (e != cudaSuccess) return e;
   int64_t g = p.ntiles < grid ? p.ntiles : grid;
   if (g < 1) g = 1;

@@ -61,6 +61,9 @@ struct Pool2DParams {
 };
 
 void note_launch();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize = kSmemBudget) once per kernel
+// per device (thread-safe); returns the first call's status afterwards.
+cudaError_t ensure_smem_attr(const void* kfn);
 int num_sms(int device);
 
 cudaError_t launch_conv_tma(Slide1DParams& p, int KT, cudaStream_t stream, int grid);
