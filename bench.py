@@ -406,8 +406,11 @@ def run_ours(args):
 
     world, rank, local = dist_env()
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # test mode: several ranks may share a GPU; host-staged halo
+            dist.init_process_group("gloo")
     else:
         torch.cuda.set_device(0)
     device = torch.device("cuda", torch.cuda.current_device())
@@ -415,15 +418,21 @@ def run_ours(args):
     R = Runner(args.workload, world, rank, device)
     torch.cuda.synchronize()
 
+    coll_dev = device if args.dist_backend == "nccl" else torch.device("cpu")
+
     def barrier():
+        torch.cuda.synchronize()
         if world > 1:
-            dist.barrier(device_ids=[torch.cuda.current_device()])
+            if args.dist_backend == "nccl":
+                dist.barrier(device_ids=[torch.cuda.current_device()])
+            else:
+                dist.barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=device)
+        t = torch.tensor([v], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -449,7 +458,7 @@ def run_ours(args):
         c.times.append(a.elapsed_time(b))
     out_local = sum(c.n_out for c in R.cells) * args.steps
     bytes_local = sum(c.bytes for c in R.cells) * args.steps
-    tot = torch.tensor([out_local, bytes_local], dtype=torch.float64, device=device)
+    tot = torch.tensor([out_local, bytes_local], dtype=torch.float64, device=coll_dev)
     if world > 1:
         dist.all_reduce(tot)
     out_total, bytes_total = float(tot[0]), float(tot[1])
@@ -655,6 +664,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--cells-out", default=None)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo = test mode (ranks may share one GPU, host-staged halo)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup raised to 3 (timing rule)", file=sys.stderr)

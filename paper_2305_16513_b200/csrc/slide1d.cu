@@ -52,7 +52,6 @@ constexpr int kStageAlign = 1024;
 constexpr int kStagingBytes = kWarpRows * 128;  // 2 KB per warp buffer
 constexpr int kStagingBufs = 1;                 // output staging buffers per warp
 constexpr int kMaxStages = 5;
-constexpr int kConvPass = 32;                   // taps per register pass
 constexpr int kBSWarpBytes = 4 * (32 + 64 + 8);  // per-warp block totals (+64 following, +8 over-read)
 constexpr int kBSBytes = kSlideWarps * kBSWarpBytes / 2;  // (2 * kBSBytes reserved in smem)
 
@@ -132,54 +131,51 @@ struct ConvKind {
   // elements read past the thread's first input (max over SH): chunks cover
   // [0, SH + 16 + KT) rounded up to a chunk
   static constexpr int kSpan = 4 * ((3 + kR + KT + 3) / 4) - kR;
+  static constexpr int kPrefetch = 3;  // chunks loaded ahead of the tap that first needs them
 
   template <int SH>
   static __device__ __forceinline__ void compute(const Slide1DParams& p, uint32_t st_s, int c0,
                                                  float (&y)[kR]) {
-    constexpr int PI0 = SH & 1;        // first output of the pairs of even taps is -PI0 (mod 2)
+    constexpr int PI0 = SH & 1;        // pairs of even taps start at outputs -PI0 (mod 2)
     constexpr int PI1 = (SH + 1) & 1;  // ... of odd taps
     constexpr int N0 = kR / 2 + PI0, N1 = kR / 2 + PI1;
+    constexpr int NC = (SH + kR + KT + 3) / 4;  // chunks of the whole run
     float2 A0[N0], A1[N1];  // A_c[i]: outputs (2i - PI_c, 2i - PI_c + 1)
 #pragma unroll
     for (int i = 0; i < N0; ++i) A0[i] = make_float2(0.0f, 0.0f);
 #pragma unroll
     for (int i = 0; i < N1; ++i) A1[i] = make_float2(0.0f, 0.0f);
+    float2 E[2 * NC];  // E[m] = (raw[2m], raw[2m+1]); chunk c fills E[2c], E[2c+1]
+    auto load = [&](int c) {
+      uint32_t a0, a1, a2, a3;
+      lds_v4(chunk_addr(st_s, c0 + c), a0, a1, a2, a3);
+      E[2 * c] = make_float2(__uint_as_float(a0), __uint_as_float(a1));
+      E[2 * c + 1] = make_float2(__uint_as_float(a2), __uint_as_float(a3));
+    };
+    // tap j reads raw[SH - 1 + j .. SH + 16 + j]: chunks up to (SH + 17 + j) / 4
+    constexpr int C_FIRST = (SH + kR + 1) / 4 + 1;  // chunks needed by tap 0
 #pragma unroll
-    for (int j0 = 0; j0 < KT; j0 += kConvPass) {
-      constexpr int JMAX = KT < kConvPass ? KT : kConvPass;
-      const int J = KT - j0 < JMAX ? KT - j0 : JMAX;  // compile-time after unrolling
-      // raw elements [0, SH + 16 + J) relative to chunk c0 + j0/4 (j0 % 4 == 0)
-      constexpr int NC = (SH + kR + JMAX + 3) / 4;
-      float2 E[2 * NC];  // E[m] = (raw[2m], raw[2m+1])
+    for (int c = 0; c < (C_FIRST + kPrefetch < NC ? C_FIRST + kPrefetch : NC); ++c) load(c);
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        if (4 * c < SH + kR + J) {
-          uint32_t a0, a1, a2, a3;
-          lds_v4(chunk_addr(st_s, c0 + j0 / 4 + c), a0, a1, a2, a3);
-          E[2 * c] = make_float2(__uint_as_float(a0), __uint_as_float(a1));
-          E[2 * c + 1] = make_float2(__uint_as_float(a2), __uint_as_float(a3));
-        } else {
-          E[2 * c] = E[2 * c + 1] = make_float2(0.0f, 0.0f);
-        }
+    for (int jj = 0; jj < KT; ++jj) {
+      // prefetch the chunk tap jj + 4*kPrefetch will first need
+      if ((jj & 3) == 0) {
+        const int c = (SH + kR + 1 + jj) / 4 + 1 + kPrefetch;
+        if (c < NC && c >= C_FIRST + kPrefetch) load(c);
       }
+      const float f = p.taps[jj];
+      const float2 f2 = make_float2(f, f);
+      if ((jj & 1) == 0) {
 #pragma unroll
-      for (int jj = 0; jj < JMAX; ++jj) {
-        if (jj < J) {
-          const float f = p.taps[j0 + jj];
-          const float2 f2 = make_float2(f, f);
-          if ((jj & 1) == 0) {
+        for (int i = 0; i < N0; ++i) {
+          const int idx = SH + 2 * i - PI0 + jj;  // even by construction
+          A0[i] = __ffma2_rn(E[idx >> 1], f2, A0[i]);
+        }
+      } else {
 #pragma unroll
-            for (int i = 0; i < N0; ++i) {
-              const int idx = SH + 2 * i - PI0 + jj;  // even by construction
-              A0[i] = __ffma2_rn(E[idx >> 1], f2, A0[i]);
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < N1; ++i) {
-              const int idx = SH + 2 * i - PI1 + jj;
-              A1[i] = __ffma2_rn(E[idx >> 1], f2, A1[i]);
-            }
-          }
+        for (int i = 0; i < N1; ++i) {
+          const int idx = SH + 2 * i - PI1 + jj;
+          A1[i] = __ffma2_rn(E[idx >> 1], f2, A1[i]);
         }
       }
     }
@@ -444,6 +440,19 @@ __device__ __forceinline__ TileGeom tile_geom(const Slide1DParams& p, const Tile
 }
 
 // ------------------------------------------------------------- the kernel
+// Per-stage tile header written by the producer before it arms the stage's
+// full barrier (release) and read by the consumers after their wait
+// (acquire): consumers never redo the 64-bit tile arithmetic.
+struct TileHdr {
+  int64_t yrow0;  // first y-view row of the tile
+  int64_t y_lo;   // valid outputs of the batch row: [y_lo, y_hi) in y-view elements
+  int64_t y_hi;
+  int64_t dxy;    // x-view index of output o's first input = o + dxy
+  int32_t m;      // tile misalignment (element offset of the first input in its row)
+  int32_t flags;  // bit 0: slow (direct path), bit 1: done (no more tiles)
+  int64_t pad;
+};
+
 template <class Kind>
 __global__ void __launch_bounds__(kThreads, 1)
 slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
@@ -457,6 +466,7 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
   uint8_t* bsbuf = staging + kWarps * kStagingBufs * kStagingBytes;  // block totals
   uint64_t* full = reinterpret_cast<uint64_t*>(bsbuf + 2 * kBSBytes);
   uint64_t* empty = full + S;
+  TileHdr* hdr = reinterpret_cast<TileHdr*>(empty + S);
   const uint32_t smem_s = smem_u32(smem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -473,11 +483,11 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
     if (p.has_y_map) prefetch_tmap(&p.tm_y);
   }
   __syncthreads();
-  const int64_t tpr = p.tiles_per_row;
 
   if (warp == kWarps) {
-    // ---------------- producer: one lane issues the TMA loads
+    // ---------------- producer: one lane walks the tiles, publishes headers, issues TMA
     if (lane == 0) {
+      const int64_t tpr = p.tiles_per_row;
       int it = 0;
       TileCursor tc;
       tc.init(blockIdx.x, tpr);
@@ -485,8 +495,14 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
         const TileGeom g = tile_geom(p, tc);
         if (g.empty) continue;
         const int s = it % S;
-        const uint32_t ph = (uint32_t)(it / S) & 1u;
-        mbar_wait(&empty[s], ph ^ 1u);
+        mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
+        TileHdr& h = hdr[s];
+        h.yrow0 = g.yrow0;
+        h.y_lo = g.e_y;
+        h.y_hi = g.e_y + p.L;
+        h.dxy = p.shift_x + tc.b * p.N - g.e_y;
+        h.m = g.m;
+        h.flags = g.slow ? 1 : 0;
         uint8_t* dst = smem + (size_t)s * stage_bytes;
         if (g.slow) {  // consumers read global memory directly for this tile
           mbar_arrive(&full[s]);
@@ -494,12 +510,16 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
           const uint32_t bytes = (uint32_t)(kTileRows + kHaloBoxRows * g.halo_boxes) * 128u;
           mbar_arrive_expect_tx(&full[s], bytes);
           tma_load_2d(dst, &p.tm_x_main, 0, (int32_t)g.xrow0, &full[s]);
-          for (int h = 0; h < g.halo_boxes; ++h)
-            tma_load_2d(dst + (size_t)(kTileRows + kHaloBoxRows * h) * 128, &p.tm_x_halo, 0,
-                        (int32_t)(g.xrow0 + kTileRows + kHaloBoxRows * h), &full[s]);
+          for (int h2 = 0; h2 < g.halo_boxes; ++h2)
+            tma_load_2d(dst + (size_t)(kTileRows + kHaloBoxRows * h2) * 128, &p.tm_x_halo, 0,
+                        (int32_t)(g.xrow0 + kTileRows + kHaloBoxRows * h2), &full[s]);
         }
         ++it;
       }
+      const int s = it % S;  // end marker
+      mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
+      hdr[s].flags = 2;
+      mbar_arrive(&full[s]);
     }
     return;
   }
@@ -509,57 +529,56 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
   const int row = kWarpRows * warp + row_in_warp;  // output row within the tile
   uint8_t* my_staging = staging + warp * kStagingBufs * kStagingBytes;
   const uint32_t my_staging_s = smem_u32(my_staging);
-  int it = 0;
-  TileCursor tc;
-  tc.init(blockIdx.x, tpr);
-  for (int64_t tau = blockIdx.x; tau < p.ntiles; tau += gridDim.x, tc.advance(gridDim.x, tpr)) {
-    const TileGeom g = tile_geom(p, tc);
-    if (g.empty) continue;
+  for (int it = 0;; ++it) {
     const int s = it % S;
-    const uint32_t ph = (uint32_t)(it / S) & 1u;
+    mbar_wait(&full[s], (uint32_t)(it / S) & 1u);
+    const TileHdr& h = hdr[s];
+    const int flags = h.flags;
+    if (flags & 2) break;
+    const int64_t yrow0 = h.yrow0, y_lo = h.y_lo, y_hi = h.y_hi;
+    const int m = h.m;
+    const bool slow = flags & 1;
     const uint32_t st_s = smem_s + (uint32_t)s * stage_bytes;
 
-    const int64_t wrow0 = g.yrow0 + kWarpRows * warp;  // first y-view row of this warp
-    const int64_t y_lo = g.e_y, y_hi = g.e_y + p.L;     // valid outputs [y_lo, y_hi)
+    const int64_t wrow0 = yrow0 + kWarpRows * warp;  // first y-view row of this warp
     const bool warp_active = 32 * wrow0 < y_hi && 32 * (wrow0 + kWarpRows) > y_lo;
     const bool warp_full = 32 * wrow0 >= y_lo && 32 * (wrow0 + kWarpRows) <= y_hi;
     const int64_t o0 = 32 * (wrow0 + row_in_warp) + kR * half;  // my first output (y view)
 
-    mbar_wait(&full[s], ph);
     T y[kR];
     if constexpr (Kind::kTwoPhase) {
-      if (warp_active && !g.slow) {
-        const int p0 = 32 * row + kR * half + g.m;
+      if (warp_active && !slow) {
+        const int p0 = 32 * row + kR * half + m;
         const int c0 = p0 >> 2;
         // block order inside the warp: lb = 2*row_in_warp + half (consecutive blocks)
         const int lb = 2 * row_in_warp + half;
         const uint32_t bs_s = smem_u32(bsbuf) + (uint32_t)warp * kBSWarpBytes;
-        switch (g.m & 3) {
+        switch (m & 3) {
           case 0: Kind::template run<0>(p, st_s, c0, bs_s, lb, lane, y); break;
           case 1: Kind::template run<1>(p, st_s, c0, bs_s, lb, lane, y); break;
           case 2: Kind::template run<2>(p, st_s, c0, bs_s, lb, lane, y); break;
           default: Kind::template run<3>(p, st_s, c0, bs_s, lb, lane, y); break;
         }
       }
-    } else if (warp_active && !g.slow) {
-      const int p0 = 32 * row + kR * half + g.m;  // stage element of my first input
+    } else if (warp_active && !slow) {
+      const int p0 = 32 * row + kR * half + m;  // stage element of my first input
       const int c0 = p0 >> 2;
-      switch (g.m & 3) {
+      switch (m & 3) {
         case 0: Kind::template compute<0>(p, st_s, c0, y); break;
         case 1: Kind::template compute<1>(p, st_s, c0, y); break;
         case 2: Kind::template compute<2>(p, st_s, c0, y); break;
         default: Kind::template compute<3>(p, st_s, c0, y); break;
       }
     }
+    const int64_t dxy = h.dxy;  // read before releasing the stage (header reuse)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 
     if (warp_active) {
-      if (g.slow) {
+      if (slow) {
         // array-end tile: direct windows from global memory (valid outputs only)
         const T* xg = reinterpret_cast<const T*>(p.x_view);
         T* yv = reinterpret_cast<T*>(p.y_view);
-        const int64_t dxy = p.shift_x + tc.b * p.N - g.e_y;  // x-view index = o + dxy
         for (int r = 0; r < kR; ++r) {
           const int64_t o = o0 + r;
           if (o >= y_lo && o < y_hi) yv[o] = SlowPath<Kind>::eval(p, xg + o + dxy);
@@ -592,7 +611,6 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
         }
       }
     }
-    ++it;
   }
   if (lane == 0) bulk_wait_all();
 }
@@ -606,7 +624,7 @@ static cudaError_t launch_kind(Slide1DParams& p, cudaStream_t stream, int grid) 
   const int halo_cap =
       max_halo_rows > 0 ? ((max_halo_rows + kHaloBoxRows - 1) / kHaloBoxRows) * kHaloBoxRows : 0;
   p.stage_bytes = (uint32_t)(kTileRows + halo_cap) * 128u;
-  const size_t fixed = (size_t)kWarps * kStagingBufs * kStagingBytes + 2 * kBSBytes + kStageAlign + 256;
+  const size_t fixed = (size_t)kWarps * kStagingBufs * kStagingBytes + 2 * kBSBytes + kStageAlign + 16 * kMaxStages + sizeof(TileHdr) * kMaxStages + 256;
   int S = kMaxStages;
   while (S > 2 && (size_t)S * p.stage_bytes + fixed > (size_t)kSmemBudget) --S;
   if ((size_t)S * p.stage_bytes + fixed > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;

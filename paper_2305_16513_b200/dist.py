@@ -82,7 +82,32 @@ def halo_start(xbuf: torch.Tensor, shard: SeqShard, group=None):
         ops.append(dist.P2POp(dist.irecv, xbuf[shard.size:shard.size + shard.halo], shard.rank + 1, group))
     if not ops:
         return []
+    if xbuf.is_cuda and dist.get_backend(group) == "gloo":
+        return _halo_gloo_staged(xbuf, shard, h_send, group)
     return dist.batch_isend_irecv(ops)
+
+
+def _halo_gloo_staged(xbuf: torch.Tensor, shard: SeqShard, h_send: int, group=None):
+    """Blocking host-staged exchange for CUDA buffers under the gloo backend
+    (used to exercise the multi-rank path with several ranks on one device;
+    the production path is NCCL).  Sends go first on even ranks to avoid a
+    cycle of blocking sends."""
+    def send():
+        if shard.rank > 0 and h_send > 0:
+            dist.send(xbuf[:h_send].cpu(), shard.rank - 1, group)
+
+    def recv():
+        if not shard.is_last and shard.halo > 0:
+            t = torch.empty(shard.halo, dtype=xbuf.dtype)
+            dist.recv(t, shard.rank + 1, group)
+            xbuf[shard.size:shard.size + shard.halo].copy_(t)
+    if shard.rank % 2 == 0:
+        send()
+        recv()
+    else:
+        recv()
+        send()
+    return []
 
 
 def run_interior(xbuf: torch.Tensor, shard: SeqShard, w: int, compute, y: torch.Tensor) -> None:
