@@ -100,6 +100,10 @@ static bool make_map(CUtensorMap* m, const void* base, int64_t rows, int box_row
   return r == CUDA_SUCCESS;
 }
 
+bool encode_rows_map(CUtensorMap* m, const void* base, int64_t rows, int box_rows) {
+  return make_map(m, base, rows, box_rows);
+}
+
 // Fill the TMA-kernel geometry; false if this problem cannot take that path.
 static bool make_slide_params(Slide1DParams& p, const void* x, void* y, int64_t N, int64_t batch,
                               int64_t L) {
@@ -121,9 +125,8 @@ static bool make_slide_params(Slide1DParams& p, const void* x, void* y, int64_t 
   if (y_rows >= (int64_t(1) << 31) - 1024) return false;
   if (!make_map(&p.tm_x_main, p.x_view, x_rows, kSlideTileRows)) return false;
   if (!make_map(&p.tm_x_halo, p.x_view, x_rows, 8)) return false;
+  p.y_rows = y_rows;
   p.has_y_map = y_rows >= 1 && make_map(&p.tm_y, p.y_view, y_rows, 16);
-  p.tiles_per_row = (L / 32 + 2 + kSlideTileRows - 1) / kSlideTileRows;
-  p.ntiles = batch * p.tiles_per_row;
   return true;
 }
 

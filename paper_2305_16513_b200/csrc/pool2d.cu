@@ -208,11 +208,12 @@ pool2d_vec_kernel(const __grid_constant__ Pool2DParams p) {
     mbar_wait(&full[s], (uint32_t)(it / S) & 1u);
     const uint32_t xs = smem_s + (uint32_t)s * p.stage_bytes;
     float* yp = p.y + pl * OH * OW;
-    for (int64_t c0 = (int64_t)VO * lane; c0 < OW; c0 += 32 * VO) {  // 128-input-column strips
+    const uint32_t W4 = (uint32_t)W * 4u;  // smem row pitch (plane <= 100 KB: 32-bit offsets)
+    const int OWi = (int)OW;
+    for (int c0 = VO * lane; c0 < OWi; c0 += 32 * VO) {  // 128-input-column strips
       const uint32_t colb = (uint32_t)(c0 * SW) * 4u;  // byte offset of the lane's first input column
-      auto row_res = [&](int64_t ri, float (&rr)[VO]) {
+      auto row_res = [&](uint32_t a, float (&rr)[VO]) {  // a: smem address of the row's 1st input
         float x[4 + XE];
-        const uint32_t a = xs + (uint32_t)(ri * W) * 4u + colb;
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                      : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]) : "r"(a));
         if constexpr (XE > 0) {
@@ -235,18 +236,22 @@ pool2d_vec_kernel(const __grid_constant__ Pool2DParams p) {
         }
       };
       float ring[KH][VO];
-      int64_t r = ra;
-      if (r < rb) {
+      int r = (int)ra;
+      uint32_t arow = xs + (uint32_t)(r * SH) * W4 + colb;  // input row r*SH, my columns
+      float* yr = yp + (int64_t)r * OW + c0;
+      const bool vec_ok = c0 + VO <= OWi && ((reinterpret_cast<uintptr_t>(yp + c0) & 7) == 0) &&
+                          ((OW & 1) == 0);
+      if (r < (int)rb) {
 #pragma unroll
-        for (int i = 0; i < KH - SH; ++i) row_res(r * SH + i, ring[i + SH]);
+        for (int i = 0; i < KH - SH; ++i) row_res(arow + (uint32_t)i * W4, ring[i + SH]);
       }
-      for (; r < rb; ++r) {
+      for (; r < (int)rb; ++r, arow += SH * W4, yr += OW) {
 #pragma unroll
         for (int i = 0; i < KH - SH; ++i)  // slide the ring by SH rows
 #pragma unroll
           for (int o = 0; o < VO; ++o) ring[i][o] = ring[i + SH][o];
 #pragma unroll
-        for (int i = (KH - SH > 0 ? KH - SH : 0); i < KH; ++i) row_res(r * SH + i, ring[i]);
+        for (int i = (KH - SH > 0 ? KH - SH : 0); i < KH; ++i) row_res(arow + (uint32_t)i * W4, ring[i]);
         float out[VO];
 #pragma unroll
         for (int o = 0; o < VO; ++o) {
@@ -255,8 +260,7 @@ pool2d_vec_kernel(const __grid_constant__ Pool2DParams p) {
           for (int i = 1; i < KH; ++i) acc = Op::combine(acc, ring[i][o]);
           out[o] = p.mode == 1 ? __fmul_rn(acc, p.inv_area) : acc;
         }
-        float* yr = yp + r * OW + c0;
-        if (c0 + VO <= OW && ((reinterpret_cast<uintptr_t>(yr) & 7) == 0)) {
+        if (vec_ok) {
 #pragma unroll
           for (int o = 0; o < VO; o += 2)
             asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(yr + o), "f"(out[o]), "f"(out[o + 1])
@@ -264,7 +268,7 @@ pool2d_vec_kernel(const __grid_constant__ Pool2DParams p) {
         } else {
 #pragma unroll
           for (int o = 0; o < VO; ++o)
-            if (c0 + o < OW) yr[o] = out[o];
+            if (c0 + o < OWi) yr[o] = out[o];
         }
       }
     }

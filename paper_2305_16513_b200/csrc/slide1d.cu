@@ -44,12 +44,10 @@ namespace ss {
 
 constexpr int kWarps = kSlideWarps;          // consumer warps per CTA
 constexpr int kThreads = (kWarps + 1) * 32;  // + 1 producer warp
-constexpr int kR = 16;                       // outputs per thread
-constexpr int kTileRows = kSlideTileRows;    // 240 output rows = 7680 outputs
-constexpr int kWarpRows = 16;                // output rows per warp
+constexpr int kR = 16;                       // outputs per thread of the pool kinds
+constexpr int kMainBoxRows = kSlideTileRows; // rows per main TMA box (240)
 constexpr int kHaloBoxRows = 8;
 constexpr int kStageAlign = 1024;
-constexpr int kStagingBytes = kWarpRows * 128;  // 2 KB per warp buffer
 constexpr int kStagingBufs = 1;                 // output staging buffers per warp
 constexpr int kMaxStages = 5;
 constexpr int kBSWarpBytes = 4 * (32 + 64 + 8);  // per-warp block totals (+64 following, +8 over-read)
@@ -124,22 +122,26 @@ __device__ __forceinline__ void load_run_rt(uint32_t st_s, int e0, T (&v)[NV]) {
 // FFMA2 (two FMAs per instruction) read every input pair as an aligned
 // register pair: for tap parity c the output pairs start at r0 with
 // (SH + r0 + c) even, so x_{p0+r0+j}, x_{p0+r0+j+1} is (raw[2m], raw[2m+1]).
-template <int KT>
+template <int KT, int R>
 struct ConvKind {
   using T = float;
   static constexpr bool kTwoPhase = false;
+  static constexpr int kRt = R;  // outputs per thread (16: half a 128-B row; 32: a full row)
   // elements read past the thread's first input (max over SH): chunks cover
-  // [0, SH + 16 + KT) rounded up to a chunk
-  static constexpr int kSpan = 4 * ((3 + kR + KT + 3) / 4) - kR;
-  static constexpr int kPrefetch = 3;  // chunks loaded ahead of the tap that first needs them
+  // [0, SH + R + KT) rounded up to a chunk
+  static constexpr int kSpan = 4 * ((3 + R + KT + 3) / 4) - R;
+#ifndef SS_CONV_PREFETCH
+#define SS_CONV_PREFETCH 3
+#endif
+  static constexpr int kPrefetch = SS_CONV_PREFETCH;  // chunks loaded ahead of the tap that first needs them
 
   template <int SH>
   static __device__ __forceinline__ void compute(const Slide1DParams& p, uint32_t st_s, int c0,
-                                                 float (&y)[kR]) {
+                                                 float (&y)[R]) {
     constexpr int PI0 = SH & 1;        // pairs of even taps start at outputs -PI0 (mod 2)
     constexpr int PI1 = (SH + 1) & 1;  // ... of odd taps
-    constexpr int N0 = kR / 2 + PI0, N1 = kR / 2 + PI1;
-    constexpr int NC = (SH + kR + KT + 3) / 4;  // chunks of the whole run
+    constexpr int N0 = R / 2 + PI0, N1 = R / 2 + PI1;
+    constexpr int NC = (SH + R + KT + 3) / 4;  // chunks of the whole run
     float2 A0[N0], A1[N1];  // A_c[i]: outputs (2i - PI_c, 2i - PI_c + 1)
 #pragma unroll
     for (int i = 0; i < N0; ++i) A0[i] = make_float2(0.0f, 0.0f);
@@ -152,35 +154,40 @@ struct ConvKind {
       E[2 * c] = make_float2(__uint_as_float(a0), __uint_as_float(a1));
       E[2 * c + 1] = make_float2(__uint_as_float(a2), __uint_as_float(a3));
     };
-    // tap j reads raw[SH - 1 + j .. SH + 16 + j]: chunks up to (SH + 17 + j) / 4
-    constexpr int C_FIRST = (SH + kR + 1) / 4 + 1;  // chunks needed by tap 0
+    // Diagonal order: walk the input pairs E[m] in increasing m and apply every
+    // (output pair, tap) that uses E[m] back to back, so the pair stays in the
+    // operand-reuse cache.  For a fixed accumulator the taps still arrive in
+    // increasing order (jj = 2m + const - 2i grows with m), so each output's
+    // association is unchanged.
+    constexpr int M_END = (SH + R + KT + 1) / 2 + 1;  // pairs touched by any tap
+    constexpr int C_FIRST = kPrefetch + 1;
 #pragma unroll
-    for (int c = 0; c < (C_FIRST + kPrefetch < NC ? C_FIRST + kPrefetch : NC); ++c) load(c);
+    for (int c = 0; c < (C_FIRST < NC ? C_FIRST : NC); ++c) load(c);
 #pragma unroll
-    for (int jj = 0; jj < KT; ++jj) {
-      // prefetch the chunk tap jj + 4*kPrefetch will first need
-      if ((jj & 3) == 0) {
-        const int c = (SH + kR + 1 + jj) / 4 + 1 + kPrefetch;
-        if (c < NC && c >= C_FIRST + kPrefetch) load(c);
+    for (int mm = 0; mm < M_END; ++mm) {
+      if ((mm & 1) == 0) {  // entering chunk mm/2: prefetch chunk mm/2 + C_FIRST
+        const int c = mm / 2 + C_FIRST;
+        if (c < NC) load(c);
       }
-      const float f = p.taps[jj];
-      const float2 f2 = make_float2(f, f);
-      if ((jj & 1) == 0) {
 #pragma unroll
-        for (int i = 0; i < N0; ++i) {
-          const int idx = SH + 2 * i - PI0 + jj;  // even by construction
-          A0[i] = __ffma2_rn(E[idx >> 1], f2, A0[i]);
+      for (int i = 0; i < N0; ++i) {
+        const int jj = 2 * mm - SH + PI0 - 2 * i;  // even tap using E[mm] for pair i
+        if (jj >= 0 && jj < KT) {
+          const float f = p.taps[jj];
+          A0[i] = __ffma2_rn(E[mm], make_float2(f, f), A0[i]);
         }
-      } else {
+      }
 #pragma unroll
-        for (int i = 0; i < N1; ++i) {
-          const int idx = SH + 2 * i - PI1 + jj;
-          A1[i] = __ffma2_rn(E[idx >> 1], f2, A1[i]);
+      for (int i = 0; i < N1; ++i) {
+        const int jj = 2 * mm - SH + PI1 - 2 * i;  // odd tap
+        if (jj >= 0 && jj < KT) {
+          const float f = p.taps[jj];
+          A1[i] = __ffma2_rn(E[mm], make_float2(f, f), A1[i]);
         }
       }
     }
 #pragma unroll
-    for (int r = 0; r < kR; ++r) {
+    for (int r = 0; r < R; ++r) {
       const int i0 = (r + PI0) >> 1, i1 = (r + PI1) >> 1;
       const float s0 = ((r + PI0) & 1) ? A0[i0].y : A0[i0].x;
       const float s1 = ((r + PI1) & 1) ? A1[i1].y : A1[i1].x;
@@ -195,6 +202,7 @@ template <class Op, int P>
 struct PoolKind {
   using T = typename Op::T;
   static constexpr bool kTwoPhase = false;
+  static constexpr int kRt = kR;
   static constexpr int kOwn = P < 16 ? kR + P - 1 : kR;  // own run length
   static constexpr int kSpan = -1;                        // runtime: w + 20
 
@@ -290,6 +298,7 @@ template <class Op>
 struct PoolBlockKind {
   using T = typename Op::T;
   static constexpr bool kTwoPhase = true;
+  static constexpr int kRt = kR;
   static constexpr int kSpan = -1;  // runtime: w + 20
 
   template <int SH>
@@ -363,8 +372,8 @@ struct PoolBlockKind {
 template <class Kind>
 struct SlowPath;  // direct windows from global memory (array-end tiles)
 
-template <int KT>
-struct SlowPath<ConvKind<KT>> {
+template <int KT, int R>
+struct SlowPath<ConvKind<KT, R>> {
   static __device__ __forceinline__ float eval(const Slide1DParams& p, const float* x) {
     float s0 = 0.0f, s1 = 0.0f;  // even taps, odd taps (same association as compute())
     for (int j = 0; j < (int)p.w; j += 2) s0 = __fmaf_rn(p.taps[j], __ldg(x + j), s0);
@@ -415,6 +424,7 @@ __device__ __forceinline__ int64_t floor_div32(int64_t a) {
   return a >= 0 ? (a >> 5) : -((31 - a) >> 5);
 }
 
+template <int kTileRows>
 __device__ __forceinline__ TileGeom tile_geom(const Slide1DParams& p, const TileCursor& tc) {
   TileGeom g;
   g.e_y = p.shift_y + tc.b * p.L;
@@ -457,6 +467,10 @@ template <class Kind>
 __global__ void __launch_bounds__(kThreads, 1)
 slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
   using T = typename Kind::T;
+  constexpr int KR = Kind::kRt;                       // outputs per thread
+  constexpr int kWarpRows = KR == 32 ? 32 : 16;       // output rows per warp
+  constexpr int kTileRows = kWarps * kWarpRows;       // 240 or 480
+  constexpr int kStagingBytes = kWarpRows * 128;      // per warp buffer
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + kStageAlign - 1) & ~uintptr_t(kStageAlign - 1));
@@ -492,7 +506,7 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
       TileCursor tc;
       tc.init(blockIdx.x, tpr);
       for (int64_t tau = blockIdx.x; tau < p.ntiles; tau += gridDim.x, tc.advance(gridDim.x, tpr)) {
-        const TileGeom g = tile_geom(p, tc);
+        const TileGeom g = tile_geom<kTileRows>(p, tc);
         if (g.empty) continue;
         const int s = it % S;
         mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
@@ -509,7 +523,10 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
         } else {
           const uint32_t bytes = (uint32_t)(kTileRows + kHaloBoxRows * g.halo_boxes) * 128u;
           mbar_arrive_expect_tx(&full[s], bytes);
-          tma_load_2d(dst, &p.tm_x_main, 0, (int32_t)g.xrow0, &full[s]);
+#pragma unroll
+          for (int mb = 0; mb < kTileRows / kMainBoxRows; ++mb)
+            tma_load_2d(dst + (size_t)mb * kMainBoxRows * 128, &p.tm_x_main, 0,
+                        (int32_t)(g.xrow0 + mb * kMainBoxRows), &full[s]);
           for (int h2 = 0; h2 < g.halo_boxes; ++h2)
             tma_load_2d(dst + (size_t)(kTileRows + kHaloBoxRows * h2) * 128, &p.tm_x_halo, 0,
                         (int32_t)(g.xrow0 + kTileRows + kHaloBoxRows * h2), &full[s]);
@@ -525,7 +542,8 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
   }
 
   // ---------------- consumers
-  const int row_in_warp = lane & 15, half = lane >> 4;
+  const int row_in_warp = KR == 32 ? lane : (lane & 15);
+  const int half = KR == 32 ? 0 : (lane >> 4);
   const int row = kWarpRows * warp + row_in_warp;  // output row within the tile
   uint8_t* my_staging = staging + warp * kStagingBufs * kStagingBytes;
   const uint32_t my_staging_s = smem_u32(my_staging);
@@ -543,12 +561,12 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
     const int64_t wrow0 = yrow0 + kWarpRows * warp;  // first y-view row of this warp
     const bool warp_active = 32 * wrow0 < y_hi && 32 * (wrow0 + kWarpRows) > y_lo;
     const bool warp_full = 32 * wrow0 >= y_lo && 32 * (wrow0 + kWarpRows) <= y_hi;
-    const int64_t o0 = 32 * (wrow0 + row_in_warp) + kR * half;  // my first output (y view)
+    const int64_t o0 = 32 * (wrow0 + row_in_warp) + KR * half;  // my first output (y view)
 
-    T y[kR];
+    T y[KR];
     if constexpr (Kind::kTwoPhase) {
       if (warp_active && !slow) {
-        const int p0 = 32 * row + kR * half + m;
+        const int p0 = 32 * row + KR * half + m;
         const int c0 = p0 >> 2;
         // block order inside the warp: lb = 2*row_in_warp + half (consecutive blocks)
         const int lb = 2 * row_in_warp + half;
@@ -561,7 +579,7 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
         }
       }
     } else if (warp_active && !slow) {
-      const int p0 = 32 * row + kR * half + m;  // stage element of my first input
+      const int p0 = 32 * row + KR * half + m;  // stage element of my first input
       const int c0 = p0 >> 2;
       switch (m & 3) {
         case 0: Kind::template compute<0>(p, st_s, c0, y); break;
@@ -579,7 +597,7 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
         // array-end tile: direct windows from global memory (valid outputs only)
         const T* xg = reinterpret_cast<const T*>(p.x_view);
         T* yv = reinterpret_cast<T*>(p.y_view);
-        for (int r = 0; r < kR; ++r) {
+        for (int r = 0; r < KR; ++r) {
           const int64_t o = o0 + r;
           if (o >= y_lo && o < y_hi) yv[o] = SlowPath<Kind>::eval(p, xg + o + dxy);
         }
@@ -589,7 +607,7 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
         __syncwarp();
         const uint32_t base = my_staging_s + buf * kStagingBytes;
 #pragma unroll
-        for (int c = 0; c < kR / 4; ++c) {
+        for (int c = 0; c < KR / 4; ++c) {
           const uint32_t off = swz128((uint32_t)row_in_warp * 128u + 64u * half + 16u * c);
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(base + off),
                        "r"(bitcast<uint32_t>(y[4 * c + 0])), "r"(bitcast<uint32_t>(y[4 * c + 1])),
@@ -605,7 +623,7 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
       } else {
         T* yv = reinterpret_cast<T*>(p.y_view);
 #pragma unroll
-        for (int r = 0; r < kR; ++r) {
+        for (int r = 0; r < KR; ++r) {
           const int64_t o = o0 + r;
           if (o >= y_lo && o < y_hi) yv[o] = y[r];
         }
@@ -618,13 +636,22 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
 // ------------------------------------------------------------- host launch
 template <class Kind>
 static cudaError_t launch_kind(Slide1DParams& p, cudaStream_t stream, int grid) {
+  constexpr int KR = Kind::kRt;
+  constexpr int kWarpRows = KR == 32 ? 32 : 16;
+  constexpr int kTileRows = kWarps * kWarpRows;
+  constexpr int kStagingBytes = kWarpRows * 128;
   const int span = Kind::kSpan >= 0 ? Kind::kSpan : (int)p.w + 20;
   p.span = span;
+  p.tiles_per_row = (p.L / 32 + 2 + kTileRows - 1) / kTileRows;
+  p.ntiles = p.batch * p.tiles_per_row;
+  if (p.has_y_map && kWarpRows != 16 && !encode_rows_map(&p.tm_y, p.y_view, p.y_rows, kWarpRows))
+    p.has_y_map = 0;
   const int max_halo_rows = (32 * (kTileRows - 1) + 31 + 31 + span) / 32 + 1 - kTileRows;
   const int halo_cap =
       max_halo_rows > 0 ? ((max_halo_rows + kHaloBoxRows - 1) / kHaloBoxRows) * kHaloBoxRows : 0;
   p.stage_bytes = (uint32_t)(kTileRows + halo_cap) * 128u;
-  const size_t fixed = (size_t)kWarps * kStagingBufs * kStagingBytes + 2 * kBSBytes + kStageAlign + 16 * kMaxStages + sizeof(TileHdr) * kMaxStages + 256;
+  const size_t fixed = (size_t)kWarps * kStagingBufs * kStagingBytes + 2 * kBSBytes + kStageAlign +
+                       16 * kMaxStages + sizeof(TileHdr) * kMaxStages + 256;
   int S = kMaxStages;
   while (S > 2 && (size_t)S * p.stage_bytes + fixed > (size_t)kSmemBudget) --S;
   if ((size_t)S * p.stage_bytes + fixed > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
@@ -642,21 +669,21 @@ static cudaError_t launch_kind(Slide1DParams& p, cudaStream_t stream, int grid) 
 
 cudaError_t launch_conv_tma(Slide1DParams& p, int KT, cudaStream_t stream, int grid) {
   switch (KT) {
-    case 1: return launch_kind<ConvKind<1>>(p, stream, grid);
-    case 2: return launch_kind<ConvKind<2>>(p, stream, grid);
-    case 3: return launch_kind<ConvKind<3>>(p, stream, grid);
-    case 4: return launch_kind<ConvKind<4>>(p, stream, grid);
-    case 5: return launch_kind<ConvKind<5>>(p, stream, grid);
-    case 7: return launch_kind<ConvKind<7>>(p, stream, grid);
-    case 8: return launch_kind<ConvKind<8>>(p, stream, grid);
-    case 15: return launch_kind<ConvKind<15>>(p, stream, grid);
-    case 16: return launch_kind<ConvKind<16>>(p, stream, grid);
-    case 24: return launch_kind<ConvKind<24>>(p, stream, grid);
-    case 31: return launch_kind<ConvKind<31>>(p, stream, grid);
-    case 32: return launch_kind<ConvKind<32>>(p, stream, grid);
-    case 48: return launch_kind<ConvKind<48>>(p, stream, grid);
-    case 63: return launch_kind<ConvKind<63>>(p, stream, grid);
-    case 64: return launch_kind<ConvKind<64>>(p, stream, grid);
+    case 1: return launch_kind<ConvKind<1, 16>>(p, stream, grid);
+    case 2: return launch_kind<ConvKind<2, 16>>(p, stream, grid);
+    case 3: return launch_kind<ConvKind<3, 16>>(p, stream, grid);
+    case 4: return launch_kind<ConvKind<4, 16>>(p, stream, grid);
+    case 5: return launch_kind<ConvKind<5, 16>>(p, stream, grid);
+    case 7: return launch_kind<ConvKind<7, 16>>(p, stream, grid);
+    case 8: return launch_kind<ConvKind<8, 16>>(p, stream, grid);
+    case 15: return launch_kind<ConvKind<15, 16>>(p, stream, grid);
+    case 16: return launch_kind<ConvKind<16, 16>>(p, stream, grid);
+    case 24: return launch_kind<ConvKind<24, 32>>(p, stream, grid);
+    case 31: return launch_kind<ConvKind<31, 32>>(p, stream, grid);
+    case 32: return launch_kind<ConvKind<32, 32>>(p, stream, grid);
+    case 48: return launch_kind<ConvKind<48, 32>>(p, stream, grid);
+    case 63: return launch_kind<ConvKind<63, 32>>(p, stream, grid);
+    case 64: return launch_kind<ConvKind<64, 32>>(p, stream, grid);
     default: return cudaErrorInvalidValue;
   }
 }

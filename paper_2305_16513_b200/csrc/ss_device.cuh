@@ -34,7 +34,9 @@ struct OpMaxI32 {
 struct OpMaxF32 {
   using T = float;
   static __device__ __forceinline__ T identity() { return -INFINITY; }
-  static __device__ __forceinline__ T combine(T a, T b) { return a > b ? a : b; }
+  // FMNMX: equals `a > b ? a : b` for finite inputs (ss.h: NaN unsupported,
+  // the sign of a zero maximum unspecified)
+  static __device__ __forceinline__ T combine(T a, T b) { return fmaxf(a, b); }
 };
 
 // ---------------------------------------------------------------- smem / PTX

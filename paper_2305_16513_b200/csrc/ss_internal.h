@@ -30,6 +30,7 @@ struct alignas(64) Slide1DParams {
   int64_t x_full_elems;   // elements covered by tm_x_* (32 * full rows)
   int64_t x_total_elems;  // shift_x + batch * N
   int64_t tiles_per_row, ntiles;
+  int64_t y_rows;         // full 128-B rows of the y view
   int64_t w;              // window (pool)
   uint32_t stage_bytes;
   int stages;
@@ -64,6 +65,8 @@ void note_launch();
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize = kSmemBudget) once per kernel
 // per device (thread-safe); returns the first call's status afterwards.
 cudaError_t ensure_smem_attr(const void* kfn);
+// 2-D [rows][32] view of 4-byte elements, 128-B swizzle, box {32, box_rows}.
+bool encode_rows_map(CUtensorMap* m, const void* base, int64_t rows, int box_rows);
 int num_sms(int device);
 
 cudaError_t launch_conv_tma(Slide1DParams& p, int KT, cudaStream_t stream, int grid);
