@@ -58,8 +58,9 @@ class Cell:
     """One kernel launch of the workload."""
 
     def __init__(self, cfg, name, op, *, w=None, f=None, kh=None, kw=None, sh=None, sw=None,
-                 mode=None, inp=None):
+                 mode=None, inp=None, stride=1):
         self.cfg, self.name, self.op = cfg, name, op
+        self.stride = stride
         self.w, self.f, self.kh, self.kw, self.sh, self.sw, self.mode = w, f, kh, kw, sh, sw, mode
         self.inp = inp  # key of the input tensor it reads
         self.n_out = 0
@@ -102,6 +103,14 @@ def cfg_cells(workload: str):
         cells.append(Cell("cfg5", "cfg5_conv_k31", "conv", w=31,
                           f=synth.normal(7, 31, sigma=synth.cfg_sigma_filter(31)), inp="x5"))
         cells.append(Cell("cfg5", "cfg5_max_w64", "max", w=64, inp="x5"))
+    if workload == "stride":  # row a4 (strided 1-D windows); not a BASELINE.json config
+        inputs["xs"] = dict(rows=64, n=1 << 20, dtype="float32", dist="normal", seed=3, kw={},
+                            shard="batch")
+        cells.append(Cell("stride", "stride_max_w3_s2", "max", w=3, stride=2, inp="xs"))
+        cells.append(Cell("stride", "stride_sum_w2_s2", "sum", w=2, stride=2, inp="xs"))
+        cells.append(Cell("stride", "stride_sum_w4_s4", "sum", w=4, stride=4, inp="xs"))
+        cells.append(Cell("stride", "stride_conv_k7_s2", "conv", w=7, stride=2,
+                          f=synth.normal(4, 7, sigma=synth.cfg_sigma_filter(7)), inp="xs"))
     if not cells:
         raise SystemExit(f"unknown workload {workload}")
     return inputs, cells
@@ -249,7 +258,7 @@ class Runner:
                 c.bytes = (sh.size + c.n_out) * es
             elif kind == "batch":
                 rows, n = geo
-                L = n - c.w + 1
+                L = (n - c.w) // c.stride + 1
                 self.y[c.name] = torch.empty((rows, L), dtype=x.dtype, device=self.device)
                 c.n_out = rows * L
                 c.bytes = (rows * n + c.n_out) * es
@@ -271,11 +280,11 @@ class Runner:
         else:
             B, N = x.shape
         if c.op == "conv":
-            st = ss.ss_conv1d(x.data_ptr(), y.data_ptr(), N, B, c.f, c.w, 1, code, s)
+            st = ss.ss_conv1d(x.data_ptr(), y.data_ptr(), N, B, c.f, c.w, c.stride, code, s)
         elif c.op == "sum":
-            st = ss.ss_pool_sum(x.data_ptr(), y.data_ptr(), N, B, c.w, 1, code, s)
+            st = ss.ss_pool_sum(x.data_ptr(), y.data_ptr(), N, B, c.w, c.stride, code, s)
         else:
-            st = ss.ss_pool_max(x.data_ptr(), y.data_ptr(), N, B, c.w, 1, code, s)
+            st = ss.ss_pool_max(x.data_ptr(), y.data_ptr(), N, B, c.w, c.stride, code, s)
         ss.check(st)
 
     def _launch_cell(self, c, events=None):
@@ -657,7 +666,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="suite", choices=["suite", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--workload", default="suite", choices=["suite", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "stride"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)

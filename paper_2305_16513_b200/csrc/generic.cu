@@ -1,6 +1,6 @@
 // generic.cu -- direct-window kernels for the cases the TMA tile kernel does
 // not take (stride > 1, tiny or misaligned inputs, very long windows, k > 64).
-// One output per thread, window loop over the read-only path (Eq. 3 as
+// Window loops over the read-only path, 4 outputs per thread (Eq. 3 as
 // written; conv as Sec. 2.5, l.86-87).  Conv uses the tile
 // kernel's association (even-tap and odd-tap FMA chains, then one add), so
 // both produce bitwise-identical outputs.
@@ -12,36 +12,75 @@
 
 namespace ss {
 
+// Grid: blockIdx.y walks batch rows, blockIdx.x chunks of kGenChunk outputs
+// of a row; each thread evaluates kGenOuts outputs (ILP), consecutive threads
+// consecutive outputs (coalesced stores, L1-shared window loads).
+constexpr int kGenThreads = 256;
+constexpr int kGenOuts = 4;
+constexpr int kGenChunk = kGenThreads * kGenOuts;
+
 template <class Op>
-__global__ void __launch_bounds__(256) pool_generic_kernel(const __grid_constant__ GenericParams p) {
+__global__ void __launch_bounds__(kGenThreads) pool_generic_kernel(const __grid_constant__ GenericParams p) {
   using T = typename Op::T;
-  const T* __restrict__ x = static_cast<const T*>(p.x);
-  T* __restrict__ y = static_cast<T*>(p.y);
-  const int64_t total = p.batch * p.L;
-  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
-       o += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = o / p.L, i = o - b * p.L;
-    const T* xr = x + b * p.N + i * p.stride;
-    T acc = __ldg(xr);
-    for (int64_t j = 1; j < p.w; ++j) acc = Op::combine(acc, __ldg(xr + j));
-    y[o] = acc;
+  const int w = (int)p.w;
+  for (int64_t b = blockIdx.y; b < p.batch; b += gridDim.y) {
+    const T* __restrict__ xr = static_cast<const T*>(p.x) + b * p.N;
+    T* __restrict__ yr = static_cast<T*>(p.y) + b * p.L;
+    for (int64_t i0 = (int64_t)blockIdx.x * kGenChunk; i0 < p.L; i0 += (int64_t)gridDim.x * kGenChunk) {
+      T acc[kGenOuts];
+      const T* xs[kGenOuts];
+#pragma unroll
+      for (int k = 0; k < kGenOuts; ++k) {
+        const int64_t i = i0 + threadIdx.x + k * kGenThreads;
+        xs[k] = xr + (i < p.L ? i : p.L - 1) * p.stride;
+        acc[k] = __ldg(xs[k]);
+      }
+      for (int j = 1; j < w; ++j) {
+#pragma unroll
+        for (int k = 0; k < kGenOuts; ++k) acc[k] = Op::combine(acc[k], __ldg(xs[k] + j));
+      }
+#pragma unroll
+      for (int k = 0; k < kGenOuts; ++k) {
+        const int64_t i = i0 + threadIdx.x + k * kGenThreads;
+        if (i < p.L) yr[i] = acc[k];
+      }
+    }
   }
 }
 
-__global__ void __launch_bounds__(256) conv_generic_kernel(const __grid_constant__ GenericParams p) {
-  const float* __restrict__ x = static_cast<const float*>(p.x);
-  float* __restrict__ y = static_cast<float*>(p.y);
-  const int64_t total = p.batch * p.L;
-  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
-       o += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = o / p.L, i = o - b * p.L;
-    const float* xr = x + b * p.N + i * p.stride;
-    // even-tap and odd-tap partial sums, each in increasing j, then added:
-    // the association of the tile kernel (slide1d.cu ConvKind)
-    float s0 = 0.0f, s1 = 0.0f;
-    for (int64_t j = 0; j < p.w; j += 2) s0 = __fmaf_rn(p.taps[j], __ldg(xr + j), s0);
-    for (int64_t j = 1; j < p.w; j += 2) s1 = __fmaf_rn(p.taps[j], __ldg(xr + j), s1);
-    y[o] = __fadd_rn(s0, s1);
+__global__ void __launch_bounds__(kGenThreads) conv_generic_kernel(const __grid_constant__ GenericParams p) {
+  const int k = (int)p.w;
+  for (int64_t b = blockIdx.y; b < p.batch; b += gridDim.y) {
+    const float* __restrict__ xr = static_cast<const float*>(p.x) + b * p.N;
+    float* __restrict__ yr = static_cast<float*>(p.y) + b * p.L;
+    for (int64_t i0 = (int64_t)blockIdx.x * kGenChunk; i0 < p.L; i0 += (int64_t)gridDim.x * kGenChunk) {
+      // even-tap and odd-tap partial sums, each in increasing j, then added:
+      // the association of the tile kernel (slide1d.cu ConvKind)
+      float s0[kGenOuts], s1[kGenOuts];
+      const float* xs[kGenOuts];
+#pragma unroll
+      for (int q = 0; q < kGenOuts; ++q) {
+        const int64_t i = i0 + threadIdx.x + q * kGenThreads;
+        xs[q] = xr + (i < p.L ? i : p.L - 1) * p.stride;
+        s0[q] = 0.0f;
+        s1[q] = 0.0f;
+      }
+      for (int j = 0; j < k; j += 2) {
+        const float f = p.taps[j];
+#pragma unroll
+        for (int q = 0; q < kGenOuts; ++q) s0[q] = __fmaf_rn(f, __ldg(xs[q] + j), s0[q]);
+      }
+      for (int j = 1; j < k; j += 2) {
+        const float f = p.taps[j];
+#pragma unroll
+        for (int q = 0; q < kGenOuts; ++q) s1[q] = __fmaf_rn(f, __ldg(xs[q] + j), s1[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < kGenOuts; ++q) {
+        const int64_t i = i0 + threadIdx.x + q * kGenThreads;
+        if (i < p.L) yr[i] = __fadd_rn(s0[q], s1[q]);
+      }
+    }
   }
 }
 
@@ -69,21 +108,29 @@ static int64_t grid_for(int64_t total, int grid_cap) {
   return g < 1 ? 1 : g;
 }
 
+static dim3 grid_1d(const GenericParams& p, int sms) {
+  int64_t gy = p.batch < 65535 ? p.batch : 65535;
+  int64_t gx = (p.L + kGenChunk - 1) / kGenChunk;
+  const int64_t cap = (int64_t)sms * 16;  // enough resident blocks to cover latency
+  if (gx * gy > cap) gx = cap / gy > 0 ? cap / gy : 1;
+  return dim3((unsigned)(gx < 1 ? 1 : gx), (unsigned)gy, 1);
+}
+
 cudaError_t launch_pool_generic(const GenericParams& p, int op, int dtype, cudaStream_t stream,
                                 int grid) {
-  const int64_t g = grid_for(p.batch * p.L, grid);
-  if (op == kOpSum && dtype == 1) pool_generic_kernel<OpSumI32><<<(unsigned)g, 256, 0, stream>>>(p);
-  else if (op == kOpSum && dtype == 0) pool_generic_kernel<OpSumF32><<<(unsigned)g, 256, 0, stream>>>(p);
-  else if (op == kOpMax && dtype == 1) pool_generic_kernel<OpMaxI32><<<(unsigned)g, 256, 0, stream>>>(p);
-  else if (op == kOpMax && dtype == 0) pool_generic_kernel<OpMaxF32><<<(unsigned)g, 256, 0, stream>>>(p);
+  const dim3 g = grid_1d(p, grid / 8 > 0 ? grid / 8 : 148);
+  if (op == kOpSum && dtype == 1) pool_generic_kernel<OpSumI32><<<g, kGenThreads, 0, stream>>>(p);
+  else if (op == kOpSum && dtype == 0) pool_generic_kernel<OpSumF32><<<g, kGenThreads, 0, stream>>>(p);
+  else if (op == kOpMax && dtype == 1) pool_generic_kernel<OpMaxI32><<<g, kGenThreads, 0, stream>>>(p);
+  else if (op == kOpMax && dtype == 0) pool_generic_kernel<OpMaxF32><<<g, kGenThreads, 0, stream>>>(p);
   else return cudaErrorInvalidValue;
   note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_conv_generic(const GenericParams& p, cudaStream_t stream, int grid) {
-  const int64_t g = grid_for(p.batch * p.L, grid);
-  conv_generic_kernel<<<(unsigned)g, 256, 0, stream>>>(p);
+  const dim3 g = grid_1d(p, grid / 8 > 0 ? grid / 8 : 148);
+  conv_generic_kernel<<<g, kGenThreads, 0, stream>>>(p);
   note_launch();
   return cudaGetLastError();
 }
