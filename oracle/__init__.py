@@ -63,6 +63,15 @@ def lib() -> ctypes.CDLL:
             L.oracle_pool2d_f32.argtypes = [vp, i64, i64, i64, i64, i64, i64, i64,
                                             ctypes.c_int, vp, vp]
             L.oracle_pool2d_f32.restype = ctypes.c_int
+            L.oracle_out_len_ex.argtypes = [i64] * 6
+            L.oracle_out_len_ex.restype = i64
+            for name in ("oracle_pool_sum_ex_i32", "oracle_pool_max_ex_i32", "oracle_pool_max_ex_f32"):
+                getattr(L, name).argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, vp]
+                getattr(L, name).restype = ctypes.c_int
+            L.oracle_pool_sum_ex_f32.argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, vp, vp]
+            L.oracle_pool_sum_ex_f32.restype = ctypes.c_int
+            L.oracle_conv1d_ex_f32.argtypes = [vp, i64, i64, vp, i64, i64, i64, i64, i64, vp, vp]
+            L.oracle_conv1d_ex_f32.restype = ctypes.c_int
             L.oracle_gamma_combine.argtypes = [dp, dp, dp, dp, vp, vp]
             L.oracle_gamma_combine.restype = None
             L.oracle_gamma_sequence.argtypes = [vp, vp, i64, vp, vp]
@@ -149,6 +158,52 @@ def pool2d(x: np.ndarray, kh: int, kw: int, sh: int, sw: int, mode: int):
     m = np.empty((P, OH, OW), np.float64)
     _check(lib().oracle_pool2d_f32(_p(x), P, H, W, kh, kw, sh, sw, mode, _p(y), _p(m)))
     return y, m
+
+
+def out_len_ex(N: int, w: int, s: int = 1, d: int = 1, pl: int = 0, pr: int = 0) -> int:
+    return int(lib().oracle_out_len_ex(N, w, s, d, pl, pr))
+
+
+def _ex_len(N, w, s, d, pl, pr):
+    L = out_len_ex(N, w, s, d, pl, pr)
+    if L < 0:
+        raise ValueError("invalid window spec")
+    return L
+
+
+def pool_sum_ex(x: np.ndarray, w: int, s: int = 1, d: int = 1, pl: int = 0, pr: int = 0):
+    """Zero-padded, dilated sliding sum (NEXT #1).  int32 -> int64; float32 -> (double, absmag)."""
+    x, N, B = _rows(x)
+    L = _ex_len(N, w, s, d, pl, pr)
+    if x.dtype == np.int32:
+        y = np.empty((B, L), np.int64)
+        _check(lib().oracle_pool_sum_ex_i32(_p(x), N, B, w, s, d, pl, pr, _p(y)))
+        return y if x.ndim == 2 else y[0]
+    y = np.empty((B, L), np.float64)
+    m = np.empty((B, L), np.float64)
+    _check(lib().oracle_pool_sum_ex_f32(_p(x), N, B, w, s, d, pl, pr, _p(y), _p(m)))
+    return (y, m) if x.ndim == 2 else (y[0], m[0])
+
+
+def pool_max_ex(x: np.ndarray, w: int, s: int = 1, d: int = 1, pl: int = 0, pr: int = 0):
+    x, N, B = _rows(x)
+    L = _ex_len(N, w, s, d, pl, pr)
+    y = np.empty((B, L), x.dtype)
+    fn = {np.dtype(np.int32): lib().oracle_pool_max_ex_i32,
+          np.dtype(np.float32): lib().oracle_pool_max_ex_f32}[x.dtype]
+    _check(fn(_p(x), N, B, w, s, d, pl, pr, _p(y)))
+    return y if x.ndim == 2 else y[0]
+
+
+def conv1d_ex(x: np.ndarray, f: np.ndarray, s: int = 1, d: int = 1, pl: int = 0, pr: int = 0):
+    x, N, B = _rows(x)
+    f = np.ascontiguousarray(f, np.float32)
+    k = f.shape[0]
+    L = _ex_len(N, k, s, d, pl, pr)
+    y = np.empty((B, L), np.float64)
+    m = np.empty((B, L), np.float64)
+    _check(lib().oracle_conv1d_ex_f32(_p(x), N, B, _p(f), k, s, d, pl, pr, _p(y), _p(m)))
+    return (y, m) if x.ndim == 2 else (y[0], m[0])
 
 
 def gamma_combine(gi, gj):

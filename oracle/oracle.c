@@ -8,6 +8,7 @@
 
 #include <math.h>
 #include <stddef.h>
+#include <stdint.h>
 
 /* Output length of a valid-padding window of w addends at stride s
  * (Eq. 3 gives N-w+1 at s=1; stride reading R4 in DESIGN.md). */
@@ -152,6 +153,114 @@ int oracle_pool2d_f32(const float* x, int64_t planes, int64_t H, int64_t W,
       }
     }
   }
+  return 0;
+}
+
+/* ---- window spec with dilation d and zero padding (pl, pr): see oracle.h ---- */
+int64_t oracle_out_len_ex(int64_t N, int64_t w, int64_t s, int64_t d, int64_t pl, int64_t pr) {
+  if (N < 1 || w < 1 || s < 1 || d < 1 || pl < 0 || pr < 0) return -1;
+  int64_t E = (w - 1) * d + 1, Np = N + pl + pr;
+  if (E > Np) return -1;
+  return (Np - E) / s + 1;
+}
+
+static int bad_ex(const void* x, const void* y, int64_t N, int64_t batch, int64_t w, int64_t s,
+                  int64_t d, int64_t pl, int64_t pr) {
+  return x == NULL || y == NULL || batch < 1 || oracle_out_len_ex(N, w, s, d, pl, pr) < 0;
+}
+
+int oracle_pool_sum_ex_i32(const int32_t* x, int64_t N, int64_t batch, int64_t w, int64_t s,
+                           int64_t d, int64_t pl, int64_t pr, int64_t* y) {
+  if (bad_ex(x, y, N, batch, w, s, d, pl, pr)) return -1;
+  int64_t L = oracle_out_len_ex(N, w, s, d, pl, pr);
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t i = 0; i < L; ++i) {
+      int64_t acc = 0;
+      for (int64_t j = 0; j < w; ++j) {
+        int64_t t = i * s + j * d - pl;
+        if (t >= 0 && t < N) acc += (int64_t)x[b * N + t];
+      }
+      y[b * L + i] = acc;
+    }
+  return 0;
+}
+
+int oracle_pool_sum_ex_f32(const float* x, int64_t N, int64_t batch, int64_t w, int64_t s,
+                           int64_t d, int64_t pl, int64_t pr, double* y, double* absmag) {
+  if (bad_ex(x, y, N, batch, w, s, d, pl, pr)) return -1;
+  int64_t L = oracle_out_len_ex(N, w, s, d, pl, pr);
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t i = 0; i < L; ++i) {
+      double acc = 0.0, mag = 0.0;
+      for (int64_t j = 0; j < w; ++j) {
+        int64_t t = i * s + j * d - pl;
+        if (t >= 0 && t < N) {
+          acc += (double)x[b * N + t];
+          mag += fabs((double)x[b * N + t]);
+        }
+      }
+      y[b * L + i] = acc;
+      if (absmag) absmag[b * L + i] = mag;
+    }
+  return 0;
+}
+
+int oracle_pool_max_ex_i32(const int32_t* x, int64_t N, int64_t batch, int64_t w, int64_t s,
+                           int64_t d, int64_t pl, int64_t pr, int32_t* y) {
+  if (bad_ex(x, y, N, batch, w, s, d, pl, pr)) return -1;
+  int64_t L = oracle_out_len_ex(N, w, s, d, pl, pr);
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t i = 0; i < L; ++i) {
+      int32_t m = INT32_MIN;
+      for (int64_t j = 0; j < w; ++j) {
+        int64_t t = i * s + j * d - pl;
+        if (t >= 0 && t < N) {
+          int32_t v = x[b * N + t];
+          m = v > m ? v : m;
+        }
+      }
+      y[b * L + i] = m;
+    }
+  return 0;
+}
+
+int oracle_pool_max_ex_f32(const float* x, int64_t N, int64_t batch, int64_t w, int64_t s,
+                           int64_t d, int64_t pl, int64_t pr, float* y) {
+  if (bad_ex(x, y, N, batch, w, s, d, pl, pr)) return -1;
+  int64_t L = oracle_out_len_ex(N, w, s, d, pl, pr);
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t i = 0; i < L; ++i) {
+      float m = -INFINITY;
+      for (int64_t j = 0; j < w; ++j) {
+        int64_t t = i * s + j * d - pl;
+        if (t >= 0 && t < N) {
+          float v = x[b * N + t];
+          m = v > m ? v : m;
+        }
+      }
+      y[b * L + i] = m;
+    }
+  return 0;
+}
+
+int oracle_conv1d_ex_f32(const float* x, int64_t N, int64_t batch, const float* f, int64_t k,
+                         int64_t s, int64_t d, int64_t pl, int64_t pr, double* y, double* absmag) {
+  if (bad_ex(x, y, N, batch, k, s, d, pl, pr) || f == NULL) return -1;
+  int64_t L = oracle_out_len_ex(N, k, s, d, pl, pr);
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t i = 0; i < L; ++i) {
+      double acc = 0.0, mag = 0.0;
+      for (int64_t j = 0; j < k; ++j) {
+        int64_t t = i * s + j * d - pl;
+        if (t >= 0 && t < N) {
+          double p = (double)f[j] * (double)x[b * N + t];
+          acc += p;
+          mag += fabs(p);
+        }
+      }
+      y[b * L + i] = acc;
+      if (absmag) absmag[b * L + i] = mag;
+    }
   return 0;
 }
 

@@ -66,6 +66,25 @@ int oracle_pool2d_f32(const float* x, int64_t planes, int64_t H, int64_t W,
                       int64_t kh, int64_t kw, int64_t sh, int64_t sw, int mode,
                       double* y, double* absmag);
 
+/* Window spec with dilation and zero padding (SPEC.md
+ * l.263-268 WindowSpec, l.282 / l.332 pad semantics):
+ *   xp[t] = x[t - pl] for 0 <= t - pl < N, else padding;
+ *   output i covers xp[i*s + j*d], j < w;  extent E = (w-1)*d + 1;
+ *   out_len = (N + pl + pr - E) / s + 1  (-1 if invalid or E > N + pl + pr).
+ * Padding contributes 0 to sums and dot products and never wins a max (the
+ * max of a window made only of padding is the identity: -inf / INT32_MIN). */
+int64_t oracle_out_len_ex(int64_t N, int64_t w, int64_t s, int64_t d, int64_t pl, int64_t pr);
+int oracle_pool_sum_ex_i32(const int32_t* x, int64_t N, int64_t batch, int64_t w, int64_t s,
+                           int64_t d, int64_t pl, int64_t pr, int64_t* y);
+int oracle_pool_sum_ex_f32(const float* x, int64_t N, int64_t batch, int64_t w, int64_t s,
+                           int64_t d, int64_t pl, int64_t pr, double* y, double* absmag);
+int oracle_pool_max_ex_i32(const int32_t* x, int64_t N, int64_t batch, int64_t w, int64_t s,
+                           int64_t d, int64_t pl, int64_t pr, int32_t* y);
+int oracle_pool_max_ex_f32(const float* x, int64_t N, int64_t batch, int64_t w, int64_t s,
+                           int64_t d, int64_t pl, int64_t pr, float* y);
+int oracle_conv1d_ex_f32(const float* x, int64_t N, int64_t batch, const float* f, int64_t k,
+                         int64_t s, int64_t d, int64_t pl, int64_t pr, double* y, double* absmag);
+
 /* Eq. 8: gamma_i (+) gamma_j = (u_i*u_j, u_j*v_i + v_j). */
 void oracle_gamma_combine(double ui, double vi, double uj, double vj,
                           double* u_out, double* v_out);

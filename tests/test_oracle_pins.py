@@ -314,3 +314,79 @@ def test_generator_counter_based_and_distributions():
     u = synth.uniform_pm1(0, 100000)
     assert u.min() >= -1.0 and u.max() < 1.0
     assert np.all((u * 2 ** 23) == np.round(u * 2 ** 23))
+
+
+# ------------------------------------------- NEXT #1: zero padding + dilation (window spec)
+@pytest.mark.parametrize("case", GOLD["window_ex"], ids=lambda c: c["cite"])
+def test_golden_window_ex(case):
+    x = np.array(case["x"], np.float32)
+    a = (case["s"], case["d"], case["pl"], case["pr"])
+    if case["op"] == "conv":
+        y, _ = oracle.conv1d_ex(x, np.array(case["f"], np.float32), *a)
+    else:
+        y, _ = oracle.pool_sum_ex(x, case["w"], *a)
+        if case["op"] == "avg":
+            y = y / case["w"]
+    np.testing.assert_array_equal(y, np.array(case["y"], np.float64))
+
+
+EX_SPECS = [(1, 1, 0, 0), (2, 1, 0, 0), (1, 2, 0, 0), (1, 1, 2, 3), (3, 2, 1, 4), (2, 4, 5, 0), (1, 8, 7, 7)]
+
+
+@pytest.mark.parametrize("s,d,pl,pr", EX_SPECS)
+@pytest.mark.parametrize("w", [1, 2, 3, 7])
+def test_window_ex_vs_torch(w, s, d, pl, pr):
+    x = synth.normal(12, 3 * 500).reshape(3, 500)
+    xt = torch.from_numpy(x.astype(np.float64)).unsqueeze(1)
+    f = synth.normal(4, w, sigma=synth.cfg_sigma_filter(w))
+    ft = torch.from_numpy(f.astype(np.float64)).view(1, 1, w)
+    ref = F.conv1d(F.pad(xt, (pl, pr)), ft, stride=s, dilation=d).squeeze(1).numpy()
+    y, mag = oracle.conv1d_ex(x, f, s, d, pl, pr)
+    np.testing.assert_allclose(y, ref, rtol=1e-12, atol=1e-12)
+    ref_mag = F.conv1d(F.pad(xt.abs(), (pl, pr)), ft.abs(), stride=s, dilation=d).squeeze(1).numpy()
+    np.testing.assert_allclose(mag, ref_mag, rtol=1e-12, atol=1e-12)
+    ones = torch.ones(1, 1, w, dtype=torch.float64)
+    ys, _ = oracle.pool_sum_ex(x, w, s, d, pl, pr)
+    np.testing.assert_allclose(ys, F.conv1d(F.pad(xt, (pl, pr)), ones, stride=s, dilation=d).squeeze(1).numpy(),
+                               rtol=1e-12, atol=1e-12)
+    xm = F.pad(xt, (pl, pr), value=-np.inf)  # max padding never wins
+    refm = F.max_pool1d(xm, w, s, dilation=d).squeeze(1).numpy()
+    np.testing.assert_array_equal(oracle.pool_max_ex(x, w, s, d, pl, pr).astype(np.float64), refm)
+    xi = synth.randint(2, 3 * 500, -1000, 1000).reshape(3, 500)
+    yi = oracle.pool_sum_ex(xi, w, s, d, pl, pr)
+    np.testing.assert_array_equal(yi, np.rint(F.conv1d(F.pad(torch.from_numpy(xi.astype(np.float64)).unsqueeze(1), (pl, pr)),
+                                                       ones, stride=s, dilation=d).squeeze(1).numpy()).astype(np.int64))
+
+
+def test_window_ex_reduces_to_valid_ops():
+    x = synth.randint(3, 2 * 300, -1000, 1000).reshape(2, 300)
+    xf = synth.normal(3, 2 * 300).reshape(2, 300)
+    f = synth.normal(4, 5)
+    for w, s in ((1, 1), (3, 1), (5, 2), (8, 3)):
+        np.testing.assert_array_equal(oracle.pool_sum_ex(x, w, s), oracle.pool_sum(x, w, s))
+        np.testing.assert_array_equal(oracle.pool_max_ex(x, w, s), oracle.pool_max(x, w, s))
+        np.testing.assert_array_equal(oracle.pool_max_ex(xf, w, s), oracle.pool_max(xf, w, s))
+    np.testing.assert_array_equal(oracle.conv1d_ex(xf, f, 2)[0], oracle.conv1d(xf, f, 2)[0])
+
+
+def test_window_ex_brute_force_and_all_padding():
+    vals = [-2, 0, 1, 2]
+    for N in range(1, 5):
+        for xs in itertools.product(vals, repeat=N):
+            x = np.array(xs, np.int32)
+            for w, s, d, pl, pr in ((1, 1, 1, 2, 1), (2, 1, 2, 1, 1), (3, 2, 1, 2, 2), (2, 3, 3, 3, 0)):
+                L = oracle.out_len_ex(N, w, s, d, pl, pr)
+                if L < 0:
+                    continue
+                xp = [None] * pl + list(xs) + [None] * pr
+                exp_sum, exp_max = [], []
+                for i in range(L):
+                    win = [xp[i * s + j * d] for j in range(w)]
+                    valid = [v for v in win if v is not None]
+                    exp_sum.append(sum(valid))
+                    exp_max.append(max(valid) if valid else -2 ** 31)
+                assert oracle.pool_sum_ex(x, w, s, d, pl, pr).tolist() == exp_sum
+                assert oracle.pool_max_ex(x, w, s, d, pl, pr).tolist() == exp_max
+    # a window made only of padding: sum 0, max = identity
+    assert oracle.pool_max_ex(np.array([5.0], np.float32), 1, 1, 1, 1, 0)[0] == -np.inf
+    assert oracle.out_len_ex(3, 4, 1, 1, 0, 0) == -1 and oracle.out_len_ex(3, 4, 1, 1, 1, 0) == 1
