@@ -58,9 +58,9 @@ class Cell:
     """One kernel launch of the workload."""
 
     def __init__(self, cfg, name, op, *, w=None, f=None, kh=None, kw=None, sh=None, sw=None,
-                 mode=None, inp=None, stride=1):
+                 mode=None, inp=None, stride=1, dilation=1, pads=(0, 0)):
         self.cfg, self.name, self.op = cfg, name, op
-        self.stride = stride
+        self.stride, self.dilation, self.pads = stride, dilation, pads
         self.w, self.f, self.kh, self.kw, self.sh, self.sw, self.mode = w, f, kh, kw, sh, sw, mode
         self.inp = inp  # key of the input tensor it reads
         self.n_out = 0
@@ -111,6 +111,14 @@ def cfg_cells(workload: str):
         cells.append(Cell("stride", "stride_sum_w4_s4", "sum", w=4, stride=4, inp="xs"))
         cells.append(Cell("stride", "stride_conv_k7_s2", "conv", w=7, stride=2,
                           f=synth.normal(4, 7, sigma=synth.cfg_sigma_filter(7)), inp="xs"))
+    if workload == "winspec":  # zero padding + dilation; not a BASELINE config
+        inputs["xw"] = dict(rows=64, n=1 << 20, dtype="float32", dist="normal", seed=3, kw={},
+                            shard="batch")
+        for k, d, pad in ((7, 1, 3), (31, 1, 15), (7, 4, 12), (15, 8, 0)):
+            cells.append(Cell("winspec", f"winspec_conv_k{k}_d{d}_p{pad}", "conv", w=k, dilation=d, pads=(pad, pad),
+                              f=synth.normal(4, k, sigma=synth.cfg_sigma_filter(k)), inp="xw"))
+        cells.append(Cell("winspec", "winspec_max_w3_p1", "max", w=3, pads=(1, 1), inp="xw"))
+        cells.append(Cell("winspec", "winspec_sum_w8_d2", "sum", w=8, dilation=2, inp="xw"))
     if not cells:
         raise SystemExit(f"unknown workload {workload}")
     return inputs, cells
@@ -258,7 +266,7 @@ class Runner:
                 c.bytes = (sh.size + c.n_out) * es
             elif kind == "batch":
                 rows, n = geo
-                L = (n - c.w) // c.stride + 1
+                L = (n + sum(c.pads) - ((c.w - 1) * c.dilation + 1)) // c.stride + 1
                 self.y[c.name] = torch.empty((rows, L), dtype=x.dtype, device=self.device)
                 c.n_out = rows * L
                 c.bytes = (rows * n + c.n_out) * es
@@ -279,12 +287,13 @@ class Runner:
             N, B = x.shape[0], 1
         else:
             B, N = x.shape
+        win = (c.stride, c.dilation, c.pads[0], c.pads[1], code, s)
         if c.op == "conv":
-            st = ss.ss_conv1d(x.data_ptr(), y.data_ptr(), N, B, c.f, c.w, c.stride, code, s)
+            st = ss.ss_conv1d_ex(x.data_ptr(), y.data_ptr(), N, B, c.f, c.w, *win)
         elif c.op == "sum":
-            st = ss.ss_pool_sum(x.data_ptr(), y.data_ptr(), N, B, c.w, c.stride, code, s)
+            st = ss.ss_pool_sum_ex(x.data_ptr(), y.data_ptr(), N, B, c.w, *win)
         else:
-            st = ss.ss_pool_max(x.data_ptr(), y.data_ptr(), N, B, c.w, c.stride, code, s)
+            st = ss.ss_pool_max_ex(x.data_ptr(), y.data_ptr(), N, B, c.w, *win)
         ss.check(st)
 
     def _launch_cell(self, c, events=None):
@@ -666,7 +675,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="suite", choices=["suite", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "stride"])
+    ap.add_argument("--workload", default="suite", choices=["suite", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "stride", "winspec"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)

@@ -24,8 +24,9 @@
  *  Layout     1-D: x is [batch][N] row-major contiguous (row pitch N);
  *             y is [batch][out_len] contiguous, out_len = ss_out_len(N,w,s).
  *             2-D: x is [planes][H][W], y is [planes][OH][OW], contiguous.
- *             Valid padding only: output i covers x[i*s .. i*s+w-1]
- *             (readings R1-R4).
+ *             Valid padding: output i covers x[i*s .. i*s+w-1] (DESIGN.md
+ *             readings R1-R4); the *_ex calls below add dilation and zero
+ *             padding.
  *  Sizes      int64_t throughout (N = 2^32 is supported).
  *  Stream     `stream` is a cudaStream_t passed as void* (NULL = the legacy
  *             default stream).  Every call only ENQUEUES work on `stream`
@@ -40,10 +41,11 @@
  *  Memory     The library allocates no device memory and keeps no per-call
  *             state; it caches per-device attributes (SM count) only.
  *  Numerics   int32 + wraps modulo 2^32.  fp32 uses IEEE round-to-nearest
- *             FMA/adds (no fast-math, no flush-to-zero).  max uses
- *             `a > b ? a : b` (inputs are finite; NaN unsupported).  Results
- *             are bitwise deterministic run to run; conv1d and max results
- *             are also independent of tiling and of sharding.  fp32 results
+ *             FMA/adds (no fast-math, no flush-to-zero).  max equals
+ *             `a > b ? a : b` for finite inputs (NaN unsupported; the sign of
+ *             a zero maximum is unspecified).  Results are bitwise
+ *             deterministic run to run; conv1d and max results are also
+ *             independent of tiling and of sharding.  fp32 results
  *             satisfy |y - y_exact| <= 1e-5 * sum_j |x_j f_j| + 1e-6
  *             (BASELINE.json north_star; f = 1 for sums, 1/(kh*kw) for avg).
  */
@@ -56,7 +58,7 @@
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 1
+#define SS_ABI_VERSION 2
 
 typedef enum { SS_F32 = 0, SS_I32 = 1 } ss_dtype_t;
 typedef enum { SS_POOL_MAX = 0, SS_POOL_AVG = 1 } ss_pool_mode_t;
@@ -66,7 +68,8 @@ typedef enum {
   SS_ERR_NULL = 1,                  /* a required pointer is NULL              */
   SS_ERR_BAD_SIZE = 2,              /* N/batch/w/k/stride/planes/H/W < 1, or a  */
                                     /* size whose byte count overflows int64    */
-  SS_ERR_WINDOW_EXCEEDS_INPUT = 3,  /* w > N ("window exceeds")  */
+  SS_ERR_WINDOW_EXCEEDS_INPUT = 3,  /* w > N ("window exceeds"); */
+                                    /* _ex: (w-1)*dilation+1 > N+pads           */
   SS_ERR_UNSUPPORTED = 4,           /* dtype/op combination not provided,      */
                                     /* or k > SS_K_MAX                          */
   SS_ERR_CUDA = 5,                  /* CUDA launch/attribute failure           */
@@ -97,7 +100,9 @@ ss_status_t ss_pool_max(const void* x, void* y, int64_t N, int64_t batch,
 /* Sliding dot product = 1-D convolution with a length-k filter (PAPER.md
  * l.86-87, Sec. 2.5; Eq. 4 per window), cross-correlation orientation
  * (reading R2): y[b][i] = sum_{j<k} filter[j] * x[b][i*stride + j],
- * accumulated in fp32 FMA in the fixed order j = 0..k-1.  One filter shared
+ * accumulated in fp32 as fl(S_even + S_odd): S_even / S_odd are FMA chains over
+ * the even / odd taps in increasing j from 0 (an association fixed by the tap
+ * index alone, so every output is independent of tiling).  One filter shared
  * by all rows.  `filter_host` (k floats, HOST memory) is read before the call
  * returns and may be freed immediately.  dtype must be SS_F32; 1 <= k <= SS_K_MAX. */
 ss_status_t ss_conv1d(const void* x, void* y, int64_t N, int64_t batch,
@@ -113,6 +118,31 @@ ss_status_t ss_conv1d(const void* x, void* y, int64_t N, int64_t batch,
 ss_status_t ss_pool2d(const void* x, void* y, int64_t planes, int64_t H, int64_t W,
                       int64_t kh, int64_t kw, int64_t sh, int64_t sw,
                       ss_pool_mode_t mode, ss_dtype_t dtype, void* stream);
+
+/* ---- window spec: stride, dilation, zero padding -------
+ * The input is logically extended by pad_left / pad_right positions of
+ * padding: xp[t] = x[t - pad_left] for 0 <= t - pad_left < N.  Output i of a
+ * row covers xp[i*stride + j*dilation], j < w (or k), so
+ *   out_len = (N + pad_left + pad_right - ((w-1)*dilation + 1)) / stride + 1
+ * (SPEC.md l.263-268 WindowSpec).  Padding adds 0 to sums and dot products and
+ * never wins a max; a window made only of padding yields the
+ * identity (0, -inf, INT32_MIN).  dilation >= 1, pads >= 0; everything else,
+ * layout (y is [batch][out_len]), errors, streams and numerics as for the
+ * valid-padding calls above (which equal these with dilation 1, pads 0).
+ * Stride 1 without dilation runs the TMA tile kernel on the interior outputs
+ * and a direct kernel on the pad_left + pad_right edge outputs of each row. */
+int64_t ss_out_len_ex(int64_t N, int64_t w, int64_t stride, int64_t dilation,
+                      int64_t pad_left, int64_t pad_right);
+ss_status_t ss_pool_sum_ex(const void* x, void* y, int64_t N, int64_t batch, int64_t w,
+                           int64_t stride, int64_t dilation, int64_t pad_left,
+                           int64_t pad_right, ss_dtype_t dtype, void* stream);
+ss_status_t ss_pool_max_ex(const void* x, void* y, int64_t N, int64_t batch, int64_t w,
+                           int64_t stride, int64_t dilation, int64_t pad_left,
+                           int64_t pad_right, ss_dtype_t dtype, void* stream);
+ss_status_t ss_conv1d_ex(const void* x, void* y, int64_t N, int64_t batch,
+                         const float* filter_host, int64_t k, int64_t stride,
+                         int64_t dilation, int64_t pad_left, int64_t pad_right,
+                         ss_dtype_t dtype, void* stream);
 
 /* Static description of a status code. */
 const char* ss_status_string(ss_status_t s);

@@ -33,7 +33,8 @@ SS_ERR_OVERLAP = 6
 SS_K_MAX = 1024
 
 EXPORTED = ("ss_abi_version", "ss_out_len", "ss_pool_sum", "ss_pool_max", "ss_conv1d",
-            "ss_pool2d", "ss_status_string", "ss_last_error", "ss_launch_count")
+            "ss_pool2d", "ss_status_string", "ss_last_error", "ss_launch_count",
+            "ss_out_len_ex", "ss_pool_sum_ex", "ss_pool_max_ex", "ss_conv1d_ex")
 
 
 class SSError(RuntimeError):
@@ -60,6 +61,14 @@ def _load() -> ctypes.CDLL:
     L.ss_conv1d.restype = i32
     L.ss_pool2d.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, i32, i32, vp]
     L.ss_pool2d.restype = i32
+    L.ss_out_len_ex.argtypes = [i64] * 6
+    L.ss_out_len_ex.restype = i64
+    for n in ("ss_pool_sum_ex", "ss_pool_max_ex"):
+        getattr(L, n).argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, i32, vp]
+        getattr(L, n).restype = i32
+    L.ss_conv1d_ex.argtypes = [vp, vp, i64, i64, ctypes.POINTER(ctypes.c_float), i64, i64, i64, i64, i64,
+                               i32, vp]
+    L.ss_conv1d_ex.restype = i32
     L.ss_status_string.argtypes = [i32]
     L.ss_status_string.restype = ctypes.c_char_p
     L.ss_last_error.argtypes = []
@@ -118,6 +127,25 @@ def ss_pool2d(x_ptr: int, y_ptr: int, planes: int, H: int, W: int, kh: int, kw: 
     return _lib.ss_pool2d(x_ptr, y_ptr, planes, H, W, kh, kw, sh, sw, mode, dtype, stream)
 
 
+def ss_out_len_ex(N: int, w: int, stride: int = 1, dilation: int = 1, pad_left: int = 0,
+                  pad_right: int = 0) -> int:
+    return int(_lib.ss_out_len_ex(N, w, stride, dilation, pad_left, pad_right))
+
+
+def ss_pool_sum_ex(x_ptr, y_ptr, N, batch, w, stride, dilation, pad_left, pad_right, dtype, stream=0) -> int:
+    return _lib.ss_pool_sum_ex(x_ptr, y_ptr, N, batch, w, stride, dilation, pad_left, pad_right, dtype, stream)
+
+
+def ss_pool_max_ex(x_ptr, y_ptr, N, batch, w, stride, dilation, pad_left, pad_right, dtype, stream=0) -> int:
+    return _lib.ss_pool_max_ex(x_ptr, y_ptr, N, batch, w, stride, dilation, pad_left, pad_right, dtype, stream)
+
+
+def ss_conv1d_ex(x_ptr, y_ptr, N, batch, filter_host, k, stride, dilation, pad_left, pad_right,
+                 dtype=SS_F32, stream=0) -> int:
+    fp = None if filter_host is None else (ctypes.c_float * len(filter_host))(*[float(v) for v in filter_host])
+    return _lib.ss_conv1d_ex(x_ptr, y_ptr, N, batch, fp, k, stride, dilation, pad_left, pad_right, dtype, stream)
+
+
 def check(status: int) -> None:
     if status != SS_OK:
         raise SSError(status, ss_last_error())
@@ -166,39 +194,55 @@ def _out(x, L, out):
     return out
 
 
-def pool_sum(x, w: int, stride: int = 1, out=None, stream=None):
-    """Eq. 3 with + (raw window sums) over the last dim of a CUDA [N] / [B, N] tensor."""
+def _pads(padding):
+    if isinstance(padding, (tuple, list)):
+        return int(padding[0]), int(padding[1])
+    return int(padding), int(padding)
+
+
+def pool_sum(x, w: int, stride: int = 1, out=None, stream=None, dilation: int = 1, padding=0):
+    """Eq. 3 with + (raw window sums) over the last dim of a CUDA [N] / [B, N] tensor;
+    optional dilation and zero padding (int or (left, right))."""
     N, B = _rows(x)
-    L = ss_out_len(N, w, stride)
+    pl, pr = _pads(padding)
+    L = ss_out_len_ex(N, w, stride, dilation, pl, pr)
+    args = (N, B, w, stride, dilation, pl, pr, _dtype_code(x), _stream(stream))
     if L < 0:
-        check(ss_pool_sum(x.data_ptr(), 0, N, B, w, stride, _dtype_code(x), _stream(stream)) or SS_ERR_BAD_SIZE)
+        check(ss_pool_sum_ex(x.data_ptr(), 0, *args) or SS_ERR_BAD_SIZE)
     y = _out(x, L, out)
-    check(ss_pool_sum(x.data_ptr(), y.data_ptr(), N, B, w, stride, _dtype_code(x), _stream(stream)))
+    check(ss_pool_sum_ex(x.data_ptr(), y.data_ptr(), *args))
     return y
 
 
-def pool_max(x, w: int, stride: int = 1, out=None, stream=None):
-    """Eq. 3 with max over the last dim of a CUDA [N] / [B, N] tensor."""
+def pool_max(x, w: int, stride: int = 1, out=None, stream=None, dilation: int = 1, padding=0):
+    """Eq. 3 with max over the last dim of a CUDA [N] / [B, N] tensor; optional
+    dilation and padding (padding never wins)."""
     N, B = _rows(x)
-    L = ss_out_len(N, w, stride)
+    pl, pr = _pads(padding)
+    L = ss_out_len_ex(N, w, stride, dilation, pl, pr)
+    args = (N, B, w, stride, dilation, pl, pr, _dtype_code(x), _stream(stream))
     if L < 0:
-        check(ss_pool_max(x.data_ptr(), 0, N, B, w, stride, _dtype_code(x), _stream(stream)) or SS_ERR_BAD_SIZE)
+        check(ss_pool_max_ex(x.data_ptr(), 0, *args) or SS_ERR_BAD_SIZE)
     y = _out(x, L, out)
-    check(ss_pool_max(x.data_ptr(), y.data_ptr(), N, B, w, stride, _dtype_code(x), _stream(stream)))
+    check(ss_pool_max_ex(x.data_ptr(), y.data_ptr(), *args))
     return y
 
 
-def conv1d(x, filt, stride: int = 1, out=None, stream=None):
+def conv1d(x, filt, stride: int = 1, out=None, stream=None, dilation: int = 1, padding=0):
     """Sliding dot product (cross-correlation) of a CUDA fp32 [N]/[B, N] tensor with
-    a host filter (sequence of floats, numpy array or CPU tensor)."""
+    a host filter (sequence of floats, numpy array or CPU tensor); optional
+    dilation and zero padding."""
     N, B = _rows(x)
     f = [float(v) for v in (filt.tolist() if hasattr(filt, "tolist") else filt)]
     k = len(f)
-    L = ss_out_len(N, k, stride)
+    pl, pr = _pads(padding)
+    L = ss_out_len_ex(N, k, stride, dilation, pl, pr)
     if L < 0:
-        check(ss_conv1d(x.data_ptr(), 0, N, B, f, k, stride, _dtype_code(x), _stream(stream)) or SS_ERR_BAD_SIZE)
+        check(ss_conv1d_ex(x.data_ptr(), 0, N, B, f, k, stride, dilation, pl, pr, _dtype_code(x),
+                           _stream(stream)) or SS_ERR_BAD_SIZE)
     y = _out(x, L, out)
-    check(ss_conv1d(x.data_ptr(), y.data_ptr(), N, B, f, k, stride, _dtype_code(x), _stream(stream)))
+    check(ss_conv1d_ex(x.data_ptr(), y.data_ptr(), N, B, f, k, stride, dilation, pl, pr, _dtype_code(x),
+                       _stream(stream)))
     return y
 
 

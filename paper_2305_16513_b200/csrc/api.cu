@@ -106,7 +106,8 @@ bool encode_rows_map(CUtensorMap* m, const void* base, int64_t rows, int box_row
 
 // Fill the TMA-kernel geometry; false if this problem cannot take that path.
 static bool make_slide_params(Slide1DParams& p, const void* x, void* y, int64_t N, int64_t batch,
-                              int64_t L) {
+                              int64_t L, int64_t y_pitch = -1, int64_t y_off = 0) {
+  if (y_pitch < 0) y_pitch = L;
   memset(&p, 0, sizeof p);
   const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
   if ((xa & 3) || (ya & 3)) return false;
@@ -121,7 +122,9 @@ static bool make_slide_params(Slide1DParams& p, const void* x, void* y, int64_t 
   const int64_t x_rows = p.x_total_elems / 32;
   if (x_rows < 8 || x_rows >= (int64_t(1) << 31) - 1024) return false;
   p.x_full_elems = 32 * x_rows;
-  const int64_t y_rows = (p.shift_y + batch * L) / 32;
+  p.y_pitch = y_pitch;
+  p.y_off = y_off;
+  const int64_t y_rows = (p.shift_y + batch * y_pitch) / 32;
   if (y_rows >= (int64_t(1) << 31) - 1024) return false;
   if (!make_map(&p.tm_x_main, p.x_view, x_rows, kSlideTileRows)) return false;
   if (!make_map(&p.tm_x_halo, p.x_view, x_rows, 8)) return false;
@@ -135,19 +138,36 @@ static bool overlaps(const void* a, int64_t abytes, const void* b, int64_t bbyte
   return a0 < b0 + (uintptr_t)bbytes && b0 < a0 + (uintptr_t)abytes;
 }
 
+// Window spec (ss.h): stride s, dilation d, zero padding pl/pr.  Computes the
+// output length; validates everything before anything is enqueued.
 static ss_status_t validate_1d(const void* x, const void* y, int64_t N, int64_t batch, int64_t w,
-                               int64_t stride, const char* wname, int64_t* L) {
+                               int64_t stride, int64_t d, int64_t pl, int64_t pr, const char* wname,
+                               int64_t* L) {
   if (!x || !y) return fail(SS_ERR_NULL, "x and y must be non-NULL device pointers");
-  if (N < 1 || batch < 1 || w < 1 || stride < 1)
-    return fail(SS_ERR_BAD_SIZE, "N=%lld batch=%lld %s=%lld stride=%lld must all be >= 1",
-                (long long)N, (long long)batch, wname, (long long)w, (long long)stride);
-  if (N > INT64_MAX / 8 / batch) return fail(SS_ERR_BAD_SIZE, "batch*N*4 overflows int64");
-  if (w > N)
-    return fail(SS_ERR_WINDOW_EXCEEDS_INPUT, "window exceeds input: %s=%lld > N=%lld", wname,
-                (long long)w, (long long)N);
-  *L = (N - w) / stride + 1;
+  if (N < 1 || batch < 1 || w < 1 || stride < 1 || d < 1)
+    return fail(SS_ERR_BAD_SIZE, "N=%lld batch=%lld %s=%lld stride=%lld dilation=%lld must all be >= 1",
+                (long long)N, (long long)batch, wname, (long long)w, (long long)stride, (long long)d);
+  if (pl < 0 || pr < 0) return fail(SS_ERR_BAD_SIZE, "padding must be >= 0");
+  if (N > INT64_MAX / 8 / batch || pl > INT64_MAX / 8 - N || pr > INT64_MAX / 8 - N - pl ||
+      w > INT64_MAX / 8 / d)
+    return fail(SS_ERR_BAD_SIZE, "sizes overflow int64");
+  const int64_t E = (w - 1) * d + 1, Np = N + pl + pr;
+  if (E > Np)
+    return fail(SS_ERR_WINDOW_EXCEEDS_INPUT, "window exceeds input: extent %lld > padded N=%lld",
+                (long long)E, (long long)Np);
+  *L = (Np - E) / stride + 1;
+  if (*L > INT64_MAX / 8 / batch) return fail(SS_ERR_BAD_SIZE, "batch*out_len*4 overflows int64");
   if (overlaps(x, batch * N * 4, y, batch * *L * 4)) return fail(SS_ERR_OVERLAP, "x and y overlap");
   return SS_OK;
+}
+
+static GenericParams generic_params(const void* x, void* y, int64_t N, int64_t L, int64_t batch,
+                                    int64_t w, int64_t stride, int64_t d, int64_t pl) {
+  GenericParams g;
+  memset(&g, 0, sizeof g);
+  g.x = x; g.y = y; g.N = N; g.L = L; g.batch = batch; g.w = w; g.stride = stride;
+  g.dilation = d; g.pad_left = pl;
+  return g;
 }
 
 static int pool_pivot(int64_t w) {
@@ -166,28 +186,59 @@ static int conv_bucket(int64_t k) {
   return 0;
 }
 
-static ss_status_t pool_impl(int op, const void* x, void* y, int64_t N, int64_t batch, int64_t w,
-                             int64_t stride, ss_dtype_t dtype, void* stream) {
+// One 1-D window op.  Stride 1 without dilation takes the TMA tile kernel
+// for every output whose window lies inside the row (with zero padding the
+// tile kernel writes the interior of each padded output row, and a small
+// generic launch fills the pl + pr edge outputs); everything else runs the
+// direct-window generic kernels.
+static ss_status_t window_impl(int op, const void* x, void* y, int64_t N, int64_t batch, int64_t w,
+                               int64_t stride, int64_t d, int64_t pl, int64_t pr, ss_dtype_t dtype,
+                               const float* taps, void* stream) {
   int64_t L = 0;
-  ss_status_t st = validate_1d(x, y, N, batch, w, stride, "w", &L);
+  ss_status_t st = validate_1d(x, y, N, batch, w, stride, d, pl, pr, op == kOpConv ? "k" : "w", &L);
   if (st != SS_OK) return st;
-  if (dtype != SS_F32 && dtype != SS_I32) return fail(SS_ERR_UNSUPPORTED, "dtype %d", (int)dtype);
+  if (op == kOpConv) {
+    if (dtype != SS_F32) return fail(SS_ERR_UNSUPPORTED, "conv1d supports SS_F32 only");
+    if (w > SS_K_MAX) return fail(SS_ERR_UNSUPPORTED, "k=%lld > SS_K_MAX=%d", (long long)w, SS_K_MAX);
+  } else if (dtype != SS_F32 && dtype != SS_I32) {
+    return fail(SS_ERR_UNSUPPORTED, "dtype %d", (int)dtype);
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int grid = current_sms();
-  if (stride == 1 && w <= kPoolTmaMaxW) {
-    Slide1DParams p;
-    if (make_slide_params(p, x, y, N, batch, L)) {
-      p.w = w;
-      cudaError_t e = launch_pool_tma(p, op, dtype == SS_I32 ? 1 : 0, pool_pivot(w), s, grid);
-      if (e == cudaSuccess) return SS_OK;
-      if (e != cudaErrorInvalidConfiguration) return cuda_fail(e, "pool tma launch");
+  const int dt = dtype == SS_I32 ? 1 : 0;
+  const int64_t L_int = N - w + 1;  // outputs whose window is inside the row (stride 1, d 1)
+  bool interior_done = false;
+  if (stride == 1 && d == 1 && L_int >= 1) {
+    const int KT = op == kOpConv ? conv_bucket(w) : 0;
+    if (op == kOpConv ? KT > 0 : w <= kPoolTmaMaxW) {
+      Slide1DParams p;
+      // interior outputs land at y[b*L + pl + i], i < L_int
+      char* y_int = static_cast<char*>(y) + 4 * pl;
+      if (make_slide_params(p, x, y_int, N, batch, L_int, L, 0)) {
+        p.w = w;
+        cudaError_t e;
+        if (op == kOpConv) {
+          for (int j = 0; j < KT; ++j) p.taps[j] = j < w ? taps[j] : 0.0f;
+          e = launch_conv_tma(p, KT, s, grid);
+        } else {
+          e = launch_pool_tma(p, op, dt, pool_pivot(w), s, grid);
+        }
+        if (e == cudaSuccess) interior_done = true;
+        else if (e != cudaErrorInvalidConfiguration) return cuda_fail(e, "tma launch");
+      }
     }
   }
-  GenericParams g;
-  memset(&g, 0, sizeof g);
-  g.x = x; g.y = y; g.N = N; g.L = L; g.batch = batch; g.w = w; g.stride = stride;
-  cudaError_t e = launch_pool_generic(g, op, dtype == SS_I32 ? 1 : 0, s, grid * 8);
-  return e == cudaSuccess ? SS_OK : cuda_fail(e, "pool generic launch");
+  if (interior_done && pl == 0 && pr == 0) return SS_OK;
+  GenericParams g = generic_params(x, y, N, L, batch, w, stride, d, pl);
+  if (interior_done) {
+    g.skip_lo = pl;
+    g.skip_hi = pl + L_int;
+  }
+  if (op == kOpConv)
+    for (int64_t j = 0; j < w; ++j) g.taps[j] = taps[j];
+  cudaError_t e = op == kOpConv ? launch_conv_generic(g, s, grid * 8)
+                                : launch_pool_generic(g, op, dt, s, grid * 8);
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "generic launch");
 }
 
 }  // namespace ss
@@ -205,41 +256,50 @@ int64_t ss_out_len(int64_t N, int64_t w, int64_t stride) {
 
 ss_status_t ss_pool_sum(const void* x, void* y, int64_t N, int64_t batch, int64_t w,
                         int64_t stride, ss_dtype_t dtype, void* stream) {
-  return pool_impl(kOpSum, x, y, N, batch, w, stride, dtype, stream);
+  return window_impl(kOpSum, x, y, N, batch, w, stride, 1, 0, 0, dtype, nullptr, stream);
 }
 
 ss_status_t ss_pool_max(const void* x, void* y, int64_t N, int64_t batch, int64_t w,
                         int64_t stride, ss_dtype_t dtype, void* stream) {
-  return pool_impl(kOpMax, x, y, N, batch, w, stride, dtype, stream);
+  return window_impl(kOpMax, x, y, N, batch, w, stride, 1, 0, 0, dtype, nullptr, stream);
 }
 
 ss_status_t ss_conv1d(const void* x, void* y, int64_t N, int64_t batch, const float* filter_host,
                       int64_t k, int64_t stride, ss_dtype_t dtype, void* stream) {
-  int64_t L = 0;
   if (!filter_host) return fail(SS_ERR_NULL, "filter_host must be non-NULL");
-  ss_status_t st = validate_1d(x, y, N, batch, k, stride, "k", &L);
-  if (st != SS_OK) return st;
-  if (dtype != SS_F32) return fail(SS_ERR_UNSUPPORTED, "conv1d supports SS_F32 only");
-  if (k > SS_K_MAX) return fail(SS_ERR_UNSUPPORTED, "k=%lld > SS_K_MAX=%d", (long long)k, SS_K_MAX);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int grid = current_sms();
-  const int KT = conv_bucket(k);
-  if (stride == 1 && KT > 0) {
-    Slide1DParams p;
-    if (make_slide_params(p, x, y, N, batch, L)) {
-      for (int j = 0; j < KT; ++j) p.taps[j] = j < k ? filter_host[j] : 0.0f;
-      p.w = k;
-      cudaError_t e = launch_conv_tma(p, KT, s, grid);
-      if (e == cudaSuccess) return SS_OK;
-      if (e != cudaErrorInvalidConfiguration) return cuda_fail(e, "conv tma launch");
-    }
-  }
-  GenericParams g;
-  memset(&g, 0, sizeof g);
-  g.x = x; g.y = y; g.N = N; g.L = L; g.batch = batch; g.w = k; g.stride = stride;
-  for (int64_t j = 0; j < k; ++j) g.taps[j] = filter_host[j];
-  cudaError_t e = launch_conv_generic(g, s, grid * 8);
-  return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv generic launch");
+  return window_impl(kOpConv, x, y, N, batch, k, stride, 1, 0, 0, dtype, filter_host, stream);
+}
+
+ss_status_t ss_pool_sum_ex(const void* x, void* y, int64_t N, int64_t batch, int64_t w,
+                           int64_t stride, int64_t dilation, int64_t pad_left, int64_t pad_right,
+                           ss_dtype_t dtype, void* stream) {
+  return window_impl(kOpSum, x, y, N, batch, w, stride, dilation, pad_left, pad_right, dtype, nullptr,
+                     stream);
+}
+
+ss_status_t ss_pool_max_ex(const void* x, void* y, int64_t N, int64_t batch, int64_t w,
+                           int64_t stride, int64_t dilation, int64_t pad_left, int64_t pad_right,
+                           ss_dtype_t dtype, void* stream) {
+  return window_impl(kOpMax, x, y, N, batch, w, stride, dilation, pad_left, pad_right, dtype, nullptr,
+                     stream);
+}
+
+ss_status_t ss_conv1d_ex(const void* x, void* y, int64_t N, int64_t batch, const float* filter_host,
+                         int64_t k, int64_t stride, int64_t dilation, int64_t pad_left,
+                         int64_t pad_right, ss_dtype_t dtype, void* stream) {
+  if (!filter_host) return fail(SS_ERR_NULL, "filter_host must be non-NULL");
+  return window_impl(kOpConv, x, y, N, batch, k, stride, dilation, pad_left, pad_right, dtype,
+                     filter_host, stream);
+}
+
+int64_t ss_out_len_ex(int64_t N, int64_t w, int64_t stride, int64_t dilation, int64_t pad_left,
+                      int64_t pad_right) {
+  if (N < 1 || w < 1 || stride < 1 || dilation < 1 || pad_left < 0 || pad_right < 0) return -1;
+  if (w > INT64_MAX / 8 / dilation || pad_left > INT64_MAX / 8 - N || pad_right > INT64_MAX / 8 - N - pad_left)
+    return -1;
+  const int64_t E = (w - 1) * dilation + 1, Np = N + pad_left + pad_right;
+  if (E > Np) return -1;
+  return (Np - E) / stride + 1;
 }
 
 ss_status_t ss_pool2d(const void* x, void* y, int64_t planes, int64_t H, int64_t W, int64_t kh,

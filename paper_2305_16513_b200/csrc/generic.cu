@@ -48,6 +48,69 @@ __global__ void __launch_bounds__(kGenThreads) pool_generic_kernel(const __grid_
   }
 }
 
+// Window spec with dilation and zero padding (NEXT #1): tap j of output i
+// reads x[i*s + j*d - pl] when in range; padding adds nothing to a sum and
+// never wins a max (identity).  Full mode: kGenOuts outputs per thread with
+// an unchecked loop when all of their windows lie inside the row.  Skip mode
+// (skip_lo < skip_hi): only outputs outside [skip_lo, skip_hi) -- the edges
+// around an interior the tile kernel computed -- one per thread.
+template <class Op>
+__device__ __forceinline__ typename Op::T window_checked(const typename Op::T* __restrict__ xr,
+                                                         int64_t t0, const GenericParams& p) {
+  typename Op::T acc = Op::identity();
+  for (int j = 0; j < (int)p.w; ++j) {
+    const int64_t t = t0 + (int64_t)j * p.dilation;
+    if (t >= 0 && t < p.N) acc = Op::combine(acc, __ldg(xr + t));
+  }
+  return acc;
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kGenThreads) pool_generic_ex_kernel(const __grid_constant__ GenericParams p) {
+  using T = typename Op::T;
+  const int w = (int)p.w;
+  const int64_t ext = (int64_t)(w - 1) * p.dilation;
+  if (p.skip_lo < p.skip_hi) {
+    const int64_t n_lo = p.skip_lo, n_work = n_lo + (p.L - p.skip_hi);
+    for (int64_t b = blockIdx.y; b < p.batch; b += gridDim.y) {
+      const T* __restrict__ xr = static_cast<const T*>(p.x) + b * p.N;
+      T* __restrict__ yr = static_cast<T*>(p.y) + b * p.L;
+      for (int64_t q = (int64_t)blockIdx.x * kGenThreads + threadIdx.x; q < n_work;
+           q += (int64_t)gridDim.x * kGenThreads) {
+        const int64_t i = q < n_lo ? q : p.skip_hi + (q - n_lo);
+        yr[i] = window_checked<Op>(xr, i * p.stride - p.pad_left, p);
+      }
+    }
+    return;
+  }
+  for (int64_t b = blockIdx.y; b < p.batch; b += gridDim.y) {
+    const T* __restrict__ xr = static_cast<const T*>(p.x) + b * p.N;
+    T* __restrict__ yr = static_cast<T*>(p.y) + b * p.L;
+    for (int64_t i0 = (int64_t)blockIdx.x * kGenChunk; i0 < p.L; i0 += (int64_t)gridDim.x * kGenChunk) {
+      const int64_t ia = i0 + threadIdx.x, ib = ia + (kGenOuts - 1) * kGenThreads;
+      const int64_t ta = ia * p.stride - p.pad_left, tb = ib * p.stride - p.pad_left;
+      if (ta >= 0 && tb + ext < p.N && ib < p.L) {  // every window of this thread is inside
+        T acc[kGenOuts];
+#pragma unroll
+        for (int k = 0; k < kGenOuts; ++k) acc[k] = __ldg(xr + ta + (int64_t)k * kGenThreads * p.stride);
+        for (int j = 1; j < w; ++j) {
+#pragma unroll
+          for (int k = 0; k < kGenOuts; ++k)
+            acc[k] = Op::combine(acc[k], __ldg(xr + ta + (int64_t)k * kGenThreads * p.stride + (int64_t)j * p.dilation));
+        }
+#pragma unroll
+        for (int k = 0; k < kGenOuts; ++k) yr[ia + k * kGenThreads] = acc[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < kGenOuts; ++k) {
+          const int64_t i = ia + k * kGenThreads;
+          if (i < p.L) yr[i] = window_checked<Op>(xr, i * p.stride - p.pad_left, p);
+        }
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kGenThreads) conv_generic_kernel(const __grid_constant__ GenericParams p) {
   const int k = (int)p.w;
   for (int64_t b = blockIdx.y; b < p.batch; b += gridDim.y) {
@@ -79,6 +142,71 @@ __global__ void __launch_bounds__(kGenThreads) conv_generic_kernel(const __grid_
       for (int q = 0; q < kGenOuts; ++q) {
         const int64_t i = i0 + threadIdx.x + q * kGenThreads;
         if (i < p.L) yr[i] = __fadd_rn(s0[q], s1[q]);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ float conv_checked(const float* __restrict__ xr, int64_t t0,
+                                              const GenericParams& p) {
+  float s0 = 0.0f, s1 = 0.0f;  // same association as conv_generic_kernel / ConvKind
+  for (int j = 0; j < (int)p.w; j += 2) {
+    const int64_t t = t0 + (int64_t)j * p.dilation;
+    if (t >= 0 && t < p.N) s0 = __fmaf_rn(p.taps[j], __ldg(xr + t), s0);
+  }
+  for (int j = 1; j < (int)p.w; j += 2) {
+    const int64_t t = t0 + (int64_t)j * p.dilation;
+    if (t >= 0 && t < p.N) s1 = __fmaf_rn(p.taps[j], __ldg(xr + t), s1);
+  }
+  return __fadd_rn(s0, s1);
+}
+
+__global__ void __launch_bounds__(kGenThreads) conv_generic_ex_kernel(const __grid_constant__ GenericParams p) {
+  const int k = (int)p.w;
+  const int64_t ext = (int64_t)(k - 1) * p.dilation;
+  if (p.skip_lo < p.skip_hi) {
+    const int64_t n_lo = p.skip_lo, n_work = n_lo + (p.L - p.skip_hi);
+    for (int64_t b = blockIdx.y; b < p.batch; b += gridDim.y) {
+      const float* __restrict__ xr = static_cast<const float*>(p.x) + b * p.N;
+      float* __restrict__ yr = static_cast<float*>(p.y) + b * p.L;
+      for (int64_t q = (int64_t)blockIdx.x * kGenThreads + threadIdx.x; q < n_work;
+           q += (int64_t)gridDim.x * kGenThreads) {
+        const int64_t i = q < n_lo ? q : p.skip_hi + (q - n_lo);
+        yr[i] = conv_checked(xr, i * p.stride - p.pad_left, p);
+      }
+    }
+    return;
+  }
+  for (int64_t b = blockIdx.y; b < p.batch; b += gridDim.y) {
+    const float* __restrict__ xr = static_cast<const float*>(p.x) + b * p.N;
+    float* __restrict__ yr = static_cast<float*>(p.y) + b * p.L;
+    for (int64_t i0 = (int64_t)blockIdx.x * kGenChunk; i0 < p.L; i0 += (int64_t)gridDim.x * kGenChunk) {
+      const int64_t ia = i0 + threadIdx.x, ib = ia + (kGenOuts - 1) * kGenThreads;
+      const int64_t ta = ia * p.stride - p.pad_left, tb = ib * p.stride - p.pad_left;
+      if (ta >= 0 && tb + ext < p.N && ib < p.L) {
+        float s0[kGenOuts], s1[kGenOuts];
+#pragma unroll
+        for (int q = 0; q < kGenOuts; ++q) s0[q] = s1[q] = 0.0f;
+        for (int j = 0; j < k; j += 2) {
+          const float f = p.taps[j];
+#pragma unroll
+          for (int q = 0; q < kGenOuts; ++q)
+            s0[q] = __fmaf_rn(f, __ldg(xr + ta + (int64_t)q * kGenThreads * p.stride + (int64_t)j * p.dilation), s0[q]);
+        }
+        for (int j = 1; j < k; j += 2) {
+          const float f = p.taps[j];
+#pragma unroll
+          for (int q = 0; q < kGenOuts; ++q)
+            s1[q] = __fmaf_rn(f, __ldg(xr + ta + (int64_t)q * kGenThreads * p.stride + (int64_t)j * p.dilation), s1[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < kGenOuts; ++q) yr[ia + q * kGenThreads] = __fadd_rn(s0[q], s1[q]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < kGenOuts; ++q) {
+          const int64_t i = ia + q * kGenThreads;
+          if (i < p.L) yr[i] = conv_checked(xr, i * p.stride - p.pad_left, p);
+        }
       }
     }
   }
@@ -116,21 +244,37 @@ static dim3 grid_1d(const GenericParams& p, int sms) {
   return dim3((unsigned)(gx < 1 ? 1 : gx), (unsigned)gy, 1);
 }
 
+static bool is_ex(const GenericParams& p) {
+  return p.dilation != 1 || p.pad_left != 0 || p.skip_lo < p.skip_hi ||
+         (p.L - 1) * p.stride + p.w > p.N;  // right padding
+}
+
 cudaError_t launch_pool_generic(const GenericParams& p, int op, int dtype, cudaStream_t stream,
                                 int grid) {
   const dim3 g = grid_1d(p, grid / 8 > 0 ? grid / 8 : 148);
-  if (op == kOpSum && dtype == 1) pool_generic_kernel<OpSumI32><<<g, kGenThreads, 0, stream>>>(p);
-  else if (op == kOpSum && dtype == 0) pool_generic_kernel<OpSumF32><<<g, kGenThreads, 0, stream>>>(p);
-  else if (op == kOpMax && dtype == 1) pool_generic_kernel<OpMaxI32><<<g, kGenThreads, 0, stream>>>(p);
-  else if (op == kOpMax && dtype == 0) pool_generic_kernel<OpMaxF32><<<g, kGenThreads, 0, stream>>>(p);
-  else return cudaErrorInvalidValue;
+  if (is_ex(p)) {
+    const dim3 ge = p.skip_lo < p.skip_hi ? dim3(g.x * kGenOuts, g.y, 1) : g;
+    if (op == kOpSum && dtype == 1) pool_generic_ex_kernel<OpSumI32><<<ge, kGenThreads, 0, stream>>>(p);
+    else if (op == kOpSum && dtype == 0) pool_generic_ex_kernel<OpSumF32><<<ge, kGenThreads, 0, stream>>>(p);
+    else if (op == kOpMax && dtype == 1) pool_generic_ex_kernel<OpMaxI32><<<ge, kGenThreads, 0, stream>>>(p);
+    else if (op == kOpMax && dtype == 0) pool_generic_ex_kernel<OpMaxF32><<<ge, kGenThreads, 0, stream>>>(p);
+    else return cudaErrorInvalidValue;
+  } else {
+    if (op == kOpSum && dtype == 1) pool_generic_kernel<OpSumI32><<<g, kGenThreads, 0, stream>>>(p);
+    else if (op == kOpSum && dtype == 0) pool_generic_kernel<OpSumF32><<<g, kGenThreads, 0, stream>>>(p);
+    else if (op == kOpMax && dtype == 1) pool_generic_kernel<OpMaxI32><<<g, kGenThreads, 0, stream>>>(p);
+    else if (op == kOpMax && dtype == 0) pool_generic_kernel<OpMaxF32><<<g, kGenThreads, 0, stream>>>(p);
+    else return cudaErrorInvalidValue;
+  }
   note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_conv_generic(const GenericParams& p, cudaStream_t stream, int grid) {
   const dim3 g = grid_1d(p, grid / 8 > 0 ? grid / 8 : 148);
-  conv_generic_kernel<<<g, kGenThreads, 0, stream>>>(p);
+  if (is_ex(p))
+    conv_generic_ex_kernel<<<p.skip_lo < p.skip_hi ? dim3(g.x * kGenOuts, g.y, 1) : g, kGenThreads, 0, stream>>>(p);
+  else conv_generic_kernel<<<g, kGenThreads, 0, stream>>>(p);
   note_launch();
   return cudaGetLastError();
 }

@@ -427,7 +427,7 @@ __device__ __forceinline__ int64_t floor_div32(int64_t a) {
 template <int kTileRows>
 __device__ __forceinline__ TileGeom tile_geom(const Slide1DParams& p, const TileCursor& tc) {
   TileGeom g;
-  g.e_y = p.shift_y + tc.b * p.L;
+  g.e_y = p.shift_y + tc.b * p.y_pitch + p.y_off;
   g.yrow0 = (g.e_y >> 5) + (int64_t)kTileRows * tc.j;
   g.empty = 32 * g.yrow0 >= g.e_y + p.L;
   const int64_t ix0 = p.shift_x + tc.b * p.N + (32 * g.yrow0 - g.e_y);

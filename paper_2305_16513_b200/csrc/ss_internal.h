@@ -9,6 +9,7 @@ namespace ss {
 
 constexpr int kOpSum = 0;
 constexpr int kOpMax = 1;
+constexpr int kOpConv = 2;
 constexpr int kSmemBudget = 227 * 1024;  // max dynamic smem per CTA on sm_100a
 constexpr int kConvTmaMaxK = 64;          // largest k served by the TMA conv kernel
 constexpr int kPoolTmaMaxW = 1024;        // largest w served by the TMA pool kernel
@@ -31,6 +32,8 @@ struct alignas(64) Slide1DParams {
   int64_t x_total_elems;  // shift_x + batch * N
   int64_t tiles_per_row, ntiles;
   int64_t y_rows;         // full 128-B rows of the y view
+  int64_t y_pitch;        // y elements between consecutive batch rows (= L unless padded)
+  int64_t y_off;          // offset of output 0 inside its y row (left zero padding)
   int64_t w;              // window (pool)
   uint32_t stage_bytes;
   int stages;
@@ -44,7 +47,9 @@ struct GenericParams {
   const void* x;
   void* y;
   int64_t N, L, batch, w, stride;
-  float taps[1024];  // SS_K_MAX
+  int64_t dilation, pad_left;  // window spec (NEXT #1): x index of tap j of output i = i*s + j*d - pl
+  int64_t skip_lo, skip_hi;    // if skip_lo < skip_hi: outputs in [skip_lo, skip_hi) are not computed
+  float taps[1024];            // SS_K_MAX
 };
 
 struct Pool2DParams {

@@ -47,7 +47,7 @@ def test_library_is_sm100a(ss):
 
 
 def test_abi_version_and_out_len(ss):
-    assert ss.ss_abi_version() == 1
+    assert ss.ss_abi_version() == 2
     assert ss.ss_out_len(10, 3, 1) == 8
     assert ss.ss_out_len(10, 3, 4) == 2
     assert ss.ss_out_len(2 ** 32, 31, 1) == 2 ** 32 - 30
@@ -110,3 +110,17 @@ def test_product_package_never_imports_oracle():
             if fn.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, fn)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", src).lower().replace("oracle_", "x"), fn
+
+
+def test_window_spec_validation(ss):
+    assert ss.ss_out_len_ex(10, 3, 1, 1, 0, 0) == 8
+    assert ss.ss_out_len_ex(10, 3, 1, 2, 0, 0) == 6
+    assert ss.ss_out_len_ex(3, 2, 1, 1, 1, 1) == 4
+    assert ss.ss_out_len_ex(3, 4, 1, 2, 1, 1) == -1
+    assert ss.ss_out_len_ex(3, 4, 1, 1, 0, 0) == -1
+    assert ss.ss_out_len_ex(10, 3, 1, 0, 0, 0) == -1
+    assert ss.ss_pool_sum_ex(FAKE_X, FAKE_Y, 10, 1, 3, 1, 0, 0, 0, ss.SS_F32) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_pool_max_ex(FAKE_X, FAKE_Y, 10, 1, 3, 1, 1, -2, 0, ss.SS_F32) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_pool_max_ex(FAKE_X, FAKE_Y, 3, 1, 3, 1, 2, 0, 0, ss.SS_F32) == ss.SS_ERR_WINDOW_EXCEEDS_INPUT
+    assert ss.ss_conv1d_ex(FAKE_X, FAKE_Y, 10, 1, None, 3, 1, 1, 0, 0, ss.SS_F32) == ss.SS_ERR_NULL
+    assert ss.ss_conv1d_ex(FAKE_X, FAKE_Y, 10, 1, [1.0] * 3, 3, 1, 1, 0, 0, ss.SS_I32) == ss.SS_ERR_UNSUPPORTED

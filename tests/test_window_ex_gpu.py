@@ -1,0 +1,97 @@
+"""GPU parity for the window-spec entry points (ss_*_ex: dilation + zero
+padding) against the oracle's *_ex routines.  Covers the
+stride-1 padded path (TMA tile kernel on the interior + direct kernel on the
+edges), dilation / stride combinations (direct kernel), windows made only of
+padding, misaligned pointers and canaries around y."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ss():
+    from paper_2305_16513_b200 import build
+    build.build_libss()
+    import paper_2305_16513_b200 as ss
+    return ss
+
+
+SPECS = [  # (N, B, w, s, d, pl, pr)
+    (20011, 3, 3, 1, 1, 1, 1), (20011, 2, 16, 1, 1, 5, 0), (30011, 2, 64, 1, 1, 0, 7),
+    (30011, 1, 256, 1, 1, 100, 100), (9000, 2, 7, 1, 1, 6, 6), (9000, 2, 3, 2, 1, 1, 1),
+    (9000, 2, 5, 1, 2, 0, 0), (9000, 3, 4, 2, 3, 2, 5), (5000, 1, 2, 1, 8, 3, 3),
+    (100, 2, 8, 3, 4, 9, 9), (3, 1, 2, 1, 1, 4, 4), (1, 1, 1, 1, 1, 0, 2),
+]
+
+
+def run(ss, fn, x_np, extra, L, xoff=0, yoff=0, dt=torch.float32):
+    B, N = x_np.shape
+    xbuf = torch.empty(x_np.size + xoff + 3, dtype=torch.from_numpy(x_np[:0]).dtype, device="cuda")
+    x = xbuf[xoff:xoff + x_np.size]
+    x.copy_(torch.from_numpy(x_np.reshape(-1)).cuda())
+    ybuf = torch.full((B * L + yoff + 5,), -77, dtype=dt, device="cuda")
+    y = ybuf[yoff:yoff + B * L]
+    ss.check(fn(x.data_ptr(), y.data_ptr(), N, B, *extra))
+    torch.cuda.synchronize()
+    h = ybuf.cpu().numpy()
+    assert np.all(h[:yoff] == -77) and np.all(h[yoff + B * L:] == -77), "canary overwritten"
+    return y.cpu().numpy().reshape(B, L)
+
+
+@pytest.mark.parametrize("N,B,w,s,d,pl,pr", SPECS)
+@pytest.mark.parametrize("off", [(0, 0), (1, 2)])
+def test_pool_ex(ss, N, B, w, s, d, pl, pr, off):
+    L = ss.ss_out_len_ex(N, w, s, d, pl, pr)
+    if L < 0:
+        pytest.skip("window exceeds padded input")
+    assert L == oracle.out_len_ex(N, w, s, d, pl, pr)
+    xi = synth.randint(2, B * N, -1000, 1000).reshape(B, N)
+    ys = run(ss, ss.ss_pool_sum_ex, xi, (w, s, d, pl, pr, ss.SS_I32), L, *off, dt=torch.int32)
+    np.testing.assert_array_equal(ys, (oracle.pool_sum_ex(xi, w, s, d, pl, pr) & 0xFFFFFFFF).astype(np.uint32).view(np.int32))
+    ym = run(ss, ss.ss_pool_max_ex, xi, (w, s, d, pl, pr, ss.SS_I32), L, *off, dt=torch.int32)
+    np.testing.assert_array_equal(ym, oracle.pool_max_ex(xi, w, s, d, pl, pr))
+    xf = synth.uniform_pm1(0, B * N).reshape(B, N)
+    ymf = run(ss, ss.ss_pool_max_ex, xf, (w, s, d, pl, pr, ss.SS_F32), L, *off)
+    np.testing.assert_array_equal(ymf, oracle.pool_max_ex(xf, w, s, d, pl, pr))
+    ysf = run(ss, ss.ss_pool_sum_ex, xf, (w, s, d, pl, pr, ss.SS_F32), L, *off)
+    ref, mag = oracle.pool_sum_ex(xf, w, s, d, pl, pr)
+    assert np.all(np.abs(ysf - ref) <= 1e-5 * mag + 1e-6)
+
+
+@pytest.mark.parametrize("N,B,w,s,d,pl,pr", SPECS + [(40011, 2, 31, 1, 1, 15, 15), (40011, 2, 63, 1, 1, 31, 31),
+                                                     (40011, 1, 63, 1, 1, 62, 0), (20000, 2, 15, 1, 3, 21, 21)])
+def test_conv_ex(ss, N, B, w, s, d, pl, pr):
+    L = ss.ss_out_len_ex(N, w, s, d, pl, pr)
+    if L < 0:
+        pytest.skip("window exceeds padded input")
+    x = synth.normal(3, B * N).reshape(B, N)
+    f = synth.normal(4, w, sigma=synth.cfg_sigma_filter(w))
+    y = run(ss, lambda xp, yp, N_, B_, *a: ss.ss_conv1d_ex(xp, yp, N_, B_, f.tolist(), w, *a),
+            x, (s, d, pl, pr, ss.SS_F32), L, 1, 1)
+    ref, mag = oracle.conv1d_ex(x, f, s, d, pl, pr)
+    err = np.abs(y.astype(np.float64) - ref)
+    assert np.all(err <= 1e-5 * mag + 1e-6), float((err / (1e-5 * mag + 1e-6)).max())
+
+
+def test_padded_equals_valid_interior_bitwise(ss):
+    # the padded call's interior equals the valid call bitwise (same kernels / association)
+    x = torch.from_numpy(synth.normal(3, 2 * 50000).reshape(2, 50000)).cuda()
+    f = synth.normal(4, 31, sigma=synth.cfg_sigma_filter(31))
+    yv = ss.conv1d(x, f)
+    yp = ss.conv1d(x, f, padding=(15, 15))
+    assert torch.equal(yp[:, 15:15 + yv.shape[1]], yv)
+    ym = ss.pool_max(x, 64, padding=3)
+    assert torch.equal(ym[:, 3:3 + x.shape[1] - 63], ss.pool_max(x, 64))
+
+
+def test_ex_validation(ss):
+    FX, FY = 0x10000000, 0x20000000
+    assert ss.ss_pool_sum_ex(FX, FY, 10, 1, 3, 1, 0, 0, 0, ss.SS_F32) == ss.SS_ERR_BAD_SIZE  # dilation 0
+    assert ss.ss_pool_sum_ex(FX, FY, 10, 1, 3, 1, 1, -1, 0, ss.SS_F32) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_pool_max_ex(FX, FY, 3, 1, 3, 1, 2, 0, 0, ss.SS_F32) == ss.SS_ERR_WINDOW_EXCEEDS_INPUT
+    # (no valid call with fake pointers: it would launch)
