@@ -72,6 +72,8 @@ def lib() -> ctypes.CDLL:
             L.oracle_pool_sum_ex_f32.restype = ctypes.c_int
             L.oracle_conv1d_ex_f32.argtypes = [vp, i64, i64, vp, i64, i64, i64, i64, i64, vp, vp]
             L.oracle_conv1d_ex_f32.restype = ctypes.c_int
+            L.oracle_affine_window.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp, vp]
+            L.oracle_affine_window.restype = ctypes.c_int
             L.oracle_gamma_combine.argtypes = [dp, dp, dp, dp, vp, vp]
             L.oracle_gamma_combine.restype = None
             L.oracle_gamma_sequence.argtypes = [vp, vp, i64, vp, vp]
@@ -204,6 +206,23 @@ def conv1d_ex(x: np.ndarray, f: np.ndarray, s: int = 1, d: int = 1, pl: int = 0,
     m = np.empty((B, L), np.float64)
     _check(lib().oracle_conv1d_ex_f32(_p(x), N, B, _p(f), k, s, d, pl, pr, _p(y), _p(m)))
     return (y, m) if x.ndim == 2 else (y[0], m[0])
+
+
+def affine_window(u: np.ndarray, v: np.ndarray, w: int, s: int = 1):
+    """Sliding window of gamma pairs (Eq. 3 with the Eq. 8 operator).
+    Returns (U, V, magV) in double, shaped like the outputs."""
+    u, N, B = _rows(np.ascontiguousarray(u, np.float32))
+    v = np.ascontiguousarray(v, np.float32).reshape(u.shape)
+    L = out_len(N, w, s)
+    if L < 0:
+        raise ValueError("window exceeds input")
+    U = np.empty((B, L))
+    V = np.empty((B, L))
+    M = np.empty((B, L))
+    _check(lib().oracle_affine_window(_p(u), _p(v), N, B, w, s, _p(U), _p(V), _p(M)))
+    if u.ndim == 1:
+        return U[0], V[0], M[0]
+    return U, V, M
 
 
 def gamma_combine(gi, gj):

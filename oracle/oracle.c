@@ -264,6 +264,34 @@ int oracle_conv1d_ex_f32(const float* x, int64_t N, int64_t batch, const float* 
   return 0;
 }
 
+/* Sliding window of gamma pairs: Eq. 3's window with Eq. 8's operator, each
+ * window folded left to right (delta = delta (+) gamma, Eq. 9). */
+int oracle_affine_window(const float* u, const float* v, int64_t N, int64_t batch, int64_t w,
+                         int64_t s, double* U, double* V, double* magV) {
+  if (u == NULL || v == NULL || V == NULL || batch < 1 || oracle_out_len(N, w, s) < 0) return -1;
+  int64_t L = oracle_out_len(N, w, s);
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t i = 0; i < L; ++i) {
+      int64_t t0 = b * N + i * s;
+      double du = (double)u[t0], dv = (double)v[t0];
+      double au = fabs((double)u[t0]), av = fabs((double)v[t0]);
+      for (int64_t j = 1; j < w; ++j) {
+        double nu, nv;
+        oracle_gamma_combine(du, dv, (double)u[t0 + j], (double)v[t0 + j], &nu, &nv);
+        du = nu;
+        dv = nv;
+        double anu, anv;
+        oracle_gamma_combine(au, av, fabs((double)u[t0 + j]), fabs((double)v[t0 + j]), &anu, &anv);
+        au = anu;
+        av = anv;
+      }
+      if (U) U[b * L + i] = du;
+      V[b * L + i] = dv;
+      if (magV) magV[b * L + i] = av;
+    }
+  return 0;
+}
+
 /* Eq. 8. */
 void oracle_gamma_combine(double ui, double vi, double uj, double vj,
                           double* u_out, double* v_out) {

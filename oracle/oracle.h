@@ -85,6 +85,15 @@ int oracle_pool_max_ex_f32(const float* x, int64_t N, int64_t batch, int64_t w, 
 int oracle_conv1d_ex_f32(const float* x, int64_t N, int64_t batch, const float* f, int64_t k,
                          int64_t s, int64_t d, int64_t pl, int64_t pr, double* y, double* absmag);
 
+/* Sliding window of gamma pairs (Eq. 3 with the pair operator of Eq. 8; the
+ * windowed linear recurrence s_t = u_t s_{t-1} + v_t):
+ *   (U_i, V_i) = gamma_{i*s} (+) gamma_{i*s+1} (+) ... (+) gamma_{i*s+w-1},
+ * folded left to right in double (Eq. 9's recurrence restricted to a window):
+ *   U_i = prod_j u_j,  V_i = sum_j v_j prod_{l>j, l in window} u_l.
+ * magV_i = sum_j |v_j| prod_{l>j} |u_l| (error-bound scale).  U and magV may be NULL. */
+int oracle_affine_window(const float* u, const float* v, int64_t N, int64_t batch, int64_t w,
+                         int64_t s, double* U, double* V, double* magV);
+
 /* Eq. 8: gamma_i (+) gamma_j = (u_i*u_j, u_j*v_i + v_j). */
 void oracle_gamma_combine(double ui, double vi, double uj, double vj,
                           double* u_out, double* v_out);

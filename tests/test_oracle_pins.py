@@ -390,3 +390,61 @@ def test_window_ex_brute_force_and_all_padding():
     # a window made only of padding: sum 0, max = identity
     assert oracle.pool_max_ex(np.array([5.0], np.float32), 1, 1, 1, 1, 0)[0] == -np.inf
     assert oracle.out_len_ex(3, 4, 1, 1, 0, 0) == -1 and oracle.out_len_ex(3, 4, 1, 1, 1, 0) == 1
+
+
+# ------------------------------------------- NEXT #3: sliding window of gamma pairs (Eq. 8)
+def test_affine_window_reduces_to_sliding_sum_and_product():
+    v = synth.normal(13, 2000)
+    u1 = np.ones(2000, np.float32)
+    for w in (1, 2, 5, 33):
+        U, V, M = oracle.affine_window(u1, v, w)
+        ref, mag = oracle.pool_sum(v, w)  # u = 1: plain Eq. 3 sliding sum of v
+        np.testing.assert_allclose(V, ref, rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(M, mag, rtol=1e-12, atol=1e-12)
+        np.testing.assert_array_equal(U, np.ones_like(U))
+    u = (0.5 + 0.5 * synth.uniform01(14, 2000)).astype(np.float32)
+    for w in (1, 3, 8):
+        U, V, _ = oracle.affine_window(u, np.zeros(2000, np.float32), w)
+        np.testing.assert_array_equal(V, np.zeros_like(V))
+        logp = np.convolve(np.log(u.astype(np.float64)), np.ones(w), mode="valid")  # sliding log-sum
+        np.testing.assert_allclose(U, np.exp(logp), rtol=1e-12)
+
+
+def test_affine_window_geometric_is_a_convolution():
+    # u = c constant: V_i = sum_j v_{i+j} c^{w-1-j}  (an exponentially weighted window)
+    c = np.float32(0.75)
+    v = synth.normal(15, 3000)
+    for w in (2, 7, 40):
+        _, V, _ = oracle.affine_window(np.full(3000, c, np.float32), v, w)
+        kern = np.array([float(c) ** (w - 1 - j) for j in range(w)])
+        ref = np.convolve(v.astype(np.float64), kern[::-1], mode="valid")
+        np.testing.assert_allclose(V, ref, rtol=1e-12, atol=1e-12)
+
+
+def test_affine_window_exact_rationals_brute_force():
+    from fractions import Fraction
+    rng = np.random.default_rng(3)
+    u = rng.integers(-4, 5, 12).astype(np.float32) / 4
+    v = rng.integers(-8, 9, 12).astype(np.float32) / 8
+    for w, s in ((1, 1), (3, 1), (4, 2), (12, 1), (5, 3)):
+        U, V, _ = oracle.affine_window(u, v, w, s)
+        for i in range(len(V)):
+            acc_u, acc_v = Fraction(1), Fraction(0)
+            for j in range(i * s, i * s + w):   # fold from the identity (1, 0), Eq. 8
+                acc_u, acc_v = acc_u * Fraction(float(u[j])), Fraction(float(u[j])) * acc_v + Fraction(float(v[j]))
+            assert Fraction(U[i]) == acc_u and Fraction(V[i]) == acc_v
+
+
+def test_affine_window_is_order_sensitive_and_gives_the_dot_product():
+    u = np.array([2.0, 0.5, 3.0], np.float32)
+    v = np.array([1.0, 4.0, -2.0], np.float32)
+    _, V, _ = oracle.affine_window(u, v, 3)
+    _, Vr, _ = oracle.affine_window(u[::-1].copy(), v[::-1].copy(), 3)
+    assert V[0] != Vr[0]  # non-commutative
+    # Eq. 9: the window over the whole gamma sequence of (a, b) yields the dot product
+    a = np.array([2.0, 0.0, 4.0, -1.0, 0.5])  # ratios of powers of two: exact in fp32
+    b = np.array([1.0, 5.0, 7.0, 2.0, -3.0])
+    gu, gv = oracle.gamma_sequence(a, b)
+    _, Vd, _ = oracle.affine_window(gu.astype(np.float32), gv.astype(np.float32), len(gu))
+    assert np.all(gu.astype(np.float32) == gu) and np.all(gv.astype(np.float32) == gv)
+    assert Vd[0] == float(np.dot(a, b))
