@@ -58,8 +58,9 @@ class Cell:
     """One kernel launch of the workload."""
 
     def __init__(self, cfg, name, op, *, w=None, f=None, kh=None, kw=None, sh=None, sw=None,
-                 mode=None, inp=None, stride=1, dilation=1, pads=(0, 0)):
+                 mode=None, inp=None, inp2=None, stride=1, dilation=1, pads=(0, 0)):
         self.cfg, self.name, self.op = cfg, name, op
+        self.inp2 = inp2  # second input (affine: v), None otherwise
         self.stride, self.dilation, self.pads = stride, dilation, pads
         self.w, self.f, self.kh, self.kw, self.sh, self.sw, self.mode = w, f, kh, kw, sh, sw, mode
         self.inp = inp  # key of the input tensor it reads
@@ -67,6 +68,9 @@ class Cell:
         self.bytes = 0
         self.flops = 0
         self.times = []
+
+    def inputs(self):
+        return [self.inp] + ([self.inp2] if self.inp2 else [])
 
 
 def cfg_cells(workload: str):
@@ -119,6 +123,13 @@ def cfg_cells(workload: str):
                               f=synth.normal(4, k, sigma=synth.cfg_sigma_filter(k)), inp="xw"))
         cells.append(Cell("winspec", "winspec_max_w3_p1", "max", w=3, pads=(1, 1), inp="xw"))
         cells.append(Cell("winspec", "winspec_sum_w8_d2", "sum", w=8, dilation=2, inp="xw"))
+    if workload == "affine":  # sliding window of gamma pairs; not a BASELINE config
+        inputs["xa_u"] = dict(rows=8, n=1 << 24, dtype="float32", dist="uab", seed=31,
+                              kw=dict(lo=0.5, hi=1.0), shard="batch")
+        inputs["xa_v"] = dict(rows=8, n=1 << 24, dtype="float32", dist="normal", seed=32, kw={},
+                              shard="batch")
+        for w in (8, 64, 1024):
+            cells.append(Cell("affine", f"affine_w{w}", "affine", w=w, inp="xa_u", inp2="xa_v"))
     if not cells:
         raise SystemExit(f"unknown workload {workload}")
     return inputs, cells
@@ -264,6 +275,12 @@ class Runner:
                 c.n_out = sh.n_outputs(c.w)
                 self.y[c.name] = torch.empty(max(c.n_out, 1), dtype=x.dtype, device=self.device)
                 c.bytes = (sh.size + c.n_out) * es
+            elif kind == "batch" and c.op == "affine":  # y = [U; V]
+                rows, n = geo
+                L = (n - c.w) // c.stride + 1
+                self.y[c.name] = torch.empty((2, rows, L), dtype=x.dtype, device=self.device)
+                c.n_out = rows * L
+                c.bytes = 2 * (rows * n + c.n_out) * es
             elif kind == "batch":
                 rows, n = geo
                 L = (n + sum(c.pads) - ((c.w - 1) * c.dilation + 1)) // c.stride + 1
@@ -288,7 +305,11 @@ class Runner:
         else:
             B, N = x.shape
         win = (c.stride, c.dilation, c.pads[0], c.pads[1], code, s)
-        if c.op == "conv":
+        if c.op == "affine":
+            v = self.x[c.inp2]
+            st = ss.ss_affine_window(x.data_ptr(), v.data_ptr(), y[0].data_ptr(), y[1].data_ptr(), N, B, c.w,
+                                     c.stride, s)
+        elif c.op == "conv":
             st = ss.ss_conv1d_ex(x.data_ptr(), y.data_ptr(), N, B, c.f, c.w, *win)
         elif c.op == "sum":
             st = ss.ss_pool_sum_ex(x.data_ptr(), y.data_ptr(), N, B, c.w, *win)
@@ -378,7 +399,7 @@ class Runner:
         self.ev_out_free = {c.name: ev() for c in self.cells}
         for e in list(self.ev_in_free.values()) + list(self.ev_out_free.values()):
             e.record(self.stream)
-        self.last_reader = {c.inp: c.name for c in self.cells}  # last cell reading each input
+        self.last_reader = {k: c.name for c in self.cells for k in c.inputs()}  # last reader of each input
 
     def step_e2e(self):
         """One end-to-end step through the public C ABI: H2D of every input from
@@ -394,13 +415,15 @@ class Runner:
             self.ev_in_ready[k].record(self.s_h2d)
 
         def before(c):
-            self.stream.wait_event(self.ev_in_ready[c.inp])
+            for k in c.inputs():
+                self.stream.wait_event(self.ev_in_ready[k])
             self.stream.wait_event(self.ev_out_free[c.name])
 
         def after(c):
             self.ev_out_ready[c.name].record(self.stream)
-            if self.last_reader[c.inp] == c.name:
-                self.ev_in_free[c.inp].record(self.stream)
+            for k in c.inputs():
+                if self.last_reader[k] == c.name:
+                    self.ev_in_free[k].record(self.stream)
             self.s_d2h.wait_event(self.ev_out_ready[c.name])
             with torch.cuda.stream(self.s_d2h):
                 self.hy[c.name].copy_(self.y[c.name], non_blocking=True)
@@ -608,6 +631,11 @@ def oracle_sample_plan(workload: str, frac: float):
                 rows = 1
             x = synth.normal(3, rows * n).reshape(rows, n)
             plan.append((c, lambda x=x, c=c: (oracle.conv1d(x, c.f), x.shape[0] * (x.shape[1] - c.w + 1))[1]))
+        elif c.cfg == "affine":
+            n = max(c.w, int(8 * (1 << 24) * frac))
+            u = synth.uab(31, n, 0.5, 1.0)
+            v = synth.normal(32, n)
+            plan.append((c, lambda u=u, v=v, c=c: (oracle.affine_window(u, v, c.w), u.size - c.w + 1)[1]))
         else:  # cfg4
             planes = max(1, int(round(32 * 64 * frac)))
             x = synth.uniform01(5, planes * 112 * 112).reshape(planes, 112, 112)
@@ -675,7 +703,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="suite", choices=["suite", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "stride", "winspec"])
+    ap.add_argument("--workload", default="suite", choices=["suite", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "stride", "winspec", "affine"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)

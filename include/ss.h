@@ -58,7 +58,7 @@
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 2
+#define SS_ABI_VERSION 3
 
 typedef enum { SS_F32 = 0, SS_I32 = 1 } ss_dtype_t;
 typedef enum { SS_POOL_MAX = 0, SS_POOL_AVG = 1 } ss_pool_mode_t;
@@ -143,6 +143,30 @@ ss_status_t ss_conv1d_ex(const void* x, void* y, int64_t N, int64_t batch,
                          const float* filter_host, int64_t k, int64_t stride,
                          int64_t dilation, int64_t pad_left, int64_t pad_right,
                          ss_dtype_t dtype, void* stream);
+
+/* ---- sliding window of gamma pairs --------------------
+ * The paper's pair operator (Eq. 8)
+ *     (u_i, v_i) (+) (u_j, v_j) = (u_i u_j, u_j v_i + v_j)
+ * is associative and NOT commutative; slid over a sequence of pairs with
+ * window w (Eq. 3) it gives, for output i of a row,
+ *     (U_i, V_i) = gamma_{i*s} (+) gamma_{i*s+1} (+) ... (+) gamma_{i*s+w-1},
+ *     U_i = prod_j u_j,   V_i = sum_j v_j prod_{l > j in the window} u_l,
+ * the recurrence s_t = u_t s_{t-1} + v_t run over each window from s = 0 (V)
+ * and its gain (U): exponentially weighted / decaying windowed sums,
+ * windowed first-order IIR filters, and Eq. 9's dot product when u, v come
+ * from Eq. 7.  u, v are DEVICE [batch][N] fp32 (planar: one array per pair
+ * component); U, V are DEVICE [batch][L], L = ss_out_len(N, w, stride).
+ * U may be NULL (V only).  No argument may overlap another output.
+ * Numerics: fp32 with one rounding per product and one per FMA; the
+ * evaluation order is a fixed tree of (+) (left-to-right order preserved), so
+ *     |V - V_exact| <= 2 w 2^-24 sum_j |v_j| prod_{l>j} |u_l| + 1e-6
+ *     |U - U_exact| <= 2 w 2^-24 |U_exact| + 1e-30   (reading R15).
+ * Stride 1 costs O(1) (+) per output for any w (two-level P-block pivot);
+ * stride > 1 folds each window directly (O(w) per output).
+ * Statuses as above; w > SS_AFFINE_W_MAX -> SS_ERR_UNSUPPORTED. */
+#define SS_AFFINE_W_MAX 65536
+ss_status_t ss_affine_window(const float* u, const float* v, float* U, float* V, int64_t N,
+                             int64_t batch, int64_t w, int64_t stride, void* stream);
 
 /* Static description of a status code. */
 const char* ss_status_string(ss_status_t s);

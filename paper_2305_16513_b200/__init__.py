@@ -31,10 +31,12 @@ SS_ERR_UNSUPPORTED = 4
 SS_ERR_CUDA = 5
 SS_ERR_OVERLAP = 6
 SS_K_MAX = 1024
+SS_AFFINE_W_MAX = 65536
 
 EXPORTED = ("ss_abi_version", "ss_out_len", "ss_pool_sum", "ss_pool_max", "ss_conv1d",
             "ss_pool2d", "ss_status_string", "ss_last_error", "ss_launch_count",
-            "ss_out_len_ex", "ss_pool_sum_ex", "ss_pool_max_ex", "ss_conv1d_ex")
+            "ss_out_len_ex", "ss_pool_sum_ex", "ss_pool_max_ex", "ss_conv1d_ex",
+            "ss_affine_window")
 
 
 class SSError(RuntimeError):
@@ -69,6 +71,8 @@ def _load() -> ctypes.CDLL:
     L.ss_conv1d_ex.argtypes = [vp, vp, i64, i64, ctypes.POINTER(ctypes.c_float), i64, i64, i64, i64, i64,
                                i32, vp]
     L.ss_conv1d_ex.restype = i32
+    L.ss_affine_window.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64, vp]
+    L.ss_affine_window.restype = i32
     L.ss_status_string.argtypes = [i32]
     L.ss_status_string.restype = ctypes.c_char_p
     L.ss_last_error.argtypes = []
@@ -144,6 +148,10 @@ def ss_conv1d_ex(x_ptr, y_ptr, N, batch, filter_host, k, stride, dilation, pad_l
                  dtype=SS_F32, stream=0) -> int:
     fp = None if filter_host is None else (ctypes.c_float * len(filter_host))(*[float(v) for v in filter_host])
     return _lib.ss_conv1d_ex(x_ptr, y_ptr, N, batch, fp, k, stride, dilation, pad_left, pad_right, dtype, stream)
+
+
+def ss_affine_window(u_ptr, v_ptr, U_ptr, V_ptr, N, batch, w, stride=1, stream=0) -> int:
+    return _lib.ss_affine_window(u_ptr, v_ptr, U_ptr, V_ptr, N, batch, w, stride, stream)
 
 
 def check(status: int) -> None:
@@ -263,3 +271,27 @@ def pool2d(x, kernel, stride, mode: str = "max", out=None, stream=None):
     y = torch.empty(shape, dtype=x.dtype, device=x.device) if out is None else out
     check(ss_pool2d(x.data_ptr(), y.data_ptr(), planes, H, W, kh, kw, sh, sw, m, _dtype_code(x), _stream(stream)))
     return y
+
+
+def affine_window(u, v, w: int, stride: int = 1, want_U: bool = True, out=None, stream=None):
+    """Sliding window of gamma pairs (Eq. 8 operator, ss.h ss_affine_window) over the
+    last dim of CUDA fp32 [N] / [B, N] tensors u, v.  Returns (U, V); U is None
+    when want_U is False.  `out` = (U, V) preallocated (U may be None)."""
+    N, B = _rows(u)
+    if v.shape != u.shape or not v.is_cuda or not v.is_contiguous() or v.dtype != u.dtype:
+        raise ValueError("v must be a contiguous CUDA tensor shaped like u")
+    if _dtype_code(u) != SS_F32:
+        raise TypeError("affine_window takes fp32 tensors")
+    L = ss_out_len(N, w, stride)
+    if L < 0:
+        check(ss_affine_window(u.data_ptr(), v.data_ptr(), 0, 0, N, B, w, stride) or SS_ERR_BAD_SIZE)
+    if out is None:
+        V = _out(u, L, None)
+        U = _out(u, L, None) if want_U else None
+    else:
+        U, V = out
+        V = _out(u, L, V)
+        U = _out(u, L, U) if U is not None else None
+    check(ss_affine_window(u.data_ptr(), v.data_ptr(), 0 if U is None else U.data_ptr(), V.data_ptr(),
+                           N, B, w, stride, _stream(stream)))
+    return U, V

@@ -336,6 +336,33 @@ ss_status_t ss_pool2d(const void* x, void* y, int64_t planes, int64_t H, int64_t
   return cuda_fail(e, "pool2d launch");
 }
 
+ss_status_t ss_affine_window(const float* u, const float* v, float* U, float* V, int64_t N,
+                             int64_t batch, int64_t w, int64_t stride, void* stream) {
+  if (!u || !v || !V) return fail(SS_ERR_NULL, "u, v and V must be non-NULL device pointers");
+  if (N < 1 || batch < 1 || w < 1 || stride < 1)
+    return fail(SS_ERR_BAD_SIZE, "N, batch, w, stride must all be >= 1");
+  if (N > INT64_MAX / 8 / batch) return fail(SS_ERR_BAD_SIZE, "batch*N*4 overflows int64");
+  if (w > N)
+    return fail(SS_ERR_WINDOW_EXCEEDS_INPUT, "window exceeds input: w=%lld > N=%lld", (long long)w,
+                (long long)N);
+  if (w > SS_AFFINE_W_MAX) return fail(SS_ERR_UNSUPPORTED, "w > SS_AFFINE_W_MAX");
+  if ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(v) |
+       reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(V)) & 3)
+    return fail(SS_ERR_BAD_SIZE, "u, v, U, V must be 4-byte aligned");
+  const int64_t L = (N - w) / stride + 1;
+  const int64_t in_b = batch * N * 4, out_b = batch * L * 4;
+  if (overlaps(u, in_b, V, out_b) || overlaps(v, in_b, V, out_b) ||
+      (U && (overlaps(u, in_b, U, out_b) || overlaps(v, in_b, U, out_b) || overlaps(U, out_b, V, out_b))))
+    return fail(SS_ERR_OVERLAP, "outputs overlap an input or each other");
+  AffineParams p;
+  memset(&p, 0, sizeof p);
+  p.u = u; p.v = v; p.U = U; p.V = V;
+  p.N = N; p.L = L; p.batch = batch; p.w = w; p.stride = stride;
+  const cudaError_t e = launch_affine(p, static_cast<cudaStream_t>(stream), current_sms());
+  if (e == cudaSuccess) return SS_OK;
+  return cuda_fail(e, "affine_window launch");
+}
+
 const char* ss_status_string(ss_status_t s) {
   switch (s) {
     case SS_OK: return "SS_OK";

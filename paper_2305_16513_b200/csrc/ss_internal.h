@@ -81,6 +81,20 @@ cudaError_t launch_pool_generic(const GenericParams& p, int op, int dtype, cudaS
                                 int grid);
 cudaError_t launch_conv_generic(const GenericParams& p, cudaStream_t stream, int grid);
 cudaError_t launch_pool2d(Pool2DParams& p, cudaStream_t stream, int grid);
+
+// Sliding window of gamma pairs (affine.cu).  u, v: [batch][N]; U, V:
+// [batch][L]; U may be null.
+struct AffineParams {
+  const float* u;
+  const float* v;
+  float* U;
+  float* V;
+  int64_t N, L, batch, w, stride;
+  int64_t tiles_per_row;  // set by launch_affine
+  int q, nB;              // set by launch_affine
+};
+size_t affine_smem_bytes(int64_t w);
+cudaError_t launch_affine(AffineParams& p, cudaStream_t stream, int num_sms);
 cudaError_t launch_pool2d_direct(const Pool2DParams& p, cudaStream_t stream, int grid);
 
 }  // namespace ss

@@ -60,6 +60,13 @@ def uniform_pm1(seed: int, n: int, start: int = 0) -> np.ndarray:
     return (np.float32(2.0) * u - np.float32(1.0)).astype(np.float32)
 
 
+def uab(seed: int, n: int, lo: float, hi: float, start: int = 0) -> np.ndarray:
+    """Uniform on [lo, hi): fl(lo + fl((hi - lo) * u01)) in fp32 (device twin k_uab)."""
+    u = uniform01(seed, n, start)
+    span = np.float32(np.float32(hi) - np.float32(lo))
+    return (np.float32(lo) + span * u).astype(np.float32)
+
+
 def randint(seed: int, n: int, lo: int, hi: int, start: int = 0) -> np.ndarray:
     z = splitmix64(seed, _idx(start, n))
     span = np.uint64(hi - lo + 1)
@@ -94,6 +101,8 @@ def generate(dist: str, seed: int, n: int, start: int = 0, **kw) -> np.ndarray:
         return uniform_pm1(seed, n, start)
     if dist == "int":
         return randint(seed, n, kw["lo"], kw["hi"], start)
+    if dist == "uab":
+        return uab(seed, n, kw["lo"], kw["hi"], start)
     if dist == "normal":
         return normal(seed, n, kw.get("sigma", 1.0), start)
     raise ValueError(dist)
@@ -129,6 +138,7 @@ def _dev():
         L.synth_uniform_pm1.argtypes = [vp, i64, u64, i64, vp]
         L.synth_randint.argtypes = [vp, i64, u64, i64, i64, i64, vp]
         L.synth_normal.argtypes = [vp, i64, u64, _ct.c_double, i64, vp]
+        L.synth_uab.argtypes = [vp, i64, u64, _ct.c_float, _ct.c_float, i64, vp]
         _syn = L
     return _syn
 
@@ -145,6 +155,9 @@ def fill_device(t, dist: str, seed: int, start: int = 0, stream=None, **kw):
         rc = L.synth_uniform_pm1(t.data_ptr(), n, seed, start, s)
     elif dist == "int":
         rc = L.synth_randint(t.data_ptr(), n, seed, kw["lo"], kw["hi"], start, s)
+    elif dist == "uab":
+        span = float(np.float32(np.float32(kw["hi"]) - np.float32(kw["lo"])))
+        rc = L.synth_uab(t.data_ptr(), n, seed, float(np.float32(kw["lo"])), span, start, s)
     elif dist == "normal":
         rc = L.synth_normal(t.data_ptr(), n, seed, float(kw.get("sigma", 1.0)), start, s)
     else:

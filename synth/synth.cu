@@ -20,6 +20,15 @@ __global__ void k_uniform(float* out, int64_t n, uint64_t seed, int64_t start, i
   }
 }
 
+// uniform on [lo, lo+span): fl(lo + fl(span * u01)), the host twin's order.
+__global__ void k_uab(float* out, int64_t n, uint64_t seed, float lo, float span, int64_t start) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t z = sm64(seed, (uint64_t)(start + i));
+    const float u = __fmul_rn((float)(uint32_t)(z >> 40), 5.9604644775390625e-08f);  // 2^-24
+    out[i] = __fadd_rn(lo, __fmul_rn(span, u));
+  }
+}
+
 __global__ void k_randint(int32_t* out, int64_t n, uint64_t seed, int64_t lo, uint64_t span, int64_t start) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t z = sm64(seed, (uint64_t)(start + i));
@@ -55,6 +64,10 @@ int synth_uniform01(float* out, int64_t n, uint64_t seed, int64_t start, void* s
 }
 int synth_uniform_pm1(float* out, int64_t n, uint64_t seed, int64_t start, void* stream) {
   k_uniform<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(out, n, seed, start, 1);
+  return (int)cudaGetLastError();
+}
+int synth_uab(float* out, int64_t n, uint64_t seed, float lo, float span, int64_t start, void* stream) {
+  k_uab<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(out, n, seed, lo, span, start);
   return (int)cudaGetLastError();
 }
 int synth_randint(int32_t* out, int64_t n, uint64_t seed, int64_t lo, int64_t hi, int64_t start, void* stream) {

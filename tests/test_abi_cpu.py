@@ -47,7 +47,7 @@ def test_library_is_sm100a(ss):
 
 
 def test_abi_version_and_out_len(ss):
-    assert ss.ss_abi_version() == 2
+    assert ss.ss_abi_version() == 3
     assert ss.ss_out_len(10, 3, 1) == 8
     assert ss.ss_out_len(10, 3, 4) == 2
     assert ss.ss_out_len(2 ** 32, 31, 1) == 2 ** 32 - 30
@@ -124,3 +124,19 @@ def test_window_spec_validation(ss):
     assert ss.ss_pool_max_ex(FAKE_X, FAKE_Y, 3, 1, 3, 1, 2, 0, 0, ss.SS_F32) == ss.SS_ERR_WINDOW_EXCEEDS_INPUT
     assert ss.ss_conv1d_ex(FAKE_X, FAKE_Y, 10, 1, None, 3, 1, 1, 0, 0, ss.SS_F32) == ss.SS_ERR_NULL
     assert ss.ss_conv1d_ex(FAKE_X, FAKE_Y, 10, 1, [1.0] * 3, 3, 1, 1, 0, 0, ss.SS_I32) == ss.SS_ERR_UNSUPPORTED
+
+
+def test_affine_window_validation(ss):
+    f = ss.ss_affine_window
+    X, Y, U, V = FAKE_X, FAKE_X + 0x1000000, FAKE_Y, FAKE_Y + 0x1000000
+    assert f(0, Y, U, V, 10, 1, 3) == ss.SS_ERR_NULL
+    assert f(X, Y, U, 0, 10, 1, 3) == ss.SS_ERR_NULL
+    assert f(X, Y, U, V, 10, 1, 0) == ss.SS_ERR_BAD_SIZE
+    assert f(X, Y, U, V, 10, 1, 3, 0) == ss.SS_ERR_BAD_SIZE
+    assert f(X, Y, U, V, 10, 0, 3) == ss.SS_ERR_BAD_SIZE
+    assert f(X, Y, U, V, 10, 1, 11) == ss.SS_ERR_WINDOW_EXCEEDS_INPUT
+    assert f(X, Y, U, V, 10 ** 6, 1, ss.SS_AFFINE_W_MAX + 1) == ss.SS_ERR_UNSUPPORTED
+    assert f(X, Y, U, X + 4, 10, 1, 3) == ss.SS_ERR_OVERLAP
+    assert f(X, Y, V + 8, V, 10, 1, 3) == ss.SS_ERR_OVERLAP
+    assert f(X, Y, U, V + 2, 10, 1, 3) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_launch_count() == 0

@@ -246,7 +246,8 @@ def test_pool2d_misaligned_fallback(ss):
 def test_device_generator_matches_host():
     n = 1 << 20
     for dist, seed, kw in (("upm1", 0, {}), ("u01", 5, {}), ("int", 2, {"lo": -1000, "hi": 1000}),
-                           ("normal", 3, {}), ("normal", 4, {"sigma": synth.cfg_sigma_filter(31)})):
+                           ("normal", 3, {}), ("normal", 4, {"sigma": synth.cfg_sigma_filter(31)}),
+                           ("uab", 21, {"lo": 0.5, "hi": 1.0})):
         dt = torch.int32 if dist == "int" else torch.float32
         t = torch.empty(n, dtype=dt, device="cuda")
         synth.fill_device(t, dist, seed, start=12345, **kw)
