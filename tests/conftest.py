@@ -11,6 +11,9 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running test")
+    # a fresh checkout has no built libraries; build() is a no-op when they are current
+    import __graft_entry__
+    __graft_entry__.build()
 
 
 def _has_cuda():

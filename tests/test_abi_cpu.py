@@ -13,8 +13,6 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.fixture(scope="module")
 def ss():
-    from paper_2305_16513_b200 import build
-    build.build_libss()
     import paper_2305_16513_b200 as ss
     return ss
 

@@ -19,8 +19,6 @@ EPS = 2.0 ** -24
 
 @pytest.fixture(scope="module")
 def ss():
-    from paper_2305_16513_b200 import build
-    build.build_libss()
     import paper_2305_16513_b200 as ss
     return ss
 

@@ -20,8 +20,6 @@ TOL_REL, TOL_ABS = 1e-5, 1e-6
 
 @pytest.fixture(scope="module")
 def ss():
-    from paper_2305_16513_b200 import build
-    build.build_libss()
     import paper_2305_16513_b200 as ss
     return ss
 
