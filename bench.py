@@ -51,6 +51,22 @@ import numpy as np  # noqa: E402
 METRIC = "output GElem/s and achieved HBM GB/s (% of ~8 TB/s) for sliding pool/conv1d"
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback if MEASURED_PEAKS.json is absent
 FP32_FMA_PEAK = 148 * 128 * 1.965e9  # FMA/s: SMs x FP32 lanes x max SM clock
+# Tensor-core conv1d (csrc/conv_tc.cu): 33 <= k <= 64 at stride 1, dilation 1; every
+# output costs 3 TF32 MMA products (3xTF32) over the K = 192 Toeplitz depth.
+TC_CONV_K = (33, 64)
+TC_FLOP_PER_OUT = 3 * 192 * 2
+
+
+def conv_on_tensor_cores(c) -> bool:
+    return (c.op == "conv" and TC_CONV_K[0] <= c.w <= TC_CONV_K[1] and c.stride == 1 and c.dilation == 1)
+
+
+def tf32_peak_tflops():
+    """Dense TF32 peak: the measured bf16 number (MEASURED_PEAKS.json) x the nominal tf32/bf16 ratio 1/2."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]) / 2
+    except Exception:  # noqa: BLE001
+        return 2250.0 / 2
 
 
 # ============================================================== workload cells
@@ -516,7 +532,9 @@ def run_ours(args):
              "gelem_s": round(c.n_out / (avg_ms * 1e-3) / 1e9, 2), "gbs": round(gbs, 1),
              "frac_hbm": round(gbs / peak_hbm, 4), "frac_8tbs": round(gbs / 8000.0, 4),
              "share": 0.0}
-        if c.op == "conv":
+        if conv_on_tensor_cores(c):
+            d["tc_frac"] = round(c.n_out * TC_FLOP_PER_OUT / (avg_ms * 1e-3) / 1e12 / tf32_peak_tflops(), 4)
+        elif c.op == "conv":
             fma_s = c.n_out * c.w / (avg_ms * 1e-3)
             d["fma_frac"] = round(fma_s / FP32_FMA_PEAK, 4)
         cells.append(d)
@@ -535,6 +553,11 @@ def run_ours(args):
     else:
         roofline = {"bound": "hbm", "kernel": dom["cell"], "achieved": dom["gbs"], "peak": peak_hbm,
                     "unit": "GB/s", "frac": dom["frac_hbm"], "peak_source": peak_src, "traffic": None}
+        if "tc_frac" in dom:  # tensor-core conv: HBM is the roofline (its TC ceiling is higher)
+            roofline["tensor_frac"] = dom["tc_frac"]
+            roofline["tensor_peak_tflops"] = round(tf32_peak_tflops(), 1)
+            roofline["tensor_note"] = ("executed 3xTF32 MMA work (1152 flop/output) / dense TF32 peak "
+                                       "(measured bf16 / 2)")
     roofline["share_of_step"] = dom["share"]
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):  # dram bytes per launch from a committed `ncu --set full` capture

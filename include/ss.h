@@ -41,11 +41,13 @@
  *  Memory     The library allocates no device memory and keeps no per-call
  *             state; it caches per-device attributes (SM count) only.
  *  Numerics   int32 + wraps modulo 2^32.  fp32 uses IEEE round-to-nearest
- *             FMA/adds (no fast-math, no flush-to-zero).  max equals
+ *             FMA/adds (no fast-math, no flush-to-zero), except the
+ *             tensor-core conv1d path (see ss_conv1d).  max equals
  *             `a > b ? a : b` for finite inputs (NaN unsupported; the sign of
  *             a zero maximum is unspecified).  Results are bitwise
- *             deterministic run to run; conv1d and max results are also
- *             independent of tiling and of sharding.  fp32 results
+ *             deterministic run to run; max results and conv1d results
+ *             with k <= 32 are also independent of tiling and sharding.
+ *             fp32 results
  *             satisfy |y - y_exact| <= 1e-5 * sum_j |x_j f_j| + 1e-6
  *             (BASELINE.json north_star; f = 1 for sums, 1/(kh*kw) for avg).
  */
@@ -99,12 +101,19 @@ ss_status_t ss_pool_max(const void* x, void* y, int64_t N, int64_t batch,
 
 /* Sliding dot product = 1-D convolution with a length-k filter (PAPER.md
  * l.86-87, Sec. 2.5; Eq. 4 per window), cross-correlation orientation
- * (reading R2): y[b][i] = sum_{j<k} filter[j] * x[b][i*stride + j],
- * accumulated in fp32 as fl(S_even + S_odd): S_even / S_odd are FMA chains over
- * the even / odd taps in increasing j from 0 (an association fixed by the tap
- * index alone, so every output is independent of tiling).  One filter shared
- * by all rows.  `filter_host` (k floats, HOST memory) is read before the call
- * returns and may be freed immediately.  dtype must be SS_F32; 1 <= k <= SS_K_MAX. */
+ * (reading R2): y[b][i] = sum_{j<k} filter[j] * x[b][i*stride + j].
+ * Accumulation (fp32):
+ *   k <= 32, or any stride / dilation: fl(S_even + S_odd), S_even / S_odd FMA
+ *     chains over the even / odd taps in increasing j from 0 -- fixed by the
+ *     tap index alone, so every output is independent of tiling and sharding.
+ *   33 <= k <= 64 at stride 1 (dilation 1): tensor cores (Toeplitz matrix
+ *     product), 3xTF32 (x f ~ xh fh + xh fl + xl fh) with fp32
+ *     accumulation; within the bound below with >10x margin, bitwise
+ *     deterministic run to run, but an output's rounding depends on its
+ *     position modulo 8 in the 16-B-aligned view of x.
+ * One filter shared by all rows.  `filter_host` (k floats, HOST memory) is read
+ * before the call returns and may be freed immediately.  dtype must be SS_F32;
+ * 1 <= k <= SS_K_MAX. */
 ss_status_t ss_conv1d(const void* x, void* y, int64_t N, int64_t batch,
                       const float* filter_host, int64_t k, int64_t stride,
                       ss_dtype_t dtype, void* stream);

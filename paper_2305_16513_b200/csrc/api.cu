@@ -104,6 +104,88 @@ bool encode_rows_map(CUtensorMap* m, const void* base, int64_t rows, int box_row
   return make_map(m, base, rows, box_rows);
 }
 
+// Overlapping-chunk view for the tensor-core conv (conv_tc.cu): element
+// (e, m, a) = base[128 m + 32 a + e], i.e. chunk m's K-atom a is the 128-B row
+// 4m + a; box {32, nc, 3} at {0, m0, a0} lands in smem as three nc x 128-B
+// K-major SWIZZLE_128B operands, K-atoms a0 .. a0 + 2.
+bool encode_chunk_map(CUtensorMap* m, const void* base, int64_t m_ext, int atoms, int nc) {
+  auto enc = encode_fn();
+  if (!enc || m_ext < 1 || m_ext > (int64_t(1) << 31) - 1024) return false;
+  cuuint64_t dims[3] = {32, (cuuint64_t)m_ext, (cuuint64_t)atoms};
+  cuuint64_t strides[2] = {512, 128};
+  cuuint32_t box[3] = {32, (cuuint32_t)nc, 3};  // one group of 3 K-atoms per load
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Tensor-core conv selection: k in [tc_min_k, kConvTcMaxK] at stride 1 without
+// dilation (default 33: measured faster than the FFMA2 tile kernel for every
+// k >= 33 on config 3).  SS_CONV_TC_MIN_K (read once) overrides the threshold, 0 disables
+// the path; SS_CONV_TC_NC picks the chunk count per tile (32 / 48 / 64).
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  return atoi(v);
+}
+static int tc_min_k() {
+  static int v = env_int("SS_CONV_TC_MIN_K", 33);
+  return v;
+}
+// SS_CONV_TC_TRACE=1: a 64 x 8 device buffer of CTA-0 role timestamps
+// (debugging only; read back through ss_debug_conv_tc_trace).
+static unsigned long long* g_tc_trace = nullptr;
+static std::atomic<uint64_t> g_tc_launches{0};
+static unsigned long long* tc_trace_buf() {
+  static int on = env_int("SS_CONV_TC_TRACE", 0);
+  if (!on) return nullptr;
+  if (!g_tc_trace && cudaMalloc(&g_tc_trace, 1024 * sizeof(unsigned long long)) != cudaSuccess) g_tc_trace = nullptr;
+  return g_tc_trace;
+}
+static int tc_nc() {
+  static int v = env_int("SS_CONV_TC_NC", 64);
+  return v;
+}
+
+// Try the tensor-core conv for the interior outputs of every row (y_int =
+// first interior output of row 0, rows y_pitch apart).  false: not applicable.
+static bool try_conv_tc(const void* x, float* y_int, int64_t N, int64_t batch, int64_t k, int64_t y_pitch,
+                        const float* taps, cudaStream_t s, int grid, cudaError_t* err) {
+  *err = cudaSuccess;
+  const int mk = tc_min_k();
+  if (mk <= 0 || k < mk || k > kConvTcMaxK) return false;
+  const uintptr_t xa = reinterpret_cast<uintptr_t>(x);
+  if (xa & 3) return false;
+  ConvTCParams p;
+  memset(&p, 0, sizeof p);
+  p.x_view = reinterpret_cast<const float*>(xa & ~uintptr_t(15));
+  p.shift_x = (int64_t)((xa & 15) >> 2);
+  p.y = y_int;
+  p.N = N;
+  p.L_int = N - k + 1;
+  p.batch = batch;
+  p.y_pitch = y_pitch;
+  p.y_off = 0;
+  p.total_view = p.shift_x + batch * N;
+  p.k = (int)k;
+  p.K = 192;  // conv_tc.cu: fixed MMA depth, Toeplitz zero beyond k (k <= 65)
+  p.atoms = 6;
+  if (p.total_view < 32 * p.atoms + 128 * 4) return false;
+  p.m_ext = (p.total_view - 32 * p.atoms) / 128 + 1;
+  const int nc = tc_nc();
+  if (!encode_chunk_map(&p.tm_b, p.x_view, p.m_ext, p.atoms, nc)) return false;
+  for (int j = 0; j < (int)k; ++j) p.taps[j] = taps[j];
+  p.trace = tc_trace_buf();
+  static int lo_slots = env_int("SS_CONV_TC_LO", 0);
+  p.lo_bufs = lo_slots;
+  *err = launch_conv_tc(p, nc, s, grid);
+  if (*err == cudaErrorInvalidConfiguration) { *err = cudaSuccess; return false; }
+  g_tc_launches.fetch_add(1, std::memory_order_relaxed);
+  return true;
+}
+
 // Fill the TMA-kernel geometry; false if this problem cannot take that path.
 static bool make_slide_params(Slide1DParams& p, const void* x, void* y, int64_t N, int64_t batch,
                               int64_t L, int64_t y_pitch = -1, int64_t y_off = 0) {
@@ -208,7 +290,14 @@ static ss_status_t window_impl(int op, const void* x, void* y, int64_t N, int64_
   const int dt = dtype == SS_I32 ? 1 : 0;
   const int64_t L_int = N - w + 1;  // outputs whose window is inside the row (stride 1, d 1)
   bool interior_done = false;
-  if (stride == 1 && d == 1 && L_int >= 1) {
+  if (stride == 1 && d == 1 && L_int >= 1 && op == kOpConv) {
+    cudaError_t e;
+    if (try_conv_tc(x, static_cast<float*>(y) + pl, N, batch, w, L, taps, s, grid, &e)) {
+      if (e != cudaSuccess) return cuda_fail(e, "tensor-core conv launch");
+      interior_done = true;
+    }
+  }
+  if (!interior_done && stride == 1 && d == 1 && L_int >= 1) {
     const int KT = op == kOpConv ? conv_bucket(w) : 0;
     if (op == kOpConv ? KT > 0 : w <= kPoolTmaMaxW) {
       Slide1DParams p;
@@ -248,6 +337,17 @@ using namespace ss;
 extern "C" {
 
 int ss_abi_version(void) { return SS_ABI_VERSION; }
+
+/* Debug hook (not in ss.h): number of conv1d calls served by the tensor-core
+ * kernel (tests use it to check which path ran). */
+uint64_t ss_debug_conv_tc_launches(void) { return g_tc_launches.load(std::memory_order_relaxed); }
+
+/* Debug hook (not in ss.h): copies the tensor-core conv trace (64 x 8 clock64
+ * values) to host memory; returns 0 if tracing is off. */
+int ss_debug_conv_tc_trace(unsigned long long* host) {
+  if (!g_tc_trace) return 0;
+  return cudaMemcpy(host, g_tc_trace, 1024 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) == cudaSuccess;
+}
 
 int64_t ss_out_len(int64_t N, int64_t w, int64_t stride) {
   if (N < 1 || w < 1 || stride < 1 || w > N) return -1;

@@ -1,0 +1,421 @@
+// conv_tc.cu -- conv1d on the 5th-generation tensor cores (SURVEY 8f NEXT #2:
+// the Conclusion's "small matrix multiplication" reformulation, PAPER.md
+// l.228), for filters long enough that the FP32 FMA pipe, not HBM, bounds the
+// FFMA2 tile kernel (k = 63 runs at ~0.65 of the FP32 peak there).
+//
+// Formulation.  The sliding dot product (Sec. 2.5, l.86-87) over a block of
+// 128 consecutive outputs is a matrix product with a Toeplitz matrix:
+//     D[r][m] = sum_kk A[r][kk] * B[m][kk] = y(P0 + 128 m + r)
+//     A[r][kk] = f[kk - r]                (128 x K, K = 127 + k rounded to 8)
+//     B[m][kk] = x(P0 + 128 m + kk)        (NC chunks of the input, K-major)
+// A (the filter, fixed) lives in tensor memory for the whole kernel; B is the
+// input itself, staged by TMA straight from HBM -- K-atom a of chunk m is the
+// 128-B input row 4m + a, so a 3-D tensor map with strides {512 B, 128 B}
+// lays the overlapping rows out as the canonical SWIZZLE_128B K-major operand
+// (no im2col copy in HBM; the 1.5x overlap is re-read from L2 only).
+//
+// fp32 accuracy with TF32 MMAs (kind::tf32, fp32 accumulation in TMEM):
+// the tensor core truncates fp32 operands to TF32 (measured:
+// tools/ubench/tc_conv_probe.cu), so with x = xh + xl, xh = trunc(x),
+// xl = x - xh (exact), and likewise f = fh + fl,
+//     x f ~= xh fh + xh fl + xl fh
+// ("3xTF32"): relative error per product <= ~3 * 2^-22, i.e. within the
+// BASELINE.json bound 1e-5 * sum|x f| + 1e-6 with > 10x margin.  The
+// Toeplitz rows of fh and fl are written to TMEM once; xl is computed per
+// tile by 4 "split" warps into a second smem buffer.
+//
+// Warp roles (persistent CTA per SM, 576 threads):
+//   warp 0      TMA producer (one lane): 3-D box {32, NC, atoms} per tile
+//   warp 1      MMA issuer (one elected lane, warp-uniform operands):
+//               per K-step  D += Alo*Bhi, D += Ahi*Blo, D += Ahi*Bhi
+//   warps 2-9   split: Blo = x - trunc(x) over the staged tile
+//   warps 10-17 epilogue: TMEM -> registers (tcgen05.ld 32x32b) -> one
+//               coalesced 128-B store per warp per chunk column (a tile
+//               inside one batch row stores with immediate offsets; tiles
+//               crossing a row edge mask outputs whose window leaves the row)
+// Pipelines: hi stages (TMA -> split/MMA), lo buffers (split -> MMA), two
+// TMEM accumulators (MMA -> epilogue).
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "ss_device.cuh"
+#include "ss_internal.h"
+
+namespace ss {
+
+namespace {
+
+constexpr int kTcWarpProducer = 0;
+constexpr int kTcWarpMma = 1;
+constexpr int kTcWarpSplit0 = 2;
+constexpr int kTcSplitWarps = 8;
+constexpr int kTcWarpEpi0 = kTcWarpSplit0 + kTcSplitWarps;
+constexpr int kTcEpiWarps = 8;  // two per TMEM lane quarter, each half of the chunk columns
+constexpr int kTcThreads = 32 * (kTcWarpEpi0 + kTcEpiWarps);
+
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);  // start address
+  d |= (uint64_t)1 << 16;                  // LBO (ignored for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;        // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                  // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                  // SWIZZLE_128B
+  return d;
+}
+// kind::tf32 instruction descriptor: D f32, A/B tf32, K-major both, N, M.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// D[tmem] (+)= A[tmem] * B[smem desc]; issued by one elected lane of the
+// calling (converged) warp.
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Arrive on `bar` when every tcgen05 op issued so far by this thread is done.
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+      "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+      "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+      "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// mbarrier wait without a suspend-time hint: a warp parked on a hinted
+// try_wait is not woken promptly by tcgen05.commit arrivals (measured: 10 us
+// per tile), so these pipelines poll.
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                            int32_t c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace
+
+// Debug trace (SS_CONV_TC_TRACE): CTA 0 records clock64() per tile and role
+// event into p.trace[tile_iter * 8 + event].
+#define TC_TRACE(it, ev)                                                                 \
+  do {                                                                                   \
+    if (p.trace && blockIdx.x == 0 && (it) < 64) p.trace[(it) * 8 + (ev)] = clock64(); \
+  } while (0)
+
+// Fixed MMA depth: K = 192 (6 K-atoms of 32, 24 K-steps of 8) serves every
+// k <= 65 (the Toeplitz is zero beyond k); the pipelines move groups of
+// kGroup K-atoms (one TMA box, one split pass, 12 kGroup MMAs per sync).
+constexpr int kTcK = 192;
+constexpr int kTcAtoms = kTcK / 32;
+constexpr int kGroup = 3;
+constexpr int kGroups = kTcAtoms / kGroup;
+
+template <int NC>
+__global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_constant__ ConvTCParams p) {
+  static_assert(NC % 32 == 0 && NC <= 64, "NC/2 columns per epilogue warp, loaded 16 at a time");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Rings of group slots (kGroup K-atoms of all NC chunks, each atom NC x 128 B).
+  const int SH = p.hi_stages, SL = p.lo_bufs;
+  constexpr uint32_t kAtomBytes = NC * 128u;
+  constexpr uint32_t kSlot = kGroup * kAtomBytes;
+  uint8_t* hi = smem;
+  uint8_t* lo = smem + (size_t)SH * kSlot;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lo + (size_t)SL * kSlot);
+  uint64_t* full = bars;                // [SH] TMA -> split, MMA
+  uint64_t* empty = full + SH;          // [SH] MMA commit -> producer
+  uint64_t* lofull = empty + SH;        // [SL] split -> MMA
+  uint64_t* loempty = lofull + SL;      // [SL] MMA commit -> split
+  uint64_t* dfull = loempty + SL;       // [2]  MMA commit -> epilogue
+  uint64_t* dempty = dfull + 2;         // [2]  epilogue -> MMA
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
+  float* fsm = reinterpret_cast<float*>(tslot + 4);  // [2][kConvTcMaxK + 256] zero-padded hi/lo taps
+
+  // ---- setup: barriers, TMEM, taps -----------------------------------------
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < SH; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
+    for (int i = 0; i < SL; ++i) { mbar_init(lofull + i, kTcSplitWarps); mbar_init(loempty + i, 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(dfull + i, 1); mbar_init(dempty + i, kTcEpiWarps); }
+    fence_mbar_init();
+    prefetch_tmap(&p.tm_b);
+  }
+  // fsm[0][128 + t] = hi(f_t), fsm[1][128 + t] = lo(f_t); zeros around, so the
+  // Toeplitz row r reads fsm[.][128 + kk - r] without bounds checks.
+  constexpr int kFPad = kConvTcMaxK + 256;
+  static_assert(128 + kTcK <= kFPad, "Toeplitz reads stay inside fsm");
+  for (int i = threadIdx.x; i < kFPad; i += kTcThreads) {
+    const int t = i - 128;
+    const float f = (t >= 0 && t < p.k) ? p.taps[t] : 0.0f;
+    const float fh = tf32_trunc(f);
+    fsm[i] = fh;
+    fsm[kFPad + i] = tf32_trunc(f - fh);
+  }
+  if (warp == kTcWarpMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  // TMEM columns: A_hi [0, 192), A_lo [192, 384), accumulators [512 - 2 NC, 512)
+  const uint32_t a_hi = tmem, a_lo = tmem + (uint32_t)kTcK;
+  const uint32_t d_col0 = tmem + 512u - 2u * NC;
+  static_assert(2 * kTcK + 2 * NC <= 512, "TMEM budget");
+
+  const int64_t ntiles = p.ntiles;
+
+  if (warp >= kTcWarpEpi0 && warp < kTcWarpEpi0 + 4) {
+    // Toeplitz rows of fh / fl into TMEM: lane r holds A[r][kk] = f[kk - r].
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int r = 32 * q + lane;
+    const uint32_t lanebits = (uint32_t)(32 * q) << 16;
+#pragma unroll 1
+    for (int c = 0; c < kTcK; c += 32) {
+      float vh[32], vl[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int t = 128 + c + j - r;  // in [1, 128 + K) -> inside fsm
+        vh[j] = fsm[t];
+        vl[j] = fsm[kFPad + t];
+      }
+      tmem_st32(a_hi + lanebits + (uint32_t)c, vh);
+      tmem_st32(a_lo + lanebits + (uint32_t)c, vl);
+    }
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  if (warp == kTcWarpProducer) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      int it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        TC_TRACE(it, 0);
+#pragma unroll 1
+        for (int g = 0; g < kGroups; ++g) {
+          bar_wait(empty + s, ph ^ 1);
+          mbar_arrive_expect_tx(full + s, kSlot);
+          tma_load_3d(hi + (size_t)s * kSlot, &p.tm_b, 0, (int32_t)(t * NC), kGroup * g, full + s);
+          if (++s == SH) { s = 0; ph ^= 1; }
+        }
+        TC_TRACE(it, 1);
+      }
+    }
+  } else if (warp == kTcWarpMma) {
+    constexpr uint32_t idesc = idesc_tf32(128, NC);
+    // warp-uniform bases; descriptors advance by adding to the start-address field
+    const uint64_t dhi0 = sw128_desc(__shfl_sync(0xffffffffu, smem_u32(hi), 0));
+    const uint64_t dlo0 = sw128_desc(__shfl_sync(0xffffffffu, smem_u32(lo), 0));
+    const uint32_t ahi = __shfl_sync(0xffffffffu, a_hi, 0), alo = __shfl_sync(0xffffffffu, a_lo, 0);
+    const uint32_t dc0 = __shfl_sync(0xffffffffu, d_col0, 0);
+    int s = 0, l = 0, d = 0;
+    uint32_t ph = 0, lph = 0, dph = 0;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      bar_wait(dempty + d, dph ^ 1);
+      if (lane == 0) TC_TRACE(it, 2);
+      const uint32_t dcol = dc0 + (uint32_t)(d * NC);
+#pragma unroll 1
+      for (int g = 0; g < kGroups; ++g) {
+        bar_wait(full + s, ph);
+        bar_wait(lofull + l, lph);
+        if (lane == 0 && g == 0) TC_TRACE(it, 3);
+        tc_fence_after();
+        const uint64_t dh = dhi0 + (uint64_t)((s * kSlot) >> 4), dl = dlo0 + (uint64_t)((l * kSlot) >> 4);
+        const uint32_t kb0 = (uint32_t)(g * kGroup * 4);
+#pragma unroll
+        for (int j = 0; j < kGroup * 4; ++j) {
+          // K-step kb = kb0 + j: atom j/4 of the group, 32-B column block j%4
+          const uint64_t off = (uint64_t)(((j >> 2) * kAtomBytes + 32u * (j & 3)) >> 4);
+          const uint32_t kb = kb0 + (uint32_t)j;
+          // small terms first: xh*fl and xl*fh, then xh*fh
+          mma_tf32_ts(dcol, alo + 8u * kb, dh + off, idesc, (g > 0 || j > 0) ? 1u : 0u);
+          mma_tf32_ts(dcol, ahi + 8u * kb, dl + off, idesc, 1u);
+          mma_tf32_ts(dcol, ahi + 8u * kb, dh + off, idesc, 1u);
+        }
+        mma_commit(empty + s);
+        mma_commit(loempty + l);
+        if (++s == SH) { s = 0; ph ^= 1; }
+        if (++l == SL) { l = 0; lph ^= 1; }
+      }
+      mma_commit(dfull + d);
+      if (lane == 0) TC_TRACE(it, 4);
+      if (++d == 2) { d = 0; dph ^= 1; }
+    }
+  } else if (warp < kTcWarpEpi0) {
+    // split warps: Blo = x - trunc(x), elementwise (swizzle-agnostic), one group slot at a time
+    const int st = threadIdx.x - 32 * kTcWarpSplit0;  // 0 .. 32 kTcSplitWarps - 1
+    constexpr int kN16 = (int)(kSlot >> 4);
+    static_assert(kN16 % (32 * kTcSplitWarps) == 0, "whole float4s per split thread");
+    int s = 0, l = 0;
+    uint32_t ph = 0, lph = 0;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+#pragma unroll 1
+      for (int g = 0; g < kGroups; ++g) {
+        bar_wait(full + s, ph);
+        if (st == 0 && g == 0) TC_TRACE(it, 5);
+        bar_wait(loempty + l, lph ^ 1);
+        const uint32_t src = smem_u32(hi + (size_t)s * kSlot), dst = smem_u32(lo + (size_t)l * kSlot);
+#pragma unroll
+        for (int i = st; i < kN16; i += 32 * kTcSplitWarps) {
+          const float4 v = lds128(src + 16u * i);
+          sts128(dst + 16u * i, v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
+                 v.w - tf32_trunc(v.w));
+        }
+        fence_proxy_async_smem();  // generic-proxy writes -> tensor core reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(lofull + l);
+        if (st == 0 && g == kGroups - 1) TC_TRACE(it, 6);
+        if (++s == SH) { s = 0; ph ^= 1; }
+        if (++l == SL) { l = 0; lph ^= 1; }
+      }
+    }
+  } else {
+    // epilogue: lane r of quarter q owns output row r = 32q + lane of each chunk;
+    // warp half h stores chunk columns [h NC/2, (h+1) NC/2)
+    constexpr int NH = NC / 2;
+    const int q = warp & 3;
+    const int h = (warp - kTcWarpEpi0) >> 2;
+    const int r = 32 * q + lane;
+    const uint32_t lanebits = (uint32_t)(32 * q) << 16;
+    int d = 0;
+    uint32_t dph = 0;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      bar_wait(dfull + d, dph);
+      if (warp == kTcWarpEpi0 && lane == 0) TC_TRACE(it, 7);
+      tc_fence_after();
+      uint32_t v[NH];
+#pragma unroll
+      for (int c = 0; c < NH; c += 16) tmem_ld16(d_col0 + lanebits + (uint32_t)(d * NC + h * NH + c), v + c);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dempty + d);
+      // chunk c covers view positions 128 (t NC + c) + [0, 128)
+      const int64_t m0 = t * NC + h * NH;
+      const int64_t cmax = p.m_ext - m0 < NH ? p.m_ext - m0 : NH;  // chunks inside the map
+      if (cmax <= 0) {
+        // nothing (tail chunks are done below)
+      } else {
+        // warp-uniform fast path: every position of these columns is a valid
+        // output of one batch row
+        const int64_t q0 = 128 * m0 - p.shift_x, q1 = 128 * (m0 + cmax) - 1 - p.shift_x;
+        const int64_t b0 = q0 >= 0 ? q0 / p.N : -1;
+        const bool fast = cmax == NH && b0 >= 0 && q1 - b0 * p.N < p.L_int;
+        if (fast) {
+          float* __restrict__ yr = p.y + b0 * p.y_pitch + p.y_off + (q0 - b0 * p.N) + r;
+#pragma unroll
+          for (int c = 0; c < NH; ++c) yr[128 * c] = __uint_as_float(v[c]);
+        } else {
+          int64_t qq = q0 + r;
+#pragma unroll
+          for (int c = 0; c < NH; ++c, qq += 128) {
+            if (c < cmax && qq >= 0) {
+              const int64_t b = qq / p.N, i = qq - b * p.N;
+              if (b < p.batch && i < p.L_int) p.y[b * p.y_pitch + p.y_off + i] = __uint_as_float(v[c]);
+            }
+          }
+        }
+      }
+      if (++d == 2) { d = 0; dph ^= 1; }
+    }
+    // view positions beyond the tensor map (array tail): direct FMA windows
+    if (blockIdx.x == gridDim.x - 1 && h == 0) {
+      const float* __restrict__ xv = p.x_view;
+      for (int64_t pos = 128 * p.m_ext + r; pos < p.total_view; pos += 128) {
+        const int64_t qq = pos - p.shift_x;
+        if (qq < 0) continue;
+        const int64_t b = qq / p.N, i = qq - b * p.N;
+        if (b >= p.batch || i >= p.L_int) continue;
+        float acc = 0.0f;
+        for (int j = 0; j < p.k; ++j) acc = __fmaf_rn(p.taps[j], __ldg(xv + pos + j), acc);
+        p.y[b * p.y_pitch + p.y_off + i] = acc;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kTcWarpMma) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+size_t conv_tc_smem_bytes(int hi_slots, int lo_slots, int nc) {
+  return 1024 + (size_t)(hi_slots + lo_slots) * kGroup * nc * 128 + 8 * (2 * hi_slots + 2 * lo_slots + 4) + 16 +
+         2 * sizeof(float) * (kConvTcMaxK + 256);
+}
+
+template <int NC>
+static cudaError_t launch_nc(ConvTCParams& p, cudaStream_t stream, int grid) {
+  // lo ring: four group slots (the split runs ahead of the MMAs);
+  // hi ring: every remaining slot (TMA prefetch depth)
+  if (p.lo_bufs < 1) p.lo_bufs = 4;
+  int SH = 32;
+  while (SH > kGroups && conv_tc_smem_bytes(SH, p.lo_bufs, NC) > (size_t)kSmemBudget) --SH;
+  if (conv_tc_smem_bytes(SH, p.lo_bufs, NC) > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
+  p.hi_stages = SH;
+  p.ntiles = (p.m_ext + NC - 1) / NC;
+  auto kfn = conv_tc_kernel<NC>;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
+  if (e != cudaSuccess) return e;
+  int64_t g = p.ntiles < grid ? p.ntiles : grid;
+  if (g < 1) g = 1;
+  kfn<<<(unsigned)g, kTcThreads, conv_tc_smem_bytes(SH, p.lo_bufs, NC), stream>>>(p);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv_tc(ConvTCParams& p, int nc, cudaStream_t stream, int grid) {
+  switch (nc) {
+    case 32: return launch_nc<32>(p, stream, grid);
+    case 64: return launch_nc<64>(p, stream, grid);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace ss

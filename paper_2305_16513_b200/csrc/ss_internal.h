@@ -97,4 +97,26 @@ size_t affine_smem_bytes(int64_t w);
 cudaError_t launch_affine(AffineParams& p, cudaStream_t stream, int num_sms);
 cudaError_t launch_pool2d_direct(const Pool2DParams& p, cudaStream_t stream, int grid);
 
+// Tensor-core conv1d (conv_tc.cu).  The input is viewed
+// from x_view (x aligned down to 16 B; shift_x = x's element offset in it) as
+// overlapping 128-element chunks: chunk m = view elements [128 m, 128 m + K).
+// Output at view position P (window start) goes to
+// y[b * y_pitch + y_off + i] with P - shift_x = b * N + i, if i < L_int.
+constexpr int kConvTcMaxK = 64;  // K = 127 + k rounded to 8 must fit 2 x 192 TMEM columns
+struct alignas(64) ConvTCParams {
+  CUtensorMap tm_b;        // 3-D {32, m_ext, atoms}, strides {512 B, 128 B}, box {32, NC, 3}, SW128
+  const float* x_view;
+  float* y;
+  int64_t N, L_int, batch, shift_x, y_pitch, y_off;
+  int64_t m_ext;           // chunks whose whole K span lies inside the view
+  int64_t total_view;      // shift_x + batch * N
+  int64_t ntiles;          // set by launch_conv_tc
+  int k, K, atoms;         // filter length, MMA K (192), K-atoms (6)
+  int hi_stages, lo_bufs;  // group slots (3 K-atoms) of the hi / lo rings (set by launch_conv_tc)
+  unsigned long long* trace;  // debug: per-tile role timestamps of CTA 0 (null = off)
+  float taps[kConvTcMaxK];
+};
+bool encode_chunk_map(CUtensorMap* m, const void* base, int64_t m_ext, int atoms, int nc);
+cudaError_t launch_conv_tc(ConvTCParams& p, int nc, cudaStream_t stream, int grid);
+
 }  // namespace ss

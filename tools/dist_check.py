@@ -3,8 +3,10 @@
 Each rank runs bench.Runner on its share of configs 2 (sequence-sharded with
 the halo exchange), 3 and 4 (batch-sharded) at reduced sizes, gathers its
 outputs to rank 0, and rank 0 compares them bitwise with an unsharded
-single-process run of the same kernels (conv and max are shard-invariant
-bitwise; int32 sums are exact)."""
+single-process run of the same kernels (max, int32 sums and FFMA conv
+(k <= 32) are shard-invariant bitwise; the tensor-core conv (33 <= k <= 64)
+rounds by position, so those cells are compared within twice the
+BASELINE.json bound 1e-5 * sum|x f| + 1e-6)."""
 import argparse
 import os
 import sys
@@ -27,6 +29,21 @@ def small(inputs, cells):
         if sp.get("shard") == "image":
             sp["images"], sp["C"] = 3, 4
     return inputs, cells
+
+
+def tc_cell(c):
+    return c.op == "conv" and 33 <= c.w <= 64 and c.stride == 1 and c.dilation == 1 and tuple(c.pads) == (0, 0)
+
+
+def close_within_bound(a, b, R1, c):
+    """|a - b| <= 2 (1e-5 sum_j |x_{i+j} f_j| + 1e-6), magnitudes from the unsharded input."""
+    import torch.nn.functional as F
+    x = R1.x[c.inp].float()
+    x = x.reshape(-1, x.shape[-1])
+    f = torch.tensor(list(c.f), dtype=torch.float32, device=x.device)
+    mag = F.conv1d(x.abs()[:, None, :].double(), f.abs().double()[None, None, :]).reshape(-1).cpu()
+    d = (a.double() - b.double()).abs()
+    return bool((d <= 2 * (1e-5 * mag[:d.numel()] + 1e-6)).all())
 
 
 def outputs(R):
@@ -59,9 +76,16 @@ def main():
         R1.step()
         torch.cuda.synchronize()
         ref = outputs(R1)
+        cells = {c.name: c for c in R1.cells}
         for name in ref:
-            same = torch.equal(gathered[name], ref[name].cpu())
-            print(f"{name:18s} sharded x{world} == unsharded: {same} ({ref[name].numel()} outputs)")
+            c = cells[name]
+            if tc_cell(c):
+                same = close_within_bound(gathered[name], ref[name].cpu(), R1, c)
+                how = "within bound"
+            else:
+                same = torch.equal(gathered[name], ref[name].cpu())
+                how = "bitwise"
+            print(f"{name:18s} sharded x{world} == unsharded ({how}): {same} ({ref[name].numel()} outputs)")
             ok &= same
         print("DIST_CHECK", "PASS" if ok else "FAIL")
     dist.barrier()

@@ -1,0 +1,108 @@
+"""Quick GPU check of the tensor-core conv path (csrc/conv_tc.cu): parity against
+the oracle over shapes / alignments, forced onto the TC path with
+SS_CONV_TC_MIN_K=1, then per-NC timing of BASELINE config 3 (64 x 2^20,
+k in {31, 48, 63}) against the FFMA2 tile kernel.  Usage (GPU box):
+    SS_CONV_TC_MIN_K=1 SS_CONV_TC_NC=64 python tools/tc_conv_check.py [parity|time]"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+import paper_2305_16513_b200 as ss  # noqa: E402
+import synth  # noqa: E402
+
+
+def parity():
+    cases = [(1, 200, 1), (1, 5000, 8), (3, 1000, 33), (2, 70001, 63), (1, 65536, 64), (5, 9999, 40),
+             (64, 4096, 63), (7, 333, 64), (1, 1 << 18, 48), (4, 12345, 17), (2, 190, 63), (3, 130, 64)]
+    worst = 0.0
+    for (B, N, k) in cases:
+        for xoff in (0, 1, 3):
+            x = synth.normal(3, B * N).reshape(B, N)
+            f = synth.normal(4, k, sigma=synth.cfg_sigma_filter(k))
+            buf = torch.zeros(B * N + 8, device="cuda")
+            buf[xoff:xoff + B * N] = torch.from_numpy(x.reshape(-1)).cuda()
+            xd = buf[xoff:xoff + B * N].view(B, N)
+            L = N - k + 1
+            ybuf = torch.full((B * L + 9,), -777.0, device="cuda")
+            y = ybuf[1:1 + B * L].view(B, L)
+            n0 = ss.ss_launch_count()
+            ss.conv1d(xd, f, out=y)
+            torch.cuda.synchronize()
+            h = ybuf.cpu().numpy()
+            assert h[0] == -777.0 and np.all(h[1 + B * L:] == -777.0), "canary"
+            ref, mag = oracle.conv1d(x, f)
+            err = np.abs(y.cpu().numpy().astype(np.float64) - ref)
+            ratio = float((err / (1e-5 * mag + 1e-6)).max())
+            worst = max(worst, ratio)
+            bad = int((err > 1e-5 * mag + 1e-6).sum())
+            print(f"B={B} N={N} k={k} xoff={xoff}: launches {ss.ss_launch_count() - n0} max err/bound {ratio:.3g} bad {bad}",
+                  flush=True)
+            assert bad == 0
+    print("parity ok, worst err/bound", worst)
+
+
+def timing():
+    B, N = 64, 1 << 20
+    x = torch.empty(B, N, device="cuda")
+    synth.fill_device(x, "normal", 3)
+    ks = [int(v) for v in os.environ.get("KS", "31,48,63").split(",")]
+    reps = int(os.environ.get("REPS", "12"))
+    for k in ks:
+        f = synth.normal(4, k, sigma=synth.cfg_sigma_filter(k))
+        y = torch.empty(B, N - k + 1, device="cuda")
+        flush = torch.empty(64 << 20, device="cuda")
+        ts = []
+        for it in range(reps):
+            flush.fill_(1.0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            ss.conv1d(x, f, out=y)
+            b.record()
+            torch.cuda.synchronize()
+            if it >= min(2, reps - 1):
+                ts.append(a.elapsed_time(b))
+        t = sorted(ts)[len(ts) // 2]
+        outs = B * (N - k + 1)
+        print(f"k={k}: {t * 1e3:.1f} us  {outs / t / 1e6:.1f} GElem/s  {8 * outs / t / 1e6:.0f} GB/s", flush=True)
+
+
+def trace():
+    import ctypes
+    B, N, k = 64, 1 << 20, int(os.environ.get("KS", "63"))
+    x = torch.empty(B, N, device="cuda")
+    synth.fill_device(x, "normal", 3)
+    f = synth.normal(4, k, sigma=synth.cfg_sigma_filter(k))
+    y = torch.empty(B, N - k + 1, device="cuda")
+    for _ in range(3):
+        ss.conv1d(x, f, out=y)
+    torch.cuda.synchronize()
+    buf = (ctypes.c_ulonglong * 1024)()
+    assert ss.lib.ss_debug_conv_tc_trace(buf)
+    allv = np.array(buf, dtype=np.int64)
+    t = allv[:512].reshape(64, 8)
+
+    t0 = t[0, 0]
+    names = ["P.start", "P.issued", "M.dempty", "M.data", "M.issued", "S.full0", "S.done", "E.dfull"]
+    print("tile " + " ".join(f"{n:>9s}" for n in names))
+    for i in range(min(40, t.shape[0])):
+        if t[i, 0] == 0:
+            break
+        print(f"{i:4d} " + " ".join(f"{v - t0:9d}" for v in t[i]))
+    d = np.diff(t[5:40, 4])
+    print("MMA issue-done period (clk): median", np.median(d))
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "parity"
+    if what == "parity":
+        parity()
+    elif what == "trace":
+        trace()
+    else:
+        timing()
