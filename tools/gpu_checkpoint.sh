@@ -10,4 +10,4 @@ python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$TA
 CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/plain_$TAG.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "ncu-launches rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"slide1d_tma_kernel|pool2d_vec" -s 18 -c 18 -o gpurun_out/prof_full_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu-full rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:"slide1d_tma_kernel|pool2d_vec|conv_tc" -s 18 -c 18 -o gpurun_out/prof_full_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu-full rc=$?"
