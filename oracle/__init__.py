@@ -80,6 +80,16 @@ def lib() -> ctypes.CDLL:
             L.oracle_gamma_sequence.restype = ctypes.c_int
             L.oracle_gamma_dot.argtypes = [vp, vp, i64, vp]
             L.oracle_gamma_dot.restype = dp
+            L.oracle_pool_sum_backward_f32.argtypes = [vp, i64, i64, i64, i64, vp, vp]
+            L.oracle_pool_max_backward_f32.argtypes = [vp, vp, i64, i64, i64, i64, vp]
+            L.oracle_conv1d_backward_input_f32.argtypes = [vp, i64, i64, vp, i64, i64, vp, vp]
+            L.oracle_conv1d_backward_filter_f32.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp]
+            L.oracle_pool2d_backward_f32.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64,
+                                                     ctypes.c_int, vp, vp]
+            for n in ("oracle_pool_sum_backward_f32", "oracle_pool_max_backward_f32",
+                      "oracle_conv1d_backward_input_f32", "oracle_conv1d_backward_filter_f32",
+                      "oracle_pool2d_backward_f32"):
+                getattr(L, n).restype = ctypes.c_int
             _lib = L
     return _lib
 
@@ -251,3 +261,73 @@ def gamma_dot(a: np.ndarray, b: np.ndarray):
     u = ctypes.c_double()
     v = lib().oracle_gamma_dot(_p(a), _p(b), a.shape[0], ctypes.byref(u))
     return v, u.value
+
+
+# ---------------------------------------------------------------- backward passes
+# Vector-Jacobian products of the forward definitions.
+# dy has the forward output's shape ([B, L]); dx the input's ([B, N]).
+
+def _bwd_rows(dy: np.ndarray, N: int, w: int, s: int):
+    dy = np.ascontiguousarray(dy, np.float32)
+    squeeze = dy.ndim == 1
+    dy2 = dy.reshape(1, -1) if squeeze else dy
+    B = dy2.shape[0]
+    L = out_len(N, w, s)
+    if L < 0 or dy2.shape[1] != L:
+        raise ValueError("dy does not match the forward output length")
+    return dy2, B, squeeze
+
+
+def pool_sum_backward(dy: np.ndarray, N: int, w: int, s: int = 1):
+    """dx of Eq. 3 with + : dx_t = sum of dy_i over the windows i containing t; (dx, absmag)."""
+    dy2, B, sq = _bwd_rows(dy, N, w, s)
+    dx = np.empty((B, N), np.float64)
+    m = np.empty((B, N), np.float64)
+    _check(lib().oracle_pool_sum_backward_f32(_p(dy2), N, B, w, s, _p(dx), _p(m)))
+    return (dx[0], m[0]) if sq else (dx, m)
+
+
+def pool_max_backward(x: np.ndarray, dy: np.ndarray, w: int, s: int = 1) -> np.ndarray:
+    """dx of Eq. 3 with max: each window's dy goes to its first maximum (reading R16)."""
+    x, N, B = _rows(np.asarray(x, np.float32))
+    dy2, B2, sq = _bwd_rows(dy, N, w, s)
+    assert B2 == B
+    dx = np.empty((B, N), np.float64)
+    _check(lib().oracle_pool_max_backward_f32(_p(x), _p(dy2), N, B, w, s, _p(dx)))
+    return dx[0] if sq else dx
+
+
+def conv1d_backward_input(dy: np.ndarray, f: np.ndarray, N: int, s: int = 1):
+    """dx of the sliding dot product: dx_t = sum_{is+j=t} f_j dy_i; (dx, absmag)."""
+    f = np.ascontiguousarray(f, np.float32)
+    dy2, B, sq = _bwd_rows(dy, N, f.shape[0], s)
+    dx = np.empty((B, N), np.float64)
+    m = np.empty((B, N), np.float64)
+    _check(lib().oracle_conv1d_backward_input_f32(_p(dy2), N, B, _p(f), f.shape[0], s, _p(dx), _p(m)))
+    return (dx[0], m[0]) if sq else (dx, m)
+
+
+def conv1d_backward_filter(x: np.ndarray, dy: np.ndarray, k: int, s: int = 1):
+    """df of the sliding dot product: df_j = sum_b sum_i dy_i x_{is+j}; (df, absmag)."""
+    x, N, B = _rows(np.asarray(x, np.float32))
+    dy2, B2, _ = _bwd_rows(dy, N, k, s)
+    assert B2 == B
+    df = np.empty(k, np.float64)
+    m = np.empty(k, np.float64)
+    _check(lib().oracle_conv1d_backward_filter_f32(_p(x), _p(dy2), N, B, k, s, _p(df), _p(m)))
+    return df, m
+
+
+def pool2d_backward(x, dy: np.ndarray, H: int, W: int, kh: int, kw: int, sh: int, sw: int, mode: int):
+    """dx of the direct 2-D pooling (mode POOL2D_MAX / POOL2D_AVG); (dx, absmag)."""
+    dy = np.ascontiguousarray(dy, np.float32)
+    P = dy.shape[0]
+    if mode == 0:
+        x = np.ascontiguousarray(x, np.float32)
+        xp = _p(x)
+    else:
+        xp = None
+    dx = np.empty((P, H, W), np.float64)
+    m = np.empty((P, H, W), np.float64)
+    _check(lib().oracle_pool2d_backward_f32(xp, _p(dy), P, H, W, kh, kw, sh, sw, mode, _p(dx), _p(m)))
+    return dx, m

@@ -355,3 +355,133 @@ double oracle_gamma_dot(const double* a, const double* b, int64_t M, double* u_o
   if (u_out) *u_out = du;
   return dv;
 }
+
+/* ---- backward passes (the abstract's "training", PAPER.md
+ * l.7).  Each is the vector-Jacobian product of the forward definition above,
+ * written as the scatter J^T dy: every forward term y_i <- x_t sends dy_i back
+ * to dx_t (times its coefficient).  Accumulation in double; absmag = the sum of
+ * the magnitudes of the terms (BASELINE.json tolerance form). */
+
+/* Eq. 3 with +:  y_i = sum_{j<w} x_{is+j}  =>  dx_t = sum_{i: is <= t < is+w} dy_i. */
+int oracle_pool_sum_backward_f32(const float* dy, int64_t N, int64_t batch, int64_t w,
+                                 int64_t s, double* dx, double* absmag) {
+  if (bad_1d(dy, dx, N, batch, w, s)) return -1;
+  int64_t L = oracle_out_len(N, w, s);
+  for (int64_t t = 0; t < batch * N; ++t) {
+    dx[t] = 0.0;
+    if (absmag) absmag[t] = 0.0;
+  }
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t i = 0; i < L; ++i)
+      for (int64_t j = 0; j < w; ++j) {
+        double g = (double)dy[b * L + i];
+        dx[b * N + i * s + j] += g;
+        if (absmag) absmag[b * N + i * s + j] += fabs(g);
+      }
+  return 0;
+}
+
+/* Eq. 3 with max:  y_i = x_{a_i}, a_i = the FIRST index of the maximum of
+ * window i (scan left to right, replace on strictly greater)  =>
+ * dx_t = sum_{i: a_i = t} dy_i  (the subgradient that routes each window's
+ * gradient to its first maximum; reading R16). */
+int oracle_pool_max_backward_f32(const float* x, const float* dy, int64_t N, int64_t batch,
+                                 int64_t w, int64_t s, double* dx) {
+  if (bad_1d(x, dx, N, batch, w, s) || dy == NULL) return -1;
+  int64_t L = oracle_out_len(N, w, s);
+  for (int64_t t = 0; t < batch * N; ++t) dx[t] = 0.0;
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t i = 0; i < L; ++i) {
+      const float* xw = x + b * N + i * s;
+      int64_t a = 0;
+      float m = xw[0];
+      for (int64_t j = 1; j < w; ++j)
+        if (xw[j] > m) {
+          m = xw[j];
+          a = j;
+        }
+      dx[b * N + i * s + a] += (double)dy[b * L + i];
+    }
+  return 0;
+}
+
+/* Sec. 2.5:  y_i = sum_j f_j x_{is+j}  =>  dx_t = sum_{(i,j): is+j = t} f_j dy_i. */
+int oracle_conv1d_backward_input_f32(const float* dy, int64_t N, int64_t batch, const float* f,
+                                     int64_t k, int64_t s, double* dx, double* absmag) {
+  if (bad_1d(dy, dx, N, batch, k, s) || f == NULL) return -1;
+  int64_t L = oracle_out_len(N, k, s);
+  for (int64_t t = 0; t < batch * N; ++t) {
+    dx[t] = 0.0;
+    if (absmag) absmag[t] = 0.0;
+  }
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t i = 0; i < L; ++i)
+      for (int64_t j = 0; j < k; ++j) {
+        double p = (double)f[j] * (double)dy[b * L + i];
+        dx[b * N + i * s + j] += p;
+        if (absmag) absmag[b * N + i * s + j] += fabs(p);
+      }
+  return 0;
+}
+
+/* Sec. 2.5:  y_i = sum_j f_j x_{is+j}  =>  df_j = sum_b sum_i dy_i x_{is+j}. */
+int oracle_conv1d_backward_filter_f32(const float* x, const float* dy, int64_t N, int64_t batch,
+                                      int64_t k, int64_t s, double* df, double* absmag) {
+  if (bad_1d(x, df, N, batch, k, s) || dy == NULL) return -1;
+  int64_t L = oracle_out_len(N, k, s);
+  for (int64_t j = 0; j < k; ++j) {
+    df[j] = 0.0;
+    if (absmag) absmag[j] = 0.0;
+  }
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t i = 0; i < L; ++i)
+      for (int64_t j = 0; j < k; ++j) {
+        double p = (double)dy[b * L + i] * (double)x[b * N + i * s + j];
+        df[j] += p;
+        if (absmag) absmag[j] += fabs(p);
+      }
+  return 0;
+}
+
+/* 2-D pooling (direct window, as oracle_pool2d_f32):  avg: y = (1/(kh kw)) sum of
+ * the window => dx gets dy/(kh kw) at every window position; max: y = x at the
+ * first maximum in row-major scan order => dx gets dy there. */
+int oracle_pool2d_backward_f32(const float* x, const float* dy, int64_t planes, int64_t H,
+                               int64_t W, int64_t kh, int64_t kw, int64_t sh, int64_t sw,
+                               int mode, double* dx, double* absmag) {
+  int64_t OH = oracle_out_len(H, kh, sh), OW = oracle_out_len(W, kw, sw);
+  if (dy == NULL || dx == NULL || planes < 1 || OH < 0 || OW < 0) return -1;
+  if (mode == 0 && x == NULL) return -1;
+  for (int64_t t = 0; t < planes * H * W; ++t) {
+    dx[t] = 0.0;
+    if (absmag) absmag[t] = 0.0;
+  }
+  double inv = 1.0 / (double)(kh * kw);
+  for (int64_t p = 0; p < planes; ++p)
+    for (int64_t r = 0; r < OH; ++r)
+      for (int64_t c = 0; c < OW; ++c) {
+        double g = (double)dy[(p * OH + r) * OW + c];
+        if (mode == 1) {
+          for (int64_t a = 0; a < kh; ++a)
+            for (int64_t e = 0; e < kw; ++e) {
+              int64_t t = (p * H + r * sh + a) * W + c * sw + e;
+              dx[t] += g * inv;
+              if (absmag) absmag[t] += fabs(g * inv);
+            }
+        } else {
+          int64_t best = (p * H + r * sh) * W + c * sw;
+          float m = x[best];
+          for (int64_t a = 0; a < kh; ++a)
+            for (int64_t e = 0; e < kw; ++e) {
+              int64_t t = (p * H + r * sh + a) * W + c * sw + e;
+              if (x[t] > m) {
+                m = x[t];
+                best = t;
+              }
+            }
+          dx[best] += g;
+          if (absmag) absmag[best] += fabs(g);
+        }
+      }
+  return 0;
+}

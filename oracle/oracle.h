@@ -105,6 +105,22 @@ int oracle_gamma_sequence(const double* a, const double* b, int64_t M,
  * and u(delta_M) in *u_out. */
 double oracle_gamma_dot(const double* a, const double* b, int64_t M, double* u_out);
 
+/* Backward passes (vector-Jacobian products of the forward definitions; SURVEY
+ * 8f NEXT #4).  dy is [batch][L] (L = oracle_out_len), dx is [batch][N]; for
+ * 2-D, dy is [planes][OH][OW] and dx [planes][H][W].  Results in double;
+ * absmag (optional) = per-output sum of term magnitudes. */
+int oracle_pool_sum_backward_f32(const float* dy, int64_t N, int64_t batch, int64_t w,
+                                 int64_t s, double* dx, double* absmag);
+int oracle_pool_max_backward_f32(const float* x, const float* dy, int64_t N, int64_t batch,
+                                 int64_t w, int64_t s, double* dx);
+int oracle_conv1d_backward_input_f32(const float* dy, int64_t N, int64_t batch, const float* f,
+                                     int64_t k, int64_t s, double* dx, double* absmag);
+int oracle_conv1d_backward_filter_f32(const float* x, const float* dy, int64_t N, int64_t batch,
+                                      int64_t k, int64_t s, double* df, double* absmag);
+int oracle_pool2d_backward_f32(const float* x, const float* dy, int64_t planes, int64_t H,
+                               int64_t W, int64_t kh, int64_t kw, int64_t sh, int64_t sw,
+                               int mode, double* dx, double* absmag);
+
 #ifdef __cplusplus
 }
 #endif
