@@ -54,13 +54,14 @@
 #ifndef SS_H
 #define SS_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 3
+#define SS_ABI_VERSION 4
 
 typedef enum { SS_F32 = 0, SS_I32 = 1 } ss_dtype_t;
 typedef enum { SS_POOL_MAX = 0, SS_POOL_AVG = 1 } ss_pool_mode_t;
@@ -176,6 +177,46 @@ ss_status_t ss_conv1d_ex(const void* x, void* y, int64_t N, int64_t batch,
 #define SS_AFFINE_W_MAX 65536
 ss_status_t ss_affine_window(const float* u, const float* v, float* U, float* V, int64_t N,
                              int64_t batch, int64_t w, int64_t stride, void* stream);
+
+/* ---- backward passes (training) ----------
+ * Vector-Jacobian products of the forward calls above (DESIGN.md reading
+ * R16): given dy = dLoss/dy (the forward output's shape, [batch][L] with
+ * L = ss_out_len(N, w or k, stride)), write dx = dLoss/dx ([batch][N], fully
+ * overwritten: positions no window touches get 0) or df.  Each result is a
+ * gather over the windows touching an output position in increasing window
+ * order (no atomics): bitwise deterministic.  Errors, streams and ownership
+ * as above; dx / df must not overlap any input.  Stride-1 sum and conv input
+ * gradients run the forward kernels on dy zero-padded by w-1 (k-1) with the
+ * filter flipped, so their numerics are the forward ones.
+ *
+ *   ss_pool_sum_backward   dx_t = sum_{i: i*s <= t < i*s+w} dy_i.  SS_F32 or SS_I32 (wraps).
+ *   ss_pool_max_backward   dx_t = sum of dy_i over the windows whose FIRST maximum
+ *                          (left-to-right, replaced on strictly greater) is x_t.
+ *                          x = the forward input.  SS_F32 only.
+ *   ss_conv1d_backward_input   dx_t = sum_{(i,j): i*s+j = t} f_j dy_i.  SS_F32.
+ *   ss_conv1d_backward_filter  df_j = sum_b sum_i dy[b][i] x[b][i*s+j]  (df: DEVICE,
+ *                          k floats; fp32 products summed in fp32 runs of 16, then
+ *                          fp64; stride <= 64).  `workspace` (DEVICE, caller-owned,
+ *                          >= ss_conv1d_backward_filter_workspace(k) bytes on the
+ *                          current device) holds per-CTA fp64 partials.
+ *   ss_pool2d_backward     [planes][H][W] gradient of ss_pool2d: avg spreads
+ *                          dy/(kh*kw) over each window; max routes dy to the window's
+ *                          first maximum in row-major order (x may be NULL for avg).
+ */
+ss_status_t ss_pool_sum_backward(const void* dy, void* dx, int64_t N, int64_t batch, int64_t w,
+                                 int64_t stride, ss_dtype_t dtype, void* stream);
+ss_status_t ss_pool_max_backward(const void* x, const void* dy, void* dx, int64_t N, int64_t batch,
+                                 int64_t w, int64_t stride, ss_dtype_t dtype, void* stream);
+ss_status_t ss_conv1d_backward_input(const void* dy, void* dx, int64_t N, int64_t batch,
+                                     const float* filter_host, int64_t k, int64_t stride,
+                                     ss_dtype_t dtype, void* stream);
+size_t ss_conv1d_backward_filter_workspace(int64_t k);
+ss_status_t ss_conv1d_backward_filter(const void* x, const void* dy, float* df, int64_t N,
+                                      int64_t batch, int64_t k, int64_t stride, void* workspace,
+                                      size_t workspace_bytes, void* stream);
+ss_status_t ss_pool2d_backward(const void* x, const void* dy, void* dx, int64_t planes, int64_t H,
+                               int64_t W, int64_t kh, int64_t kw, int64_t sh, int64_t sw,
+                               ss_pool_mode_t mode, ss_dtype_t dtype, void* stream);
 
 /* Static description of a status code. */
 const char* ss_status_string(ss_status_t s);

@@ -36,7 +36,9 @@ SS_AFFINE_W_MAX = 65536
 EXPORTED = ("ss_abi_version", "ss_out_len", "ss_pool_sum", "ss_pool_max", "ss_conv1d",
             "ss_pool2d", "ss_status_string", "ss_last_error", "ss_launch_count",
             "ss_out_len_ex", "ss_pool_sum_ex", "ss_pool_max_ex", "ss_conv1d_ex",
-            "ss_affine_window")
+            "ss_affine_window", "ss_pool_sum_backward", "ss_pool_max_backward",
+            "ss_conv1d_backward_input", "ss_conv1d_backward_filter_workspace", "ss_conv1d_backward_filter",
+            "ss_pool2d_backward")
 
 
 class SSError(RuntimeError):
@@ -73,6 +75,18 @@ def _load() -> ctypes.CDLL:
     L.ss_conv1d_ex.restype = i32
     L.ss_affine_window.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64, vp]
     L.ss_affine_window.restype = i32
+    L.ss_pool_sum_backward.argtypes = [vp, vp, i64, i64, i64, i64, i32, vp]
+    L.ss_pool_sum_backward.restype = i32
+    L.ss_pool_max_backward.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32, vp]
+    L.ss_pool_max_backward.restype = i32
+    L.ss_conv1d_backward_input.argtypes = [vp, vp, i64, i64, ctypes.POINTER(ctypes.c_float), i64, i64, i32, vp]
+    L.ss_conv1d_backward_input.restype = i32
+    L.ss_conv1d_backward_filter_workspace.argtypes = [i64]
+    L.ss_conv1d_backward_filter_workspace.restype = ctypes.c_size_t
+    L.ss_conv1d_backward_filter.argtypes = [vp, vp, vp, i64, i64, i64, i64, vp, ctypes.c_size_t, vp]
+    L.ss_conv1d_backward_filter.restype = i32
+    L.ss_pool2d_backward.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i64, i32, i32, vp]
+    L.ss_pool2d_backward.restype = i32
     L.ss_status_string.argtypes = [i32]
     L.ss_status_string.restype = ctypes.c_char_p
     L.ss_last_error.argtypes = []
@@ -152,6 +166,31 @@ def ss_conv1d_ex(x_ptr, y_ptr, N, batch, filter_host, k, stride, dilation, pad_l
 
 def ss_affine_window(u_ptr, v_ptr, U_ptr, V_ptr, N, batch, w, stride=1, stream=0) -> int:
     return _lib.ss_affine_window(u_ptr, v_ptr, U_ptr, V_ptr, N, batch, w, stride, stream)
+
+
+def ss_pool_sum_backward(dy_ptr, dx_ptr, N, batch, w, stride, dtype, stream=0) -> int:
+    return _lib.ss_pool_sum_backward(dy_ptr, dx_ptr, N, batch, w, stride, dtype, stream)
+
+
+def ss_pool_max_backward(x_ptr, dy_ptr, dx_ptr, N, batch, w, stride, dtype=SS_F32, stream=0) -> int:
+    return _lib.ss_pool_max_backward(x_ptr, dy_ptr, dx_ptr, N, batch, w, stride, dtype, stream)
+
+
+def ss_conv1d_backward_input(dy_ptr, dx_ptr, N, batch, filter_host, k, stride, dtype=SS_F32, stream=0) -> int:
+    fp = None if filter_host is None else (ctypes.c_float * len(filter_host))(*[float(v) for v in filter_host])
+    return _lib.ss_conv1d_backward_input(dy_ptr, dx_ptr, N, batch, fp, k, stride, dtype, stream)
+
+
+def ss_conv1d_backward_filter_workspace(k: int) -> int:
+    return int(_lib.ss_conv1d_backward_filter_workspace(k))
+
+
+def ss_conv1d_backward_filter(x_ptr, dy_ptr, df_ptr, N, batch, k, stride, ws_ptr, ws_bytes, stream=0) -> int:
+    return _lib.ss_conv1d_backward_filter(x_ptr, dy_ptr, df_ptr, N, batch, k, stride, ws_ptr, ws_bytes, stream)
+
+
+def ss_pool2d_backward(x_ptr, dy_ptr, dx_ptr, planes, H, W, kh, kw, sh, sw, mode, dtype=SS_F32, stream=0) -> int:
+    return _lib.ss_pool2d_backward(x_ptr, dy_ptr, dx_ptr, planes, H, W, kh, kw, sh, sw, mode, dtype, stream)
 
 
 def check(status: int) -> None:
@@ -295,3 +334,70 @@ def affine_window(u, v, w: int, stride: int = 1, want_U: bool = True, out=None, 
     check(ss_affine_window(u.data_ptr(), v.data_ptr(), 0 if U is None else U.data_ptr(), V.data_ptr(),
                            N, B, w, stride, _stream(stream)))
     return U, V
+
+
+# ------------------------------------------------------------ backward passes
+def _grad_out(dy, N, out):
+    torch = _torch()
+    shape = (N,) if dy.dim() == 1 else (dy.shape[0], N)
+    if out is None:
+        return torch.empty(shape, dtype=dy.dtype, device=dy.device)
+    assert tuple(out.shape) == shape and out.dtype == dy.dtype and out.is_contiguous()
+    return out
+
+
+def pool_sum_backward(dy, N: int, w: int, stride: int = 1, out=None, stream=None):
+    """dx of pool_sum (valid padding): dx_t = sum of dy over the windows containing t."""
+    L, B = _rows(dy)
+    dx = _grad_out(dy, N, out)
+    check(ss_pool_sum_backward(dy.data_ptr(), dx.data_ptr(), N, B, w, stride, _dtype_code(dy), _stream(stream)))
+    return dx
+
+
+def pool_max_backward(x, dy, w: int, stride: int = 1, out=None, stream=None):
+    """dx of pool_max: each window's dy goes to its first maximum in x."""
+    N, B = _rows(x)
+    dx = _grad_out(dy, N, out)
+    check(ss_pool_max_backward(x.data_ptr(), dy.data_ptr(), dx.data_ptr(), N, B, w, stride, _dtype_code(x),
+                               _stream(stream)))
+    return dx
+
+
+def conv1d_backward_input(dy, filt, N: int, stride: int = 1, out=None, stream=None):
+    """dx of conv1d (valid padding, cross-correlation) for a host filter."""
+    L, B = _rows(dy)
+    f = [float(v) for v in (filt.tolist() if hasattr(filt, "tolist") else filt)]
+    dx = _grad_out(dy, N, out)
+    check(ss_conv1d_backward_input(dy.data_ptr(), dx.data_ptr(), N, B, f, len(f), stride, _dtype_code(dy),
+                                   _stream(stream)))
+    return dx
+
+
+def conv1d_backward_filter(x, dy, k: int, stride: int = 1, out=None, workspace=None, stream=None):
+    """df of conv1d: df_j = sum over rows and outputs of dy_i x_{i*stride+j} (device tensor of k floats)."""
+    torch = _torch()
+    N, B = _rows(x)
+    df = torch.empty(k, dtype=torch.float32, device=x.device) if out is None else out
+    need = ss_conv1d_backward_filter_workspace(k)
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+    check(ss_conv1d_backward_filter(x.data_ptr(), dy.data_ptr(), df.data_ptr(), N, B, k, stride,
+                                    workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+                                    _stream(stream)))
+    return df
+
+
+def pool2d_backward(x, dy, kernel, stride, mode: str = "max", out=None, stream=None):
+    """dx of pool2d for [..., H, W] tensors (x may be None for avg)."""
+    torch = _torch()
+    kh, kw = kernel
+    sh, sw = stride
+    H, W = (x.shape[-2], x.shape[-1]) if x is not None else (None, None)
+    if H is None:
+        raise ValueError("pass x (or a tensor of its shape) to size dx")
+    planes = x.numel() // (H * W)
+    dx = torch.empty_like(x) if out is None else out
+    m = SS_POOL_MAX if mode == "max" else SS_POOL_AVG
+    check(ss_pool2d_backward(x.data_ptr() if mode == "max" else 0, dy.data_ptr(), dx.data_ptr(), planes, H, W,
+                             kh, kw, sh, sw, m, _dtype_code(dy), _stream(stream)))
+    return dx

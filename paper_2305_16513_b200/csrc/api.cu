@@ -392,6 +392,152 @@ ss_status_t ss_conv1d_ex(const void* x, void* y, int64_t N, int64_t batch, const
                      filter_host, stream);
 }
 
+// ---- backward passes (backward.cu) -----------------------
+static ss_status_t validate_bwd(const void* a, const void* b, const void* dx, int64_t N, int64_t batch,
+                                int64_t w, int64_t stride, const char* wname, int64_t* L) {
+  if (!a || !b || !dx) return fail(SS_ERR_NULL, "pointers must be non-NULL device pointers");
+  if (N < 1 || batch < 1 || w < 1 || stride < 1)
+    return fail(SS_ERR_BAD_SIZE, "N=%lld batch=%lld %s=%lld stride=%lld must all be >= 1", (long long)N,
+                (long long)batch, wname, (long long)w, (long long)stride);
+  if (N > INT64_MAX / 8 / batch) return fail(SS_ERR_BAD_SIZE, "sizes overflow int64");
+  if (w > N) return fail(SS_ERR_WINDOW_EXCEEDS_INPUT, "window exceeds input: %s=%lld > N=%lld", wname,
+                         (long long)w, (long long)N);
+  *L = (N - w) / stride + 1;
+  return SS_OK;
+}
+
+static ss_status_t pool_sum_backward_impl(const void* dy, void* dx, int64_t N, int64_t batch, int64_t w, int64_t stride,
+                                   ss_dtype_t dtype, void* stream) {
+  int64_t L = 0;
+  ss_status_t st = validate_bwd(dy, dy, dx, N, batch, w, stride, "w", &L);
+  if (st != SS_OK) return st;
+  if (dtype != SS_F32 && dtype != SS_I32) return fail(SS_ERR_UNSUPPORTED, "dtype %d", (int)dtype);
+  if (overlaps(dy, batch * L * 4, dx, batch * N * 4)) return fail(SS_ERR_OVERLAP, "dy and dx overlap");
+  if (stride == 1)  // dx = sliding sum of dy zero-padded by w-1 on both sides (length L + w - 1 = N)
+    return window_impl(kOpSum, dy, dx, L, batch, w, 1, 1, w - 1, w - 1, dtype, nullptr, stream);
+  BackwardParams p;
+  memset(&p, 0, sizeof p);
+  p.dy = dy; p.dx = dx; p.N = N; p.L = L; p.batch = batch; p.w = w; p.stride = stride;
+  cudaError_t e = launch_transpose_window(p, kOpSum, dtype == SS_I32 ? 1 : 0, static_cast<cudaStream_t>(stream),
+                                          current_sms());
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "pool_sum_backward launch");
+}
+
+static ss_status_t conv1d_backward_input_impl(const void* dy, void* dx, int64_t N, int64_t batch, const float* f,
+                                       int64_t k, int64_t stride, ss_dtype_t dtype, void* stream) {
+  if (!f) return fail(SS_ERR_NULL, "filter_host must be non-NULL");
+  int64_t L = 0;
+  ss_status_t st = validate_bwd(dy, dy, dx, N, batch, k, stride, "k", &L);
+  if (st != SS_OK) return st;
+  if (dtype != SS_F32) return fail(SS_ERR_UNSUPPORTED, "conv1d backward supports SS_F32 only");
+  if (k > SS_K_MAX) return fail(SS_ERR_UNSUPPORTED, "k=%lld > SS_K_MAX=%d", (long long)k, SS_K_MAX);
+  if (overlaps(dy, batch * L * 4, dx, batch * N * 4)) return fail(SS_ERR_OVERLAP, "dy and dx overlap");
+  if (stride == 1) {  // dx = dy zero-padded by k-1 on both sides, correlated with the flipped filter
+    float flipped[SS_K_MAX];
+    for (int64_t j = 0; j < k; ++j) flipped[j] = f[k - 1 - j];
+    return window_impl(kOpConv, dy, dx, L, batch, k, 1, 1, k - 1, k - 1, SS_F32, flipped, stream);
+  }
+  BackwardParams p;
+  memset(&p, 0, sizeof p);
+  p.dy = dy; p.dx = dx; p.N = N; p.L = L; p.batch = batch; p.w = k; p.stride = stride;
+  for (int64_t j = 0; j < k; ++j) p.taps[j] = f[j];
+  cudaError_t e = launch_transpose_window(p, kOpConv, 0, static_cast<cudaStream_t>(stream), current_sms());
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv1d_backward_input launch");
+}
+
+static ss_status_t pool_max_backward_impl(const void* x, const void* dy, void* dx, int64_t N, int64_t batch, int64_t w,
+                                   int64_t stride, ss_dtype_t dtype, void* stream) {
+  int64_t L = 0;
+  ss_status_t st = validate_bwd(x, dy, dx, N, batch, w, stride, "w", &L);
+  if (st != SS_OK) return st;
+  if (dtype != SS_F32) return fail(SS_ERR_UNSUPPORTED, "pool_max backward supports SS_F32 only");
+  if (overlaps(dy, batch * L * 4, dx, batch * N * 4) || overlaps(x, batch * N * 4, dx, batch * N * 4))
+    return fail(SS_ERR_OVERLAP, "dx overlaps an input");
+  BackwardParams p;
+  memset(&p, 0, sizeof p);
+  p.x = x; p.dy = dy; p.dx = dx; p.N = N; p.L = L; p.batch = batch; p.w = w; p.stride = stride;
+  cudaError_t e = launch_pool_max_backward(p, static_cast<cudaStream_t>(stream), current_sms());
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "pool_max_backward launch");
+}
+
+static ss_status_t conv1d_backward_filter_impl(const void* x, const void* dy, float* df, int64_t N, int64_t batch, int64_t k,
+                                        int64_t stride, void* workspace, size_t ws_bytes, void* stream) {
+  int64_t L = 0;
+  ss_status_t st = validate_bwd(x, dy, df, N, batch, k, stride, "k", &L);
+  if (st != SS_OK) return st;
+  if (k > SS_K_MAX) return fail(SS_ERR_UNSUPPORTED, "k=%lld > SS_K_MAX=%d", (long long)k, SS_K_MAX);
+  if (stride > 64) return fail(SS_ERR_UNSUPPORTED, "filter gradient supports stride <= 64");
+  const int ctas = current_sms();
+  const size_t need = conv_filter_grad_workspace(k, ctas);
+  if (!workspace || ws_bytes < need)
+    return fail(SS_ERR_BAD_SIZE, "workspace of %zu bytes needed (ss_conv1d_backward_filter_workspace)", need);
+  if (overlaps(workspace, (int64_t)need, x, batch * N * 4) || overlaps(workspace, (int64_t)need, dy, batch * L * 4) ||
+      overlaps(workspace, (int64_t)need, df, k * 4) || overlaps(df, k * 4, x, batch * N * 4) ||
+      overlaps(df, k * 4, dy, batch * L * 4))
+    return fail(SS_ERR_OVERLAP, "df / workspace overlap an input");
+  BackwardParams p;
+  memset(&p, 0, sizeof p);
+  p.x = x; p.dy = dy; p.N = N; p.L = L; p.batch = batch; p.w = k; p.stride = stride;
+  cudaError_t e = launch_conv_filter_grad(p, df, workspace, ctas, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv1d_backward_filter launch");
+}
+
+static size_t conv1d_backward_filter_workspace_impl(int64_t k) {
+  if (k < 1 || k > SS_K_MAX) return 0;
+  return conv_filter_grad_workspace(k, current_sms());
+}
+
+static ss_status_t pool2d_backward_impl(const void* x, const void* dy, void* dx, int64_t planes, int64_t H, int64_t W,
+                                 int64_t kh, int64_t kw, int64_t sh, int64_t sw, ss_pool_mode_t mode,
+                                 ss_dtype_t dtype, void* stream) {
+  if (!dy || !dx || (mode == SS_POOL_MAX && !x)) return fail(SS_ERR_NULL, "pointers must be non-NULL");
+  if (planes < 1 || H < 1 || W < 1 || kh < 1 || kw < 1 || sh < 1 || sw < 1)
+    return fail(SS_ERR_BAD_SIZE, "planes/H/W/kh/kw/sh/sw must be >= 1");
+  if (kh > H || kw > W) return fail(SS_ERR_WINDOW_EXCEEDS_INPUT, "window exceeds input");
+  if (mode != SS_POOL_MAX && mode != SS_POOL_AVG) return fail(SS_ERR_UNSUPPORTED, "mode %d", (int)mode);
+  if (dtype != SS_F32) return fail(SS_ERR_UNSUPPORTED, "pool2d backward supports SS_F32 only");
+  if (H > INT64_MAX / 8 / W || H * W > INT64_MAX / 8 / planes) return fail(SS_ERR_BAD_SIZE, "sizes overflow int64");
+  Pool2DBackwardParams p;
+  memset(&p, 0, sizeof p);
+  p.x = static_cast<const float*>(x); p.dy = static_cast<const float*>(dy); p.dx = static_cast<float*>(dx);
+  p.planes = planes; p.H = H; p.W = W; p.kh = kh; p.kw = kw; p.sh = sh; p.sw = sw;
+  p.OH = (H - kh) / sh + 1; p.OW = (W - kw) / sw + 1;
+  p.mode = mode == SS_POOL_AVG ? 1 : 0;
+  p.inv_area = 1.0f / (float)(kh * kw);
+  const int64_t nx = planes * H * W * 4, ny = planes * p.OH * p.OW * 4;
+  if (overlaps(dy, ny, dx, nx) || (x && overlaps(x, nx, dx, nx))) return fail(SS_ERR_OVERLAP, "dx overlaps an input");
+  cudaError_t e = launch_pool2d_backward(p, static_cast<cudaStream_t>(stream), current_sms());
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "pool2d_backward launch");
+}
+
+ss_status_t ss_pool_sum_backward(const void* dy, void* dx, int64_t N, int64_t batch, int64_t w, int64_t stride,
+                                 ss_dtype_t dtype, void* stream) {
+  return pool_sum_backward_impl(dy, dx, N, batch, w, stride, dtype, stream);
+}
+
+ss_status_t ss_pool_max_backward(const void* x, const void* dy, void* dx, int64_t N, int64_t batch, int64_t w,
+                                 int64_t stride, ss_dtype_t dtype, void* stream) {
+  return pool_max_backward_impl(x, dy, dx, N, batch, w, stride, dtype, stream);
+}
+
+ss_status_t ss_conv1d_backward_input(const void* dy, void* dx, int64_t N, int64_t batch, const float* filter_host,
+                                     int64_t k, int64_t stride, ss_dtype_t dtype, void* stream) {
+  return conv1d_backward_input_impl(dy, dx, N, batch, filter_host, k, stride, dtype, stream);
+}
+
+size_t ss_conv1d_backward_filter_workspace(int64_t k) { return conv1d_backward_filter_workspace_impl(k); }
+
+ss_status_t ss_conv1d_backward_filter(const void* x, const void* dy, float* df, int64_t N, int64_t batch, int64_t k,
+                                      int64_t stride, void* workspace, size_t workspace_bytes, void* stream) {
+  return conv1d_backward_filter_impl(x, dy, df, N, batch, k, stride, workspace, workspace_bytes, stream);
+}
+
+ss_status_t ss_pool2d_backward(const void* x, const void* dy, void* dx, int64_t planes, int64_t H, int64_t W,
+                               int64_t kh, int64_t kw, int64_t sh, int64_t sw, ss_pool_mode_t mode, ss_dtype_t dtype,
+                               void* stream) {
+  return pool2d_backward_impl(x, dy, dx, planes, H, W, kh, kw, sh, sw, mode, dtype, stream);
+}
+
 int64_t ss_out_len_ex(int64_t N, int64_t w, int64_t stride, int64_t dilation, int64_t pad_left,
                       int64_t pad_right) {
   if (N < 1 || w < 1 || stride < 1 || dilation < 1 || pad_left < 0 || pad_right < 0) return -1;

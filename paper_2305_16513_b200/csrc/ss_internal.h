@@ -119,4 +119,28 @@ struct alignas(64) ConvTCParams {
 bool encode_chunk_map(CUtensorMap* m, const void* base, int64_t m_ext, int atoms, int nc);
 cudaError_t launch_conv_tc(ConvTCParams& p, int nc, cudaStream_t stream, int grid);
 
+// Backward passes (backward.cu).  dy: [batch][L] (the
+// forward output), dx: [batch][N]; x: the forward input (max / filter grad).
+struct BackwardParams {
+  const void* x;
+  const void* dy;
+  void* dx;
+  int64_t N, L, batch, w, stride;
+  float taps[1024];  // conv input gradient: the forward filter f (SS_K_MAX)
+};
+struct Pool2DBackwardParams {
+  const float* x;
+  const float* dy;
+  float* dx;
+  int64_t planes, H, W, OH, OW, kh, kw, sh, sw;
+  int mode;  // 0 max, 1 avg
+  float inv_area;
+};
+cudaError_t launch_transpose_window(const BackwardParams& p, int op, int dtype, cudaStream_t stream, int sms);
+cudaError_t launch_pool_max_backward(const BackwardParams& p, cudaStream_t stream, int sms);
+size_t conv_filter_grad_workspace(int64_t k, int ctas);
+cudaError_t launch_conv_filter_grad(const BackwardParams& p, float* df, void* workspace, int ctas,
+                                    cudaStream_t stream);
+cudaError_t launch_pool2d_backward(const Pool2DBackwardParams& p, cudaStream_t stream, int sms);
+
 }  // namespace ss

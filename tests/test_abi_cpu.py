@@ -45,7 +45,7 @@ def test_library_is_sm100a(ss):
 
 
 def test_abi_version_and_out_len(ss):
-    assert ss.ss_abi_version() == 3
+    assert ss.ss_abi_version() == 4
     assert ss.ss_out_len(10, 3, 1) == 8
     assert ss.ss_out_len(10, 3, 4) == 2
     assert ss.ss_out_len(2 ** 32, 31, 1) == 2 ** 32 - 30
@@ -137,4 +137,29 @@ def test_affine_window_validation(ss):
     assert f(X, Y, U, X + 4, 10, 1, 3) == ss.SS_ERR_OVERLAP
     assert f(X, Y, V + 8, V, 10, 1, 3) == ss.SS_ERR_OVERLAP
     assert f(X, Y, U, V + 2, 10, 1, 3) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_launch_count() == 0
+
+
+def test_backward_validation(ss):
+    # every invalid call returns its status before any launch (no GPU needed)
+    X, G, D = FAKE_X, FAKE_X + 0x1000000, FAKE_Y
+    assert ss.ss_pool_sum_backward(0, D, 10, 1, 3, 1, ss.SS_F32) == ss.SS_ERR_NULL
+    assert ss.ss_pool_sum_backward(G, D, 10, 1, 0, 1, ss.SS_F32) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_pool_sum_backward(G, D, 10, 1, 3, 0, ss.SS_F32) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_pool_sum_backward(G, D, 2, 1, 3, 1, ss.SS_F32) == ss.SS_ERR_WINDOW_EXCEEDS_INPUT
+    assert ss.ss_pool_sum_backward(G, G + 4, 10, 1, 3, 1, ss.SS_F32) == ss.SS_ERR_OVERLAP
+    assert ss.ss_pool_sum_backward(G, D, 10, 1, 3, 1, 7) == ss.SS_ERR_UNSUPPORTED
+    assert ss.ss_pool_max_backward(X, G, D, 10, 1, 3, 1, ss.SS_I32) == ss.SS_ERR_UNSUPPORTED
+    assert ss.ss_pool_max_backward(0, G, D, 10, 1, 3, 1) == ss.SS_ERR_NULL
+    assert ss.ss_pool_max_backward(X, G, X + 8, 10, 1, 3, 1) == ss.SS_ERR_OVERLAP
+    assert ss.ss_conv1d_backward_input(G, D, 10, 1, None, 3, 1) == ss.SS_ERR_NULL
+    assert ss.ss_conv1d_backward_input(G, D, 10, 1, [1.0] * 3, 3, 1, ss.SS_I32) == ss.SS_ERR_UNSUPPORTED
+    assert ss.ss_conv1d_backward_input(G, D, 2000, 1, [1.0] * 1025, 1025, 1) == ss.SS_ERR_UNSUPPORTED
+    assert ss.ss_conv1d_backward_filter_workspace(0) == 0
+    assert ss.ss_conv1d_backward_filter_workspace(63) > 0
+    assert ss.ss_conv1d_backward_filter(X, G, D, 10, 1, 3, 1, 0, 0) == ss.SS_ERR_BAD_SIZE  # no workspace
+    assert ss.ss_conv1d_backward_filter(X, G, D, 10, 1, 11, 1, D + 4096, 1 << 20) == ss.SS_ERR_WINDOW_EXCEEDS_INPUT
+    assert ss.ss_pool2d_backward(0, G, D, 1, 8, 8, 2, 2, 2, 2, ss.SS_POOL_MAX) == ss.SS_ERR_NULL
+    assert ss.ss_pool2d_backward(X, G, D, 1, 8, 8, 9, 2, 2, 2, ss.SS_POOL_AVG) == ss.SS_ERR_WINDOW_EXCEEDS_INPUT
+    assert ss.ss_pool2d_backward(X, G, D, 1, 8, 8, 2, 2, 2, 2, 5) == ss.SS_ERR_UNSUPPORTED
     assert ss.ss_launch_count() == 0

@@ -1,0 +1,180 @@
+"""GPU parity of the backward passes (csrc/backward.cu +
+stride-1 reuse of the forward kernels) against the oracle's vector-Jacobian
+products (tests/test_oracle_backward_pins.py pins those).  fp32 results within
+1e-5 * sum|terms| + 1e-6 (BASELINE.json form; sum|terms| from the oracle, or
+the max routing of |dy|), int32 sums bit-exact modulo 2^32; every dx element is
+written (positions no window touches are 0) and canaries around dx survive."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+TOL_REL, TOL_ABS = 1e-5, 1e-6
+
+
+@pytest.fixture(scope="module")
+def ss():
+    import paper_2305_16513_b200 as ss
+    return ss
+
+
+def dev(a, off=0):
+    a = np.ascontiguousarray(a)
+    buf = torch.zeros(a.size + off + 4, dtype=torch.from_numpy(a[:0]).dtype if a.size else torch.float32,
+                      device="cuda")
+    buf[off:off + a.size] = torch.from_numpy(a.reshape(-1)).cuda()
+    return buf[off:off + a.size]
+
+
+def out_buf(n, dtype=torch.float32, off=0, fill=-4321):
+    buf = torch.full((n + off + 6,), fill, dtype=dtype, device="cuda")
+    return buf, buf[off:off + n]
+
+
+def canary_ok(buf, off, n, fill=-4321):
+    h = buf.cpu().numpy()
+    return np.all(h[:off] == fill) and np.all(h[off + n:] == fill)
+
+
+def within(y, ref, mag, what):
+    err = np.abs(y.astype(np.float64) - ref)
+    bound = TOL_REL * mag + TOL_ABS
+    assert np.all(err <= bound), f"{what}: {(err > bound).sum()} out of bound, max err/bound {(err / bound).max():.3g}"
+
+
+POOL_CASES = [  # (B, N, w, s)
+    (1, 1, 1, 1), (2, 9, 3, 1), (3, 1000, 8, 1), (2, 70001, 64, 1), (1, 40000, 257, 1), (2, 1001, 4, 2),
+    (3, 999, 7, 3), (1, 5000, 2, 2), (2, 777, 9, 4), (1, 3000, 1, 5), (4, 20000, 33, 1),
+]
+
+
+@pytest.mark.parametrize("B,N,w,s", POOL_CASES)
+@pytest.mark.parametrize("off", [0, 1])
+def test_pool_sum_backward_f32(ss, B, N, w, s, off):
+    L = (N - w) // s + 1
+    dy = synth.normal(21, B * L).reshape(B, L)
+    buf, dx = out_buf(B * N, off=off)
+    dyd = dev(dy, off)  # keep the device copies alive until the launch has run
+    ss.check(ss.ss_pool_sum_backward(dyd.data_ptr(), dx.data_ptr(), N, B, w, s, ss.SS_F32))
+    torch.cuda.synchronize()
+    assert canary_ok(buf, off, B * N)
+    ref, mag = oracle.pool_sum_backward(dy, N, w, s)
+    within(dx.cpu().numpy().reshape(B, N), ref, mag, f"sum bwd B={B} N={N} w={w} s={s}")
+
+
+@pytest.mark.parametrize("B,N,w,s", POOL_CASES)
+def test_pool_sum_backward_i32_exact(ss, B, N, w, s):
+    L = (N - w) // s + 1
+    dy = synth.randint(22, B * L, -1000, 1000).reshape(B, L)
+    buf, dx = out_buf(B * N, torch.int32)
+    dyd = dev(dy)
+    ss.check(ss.ss_pool_sum_backward(dyd.data_ptr(), dx.data_ptr(), N, B, w, s, ss.SS_I32))
+    torch.cuda.synchronize()
+    assert canary_ok(buf, 0, B * N)
+    ref, _ = oracle.pool_sum_backward(dy.astype(np.float32), N, w, s)  # |dy| <= 1000: exact in fp32 / double
+    np.testing.assert_array_equal(dx.cpu().numpy().reshape(B, N).astype(np.int64), ref.astype(np.int64))
+
+
+@pytest.mark.parametrize("B,N,w,s", POOL_CASES)
+@pytest.mark.parametrize("ties", [False, True])
+def test_pool_max_backward(ss, B, N, w, s, ties):
+    L = (N - w) // s + 1
+    x = (synth.randint(23, B * N, -2, 2).astype(np.float32) if ties else synth.normal(23, B * N)).reshape(B, N)
+    dy = synth.normal(24, B * L).reshape(B, L)
+    buf, dx = out_buf(B * N, off=1)
+    xd, dyd = dev(x), dev(dy, 3)
+    ss.check(ss.ss_pool_max_backward(xd.data_ptr(), dyd.data_ptr(), dx.data_ptr(), N, B, w, s))
+    torch.cuda.synchronize()
+    assert canary_ok(buf, 1, B * N)
+    ref = oracle.pool_max_backward(x, dy, w, s)
+    mag = oracle.pool_max_backward(x, np.abs(dy), w, s)  # same routing, |dy|
+    within(dx.cpu().numpy().reshape(B, N), ref, mag, f"max bwd B={B} N={N} w={w} s={s} ties={ties}")
+    if w <= s:  # windows disjoint: one dy per position -> exact
+        np.testing.assert_array_equal(dx.cpu().numpy().reshape(B, N).astype(np.float64), ref)
+
+
+CONV_CASES = [  # (B, N, k, s)
+    (1, 10, 1, 1), (2, 1000, 3, 1), (3, 20001, 7, 1), (2, 70000, 31, 1), (2, 50000, 40, 1), (1, 80001, 63, 1),
+    (3, 30000, 64, 1), (1, 9000, 100, 1), (2, 3001, 5, 2), (3, 4000, 9, 3), (1, 5000, 64, 4), (2, 999, 13, 7),
+]
+
+
+@pytest.mark.parametrize("B,N,k,s", CONV_CASES)
+def test_conv_backward_input(ss, B, N, k, s):
+    L = (N - k) // s + 1
+    dy = synth.normal(25, B * L).reshape(B, L)
+    f = synth.normal(26, k, sigma=synth.cfg_sigma_filter(k))
+    buf, dx = out_buf(B * N, off=2)
+    dyd = dev(dy, 1)
+    ss.check(ss.ss_conv1d_backward_input(dyd.data_ptr(), dx.data_ptr(), N, B, f.tolist(), k, s))
+    torch.cuda.synchronize()
+    assert canary_ok(buf, 2, B * N)
+    ref, mag = oracle.conv1d_backward_input(dy, f, N, s)
+    within(dx.cpu().numpy().reshape(B, N), ref, mag, f"conv bwd input B={B} N={N} k={k} s={s}")
+
+
+FILTER_CASES = CONV_CASES + [(1, 5000, 65, 1), (2, 3000, 130, 1), (1, 7000, 200, 3), (64, 4096, 63, 1),
+                             (5, 1500, 1024, 1)]
+
+
+@pytest.mark.parametrize("B,N,k,s", FILTER_CASES)
+def test_conv_backward_filter(ss, B, N, k, s):
+    L = (N - k) // s + 1
+    x = synth.normal(27, B * N).reshape(B, N)
+    dy = synth.normal(28, B * L).reshape(B, L)
+    df = ss.conv1d_backward_filter(dev(x, 1).view(B, N), dev(dy, 2).view(B, L), k, s).cpu().numpy()
+    ref, mag = oracle.conv1d_backward_filter(x, dy, k, s)
+    within(df, ref, mag, f"conv bwd filter B={B} N={N} k={k} s={s}")
+
+
+def test_conv_backward_filter_deterministic(ss):
+    x = torch.from_numpy(synth.normal(29, 8 * 100000).reshape(8, -1)).cuda()
+    dy = torch.from_numpy(synth.normal(30, 8 * (100000 - 62)).reshape(8, -1)).cuda()
+    a = ss.conv1d_backward_filter(x, dy, 63)
+    b = ss.conv1d_backward_filter(x, dy, 63)
+    assert torch.equal(a, b)
+
+
+P2_CASES = [(3, 16, 17, 3, 3, 1, 1), (2, 31, 30, 2, 2, 2, 2), (2, 20, 21, 3, 2, 2, 1), (1, 112, 112, 3, 3, 1, 1),
+            (4, 9, 9, 9, 9, 1, 1), (2, 15, 40, 1, 5, 1, 3)]
+
+
+@pytest.mark.parametrize("P,H,W,kh,kw,sh,sw", P2_CASES)
+@pytest.mark.parametrize("mode", ["max", "avg"])
+def test_pool2d_backward(ss, mode, P, H, W, kh, kw, sh, sw):
+    OH, OW = (H - kh) // sh + 1, (W - kw) // sw + 1
+    x = synth.uniform01(31, P * H * W).reshape(P, H, W)
+    dy = synth.normal(32, P * OH * OW).reshape(P, OH, OW)
+    m = ss.SS_POOL_MAX if mode == "max" else ss.SS_POOL_AVG
+    buf, dx = out_buf(P * H * W, off=1)
+    xd, dyd = dev(x), dev(dy)
+    ss.check(ss.ss_pool2d_backward(xd.data_ptr() if mode == "max" else 0, dyd.data_ptr(), dx.data_ptr(),
+                                   P, H, W, kh, kw, sh, sw, m))
+    torch.cuda.synchronize()
+    assert canary_ok(buf, 1, P * H * W)
+    ref, mag = oracle.pool2d_backward(x, dy, H, W, kh, kw, sh, sw, oracle.POOL2D_MAX if mode == "max" else
+                                      oracle.POOL2D_AVG)
+    within(dx.cpu().numpy().reshape(P, H, W), ref, mag, f"pool2d bwd {mode} {(P, H, W, kh, kw, sh, sw)}")
+
+
+def test_backward_matches_torch_autograd_cfg3_slice(ss):
+    # a config-3-shaped slice (rows of 2^20, k = 63) end to end against torch
+    # float64 autograd of F.conv1d (test-only library reference)
+    B, N, k = 4, 1 << 20, 63
+    x = torch.empty(B, N, device="cuda")
+    synth.fill_device(x, "normal", 3)
+    f = synth.normal(4, k, sigma=synth.cfg_sigma_filter(k))
+    dy = torch.empty(B, N - k + 1, device="cuda")
+    synth.fill_device(dy, "normal", 33)
+    dx = ss.conv1d_backward_input(dy, f, N)
+    df = ss.conv1d_backward_filter(x, dy, k)
+    xt = x.double().requires_grad_(True)
+    ft = torch.tensor(f, dtype=torch.float64, device="cuda", requires_grad=True)
+    torch.nn.functional.conv1d(xt[:, None, :], ft[None, None, :])[:, 0, :].backward(dy.double())
+    mag_x = torch.nn.functional.conv_transpose1d(dy.double().abs()[:, None, :], ft.detach().abs()[None, None, :])[:, 0, :]
+    assert torch.all((dx.double() - xt.grad).abs() <= TOL_REL * mag_x + TOL_ABS)
+    mag_f = (x.double().abs()[:, None, :].unfold(2, N - k + 1, 1)[:, 0] * dy.double().abs()[:, None, :]).sum((0, 2))
+    assert torch.all((df.double() - ft.grad).abs() <= TOL_REL * mag_f + TOL_ABS)
