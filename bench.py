@@ -57,8 +57,13 @@ TC_CONV_K = (33, 64)
 TC_FLOP_PER_OUT = 3 * 192 * 2
 
 
+BWD_OPS = ("conv_bwd_in", "conv_bwd_f", "sum_bwd", "max_bwd", "pool2d_bwd")
+
+
 def conv_on_tensor_cores(c) -> bool:
-    return (c.op == "conv" and TC_CONV_K[0] <= c.w <= TC_CONV_K[1] and c.stride == 1 and c.dilation == 1)
+    # forward conv, and the stride-1 input gradient (forward kernels on padded dy)
+    return (c.op in ("conv", "conv_bwd_in") and TC_CONV_K[0] <= c.w <= TC_CONV_K[1] and c.stride == 1
+            and c.dilation == 1)
 
 
 def tf32_peak_tflops():
@@ -146,6 +151,25 @@ def cfg_cells(workload: str):
                               shard="batch")
         for w in (8, 64, 1024):
             cells.append(Cell("affine", f"affine_w{w}", "affine", w=w, inp="xa_u", inp2="xa_v"))
+    if workload == "backward":  # backward passes on config-3 / config-4 shapes; not a BJ config
+        inputs["xb"] = dict(rows=64, n=1 << 20, dtype="float32", dist="normal", seed=3, kw={}, shard="batch")
+        for k in (7, 31, 63):
+            inputs[f"gb{k}"] = dict(rows=64, n=(1 << 20) - k + 1, dtype="float32", dist="normal", seed=33, kw={},
+                                    shard="batch")
+            f = synth.normal(4, k, sigma=synth.cfg_sigma_filter(k))
+            cells.append(Cell("backward", f"bwd_conv_input_k{k}", "conv_bwd_in", w=k, f=f, inp=f"gb{k}"))
+            cells.append(Cell("backward", f"bwd_conv_filter_k{k}", "conv_bwd_f", w=k, f=f, inp="xb", inp2=f"gb{k}"))
+        inputs["gb16"] = dict(rows=64, n=(1 << 20) - 15, dtype="float32", dist="normal", seed=33, kw={}, shard="batch")
+        cells.append(Cell("backward", "bwd_sum_w16", "sum_bwd", w=16, inp="gb16"))
+        cells.append(Cell("backward", "bwd_max_w16", "max_bwd", w=16, inp="xb", inp2="gb16"))
+        inputs["x4b"] = dict(images=32, C=64, H=112, W=112, dtype="float32", dist="u01", seed=5, kw={}, shard="image")
+        for kk, st in ((3, 1), (2, 2)):
+            oh = (112 - kk) // st + 1
+            inputs[f"g4_{kk}"] = dict(images=32, C=64, H=oh, W=oh, dtype="float32", dist="normal", seed=34, kw={},
+                                      shard="image")
+            for mode in ("max", "avg"):
+                cells.append(Cell("backward", f"bwd_pool2d_{mode}_{kk}x{kk}_s{st}", "pool2d_bwd", kh=kk, kw=kk, sh=st,
+                                  sw=st, mode=mode, inp="x4b", inp2=f"g4_{kk}"))
     if not cells:
         raise SystemExit(f"unknown workload {workload}")
     return inputs, cells
@@ -280,6 +304,9 @@ class Runner:
             kind, geo = self.meta[c.inp]
             x = self.x[c.inp]
             es = x.element_size()
+            if c.op in BWD_OPS:
+                self._alloc_bwd(c)
+                continue
             if c.op == "pool2d":
                 B, C, H, W = geo
                 OH, OW = (H - c.kh) // c.sh + 1, (W - c.kw) // c.sw + 1
@@ -311,6 +338,67 @@ class Runner:
                 c.bytes = (n + L) * es
             c.flops = 2 * c.w * c.n_out if c.op == "conv" else 0
 
+    def _alloc_bwd(self, c):
+        """Backward cells: dx (or df + workspace) and the algorithmic bytes / unit counts.
+        n_out = gradient elements written (dx), or for the filter gradient the
+        rows x L products it reduces."""
+        torch = self.torch
+        x = self.x[c.inp]
+        if c.op == "pool2d_bwd":
+            g = self.x[c.inp2]
+            self.y[c.name] = torch.empty_like(x)
+            c.n_out = x.numel()
+            c.bytes = 4 * (x.numel() * (2 if c.mode == "max" else 1) + g.numel())
+            return
+        if c.op in ("conv_bwd_in", "sum_bwd"):  # inp = dy [rows, L]
+            rows, L = x.shape
+            N = L + c.w - 1
+            self.y[c.name] = torch.empty((rows, N), dtype=x.dtype, device=self.device)
+            c.n_out = rows * N
+            c.bytes = 4 * (rows * L + rows * N)
+            c.flops = 2 * c.w * rows * L if c.op == "conv_bwd_in" else 0
+            return
+        rows, N = x.shape                          # inp = x [rows, N], inp2 = dy [rows, L]
+        L = self.x[c.inp2].shape[1]
+        if c.op == "max_bwd":
+            self.y[c.name] = torch.empty((rows, N), dtype=x.dtype, device=self.device)
+            c.n_out = rows * N
+            c.bytes = 4 * (2 * rows * N + rows * L)
+        else:  # conv_bwd_f
+            self.y[c.name] = torch.empty(c.w, dtype=torch.float32, device=self.device)
+            self.ws = getattr(self, "ws", {})
+            self.ws[c.name] = torch.empty(self.ss.ss_conv1d_backward_filter_workspace(c.w), dtype=torch.uint8,
+                                          device=self.device)
+            c.n_out = rows * L
+            c.bytes = 4 * (rows * N + rows * L + c.w)
+            c.flops = 2 * c.w * rows * L
+
+    def _launch_bwd(self, c):
+        ss, st = self.ss, self.stream.cuda_stream
+        x, y = self.x[c.inp], self.y[c.name]
+        if c.op == "pool2d_bwd":
+            B, C, H, W = x.shape
+            g = self.x[c.inp2]
+            ss.check(ss.ss_pool2d_backward(x.data_ptr(), g.data_ptr(), y.data_ptr(), B * C, H, W, c.kh, c.kw, c.sh,
+                                           c.sw, ss.SS_POOL_MAX if c.mode == "max" else ss.SS_POOL_AVG,
+                                           ss.SS_F32, st))
+        elif c.op == "conv_bwd_in":
+            rows, L = x.shape
+            ss.check(ss.ss_conv1d_backward_input(x.data_ptr(), y.data_ptr(), L + c.w - 1, rows, c.f, c.w, 1,
+                                                 ss.SS_F32, st))
+        elif c.op == "sum_bwd":
+            rows, L = x.shape
+            ss.check(ss.ss_pool_sum_backward(x.data_ptr(), y.data_ptr(), L + c.w - 1, rows, c.w, 1, ss.SS_F32, st))
+        elif c.op == "max_bwd":
+            rows, N = x.shape
+            ss.check(ss.ss_pool_max_backward(x.data_ptr(), self.x[c.inp2].data_ptr(), y.data_ptr(), N, rows, c.w, 1,
+                                             ss.SS_F32, st))
+        else:
+            rows, N = x.shape
+            ws = self.ws[c.name]
+            ss.check(ss.ss_conv1d_backward_filter(x.data_ptr(), self.x[c.inp2].data_ptr(), y.data_ptr(), N, rows,
+                                                  c.w, 1, ws.data_ptr(), ws.numel(), st))
+
     # ---- one launch
     def _launch_1d(self, c, x, y):
         ss = self.ss
@@ -336,7 +424,11 @@ class Runner:
     def _launch_cell(self, c, events=None):
         kind, geo = self.meta[c.inp]
         x, y = self.x[c.inp], self.y[c.name]
-        if c.op == "pool2d":
+        if c.op in BWD_OPS:
+            ev0 = self._ev(events)
+            self._launch_bwd(c)
+            self._ev_end(events, c, ev0)
+        elif c.op == "pool2d":
             B, C, H, W = geo
             ev0 = self._ev(events)
             self.ss.check(self.ss.ss_pool2d(x.data_ptr(), y.data_ptr(), B * C, H, W, c.kh, c.kw, c.sh, c.sw,
@@ -534,8 +626,8 @@ def run_ours(args):
              "share": 0.0}
         if conv_on_tensor_cores(c):
             d["tc_frac"] = round(c.n_out * TC_FLOP_PER_OUT / (avg_ms * 1e-3) / 1e12 / tf32_peak_tflops(), 4)
-        elif c.op == "conv":
-            fma_s = c.n_out * c.w / (avg_ms * 1e-3)
+        elif c.op in ("conv", "conv_bwd_in", "conv_bwd_f"):
+            fma_s = c.flops / 2 / (avg_ms * 1e-3)
             d["fma_frac"] = round(fma_s / FP32_FMA_PEAK, 4)
         cells.append(d)
     tot_k = sum(d["avg_ms"] for d in cells)
@@ -543,8 +635,8 @@ def run_ours(args):
         d["share"] = round(d["avg_ms"] / tot_k, 4)
     dom = max(cells, key=lambda d: d["avg_ms"])
     dom_cell = next(c for c in R.cells if c.name == dom["cell"])
-    if dom_cell.op == "conv" and dom.get("fma_frac", 0) > dom["frac_hbm"]:
-        achieved = dom_cell.n_out * dom_cell.w * 2 / (dom["avg_ms"] * 1e-3) / 1e12
+    if dom_cell.op in ("conv", "conv_bwd_in", "conv_bwd_f") and dom.get("fma_frac", 0) > dom["frac_hbm"]:
+        achieved = dom_cell.flops / (dom["avg_ms"] * 1e-3) / 1e12
         roofline = {"bound": "alu", "kernel": dom["cell"], "achieved": round(achieved, 2),
                     "peak": round(2 * FP32_FMA_PEAK / 1e12, 2), "unit": "TFLOP/s",
                     "frac": round(achieved / (2 * FP32_FMA_PEAK / 1e12), 4),
@@ -654,6 +746,32 @@ def oracle_sample_plan(workload: str, frac: float):
                 rows = 1
             x = synth.normal(3, rows * n).reshape(rows, n)
             plan.append((c, lambda x=x, c=c: (oracle.conv1d(x, c.f), x.shape[0] * (x.shape[1] - c.w + 1))[1]))
+        elif c.cfg == "backward" and c.op == "pool2d_bwd":
+            planes = max(1, int(round(32 * 64 * frac)))
+            oh = (112 - c.kh) // c.sh + 1
+            x = synth.uniform01(5, planes * 112 * 112).reshape(planes, 112, 112)
+            g = synth.normal(34, planes * oh * oh).reshape(planes, oh, oh)
+            m = oracle.POOL2D_MAX if c.mode == "max" else oracle.POOL2D_AVG
+            plan.append((c, lambda x=x, g=g, c=c, m=m: (oracle.pool2d_backward(x, g, 112, 112, c.kh, c.kw, c.sh,
+                                                                               c.sw, m), x.size)[1]))
+        elif c.cfg == "backward":
+            rows = max(1, int(round(64 * frac)))
+            n = 1 << 20
+            if rows * n > 64 * n * frac * 1.5:  # frac below one row: shorten the row instead
+                n = max(c.w + 1, int(64 * (1 << 20) * frac))
+                rows = 1
+            L = n - c.w + 1
+            x = synth.normal(3, rows * n).reshape(rows, n)
+            g = synth.normal(33, rows * L).reshape(rows, L)
+            if c.op == "conv_bwd_in":
+                fn = (lambda g=g, c=c, n=n: (oracle.conv1d_backward_input(g, c.f, n), g.shape[0] * n)[1])
+            elif c.op == "conv_bwd_f":
+                fn = (lambda x=x, g=g, c=c: (oracle.conv1d_backward_filter(x, g, c.w), g.size)[1])
+            elif c.op == "sum_bwd":
+                fn = (lambda g=g, c=c, n=n: (oracle.pool_sum_backward(g, n, c.w), g.shape[0] * n)[1])
+            else:
+                fn = (lambda x=x, g=g, c=c: (oracle.pool_max_backward(x, g, c.w), x.size)[1])
+            plan.append((c, fn))
         elif c.cfg == "affine":
             n = max(c.w, int(8 * (1 << 24) * frac))
             u = synth.uab(31, n, 0.5, 1.0)
@@ -726,7 +844,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="suite", choices=["suite", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "stride", "winspec", "affine"])
+    ap.add_argument("--workload", default="suite", choices=["suite", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "stride", "winspec", "affine", "backward"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)

@@ -195,8 +195,8 @@ ss_status_t ss_affine_window(const float* u, const float* v, float* U, float* V,
  *                          x = the forward input.  SS_F32 only.
  *   ss_conv1d_backward_input   dx_t = sum_{(i,j): i*s+j = t} f_j dy_i.  SS_F32.
  *   ss_conv1d_backward_filter  df_j = sum_b sum_i dy[b][i] x[b][i*s+j]  (df: DEVICE,
- *                          k floats; fp32 products summed in fp32 runs of 16, then
- *                          fp64; stride <= 64).  `workspace` (DEVICE, caller-owned,
+ *                          k floats; fp32 products summed in fp32 runs of 64, then
+ *                          fp64).  `workspace` (DEVICE, caller-owned,
  *                          >= ss_conv1d_backward_filter_workspace(k) bytes on the
  *                          current device) holds per-CTA fp64 partials.
  *   ss_pool2d_backward     [planes][H][W] gradient of ss_pool2d: avg spreads

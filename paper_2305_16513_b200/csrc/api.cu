@@ -466,8 +466,7 @@ static ss_status_t conv1d_backward_filter_impl(const void* x, const void* dy, fl
   ss_status_t st = validate_bwd(x, dy, df, N, batch, k, stride, "k", &L);
   if (st != SS_OK) return st;
   if (k > SS_K_MAX) return fail(SS_ERR_UNSUPPORTED, "k=%lld > SS_K_MAX=%d", (long long)k, SS_K_MAX);
-  if (stride > 64) return fail(SS_ERR_UNSUPPORTED, "filter gradient supports stride <= 64");
-  const int ctas = current_sms();
+  const int ctas = conv_filter_grad_ctas(current_sms());
   const size_t need = conv_filter_grad_workspace(k, ctas);
   if (!workspace || ws_bytes < need)
     return fail(SS_ERR_BAD_SIZE, "workspace of %zu bytes needed (ss_conv1d_backward_filter_workspace)", need);
@@ -484,7 +483,7 @@ static ss_status_t conv1d_backward_filter_impl(const void* x, const void* dy, fl
 
 static size_t conv1d_backward_filter_workspace_impl(int64_t k) {
   if (k < 1 || k > SS_K_MAX) return 0;
-  return conv_filter_grad_workspace(k, current_sms());
+  return conv_filter_grad_workspace(k, conv_filter_grad_ctas(current_sms()));
 }
 
 static ss_status_t pool2d_backward_impl(const void* x, const void* dy, void* dx, int64_t planes, int64_t H, int64_t W,

@@ -61,12 +61,109 @@ __global__ void __launch_bounds__(kBwThreads) transpose_window_kernel(const __gr
 }
 
 // ---------------------------------------------------------------- max pooling
-// CTA tile: kMaxTile input positions of one row.  The windows that can route a
-// gradient into the tile form a contiguous range; they are processed in
-// chunks of kMaxChunk: argmax (first maximum) of each window into shared
-// memory, then every position gathers the dy of the chunk's windows whose
-// argmax it is, in increasing window order.
+// Tile kernel (w <= kMaxTileW, stride <= kMaxTileS): kMaxTile positions of one
+// row.  (1) Stage the x span of every window touching the tile.  (2) First
+// maximum of every such window in O(1) from block-wise prefix / suffix
+// argmax scans (blocks of w aligned at the span start; Alg. 2's prefix/suffix
+// split, on (value, index) pairs: the earlier index wins ties, so
+// suffix scans replace on >=, prefix scans on >).  (3) The window argmax a_i
+// is non-decreasing in i (an element dropped from a window was not after its
+// first maximum), so the windows routed to a position form one contiguous
+// run: the thread of each run's first window sums its dy in increasing order
+// into the staged dx tile (zero elsewhere), which is then stored coalesced.
 constexpr int kMaxTile = 1024;
+constexpr int kMaxTileW = 1024;
+constexpr int kMaxTileS = 64;
+constexpr int kMaxSpan = kMaxTile + 2 * kMaxTileW + kMaxTileS;  // x elements staged per tile (bound)
+constexpr int kMaxWin = kMaxTile + kMaxTileW + 2;               // windows per tile (bound)
+// shared arrays indexed by the padded position of span element e: block e / w
+// at pitch w | 1 (odd), so the lanes of a warp scanning consecutive blocks hit
+// distinct banks
+constexpr int kMaxSpanPad = kMaxSpan + kMaxSpan / 2 + 2;
+constexpr size_t kMaxTileSmem = (size_t)kMaxSpanPad * (4 + 4 + 4) + (size_t)kMaxWin * (4 + 4) + kMaxTile * 4;
+
+__global__ void __launch_bounds__(kBwThreads) pool_max_backward_tile_kernel(const __grid_constant__ BackwardParams p) {
+  extern __shared__ __align__(16) float mb_smem[];
+  float* xs = mb_smem;                                        // [kMaxSpanPad], padded positions
+  int* S = reinterpret_cast<int*>(xs + kMaxSpanPad);          // suffix argmax (span-relative, unpadded)
+  int* P = S + kMaxSpanPad;                                   // prefix argmax
+  int* A = P + kMaxSpan;                                      // window argmax [kMaxWin]
+  float* gs = reinterpret_cast<float*>(A + kMaxWin);          // dy of the tile's windows
+  float* dxs = gs + kMaxWin;                                  // dx tile [kMaxTile]
+  const float* __restrict__ x = static_cast<const float*>(p.x);
+  const float* __restrict__ dy = static_cast<const float*>(p.dy);
+  float* __restrict__ dx = static_cast<float*>(p.dx);
+  const int w = (int)p.w, s = (int)p.stride;
+  const int pitch = w | 1;
+  auto pad = [&](int e) { const int q = e / w; return q * pitch + (e - q * w); };
+  const int64_t tiles_per_row = (p.N + kMaxTile - 1) / kMaxTile;
+  const int64_t ntiles = p.batch * tiles_per_row;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t b = tile / tiles_per_row;
+    const int64_t t0 = (tile - b * tiles_per_row) * kMaxTile;
+    const int nt = (int)(t0 + kMaxTile < p.N ? kMaxTile : p.N - t0);
+    const int64_t wlo = first_window(t0, p.w, p.stride);
+    int64_t whi = (t0 + nt - 1) / p.stride;
+    if (whi > p.L - 1) whi = p.L - 1;
+    const int nwin = whi >= wlo ? (int)(whi - wlo + 1) : 0;
+    const int64_t xa = wlo * p.stride;
+    const int span = nwin ? (int)((whi - wlo) * s + w) : 0;
+    const float* __restrict__ xr = x + b * p.N;
+    const float* __restrict__ gr = dy + b * p.L;
+    __syncthreads();  // previous tile's readers are done
+    for (int e = threadIdx.x; e < span; e += kBwThreads) xs[pad(e)] = __ldg(xr + xa + e);
+    for (int e = threadIdx.x; e < nwin; e += kBwThreads) gs[e] = __ldg(gr + wlo + e);
+    for (int e = threadIdx.x; e < nt; e += kBwThreads) dxs[e] = 0.0f;
+    __syncthreads();
+    // (2a) block-wise prefix / suffix argmax, one block of w per thread
+    const int nb = (span + w - 1) / w;
+    for (int blk = threadIdx.x; blk < nb; blk += kBwThreads) {
+      const int lo = blk * w, n = min(lo + w, span) - lo, base = blk * pitch;
+      int best = 0;
+      float bv = xs[base];
+      P[base] = lo;
+      for (int u = 1; u < n; ++u) {
+        const float v = xs[base + u];
+        if (v > bv) { bv = v; best = u; }
+        P[base + u] = lo + best;
+      }
+      best = n - 1;
+      bv = xs[base + n - 1];
+      S[base + n - 1] = lo + n - 1;
+      for (int u = n - 2; u >= 0; --u) {
+        const float v = xs[base + u];
+        if (v >= bv) { bv = v; best = u; }
+        S[base + u] = lo + best;
+      }
+    }
+    __syncthreads();
+    // (2b) first maximum of each window [u, u + w - 1], u = (i - wlo) s
+    for (int j = threadIdx.x; j < nwin; j += kBwThreads) {
+      const int u = j * s;
+      int a = S[pad(u)];
+      if (u % w) {
+        const int a2 = P[pad(u + w - 1)];
+        if (xs[pad(a2)] > xs[pad(a)]) a = a2;
+      }
+      A[j] = a;
+    }
+    __syncthreads();
+    // (3) run sums, written by each run's first window
+    for (int j = threadIdx.x; j < nwin; j += kBwThreads) {
+      const int a = A[j];
+      const int64_t t = xa + a;
+      if (t < t0 || t >= t0 + nt || (j > 0 && A[j - 1] == a)) continue;
+      float acc = 0.0f;
+      for (int jj = j; jj < nwin && A[jj] == a; ++jj) acc = __fadd_rn(acc, gs[jj]);
+      dxs[t - t0] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nt; e += kBwThreads) dx[b * p.N + t0 + e] = dxs[e];
+  }
+}
+
+// Fallback for w > kMaxTileW: windows in chunks, argmax of each recomputed from
+// global memory, then each position gathers the chunk's windows routed to it.
 constexpr int kMaxChunk = 1024;
 
 __global__ void __launch_bounds__(kBwThreads) pool_max_backward_kernel(const __grid_constant__ BackwardParams p) {
@@ -125,28 +222,40 @@ __global__ void __launch_bounds__(kBwThreads) pool_max_backward_kernel(const __g
 }
 
 // ---------------------------------------------------------------- conv filter gradient
-// Pass 1: grid (ctas, tap blocks of 64).  Tile = kFgTile consecutive outputs i
-// of one row; the CTA's 256 threads are 4 tap groups (16 taps) x 64 run slots
-// (16 outputs).  Per tile a thread adds dy_i x_{is+j} over its 16 x 16 block
-// in fp32 (stride 1: the 31 inputs it needs sit in registers), then folds the
-// 16 partial sums into fp64 accumulators; at the end the 64 run slots of each
-// tap group are reduced in fixed order and the CTA writes 64 fp64 partials.
-// Pass 2 sums the CTA partials in fixed order.  Shared-memory x / dy are padded
-// by 4 floats per 16 so the LDS.128 of 8 consecutive run slots hit distinct
-// bank groups.
+// Unit stride (the common case): grid (ctas, tap blocks of 64).  Tile =
+// kFgTile consecutive outputs i of one row; the CTA's 256 threads are 4 tap
+// groups (16 taps) x 64 run slots (16 outputs).  Per tile a thread adds
+// dy_i x_{i+j} over its 16 x 16 block in fp32 with the 31 inputs it needs in
+// registers, then folds the 16 partial sums into fp64 accumulators; at the end
+// the 64 run slots of each tap group are reduced in fixed order and the CTA
+// writes 64 fp64 partials.  Tiles stream through a kFgStages-deep ring of
+// shared-memory stages filled with 4-B cp.async (rows have any alignment),
+// padded by 4 floats per 16 so the LDS.128 of 8 consecutive run slots hit
+// distinct bank groups.
+// Strided: grid (ctas, k); each CTA sums dy_i x_{is+j} for one tap over a
+// grid-strided share of the outputs (fp32 runs of 16, then fp64).
+// Finish: sums the CTA partials of each tap in fixed order.
 constexpr int kFgTaps = 64;
 constexpr int kFgRun = 16;
 constexpr int kFgSlots = 64;
 constexpr int kFgTile = kFgRun * kFgSlots;  // 1024 outputs
-__device__ __forceinline__ int fg_pad(int e) { return e + 4 * (e >> 4); }
+constexpr int kFgStages = 4;
+constexpr int kFgFold = 4;  // tiles accumulated in fp32 (64 terms per partial) before folding into fp64
+constexpr int kFgXSpan = kFgTile + kFgTaps;  // inputs one tile needs (unit stride)
+__host__ __device__ constexpr int fg_pad(int e) { return e + 4 * (e >> 4); }
+constexpr int kFgXStride = (fg_pad(kFgXSpan) + 16) & ~3;          // padded x floats per stage
+constexpr int kFgStageFloats = kFgXStride + fg_pad(kFgTile);       // + padded dy
+constexpr size_t kFgSmem = (size_t)kFgStages * kFgStageFloats * sizeof(float);
 
-template <bool kUnitStride>
-__global__ void __launch_bounds__(kBwThreads) conv_filter_grad_kernel(const __grid_constant__ BackwardParams p,
-                                                                      double* __restrict__ partials) {
+// Unit-stride filter gradient.  Inner product per thread and tile: 16 outputs
+// m x 16 taps jj, acc[jj] += dy_m x_{m+jj}, as FFMA2 over tap pairs
+// (acc[jj], acc[jj+1]) += dy_m * (x_{m+jj}, x_{m+jj+1}); the input window is
+// kept twice (pairs starting at even and at odd offsets) so every pair is an
+// aligned register pair.  x / dy rows that are 16-B aligned stream with 16-B
+// cp.async, others with 4-B cp.async.
+__global__ void __launch_bounds__(kBwThreads, 2) conv_filter_grad_kernel(const __grid_constant__ BackwardParams p,
+                                                                         double* __restrict__ partials) {
   extern __shared__ __align__(16) float fg_smem[];
-  const int xspan = kUnitStride ? kFgTile + kFgTaps : (int)((kFgTile - 1) * p.stride + kFgTaps);
-  float* xs = fg_smem;                      // fg_pad(xspan) floats
-  float* gs = fg_smem + ((fg_pad(xspan) + 16) & ~3);  // fg_pad(kFgTile) floats, 16-B aligned
   double* red = reinterpret_cast<double*>(fg_smem);  // reused for the final reduction
   const float* __restrict__ x = static_cast<const float*>(p.x);
   const float* __restrict__ dy = static_cast<const float*>(p.dy);
@@ -154,60 +263,100 @@ __global__ void __launch_bounds__(kBwThreads) conv_filter_grad_kernel(const __gr
   const int q = threadIdx.x & 3, r = threadIdx.x >> 2;  // tap group, run slot
   const int64_t tiles_per_row = (p.L + kFgTile - 1) / kFgTile;
   const int64_t ntiles = p.batch * tiles_per_row;
+  // issue the cp.async copies of tile `tile` into stage `st` (one commit group per tile)
+  auto issue = [&](int64_t tile, int st) {
+    if (tile < ntiles) {
+      float* xs = fg_smem + st * kFgStageFloats;
+      float* gs = xs + kFgXStride;
+      const int64_t b = tile / tiles_per_row;
+      const int64_t i0 = (tile - b * tiles_per_row) * kFgTile;
+      const int64_t nout = p.L - i0 < kFgTile ? p.L - i0 : kFgTile;
+      const float* __restrict__ xr = x + b * p.N + i0 + j0;
+      const int64_t xlim = p.N - i0 - j0;  // elements of the row from xr on
+      const float* __restrict__ gr = dy + b * p.L + i0;
+      if (((reinterpret_cast<uintptr_t>(xr) | reinterpret_cast<uintptr_t>(gr)) & 15) == 0) {
+        for (int e = 4 * threadIdx.x; e < kFgXSpan; e += 4 * kBwThreads) {
+          const int64_t left = xlim - e;
+          const uint32_t nb = left >= 4 ? 16u : (left > 0 ? 4u * (uint32_t)left : 0u);
+          cp_async16(smem_u32(xs + fg_pad(e)), nb ? xr + e : x, nb);
+        }
+        for (int e = 4 * threadIdx.x; e < kFgTile; e += 4 * kBwThreads) {
+          const int64_t left = nout - e;
+          const uint32_t nb = left >= 4 ? 16u : (left > 0 ? 4u * (uint32_t)left : 0u);
+          cp_async16(smem_u32(gs + fg_pad(e)), nb ? gr + e : dy, nb);
+        }
+      } else {
+        for (int e = threadIdx.x; e < kFgXSpan; e += kBwThreads)
+          cp_async4(smem_u32(xs + fg_pad(e)), e < xlim ? xr + e : x, e < xlim ? 4u : 0u);
+        for (int e = threadIdx.x; e < kFgTile; e += kBwThreads)
+          cp_async4(smem_u32(gs + fg_pad(e)), e < nout ? gr + e : dy, e < nout ? 4u : 0u);
+      }
+    }
+    cp_async_commit();
+  };
+  int64_t tile = blockIdx.x;
+#pragma unroll 1
+  for (int st = 0; st < kFgStages - 1; ++st) issue(tile + (int64_t)st * gridDim.x, st);
   double acc64[16];
 #pragma unroll
   for (int jj = 0; jj < 16; ++jj) acc64[jj] = 0.0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t b = tile / tiles_per_row;
-    const int64_t i0 = (tile - b * tiles_per_row) * kFgTile;
-    const int64_t nout = p.L - i0 < kFgTile ? p.L - i0 : kFgTile;
-    const float* __restrict__ xr = x + b * p.N;
-    const int64_t xbase = i0 * p.stride + j0;
-    __syncthreads();
-    for (int e = threadIdx.x; e < xspan; e += kBwThreads) {
-      const int64_t t = xbase + e;
-      xs[fg_pad(e)] = t < p.N ? __ldg(xr + t) : 0.0f;
-    }
-    for (int e = threadIdx.x; e < kFgTile; e += kBwThreads)
-      gs[fg_pad(e)] = e < nout ? __ldg(dy + b * p.L + i0 + e) : 0.0f;
-    __syncthreads();
+  float2 acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = make_float2(0.0f, 0.0f);
+  int st = 0, nfold = 0;
+  for (; tile < ntiles; tile += gridDim.x) {
+    issue(tile + (int64_t)(kFgStages - 1) * gridDim.x, (st + kFgStages - 1) % kFgStages);
+    cp_async_wait<kFgStages - 1>();  // this tile's group has landed (for this thread)
+    __syncthreads();                 // ... and for every thread
+    const float* xs = fg_smem + st * kFgStageFloats;
+    const float* gs = xs + kFgXStride;
     const int m0 = kFgRun * r;
-    if (m0 >= nout) continue;
-    float g[kFgRun];
+    // window x[m0 + 16q + (0..31)] as even-start pairs E[i] = (x_{2i}, x_{2i+1}) and
+    // odd-start pairs O[i] = (x_{2i+1}, x_{2i+2})
+    float2 E[16], O[16];
+    const int base = m0 + 16 * q;
+#pragma unroll
+    for (int c = 0; c < 32; c += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(xs + fg_pad(base + c));
+      E[c / 2] = make_float2(v.x, v.y);
+      E[c / 2 + 1] = make_float2(v.z, v.w);
+    }
+#pragma unroll
+    for (int i = 0; i < 15; ++i) O[i] = make_float2(E[i].y, E[i + 1].x);
+    O[15] = make_float2(E[15].y, 0.0f);
 #pragma unroll
     for (int m = 0; m < kFgRun; m += 4) {
-      const float4 v = *reinterpret_cast<const float4*>(gs + fg_pad(m0 + m));
-      g[m] = v.x; g[m + 1] = v.y; g[m + 2] = v.z; g[m + 3] = v.w;
-    }
-    float acc[16];
+      const float4 gv = *reinterpret_cast<const float4*>(gs + fg_pad(m0 + m));
+      const float g4[4] = {gv.x, gv.y, gv.z, gv.w};
 #pragma unroll
-    for (int jj = 0; jj < 16; ++jj) acc[jj] = 0.0f;
-    if constexpr (kUnitStride) {
-      // x_{i+j} for i = i0+m0+m, j = j0+16q+jj: window xs[m0 + 16q + (m + jj)], 31 values
-      float xw[32];
-      const int base = m0 + 16 * q;
+      for (int mm = 0; mm < 4; ++mm) {
+        const int mt = m + mm;
+        const float2 g2 = make_float2(g4[mm], g4[mm]);
 #pragma unroll
-      for (int c = 0; c < 32; c += 4) {
-        const float4 v = *reinterpret_cast<const float4*>(xs + fg_pad(base + c));
-        xw[c] = v.x; xw[c + 1] = v.y; xw[c + 2] = v.z; xw[c + 3] = v.w;
-      }
-#pragma unroll
-      for (int m = 0; m < kFgRun; ++m)
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj) acc[jj] = __fmaf_rn(g[m], xw[m + jj], acc[jj]);
-    } else {
-#pragma unroll
-      for (int m = 0; m < kFgRun; ++m) {
-        const int base = (int)((m0 + m) * p.stride) + 16 * q;
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj) acc[jj] = __fmaf_rn(g[m], xs[fg_pad(base + jj)], acc[jj]);
+        for (int i = 0; i < 8; ++i)  // taps 2i, 2i+1: inputs x_{mt+2i}, x_{mt+2i+1}
+          acc[i] = __ffma2_rn((mt & 1) ? O[(mt >> 1) + i] : E[(mt >> 1) + i], g2, acc[i]);
       }
     }
+    if (++nfold == kFgFold) {
+      nfold = 0;
 #pragma unroll
-    for (int jj = 0; jj < 16; ++jj) acc64[jj] += (double)acc[jj];
+      for (int i = 0; i < 8; ++i) {
+        acc64[2 * i] += (double)acc[i].x;
+        acc64[2 * i + 1] += (double)acc[i].y;
+        acc[i] = make_float2(0.0f, 0.0f);
+      }
+    }
+    __syncthreads();  // stage st is refilled by the next iteration's issue
+    st = st + 1 == kFgStages ? 0 : st + 1;
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    acc64[2 * i] += (double)acc[i].x;
+    acc64[2 * i + 1] += (double)acc[i].y;
   }
   // reduce the 64 run slots of each tap group, fixed order
-  __syncthreads();
 #pragma unroll
   for (int jj = 0; jj < 16; ++jj) red[(16 * q + jj) * kFgSlots + r] = acc64[jj];
   __syncthreads();
@@ -218,15 +367,45 @@ __global__ void __launch_bounds__(kBwThreads) conv_filter_grad_kernel(const __gr
   }
 }
 
-__global__ void conv_filter_grad_finish(const double* __restrict__ partials, int ctas, int64_t k,
+__global__ void __launch_bounds__(kBwThreads) conv_filter_grad_strided_kernel(const __grid_constant__ BackwardParams p,
+                                                                              double* __restrict__ partials) {
+  __shared__ double red[kBwThreads];
+  const float* __restrict__ x = static_cast<const float*>(p.x);
+  const float* __restrict__ dy = static_cast<const float*>(p.dy);
+  const int64_t j = blockIdx.y;
+  const int64_t total = p.batch * p.L;
+  const int64_t step = (int64_t)gridDim.x * kBwThreads;
+  double acc64 = 0.0;
+  int64_t e = blockIdx.x * (int64_t)kBwThreads + threadIdx.x;
+  while (e < total) {
+    float acc = 0.0f;
+    for (int n = 0; n < 16 && e < total; ++n, e += step) {
+      const int64_t b = e / p.L, i = e - b * p.L;
+      acc = __fmaf_rn(__ldg(dy + e), __ldg(x + b * p.N + i * p.stride + j), acc);
+    }
+    acc64 += (double)acc;
+  }
+  red[threadIdx.x] = acc64;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int t = 0; t < kBwThreads; ++t) s += red[t];
+    partials[j * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+__global__ void conv_filter_grad_finish(const double* __restrict__ partials, int ctas, int64_t k, int strided,
                                         float* __restrict__ df) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= k) return;
   const int64_t blk = j / kFgTaps, jj = j - blk * kFgTaps;
   double s = 0.0;
-  for (int c = 0; c < ctas; ++c) s += partials[(blk * ctas + c) * kFgTaps + jj];
+  for (int c = 0; c < ctas; ++c)
+    s += strided ? partials[j * ctas + c] : partials[(blk * ctas + c) * kFgTaps + jj];
   df[j] = (float)s;
 }
+
+int conv_filter_grad_ctas(int sms) { return 2 * sms; }
 
 size_t conv_filter_grad_workspace(int64_t k, int ctas) {
   return (size_t)((k + kFgTaps - 1) / kFgTaps) * ctas * kFgTaps * sizeof(double);
@@ -234,25 +413,19 @@ size_t conv_filter_grad_workspace(int64_t k, int ctas) {
 
 cudaError_t launch_conv_filter_grad(const BackwardParams& p, float* df, void* workspace, int ctas,
                                     cudaStream_t stream) {
-  const int tap_blocks = (int)((p.w + kFgTaps - 1) / kFgTaps);
-  const int xspan = p.stride == 1 ? kFgTile + kFgTaps : (int)((kFgTile - 1) * p.stride + kFgTaps);
-  size_t smem = (size_t)(((xspan + 4 * (xspan >> 4) + 16) & ~3) + kFgTile + 4 * (kFgTile >> 4)) * sizeof(float);
-  const size_t red = (size_t)kFgTaps * kFgSlots * sizeof(double);
-  if (smem < red) smem = red;
-  if (smem > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
   double* part = static_cast<double*>(workspace);
-  const dim3 grid((unsigned)ctas, (unsigned)tap_blocks);
-  if (p.stride == 1) {
-    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(conv_filter_grad_kernel<true>));
+  const bool strided = p.stride != 1;
+  if (!strided) {
+    static_assert(kFgSmem >= (size_t)kFgTaps * kFgSlots * sizeof(double), "reduction fits the stages");
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(conv_filter_grad_kernel));
     if (e != cudaSuccess) return e;
-    conv_filter_grad_kernel<true><<<grid, kBwThreads, smem, stream>>>(p, part);
+    const int tap_blocks = (int)((p.w + kFgTaps - 1) / kFgTaps);
+    conv_filter_grad_kernel<<<dim3((unsigned)ctas, (unsigned)tap_blocks), kBwThreads, kFgSmem, stream>>>(p, part);
   } else {
-    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(conv_filter_grad_kernel<false>));
-    if (e != cudaSuccess) return e;
-    conv_filter_grad_kernel<false><<<grid, kBwThreads, smem, stream>>>(p, part);
+    conv_filter_grad_strided_kernel<<<dim3((unsigned)ctas, (unsigned)p.w), kBwThreads, 0, stream>>>(p, part);
   }
   note_launch();
-  conv_filter_grad_finish<<<(unsigned)((p.w + 127) / 128), 128, 0, stream>>>(part, ctas, p.w, df);
+  conv_filter_grad_finish<<<(unsigned)((p.w + 127) / 128), 128, 0, stream>>>(part, ctas, p.w, strided ? 1 : 0, df);
   note_launch();
   return cudaGetLastError();
 }
@@ -292,6 +465,65 @@ __global__ void __launch_bounds__(kBwThreads) pool2d_backward_kernel(const __gri
   }
 }
 
+// Plane kernel (32-bit index math; max: each window's first maximum computed
+// once into shared memory, then every position gathers the windows routed to
+// it).  One CTA per plane (grid-strided), used when a plane's window table
+// fits shared memory.
+__device__ __forceinline__ int div_small(int a, int d) { return d == 1 ? a : (d == 2 ? a >> 1 : a / d); }
+
+template <bool kAvg, int KH = 0, int KW = 0>
+__global__ void __launch_bounds__(512) pool2d_backward_plane_kernel(const __grid_constant__ Pool2DBackwardParams p) {
+  extern __shared__ __align__(16) float s_plane[];
+  const int H = (int)p.H, W = (int)p.W, OH = (int)p.OH, OW = (int)p.OW;
+  const int kh = KH ? KH : (int)p.kh, kw = KW ? KW : (int)p.kw, sh = (int)p.sh, sw = (int)p.sw;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  float* g = s_plane;                                  // dy plane [OH][OW]
+  int* s_arg2 = reinterpret_cast<int*>(s_plane + OH * OW);  // max: window argmax [OH][OW]
+  for (int64_t pl = blockIdx.x; pl < p.planes; pl += gridDim.x) {
+    const float* __restrict__ xp = p.x + pl * H * W;
+    const float* __restrict__ gp = p.dy + pl * OH * OW;
+    float* __restrict__ d = p.dx + pl * H * W;
+    __syncthreads();  // previous plane's readers are done
+    for (int e = threadIdx.x; e < OH * OW; e += blockDim.x) g[e] = __ldg(gp + e);
+    if constexpr (kAvg) {
+      __syncthreads();
+    } else {
+      for (int r = warp; r < OH; r += nwarps)
+        for (int c = lane; c < OW; c += 32) {
+          const float* xw = xp + r * sh * W + c * sw;
+          float m = __ldg(xw);
+          int best = r * sh * W + c * sw;
+#pragma unroll
+          for (int a = 0; a < (KH ? KH : 64); ++a) {
+            if (!KH && a >= kh) break;
+#pragma unroll
+            for (int bb = 0; bb < (KW ? KW : 64); ++bb) {
+              if (!KW && bb >= kw) break;
+              const float v = __ldg(xw + a * W + bb);
+              if (v > m) { m = v; best = (r * sh + a) * W + c * sw + bb; }
+            }
+          }
+          s_arg2[r * OW + c] = best;
+        }
+      __syncthreads();
+    }
+    for (int h = warp; h < H; h += nwarps) {
+      const int r0 = h - kh + 1 <= 0 ? 0 : div_small(h - kh + sh, sh), r1 = min(div_small(h, sh), OH - 1);
+      for (int c = lane; c < W; c += 32) {
+        const int c0 = c - kw + 1 <= 0 ? 0 : div_small(c - kw + sw, sw), c1 = min(div_small(c, sw), OW - 1);
+        const int e = h * W + c;
+        float acc = 0.0f;
+        for (int r = r0; r <= r1; ++r)
+          for (int cc = c0; cc <= c1; ++cc) {
+            if constexpr (kAvg) acc = __fadd_rn(acc, g[r * OW + cc]);
+            else if (s_arg2[r * OW + cc] == e) acc = __fadd_rn(acc, g[r * OW + cc]);
+          }
+        d[e] = kAvg ? __fmul_rn(acc, p.inv_area) : acc;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- launches
 static unsigned grid_elems(int64_t total, int sms) {
   int64_t g = (total + kBwThreads - 1) / kBwThreads;
@@ -313,12 +545,36 @@ cudaError_t launch_pool_max_backward(const BackwardParams& p, cudaStream_t strea
   const int64_t tiles = p.batch * ((p.N + kMaxTile - 1) / kMaxTile);
   const int64_t cap = (int64_t)sms * 8;
   const unsigned g = (unsigned)(tiles < cap ? tiles : cap);
-  pool_max_backward_kernel<<<g < 1 ? 1 : g, kBwThreads, 0, stream>>>(p);
+  if (p.w <= kMaxTileW && p.stride <= kMaxTileS) {
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(pool_max_backward_tile_kernel));
+    if (e != cudaSuccess) return e;
+    pool_max_backward_tile_kernel<<<g < 1 ? 1 : g, kBwThreads, kMaxTileSmem, stream>>>(p);
+  } else {
+    pool_max_backward_kernel<<<g < 1 ? 1 : g, kBwThreads, 0, stream>>>(p);
+  }
   note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_pool2d_backward(const Pool2DBackwardParams& p, cudaStream_t stream, int sms) {
+  const size_t table = (size_t)p.OH * p.OW * sizeof(float) * (p.mode == 1 ? 1 : 2);  // dy (+ argmax)
+  if (p.H * p.W < (int64_t(1) << 30) && table <= (size_t)kSmemBudget) {
+    const int64_t gp = p.planes < (int64_t)sms * 4 ? p.planes : (int64_t)sms * 4;
+    if (p.mode == 1) {
+      cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(pool2d_backward_plane_kernel<true>));
+      if (e != cudaSuccess) return e;
+      pool2d_backward_plane_kernel<true><<<(unsigned)gp, 512, table, stream>>>(p);
+    } else {
+      auto kfn = pool2d_backward_plane_kernel<false>;
+      if (p.kh == 3 && p.kw == 3) kfn = pool2d_backward_plane_kernel<false, 3, 3>;
+      else if (p.kh == 2 && p.kw == 2) kfn = pool2d_backward_plane_kernel<false, 2, 2>;
+      cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
+      if (e != cudaSuccess) return e;
+      kfn<<<(unsigned)gp, 512, table, stream>>>(p);
+    }
+    note_launch();
+    return cudaGetLastError();
+  }
   const unsigned g = grid_elems(p.planes * p.H * p.W, sms);
   if (p.mode == 1) pool2d_backward_kernel<true><<<g, kBwThreads, 0, stream>>>(p);
   else pool2d_backward_kernel<false><<<g, kBwThreads, 0, stream>>>(p);

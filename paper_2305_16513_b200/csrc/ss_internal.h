@@ -138,6 +138,7 @@ struct Pool2DBackwardParams {
 };
 cudaError_t launch_transpose_window(const BackwardParams& p, int op, int dtype, cudaStream_t stream, int sms);
 cudaError_t launch_pool_max_backward(const BackwardParams& p, cudaStream_t stream, int sms);
+int conv_filter_grad_ctas(int sms);
 size_t conv_filter_grad_workspace(int64_t k, int ctas);
 cudaError_t launch_conv_filter_grad(const BackwardParams& p, float* df, void* workspace, int ctas,
                                     cudaStream_t stream);
