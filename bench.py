@@ -61,9 +61,13 @@ BWD_OPS = ("conv_bwd_in", "conv_bwd_f", "sum_bwd", "max_bwd", "pool2d_bwd")
 
 
 def conv_on_tensor_cores(c) -> bool:
-    # forward conv, and the stride-1 input gradient (forward kernels on padded dy)
-    return (c.op in ("conv", "conv_bwd_in") and TC_CONV_K[0] <= c.w <= TC_CONV_K[1] and c.stride == 1
-            and c.dilation == 1)
+    # forward conv, and the stride-1 input gradient (forward kernels on padded dy); dilated
+    # filters whose extent (k-1)d+1 <= 64 also run on the tensor cores
+    if c.op not in ("conv", "conv_bwd_in") or c.stride != 1:
+        return False
+    if c.dilation == 1:
+        return TC_CONV_K[0] <= c.w <= TC_CONV_K[1]
+    return (c.w - 1) * c.dilation + 1 <= TC_CONV_K[1]
 
 
 def tf32_peak_tflops():

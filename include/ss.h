@@ -104,10 +104,11 @@ ss_status_t ss_pool_max(const void* x, void* y, int64_t N, int64_t batch,
  * l.86-87, Sec. 2.5; Eq. 4 per window), cross-correlation orientation
  * (reading R2): y[b][i] = sum_{j<k} filter[j] * x[b][i*stride + j].
  * Accumulation (fp32):
- *   k <= 32, or any stride / dilation: fl(S_even + S_odd), S_even / S_odd FMA
+ *   otherwise (k <= 32, strides > 1, longer dilated extents): fl(S_even + S_odd), S_even / S_odd FMA
  *     chains over the even / odd taps in increasing j from 0 -- fixed by the
  *     tap index alone, so every output is independent of tiling and sharding.
- *   33 <= k <= 64 at stride 1 (dilation 1): tensor cores (Toeplitz matrix
+ *   33 <= k <= 64 at stride 1, and (conv1d_ex) dilated filters with
+ *     (k-1)*dilation + 1 <= 64 at stride 1: tensor cores (Toeplitz matrix
  *     product), 3xTF32 (x f ~ xh fh + xh fl + xl fh) with fp32
  *     accumulation; within the bound below with >10x margin, bitwise
  *     deterministic run to run, but an output's rounding depends on its

@@ -152,10 +152,10 @@ static int tc_nc() {
 // Try the tensor-core conv for the interior outputs of every row (y_int =
 // first interior output of row 0, rows y_pitch apart).  false: not applicable.
 static bool try_conv_tc(const void* x, float* y_int, int64_t N, int64_t batch, int64_t k, int64_t y_pitch,
-                        const float* taps, cudaStream_t s, int grid, cudaError_t* err) {
+                        const float* taps, cudaStream_t s, int grid, cudaError_t* err, bool any_k = false) {
   *err = cudaSuccess;
   const int mk = tc_min_k();
-  if (mk <= 0 || k < mk || k > kConvTcMaxK) return false;
+  if (mk <= 0 || (!any_k && k < mk) || k > kConvTcMaxK) return false;
   const uintptr_t xa = reinterpret_cast<uintptr_t>(x);
   if (xa & 3) return false;
   ConvTCParams p;
@@ -288,11 +288,21 @@ static ss_status_t window_impl(int op, const void* x, void* y, int64_t N, int64_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int grid = current_sms();
   const int dt = dtype == SS_I32 ? 1 : 0;
-  const int64_t L_int = N - w + 1;  // outputs whose window is inside the row (stride 1, d 1)
+  const int64_t E = (w - 1) * d + 1;  // window extent
+  const int64_t L_int = N - E + 1;     // outputs whose window is inside the row (stride 1)
   bool interior_done = false;
-  if (stride == 1 && d == 1 && L_int >= 1 && op == kOpConv) {
+  if (stride == 1 && L_int >= 1 && op == kOpConv && E <= kConvTcMaxK) {
+    // tensor cores: k >= the threshold, or any dilated filter whose extent fits (the
+    // Toeplitz of the zero-expanded filter f_e[j d] = f_j)
+    float expanded[kConvTcMaxK];
+    const float* tt = taps;
+    if (d > 1) {
+      for (int64_t t = 0; t < E; ++t) expanded[t] = 0.0f;
+      for (int64_t j = 0; j < w; ++j) expanded[j * d] = taps[j];
+      tt = expanded;
+    }
     cudaError_t e;
-    if (try_conv_tc(x, static_cast<float*>(y) + pl, N, batch, w, L, taps, s, grid, &e)) {
+    if (try_conv_tc(x, static_cast<float*>(y) + pl, N, batch, E, L, tt, s, grid, &e, d > 1)) {
       if (e != cudaSuccess) return cuda_fail(e, "tensor-core conv launch");
       interior_done = true;
     }

@@ -124,3 +124,18 @@ def test_tc_conv_forced_small_k():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "parity ok" in r.stdout
+
+
+@pytest.mark.parametrize("k,d,pad", [(7, 4, 12), (5, 2, 0), (2, 63, 0), (16, 4, 30), (3, 7, 7)])
+def test_tc_conv_dilated(ss, k, d, pad):
+    # dilated filters with extent (k-1)d+1 <= 64 run on the tensor cores as the
+    # zero-expanded filter (SURVEY 8f NEXT #1 x #2)
+    B, N = 3, 30011
+    x = synth.normal(41, B * N).reshape(B, N)
+    f = synth.normal(42, k, sigma=synth.cfg_sigma_filter(k))
+    xd = torch.from_numpy(x).cuda()
+    n0 = tc_launches(ss)
+    y = ss.conv1d(xd, f, dilation=d, padding=pad).cpu().numpy()
+    assert tc_launches(ss) - n0 == 1
+    ref, mag = oracle.conv1d_ex(x, f, 1, d, pad, pad)
+    check(y, ref, mag, f"dilated k={k} d={d} pad={pad}")
