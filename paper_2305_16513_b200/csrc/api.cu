@@ -113,7 +113,7 @@ bool encode_chunk_map(CUtensorMap* m, const void* base, int64_t m_ext, int atoms
   if (!enc || m_ext < 1 || m_ext > (int64_t(1) << 31) - 1024) return false;
   cuuint64_t dims[3] = {32, (cuuint64_t)m_ext, (cuuint64_t)atoms};
   cuuint64_t strides[2] = {512, 128};
-  cuuint32_t box[3] = {32, (cuuint32_t)nc, 3};  // one group of 3 K-atoms per load
+  cuuint32_t box[3] = {32, (cuuint32_t)nc, (cuuint32_t)(nc == 128 ? 2 : 3)};  // one group of K-atoms per load
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

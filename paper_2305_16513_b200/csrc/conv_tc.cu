@@ -147,12 +147,20 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
 // kGroup K-atoms (one TMA box, one split pass, 12 kGroup MMAs per sync).
 constexpr int kTcK = 192;
 constexpr int kTcAtoms = kTcK / 32;
-constexpr int kGroup = 3;
-constexpr int kGroups = kTcAtoms / kGroup;
+// group size and accumulator buffers per chunk count: NC = 64 keeps two TMEM
+// accumulators (epilogue of tile i overlaps the MMAs of tile i+1); NC = 128
+// (N = 128 MMAs: half the issue count) has room for one, drained by the
+// epilogue into registers before the next tile's first MMA.
+template <int NC> struct TcShape {
+  static constexpr int kGroup = NC == 128 ? 2 : 3;
+  static constexpr int kGroups = kTcAtoms / kGroup;
+  static constexpr int kDBufs = NC == 128 ? 1 : 2;
+};
 
 template <int NC>
 __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_constant__ ConvTCParams p) {
-  static_assert(NC % 32 == 0 && NC <= 64, "NC/2 columns per epilogue warp, loaded 16 at a time");
+  static_assert(NC % 32 == 0 && NC <= 128, "NC/2 columns per epilogue warp, loaded 16 at a time");
+  constexpr int kGroup = TcShape<NC>::kGroup, kGroups = TcShape<NC>::kGroups, ND = TcShape<NC>::kDBufs;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -167,8 +175,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
   uint64_t* empty = full + SH;          // [SH] MMA commit -> producer
   uint64_t* lofull = empty + SH;        // [SL] split -> MMA
   uint64_t* loempty = lofull + SL;      // [SL] MMA commit -> split
-  uint64_t* dfull = loempty + SL;       // [2]  MMA commit -> epilogue
-  uint64_t* dempty = dfull + 2;         // [2]  epilogue -> MMA
+  uint64_t* dfull = loempty + SL;       // [ND] MMA commit -> epilogue
+  uint64_t* dempty = dfull + 2;         // [ND] epilogue -> MMA
   uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
   float* fsm = reinterpret_cast<float*>(tslot + 4);  // [2][kConvTcMaxK + 256] zero-padded hi/lo taps
 
@@ -176,7 +184,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
   if (threadIdx.x == 0) {
     for (int i = 0; i < SH; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
     for (int i = 0; i < SL; ++i) { mbar_init(lofull + i, kTcSplitWarps); mbar_init(loempty + i, 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(dfull + i, 1); mbar_init(dempty + i, kTcEpiWarps); }
+    for (int i = 0; i < ND; ++i) { mbar_init(dfull + i, 1); mbar_init(dempty + i, kTcEpiWarps); }
     fence_mbar_init();
     prefetch_tmap(&p.tm_b);
   }
@@ -201,8 +209,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
   const uint32_t tmem = *tslot;
   // TMEM columns: A_hi [0, 192), A_lo [192, 384), accumulators [512 - 2 NC, 512)
   const uint32_t a_hi = tmem, a_lo = tmem + (uint32_t)kTcK;
-  const uint32_t d_col0 = tmem + 512u - 2u * NC;
-  static_assert(2 * kTcK + 2 * NC <= 512, "TMEM budget");
+  const uint32_t d_col0 = tmem + 512u - (uint32_t)(ND * NC);
+  static_assert(2 * kTcK + ND * NC <= 512, "TMEM budget");
 
   const int64_t ntiles = p.ntiles;
 
@@ -285,7 +293,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
       }
       mma_commit(dfull + d);
       if (lane == 0) TC_TRACE(it, 4);
-      if (++d == 2) { d = 0; dph ^= 1; }
+      if (++d == ND) { d = 0; dph ^= 1; }
     }
   } else if (warp < kTcWarpEpi0) {
     // split warps: Blo = x - trunc(x), elementwise (swizzle-agnostic), one group slot at a time
@@ -364,7 +372,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
           }
         }
       }
-      if (++d == 2) { d = 0; dph ^= 1; }
+      if (++d == ND) { d = 0; dph ^= 1; }
     }
     // view positions beyond the tensor map (array tail): direct FMA windows
     if (blockIdx.x == gridDim.x - 1 && h == 0) {
@@ -386,7 +394,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
 }
 
 size_t conv_tc_smem_bytes(int hi_slots, int lo_slots, int nc) {
-  return 1024 + (size_t)(hi_slots + lo_slots) * kGroup * nc * 128 + 8 * (2 * hi_slots + 2 * lo_slots + 4) + 16 +
+  const int group = nc == 128 ? TcShape<128>::kGroup : TcShape<64>::kGroup;
+  return 1024 + (size_t)(hi_slots + lo_slots) * group * nc * 128 + 8 * (2 * hi_slots + 2 * lo_slots + 4) + 16 +
          2 * sizeof(float) * (kConvTcMaxK + 256);
 }
 
@@ -394,9 +403,9 @@ template <int NC>
 static cudaError_t launch_nc(ConvTCParams& p, cudaStream_t stream, int grid) {
   // lo ring: four group slots (the split runs ahead of the MMAs);
   // hi ring: every remaining slot (TMA prefetch depth)
-  if (p.lo_bufs < 1) p.lo_bufs = 4;
+  if (p.lo_bufs < 1) p.lo_bufs = NC == 128 ? 2 : 4;
   int SH = 32;
-  while (SH > kGroups && conv_tc_smem_bytes(SH, p.lo_bufs, NC) > (size_t)kSmemBudget) --SH;
+  while (SH > TcShape<NC>::kGroups && conv_tc_smem_bytes(SH, p.lo_bufs, NC) > (size_t)kSmemBudget) --SH;
   if (conv_tc_smem_bytes(SH, p.lo_bufs, NC) > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
   p.hi_stages = SH;
   p.ntiles = (p.m_ext + NC - 1) / NC;
@@ -412,8 +421,8 @@ static cudaError_t launch_nc(ConvTCParams& p, cudaStream_t stream, int grid) {
 
 cudaError_t launch_conv_tc(ConvTCParams& p, int nc, cudaStream_t stream, int grid) {
   switch (nc) {
-    case 32: return launch_nc<32>(p, stream, grid);
     case 64: return launch_nc<64>(p, stream, grid);
+    case 128: return launch_nc<128>(p, stream, grid);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -104,7 +104,7 @@ cudaError_t launch_pool2d_direct(const Pool2DParams& p, cudaStream_t stream, int
 // y[b * y_pitch + y_off + i] with P - shift_x = b * N + i, if i < L_int.
 constexpr int kConvTcMaxK = 64;  // K = 127 + k rounded to 8 must fit 2 x 192 TMEM columns
 struct alignas(64) ConvTCParams {
-  CUtensorMap tm_b;        // 3-D {32, m_ext, atoms}, strides {512 B, 128 B}, box {32, NC, 3}, SW128
+  CUtensorMap tm_b;        // 3-D {32, m_ext, atoms}, strides {512 B, 128 B}, box {32, NC, group}, SW128
   const float* x_view;
   float* y;
   int64_t N, L_int, batch, shift_x, y_pitch, y_off;
