@@ -26,7 +26,10 @@ copy of the input, so no cell starts with its input L2-resident.
 Multi-GPU (torchrun, one rank per GPU, NCCL): cfg2 / cfg5 are sequence-
 sharded with a (w_max-1)-element halo exchanged by NCCL send/recv and
 overlapped with the interior kernels; cfg3 / cfg4 are batch-sharded with no
-collective; cfg1 runs as replicas.  Total work is fixed -> "scaling":"strong".
+collective; cfg1 runs as replicas.  Default --scaling weak: the global problem
+is the BASELINE.json shape times N (N x the rows / images / sequence length),
+so every rank processes one config-sized share ("scaling":"weak");
+--scaling strong keeps the BASELINE.json shape and splits it.
 
 --impl reference: the CPU oracle (oracle/, plain C, 1 thread) timed on a
 bounded sample of the same workload (rank 0 only) -- the tier's reference arm.
@@ -262,8 +265,21 @@ def dist_env():
 
 
 # ============================================================== our arm
+def scale_inputs(inputs, factor: int):
+    """Weak scaling: the global problem is `factor` x each sharded dimension
+    (rows, images, sequence length); replicas are unchanged."""
+    for sp in inputs.values():
+        if sp.get("shard") == "batch":
+            sp["rows"] *= factor
+        elif sp.get("shard") == "image":
+            sp["images"] *= factor
+        elif sp.get("shard") == "seq":
+            sp["n"] *= factor
+    return inputs
+
+
 class Runner:
-    def __init__(self, workload, world, rank, device):
+    def __init__(self, workload, world, rank, device, weak=False):
         import torch
 
         import paper_2305_16513_b200 as ss
@@ -272,6 +288,8 @@ class Runner:
         self.torch, self.ss, self.synth, self.ssd = torch, ss, synth, ssd
         self.world, self.rank, self.device = world, rank, device
         self.inputs_spec, self.cells = cfg_cells(workload)
+        if weak and world > 1:
+            scale_inputs(self.inputs_spec, world)
         self.stream = torch.cuda.current_stream()
         self.x = {}      # device inputs (local shard, incl. halo slots)
         self.meta = {}   # per-input sharding geometry
@@ -568,7 +586,8 @@ def run_ours(args):
         torch.cuda.set_device(0)
     device = torch.device("cuda", torch.cuda.current_device())
     import paper_2305_16513_b200 as ss
-    R = Runner(args.workload, world, rank, device)
+    weak = args.scaling == "weak"
+    R = Runner(args.workload, world, rank, device, weak=weak)
     torch.cuda.synchronize()
 
     coll_dev = device if args.dist_backend == "nccl" else torch.device("cpu")
@@ -699,7 +718,7 @@ def run_ours(args):
                "inputs": {k: {kk: vv for kk, vv in v.items() if kk != "kw"} for k, v in R.inputs_spec.items()}}
         line = {"metric": METRIC, "value": round(value, 3), "unit": "GElem/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
-                "higher_is_better": True, "scaling": "strong" if world > 1 else "strong",
+                "higher_is_better": True, "scaling": args.scaling,
                 "vs_baseline": None, "dtype": "f32/i32" if args.workload == "suite" else
                 ("i32" if args.workload == "cfg2" else "f32"),
                 "data": "synthetic (splitmix64 counter-based, BASELINE.json seeds/distributions)",
@@ -832,7 +851,7 @@ def run_reference(args):
     value = outs * args.steps / tot / 1e9
     line = {"metric": METRIC, "value": round(value, 6), "unit": "GElem/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 3),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f64/i64 accumulate", "data": "synthetic (same generator and seeds)",
             "config": {"workload": args.workload, "sample_fraction": frac},
             "impl": "reference",
@@ -850,6 +869,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="suite", choices=["suite", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "stride", "winspec", "affine", "backward"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="multi-GPU: weak = N x the BASELINE shape (config-sized share per rank), strong = split it")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
