@@ -524,6 +524,126 @@ __global__ void __launch_bounds__(512) pool2d_backward_plane_kernel(const __grid
   }
 }
 
+// Fixed-shape plane kernel (3x3/1 and 2x2/2, the DNN pooling shapes): 256
+// threads, two CTAs per SM.  avg is separable: a transposed row pass
+// R[r][c] = sum of dy[r][cc] over the <= ceil(KW/SW) windows cc covering c
+// (shared memory), then a transposed column pass dx[h][c] = inv * sum of
+// R[r][c] over the <= ceil(KH/SH) windows r covering h.  max builds the
+// window-argmax table, then gathers the <= ceil(KH/SH) x ceil(KW/SW)
+// candidate windows per position (row-major window order, as the direct path).
+template <bool kAvg, int KH, int KW, int SH, int SW>
+__global__ void __launch_bounds__(256, 2) pool2d_backward_fixed_kernel(const __grid_constant__ Pool2DBackwardParams p) {
+  extern __shared__ __align__(16) float s_fx[];
+  constexpr int NR = (KH + SH - 1) / SH, NCW = (KW + SW - 1) / SW;  // candidate windows per dimension
+  const int H = (int)p.H, W = (int)p.W, OH = (int)p.OH, OW = (int)p.OW;
+  float* g = s_fx;                          // dy plane [OH][OW]
+  float* aux = s_fx + OH * OW;              // avg: R [OH][W]; max: argmax table [OH][OW] (int)
+  int* tab = reinterpret_cast<int*>(aux);
+  for (int64_t pl = blockIdx.x; pl < p.planes; pl += gridDim.x) {
+    const float* __restrict__ gp = p.dy + pl * OH * OW;
+    float* __restrict__ d = p.dx + pl * H * W;
+    __syncthreads();
+    for (int e = threadIdx.x; e < OH * OW; e += 256) g[e] = __ldg(gp + e);
+    if constexpr (!kAvg && SH == 1) {
+      // overlapping window rows: each thread walks one window column down a band
+      // of rows with a ring of the last KH row results (first max of the row's KW
+      // inputs, value + column); the window's first row-major maximum is the
+      // first strictly greater row result in row order
+      const float* __restrict__ xp = p.x + pl * H * W;
+      const int bands = 256 / OW > 0 ? 256 / OW : 1;
+      const int band_rows = (OH + bands - 1) / bands;
+      for (int u = threadIdx.x; u < OW * bands; u += 256) {
+        const int c = u % OW, band = u / OW;
+        const int ra = band * band_rows, rb = min(ra + band_rows, OH);
+        if (ra >= rb) continue;
+        float rv[KH];
+        int rc[KH];
+        auto row_first_max = [&](int h, float& v, int& col) {
+          const float* xr = xp + h * W + c * SW;
+          v = __ldg(xr);
+          col = c * SW;
+#pragma unroll
+          for (int b = 1; b < KW; ++b) {
+            const float t = __ldg(xr + b);
+            if (t > v) { v = t; col = c * SW + b; }
+          }
+        };
+#pragma unroll
+        for (int a = 0; a < KH - 1; ++a) row_first_max(ra + a, rv[a + 1], rc[a + 1]);
+        for (int r = ra; r < rb; ++r) {
+#pragma unroll
+          for (int a = 0; a < KH - 1; ++a) { rv[a] = rv[a + 1]; rc[a] = rc[a + 1]; }
+          row_first_max(r + KH - 1, rv[KH - 1], rc[KH - 1]);
+          float m = rv[0];
+          int best = r * W + rc[0];
+#pragma unroll
+          for (int a = 1; a < KH; ++a)
+            if (rv[a] > m) { m = rv[a]; best = (r + a) * W + rc[a]; }
+          tab[r * OW + c] = best;
+        }
+      }
+    } else if constexpr (!kAvg) {
+      const float* __restrict__ xp = p.x + pl * H * W;
+      for (int e = threadIdx.x; e < OH * OW; e += 256) {
+        const int r = e / OW, c = e - r * OW;
+        const float* xw = xp + r * SH * W + c * SW;
+        float m = __ldg(xw);
+        int best = 0;
+#pragma unroll
+        for (int a = 0; a < KH; ++a)
+#pragma unroll
+          for (int b = 0; b < KW; ++b) {
+            const float v = __ldg(xw + a * W + b);
+            if (v > m) { m = v; best = a * W + b; }
+          }
+        tab[e] = (r * SH) * W + c * SW + best;
+      }
+    }
+    __syncthreads();
+    if constexpr (kAvg) {
+      for (int e = threadIdx.x; e < OH * W; e += 256) {  // row pass
+        const int r = e / W, c = e - r * W;
+        const int c0 = c - KW + 1 <= 0 ? 0 : (c - KW + SW) / SW;
+        float acc = 0.0f;
+#pragma unroll
+        for (int q = 0; q < NCW; ++q) {
+          const int cc = c0 + q;
+          if (cc * SW <= c && cc < OW) acc = __fadd_rn(acc, g[r * OW + cc]);
+        }
+        aux[e] = acc;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < H * W; e += 256) {  // column pass
+        const int h = e / W, c = e - h * W;
+        const int r0 = h - KH + 1 <= 0 ? 0 : (h - KH + SH) / SH;
+        float acc = 0.0f;
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          const int r = r0 + q;
+          if (r * SH <= h && r < OH) acc = __fadd_rn(acc, aux[r * W + c]);
+        }
+        d[e] = __fmul_rn(acc, p.inv_area);
+      }
+    } else {
+      for (int e = threadIdx.x; e < H * W; e += 256) {
+        const int h = e / W, c = e - h * W;
+        const int r0 = h - KH + 1 <= 0 ? 0 : (h - KH + SH) / SH;
+        const int c0 = c - KW + 1 <= 0 ? 0 : (c - KW + SW) / SW;
+        float acc = 0.0f;
+#pragma unroll
+        for (int qr = 0; qr < NR; ++qr)
+#pragma unroll
+          for (int qc = 0; qc < NCW; ++qc) {
+            const int r = r0 + qr, cc = c0 + qc;
+            if (r * SH <= h && r < OH && cc * SW <= c && cc < OW && tab[r * OW + cc] == e)
+              acc = __fadd_rn(acc, g[r * OW + cc]);
+          }
+        d[e] = acc;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- launches
 static unsigned grid_elems(int64_t total, int sms) {
   int64_t g = (total + kBwThreads - 1) / kBwThreads;
@@ -556,7 +676,27 @@ cudaError_t launch_pool_max_backward(const BackwardParams& p, cudaStream_t strea
   return cudaGetLastError();
 }
 
+template <int KH, int KW, int SH, int SW>
+static cudaError_t launch_pool2d_bwd_fixed(const Pool2DBackwardParams& p, cudaStream_t stream, int sms) {
+  const size_t smem = (size_t)(p.OH * p.OW + (p.mode == 1 ? p.OH * p.W : p.OH * p.OW)) * sizeof(float);
+  if (smem > (size_t)kSmemBudget / 2 || p.H * p.W >= (int64_t(1) << 30)) return cudaErrorInvalidConfiguration;
+  const int64_t g = p.planes < (int64_t)sms * 2 ? p.planes : (int64_t)sms * 2;
+  auto kfn = p.mode == 1 ? pool2d_backward_fixed_kernel<true, KH, KW, SH, SW>
+                         : pool2d_backward_fixed_kernel<false, KH, KW, SH, SW>;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
+  if (e != cudaSuccess) return e;
+  kfn<<<(unsigned)g, 256, smem, stream>>>(p);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pool2d_backward(const Pool2DBackwardParams& p, cudaStream_t stream, int sms) {
+  {
+    cudaError_t e = cudaErrorInvalidConfiguration;
+    if (p.kh == 3 && p.kw == 3 && p.sh == 1 && p.sw == 1) e = launch_pool2d_bwd_fixed<3, 3, 1, 1>(p, stream, sms);
+    else if (p.kh == 2 && p.kw == 2 && p.sh == 2 && p.sw == 2) e = launch_pool2d_bwd_fixed<2, 2, 2, 2>(p, stream, sms);
+    if (e != cudaErrorInvalidConfiguration) return e;
+  }
   const size_t table = (size_t)p.OH * p.OW * sizeof(float) * (p.mode == 1 ? 1 : 2);  // dy (+ argmax)
   if (p.H * p.W < (int64_t(1) << 30) && table <= (size_t)kSmemBudget) {
     const int64_t gp = p.planes < (int64_t)sms * 4 ? p.planes : (int64_t)sms * 4;
