@@ -587,6 +587,8 @@ def run_ours(args):
     device = torch.device("cuda", torch.cuda.current_device())
     import paper_2305_16513_b200 as ss
     weak = args.scaling == "weak"
+    if args.graph:  # graphs are captured on a non-default stream: run everything there
+        torch.cuda.set_stream(torch.cuda.Stream())
     R = Runner(args.workload, world, rank, device, weak=weak)
     torch.cuda.synchronize()
 
@@ -612,6 +614,20 @@ def run_ours(args):
         R.step()
     barrier()
     events = []
+    graph = None
+    if args.graph:
+        # launch-bound workloads (cfg1): capture one step in a CUDA graph and replay it;
+        # per-kernel durations come from one eager pass with events (below)
+        if world > 1:
+            raise SystemExit("--graph is single-GPU only (the halo exchange is not captured)")
+        n_cap0 = ss.ss_launch_count()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=R.stream):
+            R.step()
+        launches_per_step = ss.ss_launch_count() - n_cap0
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
     n_launch0 = ss.ss_launch_count()
     with ClockSampler(torch.cuda.current_device()) as clk:
         t0 = torch.cuda.Event(enable_timing=True)
@@ -619,11 +635,19 @@ def run_ours(args):
         barrier()
         t0.record(R.stream)
         for _ in range(args.steps):
-            R.step(events)
+            if graph is not None:
+                graph.replay()
+            else:
+                R.step(events)
         t1.record(R.stream)
         torch.cuda.synchronize()
         barrier()
     launches = ss.ss_launch_count() - n_launch0
+    if graph is not None:
+        launches = launches_per_step * args.steps
+        for _ in range(3):  # eager pass for the per-kernel event durations
+            R.step(events)
+        torch.cuda.synchronize()
     ms_local = t0.elapsed_time(t1)
     ms = max_over_ranks(ms_local)
     for c, a, b in events:
@@ -712,7 +736,7 @@ def run_ours(args):
         cpu = cpu_baseline(args.workload, budget_s=args.cpu_budget)
 
     if rank == 0:
-        cfg = {"workload": args.workload, "cells": [c.name for c in R.cells],
+        cfg = {"workload": args.workload, "cells": [c.name for c in R.cells], "cuda_graph": bool(args.graph),
                "parallelism": f"{'seq+batch' if args.workload == 'suite' else 'shard'} x{world}",
                "l2": "inputs > L2 (126 MB) per cell; cfg4 cells read distinct input copies",
                "inputs": {k: {kk: vv for kk, vv in v.items() if kk != "kw"} for k, v in R.inputs_spec.items()}}
@@ -872,6 +896,7 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="multi-GPU: weak = N x the BASELINE shape (config-sized share per rank), strong = split it")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="replay each timed step as a captured CUDA graph")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
