@@ -307,6 +307,18 @@ static ss_status_t window_impl(int op, const void* x, void* y, int64_t N, int64_
       interior_done = true;
     }
   }
+  if (!interior_done && stride == 1 && d > 1 && L_int >= 1 && w <= 32 && dtype == SS_F32) {
+    // dilated windows: phase-decomposed tile kernel on the interior (dilated.cu)
+    DilatedParams dp;
+    memset(&dp, 0, sizeof dp);
+    dp.x = x; dp.y = static_cast<float*>(y) + pl;
+    dp.N = N; dp.L_int = L_int; dp.batch = batch; dp.w = w; dp.d = d; dp.y_pitch = L; dp.y_off = 0;
+    if (op == kOpConv)
+      for (int64_t j = 0; j < w; ++j) dp.taps[j] = taps[j];
+    cudaError_t e = launch_dilated(dp, op, s, grid);
+    if (e == cudaSuccess) interior_done = true;
+    else if (e != cudaErrorInvalidConfiguration) return cuda_fail(e, "dilated launch");
+  }
   if (!interior_done && stride == 1 && d == 1 && L_int >= 1) {
     const int KT = op == kOpConv ? conv_bucket(w) : 0;
     if (op == kOpConv ? KT > 0 : w <= kPoolTmaMaxW) {

@@ -144,4 +144,15 @@ cudaError_t launch_conv_filter_grad(const BackwardParams& p, float* df, void* wo
                                     cudaStream_t stream);
 cudaError_t launch_pool2d_backward(const Pool2DBackwardParams& p, cudaStream_t stream, int sms);
 
+// Dilated stride-1 windows (dilated.cu): interior outputs
+// i < L_int = N - (w-1) d of each row go to y[b * y_pitch + y_off + i].
+struct DilatedParams {
+  const void* x;
+  void* y;
+  int64_t N, L_int, batch, w, d, y_pitch, y_off;
+  int stage_floats;  // set by launch_dilated
+  float taps[32];    // conv (w <= 32), zero-padded
+};
+cudaError_t launch_dilated(DilatedParams& p, int op, cudaStream_t stream, int sms);
+
 }  // namespace ss

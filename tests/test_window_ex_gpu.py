@@ -93,3 +93,32 @@ def test_ex_validation(ss):
     assert ss.ss_pool_sum_ex(FX, FY, 10, 1, 3, 1, 1, -1, 0, ss.SS_F32) == ss.SS_ERR_BAD_SIZE
     assert ss.ss_pool_max_ex(FX, FY, 3, 1, 3, 1, 2, 0, 0, ss.SS_F32) == ss.SS_ERR_WINDOW_EXCEEDS_INPUT
     # (no valid call with fake pointers: it would launch)
+
+
+DILATED = [  # (N, B, w, d, pl, pr): stride-1 dilated windows -> the phase-decomposed tile kernel
+    (50011, 2, 8, 2, 0, 0), (50011, 3, 15, 8, 56, 56), (30000, 1, 32, 3, 0, 0), (40000, 2, 5, 16, 0, 9),
+    (70001, 1, 3, 256, 0, 0), (9000, 2, 17, 7, 48, 64), (20000, 2, 2, 300, 0, 0), (5000, 2, 32, 33, 0, 0),
+]
+
+
+@pytest.mark.parametrize("N,B,w,d,pl,pr", DILATED)
+def test_dilated_tile(ss, N, B, w, d, pl, pr):
+    L = ss.ss_out_len_ex(N, w, 1, d, pl, pr)
+    if L < 0:
+        pytest.skip("window exceeds padded input")
+    xf = synth.uniform_pm1(7, B * N).reshape(B, N)
+    ymf = run(ss, ss.ss_pool_max_ex, xf, (w, 1, d, pl, pr, ss.SS_F32), L, 1, 2)
+    np.testing.assert_array_equal(ymf, oracle.pool_max_ex(xf, w, 1, d, pl, pr))
+    ysf = run(ss, ss.ss_pool_sum_ex, xf, (w, 1, d, pl, pr, ss.SS_F32), L, 3, 1)
+    ref, mag = oracle.pool_sum_ex(xf, w, 1, d, pl, pr)
+    assert np.all(np.abs(ysf - ref) <= 1e-5 * mag + 1e-6)
+    f = synth.normal(4, w, sigma=synth.cfg_sigma_filter(w))
+    y = run(ss, lambda xp, yp, N_, B_, *a: ss.ss_conv1d_ex(xp, yp, N_, B_, f.tolist(), w, *a),
+            xf, (1, d, pl, pr, ss.SS_F32), L, 2, 3)
+    ref, mag = oracle.conv1d_ex(xf, f, 1, d, pl, pr)
+    assert np.all(np.abs(y.astype(np.float64) - ref) <= 1e-5 * mag + 1e-6)
+    # integer-valued input (exact in fp32): the sum is exact in any order
+    xi = synth.randint(8, B * N, -1000, 1000).reshape(B, N).astype(np.float32)
+    ysi = run(ss, ss.ss_pool_sum_ex, xi, (w, 1, d, pl, pr, ss.SS_F32), L)
+    refi, _ = oracle.pool_sum_ex(xi, w, 1, d, pl, pr)
+    np.testing.assert_array_equal(ysi.astype(np.float64), refi)
