@@ -243,16 +243,93 @@ constexpr int kFgStages = 4;
 constexpr int kFgFold = 4;  // tiles accumulated in fp32 (64 terms per partial) before folding into fp64
 constexpr int kFgXSpan = kFgTile + kFgTaps;  // inputs one tile needs (unit stride)
 __host__ __device__ constexpr int fg_pad(int e) { return e + 4 * (e >> 4); }
-constexpr int kFgXStride = (fg_pad(kFgXSpan) + 16) & ~3;          // padded x floats per stage
-constexpr int kFgStageFloats = kFgXStride + fg_pad(kFgTile);       // + padded dy
+// stages hold x / dy from the 16-B-aligned-down address of the tile's first
+// element on (up to 3 leading elements), in the padded layout
+constexpr int kFgXStride = (fg_pad(kFgXSpan + 4) + 16) & ~3;      // padded x floats per stage
+constexpr int kFgStageFloats = kFgXStride + fg_pad(kFgTile + 8) + 8;
 constexpr size_t kFgSmem = (size_t)kFgStages * kFgStageFloats * sizeof(float);
+
+// (row, tile-in-row) of a grid-strided tile sequence, advanced without divisions
+struct TileCursor {
+  int64_t b, tr, tpr, step;
+  __device__ void init(int64_t tile, int64_t tiles_per_row, int64_t stride) {
+    tpr = tiles_per_row;
+    step = stride;
+    b = tile / tpr;
+    tr = tile - b * tpr;
+  }
+  __device__ void advance() {
+    tr += step;
+    while (tr >= tpr) { tr -= tpr; ++b; }
+  }
+};
+
+// stage `n` elements from src (any alignment) at padded local indices mis .. mis+n-1,
+// mis = src's element offset in its 16-B granule; elements of the leading granule
+// before src are filled too (never read) when they lie inside [lo_ok, src)
+__device__ __forceinline__ void fg_stage(float* sdst, const float* __restrict__ src, int n, int64_t avail,
+                                         bool aligned_ok, int mis) {
+  if (aligned_ok) {
+    const float* base = src - mis;
+    const int lim = (int)(avail < n ? avail : n) + mis;  // valid elements from base (32-bit)
+    for (int e = 4 * threadIdx.x; e < n + mis; e += 4 * kBwThreads) {
+      const int left = lim - e;
+      const uint32_t nb = left >= 4 ? 16u : (left > 0 ? 4u * (uint32_t)left : 0u);
+      cp_async16(smem_u32(sdst + fg_pad(e)), nb ? base + e : src, nb);
+    }
+  } else {
+    for (int e = threadIdx.x; e < n; e += kBwThreads)
+      cp_async4(smem_u32(sdst + fg_pad(e + mis)), e < avail ? src + e : src, e < avail ? 4u : 0u);
+  }
+}
 
 // Unit-stride filter gradient.  Inner product per thread and tile: 16 outputs
 // m x 16 taps jj, acc[jj] += dy_m x_{m+jj}, as FFMA2 over tap pairs
 // (acc[jj], acc[jj+1]) += dy_m * (x_{m+jj}, x_{m+jj+1}); the input window is
 // kept twice (pairs starting at even and at odd offsets) so every pair is an
-// aligned register pair.  x / dy rows that are 16-B aligned stream with 16-B
-// cp.async, others with 4-B cp.async.
+// aligned register pair.  x and dy stream with 16-B cp.async from their
+// aligned-down addresses; the tile-uniform misalignment of x selects one of
+// four compile-time realignments (MX), dy is read with 32-bit loads.
+template <int MX, int MG>
+__device__ __forceinline__ void fg_tile(const float* xs, const float* gs, int base, int m0, float2 (&acc)[8]) {
+  // x window [base, base + 32) sits at local indices base + MX + (0..31): 9 aligned float4;
+  // dy run [m0, m0 + 16) at local m0 + MG + (0..15): 5 aligned float4
+  float w[36], gv[20];
+#pragma unroll
+  for (int c = 0; c < 36; c += 4) {
+    const float4 v = *reinterpret_cast<const float4*>(xs + fg_pad(base + c));
+    w[c] = v.x; w[c + 1] = v.y; w[c + 2] = v.z; w[c + 3] = v.w;
+  }
+#pragma unroll
+  for (int c = 0; c < 20; c += 4) {
+    const float4 v = *reinterpret_cast<const float4*>(gs + fg_pad(m0 + c));
+    gv[c] = v.x; gv[c + 1] = v.y; gv[c + 2] = v.z; gv[c + 3] = v.w;
+  }
+  float2 E[16], O[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) E[i] = make_float2(w[MX + 2 * i], w[MX + 2 * i + 1]);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) O[i] = make_float2(w[MX + 2 * i + 1], w[MX + 2 * i + 2]);
+#pragma unroll
+  for (int mt = 0; mt < kFgRun; ++mt) {
+    const float2 g2 = make_float2(gv[MG + mt], gv[MG + mt]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)  // taps 2i, 2i+1: inputs x_{mt+2i}, x_{mt+2i+1}
+      acc[i] = __ffma2_rn((mt & 1) ? O[(mt >> 1) + i] : E[(mt >> 1) + i], g2, acc[i]);
+  }
+}
+
+template <int MX>
+__device__ __forceinline__ void fg_tile_g(const float* xs, const float* gs, int misg, int base, int m0,
+                                          float2 (&acc)[8]) {
+  switch (misg) {  // tile-uniform
+    case 0: fg_tile<MX, 0>(xs, gs, base, m0, acc); break;
+    case 1: fg_tile<MX, 1>(xs, gs, base, m0, acc); break;
+    case 2: fg_tile<MX, 2>(xs, gs, base, m0, acc); break;
+    default: fg_tile<MX, 3>(xs, gs, base, m0, acc); break;
+  }
+}
+
 __global__ void __launch_bounds__(kBwThreads, 2) conv_filter_grad_kernel(const __grid_constant__ BackwardParams p,
                                                                          double* __restrict__ partials) {
   extern __shared__ __align__(16) float fg_smem[];
@@ -263,40 +340,28 @@ __global__ void __launch_bounds__(kBwThreads, 2) conv_filter_grad_kernel(const _
   const int q = threadIdx.x & 3, r = threadIdx.x >> 2;  // tap group, run slot
   const int64_t tiles_per_row = (p.L + kFgTile - 1) / kFgTile;
   const int64_t ntiles = p.batch * tiles_per_row;
-  // issue the cp.async copies of tile `tile` into stage `st` (one commit group per tile)
-  auto issue = [&](int64_t tile, int st) {
-    if (tile < ntiles) {
+  TileCursor ic, cc;  // issue cursor (kFgStages-1 tiles ahead) and compute cursor
+  ic.init(blockIdx.x, tiles_per_row, gridDim.x);
+  cc = ic;
+  int64_t itile = blockIdx.x;
+  auto issue = [&](int st) {
+    if (itile < ntiles) {
       float* xs = fg_smem + st * kFgStageFloats;
       float* gs = xs + kFgXStride;
-      const int64_t b = tile / tiles_per_row;
-      const int64_t i0 = (tile - b * tiles_per_row) * kFgTile;
+      const int64_t i0 = ic.tr * kFgTile;
       const int64_t nout = p.L - i0 < kFgTile ? p.L - i0 : kFgTile;
-      const float* __restrict__ xr = x + b * p.N + i0 + j0;
-      const int64_t xlim = p.N - i0 - j0;  // elements of the row from xr on
-      const float* __restrict__ gr = dy + b * p.L + i0;
-      if (((reinterpret_cast<uintptr_t>(xr) | reinterpret_cast<uintptr_t>(gr)) & 15) == 0) {
-        for (int e = 4 * threadIdx.x; e < kFgXSpan; e += 4 * kBwThreads) {
-          const int64_t left = xlim - e;
-          const uint32_t nb = left >= 4 ? 16u : (left > 0 ? 4u * (uint32_t)left : 0u);
-          cp_async16(smem_u32(xs + fg_pad(e)), nb ? xr + e : x, nb);
-        }
-        for (int e = 4 * threadIdx.x; e < kFgTile; e += 4 * kBwThreads) {
-          const int64_t left = nout - e;
-          const uint32_t nb = left >= 4 ? 16u : (left > 0 ? 4u * (uint32_t)left : 0u);
-          cp_async16(smem_u32(gs + fg_pad(e)), nb ? gr + e : dy, nb);
-        }
-      } else {
-        for (int e = threadIdx.x; e < kFgXSpan; e += kBwThreads)
-          cp_async4(smem_u32(xs + fg_pad(e)), e < xlim ? xr + e : x, e < xlim ? 4u : 0u);
-        for (int e = threadIdx.x; e < kFgTile; e += kBwThreads)
-          cp_async4(smem_u32(gs + fg_pad(e)), e < nout ? gr + e : dy, e < nout ? 4u : 0u);
-      }
+      const int64_t xg = ic.b * p.N + i0 + j0, gg = ic.b * p.L + i0;  // element offsets from x / dy
+      const int misx = (int)((reinterpret_cast<uintptr_t>(x + xg) >> 2) & 3);
+      const int misg = (int)((reinterpret_cast<uintptr_t>(dy + gg) >> 2) & 3);
+      fg_stage(xs, x + xg, kFgXSpan, p.N - i0 - j0, xg >= misx, misx);
+      fg_stage(gs, dy + gg, kFgTile, nout, gg >= misg, misg);
+      ic.advance();
+      itile += gridDim.x;
     }
     cp_async_commit();
   };
-  int64_t tile = blockIdx.x;
 #pragma unroll 1
-  for (int st = 0; st < kFgStages - 1; ++st) issue(tile + (int64_t)st * gridDim.x, st);
+  for (int st = 0; st < kFgStages - 1; ++st) issue(st);
   double acc64[16];
 #pragma unroll
   for (int jj = 0; jj < 16; ++jj) acc64[jj] = 0.0;
@@ -304,38 +369,23 @@ __global__ void __launch_bounds__(kBwThreads, 2) conv_filter_grad_kernel(const _
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = make_float2(0.0f, 0.0f);
   int st = 0, nfold = 0;
-  for (; tile < ntiles; tile += gridDim.x) {
-    issue(tile + (int64_t)(kFgStages - 1) * gridDim.x, (st + kFgStages - 1) % kFgStages);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    issue((st + kFgStages - 1) % kFgStages);
     cp_async_wait<kFgStages - 1>();  // this tile's group has landed (for this thread)
     __syncthreads();                 // ... and for every thread
     const float* xs = fg_smem + st * kFgStageFloats;
     const float* gs = xs + kFgXStride;
+    const int64_t i0 = cc.tr * kFgTile;
+    const int misx = (int)((reinterpret_cast<uintptr_t>(x + cc.b * p.N + i0 + j0) >> 2) & 3);
+    const int misg = (int)((reinterpret_cast<uintptr_t>(dy + cc.b * p.L + i0) >> 2) & 3);
+    cc.advance();
     const int m0 = kFgRun * r;
-    // window x[m0 + 16q + (0..31)] as even-start pairs E[i] = (x_{2i}, x_{2i+1}) and
-    // odd-start pairs O[i] = (x_{2i+1}, x_{2i+2})
-    float2 E[16], O[16];
     const int base = m0 + 16 * q;
-#pragma unroll
-    for (int c = 0; c < 32; c += 4) {
-      const float4 v = *reinterpret_cast<const float4*>(xs + fg_pad(base + c));
-      E[c / 2] = make_float2(v.x, v.y);
-      E[c / 2 + 1] = make_float2(v.z, v.w);
-    }
-#pragma unroll
-    for (int i = 0; i < 15; ++i) O[i] = make_float2(E[i].y, E[i + 1].x);
-    O[15] = make_float2(E[15].y, 0.0f);
-#pragma unroll
-    for (int m = 0; m < kFgRun; m += 4) {
-      const float4 gv = *reinterpret_cast<const float4*>(gs + fg_pad(m0 + m));
-      const float g4[4] = {gv.x, gv.y, gv.z, gv.w};
-#pragma unroll
-      for (int mm = 0; mm < 4; ++mm) {
-        const int mt = m + mm;
-        const float2 g2 = make_float2(g4[mm], g4[mm]);
-#pragma unroll
-        for (int i = 0; i < 8; ++i)  // taps 2i, 2i+1: inputs x_{mt+2i}, x_{mt+2i+1}
-          acc[i] = __ffma2_rn((mt & 1) ? O[(mt >> 1) + i] : E[(mt >> 1) + i], g2, acc[i]);
-      }
+    switch (misx) {  // tile-uniform
+      case 0: fg_tile_g<0>(xs, gs, misg, base, m0, acc); break;
+      case 1: fg_tile_g<1>(xs, gs, misg, base, m0, acc); break;
+      case 2: fg_tile_g<2>(xs, gs, misg, base, m0, acc); break;
+      default: fg_tile_g<3>(xs, gs, misg, base, m0, acc); break;
     }
     if (++nfold == kFgFold) {
       nfold = 0;
