@@ -162,6 +162,64 @@ __global__ void __launch_bounds__(kBwThreads) pool_max_backward_tile_kernel(cons
   }
 }
 
+// Short windows (w <= kMaxDirectW): the same tile, SIMD-uniform work -- each
+// window's first maximum by a direct scan of its w staged inputs, then every
+// position gathers the <= ceil(w/s) windows that contain it (increasing
+// window order), comparing their argmax with itself.
+constexpr int kMaxDirectW = 64;
+
+__global__ void __launch_bounds__(kBwThreads) pool_max_backward_direct_kernel(const __grid_constant__ BackwardParams p) {
+  extern __shared__ __align__(16) float md_smem[];
+  float* xs = md_smem;                                   // [kMaxTile + 2 kMaxDirectW + kMaxTileS]
+  float* gs = xs + kMaxTile + 2 * kMaxDirectW + kMaxTileS;  // [kMaxTile + kMaxDirectW + 2]
+  int* A = reinterpret_cast<int*>(gs + kMaxTile + kMaxDirectW + 2);
+  const float* __restrict__ x = static_cast<const float*>(p.x);
+  const float* __restrict__ dy = static_cast<const float*>(p.dy);
+  float* __restrict__ dx = static_cast<float*>(p.dx);
+  const int w = (int)p.w, s = (int)p.stride;
+  const int64_t tiles_per_row = (p.N + kMaxTile - 1) / kMaxTile;
+  const int64_t ntiles = p.batch * tiles_per_row;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t b = tile / tiles_per_row;
+    const int64_t t0 = (tile - b * tiles_per_row) * kMaxTile;
+    const int nt = (int)(t0 + kMaxTile < p.N ? kMaxTile : p.N - t0);
+    const int64_t wlo = first_window(t0, p.w, p.stride);
+    int64_t whi = (t0 + nt - 1) / p.stride;
+    if (whi > p.L - 1) whi = p.L - 1;
+    const int nwin = whi >= wlo ? (int)(whi - wlo + 1) : 0;
+    const int64_t xa = wlo * p.stride;
+    const int span = nwin ? (nwin - 1) * s + w : 0;
+    const float* __restrict__ xr = x + b * p.N + xa;
+    const float* __restrict__ gr = dy + b * p.L + wlo;
+    __syncthreads();  // previous tile's readers are done
+    for (int e = threadIdx.x; e < span; e += kBwThreads) xs[e] = __ldg(xr + e);
+    for (int e = threadIdx.x; e < nwin; e += kBwThreads) gs[e] = __ldg(gr + e);
+    __syncthreads();
+    for (int j = threadIdx.x; j < nwin; j += kBwThreads) {
+      const int u = j * s;
+      float m = xs[u];
+      int a = u;
+      for (int q = 1; q < w; ++q) {
+        const float v = xs[u + q];
+        if (v > m) { m = v; a = u + q; }
+      }
+      A[j] = a;
+    }
+    __syncthreads();
+    const int rel0 = (int)(t0 - xa);  // span-relative position of t0
+    for (int e = threadIdx.x; e < nt; e += kBwThreads) {
+      const int rel = rel0 + e;       // t = t0 + e
+      const int64_t t = t0 + e;
+      int64_t i0 = first_window(t, p.w, p.stride), i1 = t / p.stride;
+      if (i1 > whi) i1 = whi;
+      float acc = 0.0f;
+      for (int j = (int)(i0 - wlo); j <= (int)(i1 - wlo); ++j)
+        if (A[j] == rel) acc = __fadd_rn(acc, gs[j]);
+      dx[b * p.N + t] = acc;
+    }
+  }
+}
+
 // Fallback for w > kMaxTileW: windows in chunks, argmax of each recomputed from
 // global memory, then each position gathers the chunk's windows routed to it.
 constexpr int kMaxChunk = 1024;
@@ -715,7 +773,13 @@ cudaError_t launch_pool_max_backward(const BackwardParams& p, cudaStream_t strea
   const int64_t tiles = p.batch * ((p.N + kMaxTile - 1) / kMaxTile);
   const int64_t cap = (int64_t)sms * 8;
   const unsigned g = (unsigned)(tiles < cap ? tiles : cap);
-  if (p.w <= kMaxTileW && p.stride <= kMaxTileS) {
+  if (p.w <= kMaxDirectW && p.stride <= kMaxTileS) {
+    const size_t smem = sizeof(float) * (size_t)(2 * kMaxTile + 3 * kMaxDirectW + kMaxTileS + 2) +
+                        sizeof(int) * (size_t)(kMaxTile + kMaxDirectW + 2);
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(pool_max_backward_direct_kernel));
+    if (e != cudaSuccess) return e;
+    pool_max_backward_direct_kernel<<<g < 1 ? 1 : g, kBwThreads, smem, stream>>>(p);
+  } else if (p.w <= kMaxTileW && p.stride <= kMaxTileS) {
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(pool_max_backward_tile_kernel));
     if (e != cudaSuccess) return e;
     pool_max_backward_tile_kernel<<<g < 1 ? 1 : g, kBwThreads, kMaxTileSmem, stream>>>(p);
