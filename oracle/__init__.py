@@ -86,6 +86,8 @@ def lib() -> ctypes.CDLL:
             L.oracle_conv1d_backward_filter_f32.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp]
             L.oracle_pool2d_backward_f32.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64,
                                                      ctypes.c_int, vp, vp]
+            L.oracle_conv2d_f32.argtypes = [vp, i64, i64, i64, vp, i64, i64, i64, i64, vp, vp]
+            L.oracle_conv2d_f32.restype = ctypes.c_int
             for n in ("oracle_pool_sum_backward_f32", "oracle_pool_max_backward_f32",
                       "oracle_conv1d_backward_input_f32", "oracle_conv1d_backward_filter_f32",
                       "oracle_pool2d_backward_f32"):
@@ -331,3 +333,19 @@ def pool2d_backward(x, dy: np.ndarray, H: int, W: int, kh: int, kw: int, sh: int
     m = np.empty((P, H, W), np.float64)
     _check(lib().oracle_pool2d_backward_f32(xp, _p(dy), P, H, W, kh, kw, sh, sw, mode, _p(dx), _p(m)))
     return dx, m
+
+
+def conv2d(x: np.ndarray, f: np.ndarray, sh: int = 1, sw: int = 1):
+    """2-D single-channel sliding dot product (cross-correlation) of [planes, H, W] with f [kh, kw];
+    returns (y double [planes, OH, OW], absmag)."""
+    x = np.ascontiguousarray(x, np.float32)
+    f = np.ascontiguousarray(f, np.float32)
+    P, H, W = x.shape
+    kh, kw = f.shape
+    OH, OW = out_len(H, kh, sh), out_len(W, kw, sw)
+    if OH < 0 or OW < 0:
+        raise ValueError("window exceeds input")
+    y = np.empty((P, OH, OW), np.float64)
+    m = np.empty((P, OH, OW), np.float64)
+    _check(lib().oracle_conv2d_f32(_p(x), P, H, W, _p(f), kh, kw, sh, sw, _p(y), _p(m)))
+    return y, m

@@ -485,3 +485,27 @@ int oracle_pool2d_backward_f32(const float* x, const float* dy, int64_t planes, 
       }
   return 0;
 }
+
+/* Multi-dimensional extension of the sliding dot product
+ * (Sec. 2.5) to a single-channel 2-D filter: cross-correlation of each plane
+ * with f [kh][kw] at stride (sh, sw), valid padding, taps summed in row-major
+ * order in double:  y[p][r][c] = sum_{a<kh} sum_{b<kw} f[a][b] x[p][r sh + a][c sw + b]. */
+int oracle_conv2d_f32(const float* x, int64_t planes, int64_t H, int64_t W, const float* f,
+                      int64_t kh, int64_t kw, int64_t sh, int64_t sw, double* y, double* absmag) {
+  int64_t OH = oracle_out_len(H, kh, sh), OW = oracle_out_len(W, kw, sw);
+  if (x == NULL || f == NULL || y == NULL || planes < 1 || OH < 0 || OW < 0) return -1;
+  for (int64_t p = 0; p < planes; ++p)
+    for (int64_t r = 0; r < OH; ++r)
+      for (int64_t c = 0; c < OW; ++c) {
+        double acc = 0.0, mag = 0.0;
+        for (int64_t a = 0; a < kh; ++a)
+          for (int64_t b = 0; b < kw; ++b) {
+            double t = (double)f[a * kw + b] * (double)x[(p * H + r * sh + a) * W + c * sw + b];
+            acc += t;
+            mag += fabs(t);
+          }
+        y[(p * OH + r) * OW + c] = acc;
+        if (absmag) absmag[(p * OH + r) * OW + c] = mag;
+      }
+  return 0;
+}

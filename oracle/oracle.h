@@ -121,6 +121,11 @@ int oracle_pool2d_backward_f32(const float* x, const float* dy, int64_t planes, 
                                int64_t W, int64_t kh, int64_t kw, int64_t sh, int64_t sw,
                                int mode, double* dx, double* absmag);
 
+/* 2-D single-channel sliding dot product (multi-dimensional extension,
+ * PAPER.md l.226): y [planes][OH][OW] in double, absmag optional. */
+int oracle_conv2d_f32(const float* x, int64_t planes, int64_t H, int64_t W, const float* f,
+                      int64_t kh, int64_t kw, int64_t sh, int64_t sw, double* y, double* absmag);
+
 #ifdef __cplusplus
 }
 #endif

@@ -448,3 +448,45 @@ def test_affine_window_is_order_sensitive_and_gives_the_dot_product():
     _, Vd, _ = oracle.affine_window(gu.astype(np.float32), gv.astype(np.float32), len(gu))
     assert np.all(gu.astype(np.float32) == gu) and np.all(gv.astype(np.float32) == gv)
     assert Vd[0] == float(np.dot(a, b))
+
+
+# ------------------------------------------- multi-dimensional extension: 2-D sliding dot product
+def test_conv2d_separable_filter_is_row_then_column_conv():
+    # f = u (x) v (outer product): the 2-D correlation equals the 1-D correlation of
+    # every row with v followed by every column with u -- exact on integers
+    x = synth.randint(50, 3 * 13 * 17, -9, 9).astype(np.float32).reshape(3, 13, 17)
+    u = np.array([1, -2, 3], np.float32)
+    v = np.array([2, 0, -1, 1], np.float32)
+    y, _ = oracle.conv2d(x, np.outer(u, v))
+    rows, _ = oracle.conv1d(x.reshape(-1, 17), v)                      # [3*13, 14]
+    rows = rows.reshape(3, 13, 14).transpose(0, 2, 1).reshape(-1, 13)  # columns as rows
+    cols, _ = oracle.conv1d(rows.astype(np.float32), u)                # exact: small integers
+    np.testing.assert_array_equal(y, cols.reshape(3, 14, 11).transpose(0, 2, 1))
+
+
+def test_conv2d_delta_and_box_filters():
+    x = synth.uniform01(51, 2 * 9 * 10).reshape(2, 9, 10)
+    for a, b in ((0, 0), (1, 2), (2, 1)):
+        f = np.zeros((3, 3), np.float32)
+        f[a, b] = 1.0
+        y, _ = oracle.conv2d(x, f)
+        np.testing.assert_array_equal(y, x[:, a:a + 7, b:b + 8].astype(np.float64))  # shifted plane, exact
+    xi = synth.randint(52, 2 * 9 * 10, -50, 50).astype(np.float32).reshape(2, 9, 10)
+    y, _ = oracle.conv2d(xi, np.ones((3, 2), np.float32), 2, 1)
+    avg, _ = oracle.pool2d(xi, 3, 2, 2, 1, oracle.POOL2D_AVG)
+    np.testing.assert_allclose(y, avg * 6, rtol=0, atol=1e-12)          # box filter = window sum
+
+
+def test_conv2d_vs_torch_and_1d_reduction():
+    x = synth.normal(53, 2 * 20 * 23).reshape(2, 20, 23)
+    f = synth.normal(54, 15).reshape(3, 5)
+    for sh, sw in ((1, 1), (2, 1), (2, 3)):
+        y, _ = oracle.conv2d(x, f, sh, sw)
+        ref = torch.nn.functional.conv2d(torch.tensor(x, dtype=torch.float64)[:, None],
+                                         torch.tensor(f, dtype=torch.float64)[None, None], stride=(sh, sw))
+        np.testing.assert_allclose(y, ref[:, 0].numpy(), rtol=1e-12, atol=1e-12)
+    # kh = 1: every row is the 1-D sliding dot product
+    f1 = synth.normal(55, 6).reshape(1, 6)
+    y, _ = oracle.conv2d(x, f1)
+    y1, _ = oracle.conv1d(x.reshape(-1, 23), f1[0])
+    np.testing.assert_array_equal(y.reshape(-1, 18), y1)
