@@ -158,6 +158,13 @@ def cfg_cells(workload: str):
                               shard="batch")
         for w in (8, 64, 1024):
             cells.append(Cell("affine", f"affine_w{w}", "affine", w=w, inp="xa_u", inp2="xa_v"))
+    if workload == "conv2d":  # 2-D sliding dot product on the config-4 tensor
+        for i, (kk, st) in enumerate(((3, 1), (5, 1), (7, 1), (3, 2))):
+            inputs[f"x2d_{i}"] = dict(images=32, C=64, H=112, W=112, dtype="float32", dist="u01", seed=5, kw={},
+                                      shard="image")
+            f = synth.normal(70 + kk, kk * kk, sigma=1.0 / kk).reshape(kk, kk)
+            cells.append(Cell("conv2d", f"conv2d_{kk}x{kk}_s{st}", "conv2d", kh=kk, kw=kk, sh=st, sw=st, f=f,
+                              inp=f"x2d_{i}"))
     if workload == "backward":  # backward passes on config-3 / config-4 shapes; not a BJ config
         inputs["xb"] = dict(rows=64, n=1 << 20, dtype="float32", dist="normal", seed=3, kw={}, shard="batch")
         for k in (7, 31, 63):
@@ -329,7 +336,7 @@ class Runner:
             if c.op in BWD_OPS:
                 self._alloc_bwd(c)
                 continue
-            if c.op == "pool2d":
+            if c.op in ("pool2d", "conv2d"):
                 B, C, H, W = geo
                 OH, OW = (H - c.kh) // c.sh + 1, (W - c.kw) // c.sw + 1
                 self.y[c.name] = torch.empty((B, C, OH, OW), dtype=x.dtype, device=self.device)
@@ -358,7 +365,7 @@ class Runner:
                 self.y[c.name] = torch.empty(L, dtype=x.dtype, device=self.device)
                 c.n_out = L
                 c.bytes = (n + L) * es
-            c.flops = 2 * c.w * c.n_out if c.op == "conv" else 0
+            c.flops = 2 * c.w * c.n_out if c.op == "conv" else (2 * c.kh * c.kw * c.n_out if c.op == "conv2d" else 0)
 
     def _alloc_bwd(self, c):
         """Backward cells: dx (or df + workspace) and the algorithmic bytes / unit counts.
@@ -449,6 +456,12 @@ class Runner:
         if c.op in BWD_OPS:
             ev0 = self._ev(events)
             self._launch_bwd(c)
+            self._ev_end(events, c, ev0)
+        elif c.op == "conv2d":
+            B, C, H, W = geo
+            ev0 = self._ev(events)
+            self.ss.check(self.ss.ss_conv2d(x.data_ptr(), y.data_ptr(), B * C, H, W, c.f.reshape(-1).tolist(), c.kh,
+                                            c.kw, c.sh, c.sw, self.ss.SS_F32, self.stream.cuda_stream))
             self._ev_end(events, c, ev0)
         elif c.op == "pool2d":
             B, C, H, W = geo
@@ -673,7 +686,7 @@ def run_ours(args):
              "share": 0.0}
         if conv_on_tensor_cores(c):
             d["tc_frac"] = round(c.n_out * TC_FLOP_PER_OUT / (avg_ms * 1e-3) / 1e12 / tf32_peak_tflops(), 4)
-        elif c.op in ("conv", "conv_bwd_in", "conv_bwd_f"):
+        elif c.op in ("conv", "conv_bwd_in", "conv_bwd_f", "conv2d"):
             fma_s = c.flops / 2 / (avg_ms * 1e-3)
             d["fma_frac"] = round(fma_s / FP32_FMA_PEAK, 4)
         cells.append(d)
@@ -682,7 +695,7 @@ def run_ours(args):
         d["share"] = round(d["avg_ms"] / tot_k, 4)
     dom = max(cells, key=lambda d: d["avg_ms"])
     dom_cell = next(c for c in R.cells if c.name == dom["cell"])
-    if dom_cell.op in ("conv", "conv_bwd_in", "conv_bwd_f") and dom.get("fma_frac", 0) > dom["frac_hbm"]:
+    if dom_cell.op in ("conv", "conv_bwd_in", "conv_bwd_f", "conv2d") and dom.get("fma_frac", 0) > dom["frac_hbm"]:
         achieved = dom_cell.flops / (dom["avg_ms"] * 1e-3) / 1e12
         roofline = {"bound": "alu", "kernel": dom["cell"], "achieved": round(achieved, 2),
                     "peak": round(2 * FP32_FMA_PEAK / 1e12, 2), "unit": "TFLOP/s",
@@ -793,6 +806,11 @@ def oracle_sample_plan(workload: str, frac: float):
                 rows = 1
             x = synth.normal(3, rows * n).reshape(rows, n)
             plan.append((c, lambda x=x, c=c: (oracle.conv1d(x, c.f), x.shape[0] * (x.shape[1] - c.w + 1))[1]))
+        elif c.cfg == "conv2d":
+            planes = max(1, int(round(32 * 64 * frac)))
+            x = synth.uniform01(5, planes * 112 * 112).reshape(planes, 112, 112)
+            oh = (112 - c.kh) // c.sh + 1
+            plan.append((c, lambda x=x, c=c, oh=oh: (oracle.conv2d(x, c.f, c.sh, c.sw), x.shape[0] * oh * oh)[1]))
         elif c.cfg == "backward" and c.op == "pool2d_bwd":
             planes = max(1, int(round(32 * 64 * frac)))
             oh = (112 - c.kh) // c.sh + 1
@@ -891,7 +909,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="suite", choices=["suite", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "stride", "winspec", "affine", "backward"])
+    ap.add_argument("--workload", default="suite", choices=["suite", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "stride", "winspec", "affine", "backward", "conv2d"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="multi-GPU: weak = N x the BASELINE shape (config-sized share per rank), strong = split it")

@@ -61,7 +61,7 @@
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 4
+#define SS_ABI_VERSION 5
 
 typedef enum { SS_F32 = 0, SS_I32 = 1 } ss_dtype_t;
 typedef enum { SS_POOL_MAX = 0, SS_POOL_AVG = 1 } ss_pool_mode_t;
@@ -178,6 +178,19 @@ ss_status_t ss_conv1d_ex(const void* x, void* y, int64_t N, int64_t batch,
 #define SS_AFFINE_W_MAX 65536
 ss_status_t ss_affine_window(const float* u, const float* v, float* U, float* V, int64_t N,
                              int64_t batch, int64_t w, int64_t stride, void* stream);
+
+/* ---- 2-D convolution (multi-dimensional extension, l.226) --
+ * Single-channel 2-D sliding dot product (cross-correlation, valid padding,
+ * DESIGN.md reading R17):
+ *   y[p][r][c] = sum_{a<kh} sum_{b<kw} filter[a*kw + b] * x[p][r*sh + a][c*sw + b]
+ * x is [planes][H][W], y is [planes][(H-kh)/sh+1][(W-kw)/sw+1] (DEVICE, 4-byte
+ * aligned); filter_host is kh*kw floats in HOST memory (row-major), read before
+ * the call returns; kh*kw <= SS_K_MAX.  fp32, each output's products
+ * accumulated with FMA in row-major tap order (deterministic, tiling-
+ * independent).  Statuses as ss_pool2d. */
+ss_status_t ss_conv2d(const void* x, void* y, int64_t planes, int64_t H, int64_t W,
+                      const float* filter_host, int64_t kh, int64_t kw, int64_t sh, int64_t sw,
+                      ss_dtype_t dtype, void* stream);
 
 /* ---- backward passes (training) ----------
  * Vector-Jacobian products of the forward calls above (DESIGN.md reading

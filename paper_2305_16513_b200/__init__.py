@@ -38,7 +38,7 @@ EXPORTED = ("ss_abi_version", "ss_out_len", "ss_pool_sum", "ss_pool_max", "ss_co
             "ss_out_len_ex", "ss_pool_sum_ex", "ss_pool_max_ex", "ss_conv1d_ex",
             "ss_affine_window", "ss_pool_sum_backward", "ss_pool_max_backward",
             "ss_conv1d_backward_input", "ss_conv1d_backward_filter_workspace", "ss_conv1d_backward_filter",
-            "ss_pool2d_backward")
+            "ss_pool2d_backward", "ss_conv2d")
 
 
 class SSError(RuntimeError):
@@ -87,6 +87,8 @@ def _load() -> ctypes.CDLL:
     L.ss_conv1d_backward_filter.restype = i32
     L.ss_pool2d_backward.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i64, i32, i32, vp]
     L.ss_pool2d_backward.restype = i32
+    L.ss_conv2d.argtypes = [vp, vp, i64, i64, i64, ctypes.POINTER(ctypes.c_float), i64, i64, i64, i64, i32, vp]
+    L.ss_conv2d.restype = i32
     L.ss_status_string.argtypes = [i32]
     L.ss_status_string.restype = ctypes.c_char_p
     L.ss_last_error.argtypes = []
@@ -191,6 +193,11 @@ def ss_conv1d_backward_filter(x_ptr, dy_ptr, df_ptr, N, batch, k, stride, ws_ptr
 
 def ss_pool2d_backward(x_ptr, dy_ptr, dx_ptr, planes, H, W, kh, kw, sh, sw, mode, dtype=SS_F32, stream=0) -> int:
     return _lib.ss_pool2d_backward(x_ptr, dy_ptr, dx_ptr, planes, H, W, kh, kw, sh, sw, mode, dtype, stream)
+
+
+def ss_conv2d(x_ptr, y_ptr, planes, H, W, filter_host, kh, kw, sh=1, sw=1, dtype=SS_F32, stream=0) -> int:
+    fp = None if filter_host is None else (ctypes.c_float * len(filter_host))(*[float(v) for v in filter_host])
+    return _lib.ss_conv2d(x_ptr, y_ptr, planes, H, W, fp, kh, kw, sh, sw, dtype, stream)
 
 
 def check(status: int) -> None:
@@ -309,6 +316,27 @@ def pool2d(x, kernel, stride, mode: str = "max", out=None, stream=None):
     shape = tuple(x.shape[:-2]) + (OH, OW)
     y = torch.empty(shape, dtype=x.dtype, device=x.device) if out is None else out
     check(ss_pool2d(x.data_ptr(), y.data_ptr(), planes, H, W, kh, kw, sh, sw, m, _dtype_code(x), _stream(stream)))
+    return y
+
+
+def conv2d(x, filt, stride=(1, 1), out=None, stream=None):
+    """2-D single-channel sliding dot product of a CUDA fp32 [..., H, W] tensor with a host
+    filter [kh, kw] (nested sequence, numpy array or CPU tensor); valid padding."""
+    torch = _torch()
+    if not x.is_cuda or not x.is_contiguous():
+        raise ValueError("x must be a contiguous CUDA tensor")
+    f = filt.tolist() if hasattr(filt, "tolist") else [list(r) for r in filt]
+    kh, kw = len(f), len(f[0])
+    flat = [float(v) for row in f for v in row]
+    sh, sw = stride
+    H, W = x.shape[-2], x.shape[-1]
+    planes = x.numel() // (H * W)
+    OH, OW = ss_out_len(H, kh, sh), ss_out_len(W, kw, sw)
+    if OH < 0 or OW < 0:
+        check(ss_conv2d(x.data_ptr(), 0, planes, H, W, flat, kh, kw, sh, sw, _dtype_code(x), _stream(stream))
+              or SS_ERR_BAD_SIZE)
+    y = torch.empty(tuple(x.shape[:-2]) + (OH, OW), dtype=x.dtype, device=x.device) if out is None else out
+    check(ss_conv2d(x.data_ptr(), y.data_ptr(), planes, H, W, flat, kh, kw, sh, sw, _dtype_code(x), _stream(stream)))
     return y
 
 

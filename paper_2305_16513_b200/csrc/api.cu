@@ -531,6 +531,29 @@ static ss_status_t pool2d_backward_impl(const void* x, const void* dy, void* dx,
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "pool2d_backward launch");
 }
 
+ss_status_t ss_conv2d(const void* x, void* y, int64_t planes, int64_t H, int64_t W, const float* filter_host,
+                      int64_t kh, int64_t kw, int64_t sh, int64_t sw, ss_dtype_t dtype, void* stream) {
+  if (!x || !y || !filter_host) return fail(SS_ERR_NULL, "x, y and filter_host must be non-NULL");
+  if (planes < 1 || H < 1 || W < 1 || kh < 1 || kw < 1 || sh < 1 || sw < 1)
+    return fail(SS_ERR_BAD_SIZE, "planes/H/W/kh/kw/sh/sw must be >= 1");
+  if (H > INT64_MAX / 8 / W || H * W > INT64_MAX / 8 / planes) return fail(SS_ERR_BAD_SIZE, "sizes overflow int64");
+  if (kh > H || kw > W) return fail(SS_ERR_WINDOW_EXCEEDS_INPUT, "window exceeds input: %lldx%lld > %lldx%lld",
+                                    (long long)kh, (long long)kw, (long long)H, (long long)W);
+  if (dtype != SS_F32) return fail(SS_ERR_UNSUPPORTED, "conv2d supports SS_F32 only");
+  if (kh * kw > SS_K_MAX) return fail(SS_ERR_UNSUPPORTED, "kh*kw=%lld > SS_K_MAX=%d", (long long)(kh * kw), SS_K_MAX);
+  if ((reinterpret_cast<uintptr_t>(x) & 3) || (reinterpret_cast<uintptr_t>(y) & 3))
+    return fail(SS_ERR_BAD_SIZE, "x and y must be 4-byte aligned");
+  Conv2DParams p;
+  memset(&p, 0, sizeof p);
+  p.x = static_cast<const float*>(x); p.y = static_cast<float*>(y);
+  p.planes = planes; p.H = H; p.W = W; p.kh = kh; p.kw = kw; p.sh = sh; p.sw = sw;
+  p.OH = (H - kh) / sh + 1; p.OW = (W - kw) / sw + 1;
+  if (overlaps(x, planes * H * W * 4, y, planes * p.OH * p.OW * 4)) return fail(SS_ERR_OVERLAP, "x and y overlap");
+  for (int64_t t = 0; t < kh * kw; ++t) p.taps[t] = filter_host[t];
+  cudaError_t e = launch_conv2d(p, static_cast<cudaStream_t>(stream), current_sms());
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv2d launch");
+}
+
 ss_status_t ss_pool_sum_backward(const void* dy, void* dx, int64_t N, int64_t batch, int64_t w, int64_t stride,
                                  ss_dtype_t dtype, void* stream) {
   return pool_sum_backward_impl(dy, dx, N, batch, w, stride, dtype, stream);

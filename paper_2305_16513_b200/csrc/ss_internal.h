@@ -155,4 +155,15 @@ struct DilatedParams {
 };
 cudaError_t launch_dilated(DilatedParams& p, int op, cudaStream_t stream, int sms);
 
+// 2-D single-channel sliding dot product (conv2d.cu).
+struct Conv2DParams {
+  const float* x;
+  float* y;
+  int64_t planes, H, W, OH, OW, kh, kw, sh, sw;
+  uint32_t stage_bytes;  // set by launch_conv2d
+  int stages;
+  float taps[1024];      // row-major [kh][kw], kh * kw <= SS_K_MAX
+};
+cudaError_t launch_conv2d(Conv2DParams& p, cudaStream_t stream, int grid);
+
 }  // namespace ss

@@ -45,7 +45,7 @@ def test_library_is_sm100a(ss):
 
 
 def test_abi_version_and_out_len(ss):
-    assert ss.ss_abi_version() == 4
+    assert ss.ss_abi_version() == 5
     assert ss.ss_out_len(10, 3, 1) == 8
     assert ss.ss_out_len(10, 3, 4) == 2
     assert ss.ss_out_len(2 ** 32, 31, 1) == 2 ** 32 - 30
@@ -162,4 +162,18 @@ def test_backward_validation(ss):
     assert ss.ss_pool2d_backward(0, G, D, 1, 8, 8, 2, 2, 2, 2, ss.SS_POOL_MAX) == ss.SS_ERR_NULL
     assert ss.ss_pool2d_backward(X, G, D, 1, 8, 8, 9, 2, 2, 2, ss.SS_POOL_AVG) == ss.SS_ERR_WINDOW_EXCEEDS_INPUT
     assert ss.ss_pool2d_backward(X, G, D, 1, 8, 8, 2, 2, 2, 2, 5) == ss.SS_ERR_UNSUPPORTED
+    assert ss.ss_launch_count() == 0
+
+
+def test_conv2d_validation(ss):
+    X, Y = FAKE_X, FAKE_Y
+    f = [1.0] * 9
+    assert ss.ss_conv2d(0, Y, 1, 8, 8, f, 3, 3) == ss.SS_ERR_NULL
+    assert ss.ss_conv2d(X, Y, 1, 8, 8, None, 3, 3) == ss.SS_ERR_NULL
+    assert ss.ss_conv2d(X, Y, 0, 8, 8, f, 3, 3) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_conv2d(X, Y, 1, 8, 8, f, 3, 3, 0, 1) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_conv2d(X, Y, 1, 2, 8, f, 3, 3) == ss.SS_ERR_WINDOW_EXCEEDS_INPUT
+    assert ss.ss_conv2d(X, Y, 1, 8, 8, f, 3, 3, 1, 1, ss.SS_I32) == ss.SS_ERR_UNSUPPORTED
+    assert ss.ss_conv2d(X, X + 16, 1, 8, 8, f, 3, 3) == ss.SS_ERR_OVERLAP
+    assert ss.ss_conv2d(X + 2, Y, 1, 8, 8, f, 3, 3) == ss.SS_ERR_BAD_SIZE
     assert ss.ss_launch_count() == 0
