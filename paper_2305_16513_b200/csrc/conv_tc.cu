@@ -42,6 +42,7 @@
 #include "ss_device.cuh"
 #include "ss_internal.h"
 
+
 namespace ss {
 
 namespace {
@@ -270,7 +271,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
       const uint32_t dcol = dc0 + (uint32_t)(d * NC);
 #pragma unroll 1
       for (int g = 0; g < kGroups; ++g) {
-        bar_wait(full + s, ph);
+        // the split warps observed `full` (TMA data landed) before arriving on
+        // `lofull`, so one wait covers both operands (acquire chain)
         bar_wait(lofull + l, lph);
         if (lane == 0 && g == 0) TC_TRACE(it, 3);
         tc_fence_after();
