@@ -86,6 +86,8 @@ def lib() -> ctypes.CDLL:
             L.oracle_conv1d_backward_filter_f32.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp]
             L.oracle_pool2d_backward_f32.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64,
                                                      ctypes.c_int, vp, vp]
+            L.oracle_conv1d_mc_bf16.argtypes = [vp, vp, i64, i64, i64, i64, i64, vp, vp]
+            L.oracle_conv1d_mc_bf16.restype = ctypes.c_int
             L.oracle_conv2d_f32.argtypes = [vp, i64, i64, i64, vp, i64, i64, i64, i64, vp, vp]
             L.oracle_conv2d_f32.restype = ctypes.c_int
             for n in ("oracle_pool_sum_backward_f32", "oracle_pool_max_backward_f32",
@@ -348,4 +350,32 @@ def conv2d(x: np.ndarray, f: np.ndarray, sh: int = 1, sw: int = 1):
     y = np.empty((P, OH, OW), np.float64)
     m = np.empty((P, OH, OW), np.float64)
     _check(lib().oracle_conv2d_f32(_p(x), P, H, W, _p(f), kh, kw, sh, sw, _p(y), _p(m)))
+    return y, m
+
+
+def to_bf16_bits(a: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even float32 -> bfloat16 bit patterns (uint16)."""
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    r = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
+    return r.astype(np.uint16)
+
+
+def bf16_bits_to_f32(h: np.ndarray) -> np.ndarray:
+    return (np.ascontiguousarray(h, np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+def conv1d_mc(x_bf16: np.ndarray, w_bf16: np.ndarray):
+    """Multi-channel conv1d, channels-last: x [B, N, Cin] and w [Cout, Cin, k] as bf16 bit
+    patterns (uint16); returns (y double [B, L, Cout], absmag)."""
+    x = np.ascontiguousarray(x_bf16, np.uint16)
+    w = np.ascontiguousarray(w_bf16, np.uint16)
+    B, N, cin = x.shape
+    cout, cin2, k = w.shape
+    assert cin2 == cin
+    L = N - k + 1
+    if L < 1:
+        raise ValueError("window exceeds input")
+    y = np.empty((B, L, cout), np.float64)
+    m = np.empty((B, L, cout), np.float64)
+    _check(lib().oracle_conv1d_mc_bf16(_p(x), _p(w), B, N, cin, cout, k, _p(y), _p(m)))
     return y, m

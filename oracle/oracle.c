@@ -509,3 +509,36 @@ int oracle_conv2d_f32(const float* x, int64_t planes, int64_t H, int64_t W, cons
       }
   return 0;
 }
+
+/* Multi-channel 1-D convolution ("with C_in > 1 it becomes a
+ * real contraction"): the sliding dot product of Sec. 2.5 summed over input
+ * channels, channels-last layout, inputs given as bfloat16 bit patterns
+ * (reading R18):
+ *   y[b][i][co] = sum_{j<k} sum_{ci<cin} w[co][ci][j] * x[b][i+j][ci],  i < N-k+1
+ * x [batch][N][cin], w [cout][cin][k] (torch conv1d weight order), y [batch][L][cout],
+ * accumulated in double (terms taken in j, ci order). */
+static double bf16_to_double(uint16_t h) {
+  union { uint32_t u; float f; } c;
+  c.u = (uint32_t)h << 16;
+  return (double)c.f;
+}
+
+int oracle_conv1d_mc_bf16(const uint16_t* x, const uint16_t* w, int64_t batch, int64_t N, int64_t cin,
+                          int64_t cout, int64_t k, double* y, double* absmag) {
+  if (x == NULL || w == NULL || y == NULL || batch < 1 || cin < 1 || cout < 1 || k < 1 || k > N) return -1;
+  int64_t L = N - k + 1;
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t i = 0; i < L; ++i)
+      for (int64_t co = 0; co < cout; ++co) {
+        double acc = 0.0, mag = 0.0;
+        for (int64_t j = 0; j < k; ++j)
+          for (int64_t ci = 0; ci < cin; ++ci) {
+            double t = bf16_to_double(w[(co * cin + ci) * k + j]) * bf16_to_double(x[(b * N + i + j) * cin + ci]);
+            acc += t;
+            mag += fabs(t);
+          }
+        y[(b * L + i) * cout + co] = acc;
+        if (absmag) absmag[(b * L + i) * cout + co] = mag;
+      }
+  return 0;
+}

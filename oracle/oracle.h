@@ -126,6 +126,11 @@ int oracle_pool2d_backward_f32(const float* x, const float* dy, int64_t planes, 
 int oracle_conv2d_f32(const float* x, int64_t planes, int64_t H, int64_t W, const float* f,
                       int64_t kh, int64_t kw, int64_t sh, int64_t sw, double* y, double* absmag);
 
+/* Multi-channel 1-D convolution, channels-last, bfloat16 inputs (bit patterns),
+ * double result: y[b][i][co] = sum_j sum_ci w[co][ci][j] x[b][i+j][ci]. */
+int oracle_conv1d_mc_bf16(const uint16_t* x, const uint16_t* w, int64_t batch, int64_t N, int64_t cin,
+                          int64_t cout, int64_t k, double* y, double* absmag);
+
 #ifdef __cplusplus
 }
 #endif

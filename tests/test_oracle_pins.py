@@ -490,3 +490,37 @@ def test_conv2d_vs_torch_and_1d_reduction():
     y, _ = oracle.conv2d(x, f1)
     y1, _ = oracle.conv1d(x.reshape(-1, 23), f1[0])
     np.testing.assert_array_equal(y.reshape(-1, 18), y1)
+
+
+# ------------------------------------------- multi-channel conv1d (channels-last, bf16 inputs)
+def test_bf16_rounding_helper():
+    # bf16 keeps 8 significant bits: spacing 2^-7 just above 1
+    v = np.array([1.0, 1.0078125, 1.00390625, 1.01171875, -3.14159, 65504.0, 1e-30], np.float32)
+    h = oracle.to_bf16_bits(v)
+    back = oracle.bf16_bits_to_f32(h)
+    np.testing.assert_array_equal(back[:2], [1.0, 1.0078125])                   # representable: exact
+    assert back[2] == 1.0 and back[3] == 1.015625                                # ties -> even mantissa
+    assert np.all(np.abs(back - v) <= np.abs(v) * 2.0 ** -8)                     # RN: half an ulp of 8 bits
+    np.testing.assert_array_equal(oracle.to_bf16_bits(back), h)                  # idempotent
+
+
+def test_conv1d_mc_reduces_to_single_channel_and_sums_channels():
+    B, N, k = 2, 50, 5
+    x = synth.randint(80, B * N * 3, -8, 8).astype(np.float32).reshape(B, N, 3)  # exact in bf16
+    w = synth.randint(81, 2 * 3 * k, -4, 4).astype(np.float32).reshape(2, 3, k)
+    y, _ = oracle.conv1d_mc(oracle.to_bf16_bits(x), oracle.to_bf16_bits(w))
+    for co in range(2):  # = sum over input channels of the 1-D sliding dot product (oracle.conv1d)
+        ref = sum(oracle.conv1d(np.ascontiguousarray(x[:, :, ci]), w[co, ci])[0] for ci in range(3))
+        np.testing.assert_array_equal(y[:, :, co], ref)
+
+
+def test_conv1d_mc_vs_torch():
+    B, N, cin, cout, k = 2, 40, 8, 5, 3
+    xf = synth.normal(82, B * N * cin).reshape(B, N, cin)
+    wf = synth.normal(83, cout * cin * k).reshape(cout, cin, k)
+    xb, wb = oracle.to_bf16_bits(xf), oracle.to_bf16_bits(wf)
+    y, _ = oracle.conv1d_mc(xb, wb)
+    xt = torch.tensor(oracle.bf16_bits_to_f32(xb), dtype=torch.float64).permute(0, 2, 1)  # NCW
+    wt = torch.tensor(oracle.bf16_bits_to_f32(wb), dtype=torch.float64)
+    ref = torch.nn.functional.conv1d(xt, wt).permute(0, 2, 1).numpy()
+    np.testing.assert_allclose(y, ref, rtol=1e-12, atol=1e-12)
