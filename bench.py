@@ -165,6 +165,13 @@ def cfg_cells(workload: str):
             f = synth.normal(70 + kk, kk * kk, sigma=1.0 / kk).reshape(kk, kk)
             cells.append(Cell("conv2d", f"conv2d_{kk}x{kk}_s{st}", "conv2d", kh=kk, kw=kk, sh=st, sw=st, f=f,
                               inp=f"x2d_{i}"))
+    if workload == "mc":  # multi-channel conv1d, channels-last bf16 (tensor cores)
+        for cin, cout, k in ((64, 64, 3), (128, 128, 3), (64, 64, 9)):
+            key = f"xmc{cin}"
+            inputs[key] = dict(rows=16, n=65536 * cin, dtype="bfloat16", dist="normal", seed=96, kw={},
+                               shard="batch")
+            wf = synth.normal(97, cout * cin * k, sigma=(cin * k) ** -0.5).reshape(cout, cin, k)
+            cells.append(Cell("mc", f"mc_c{cin}x{cout}_k{k}", "conv_mc", w=k, f=wf, inp=key, kh=cin, kw=cout))
     if workload == "backward":  # backward passes on config-3 / config-4 shapes; not a BJ config
         inputs["xb"] = dict(rows=64, n=1 << 20, dtype="float32", dist="normal", seed=3, kw={}, shard="batch")
         for k in (7, 31, 63):
@@ -317,6 +324,8 @@ class Runner:
                 r0, r1 = ssd.even_split(sp["rows"], self.world, self.rank)
                 t = torch.empty((r1 - r0, sp["n"]), dtype=dt, device=self.device)
                 synth.fill_device(t, sp["dist"], sp["seed"], start=r0 * sp["n"], **sp["kw"])
+                if sp["dtype"] == "bfloat16":  # generated in fp32, rounded once (untimed)
+                    t = t.to(torch.bfloat16)
                 self.meta[key] = ("batch", (r1 - r0, sp["n"]))
             elif sp["shard"] == "image":
                 i0, i1 = ssd.even_split(sp["images"], self.world, self.rank)
@@ -335,6 +344,18 @@ class Runner:
             es = x.element_size()
             if c.op in BWD_OPS:
                 self._alloc_bwd(c)
+                continue
+            if c.op == "conv_mc":
+                rows, n = geo
+                cin, cout, k = c.kh, c.kw, c.w
+                N = n // cin
+                L = N - k + 1
+                self.y[c.name] = torch.empty((rows, L, cout), dtype=torch.float32, device=self.device)
+                self.wmc = getattr(self, "wmc", {})
+                self.wmc[c.name] = torch.from_numpy(c.f).to(self.device).to(torch.bfloat16).contiguous()
+                c.n_out = rows * L * cout
+                c.bytes = rows * N * cin * 2 + c.n_out * 4 + cout * cin * k * 2
+                c.flops = 2 * k * cin * c.n_out
                 continue
             if c.op in ("pool2d", "conv2d"):
                 B, C, H, W = geo
@@ -456,6 +477,12 @@ class Runner:
         if c.op in BWD_OPS:
             ev0 = self._ev(events)
             self._launch_bwd(c)
+            self._ev_end(events, c, ev0)
+        elif c.op == "conv_mc":
+            rows, n = geo
+            ev0 = self._ev(events)
+            self.ss.check(self.ss.ss_conv1d_mc(x.data_ptr(), self.wmc[c.name].data_ptr(), y.data_ptr(), rows,
+                                               n // c.kh, c.kh, c.kw, c.w, self.stream.cuda_stream))
             self._ev_end(events, c, ev0)
         elif c.op == "conv2d":
             B, C, H, W = geo
@@ -684,7 +711,9 @@ def run_ours(args):
              "gelem_s": round(c.n_out / (avg_ms * 1e-3) / 1e9, 2), "gbs": round(gbs, 1),
              "frac_hbm": round(gbs / peak_hbm, 4), "frac_8tbs": round(gbs / 8000.0, 4),
              "share": 0.0}
-        if conv_on_tensor_cores(c):
+        if c.op == "conv_mc":
+            d["tc_frac"] = round(c.flops / (avg_ms * 1e-3) / 1e12 / (2 * tf32_peak_tflops()), 4)  # bf16 peak
+        elif conv_on_tensor_cores(c):
             d["tc_frac"] = round(c.n_out * TC_FLOP_PER_OUT / (avg_ms * 1e-3) / 1e12 / tf32_peak_tflops(), 4)
         elif c.op in ("conv", "conv_bwd_in", "conv_bwd_f", "conv2d"):
             fma_s = c.flops / 2 / (avg_ms * 1e-3)
@@ -705,7 +734,11 @@ def run_ours(args):
     else:
         roofline = {"bound": "hbm", "kernel": dom["cell"], "achieved": dom["gbs"], "peak": peak_hbm,
                     "unit": "GB/s", "frac": dom["frac_hbm"], "peak_source": peak_src, "traffic": None}
-        if "tc_frac" in dom:  # tensor-core conv: HBM is the roofline (its TC ceiling is higher)
+        if "tc_frac" in dom and dom_cell.op == "conv_mc":
+            roofline["tensor_frac"] = dom["tc_frac"]
+            roofline["tensor_peak_tflops"] = round(2 * tf32_peak_tflops(), 1)
+            roofline["tensor_note"] = "bf16 MMA work (2 k Cin flop/output) / measured dense bf16 peak"
+        elif "tc_frac" in dom:  # tensor-core conv: HBM is the roofline (its TC ceiling is higher)
             roofline["tensor_frac"] = dom["tc_frac"]
             roofline["tensor_peak_tflops"] = round(tf32_peak_tflops(), 1)
             roofline["tensor_note"] = ("executed 3xTF32 MMA work (1152 flop/output) / dense TF32 peak "
@@ -806,6 +839,12 @@ def oracle_sample_plan(workload: str, frac: float):
                 rows = 1
             x = synth.normal(3, rows * n).reshape(rows, n)
             plan.append((c, lambda x=x, c=c: (oracle.conv1d(x, c.f), x.shape[0] * (x.shape[1] - c.w + 1))[1]))
+        elif c.cfg == "mc":
+            cin, cout, k = c.kh, c.kw, c.w
+            n = max(k + 1, int(16 * 65536 * frac))
+            xb = oracle.to_bf16_bits(synth.normal(96, n * cin).reshape(1, n, cin))
+            wb = oracle.to_bf16_bits(c.f)
+            plan.append((c, lambda xb=xb, wb=wb, c=c, n=n: (oracle.conv1d_mc(xb, wb), (n - c.w + 1) * c.kw)[1]))
         elif c.cfg == "conv2d":
             planes = max(1, int(round(32 * 64 * frac)))
             x = synth.uniform01(5, planes * 112 * 112).reshape(planes, 112, 112)
@@ -909,7 +948,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="suite", choices=["suite", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "stride", "winspec", "affine", "backward", "conv2d"])
+    ap.add_argument("--workload", default="suite", choices=["suite", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "stride", "winspec", "affine", "backward", "conv2d", "mc"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="multi-GPU: weak = N x the BASELINE shape (config-sized share per rank), strong = split it")

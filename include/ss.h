@@ -61,7 +61,7 @@
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 5
+#define SS_ABI_VERSION 6
 
 typedef enum { SS_F32 = 0, SS_I32 = 1 } ss_dtype_t;
 typedef enum { SS_POOL_MAX = 0, SS_POOL_AVG = 1 } ss_pool_mode_t;
@@ -191,6 +191,18 @@ ss_status_t ss_affine_window(const float* u, const float* v, float* U, float* V,
 ss_status_t ss_conv2d(const void* x, void* y, int64_t planes, int64_t H, int64_t W,
                       const float* filter_host, int64_t kh, int64_t kw, int64_t sh, int64_t sw,
                       ss_dtype_t dtype, void* stream);
+
+/* ---- multi-channel convolution (a real contraction) -------
+ * y[b][i][co] = sum_{j<k} sum_{ci<cin} w[co][ci][j] * x[b][i+j][ci],  i < N-k+1
+ * (the Sec. 2.5 sliding dot product summed over input channels; DESIGN.md
+ * reading R18).  Channels-last: x is [batch][N][cin] bfloat16, w is
+ * [cout][cin][k] bfloat16 (torch conv1d weight order), y is [batch][N-k+1][cout]
+ * fp32, all DEVICE memory.  bf16 products are exact; accumulation is fp32.
+ * cin, cout in {64, 128}, k <= 9 with 16-B aligned x / y run on the tensor cores
+ * (kind::f16 MMAs, the tap shift is an operand start-address offset); other
+ * shapes run a direct kernel (same definition).  Statuses as above. */
+ss_status_t ss_conv1d_mc(const void* x, const void* w, float* y, int64_t batch, int64_t N,
+                         int64_t cin, int64_t cout, int64_t k, void* stream);
 
 /* ---- backward passes (training) ----------
  * Vector-Jacobian products of the forward calls above (DESIGN.md reading

@@ -38,7 +38,7 @@ EXPORTED = ("ss_abi_version", "ss_out_len", "ss_pool_sum", "ss_pool_max", "ss_co
             "ss_out_len_ex", "ss_pool_sum_ex", "ss_pool_max_ex", "ss_conv1d_ex",
             "ss_affine_window", "ss_pool_sum_backward", "ss_pool_max_backward",
             "ss_conv1d_backward_input", "ss_conv1d_backward_filter_workspace", "ss_conv1d_backward_filter",
-            "ss_pool2d_backward", "ss_conv2d")
+            "ss_pool2d_backward", "ss_conv2d", "ss_conv1d_mc")
 
 
 class SSError(RuntimeError):
@@ -88,6 +88,8 @@ def _load() -> ctypes.CDLL:
     L.ss_pool2d_backward.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i64, i32, i32, vp]
     L.ss_pool2d_backward.restype = i32
     L.ss_conv2d.argtypes = [vp, vp, i64, i64, i64, ctypes.POINTER(ctypes.c_float), i64, i64, i64, i64, i32, vp]
+    L.ss_conv1d_mc.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, vp]
+    L.ss_conv1d_mc.restype = i32
     L.ss_conv2d.restype = i32
     L.ss_status_string.argtypes = [i32]
     L.ss_status_string.restype = ctypes.c_char_p
@@ -198,6 +200,10 @@ def ss_pool2d_backward(x_ptr, dy_ptr, dx_ptr, planes, H, W, kh, kw, sh, sw, mode
 def ss_conv2d(x_ptr, y_ptr, planes, H, W, filter_host, kh, kw, sh=1, sw=1, dtype=SS_F32, stream=0) -> int:
     fp = None if filter_host is None else (ctypes.c_float * len(filter_host))(*[float(v) for v in filter_host])
     return _lib.ss_conv2d(x_ptr, y_ptr, planes, H, W, fp, kh, kw, sh, sw, dtype, stream)
+
+
+def ss_conv1d_mc(x_ptr, w_ptr, y_ptr, batch, N, cin, cout, k, stream=0) -> int:
+    return _lib.ss_conv1d_mc(x_ptr, w_ptr, y_ptr, batch, N, cin, cout, k, stream)
 
 
 def check(status: int) -> None:
@@ -429,3 +435,20 @@ def pool2d_backward(x, dy, kernel, stride, mode: str = "max", out=None, stream=N
     check(ss_pool2d_backward(x.data_ptr() if mode == "max" else 0, dy.data_ptr(), dx.data_ptr(), planes, H, W,
                              kh, kw, sh, sw, m, _dtype_code(dy), _stream(stream)))
     return dx
+
+
+def conv1d_mc(x, w, out=None, stream=None):
+    """Multi-channel conv1d, channels-last: x [B, N, Cin] bfloat16 (CUDA), w [Cout, Cin, k]
+    bfloat16 (CUDA, torch conv1d weight order) -> y [B, N-k+1, Cout] float32."""
+    torch = _torch()
+    if x.dtype != torch.bfloat16 or w.dtype != torch.bfloat16:
+        raise TypeError("conv1d_mc takes bfloat16 x and w")
+    if not (x.is_cuda and w.is_cuda and x.is_contiguous() and w.is_contiguous()):
+        raise ValueError("x and w must be contiguous CUDA tensors")
+    B, N, cin = x.shape
+    cout, cin2, k = w.shape
+    if cin2 != cin:
+        raise ValueError("w's Cin does not match x")
+    y = torch.empty((B, N - k + 1, cout), dtype=torch.float32, device=x.device) if out is None else out
+    check(ss_conv1d_mc(x.data_ptr(), w.data_ptr(), y.data_ptr(), B, N, cin, cout, k, _stream(stream)))
+    return y

@@ -121,6 +121,23 @@ bool encode_chunk_map(CUtensorMap* m, const void* base, int64_t m_ext, int atoms
   return r == CUDA_SUCCESS;
 }
 
+// Channels-last bf16 activations for the multi-channel conv (conv_mc.cu):
+// element (e, p, a) = x[p * cin + 64 a + e]; box {64, 136, cin/64} lands as
+// [atom][position][64] = the SWIZZLE_128B K-major operand, one position per row.
+bool encode_mc_map(CUtensorMap* m, const void* x, int64_t positions, int64_t cin) {
+  auto enc = encode_fn();
+  if (!enc || positions < 1 || positions > (int64_t(1) << 32) || cin % 64) return false;
+  const int64_t at = cin / 64;
+  cuuint64_t dims[3] = {64, (cuuint64_t)positions, (cuuint64_t)at};
+  cuuint64_t strides[2] = {(cuuint64_t)(cin * 2), at > 1 ? 128 : (cuuint64_t)(positions * cin * 2)};
+  cuuint32_t box[3] = {64, 136, (cuuint32_t)at};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(x), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // Tensor-core conv selection: k in [tc_min_k, kConvTcMaxK] at stride 1 without
 // dilation (default 33: measured faster than the FFMA2 tile kernel for every
 // k >= 33 on config 3).  SS_CONV_TC_MIN_K (read once) overrides the threshold, 0 disables
@@ -529,6 +546,31 @@ static ss_status_t pool2d_backward_impl(const void* x, const void* dy, void* dx,
   if (overlaps(dy, ny, dx, nx) || (x && overlaps(x, nx, dx, nx))) return fail(SS_ERR_OVERLAP, "dx overlaps an input");
   cudaError_t e = launch_pool2d_backward(p, static_cast<cudaStream_t>(stream), current_sms());
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "pool2d_backward launch");
+}
+
+ss_status_t ss_conv1d_mc(const void* x, const void* w, float* y, int64_t batch, int64_t N, int64_t cin,
+                         int64_t cout, int64_t k, void* stream) {
+  if (!x || !w || !y) return fail(SS_ERR_NULL, "x, w and y must be non-NULL device pointers");
+  if (batch < 1 || N < 1 || cin < 1 || cout < 1 || k < 1)
+    return fail(SS_ERR_BAD_SIZE, "batch/N/cin/cout/k must all be >= 1");
+  if (N > INT64_MAX / 8 / batch / cin || cout > INT64_MAX / 8 / batch / N || k > INT64_MAX / 8 / cin / cout)
+    return fail(SS_ERR_BAD_SIZE, "sizes overflow int64");
+  if (k > N) return fail(SS_ERR_WINDOW_EXCEEDS_INPUT, "window exceeds input: k=%lld > N=%lld", (long long)k,
+                         (long long)N);
+  if ((reinterpret_cast<uintptr_t>(x) & 1) || (reinterpret_cast<uintptr_t>(w) & 1) ||
+      (reinterpret_cast<uintptr_t>(y) & 3))
+    return fail(SS_ERR_BAD_SIZE, "x / w must be 2-byte and y 4-byte aligned");
+  const int64_t L = N - k + 1;
+  if (overlaps(x, batch * N * cin * 2, y, batch * L * cout * 4) || overlaps(w, cout * cin * k * 2, y, batch * L * cout * 4))
+    return fail(SS_ERR_OVERLAP, "y overlaps an input");
+  ConvMcParams p;
+  memset(&p, 0, sizeof p);
+  p.x = x; p.w = w; p.y = y; p.batch = batch; p.N = N; p.L = L; p.cin = cin; p.cout = cout; p.k = k;
+  const bool tc = (cin == 64 || cin == 128) && (cout == 64 || cout == 128) && k <= 9 &&
+                  (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
+                  encode_mc_map(&p.tm_x, x, batch * N, cin);
+  cudaError_t e = launch_conv_mc(p, tc, static_cast<cudaStream_t>(stream), current_sms());
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv1d_mc launch");
 }
 
 ss_status_t ss_conv2d(const void* x, void* y, int64_t planes, int64_t H, int64_t W, const float* filter_host,

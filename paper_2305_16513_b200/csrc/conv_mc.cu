@@ -1,0 +1,295 @@
+// conv_mc.cu -- multi-channel 1-D convolution (with C_in > 1
+// the sliding dot product of Sec. 2.5, becomes a real
+// contraction): y[b][i][co] = sum_{j<k} sum_ci w[co][ci][j] x[b][i+j][ci],
+// channels-last bf16 activations and weights, fp32 accumulation and output
+// (reading R18).
+//
+// Tensor-core formulation (kind::f16, BF16 x BF16 -> F32 in TMEM): a tile is
+// 128 consecutive positions (M = 128, TMEM lanes) x all C_out channels
+// (N = C_out).  For tap j the A operand is the staged input tile shifted by j
+// positions -- channels-last, one position's C_in channels are one 128-B
+// K-atom row (per 64 channels), so the shift is a start-address offset of j
+// rows in the canonical SWIZZLE_128B K-major layout (no im2col) -- and the B
+// operand is w[:, :, j] (C_out x C_in, K-major), staged once per CTA.  The k
+// taps x C_in/16 K-steps accumulate into one TMEM accumulator:
+//     D[m][co] += sum_ci X[p0 + m + j][ci] W_j[co][ci]
+// Products of bf16 values are exact in fp32; accumulation is fp32.
+//
+// Warps (persistent CTA per SM, 320 threads): 0 TMA producer (3-D box over
+// [flat position][atom][64] of x per tile into a 3-stage ring), 1 MMA issuer
+// (one elected lane), 2-9 epilogue (tcgen05.ld 16x256b: four lanes hold 32
+// contiguous bytes of an output row, so stores are whole sectors; channels
+// split over two warps per lane quarter; positions whose window leaves their
+// batch row are masked).  Two TMEM accumulators.
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "ss_device.cuh"
+#include "ss_internal.h"
+
+namespace ss {
+
+namespace {
+
+constexpr int kMcThreads = 320;
+constexpr int kMcWarpMma = 1;
+constexpr int kMcWarpEpi0 = 2;
+constexpr int kMcEpiWarps = 8;
+constexpr int kMcRows = 136;  // staged positions per tile: 128 + k - 1 <= 136, a multiple of 8
+constexpr int kMcStages = 3;
+
+__device__ __forceinline__ uint64_t sw128_desc_mc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// kind::f16 instruction descriptor: D f32, A bf16, B bf16, both K-major, N, M.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16_ss(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mc_commit(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mc_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n}" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ __attribute__((unused)) void mc_tmem_ld16(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+// 16 TMEM lanes x 256 bits: thread t gets columns 2(t%4), 2(t%4)+1 of lanes
+// t/4 (v0, v1) and t/4 + 8 (v2, v3) -> four threads hold 32 contiguous bytes
+// of a row, so a warp's stores are whole 32-B sectors.
+__device__ __forceinline__ void mc_tmem_ld_16x256(uint32_t taddr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_mc(void* smem_dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                               int32_t c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace
+
+template <int CIN, int COUT>
+__global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_constant__ ConvMcParams p) {
+  constexpr int AT = CIN / 64;                        // K-atoms (64 bf16 = 128 B) per position
+  constexpr uint32_t kAtomBytes = kMcRows * 128u;     // one atom of a staged tile
+  constexpr uint32_t kStage = AT * kAtomBytes;
+  constexpr uint32_t kWTap = AT * COUT * 128u;        // one tap of the weights
+  constexpr int NH = COUT / 2;                        // epilogue columns per warp
+  constexpr uint32_t kTmemCols = 2 * COUT <= 128 ? 128 : 256;
+  extern __shared__ __align__(1024) uint8_t mc_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(mc_raw) + 1023) & ~uintptr_t(1023));
+  const int k = (int)p.k;
+  uint8_t* xs = smem;                                  // [kMcStages][AT][kMcRows][128 B]
+  uint8_t* ws = smem + kMcStages * kStage;             // [k][AT][COUT][128 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ws + (size_t)k * kWTap);
+  uint64_t* full = bars;                               // [kMcStages]
+  uint64_t* empty = full + kMcStages;                  // [kMcStages]
+  uint64_t* dfull = empty + kMcStages;                 // [2]
+  uint64_t* dempty = dfull + 2;                        // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kMcStages; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(dfull + i, 1); mbar_init(dempty + i, kMcEpiWarps); }
+    fence_mbar_init();
+    prefetch_tmap(&p.tm_x);
+  }
+  // weights: w[co][ci][j] (bf16) -> tap j, atom ci/64, row co, 16-B chunk (ci%64)/8 ^ (co%8)
+  {
+    const uint16_t* __restrict__ w = static_cast<const uint16_t*>(p.w);
+    const int total = COUT * CIN * k;
+    for (int e = threadIdx.x; e < total; e += kMcThreads) {
+      const int j = e % k, ci = (e / k) % CIN, co = e / (k * CIN);
+      const uint32_t off = (uint32_t)j * kWTap + (uint32_t)(ci >> 6) * (COUT * 128u) + (uint32_t)co * 128u +
+                           ((((uint32_t)(ci & 63) >> 3) ^ ((uint32_t)co & 7u)) << 4) + 2u * (uint32_t)(ci & 7);
+      *reinterpret_cast<uint16_t*>(ws + off) = __ldg(w + e);
+    }
+  }
+  fence_proxy_async_smem();  // generic-proxy weight writes -> tensor core reads
+  if (warp == kMcWarpMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "n"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const int64_t ntiles = p.ntiles;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        mbar_wait(empty + s, ph ^ 1);
+        mbar_arrive_expect_tx(full + s, kStage);
+        tma_load_3d_mc(xs + (size_t)s * kStage, &p.tm_x, 0, (int32_t)(t * 128), 0, full + s);
+        if (++s == kMcStages) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == kMcWarpMma) {
+    constexpr uint32_t idesc = idesc_bf16(128, COUT);
+    const uint64_t dx0 = sw128_desc_mc(__shfl_sync(0xffffffffu, smem_u32(xs), 0));
+    const uint64_t dw0 = sw128_desc_mc(__shfl_sync(0xffffffffu, smem_u32(ws), 0));
+    const uint32_t dc0 = __shfl_sync(0xffffffffu, tmem, 0);
+    int s = 0, d = 0;
+    uint32_t ph = 0, dph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mc_wait(dempty + d, dph ^ 1);
+      mc_wait(full + s, ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t dcol = dc0 + (uint32_t)(d * COUT);
+      const uint64_t dxs = dx0 + (uint64_t)((s * kStage) >> 4);
+      uint32_t acc = 0;
+#pragma unroll 1
+      for (int j = 0; j < k; ++j) {
+#pragma unroll
+        for (int a = 0; a < AT; ++a)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {  // K-steps of 16 channels (32 B) inside the atom
+            const uint64_t da = dxs + (uint64_t)((a * kAtomBytes + (uint32_t)j * 128u + 32u * q) >> 4);
+            const uint64_t db = dw0 + (uint64_t)(((uint32_t)j * kWTap + a * (COUT * 128u) + 32u * q) >> 4);
+            mma_bf16_ss(dcol, da, db, idesc, acc);
+            acc = 1;
+          }
+      }
+      mc_commit(empty + s);
+      mc_commit(dfull + d);
+      if (++s == kMcStages) { s = 0; ph ^= 1; }
+      if (++d == 2) { d = 0; dph ^= 1; }
+    }
+  } else {
+    // epilogue: quarter q's lanes (positions p0 + 32 q + [0, 32)) are read as two
+    // 16-lane halves; warp half h stores channels [h NH, (h+1) NH)
+    const int q = warp & 3, h = (warp - kMcWarpEpi0) >> 2;
+    int d = 0;
+    uint32_t dph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mc_wait(dfull + d, dph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t v[2][NH / 8][4];
+#pragma unroll
+      for (int lh = 0; lh < 2; ++lh)
+#pragma unroll
+        for (int cb = 0; cb < NH / 8; ++cb)
+          mc_tmem_ld_16x256(tmem + ((uint32_t)(32 * q + 16 * lh) << 16) + (uint32_t)(d * COUT + h * NH + 8 * cb),
+                            v[lh][cb]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dempty + d);
+#pragma unroll
+      for (int lh = 0; lh < 2; ++lh)
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {  // rows lane/4 and lane/4 + 8 of this 16-lane half
+          const int m = 32 * q + 16 * lh + (lane >> 2) + 8 * rr;
+          const int64_t pos = t * 128 + m;  // flat input position = window start
+          const int64_t b = pos / p.N, i = pos - b * p.N;
+          if (b < p.batch && i < p.L) {
+            float* __restrict__ yr = p.y + (b * p.L + i) * COUT + h * NH + 2 * (lane & 3);
+#pragma unroll
+            for (int cb = 0; cb < NH / 8; ++cb)
+              *reinterpret_cast<float2*>(yr + 8 * cb) =
+                  make_float2(__uint_as_float(v[lh][cb][2 * rr]), __uint_as_float(v[lh][cb][2 * rr + 1]));
+          }
+        }
+      if (++d == 2) { d = 0; dph ^= 1; }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == kMcWarpMma)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+}
+
+// Direct kernel (any shape / alignment): one (position, channel) per thread,
+// fp32 accumulation of the exact bf16 products in (j, ci) order.
+__global__ void __launch_bounds__(256) conv_mc_direct_kernel(const __grid_constant__ ConvMcParams p) {
+  const uint16_t* __restrict__ x = static_cast<const uint16_t*>(p.x);
+  const uint16_t* __restrict__ w = static_cast<const uint16_t*>(p.w);
+  const int64_t total = p.batch * p.L * p.cout;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t co = o % p.cout, r = o / p.cout, i = r % p.L, b = r / p.L;
+    float acc = 0.0f;
+    for (int64_t j = 0; j < p.k; ++j)
+      for (int64_t ci = 0; ci < p.cin; ++ci) {
+        const float xv = __uint_as_float((uint32_t)__ldg(x + (b * p.N + i + j) * p.cin + ci) << 16);
+        const float wv = __uint_as_float((uint32_t)__ldg(w + (co * p.cin + ci) * p.k + j) << 16);
+        acc = __fmaf_rn(wv, xv, acc);
+      }
+    p.y[o] = acc;
+  }
+}
+
+size_t conv_mc_smem_bytes(int64_t cin, int64_t cout, int64_t k) {
+  const size_t stage = (size_t)(cin / 64) * kMcRows * 128;
+  return 1024 + kMcStages * stage + (size_t)k * (cin / 64) * cout * 128 + 8 * (2 * kMcStages + 4) + 16;
+}
+
+template <int CIN, int COUT>
+static cudaError_t launch_mc(ConvMcParams& p, cudaStream_t stream, int sms) {
+  const size_t smem = conv_mc_smem_bytes(CIN, COUT, p.k);
+  if (smem > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
+  auto kfn = conv_mc_kernel<CIN, COUT>;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
+  if (e != cudaSuccess) return e;
+  const int64_t g = p.ntiles < sms ? p.ntiles : sms;
+  kfn<<<(unsigned)(g < 1 ? 1 : g), kMcThreads, smem, stream>>>(p);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t stream, int sms) {
+  if (tensor_path) {
+    p.ntiles = (p.batch * p.N + 127) / 128;
+    cudaError_t e = cudaErrorInvalidConfiguration;
+    if (p.cin == 64 && p.cout == 64) e = launch_mc<64, 64>(p, stream, sms);
+    else if (p.cin == 64 && p.cout == 128) e = launch_mc<64, 128>(p, stream, sms);
+    else if (p.cin == 128 && p.cout == 64) e = launch_mc<128, 64>(p, stream, sms);
+    else if (p.cin == 128 && p.cout == 128) e = launch_mc<128, 128>(p, stream, sms);
+    if (e != cudaErrorInvalidConfiguration) return e;
+  }
+  const int64_t total = p.batch * p.L * p.cout;
+  int64_t g = (total + 255) / 256;
+  if (g > (int64_t)sms * 16) g = (int64_t)sms * 16;
+  conv_mc_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace ss

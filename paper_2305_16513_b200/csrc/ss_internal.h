@@ -166,4 +166,16 @@ struct Conv2DParams {
 };
 cudaError_t launch_conv2d(Conv2DParams& p, cudaStream_t stream, int grid);
 
+// Multi-channel conv1d, channels-last bf16 (conv_mc.cu).
+struct alignas(64) ConvMcParams {
+  CUtensorMap tm_x;  // 3-D {64, batch*N, cin/64}, strides {cin*2 B, 128 B}, box {64, 136, cin/64}, SW128, bf16
+  const void* x;     // [batch][N][cin] bf16
+  const void* w;     // [cout][cin][k] bf16
+  float* y;          // [batch][L][cout] fp32
+  int64_t batch, N, L, cin, cout, k;
+  int64_t ntiles;    // set by launch_conv_mc
+};
+bool encode_mc_map(CUtensorMap* m, const void* x, int64_t positions, int64_t cin);
+cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t stream, int sms);
+
 }  // namespace ss

@@ -45,7 +45,7 @@ def test_library_is_sm100a(ss):
 
 
 def test_abi_version_and_out_len(ss):
-    assert ss.ss_abi_version() == 5
+    assert ss.ss_abi_version() == 6
     assert ss.ss_out_len(10, 3, 1) == 8
     assert ss.ss_out_len(10, 3, 4) == 2
     assert ss.ss_out_len(2 ** 32, 31, 1) == 2 ** 32 - 30
@@ -176,4 +176,15 @@ def test_conv2d_validation(ss):
     assert ss.ss_conv2d(X, Y, 1, 8, 8, f, 3, 3, 1, 1, ss.SS_I32) == ss.SS_ERR_UNSUPPORTED
     assert ss.ss_conv2d(X, X + 16, 1, 8, 8, f, 3, 3) == ss.SS_ERR_OVERLAP
     assert ss.ss_conv2d(X + 2, Y, 1, 8, 8, f, 3, 3) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_launch_count() == 0
+
+
+def test_conv1d_mc_validation(ss):
+    X, W, Y = FAKE_X, FAKE_X + 0x1000000, FAKE_Y
+    assert ss.ss_conv1d_mc(0, W, Y, 1, 100, 64, 64, 3) == ss.SS_ERR_NULL
+    assert ss.ss_conv1d_mc(X, W, Y, 0, 100, 64, 64, 3) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_conv1d_mc(X, W, Y, 1, 100, 64, 64, 0) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_conv1d_mc(X, W, Y, 1, 2, 64, 64, 3) == ss.SS_ERR_WINDOW_EXCEEDS_INPUT
+    assert ss.ss_conv1d_mc(X + 1, W, Y, 1, 100, 64, 64, 3) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_conv1d_mc(X, W, X + 64, 1, 100, 64, 64, 3) == ss.SS_ERR_OVERLAP
     assert ss.ss_launch_count() == 0
