@@ -220,6 +220,201 @@ __global__ void __launch_bounds__(kBwThreads) pool_max_backward_direct_kernel(co
   }
 }
 
+// Unit stride, w <= 8R: O(1) work per element in registers.  A tile is
+// kRunTile(R) = 256 R - 8 R positions [t0, t0 + T); its 256 R windows start at
+// t0 - (w - 1) (the ones outside [0, L) get sentinel keys), R consecutive per
+// thread.  (1) The thread's R window argmaxes by the pivot split of Alg. 2
+// at its block end: suffix first-argmax over its own R inputs
+// (right to left, ties to the earlier index), one running prefix argmax over
+// the next w - 1 inputs (left to right, strictly greater), combined per window
+// with the suffix side winning ties; w <= R scans each window directly.
+// (2) The keys a_i are non-decreasing (see the tile kernel), so dx is a
+// reduce-by-key of dy over sorted keys: each thread sums its runs left to
+// right, a run that continues into the following threads is completed by the
+// thread where it starts from their published head partials (in order), and
+// the run owner writes dx_t into the zeroed smem tile.  x and dy are staged
+// with 4-B cp.async into a layout padded by one word per R, so the stride-R
+// reads of a warp hit distinct banks.
+template <int R>
+struct RunTile {
+  static constexpr int kWindows = kBwThreads * R;
+  static constexpr int kMaxW = 8 * R;
+  static constexpr int kPositions = kWindows - kMaxW;
+  static constexpr int kXSpan = kWindows + kMaxW;
+  __host__ __device__ static constexpr int pad(int e) { return e + e / R; }
+  static constexpr int kXFloats = (kXSpan + kXSpan / R + 4) & ~3;
+  static constexpr int kGFloats = (kWindows + kWindows / R + 4) & ~3;
+  static constexpr int kStageFloats = kXFloats + kGFloats;
+  static constexpr size_t kSmem =
+      sizeof(float) * (size_t)(2 * kStageFloats + kPositions + kPositions / R + 4) + 4 * sizeof(int) * kBwThreads;
+};
+
+template <int R>
+__global__ void __launch_bounds__(kBwThreads) pool_max_backward_run_kernel(const __grid_constant__ BackwardParams p) {
+  using RT = RunTile<R>;
+  extern __shared__ __align__(16) float mr_smem[];
+  // two stages of {x[t0 - (w-1) + e] at pad(e), dy[t0 - (w-1) + j] at pad(j)}: tile n+1 streams in
+  // while tile n is evaluated
+  float* dxs = mr_smem + 2 * RT::kStageFloats;  // dx tile at pad(t - t0): run owners write stride-R keys
+  float* Hs = dxs + RT::kPositions + RT::kPositions / R + 4;  // head-run partial of each thread
+  int* Ks = reinterpret_cast<int*>(Hs + kBwThreads);  // first key of each thread
+  int* Ls = Ks + kBwThreads;                    // last key
+  int* Fs = Ls + kBwThreads;                    // 1: the thread is one run
+  const float* __restrict__ x = static_cast<const float*>(p.x);
+  const float* __restrict__ dy = static_cast<const float*>(p.dy);
+  float* __restrict__ dx = static_cast<float*>(p.dx);
+  const int w = (int)p.w;
+  constexpr int T = RT::kPositions;
+  const int64_t tiles_per_row = (p.N + T - 1) / T;
+  const int64_t ntiles = p.batch * tiles_per_row;
+  const int tid = threadIdx.x, j0 = tid * R;
+  constexpr int kLow = INT32_MIN / 2, kHigh = INT32_MAX / 2;  // sentinel keys outside any tile
+  // (row, tile-in-row) cursors: issue runs one tile ahead of compute; advanced without divisions
+  const int64_t step_b = gridDim.x / tiles_per_row, step_t = gridDim.x - step_b * tiles_per_row;
+  int64_t ib = blockIdx.x / tiles_per_row, it = blockIdx.x - ib * tiles_per_row;
+  int64_t cb = ib, ct = it;
+  auto advance = [&](int64_t& b, int64_t& t) {
+    b += step_b;
+    t += step_t;
+    if (t >= tiles_per_row) { t -= tiles_per_row; ++b; }
+  };
+  // valid staged ranges [lo, hi) of a tile: x index ws + e in [0, N), window ws + j in [0, L)
+  struct Range { int xlo, xhi, glo, ghi; };
+  auto ranges = [&](int64_t t) {
+    const int64_t ws = t * T - (w - 1);
+    Range r;
+    r.xlo = ws < 0 ? (int)-ws : 0;
+    r.glo = r.xlo;
+    const int64_t xh = p.N - ws, gh = p.L - ws;
+    r.xhi = xh < RT::kXSpan ? (int)xh : RT::kXSpan;
+    r.ghi = gh < RT::kWindows ? (gh < 0 ? 0 : (int)gh) : RT::kWindows;
+    return r;
+  };
+  auto issue = [&](int st) {
+    if (ib < p.batch) {
+      const Range rg = ranges(it);
+      const int64_t ws = it * T - (w - 1);
+      const float* xr = x + ib * p.N + ws;   // may point before the row: only valid e are read
+      const float* gr = dy + ib * p.L + ws;
+      float* xs = mr_smem + st * RT::kStageFloats;
+      const uint32_t xd = smem_u32(xs + RT::pad(tid)), gd = smem_u32(xs + RT::kXFloats + RT::pad(tid));
+      const int xspan = RT::kWindows + w - 1;
+      // pad(e + 256 u) = pad(e) + (256 + 256 / R) u
+#pragma unroll
+      for (int u = 0; u < (RT::kXSpan + kBwThreads - 1) / kBwThreads; ++u) {
+        const int e = tid + u * kBwThreads;
+        if (e < xspan) {
+          const bool ok = e >= rg.xlo && e < rg.xhi;
+          cp_async4(xd + 4u * (kBwThreads + kBwThreads / R) * u, ok ? xr + e : x, ok ? 4u : 0u);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < RT::kWindows / kBwThreads; ++u) {
+        const int e = tid + u * kBwThreads;
+        const bool ok = e >= rg.glo && e < rg.ghi;
+        cp_async4(gd + 4u * (kBwThreads + kBwThreads / R) * u, ok ? gr + e : dy, ok ? 4u : 0u);
+      }
+      advance(ib, it);
+    }
+    cp_async_commit();
+  };
+  issue(0);
+  int st = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t t0 = ct * T;
+    const int nt = (int)(t0 + T < p.N ? T : p.N - t0);
+    const Range rg = ranges(ct);
+    float* __restrict__ dxr = dx + cb * p.N + t0;
+    advance(cb, ct);
+    for (int e = tid; e < nt; e += kBwThreads) dxs[RT::pad(e)] = 0.0f;  // own store-loop slots: already read
+    issue(st ^ 1);
+    cp_async_wait<1>();
+    __syncthreads();
+    const float* xs = mr_smem + st * RT::kStageFloats;
+    const float* gs = xs + RT::kXFloats;
+    // (1) first maximum of windows j0 .. j0 + R - 1, as positions relative to t0
+    int key[R];
+    if (w > R) {
+      float sv[R];
+      int si[R];
+#pragma unroll
+      for (int r = R - 1; r >= 0; --r) {
+        const float v = xs[RT::pad(j0 + r)];
+        if (r == R - 1 || v >= sv[r + 1 < R ? r + 1 : r]) { sv[r] = v; si[r] = j0 + r; }
+        else { sv[r] = sv[r + 1 < R ? r + 1 : r]; si[r] = si[r + 1 < R ? r + 1 : r]; }
+      }
+      float pv = -INFINITY;
+      int pi = 0;
+      for (int m = R; m < w - 1; ++m) {
+        const float v = xs[RT::pad(j0 + m)];
+        if (v > pv) { pv = v; pi = j0 + m; }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const float v = xs[RT::pad(j0 + w - 1 + r)];
+        if (v > pv) { pv = v; pi = j0 + w - 1 + r; }
+        key[r] = (pv > sv[r] ? pi : si[r]) - (w - 1);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        float m = xs[RT::pad(j0 + r)];
+        int a = j0 + r;
+        for (int q = 1; q < w; ++q) {
+          const float v = xs[RT::pad(j0 + r + q)];
+          if (v > m) { m = v; a = j0 + r + q; }
+        }
+        key[r] = a - (w - 1);
+      }
+    }
+    float g[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (j0 + r < rg.glo) key[r] = kLow;
+      else if (j0 + r >= rg.ghi) key[r] = kHigh;
+      g[r] = gs[RT::pad(j0 + r)];
+    }
+    // (2) runs: head partial, interior runs written here, last run carried
+    auto put = [&](int k, float v) {
+      if (k >= 0 && k < nt) dxs[RT::pad(k)] = v;
+    };
+    int cur = key[0];
+    float acc = g[0], head = 0.0f;
+    bool single = true;
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      if (key[r] != cur) {
+        if (single) head = acc;
+        else put(cur, acc);
+        single = false;
+        cur = key[r];
+        acc = g[r];
+      } else {
+        acc = __fadd_rn(acc, g[r]);
+      }
+    }
+    if (single) head = acc;
+    Hs[tid] = head;
+    Ks[tid] = key[0];
+    Ls[tid] = key[R - 1];
+    Fs[tid] = single ? 1 : 0;
+    __syncthreads();
+    auto chain = [&](int k, float total) {
+      for (int u = tid + 1; u < kBwThreads && Ks[u] == k; ++u) {
+        total = __fadd_rn(total, Hs[u]);
+        if (!Fs[u]) break;
+      }
+      return total;
+    };
+    if (tid == 0 || Ls[tid - 1] != key[0]) put(key[0], single ? chain(key[0], head) : head);
+    if (!single) put(cur, chain(cur, acc));
+    __syncthreads();  // dx tile complete; stage st and Hs / Ks / Ls / Fs are free again
+    for (int e = tid; e < nt; e += kBwThreads) dxr[e] = dxs[RT::pad(e)];
+    st ^= 1;
+  }
+  cp_async_wait<0>();
+}
+
 // Fallback for w > kMaxTileW: windows in chunks, argmax of each recomputed from
 // global memory, then each position gathers the chunk's windows routed to it.
 constexpr int kMaxChunk = 1024;
@@ -280,197 +475,162 @@ __global__ void __launch_bounds__(kBwThreads) pool_max_backward_kernel(const __g
 }
 
 // ---------------------------------------------------------------- conv filter gradient
-// Unit stride (the common case): grid (ctas, tap blocks of 64).  Tile =
-// kFgTile consecutive outputs i of one row; the CTA's 256 threads are 4 tap
-// groups (16 taps) x 64 run slots (16 outputs).  Per tile a thread adds
-// dy_i x_{i+j} over its 16 x 16 block in fp32 with the 31 inputs it needs in
-// registers, then folds the 16 partial sums into fp64 accumulators; at the end
-// the 64 run slots of each tap group are reduced in fixed order and the CTA
-// writes 64 fp64 partials.  Tiles stream through a kFgStages-deep ring of
-// shared-memory stages filled with 4-B cp.async (rows have any alignment),
-// padded by 4 floats per 16 so the LDS.128 of 8 consecutive run slots hit
-// distinct bank groups.
-// Strided: grid (ctas, k); each CTA sums dy_i x_{is+j} for one tap over a
-// grid-strided share of the outputs (fp32 runs of 16, then fp64).
+// Unit stride (the common case): grid (ctas, tap blocks of 64), tile-pair
+// kernel below.  Strided: grid (ctas, k); each CTA sums dy_i x_{is+j} for one
+// tap over a grid-strided share of the outputs (fp32 runs of 16, then fp64).
 // Finish: sums the CTA partials of each tap in fixed order.
-constexpr int kFgTaps = 64;
-constexpr int kFgRun = 16;
-constexpr int kFgSlots = 64;
-constexpr int kFgTile = kFgRun * kFgSlots;  // 1024 outputs
-constexpr int kFgStages = 4;
-constexpr int kFgFold = 4;  // tiles accumulated in fp32 (64 terms per partial) before folding into fp64
-constexpr int kFgXSpan = kFgTile + kFgTaps;  // inputs one tile needs (unit stride)
-__host__ __device__ constexpr int fg_pad(int e) { return e + 4 * (e >> 4); }
-// stages hold x / dy from the 16-B-aligned-down address of the tile's first
-// element on (up to 3 leading elements), in the padded layout
-constexpr int kFgXStride = (fg_pad(kFgXSpan + 4) + 16) & ~3;      // padded x floats per stage
-constexpr int kFgStageFloats = kFgXStride + fg_pad(kFgTile + 8) + 8;
-constexpr size_t kFgSmem = (size_t)kFgStages * kFgStageFloats * sizeof(float);
+constexpr int kFgTaps = 64;   // taps per tap block (partials layout)
+constexpr int kFgRun = 16;    // outputs per thread and tile
+constexpr int kFgFold = 4;    // tile pairs accumulated in fp32 (16 terms each) before folding into fp64
 
-// (row, tile-in-row) of a grid-strided tile sequence, advanced without divisions
-struct TileCursor {
-  int64_t b, tr, tpr, step;
-  __device__ void init(int64_t tile, int64_t tiles_per_row, int64_t stride) {
-    tpr = tiles_per_row;
-    step = stride;
-    b = tile / tpr;
-    tr = tile - b * tpr;
-  }
-  __device__ void advance() {
-    tr += step;
-    while (tr >= tpr) { tr -= tpr; ++b; }
-  }
+// Tile-pair kernel (unit stride).  Two tiles A, B are staged INTERLEAVED
+// (pair e = (v_A[e], v_B[e]) for x and dy), so every FFMA2 operand is an
+// aligned register pair straight from an LDS.128 -- (acc_A, acc_B)[j] +=
+// (x_A, x_B)[m+j] * (dy_A, dy_B)[m] -- with no register shuffling (the
+// per-tile tap-pair form needs odd-aligned x pairs: ~0.8 MOV per FFMA2).
+// Q tap groups of 16 taps (Q = 1, 2, 4 by k) x 256/Q run slots of 16
+// outputs; pair index e sits at float offset 2e + 4 (e >> 4), so the 16-pair
+// blocks of neighbouring run slots start in different bank groups.  Stages
+// are filled with 4-B cp.async (rows have any alignment; the interleave is
+// element-granular).  A thread accumulates its 16 x 16 block in fp32 and
+// folds into fp64 every kFgFold tile pairs; at the end the run slots of each
+// tap are reduced in fixed order and the CTA writes its fp64 partials.
+template <int Q>
+struct FgPair {
+  static constexpr int kSlots = kBwThreads / Q;
+  static constexpr int kTile = kFgRun * kSlots;  // outputs per tile
+  static constexpr int kTaps = 16 * Q;
+  static constexpr int kXSpan = kTile + kTaps;   // inputs per tile
+  static constexpr int kStages = Q == 4 ? 3 : 2;
+  __host__ __device__ static constexpr int pad2(int e) { return 2 * e + 4 * (e >> 4); }
+  static constexpr int kXFloats = pad2(kXSpan) + 8;
+  static constexpr int kStageFloats = kXFloats + pad2(kTile) + 8;
+  static constexpr size_t kSmem = (size_t)kStages * kStageFloats * sizeof(float);
 };
 
-// stage `n` elements from src (any alignment) at padded local indices mis .. mis+n-1,
-// mis = src's element offset in its 16-B granule; elements of the leading granule
-// before src are filled too (never read) when they lie inside [lo_ok, src)
-__device__ __forceinline__ void fg_stage(float* sdst, const float* __restrict__ src, int n, int64_t avail,
-                                         bool aligned_ok, int mis) {
-  if (aligned_ok) {
-    const float* base = src - mis;
-    const int lim = (int)(avail < n ? avail : n) + mis;  // valid elements from base (32-bit)
-    for (int e = 4 * threadIdx.x; e < n + mis; e += 4 * kBwThreads) {
-      const int left = lim - e;
-      const uint32_t nb = left >= 4 ? 16u : (left > 0 ? 4u * (uint32_t)left : 0u);
-      cp_async16(smem_u32(sdst + fg_pad(e)), nb ? base + e : src, nb);
-    }
-  } else {
-    for (int e = threadIdx.x; e < n; e += kBwThreads)
-      cp_async4(smem_u32(sdst + fg_pad(e + mis)), e < avail ? src + e : src, e < avail ? 4u : 0u);
-  }
-}
-
-// Unit-stride filter gradient.  Inner product per thread and tile: 16 outputs
-// m x 16 taps jj, acc[jj] += dy_m x_{m+jj}, as FFMA2 over tap pairs
-// (acc[jj], acc[jj+1]) += dy_m * (x_{m+jj}, x_{m+jj+1}); the input window is
-// kept twice (pairs starting at even and at odd offsets) so every pair is an
-// aligned register pair.  x and dy stream with 16-B cp.async from their
-// aligned-down addresses; the tile-uniform misalignment of x selects one of
-// four compile-time realignments (MX), dy is read with 32-bit loads.
-template <int MX, int MG>
-__device__ __forceinline__ void fg_tile(const float* xs, const float* gs, int base, int m0, float2 (&acc)[8]) {
-  // x window [base, base + 32) sits at local indices base + MX + (0..31): 9 aligned float4;
-  // dy run [m0, m0 + 16) at local m0 + MG + (0..15): 5 aligned float4
-  float w[36], gv[20];
-#pragma unroll
-  for (int c = 0; c < 36; c += 4) {
-    const float4 v = *reinterpret_cast<const float4*>(xs + fg_pad(base + c));
-    w[c] = v.x; w[c + 1] = v.y; w[c + 2] = v.z; w[c + 3] = v.w;
-  }
-#pragma unroll
-  for (int c = 0; c < 20; c += 4) {
-    const float4 v = *reinterpret_cast<const float4*>(gs + fg_pad(m0 + c));
-    gv[c] = v.x; gv[c + 1] = v.y; gv[c + 2] = v.z; gv[c + 3] = v.w;
-  }
-  float2 E[16], O[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) E[i] = make_float2(w[MX + 2 * i], w[MX + 2 * i + 1]);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) O[i] = make_float2(w[MX + 2 * i + 1], w[MX + 2 * i + 2]);
-#pragma unroll
-  for (int mt = 0; mt < kFgRun; ++mt) {
-    const float2 g2 = make_float2(gv[MG + mt], gv[MG + mt]);
-#pragma unroll
-    for (int i = 0; i < 8; ++i)  // taps 2i, 2i+1: inputs x_{mt+2i}, x_{mt+2i+1}
-      acc[i] = __ffma2_rn((mt & 1) ? O[(mt >> 1) + i] : E[(mt >> 1) + i], g2, acc[i]);
-  }
-}
-
-template <int MX>
-__device__ __forceinline__ void fg_tile_g(const float* xs, const float* gs, int misg, int base, int m0,
-                                          float2 (&acc)[8]) {
-  switch (misg) {  // tile-uniform
-    case 0: fg_tile<MX, 0>(xs, gs, base, m0, acc); break;
-    case 1: fg_tile<MX, 1>(xs, gs, base, m0, acc); break;
-    case 2: fg_tile<MX, 2>(xs, gs, base, m0, acc); break;
-    default: fg_tile<MX, 3>(xs, gs, base, m0, acc); break;
-  }
-}
-
-__global__ void __launch_bounds__(kBwThreads, 2) conv_filter_grad_kernel(const __grid_constant__ BackwardParams p,
-                                                                         double* __restrict__ partials) {
-  extern __shared__ __align__(16) float fg_smem[];
-  double* red = reinterpret_cast<double*>(fg_smem);  // reused for the final reduction
+template <int Q>
+__global__ void __launch_bounds__(kBwThreads) conv_filter_grad_pair_kernel(const __grid_constant__ BackwardParams p,
+                                                                           double* __restrict__ partials) {
+  using F = FgPair<Q>;
+  constexpr int S = F::kStages;
+  extern __shared__ __align__(16) float fp_smem[];
+  double* red = reinterpret_cast<double*>(fp_smem);  // reused for the final reduction
   const float* __restrict__ x = static_cast<const float*>(p.x);
   const float* __restrict__ dy = static_cast<const float*>(p.dy);
   const int64_t j0 = (int64_t)blockIdx.y * kFgTaps;
-  const int q = threadIdx.x & 3, r = threadIdx.x >> 2;  // tap group, run slot
-  const int64_t tiles_per_row = (p.L + kFgTile - 1) / kFgTile;
+  const int q = threadIdx.x % Q, r = threadIdx.x / Q;  // tap group, run slot
+  const int64_t tiles_per_row = (p.L + F::kTile - 1) / F::kTile;
   const int64_t ntiles = p.batch * tiles_per_row;
-  TileCursor ic, cc;  // issue cursor (kFgStages-1 tiles ahead) and compute cursor
-  ic.init(blockIdx.x, tiles_per_row, gridDim.x);
-  cc = ic;
-  int64_t itile = blockIdx.x;
+  const int64_t npairs = (ntiles + 1) / 2;
+  int64_t ipair = blockIdx.x;
+  // (row, tile-in-row) of tile A = 2 ipair, advanced by 2 gridDim.x tiles per issue without divisions
+  const int64_t step = 2 * (int64_t)gridDim.x, step_b = step / tiles_per_row, step_t = step - step_b * tiles_per_row;
+  int64_t cb = 2 * (int64_t)blockIdx.x / tiles_per_row, ct = 2 * (int64_t)blockIdx.x - cb * tiles_per_row;
+  // one tile into lane 0 (A) or 1 (B) of the interleaved stage; 4-B cp.async (rows have any
+  // alignment), compile-time trip counts, pad2(e + 256 u) = pad2(e) + 576 u
+  auto stage_tile = [&](float* xs, float* gs, int64_t b, int64_t t, int lane) {
+    const float* xsrc = x;
+    const float* gsrc = dy;
+    int xav = 0, gav = 0;
+    if (b < p.batch) {
+      const int64_t i0 = t * F::kTile;
+      xsrc = x + b * p.N + i0 + j0;
+      gsrc = dy + b * p.L + i0;
+      const int64_t xa = p.N - i0 - j0, ga = p.L - i0;
+      xav = xa < 0 ? 0 : (xa < F::kXSpan ? (int)xa : F::kXSpan);
+      gav = ga < F::kTile ? (int)ga : F::kTile;
+    }
+    static_assert(F::pad2(kBwThreads) == 576 && F::kTile % kBwThreads == 0, "stage stride");
+    const int tid = threadIdx.x;
+    const uint32_t xd = smem_u32(xs + F::pad2(tid) + lane), gd = smem_u32(gs + F::pad2(tid) + lane);
+#pragma unroll
+    for (int u = 0; u < (F::kXSpan + kBwThreads - 1) / kBwThreads; ++u) {
+      const int e = tid + u * kBwThreads;
+      if ((u + 1) * kBwThreads <= F::kXSpan || e < F::kXSpan) {
+        const bool ok = e < xav;
+        cp_async4(xd + 2304u * u, ok ? xsrc + e : x, ok ? 4u : 0u);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < F::kTile / kBwThreads; ++u) {
+      const int e = tid + u * kBwThreads;
+      const bool ok = e < gav;
+      cp_async4(gd + 2304u * u, ok ? gsrc + e : dy, ok ? 4u : 0u);
+    }
+  };
   auto issue = [&](int st) {
-    if (itile < ntiles) {
-      float* xs = fg_smem + st * kFgStageFloats;
-      float* gs = xs + kFgXStride;
-      const int64_t i0 = ic.tr * kFgTile;
-      const int64_t nout = p.L - i0 < kFgTile ? p.L - i0 : kFgTile;
-      const int64_t xg = ic.b * p.N + i0 + j0, gg = ic.b * p.L + i0;  // element offsets from x / dy
-      const int misx = (int)((reinterpret_cast<uintptr_t>(x + xg) >> 2) & 3);
-      const int misg = (int)((reinterpret_cast<uintptr_t>(dy + gg) >> 2) & 3);
-      fg_stage(xs, x + xg, kFgXSpan, p.N - i0 - j0, xg >= misx, misx);
-      fg_stage(gs, dy + gg, kFgTile, nout, gg >= misg, misg);
-      ic.advance();
-      itile += gridDim.x;
+    if (ipair < npairs) {
+      float* xs = fp_smem + st * F::kStageFloats;
+      float* gs = xs + F::kXFloats;
+      stage_tile(xs, gs, cb, ct, 0);
+      if (ct + 1 < tiles_per_row) stage_tile(xs, gs, cb, ct + 1, 1);
+      else stage_tile(xs, gs, cb + 1, 0, 1);
+      ipair += gridDim.x;
+      cb += step_b;
+      ct += step_t;
+      if (ct >= tiles_per_row) { ct -= tiles_per_row; ++cb; }
     }
     cp_async_commit();
   };
 #pragma unroll 1
-  for (int st = 0; st < kFgStages - 1; ++st) issue(st);
+  for (int st = 0; st < S - 1; ++st) issue(st);
   double acc64[16];
 #pragma unroll
-  for (int jj = 0; jj < 16; ++jj) acc64[jj] = 0.0;
-  float2 acc[8];
+  for (int i = 0; i < 16; ++i) acc64[i] = 0.0;
+  float2 acc[16];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) acc[i] = make_float2(0.0f, 0.0f);
+  for (int i = 0; i < 16; ++i) acc[i] = make_float2(0.0f, 0.0f);
+  const int xb = F::pad2(16 * (r + q)), gb = F::pad2(16 * r);  // 16-pair blocks: offsets are block-uniform
   int st = 0, nfold = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    issue((st + kFgStages - 1) % kFgStages);
-    cp_async_wait<kFgStages - 1>();  // this tile's group has landed (for this thread)
-    __syncthreads();                 // ... and for every thread
-    const float* xs = fg_smem + st * kFgStageFloats;
-    const float* gs = xs + kFgXStride;
-    const int64_t i0 = cc.tr * kFgTile;
-    const int misx = (int)((reinterpret_cast<uintptr_t>(x + cc.b * p.N + i0 + j0) >> 2) & 3);
-    const int misg = (int)((reinterpret_cast<uintptr_t>(dy + cc.b * p.L + i0) >> 2) & 3);
-    cc.advance();
-    const int m0 = kFgRun * r;
-    const int base = m0 + 16 * q;
-    switch (misx) {  // tile-uniform
-      case 0: fg_tile_g<0>(xs, gs, misg, base, m0, acc); break;
-      case 1: fg_tile_g<1>(xs, gs, misg, base, m0, acc); break;
-      case 2: fg_tile_g<2>(xs, gs, misg, base, m0, acc); break;
-      default: fg_tile_g<3>(xs, gs, misg, base, m0, acc); break;
+  for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+    issue((st + S - 1) % S);
+    cp_async_wait<S - 1>();
+    __syncthreads();
+    const float* xs = fp_smem + st * F::kStageFloats;
+    const float* gs = xs + F::kXFloats;
+    float2 X[32], G[16];
+#pragma unroll
+    for (int c = 0; c < 32; c += 2) {  // pairs c, c+1 of the x window; block boundary at c = 16
+      const float4 v = *reinterpret_cast<const float4*>(xs + xb + 2 * c + (c >= 16 ? 4 : 0));
+      X[c] = make_float2(v.x, v.y);
+      X[c + 1] = make_float2(v.z, v.w);
     }
+#pragma unroll
+    for (int c = 0; c < 16; c += 2) {
+      const float4 v = *reinterpret_cast<const float4*>(gs + gb + 2 * c);
+      G[c] = make_float2(v.x, v.y);
+      G[c + 1] = make_float2(v.z, v.w);
+    }
+#pragma unroll
+    for (int mt = 0; mt < kFgRun; ++mt)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] = __ffma2_rn(X[mt + i], G[mt], acc[i]);
     if (++nfold == kFgFold) {
       nfold = 0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        acc64[2 * i] += (double)acc[i].x;
-        acc64[2 * i + 1] += (double)acc[i].y;
+      for (int i = 0; i < 16; ++i) {
+        acc64[i] += (double)acc[i].x;
+        acc64[i] += (double)acc[i].y;
         acc[i] = make_float2(0.0f, 0.0f);
       }
     }
     __syncthreads();  // stage st is refilled by the next iteration's issue
-    st = st + 1 == kFgStages ? 0 : st + 1;
+    st = st + 1 == S ? 0 : st + 1;
   }
   cp_async_wait<0>();
   __syncthreads();
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    acc64[2 * i] += (double)acc[i].x;
-    acc64[2 * i + 1] += (double)acc[i].y;
+  for (int i = 0; i < 16; ++i) {
+    acc64[i] += (double)acc[i].x;
+    acc64[i] += (double)acc[i].y;
   }
-  // reduce the 64 run slots of each tap group, fixed order
+  static_assert(F::kSmem >= (size_t)F::kTaps * F::kSlots * sizeof(double), "reduction fits the stages");
 #pragma unroll
-  for (int jj = 0; jj < 16; ++jj) red[(16 * q + jj) * kFgSlots + r] = acc64[jj];
+  for (int i = 0; i < 16; ++i) red[(16 * q + i) * F::kSlots + r] = acc64[i];
   __syncthreads();
-  if (threadIdx.x < kFgTaps) {
+  if (threadIdx.x < F::kTaps) {
     double s = 0.0;
-    for (int rr = 0; rr < kFgSlots; ++rr) s += red[threadIdx.x * kFgSlots + rr];
+    for (int rr = 0; rr < F::kSlots; ++rr) s += red[threadIdx.x * F::kSlots + rr];
     partials[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * kFgTaps + threadIdx.x] = s;
   }
 }
@@ -524,11 +684,18 @@ cudaError_t launch_conv_filter_grad(const BackwardParams& p, float* df, void* wo
   double* part = static_cast<double*>(workspace);
   const bool strided = p.stride != 1;
   if (!strided) {
-    static_assert(kFgSmem >= (size_t)kFgTaps * kFgSlots * sizeof(double), "reduction fits the stages");
-    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(conv_filter_grad_kernel));
-    if (e != cudaSuccess) return e;
     const int tap_blocks = (int)((p.w + kFgTaps - 1) / kFgTaps);
-    conv_filter_grad_kernel<<<dim3((unsigned)ctas, (unsigned)tap_blocks), kBwThreads, kFgSmem, stream>>>(p, part);
+    const dim3 grid((unsigned)ctas, (unsigned)tap_blocks);
+    auto launch = [&](auto kfn, size_t smem) {
+      cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
+      if (e == cudaSuccess) kfn<<<grid, kBwThreads, smem, stream>>>(p, part);
+      return e;
+    };
+    // Q tap groups of 16: k <= 16 -> 1, k <= 32 -> 2, else 4 per 64-tap block
+    cudaError_t e = p.w <= 16   ? launch(conv_filter_grad_pair_kernel<1>, FgPair<1>::kSmem)
+                    : p.w <= 32 ? launch(conv_filter_grad_pair_kernel<2>, FgPair<2>::kSmem)
+                                : launch(conv_filter_grad_pair_kernel<4>, FgPair<4>::kSmem);
+    if (e != cudaSuccess) return e;
   } else {
     conv_filter_grad_strided_kernel<<<dim3((unsigned)ctas, (unsigned)p.w), kBwThreads, 0, stream>>>(p, part);
   }
@@ -773,6 +940,24 @@ cudaError_t launch_pool_max_backward(const BackwardParams& p, cudaStream_t strea
   const int64_t tiles = p.batch * ((p.N + kMaxTile - 1) / kMaxTile);
   const int64_t cap = (int64_t)sms * 8;
   const unsigned g = (unsigned)(tiles < cap ? tiles : cap);
+  if (p.stride == 1 && p.w <= RunTile<16>::kMaxW) {
+    auto launch = [&](auto kfn, int positions, size_t smem) {
+      cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
+      if (e != cudaSuccess) return e;
+      const int64_t t = p.batch * ((p.N + positions - 1) / positions);
+      int per_sm = 0;  // resident CTAs: one wave of the grid-strided tile loop
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kBwThreads, smem);
+      if (e != cudaSuccess) return e;
+      const int64_t c = (int64_t)sms * (per_sm < 1 ? 1 : per_sm);
+      const unsigned gr = (unsigned)(t < c ? (t < 1 ? 1 : t) : c);
+      kfn<<<gr, kBwThreads, smem, stream>>>(p);
+      note_launch();
+      return cudaGetLastError();
+    };
+    if (p.w <= RunTile<8>::kMaxW)
+      return launch(pool_max_backward_run_kernel<8>, RunTile<8>::kPositions, RunTile<8>::kSmem);
+    return launch(pool_max_backward_run_kernel<16>, RunTile<16>::kPositions, RunTile<16>::kSmem);
+  }
   if (p.w <= kMaxDirectW && p.stride <= kMaxTileS) {
     const size_t smem = sizeof(float) * (size_t)(2 * kMaxTile + 3 * kMaxDirectW + kMaxTileS + 2) +
                         sizeof(int) * (size_t)(kMaxTile + kMaxDirectW + 2);

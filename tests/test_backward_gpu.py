@@ -48,6 +48,8 @@ def within(y, ref, mag, what):
 POOL_CASES = [  # (B, N, w, s)
     (1, 1, 1, 1), (2, 9, 3, 1), (3, 1000, 8, 1), (2, 70001, 64, 1), (1, 40000, 257, 1), (2, 1001, 4, 2),
     (3, 999, 7, 3), (1, 5000, 2, 2), (2, 777, 9, 4), (1, 3000, 1, 5), (4, 20000, 33, 1),
+    # unit-stride run kernel: tile edges (1984 / 3968 positions), R = 8 and R = 16 tiles
+    (2, 5000, 16, 1), (1, 1984, 5, 1), (2, 3969, 64, 1), (1, 9000, 65, 1), (3, 7000, 128, 1), (1, 130, 129, 1),
 ]
 
 
@@ -96,6 +98,36 @@ def test_pool_max_backward(ss, B, N, w, s, ties):
         np.testing.assert_array_equal(dx.cpu().numpy().reshape(B, N).astype(np.float64), ref)
 
 
+@pytest.mark.parametrize("w", [3, 8, 9, 40, 64, 100, 128])
+@pytest.mark.parametrize("pattern", ["spikes", "rising", "falling", "flat"])
+def test_pool_max_backward_runs(ss, w, pattern):
+    # long and short routing runs: a spike is the first maximum of up to w windows
+    # (runs spanning several threads), rising / falling / flat inputs route every
+    # window to its last / first / first element
+    B, N = 2, 6000
+    L = N - w + 1
+    t = np.arange(B * N, dtype=np.float64)
+    if pattern == "spikes":
+        x = synth.normal(25, B * N).astype(np.float64)
+        x[::97] = 50.0
+    elif pattern == "rising":
+        x = t
+    elif pattern == "falling":
+        x = -t
+    else:
+        x = np.zeros(B * N)
+    x = x.astype(np.float32).reshape(B, N)
+    dy = synth.normal(26, B * L).reshape(B, L)
+    buf, dx = out_buf(B * N)
+    xd, dyd = dev(x), dev(dy)
+    ss.check(ss.ss_pool_max_backward(xd.data_ptr(), dyd.data_ptr(), dx.data_ptr(), N, B, w, 1))
+    torch.cuda.synchronize()
+    assert canary_ok(buf, 0, B * N)
+    ref = oracle.pool_max_backward(x, dy, w, 1)
+    mag = oracle.pool_max_backward(x, np.abs(dy), w, 1)
+    within(dx.cpu().numpy().reshape(B, N), ref, mag, f"max bwd runs w={w} {pattern}")
+
+
 CONV_CASES = [  # (B, N, k, s)
     (1, 10, 1, 1), (2, 1000, 3, 1), (3, 20001, 7, 1), (2, 70000, 31, 1), (2, 50000, 40, 1), (1, 80001, 63, 1),
     (3, 30000, 64, 1), (1, 9000, 100, 1), (2, 3001, 5, 2), (3, 4000, 9, 3), (1, 5000, 64, 4), (2, 999, 13, 7),
@@ -117,7 +149,9 @@ def test_conv_backward_input(ss, B, N, k, s):
 
 
 FILTER_CASES = CONV_CASES + [(1, 5000, 65, 1), (2, 3000, 130, 1), (1, 7000, 200, 3), (64, 4096, 63, 1),
-                             (5, 1500, 1024, 1)]
+                             (5, 1500, 1024, 1),
+                             # tile-pair kernel: Q = 1 / 2 / 4 tap-group edges, odd tile counts, N < one tile
+                             (2, 9000, 16, 1), (1, 12000, 17, 1), (3, 8200, 32, 1), (1, 300, 33, 1), (7, 1025, 2, 1)]
 
 
 @pytest.mark.parametrize("B,N,k,s", FILTER_CASES)
