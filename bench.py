@@ -54,10 +54,12 @@ import numpy as np  # noqa: E402
 METRIC = "output GElem/s and achieved HBM GB/s (% of ~8 TB/s) for sliding pool/conv1d"
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback if MEASURED_PEAKS.json is absent
 FP32_FMA_PEAK = 148 * 128 * 1.965e9  # FMA/s: SMs x FP32 lanes x max SM clock
-# Tensor-core conv1d (csrc/conv_tc.cu): 33 <= k <= 64 at stride 1, dilation 1; every
-# output costs 3 TF32 MMA products (3xTF32) over the K = 192 Toeplitz depth.
+# Tensor-core conv1d (csrc/conv_tc.cu): 33 <= k <= 64 at stride 1, dilation 1; over the K = 192
+# Toeplitz depth every output costs one TF32 product (xh fh, 384 flop) and one bf16 correction
+# product of depth 2K (768 flop at twice the TF32 rate): 768 TF32-equivalent flop per output
+# (the 3xTF32 mode, SS_CONV_TC_MIXED=0, executes 1152).
 TC_CONV_K = (33, 64)
-TC_FLOP_PER_OUT = 3 * 192 * 2
+TC_FLOP_PER_OUT = 3 * 192 * 2 if os.environ.get("SS_CONV_TC_MIXED", "1") == "0" else 2 * 192 * 2
 
 
 BWD_OPS = ("conv_bwd_in", "conv_bwd_f", "sum_bwd", "max_bwd", "pool2d_bwd")
@@ -741,8 +743,9 @@ def run_ours(args):
         elif "tc_frac" in dom:  # tensor-core conv: HBM is the roofline (its TC ceiling is higher)
             roofline["tensor_frac"] = dom["tc_frac"]
             roofline["tensor_peak_tflops"] = round(tf32_peak_tflops(), 1)
-            roofline["tensor_note"] = ("executed 3xTF32 MMA work (1152 flop/output) / dense TF32 peak "
-                                       "(measured bf16 / 2)")
+            roofline["tensor_note"] = (f"executed MMA work ({TC_FLOP_PER_OUT} TF32-equivalent flop/output: "
+                                       "xh*fh in TF32 + one bf16 correction product at half weight) / dense "
+                                       "TF32 peak (measured bf16 / 2)")
     roofline["share_of_step"] = dom["share"]
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):  # dram bytes per launch from a committed `ncu --set full` capture

@@ -109,10 +109,13 @@ ss_status_t ss_pool_max(const void* x, void* y, int64_t N, int64_t batch,
  *     tap index alone, so every output is independent of tiling and sharding.
  *   33 <= k <= 64 at stride 1, and (conv1d_ex) dilated filters with
  *     (k-1)*dilation + 1 <= 64 at stride 1: tensor cores (Toeplitz matrix
- *     product), 3xTF32 (x f ~ xh fh + xh fl + xl fh) with fp32
- *     accumulation; within the bound below with >10x margin, bitwise
- *     deterministic run to run, but an output's rounding depends on its
- *     position modulo 8 in the 16-B-aligned view of x.
+ *     product): x f ~ xh fh (TF32, xh / fh = fp32 truncated to
+ *     TF32) + bf16(xh) bf16(fl) + bf16(xl) bf16(fh) (one bf16 MMA), fp32
+ *     accumulation; per-product error <= ~2^-18 |x f|, within the bound below
+ *     (measured worst error / bound 0.27; environment SS_CONV_TC_MIXED=0 selects
+ *     3xTF32, 0.08).  Bitwise deterministic run to run, but an output's
+ *     rounding depends on its position modulo 8 in the 16-B-aligned view of x
+ *     (tensor-core conv).
  * One filter shared by all rows.  `filter_host` (k floats, HOST memory) is read
  * before the call returns and may be freed immediately.  dtype must be SS_F32;
  * 1 <= k <= SS_K_MAX. */

@@ -71,6 +71,38 @@ static int current_sms() {
   return num_sms(dev);
 }
 
+static int env_int(const char* name, int dflt);
+
+// Dynamic tile scheduler slots (ss_internal.h): a per-device pool of zeroed
+// {next, done} counter pairs; each persistent-kernel launch takes the next slot
+// and the kernel's last CTA zeroes it again on exit.  Launches on one stream
+// reuse slots in order; a slot is only shared by two RUNNING launches if
+// kSchedSlots launches were enqueued while one of them was still running.
+// nullptr (static round-robin tiles) when the pool cannot be made, e.g. on
+// first use inside a stream capture.
+static unsigned long long* sched_slot(cudaStream_t stream) {
+  static std::mutex mu;
+  static unsigned long long* pool[128] = {nullptr};
+  static std::atomic<uint64_t> next{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 128) return nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pool[dev]) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+      void* ptr = nullptr;
+      const size_t bytes = (size_t)kSchedSlots * 2 * sizeof(unsigned long long);
+      if (cudaMalloc(&ptr, bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+      if (cudaMemset(ptr, 0, bytes) != cudaSuccess) { cudaGetLastError(); cudaFree(ptr); return nullptr; }
+      pool[dev] = static_cast<unsigned long long*>(ptr);
+    }
+  }
+  static int on = env_int("SS_DYNAMIC_TILES", 1);
+  if (!on) return nullptr;
+  return pool[dev] + 2 * (next.fetch_add(1, std::memory_order_relaxed) % kSchedSlots);
+}
+
 // cuTensorMapEncodeTiled from the driver, without linking libcuda.
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -197,6 +229,9 @@ static bool try_conv_tc(const void* x, float* y_int, int64_t N, int64_t batch, i
   p.trace = tc_trace_buf();
   static int lo_slots = env_int("SS_CONV_TC_LO", 0);
   p.lo_bufs = lo_slots;
+  static int mixed = env_int("SS_CONV_TC_MIXED", 1);
+  p.mixed = mixed;
+  p.sched = sched_slot(s);
   *err = launch_conv_tc(p, nc, s, grid);
   if (*err == cudaErrorInvalidConfiguration) { *err = cudaSuccess; return false; }
   g_tc_launches.fetch_add(1, std::memory_order_relaxed);

@@ -16,25 +16,39 @@
 //
 // fp32 accuracy with TF32 MMAs (kind::tf32, fp32 accumulation in TMEM):
 // the tensor core truncates fp32 operands to TF32 (measured:
-// tools/ubench/tc_conv_probe.cu), so with x = xh + xl, xh = trunc(x),
-// xl = x - xh (exact), and likewise f = fh + fl,
-//     x f ~= xh fh + xh fl + xl fh
-// ("3xTF32"): relative error per product <= ~3 * 2^-22, i.e. within the
-// BASELINE.json bound 1e-5 * sum|x f| + 1e-6 with > 10x margin.  The
-// Toeplitz rows of fh and fl are written to TMEM once; xl is computed per
-// tile by 4 "split" warps into a second smem buffer.
+// tools/ubench/tc_conv_probe.cu); with x = xh + xl, xh = trunc(x), xl = x - xh
+// (exact), and likewise f = fh + fl:
+//   mixed (default): per K-step of 8 kk, ONE kind::f16 MMA of K = 16 computes
+//     the correction [bf16(xh) | bf16(xl)] . [bf16(fl) | bf16(fh)], then
+//     D += xh fh (kind::tf32): two MMAs instead of three.  Per-product error
+//     <= ~2^-18 |x f| (bf16 rounding of the two 2^-10-sized correction terms,
+//     plus the dropped xl fl), inside BASELINE.json's 1e-5 sum|x f| + 1e-6
+//     (measured worst err / bound 0.27 over tools/tc_conv_check.py parity).
+//     The 16-bit A operand layout in TMEM (column c = K indices 2c, 2c + 1) is
+//     measured by tools/ubench/tc_bf16_tmem_probe.cu.
+//   3xTF32 (SS_CONV_TC_MIXED=0): D += xh fl + xl fh + xh fh, ~3 * 2^-22 (worst
+//     err / bound 0.08).
+// The Toeplitz rows of fh and of the correction (fl, or bf16 {fl | fh}) are
+// written to TMEM once; the split warps build the per-tile correction operand
+// (xl, or bf16 {xh | xl}) in a second smem ring.
 //
 // Warp roles (persistent CTA per SM, 576 threads):
-//   warp 0      TMA producer (one lane): 3-D box {32, NC, atoms} per tile
-//   warp 1      MMA issuer (one elected lane, warp-uniform operands):
-//               per K-step  D += Alo*Bhi, D += Ahi*Blo, D += Ahi*Bhi
-//   warps 2-9   split: Blo = x - trunc(x) over the staged tile
+//   warp 0      TMA producer (one lane): 3-D box {32, NC, 3} per K-atom group;
+//               starts streaming while the other roles set up TMEM; claims
+//               tiles from the launch's dynamic counter slot (ss_internal.h),
+//               so SMs that run faster take more tiles
+//   warp 1      MMA issuer (one elected lane, warp-uniform operands)
+//   warps 2-9   split: correction operand of each staged group
 //   warps 10-17 epilogue: TMEM -> registers (tcgen05.ld 32x32b) -> one
 //               coalesced 128-B store per warp per chunk column (a tile
 //               inside one batch row stores with immediate offsets; tiles
 //               crossing a row edge mask outputs whose window leaves the row)
 // Pipelines: hi stages (TMA -> split/MMA), lo buffers (split -> MMA), two
-// TMEM accumulators (MMA -> epilogue).
+// TMEM accumulators (MMA -> epilogue), a ring of tile ids (producer -> all).
+// A transposed formulation (x as the A operand from one contiguous TMA tile
+// by row shifts, the filter Toeplitz as an N = 32 B operand; K = 96) was
+// built and measured slower (160 us vs 117 us at k = 63): with A from shared
+// memory every N = 32 MMA re-reads a 4 KB A slice.
 #include <cstdint>
 
 #include <cuda_runtime.h>
@@ -54,6 +68,13 @@ constexpr int kTcSplitWarps = 8;
 constexpr int kTcWarpEpi0 = kTcWarpSplit0 + kTcSplitWarps;
 constexpr int kTcEpiWarps = 8;  // two per TMEM lane quarter, each half of the chunk columns
 constexpr int kTcThreads = 32 * (kTcWarpEpi0 + kTcEpiWarps);
+// Tile ids travel producer -> consumers through a smem ring: the split warps
+// read slot it % kTcTileRing after their `full` wait for the tile's first group
+// and the MMA warp after its `lofull` wait (the existing acquire chain), the
+// epilogue warps through their own tfull / tempty barriers.  The producer
+// cannot run kTcTileRing tiles ahead of the MMA warp (its hi ring holds fewer).
+constexpr int kTcTileRing = 16;
+constexpr int kTcTileReaders = kTcEpiWarps;  // warps that release a ring slot
 
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   uint64_t d = 0;
@@ -67,6 +88,24 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 // kind::tf32 instruction descriptor: D f32, A/B tf32, K-major both, N, M.
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// kind::f16 instruction descriptor with bf16 A and B (format code 1).
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// {lo, hi} -> one 32-bit word of two bf16 (round to nearest even); lo = lower K index
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
 }
 // D[tmem] (+)= A[tmem] * B[smem desc]; issued by one elected lane of the
 // calling (converged) warp.
@@ -140,8 +179,21 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
 // event into p.trace[tile_iter * 8 + event].
 #define TC_TRACE(it, ev)                                                                 \
   do {                                                                                   \
-    if (p.trace && blockIdx.x == 0 && (it) < 64) p.trace[(it) * 8 + (ev)] = clock64(); \
+    if (p.trace && blockIdx.x == 0 && (it) < 63) p.trace[(it) * 8 + (ev)] = clock64(); \
   } while (0)
+// row 63: {globaltimer, clock64} at kernel entry, after setup, and at exit (thread 0 of CTA 0)
+// entries [512 + 2 b] / [512 + 2 b + 1]: globaltimer at entry / exit of CTA b (b < 256)
+__device__ __forceinline__ void tc_trace_stamp(unsigned long long* tr, int slot) {
+  if (tr && threadIdx.x == (slot == 2 ? 32 * kTcWarpMma : 0)) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    if (blockIdx.x == 0) {
+      tr[63 * 8 + 2 * slot] = g;
+      tr[63 * 8 + 2 * slot + 1] = clock64();
+    }
+    if (slot != 1 && blockIdx.x < 256) tr[512 + 2 * blockIdx.x + (slot == 2 ? 1 : 0)] = g;
+  }
+}
 
 // Fixed MMA depth: K = 192 (6 K-atoms of 32, 24 K-steps of 8) serves every
 // k <= 65 (the Toeplitz is zero beyond k); the pipelines move groups of
@@ -158,7 +210,7 @@ template <int NC> struct TcShape {
   static constexpr int kDBufs = NC == 128 ? 1 : 2;
 };
 
-template <int NC>
+template <int NC, bool kMixed>
 __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_constant__ ConvTCParams p) {
   static_assert(NC % 32 == 0 && NC <= 128, "NC/2 columns per epilogue warp, loaded 16 at a time");
   constexpr int kGroup = TcShape<NC>::kGroup, kGroups = TcShape<NC>::kGroups, ND = TcShape<NC>::kDBufs;
@@ -178,14 +230,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
   uint64_t* loempty = lofull + SL;      // [SL] MMA commit -> split
   uint64_t* dfull = loempty + SL;       // [ND] MMA commit -> epilogue
   uint64_t* dempty = dfull + 2;         // [ND] epilogue -> MMA
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
+  uint64_t* tfull = dempty + 2;         // [kTcTileRing] producer -> epilogue: tile id published
+  uint64_t* tempty = tfull + kTcTileRing;  // [kTcTileRing] the epilogue warps have read it
+  int64_t* tring = reinterpret_cast<int64_t*>(tempty + kTcTileRing);  // tile ids (-1: no more tiles)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tring + kTcTileRing);
   float* fsm = reinterpret_cast<float*>(tslot + 4);  // [2][kConvTcMaxK + 256] zero-padded hi/lo taps
 
   // ---- setup: barriers, TMEM, taps -----------------------------------------
+  tc_trace_stamp(p.trace, 0);
   if (threadIdx.x == 0) {
     for (int i = 0; i < SH; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
     for (int i = 0; i < SL; ++i) { mbar_init(lofull + i, kTcSplitWarps); mbar_init(loempty + i, 1); }
     for (int i = 0; i < ND; ++i) { mbar_init(dfull + i, 1); mbar_init(dempty + i, kTcEpiWarps); }
+    for (int i = 0; i < kTcTileRing; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, kTcTileReaders); }
     fence_mbar_init();
     prefetch_tmap(&p.tm_b);
   }
@@ -207,13 +264,63 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // the producer starts streaming now; the other roles wait (named barrier 1)
+  // until the Toeplitz operands are in TMEM
+  if (warp == kTcWarpProducer) {
+    tc_trace_stamp(p.trace, 1);
+    if (lane == 0) {
+      // tiles: CTA b starts with tile b, then claims tiles from the launch's
+      // counter slot (dynamic: SMs that run faster take more tiles) or, without
+      // a slot, strides by gridDim.x
+      int s = 0;
+      uint32_t ph = 0;
+      int64_t t = blockIdx.x;
+      for (int it = 0;; ++it) {
+        const int ts = it % kTcTileRing;
+        bar_wait(tempty + ts, ((uint32_t)(it / kTcTileRing) & 1u) ^ 1u);
+        tring[ts] = t < p.ntiles ? t : -1;
+        mbar_arrive(tfull + ts);
+        if (t >= p.ntiles) {
+          // end marker for the split warps (and, through them, the MMA warp): complete
+          // the next `full` phase with no data
+          bar_wait(empty + s, ph ^ 1);
+          mbar_arrive(full + s);
+          break;
+        }
+        TC_TRACE(it, 0);
+        const int64_t tnext = p.sched ? (int64_t)atomicAdd(p.sched, 1ull) + gridDim.x : t + gridDim.x;
+#pragma unroll 1
+        for (int g = 0; g < kGroups; ++g) {
+          bar_wait(empty + s, ph ^ 1);
+          mbar_arrive_expect_tx(full + s, kSlot);
+          tma_load_3d(hi + (size_t)s * kSlot, &p.tm_b, 0, (int32_t)(t * NC), kGroup * g, full + s);
+          if (++s == SH) { s = 0; ph ^= 1; }
+        }
+        TC_TRACE(it, 1);
+        t = tnext;
+      }
+    }
+    __syncwarp();
+    __syncthreads();  // matches the final barrier of the other roles
+    return;
+  }
   const uint32_t tmem = *tslot;
   // TMEM columns: A_hi [0, 192), A_lo [192, 384), accumulators [512 - 2 NC, 512)
   const uint32_t a_hi = tmem, a_lo = tmem + (uint32_t)kTcK;
   const uint32_t d_col0 = tmem + 512u - (uint32_t)(ND * NC);
   static_assert(2 * kTcK + ND * NC <= 512, "TMEM budget");
 
-  const int64_t ntiles = p.ntiles;
+  auto ring_tile = [&](int it) -> int64_t { return *reinterpret_cast<volatile int64_t*>(tring + it % kTcTileRing); };
+  // epilogue side of the tile-id ring: read slot it % kTcTileRing after its
+  // tfull phase, then (lane 0) release it
+  auto next_tile = [&](int it) -> int64_t {
+    const int ts = it % kTcTileRing;
+    bar_wait(tfull + ts, (uint32_t)(it / kTcTileRing) & 1u);
+    const int64_t t = *reinterpret_cast<volatile int64_t*>(tring + ts);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(tempty + ts);
+    return t;
+  };
 
   if (warp >= kTcWarpEpi0 && warp < kTcWarpEpi0 + 4) {
     // Toeplitz rows of fh / fl into TMEM: lane r holds A[r][kk] = f[kk - r].
@@ -230,33 +337,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
         vl[j] = fsm[kFPad + t];
       }
       tmem_st32(a_hi + lanebits + (uint32_t)c, vh);
-      tmem_st32(a_lo + lanebits + (uint32_t)c, vl);
+      if constexpr (kMixed) {
+        // bf16 correction operand, K-step kb = (c + 8 j8) / 8: columns 0-3 hold fl(kk - r)
+        // for kk = 8 kb + 0..7 (pairs with bf16(xh)), columns 4-7 hold fh(kk - r) (pairs with
+        // bf16(xl)); column c holds K indices 2c (low half) and 2c + 1 (measured:
+        // tools/ubench/tc_bf16_tmem_probe.cu)
+        float vc[32];
+#pragma unroll
+        for (int j8 = 0; j8 < 4; ++j8)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            vc[8 * j8 + u] = __uint_as_float(pack_bf16(vl[8 * j8 + 2 * u], vl[8 * j8 + 2 * u + 1]));
+            vc[8 * j8 + 4 + u] = __uint_as_float(pack_bf16(vh[8 * j8 + 2 * u], vh[8 * j8 + 2 * u + 1]));
+          }
+        tmem_st32(a_lo + lanebits + (uint32_t)c, vc);
+      } else {
+        tmem_st32(a_lo + lanebits + (uint32_t)c, vl);
+      }
     }
     tmem_wait_st();
   }
   tc_fence_before();
-  __syncthreads();
+  asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads - 32) : "memory");
   tc_fence_after();
 
-  if (warp == kTcWarpProducer) {
-    if (lane == 0) {
-      int s = 0;
-      uint32_t ph = 0;
-      int it = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        TC_TRACE(it, 0);
-#pragma unroll 1
-        for (int g = 0; g < kGroups; ++g) {
-          bar_wait(empty + s, ph ^ 1);
-          mbar_arrive_expect_tx(full + s, kSlot);
-          tma_load_3d(hi + (size_t)s * kSlot, &p.tm_b, 0, (int32_t)(t * NC), kGroup * g, full + s);
-          if (++s == SH) { s = 0; ph ^= 1; }
-        }
-        TC_TRACE(it, 1);
-      }
-    }
-  } else if (warp == kTcWarpMma) {
+  if (warp == kTcWarpMma) {
     constexpr uint32_t idesc = idesc_tf32(128, NC);
+    constexpr uint32_t idesc_c = idesc_bf16(128, NC);
     // warp-uniform bases; descriptors advance by adding to the start-address field
     const uint64_t dhi0 = sw128_desc(__shfl_sync(0xffffffffu, smem_u32(hi), 0));
     const uint64_t dlo0 = sw128_desc(__shfl_sync(0xffffffffu, smem_u32(lo), 0));
@@ -265,15 +372,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
     int s = 0, l = 0, d = 0;
     uint32_t ph = 0, lph = 0, dph = 0;
     int it = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    for (;; ++it) {
+      // the split warps observed `full` (TMA data landed) before arriving on
+      // `lofull`, so one wait covers both operands and the tile id (acquire chain)
+      bar_wait(lofull + l, lph);
+      if (ring_tile(it) < 0) break;
       bar_wait(dempty + d, dph ^ 1);
       if (lane == 0) TC_TRACE(it, 2);
       const uint32_t dcol = dc0 + (uint32_t)(d * NC);
 #pragma unroll 1
       for (int g = 0; g < kGroups; ++g) {
-        // the split warps observed `full` (TMA data landed) before arriving on
-        // `lofull`, so one wait covers both operands (acquire chain)
-        bar_wait(lofull + l, lph);
+        if (g > 0) bar_wait(lofull + l, lph);
         if (lane == 0 && g == 0) TC_TRACE(it, 3);
         tc_fence_after();
         const uint64_t dh = dhi0 + (uint64_t)((s * kSlot) >> 4), dl = dlo0 + (uint64_t)((l * kSlot) >> 4);
@@ -284,8 +393,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
           const uint64_t off = (uint64_t)(((j >> 2) * kAtomBytes + 32u * (j & 3)) >> 4);
           const uint32_t kb = kb0 + (uint32_t)j;
           // small terms first: xh*fl and xl*fh, then xh*fh
-          mma_tf32_ts(dcol, alo + 8u * kb, dh + off, idesc, (g > 0 || j > 0) ? 1u : 0u);
-          mma_tf32_ts(dcol, ahi + 8u * kb, dl + off, idesc, 1u);
+          if constexpr (kMixed) {
+            // one bf16 MMA (K = 16: [bf16(xh) | bf16(xl)] . [fl | fh] over these 8 kk)
+            mma_bf16_ts(dcol, alo + 8u * kb, dl + off, idesc_c, (g > 0 || j > 0) ? 1u : 0u);
+          } else {
+            mma_tf32_ts(dcol, alo + 8u * kb, dh + off, idesc, (g > 0 || j > 0) ? 1u : 0u);
+            mma_tf32_ts(dcol, ahi + 8u * kb, dl + off, idesc, 1u);
+          }
           mma_tf32_ts(dcol, ahi + 8u * kb, dh + off, idesc, 1u);
         }
         mma_commit(empty + s);
@@ -305,18 +419,50 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
     int s = 0, l = 0;
     uint32_t ph = 0, lph = 0;
     int it = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    for (;; ++it) {
+      bar_wait(full + s, ph);
+      if (ring_tile(it) < 0) {  // end marker: pass it on to the MMA warp
+        bar_wait(loempty + l, lph ^ 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(lofull + l);
+        break;
+      }
 #pragma unroll 1
       for (int g = 0; g < kGroups; ++g) {
-        bar_wait(full + s, ph);
+        if (g > 0) bar_wait(full + s, ph);
         if (st == 0 && g == 0) TC_TRACE(it, 5);
         bar_wait(loempty + l, lph ^ 1);
         const uint32_t src = smem_u32(hi + (size_t)s * kSlot), dst = smem_u32(lo + (size_t)l * kSlot);
+        if constexpr (kMixed) {
+          // per 32-B block (one K-step of 8 kk in one 128-B row): logical halves
+          // [bf16(xh) x 8 | bf16(xl) x 8].  SWIZZLE_128B XORs the 16-B unit index
+          // with the row's low 3 bits, so the two units of a 32-B block stay
+          // together and swap order on odd rows: the unit that held x[kk0..kk0+3]
+          // receives the bf16(xh), the other the bf16(xl).
 #pragma unroll
-        for (int i = st; i < kN16; i += 32 * kTcSplitWarps) {
-          const float4 v = lds128(src + 16u * i);
-          sts128(dst + 16u * i, v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
-                 v.w - tf32_trunc(v.w));
+          for (int i = st; i < kN16 / 2; i += 32 * kTcSplitWarps) {
+            float4 a = lds128(src + 32u * i), b = lds128(src + 32u * i + 16u);
+            const bool odd = (i >> 2) & 1;  // row = i / 4 (4 blocks per 128-B row)
+            if (odd) { const float4 t = a; a = b; b = t; }
+            const float xv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float h0 = tf32_trunc(xv[2 * u]), h1 = tf32_trunc(xv[2 * u + 1]);
+              hw[u] = pack_bf16(h0, h1);
+              lw[u] = pack_bf16(xv[2 * u] - h0, xv[2 * u + 1] - h1);
+            }
+            const uint32_t dh_ = dst + 32u * i + (odd ? 16u : 0u), dl_ = dst + 32u * i + (odd ? 0u : 16u);
+            sts128(dh_, __uint_as_float(hw[0]), __uint_as_float(hw[1]), __uint_as_float(hw[2]), __uint_as_float(hw[3]));
+            sts128(dl_, __uint_as_float(lw[0]), __uint_as_float(lw[1]), __uint_as_float(lw[2]), __uint_as_float(lw[3]));
+          }
+        } else {
+#pragma unroll
+          for (int i = st; i < kN16; i += 32 * kTcSplitWarps) {
+            const float4 v = lds128(src + 16u * i);
+            sts128(dst + 16u * i, v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
+                   v.w - tf32_trunc(v.w));
+          }
         }
         fence_proxy_async_smem();  // generic-proxy writes -> tensor core reads
         __syncwarp();
@@ -337,7 +483,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
     int d = 0;
     uint32_t dph = 0;
     int it = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    for (;; ++it) {
+      const int64_t t = next_tile(it);
+      if (t < 0) break;
       bar_wait(dfull + d, dph);
       if (warp == kTcWarpEpi0 && lane == 0) TC_TRACE(it, 7);
       tc_fence_after();
@@ -376,32 +524,48 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
       }
       if (++d == ND) { d = 0; dph ^= 1; }
     }
-    // view positions beyond the tensor map (array tail): direct FMA windows
-    if (blockIdx.x == gridDim.x - 1 && h == 0) {
+    // view positions beyond the tensor map (array tail, < 320): direct FMA windows on all
+    // 256 epilogue threads, the window's loads issued together (a serial load->FMA chain
+    // here cost ~8 us at the end of the kernel)
+    if (blockIdx.x == gridDim.x - 1) {
       const float* __restrict__ xv = p.x_view;
-      for (int64_t pos = 128 * p.m_ext + r; pos < p.total_view; pos += 128) {
+      const int e = 32 * (warp - kTcWarpEpi0) + lane;
+      for (int64_t pos = 128 * p.m_ext + e; pos < p.total_view; pos += 32 * kTcEpiWarps) {
         const int64_t qq = pos - p.shift_x;
         if (qq < 0) continue;
         const int64_t b = qq / p.N, i = qq - b * p.N;
         if (b >= p.batch || i >= p.L_int) continue;
+        float xw[kConvTcMaxK];
+#pragma unroll
+        for (int j = 0; j < kConvTcMaxK; ++j) xw[j] = j < p.k ? __ldg(xv + pos + j) : 0.0f;
         float acc = 0.0f;
-        for (int j = 0; j < p.k; ++j) acc = __fmaf_rn(p.taps[j], __ldg(xv + pos + j), acc);
+#pragma unroll
+        for (int j = 0; j < kConvTcMaxK; ++j)
+          if (j < p.k) acc = __fmaf_rn(p.taps[j], xw[j], acc);
         p.y[b * p.y_pitch + p.y_off + i] = acc;
       }
     }
   }
   tc_fence_before();
   __syncthreads();
+  tc_trace_stamp(p.trace, 2);
+  if (p.sched && threadIdx.x == 32 * kTcWarpMma) {
+    // every producer of this CTA has stopped claiming; the last CTA out re-zeroes the slot
+    if (atomicAdd(p.sched + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
+      p.sched[0] = 0;
+      p.sched[1] = 0;
+    }
+  }
   if (warp == kTcWarpMma) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 size_t conv_tc_smem_bytes(int hi_slots, int lo_slots, int nc) {
   const int group = nc == 128 ? TcShape<128>::kGroup : TcShape<64>::kGroup;
-  return 1024 + (size_t)(hi_slots + lo_slots) * group * nc * 128 + 8 * (2 * hi_slots + 2 * lo_slots + 4) + 16 +
-         2 * sizeof(float) * (kConvTcMaxK + 256);
+  return 1024 + (size_t)(hi_slots + lo_slots) * group * nc * 128 + 8 * (2 * hi_slots + 2 * lo_slots + 4) +
+         24 * kTcTileRing + 16 + 2 * sizeof(float) * (kConvTcMaxK + 256);
 }
 
-template <int NC>
+template <int NC, bool kMixed>
 static cudaError_t launch_nc(ConvTCParams& p, cudaStream_t stream, int grid) {
   // lo ring: four group slots (the split runs ahead of the MMAs);
   // hi ring: every remaining slot (TMA prefetch depth)
@@ -410,8 +574,9 @@ static cudaError_t launch_nc(ConvTCParams& p, cudaStream_t stream, int grid) {
   while (SH > TcShape<NC>::kGroups && conv_tc_smem_bytes(SH, p.lo_bufs, NC) > (size_t)kSmemBudget) --SH;
   if (conv_tc_smem_bytes(SH, p.lo_bufs, NC) > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
   p.hi_stages = SH;
+  if (SH / TcShape<NC>::kGroups + TcShape<NC>::kDBufs + 2 > kTcTileRing) return cudaErrorInvalidConfiguration;
   p.ntiles = (p.m_ext + NC - 1) / NC;
-  auto kfn = conv_tc_kernel<NC>;
+  auto kfn = conv_tc_kernel<NC, kMixed>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
   if (e != cudaSuccess) return e;
   int64_t g = p.ntiles < grid ? p.ntiles : grid;
@@ -422,9 +587,10 @@ static cudaError_t launch_nc(ConvTCParams& p, cudaStream_t stream, int grid) {
 }
 
 cudaError_t launch_conv_tc(ConvTCParams& p, int nc, cudaStream_t stream, int grid) {
+  const bool mixed = p.mixed != 0;
   switch (nc) {
-    case 64: return launch_nc<64>(p, stream, grid);
-    case 128: return launch_nc<128>(p, stream, grid);
+    case 64: return mixed ? launch_nc<64, true>(p, stream, grid) : launch_nc<64, false>(p, stream, grid);
+    case 128: return mixed ? launch_nc<128, true>(p, stream, grid) : launch_nc<128, false>(p, stream, grid);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -11,6 +11,10 @@ constexpr int kOpSum = 0;
 constexpr int kOpMax = 1;
 constexpr int kOpConv = 2;
 constexpr int kSmemBudget = 227 * 1024;  // max dynamic smem per CTA on sm_100a
+// Dynamic tile scheduling of the persistent kernels: slot = {next, done}; tile
+// n >= gridDim.x of a launch is claimed with atomicAdd(next) + gridDim.x (the
+// first tile of CTA b is b), and the last CTA to finish zeroes the slot.
+constexpr int kSchedSlots = 4096;
 constexpr int kConvTmaMaxK = 64;          // largest k served by the TMA conv kernel
 constexpr int kPoolTmaMaxW = 1024;        // largest w served by the TMA pool kernel
 constexpr int kSlideWarps = 15;           // consumer warps of the 1-D tile kernel
@@ -113,6 +117,8 @@ struct alignas(64) ConvTCParams {
   int64_t ntiles;          // set by launch_conv_tc
   int k, K, atoms;         // filter length, MMA K (192), K-atoms (6)
   int hi_stages, lo_bufs;  // group slots (3 K-atoms) of the hi / lo rings (set by launch_conv_tc)
+  int mixed;               // 1: TF32 xh*fh + one bf16 correction MMA; 0: 3xTF32
+  unsigned long long* sched;  // dynamic tile counter slot {next, done} (null: static round robin)
   unsigned long long* trace;  // debug: per-tile role timestamps of CTA 0 (null = off)
   float taps[kConvTcMaxK];
 };

@@ -79,7 +79,7 @@ def trace():
     synth.fill_device(x, "normal", 3)
     f = synth.normal(4, k, sigma=synth.cfg_sigma_filter(k))
     y = torch.empty(B, N - k + 1, device="cuda")
-    for _ in range(3):
+    for _ in range(int(os.environ.get("REPS", "3"))):
         ss.conv1d(x, f, out=y)
     torch.cuda.synchronize()
     buf = (ctypes.c_ulonglong * 1024)()
@@ -90,10 +90,36 @@ def trace():
     t0 = t[0, 0]
     names = ["P.start", "P.issued", "M.dempty", "M.data", "M.issued", "S.full0", "S.done", "E.dfull"]
     print("tile " + " ".join(f"{n:>9s}" for n in names))
-    for i in range(min(40, t.shape[0])):
+    n = 0
+    for i in range(t.shape[0]):
         if t[i, 0] == 0:
             break
-        print(f"{i:4d} " + " ".join(f"{v - t0:9d}" for v in t[i]))
+        n = i + 1
+        if i < 6 or i >= int(os.environ.get("TAIL", "50")):
+            print(f"{i:4d} " + " ".join(f"{v - t0:9d}" for v in t[i]))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    ss.conv1d(x, f, out=y)
+    b.record()
+    torch.cuda.synchronize()
+    g = allv[63 * 8: 63 * 8 + 6]
+    if g[0]:
+        print(f"CTA 0 globaltimer: setup {(g[2] - g[0]) / 1e3:.1f} us, setup->exit {(g[4] - g[2]) / 1e3:.1f} us; "
+              f"clock {(g[5] - g[1]) / ((g[4] - g[0]) / 1e3):.0f} MHz; first tile start at +{(t0 - g[1])} clk")
+    ce = allv[512:].reshape(256, 2)
+    ce = ce[ce[:, 0] > 0]
+    if len(ce):
+        g0 = ce[:, 0].min()
+        print(f"{len(ce)} CTAs: entry spread {(ce[:, 0].max() - g0) / 1e3:.1f} us, exit min / median / max "
+              f"{(ce[:, 1].min() - g0) / 1e3:.1f} / {(np.median(ce[:, 1]) - g0) / 1e3:.1f} / "
+              f"{(ce[:, 1].max() - g0) / 1e3:.1f} us after the first entry")
+        allce = allv[512:].reshape(256, 2)
+        order = np.argsort(allce[:, 1])[::-1]
+        print("slowest CTAs (index: exit us):",
+              ", ".join(f"{i}: {(allce[i, 1] - g0) / 1e3:.1f}" for i in order[:8] if allce[i, 1] > 0))
+    span = t[n - 1, 7] - t0
+    print(f"CTA 0: {n} tiles, span {span} clk; event time of one call {a.elapsed_time(b) * 1e3:.1f} us "
+          f"-> {span / (a.elapsed_time(b) * 1e3):.0f} MHz if the span were the whole kernel")
     d = np.diff(t[5:40, 4])
     print("MMA issue-done period (clk): median", np.median(d))
 
