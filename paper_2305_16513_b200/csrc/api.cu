@@ -379,6 +379,7 @@ static ss_status_t window_impl(int op, const void* x, void* y, int64_t N, int64_
       char* y_int = static_cast<char*>(y) + 4 * pl;
       if (make_slide_params(p, x, y_int, N, batch, L_int, L, 0)) {
         p.w = w;
+        p.sched = sched_slot(s);
         cudaError_t e;
         if (op == kOpConv) {
           for (int j = 0; j < KT; ++j) p.taps[j] = j < w ? taps[j] : 0.0f;

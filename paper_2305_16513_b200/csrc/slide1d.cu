@@ -501,42 +501,59 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
   if (warp == kWarps) {
     // ---------------- producer: one lane walks the tiles, publishes headers, issues TMA
     if (lane == 0) {
+      // CTA b starts with tile b, then claims tiles from the launch's counter slot
+      // (dynamic: SMs that stream faster take more tiles) or strides by gridDim.x
       const int64_t tpr = p.tiles_per_row;
       int it = 0;
       TileCursor tc;
       tc.init(blockIdx.x, tpr);
-      for (int64_t tau = blockIdx.x; tau < p.ntiles; tau += gridDim.x, tc.advance(gridDim.x, tpr)) {
+      for (int64_t tau = blockIdx.x; tau < p.ntiles;) {
         const TileGeom g = tile_geom<kTileRows>(p, tc);
-        if (g.empty) continue;
-        const int s = it % S;
-        mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
-        TileHdr& h = hdr[s];
-        h.yrow0 = g.yrow0;
-        h.y_lo = g.e_y;
-        h.y_hi = g.e_y + p.L;
-        h.dxy = p.shift_x + tc.b * p.N - g.e_y;
-        h.m = g.m;
-        h.flags = g.slow ? 1 : 0;
-        uint8_t* dst = smem + (size_t)s * stage_bytes;
-        if (g.slow) {  // consumers read global memory directly for this tile
-          mbar_arrive(&full[s]);
-        } else {
-          const uint32_t bytes = (uint32_t)(kTileRows + kHaloBoxRows * g.halo_boxes) * 128u;
-          mbar_arrive_expect_tx(&full[s], bytes);
+        const int64_t b_cur = tc.b;
+        // claim the next tile now: the atomic's round trip overlaps the slot wait and the TMA issue
+        const int64_t tau_next = p.sched ? (int64_t)atomicAdd(p.sched, 1ull) + gridDim.x : tau + gridDim.x;
+        if (!g.empty) {
+          const int s = it % S;
+          mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
+          TileHdr& h = hdr[s];
+          h.yrow0 = g.yrow0;
+          h.y_lo = g.e_y;
+          h.y_hi = g.e_y + p.L;
+          h.dxy = p.shift_x + b_cur * p.N - g.e_y;
+          h.m = g.m;
+          h.flags = g.slow ? 1 : 0;
+          uint8_t* dst = smem + (size_t)s * stage_bytes;
+          if (g.slow) {  // consumers read global memory directly for this tile
+            mbar_arrive(&full[s]);
+          } else {
+            const uint32_t bytes = (uint32_t)(kTileRows + kHaloBoxRows * g.halo_boxes) * 128u;
+            mbar_arrive_expect_tx(&full[s], bytes);
 #pragma unroll
-          for (int mb = 0; mb < kTileRows / kMainBoxRows; ++mb)
-            tma_load_2d(dst + (size_t)mb * kMainBoxRows * 128, &p.tm_x_main, 0,
-                        (int32_t)(g.xrow0 + mb * kMainBoxRows), &full[s]);
-          for (int h2 = 0; h2 < g.halo_boxes; ++h2)
-            tma_load_2d(dst + (size_t)(kTileRows + kHaloBoxRows * h2) * 128, &p.tm_x_halo, 0,
-                        (int32_t)(g.xrow0 + kTileRows + kHaloBoxRows * h2), &full[s]);
+            for (int mb = 0; mb < kTileRows / kMainBoxRows; ++mb)
+              tma_load_2d(dst + (size_t)mb * kMainBoxRows * 128, &p.tm_x_main, 0,
+                          (int32_t)(g.xrow0 + mb * kMainBoxRows), &full[s]);
+            for (int h2 = 0; h2 < g.halo_boxes; ++h2)
+              tma_load_2d(dst + (size_t)(kTileRows + kHaloBoxRows * h2) * 128, &p.tm_x_halo, 0,
+                          (int32_t)(g.xrow0 + kTileRows + kHaloBoxRows * h2), &full[s]);
+          }
+          ++it;
         }
-        ++it;
+        if (p.sched) {
+          tc.init(tau_next, tpr);
+        } else {
+          tc.advance(gridDim.x, tpr);
+        }
+        tau = tau_next;
       }
       const int s = it % S;  // end marker
       mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
       hdr[s].flags = 2;
       mbar_arrive(&full[s]);
+      // this CTA has stopped claiming; the last one to stop re-zeroes the slot
+      if (p.sched && atomicAdd(p.sched + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
+        p.sched[0] = 0;
+        p.sched[1] = 0;
+      }
     }
     return;
   }

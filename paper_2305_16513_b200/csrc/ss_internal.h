@@ -43,6 +43,7 @@ struct alignas(64) Slide1DParams {
   int stages;
   int span;
   int has_y_map;
+  unsigned long long* sched;  // dynamic tile counter slot {next, done} (null: static round robin)
   float taps[kConvTmaMaxK];  // conv taps, zero-padded to the kernel's KT
 };
 
