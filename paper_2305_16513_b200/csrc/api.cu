@@ -628,6 +628,7 @@ ss_status_t ss_conv2d(const void* x, void* y, int64_t planes, int64_t H, int64_t
   p.OH = (H - kh) / sh + 1; p.OW = (W - kw) / sw + 1;
   if (overlaps(x, planes * H * W * 4, y, planes * p.OH * p.OW * 4)) return fail(SS_ERR_OVERLAP, "x and y overlap");
   for (int64_t t = 0; t < kh * kw; ++t) p.taps[t] = filter_host[t];
+  p.sched = sched_slot(static_cast<cudaStream_t>(stream));
   cudaError_t e = launch_conv2d(p, static_cast<cudaStream_t>(stream), current_sms());
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv2d launch");
 }
@@ -698,6 +699,7 @@ ss_status_t ss_pool2d(const void* x, void* y, int64_t planes, int64_t H, int64_t
   p.inv_area = (float)(1.0 / (double)(kh * kw));
   p.bulk = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (W % 4 == 0);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  p.sched = sched_slot(s);
   cudaError_t e = launch_pool2d(p, s, current_sms());
   if (e == cudaErrorInvalidConfiguration) e = launch_pool2d_direct(p, s, current_sms() * 8);
   if (e == cudaSuccess) return SS_OK;

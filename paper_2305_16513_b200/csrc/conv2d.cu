@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(kC2Threads, 1) conv2d_vec_kernel(const __grid_
   const int S = p.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
   uint64_t* empty = full + S;
+  int64_t* pid = reinterpret_cast<int64_t*>(empty + S);  // plane of each stage (-1: no more)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -58,15 +59,10 @@ __global__ void __launch_bounds__(kC2Threads, 1) conv2d_vec_kernel(const __grid_
   const int64_t plane_elems = p.H * p.W;
   const uint32_t plane_bytes = (uint32_t)(plane_elems * 4);
   if (warp == kC2Warps) {  // producer
-    if (lane == 0) {
-      int it = 0;
-      for (int64_t pl = blockIdx.x; pl < p.planes; pl += gridDim.x, ++it) {
-        const int s = it % S;
-        mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
-        mbar_arrive_expect_tx(&full[s], plane_bytes);
-        bulk_load_1d(smem + (size_t)s * p.stage_bytes, p.x + pl * plane_elems, plane_bytes, &full[s]);
-      }
-    }
+    if (lane == 0) plane_producer(p.planes, p.sched, S, full, empty, pid, [&](int64_t pl, int s) {
+      mbar_arrive_expect_tx(&full[s], plane_bytes);
+      bulk_load_1d(smem + (size_t)s * p.stage_bytes, p.x + pl * plane_elems, plane_bytes, &full[s]);
+    });
     return;
   }
   const int OH = (int)p.OH, OW = (int)p.OW;
@@ -74,10 +70,11 @@ __global__ void __launch_bounds__(kC2Threads, 1) conv2d_vec_kernel(const __grid_
   const int ra = warp * rows_per, rb = min(ra + rows_per, OH);
   const uint32_t W4 = (uint32_t)p.W * 4u;
   const uint32_t smem_s = smem_u32(smem);
-  int it = 0;
-  for (int64_t pl = blockIdx.x; pl < p.planes; pl += gridDim.x, ++it) {
+  for (int it = 0;; ++it) {
     const int s = it % S;
     mbar_wait(&full[s], (uint32_t)(it / S) & 1u);
+    const int64_t pl = *reinterpret_cast<volatile int64_t*>(pid + s);
+    if (pl < 0) break;
     const uint32_t xs = smem_s + (uint32_t)s * p.stage_bytes;
     float* yp = p.y + pl * (int64_t)OH * OW;
     for (int c0 = VO * lane; c0 < OW; c0 += 32 * VO) {

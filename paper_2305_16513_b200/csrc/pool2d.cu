@@ -172,6 +172,7 @@ pool2d_vec_kernel(const __grid_constant__ Pool2DParams p) {
   const int S = p.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
   uint64_t* empty = full + S;
+  int64_t* pid = reinterpret_cast<int64_t*>(empty + S);  // plane of each stage (-1: no more)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -185,15 +186,10 @@ pool2d_vec_kernel(const __grid_constant__ Pool2DParams p) {
   const uint32_t plane_bytes = (uint32_t)(plane_elems * 4);
 
   if (warp == kP2VWarps) {  // producer
-    if (lane == 0) {
-      int it = 0;
-      for (int64_t pl = blockIdx.x; pl < p.planes; pl += gridDim.x, ++it) {
-        const int s = it % S;
-        mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
-        mbar_arrive_expect_tx(&full[s], plane_bytes);
-        bulk_load_1d(smem + (size_t)s * p.stage_bytes, p.x + pl * plane_elems, plane_bytes, &full[s]);
-      }
-    }
+    if (lane == 0) plane_producer(p.planes, p.sched, S, full, empty, pid, [&](int64_t pl, int s) {
+      mbar_arrive_expect_tx(&full[s], plane_bytes);
+      bulk_load_1d(smem + (size_t)s * p.stage_bytes, p.x + pl * plane_elems, plane_bytes, &full[s]);
+    });
     return;
   }
 
@@ -202,10 +198,11 @@ pool2d_vec_kernel(const __grid_constant__ Pool2DParams p) {
   const int64_t ra = warp * rows_per;
   const int64_t rb = ra + rows_per < OH ? ra + rows_per : OH;
   const uint32_t smem_s = smem_u32(smem);
-  int it = 0;
-  for (int64_t pl = blockIdx.x; pl < p.planes; pl += gridDim.x, ++it) {
+  for (int it = 0;; ++it) {
     const int s = it % S;
     mbar_wait(&full[s], (uint32_t)(it / S) & 1u);
+    const int64_t pl = *reinterpret_cast<volatile int64_t*>(pid + s);
+    if (pl < 0) break;
     const uint32_t xs = smem_s + (uint32_t)s * p.stage_bytes;
     float* yp = p.y + pl * OH * OW;
     const uint32_t W4 = (uint32_t)W * 4u;  // smem row pitch (plane <= 100 KB: 32-bit offsets)

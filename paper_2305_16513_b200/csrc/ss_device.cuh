@@ -178,4 +178,34 @@ __device__ __forceinline__ To bitcast(From v) {
   return r;
 }
 
+
+// Producer side of a plane (or tile) ring with dynamic claims: CTA b starts with
+// unit b, then claims units from the launch's counter slot sched = {next, done}
+// (null: strides by gridDim.x).  For each unit it waits for the stage, publishes
+// the unit id in pid[stage] and calls load(unit, stage), which must arm full[stage]
+// (release: consumers read pid after their full wait); the end marker is
+// pid = -1 with a plain arrive.  The last CTA to stop claiming re-zeroes the slot.
+template <class Load>
+__device__ __forceinline__ void plane_producer(int64_t units, unsigned long long* sched, int S, uint64_t* full,
+                                               uint64_t* empty, int64_t* pid, Load load) {
+  int64_t u = blockIdx.x;
+  for (int it = 0;; ++it) {
+    const int s = it % S;
+    mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
+    if (u >= units) {
+      pid[s] = -1;
+      mbar_arrive(&full[s]);
+      break;
+    }
+    const int64_t next = sched ? (int64_t)atomicAdd(sched, 1ull) + gridDim.x : u + gridDim.x;
+    pid[s] = u;
+    load(u, s);
+    u = next;
+  }
+  if (sched && atomicAdd(sched + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
+    sched[0] = 0;
+    sched[1] = 0;
+  }
+}
+
 }  // namespace ss

@@ -69,6 +69,7 @@ struct Pool2DParams {
   int bulk;             // 1: rows are 16-B aligned -> cp.async.bulk staging
   int mode;             // 0 max, 1 avg
   float inv_area;       // 1 / (kh * kw) for avg
+  unsigned long long* sched;  // dynamic plane counter slot (vector kernel; null: static round robin)
 };
 
 void note_launch();
@@ -169,6 +170,7 @@ struct Conv2DParams {
   int64_t planes, H, W, OH, OW, kh, kw, sh, sw;
   uint32_t stage_bytes;  // set by launch_conv2d
   int stages;
+  unsigned long long* sched;  // dynamic plane counter slot (vector kernel; null: static round robin)
   float taps[1024];      // row-major [kh][kw], kh * kw <= SS_K_MAX
 };
 cudaError_t launch_conv2d(Conv2DParams& p, cudaStream_t stream, int grid);
