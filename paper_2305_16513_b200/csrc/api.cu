@@ -136,16 +136,16 @@ bool encode_rows_map(CUtensorMap* m, const void* base, int64_t rows, int box_row
   return make_map(m, base, rows, box_rows);
 }
 
-// Overlapping-chunk view for the tensor-core conv (conv_tc.cu): element
-// (e, m, a) = base[128 m + 32 a + e], i.e. chunk m's K-atom a is the 128-B row
-// 4m + a; box {32, nc, 3} at {0, m0, a0} lands in smem as three nc x 128-B
-// K-major SWIZZLE_128B operands, K-atoms a0 .. a0 + 2.
+// Chunk view for the tensor-core conv (conv_tc.cu): element (e, m, a) =
+// base[128 m + 32 a + e], i.e. chunk m's K-atom a is the 128-B row 4m + a;
+// box {32, nc + 8, 4} at {0, m0, 0} lands in smem as four (nc + 8) x 128-B
+// K-major SWIZZLE_128B blocks, K-atoms 0..3 (atoms 4, 5 = blocks 0, 1 one row down).
 bool encode_chunk_map(CUtensorMap* m, const void* base, int64_t m_ext, int atoms, int nc) {
   auto enc = encode_fn();
   if (!enc || m_ext < 1 || m_ext > (int64_t(1) << 31) - 1024) return false;
   cuuint64_t dims[3] = {32, (cuuint64_t)m_ext, (cuuint64_t)atoms};
   cuuint64_t strides[2] = {512, 128};
-  cuuint32_t box[3] = {32, (cuuint32_t)nc, (cuuint32_t)(nc == 128 ? 2 : 3)};  // one group of K-atoms per load
+  cuuint32_t box[3] = {32, (cuuint32_t)(nc + 8), (cuuint32_t)atoms};  // one tile: nc + 8 chunks x 4 K-atoms
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -220,11 +220,14 @@ static bool try_conv_tc(const void* x, float* y_int, int64_t N, int64_t batch, i
   p.total_view = p.shift_x + batch * N;
   p.k = (int)k;
   p.K = 192;  // conv_tc.cu: fixed MMA depth, Toeplitz zero beyond k (k <= 65)
-  p.atoms = 6;
-  if (p.total_view < 32 * p.atoms + 128 * 4) return false;
-  p.m_ext = (p.total_view - 32 * p.atoms) / 128 + 1;
+  p.atoms = 4;  // staged K-atoms per chunk; atoms 4, 5 are the next chunk's 0, 1
+  if (p.total_view < 128 * 8) return false;
+  // chunk m's 4 staged atoms are view rows 4m..4m+3: the map holds m_map chunks; chunk m's
+  // outputs need chunk m + 1's atoms 0 and 1, so chunks [0, m_map - 1) run on the tensor cores
+  const int64_t m_map = (p.total_view - 128) / 128 + 1;
+  p.m_ext = m_map - 1;
   const int nc = tc_nc();
-  if (!encode_chunk_map(&p.tm_b, p.x_view, p.m_ext, p.atoms, nc)) return false;
+  if (!encode_chunk_map(&p.tm_b, p.x_view, m_map, p.atoms, nc)) return false;
   for (int j = 0; j < (int)k; ++j) p.taps[j] = taps[j];
   p.trace = tc_trace_buf();
   static int lo_slots = env_int("SS_CONV_TC_LO", 0);

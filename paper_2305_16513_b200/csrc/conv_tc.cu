@@ -196,31 +196,33 @@ __device__ __forceinline__ void tc_trace_stamp(unsigned long long* tr, int slot)
 }
 
 // Fixed MMA depth: K = 192 (6 K-atoms of 32, 24 K-steps of 8) serves every
-// k <= 65 (the Toeplitz is zero beyond k); the pipelines move groups of
-// kGroup K-atoms (one TMA box, one split pass, 12 kGroup MMAs per sync).
+// k <= 65 (the Toeplitz is zero beyond k); the pipelines move whole tiles (one
+// TMA box of 4 K-atom blocks, one split pass, 24 K-steps of MMAs per sync).
 constexpr int kTcK = 192;
 constexpr int kTcAtoms = kTcK / 32;
-// group size and accumulator buffers per chunk count: NC = 64 keeps two TMEM
+// accumulator buffers per chunk count: NC = 64 keeps two TMEM
 // accumulators (epilogue of tile i overlaps the MMAs of tile i+1); NC = 128
 // (N = 128 MMAs: half the issue count) has room for one, drained by the
 // epilogue into registers before the next tile's first MMA.
 template <int NC> struct TcShape {
-  static constexpr int kGroup = NC == 128 ? 2 : 3;
-  static constexpr int kGroups = kTcAtoms / kGroup;
+  static constexpr int kBlockRows = NC + 8;  // chunks per staged K-atom block (one extra, 1024-B aligned)
   static constexpr int kDBufs = NC == 128 ? 1 : 2;
 };
 
 template <int NC, bool kMixed>
 __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_constant__ ConvTCParams p) {
   static_assert(NC % 32 == 0 && NC <= 128, "NC/2 columns per epilogue warp, loaded 16 at a time");
-  constexpr int kGroup = TcShape<NC>::kGroup, kGroups = TcShape<NC>::kGroups, ND = TcShape<NC>::kDBufs;
+  constexpr int kBlockRows = TcShape<NC>::kBlockRows, ND = TcShape<NC>::kDBufs;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // Rings of group slots (kGroup K-atoms of all NC chunks, each atom NC x 128 B).
+  // Rings of tile stages: 4 K-atom blocks of kBlockRows chunks x 128 B.  K-atoms 4 and 5 of
+  // chunk m are atoms 0 and 1 of chunk m + 1, i.e. blocks 0 and 1 read one row further down
+  // (a whole-row shift of the operand start stays a canonical SWIZZLE_128B operand).
   const int SH = p.hi_stages, SL = p.lo_bufs;
-  constexpr uint32_t kAtomBytes = NC * 128u;
-  constexpr uint32_t kSlot = kGroup * kAtomBytes;
+  constexpr uint32_t kAtomBytes = kBlockRows * 128u;
+  constexpr uint32_t kSlot = 4 * kAtomBytes;
+  static_assert(kAtomBytes % 1024 == 0, "blocks stay 1024-B aligned");
   uint8_t* hi = smem;
   uint8_t* lo = smem + (size_t)SH * kSlot;
   uint64_t* bars = reinterpret_cast<uint64_t*>(lo + (size_t)SL * kSlot);
@@ -287,16 +289,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
           mbar_arrive(full + s);
           break;
         }
-        TC_TRACE(it, 0);
         const int64_t tnext = p.sched ? (int64_t)atomicAdd(p.sched, 1ull) + gridDim.x : t + gridDim.x;
-#pragma unroll 1
-        for (int g = 0; g < kGroups; ++g) {
-          bar_wait(empty + s, ph ^ 1);
-          mbar_arrive_expect_tx(full + s, kSlot);
-          tma_load_3d(hi + (size_t)s * kSlot, &p.tm_b, 0, (int32_t)(t * NC), kGroup * g, full + s);
-          if (++s == SH) { s = 0; ph ^= 1; }
-        }
-        TC_TRACE(it, 1);
+        bar_wait(empty + s, ph ^ 1);
+        mbar_arrive_expect_tx(full + s, kSlot);
+        tma_load_3d(hi + (size_t)s * kSlot, &p.tm_b, 0, (int32_t)(t * NC), 0, full + s);
+        if (++s == SH) { s = 0; ph ^= 1; }
+        TC_TRACE(it, 0);
         t = tnext;
       }
     }
@@ -378,99 +376,92 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
       bar_wait(lofull + l, lph);
       if (ring_tile(it) < 0) break;
       bar_wait(dempty + d, dph ^ 1);
-      if (lane == 0) TC_TRACE(it, 2);
       const uint32_t dcol = dc0 + (uint32_t)(d * NC);
-#pragma unroll 1
-      for (int g = 0; g < kGroups; ++g) {
-        if (g > 0) bar_wait(lofull + l, lph);
-        if (lane == 0 && g == 0) TC_TRACE(it, 3);
-        tc_fence_after();
-        const uint64_t dh = dhi0 + (uint64_t)((s * kSlot) >> 4), dl = dlo0 + (uint64_t)((l * kSlot) >> 4);
-        const uint32_t kb0 = (uint32_t)(g * kGroup * 4);
+      if (lane == 0) TC_TRACE(it, 3);
+      tc_fence_after();
+      const uint64_t dh = dhi0 + (uint64_t)((s * kSlot) >> 4), dl = dlo0 + (uint64_t)((l * kSlot) >> 4);
 #pragma unroll
-        for (int j = 0; j < kGroup * 4; ++j) {
-          // K-step kb = kb0 + j: atom j/4 of the group, 32-B column block j%4
-          const uint64_t off = (uint64_t)(((j >> 2) * kAtomBytes + 32u * (j & 3)) >> 4);
-          const uint32_t kb = kb0 + (uint32_t)j;
-          // small terms first: xh*fl and xl*fh, then xh*fh
-          if constexpr (kMixed) {
-            // one bf16 MMA (K = 16: [bf16(xh) | bf16(xl)] . [fl | fh] over these 8 kk)
-            mma_bf16_ts(dcol, alo + 8u * kb, dl + off, idesc_c, (g > 0 || j > 0) ? 1u : 0u);
-          } else {
-            mma_tf32_ts(dcol, alo + 8u * kb, dh + off, idesc, (g > 0 || j > 0) ? 1u : 0u);
-            mma_tf32_ts(dcol, ahi + 8u * kb, dl + off, idesc, 1u);
-          }
-          mma_tf32_ts(dcol, ahi + 8u * kb, dh + off, idesc, 1u);
+      for (int kb = 0; kb < 4 * kTcAtoms; ++kb) {
+        // K-step kb: K-atom a = kb / 4 -> block a (a < 4) or block a - 4 one row down; 32-B column block kb % 4
+        const int a = kb >> 2;
+        const uint64_t off = (uint64_t)(((uint32_t)(a & 3) * kAtomBytes + (a >= 4 ? 128u : 0u) + 32u * (kb & 3)) >> 4);
+        // small terms first: xh*fl and xl*fh, then xh*fh
+        if constexpr (kMixed) {
+          // one bf16 MMA (K = 16: [bf16(xh) | bf16(xl)] . [fl | fh] over these 8 kk)
+          mma_bf16_ts(dcol, alo + 8u * (uint32_t)kb, dl + off, idesc_c, kb > 0 ? 1u : 0u);
+        } else {
+          mma_tf32_ts(dcol, alo + 8u * (uint32_t)kb, dh + off, idesc, kb > 0 ? 1u : 0u);
+          mma_tf32_ts(dcol, ahi + 8u * (uint32_t)kb, dl + off, idesc, 1u);
         }
-        mma_commit(empty + s);
-        mma_commit(loempty + l);
-        if (++s == SH) { s = 0; ph ^= 1; }
-        if (++l == SL) { l = 0; lph ^= 1; }
+        mma_tf32_ts(dcol, ahi + 8u * (uint32_t)kb, dh + off, idesc, 1u);
       }
+      mma_commit(empty + s);
+      mma_commit(loempty + l);
+      if (++s == SH) { s = 0; ph ^= 1; }
+      if (++l == SL) { l = 0; lph ^= 1; }
       mma_commit(dfull + d);
       if (lane == 0) TC_TRACE(it, 4);
       if (++d == ND) { d = 0; dph ^= 1; }
     }
   } else if (warp < kTcWarpEpi0) {
-    // split warps: Blo = x - trunc(x), elementwise (swizzle-agnostic), one group slot at a time
+    // split warps: the correction operand of a staged tile (rows 0..NC of each of the 4 blocks;
+    // the rows past NC are never read), position by position
     const int st = threadIdx.x - 32 * kTcWarpSplit0;  // 0 .. 32 kTcSplitWarps - 1
-    constexpr int kN16 = (int)(kSlot >> 4);
-    static_assert(kN16 % (32 * kTcSplitWarps) == 0, "whole float4s per split thread");
+    constexpr int kRowsUsed = NC + 1;
     int s = 0, l = 0;
     uint32_t ph = 0, lph = 0;
-    int it = 0;
-    for (;; ++it) {
+    for (int it = 0;; ++it) {
       bar_wait(full + s, ph);
+      bar_wait(loempty + l, lph ^ 1);
       if (ring_tile(it) < 0) {  // end marker: pass it on to the MMA warp
-        bar_wait(loempty + l, lph ^ 1);
         __syncwarp();
         if (lane == 0) mbar_arrive(lofull + l);
         break;
       }
-#pragma unroll 1
-      for (int g = 0; g < kGroups; ++g) {
-        if (g > 0) bar_wait(full + s, ph);
-        if (st == 0 && g == 0) TC_TRACE(it, 5);
-        bar_wait(loempty + l, lph ^ 1);
-        const uint32_t src = smem_u32(hi + (size_t)s * kSlot), dst = smem_u32(lo + (size_t)l * kSlot);
-        if constexpr (kMixed) {
-          // per 32-B block (one K-step of 8 kk in one 128-B row): logical halves
-          // [bf16(xh) x 8 | bf16(xl) x 8].  SWIZZLE_128B XORs the 16-B unit index
-          // with the row's low 3 bits, so the two units of a 32-B block stay
-          // together and swap order on odd rows: the unit that held x[kk0..kk0+3]
-          // receives the bf16(xh), the other the bf16(xl).
+      if (st == 0) TC_TRACE(it, 2);
+      const uint32_t src = smem_u32(hi + (size_t)s * kSlot), dst = smem_u32(lo + (size_t)l * kSlot);
+      if constexpr (kMixed) {
+        // per 32-B block (one K-step of 8 kk in one 128-B row): logical halves
+        // [bf16(xh) x 8 | bf16(xl) x 8].  SWIZZLE_128B XORs the 16-B unit index
+        // with the row's low 3 bits, so the two units of a 32-B block stay
+        // together and swap order on odd rows: the unit that held x[kk0..kk0+3]
+        // receives the bf16(xh), the other the bf16(xl).  (Block bases are
+        // multiples of 1024 B, so the row parity is the in-block row's.)
+        constexpr int kItems = 4 * kRowsUsed * 4;
+        for (int i = st; i < kItems; i += 32 * kTcSplitWarps) {
+          const int blk = i / (kRowsUsed * 4), rem = i - blk * (kRowsUsed * 4);
+          const uint32_t o = (uint32_t)blk * kAtomBytes + 32u * (uint32_t)rem;  // rem = row * 4 + unit pair
+          float4 a = lds128(src + o), b = lds128(src + o + 16u);
+          const bool odd = (rem >> 2) & 1;
+          if (odd) { const float4 t = a; a = b; b = t; }
+          const float xv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+          uint32_t hw[4], lw[4];
 #pragma unroll
-          for (int i = st; i < kN16 / 2; i += 32 * kTcSplitWarps) {
-            float4 a = lds128(src + 32u * i), b = lds128(src + 32u * i + 16u);
-            const bool odd = (i >> 2) & 1;  // row = i / 4 (4 blocks per 128-B row)
-            if (odd) { const float4 t = a; a = b; b = t; }
-            const float xv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-            uint32_t hw[4], lw[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float h0 = tf32_trunc(xv[2 * u]), h1 = tf32_trunc(xv[2 * u + 1]);
-              hw[u] = pack_bf16(h0, h1);
-              lw[u] = pack_bf16(xv[2 * u] - h0, xv[2 * u + 1] - h1);
-            }
-            const uint32_t dh_ = dst + 32u * i + (odd ? 16u : 0u), dl_ = dst + 32u * i + (odd ? 0u : 16u);
-            sts128(dh_, __uint_as_float(hw[0]), __uint_as_float(hw[1]), __uint_as_float(hw[2]), __uint_as_float(hw[3]));
-            sts128(dl_, __uint_as_float(lw[0]), __uint_as_float(lw[1]), __uint_as_float(lw[2]), __uint_as_float(lw[3]));
+          for (int u = 0; u < 4; ++u) {
+            const float h0 = tf32_trunc(xv[2 * u]), h1 = tf32_trunc(xv[2 * u + 1]);
+            hw[u] = pack_bf16(h0, h1);
+            lw[u] = pack_bf16(xv[2 * u] - h0, xv[2 * u + 1] - h1);
           }
-        } else {
-#pragma unroll
-          for (int i = st; i < kN16; i += 32 * kTcSplitWarps) {
-            const float4 v = lds128(src + 16u * i);
-            sts128(dst + 16u * i, v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
-                   v.w - tf32_trunc(v.w));
-          }
+          const uint32_t dh_ = dst + o + (odd ? 16u : 0u), dl_ = dst + o + (odd ? 0u : 16u);
+          sts128(dh_, __uint_as_float(hw[0]), __uint_as_float(hw[1]), __uint_as_float(hw[2]), __uint_as_float(hw[3]));
+          sts128(dl_, __uint_as_float(lw[0]), __uint_as_float(lw[1]), __uint_as_float(lw[2]), __uint_as_float(lw[3]));
         }
-        fence_proxy_async_smem();  // generic-proxy writes -> tensor core reads
-        __syncwarp();
-        if (lane == 0) mbar_arrive(lofull + l);
-        if (st == 0 && g == kGroups - 1) TC_TRACE(it, 6);
-        if (++s == SH) { s = 0; ph ^= 1; }
-        if (++l == SL) { l = 0; lph ^= 1; }
+      } else {
+        constexpr int kItems = 4 * kRowsUsed * 8;  // 16-B units
+        for (int i = st; i < kItems; i += 32 * kTcSplitWarps) {
+          const int blk = i / (kRowsUsed * 8), rem = i - blk * (kRowsUsed * 8);
+          const uint32_t o = (uint32_t)blk * kAtomBytes + 16u * (uint32_t)rem;
+          const float4 v = lds128(src + o);
+          sts128(dst + o, v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
+                 v.w - tf32_trunc(v.w));
+        }
       }
+      fence_proxy_async_smem();  // generic-proxy writes -> tensor core reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(lofull + l);
+      if (st == 0) TC_TRACE(it, 5);
+      if (++s == SH) { s = 0; ph ^= 1; }
+      if (++l == SL) { l = 0; lph ^= 1; }
     }
   } else {
     // epilogue: lane r of quarter q owns output row r = 32q + lane of each chunk;
@@ -560,21 +551,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
 }
 
 size_t conv_tc_smem_bytes(int hi_slots, int lo_slots, int nc) {
-  const int group = nc == 128 ? TcShape<128>::kGroup : TcShape<64>::kGroup;
-  return 1024 + (size_t)(hi_slots + lo_slots) * group * nc * 128 + 8 * (2 * hi_slots + 2 * lo_slots + 4) +
+  const size_t stage = 4 * (size_t)(nc + 8) * 128;
+  return 1024 + (size_t)(hi_slots + lo_slots) * stage + 8 * (2 * hi_slots + 2 * lo_slots + 4) +
          24 * kTcTileRing + 16 + 2 * sizeof(float) * (kConvTcMaxK + 256);
 }
 
 template <int NC, bool kMixed>
 static cudaError_t launch_nc(ConvTCParams& p, cudaStream_t stream, int grid) {
-  // lo ring: four group slots (the split runs ahead of the MMAs);
-  // hi ring: every remaining slot (TMA prefetch depth)
-  if (p.lo_bufs < 1) p.lo_bufs = NC == 128 ? 2 : 4;
-  int SH = 32;
-  while (SH > TcShape<NC>::kGroups && conv_tc_smem_bytes(SH, p.lo_bufs, NC) > (size_t)kSmemBudget) --SH;
+  // lo ring: two tile stages (the split runs ahead of the MMAs); hi ring: every
+  // remaining stage (TMA prefetch depth)
+  if (p.lo_bufs < 1) p.lo_bufs = 2;
+  int SH = kTcTileRing - 4;
+  while (SH > 2 && conv_tc_smem_bytes(SH, p.lo_bufs, NC) > (size_t)kSmemBudget) --SH;
   if (conv_tc_smem_bytes(SH, p.lo_bufs, NC) > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
   p.hi_stages = SH;
-  if (SH / TcShape<NC>::kGroups + TcShape<NC>::kDBufs + 2 > kTcTileRing) return cudaErrorInvalidConfiguration;
   p.ntiles = (p.m_ext + NC - 1) / NC;
   auto kfn = conv_tc_kernel<NC, kMixed>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));

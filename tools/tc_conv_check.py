@@ -88,7 +88,7 @@ def trace():
     t = allv[:512].reshape(64, 8)
 
     t0 = t[0, 0]
-    names = ["P.start", "P.issued", "M.dempty", "M.data", "M.issued", "S.full0", "S.done", "E.dfull"]
+    names = ["P.iss0", "P.iss1", "S.full0", "M.data0", "M.issued", "S.full1", "M.data1", "E.dfull"]
     print("tile " + " ".join(f"{n:>9s}" for n in names))
     n = 0
     for i in range(t.shape[0]):
