@@ -199,7 +199,6 @@ __device__ __forceinline__ void tc_trace_stamp(unsigned long long* tr, int slot)
 // k <= 65 (the Toeplitz is zero beyond k); the pipelines move whole tiles (one
 // TMA box of 4 K-atom blocks, one split pass, 24 K-steps of MMAs per sync).
 constexpr int kTcK = 192;
-constexpr int kTcAtoms = kTcK / 32;
 // accumulator buffers per chunk count: NC = 64 keeps two TMEM
 // accumulators (epilogue of tile i overlaps the MMAs of tile i+1); NC = 128
 // (N = 128 MMAs: half the issue count) has room for one, drained by the
@@ -209,8 +208,11 @@ template <int NC> struct TcShape {
   static constexpr int kDBufs = NC == 128 ? 1 : 2;
 };
 
-template <int NC, bool kMixed>
+// KA = MMA K-atoms: 6 (K = 192) for k <= 65, 5 (K = 160) for k <= 33
+template <int NC, bool kMixed, int KA>
 __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_constant__ ConvTCParams p) {
+  static_assert(KA == 5 || KA == 6, "K-atoms 4 and 5 are read from blocks 0 and 1");
+  constexpr int kK = 32 * KA;
   static_assert(NC % 32 == 0 && NC <= 128, "NC/2 columns per epilogue warp, loaded 16 at a time");
   constexpr int kBlockRows = TcShape<NC>::kBlockRows, ND = TcShape<NC>::kDBufs;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -251,7 +253,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
   // fsm[0][128 + t] = hi(f_t), fsm[1][128 + t] = lo(f_t); zeros around, so the
   // Toeplitz row r reads fsm[.][128 + kk - r] without bounds checks.
   constexpr int kFPad = kConvTcMaxK + 256;
-  static_assert(128 + kTcK <= kFPad, "Toeplitz reads stay inside fsm");
+  static_assert(128 + kTcK <= kFPad, "Toeplitz reads stay inside fsm");  // (kK <= kTcK)
   for (int i = threadIdx.x; i < kFPad; i += kTcThreads) {
     const int t = i - 128;
     const float f = (t >= 0 && t < p.k) ? p.taps[t] : 0.0f;
@@ -326,7 +328,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
     const int r = 32 * q + lane;
     const uint32_t lanebits = (uint32_t)(32 * q) << 16;
 #pragma unroll 1
-    for (int c = 0; c < kTcK; c += 32) {
+    for (int c = 0; c < kK; c += 32) {
       float vh[32], vl[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -381,7 +383,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
       tc_fence_after();
       const uint64_t dh = dhi0 + (uint64_t)((s * kSlot) >> 4), dl = dlo0 + (uint64_t)((l * kSlot) >> 4);
 #pragma unroll
-      for (int kb = 0; kb < 4 * kTcAtoms; ++kb) {
+      for (int kb = 0; kb < 4 * KA; ++kb) {
         // K-step kb: K-atom a = kb / 4 -> block a (a < 4) or block a - 4 one row down; 32-B column block kb % 4
         const int a = kb >> 2;
         const uint64_t off = (uint64_t)(((uint32_t)(a & 3) * kAtomBytes + (a >= 4 ? 128u : 0u) + 32u * (kb & 3)) >> 4);
@@ -556,7 +558,7 @@ size_t conv_tc_smem_bytes(int hi_slots, int lo_slots, int nc) {
          24 * kTcTileRing + 16 + 2 * sizeof(float) * (kConvTcMaxK + 256);
 }
 
-template <int NC, bool kMixed>
+template <int NC, bool kMixed, int KA>
 static cudaError_t launch_nc(ConvTCParams& p, cudaStream_t stream, int grid) {
   // lo ring: two tile stages (the split runs ahead of the MMAs); hi ring: every
   // remaining stage (TMA prefetch depth)
@@ -566,7 +568,7 @@ static cudaError_t launch_nc(ConvTCParams& p, cudaStream_t stream, int grid) {
   if (conv_tc_smem_bytes(SH, p.lo_bufs, NC) > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
   p.hi_stages = SH;
   p.ntiles = (p.m_ext + NC - 1) / NC;
-  auto kfn = conv_tc_kernel<NC, kMixed>;
+  auto kfn = conv_tc_kernel<NC, kMixed, KA>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
   if (e != cudaSuccess) return e;
   int64_t g = p.ntiles < grid ? p.ntiles : grid;
@@ -577,12 +579,16 @@ static cudaError_t launch_nc(ConvTCParams& p, cudaStream_t stream, int grid) {
 }
 
 cudaError_t launch_conv_tc(ConvTCParams& p, int nc, cudaStream_t stream, int grid) {
+  // K = 32 KA >= 127 + k: 160 covers k <= 33, 192 covers k <= 65
+  const int ka = 127 + p.k <= 160 ? 5 : 6;
   const bool mixed = p.mixed != 0;
-  switch (nc) {
-    case 64: return mixed ? launch_nc<64, true>(p, stream, grid) : launch_nc<64, false>(p, stream, grid);
-    case 128: return mixed ? launch_nc<128, true>(p, stream, grid) : launch_nc<128, false>(p, stream, grid);
-    default: return cudaErrorInvalidValue;
-  }
+  if (nc != 64 && nc != 128) return cudaErrorInvalidValue;
+#define SS_TC_LAUNCH(NC_, M_, KA_) \
+  if (nc == NC_ && mixed == M_ && ka == KA_) return launch_nc<NC_, M_, KA_>(p, stream, grid);
+  SS_TC_LAUNCH(64, true, 5) SS_TC_LAUNCH(64, true, 6) SS_TC_LAUNCH(64, false, 5) SS_TC_LAUNCH(64, false, 6)
+  SS_TC_LAUNCH(128, true, 5) SS_TC_LAUNCH(128, true, 6) SS_TC_LAUNCH(128, false, 5) SS_TC_LAUNCH(128, false, 6)
+#undef SS_TC_LAUNCH
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace ss
