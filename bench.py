@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """Benchmark of the sliding-window-sum hot path (arXiv 2305.16513) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload suite|cfg1..cfg5]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload suite|cfg1..cfg5|...]
                     [--impl ours|reference] [--no-e2e] [--no-cpu-baseline] [--cells-out F]
+                    [--graph | --no-graph] [--cell-timing separate|inline]
 
 One STEP = one pass of the whole hot path over one batch of the workload's
 synthetic inputs (BASELINE.json configs, seeded, generated on the device by
@@ -18,8 +19,13 @@ HBM GB/s = (input bytes + output bytes) / time.
 
 Timing: W untimed warm-up steps, then K steps bracketed by barrier +
 cuda.synchronize on both sides, timed with CUDA events on the launch stream,
-max over ranks.  Each kernel is also bracketed by events on the same stream
-(live per-kernel durations -> the dominant kernel's roofline).  L2: every
+max over ranks.  On one GPU the step is captured once as a CUDA graph and
+replayed (--no-graph: eager launches; multi-GPU is always eager: the halo
+exchange is not captured).  Per-kernel durations (-> the dominant kernel's
+roofline) come from CUDA events around every launch on the same stream, in an
+eager pass of K more steps right after the timed ones (--cell-timing
+separate, default: an event pair between every two kernels costs ~7% of the
+step), or inside the timed eager steps (--cell-timing inline).  L2: every
 cell's input is larger than L2 (126 MB) or, for cfg4, each cell reads its own
 copy of the input, so no cell starts with its input L2-resident.
 
@@ -629,6 +635,8 @@ def run_ours(args):
     device = torch.device("cuda", torch.cuda.current_device())
     import paper_2305_16513_b200 as ss
     weak = args.scaling == "weak"
+    if args.graph is None:  # default: replay the step as a CUDA graph on one GPU (halo exchange is not captured)
+        args.graph = world == 1
     if args.graph:  # graphs are captured on a non-default stream: run everything there
         torch.cuda.set_stream(torch.cuda.Stream())
     R = Runner(args.workload, world, rank, device, weak=weak)
@@ -658,7 +666,7 @@ def run_ours(args):
     events = []
     graph = None
     if args.graph:
-        # launch-bound workloads (cfg1): capture one step in a CUDA graph and replay it;
+        # capture one step in a CUDA graph and replay it (no host launch gaps between kernels);
         # per-kernel durations come from one eager pass with events (below)
         if world > 1:
             raise SystemExit("--graph is single-GPU only (the halo exchange is not captured)")
@@ -680,14 +688,15 @@ def run_ours(args):
             if graph is not None:
                 graph.replay()
             else:
-                R.step(events)
+                R.step(events if args.cell_timing == "inline" else None)
         t1.record(R.stream)
         torch.cuda.synchronize()
         barrier()
     launches = ss.ss_launch_count() - n_launch0
     if graph is not None:
         launches = launches_per_step * args.steps
-        for _ in range(3):  # eager pass for the per-kernel event durations
+    if graph is not None or args.cell_timing == "separate":
+        for _ in range(args.steps):  # instrumented eager pass: the per-kernel event durations
             R.step(events)
         torch.cuda.synchronize()
     ms_local = t0.elapsed_time(t1)
@@ -786,6 +795,9 @@ def run_ours(args):
 
     if rank == 0:
         cfg = {"workload": args.workload, "cells": [c.name for c in R.cells], "cuda_graph": bool(args.graph),
+               "cell_timing": ("per-launch CUDA events in the timed steps" if args.cell_timing == "inline" and not
+                               args.graph else "per-launch CUDA events in an eager pass of the same steps right "
+                               "after the timed ones (the timed steps carry no per-launch events)"),
                "parallelism": f"{'seq+batch' if args.workload == 'suite' else 'shard'} x{world}",
                "l2": "inputs > L2 (126 MB) per cell; cfg4 cells read distinct input copies",
                "inputs": {k: {kk: vv for kk, vv in v.items() if kk != "kw"} for k, v in R.inputs_spec.items()}}
@@ -956,7 +968,12 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="multi-GPU: weak = N x the BASELINE shape (config-sized share per rank), strong = split it")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--graph", action="store_true", help="replay each timed step as a captured CUDA graph")
+    ap.add_argument("--graph", dest="graph", action="store_true", default=None,
+                    help="replay each timed step as a captured CUDA graph (default on 1 GPU)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false", help="launch every timed step eagerly")
+    ap.add_argument("--cell-timing", choices=("inline", "separate"), default="separate",
+                    help="per-kernel CUDA events inside the timed steps (inline) or in a second pass of the "
+                         "same steps right after them (separate: the timed steps carry no events)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
