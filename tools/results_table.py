@@ -15,9 +15,10 @@ hb = line["hbm_gbs"]
 text = (f"Suite: **{line['value']:.1f} GElem/s**, {line['ms_per_step']:.3f} ms/step, {hb:.0f} GB/s algorithmic "
         f"({hb / 6556.2 * 100:.1f}% of measured HBM,\n{hb / 8000 * 100:.0f}% of 8 TB/s); e2e {line['e2e']['value']:.1f} "
         f"GElem/s ({line['e2e']['ms_per_step']:.1f} ms/step, PCIe-bound); CPU oracle\n"
-        f"{line['cpu_baseline']['value']:.4f} GElem/s ({line['cpu_baseline']['cores']} core). Per kernel, live in the "
-        "suite (each cell also pays for the L2 write-back of\nthe previous cell's output, so isolated numbers are "
-        "higher -- e.g. cfg4 2x2 runs at 6.0 TB/s alone under ncu):\n\n"
+        f"{line['cpu_baseline']['value']:.4f} GElem/s ({line['cpu_baseline']['cores']} core); CUDA-graph replay "
+        f"of the step: {line['config'].get('cuda_graph')}. Per kernel, from the "
+        "instrumented eager pass (each cell also pays for the L2 write-back of\nthe previous cell's output and for the "
+        "event pair around it, so isolated numbers are higher -- e.g. cfg4 2x2\nruns at 6.0 TB/s alone under ncu):\n\n"
         "| cell | us | GElem/s | GB/s | of 6549 | of 8 TB/s | FP32 FMA / TC frac |\n|---|---|---|---|---|---|---|\n"
         + "\n".join(rows) + "\n\n")
 p = os.path.join(ROOT, "DESIGN.md")
