@@ -430,6 +430,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
         // receives the bf16(xh), the other the bf16(xl).  (Block bases are
         // multiples of 1024 B, so the row parity is the in-block row's.)
         constexpr int kItems = 4 * kRowsUsed * 4;
+#pragma unroll
         for (int i = st; i < kItems; i += 32 * kTcSplitWarps) {
           const int blk = i / (kRowsUsed * 4), rem = i - blk * (kRowsUsed * 4);
           const uint32_t o = (uint32_t)blk * kAtomBytes + 32u * (uint32_t)rem;  // rem = row * 4 + unit pair
@@ -450,6 +451,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
         }
       } else {
         constexpr int kItems = 4 * kRowsUsed * 8;  // 16-B units
+#pragma unroll
         for (int i = st; i < kItems; i += 32 * kTcSplitWarps) {
           const int blk = i / (kRowsUsed * 8), rem = i - blk * (kRowsUsed * 8);
           const uint32_t o = (uint32_t)blk * kAtomBytes + 16u * (uint32_t)rem;
