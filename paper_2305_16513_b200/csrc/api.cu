@@ -608,6 +608,7 @@ ss_status_t ss_conv1d_mc(const void* x, const void* w, float* y, int64_t batch, 
   const bool tc = (cin == 64 || cin == 128) && (cout == 64 || cout == 128) && k <= 9 &&
                   (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
                   encode_mc_map(&p.tm_x, x, batch * N, cin);
+  p.sched = sched_slot(static_cast<cudaStream_t>(stream));
   cudaError_t e = launch_conv_mc(p, tc, static_cast<cudaStream_t>(stream), current_sms());
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv1d_mc launch");
 }

@@ -38,6 +38,7 @@ constexpr int kMcWarpEpi0 = 2;
 constexpr int kMcEpiWarps = 8;
 constexpr int kMcRows = 136;  // staged positions per tile: 128 + k - 1 <= 136, a multiple of 8
 constexpr int kMcStages = 3;
+constexpr int kMcRing = 8;    // tile-id ring entries
 
 __device__ __forceinline__ uint64_t sw128_desc_mc(uint32_t saddr) {
   uint64_t d = 0;
@@ -119,12 +120,18 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
   uint64_t* empty = full + kMcStages;                  // [kMcStages]
   uint64_t* dfull = empty + kMcStages;                 // [2]
   uint64_t* dempty = dfull + 2;                        // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
+  // tile ids, producer -> MMA (read after its `full` wait) and epilogue (own barrier pair);
+  // the producer is at most kMcStages + 2 tiles ahead of the epilogue
+  uint64_t* tfull = dempty + 2;                        // [kMcRing]
+  uint64_t* tempty = tfull + kMcRing;                  // [kMcRing]
+  int64_t* tring = reinterpret_cast<int64_t*>(tempty + kMcRing);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tring + kMcRing);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kMcStages; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(dfull + i, 1); mbar_init(dempty + i, kMcEpiWarps); }
+    for (int i = 0; i < kMcRing; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, kMcEpiWarps); }
     fence_mbar_init();
     prefetch_tmap(&p.tm_x);
   }
@@ -152,14 +159,29 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
   const int64_t ntiles = p.ntiles;
 
   if (warp == 0) {
-    if (lane == 0) {  // producer
+    if (lane == 0) {  // producer: tile b, then dynamic claims (or + gridDim.x)
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int64_t t = blockIdx.x;
+      for (int it = 0;; ++it) {
+        const int ts = it % kMcRing;
+        mbar_wait(tempty + ts, ((uint32_t)(it / kMcRing) & 1u) ^ 1u);
+        tring[ts] = t < ntiles ? t : -1;
+        mbar_arrive(tfull + ts);
         mbar_wait(empty + s, ph ^ 1);
+        if (t >= ntiles) {  // end marker for the MMA warp: the next `full` phase without data
+          mbar_arrive(full + s);
+          break;
+        }
+        const int64_t tnext = p.sched ? (int64_t)atomicAdd(p.sched, 1ull) + gridDim.x : t + gridDim.x;
         mbar_arrive_expect_tx(full + s, kStage);
         tma_load_3d_mc(xs + (size_t)s * kStage, &p.tm_x, 0, (int32_t)(t * 128), 0, full + s);
         if (++s == kMcStages) { s = 0; ph ^= 1; }
+        t = tnext;
+      }
+      if (p.sched && atomicAdd(p.sched + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
+        p.sched[0] = 0;
+        p.sched[1] = 0;
       }
     }
   } else if (warp == kMcWarpMma) {
@@ -169,9 +191,10 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
     const uint32_t dc0 = __shfl_sync(0xffffffffu, tmem, 0);
     int s = 0, d = 0;
     uint32_t ph = 0, dph = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      mc_wait(dempty + d, dph ^ 1);
+    for (int it = 0;; ++it) {
       mc_wait(full + s, ph);
+      if (*reinterpret_cast<volatile int64_t*>(tring + it % kMcRing) < 0) break;
+      mc_wait(dempty + d, dph ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t dcol = dc0 + (uint32_t)(d * COUT);
       const uint64_t dxs = dx0 + (uint64_t)((s * kStage) >> 4);
@@ -199,7 +222,13 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
     const int q = warp & 3, h = (warp - kMcWarpEpi0) >> 2;
     int d = 0;
     uint32_t dph = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int it = 0;; ++it) {
+      const int ts = it % kMcRing;
+      mc_wait(tfull + ts, (uint32_t)(it / kMcRing) & 1u);
+      const int64_t t = *reinterpret_cast<volatile int64_t*>(tring + ts);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + ts);
+      if (t < 0) break;
       mc_wait(dfull + d, dph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       uint32_t v[2][NH / 8][4];
@@ -258,7 +287,8 @@ __global__ void __launch_bounds__(256) conv_mc_direct_kernel(const __grid_consta
 
 size_t conv_mc_smem_bytes(int64_t cin, int64_t cout, int64_t k) {
   const size_t stage = (size_t)(cin / 64) * kMcRows * 128;
-  return 1024 + kMcStages * stage + (size_t)k * (cin / 64) * cout * 128 + 8 * (2 * kMcStages + 4) + 16;
+  return 1024 + kMcStages * stage + (size_t)k * (cin / 64) * cout * 128 + 8 * (2 * kMcStages + 4) +
+         24 * kMcRing + 16;
 }
 
 template <int CIN, int COUT>

@@ -183,6 +183,7 @@ struct alignas(64) ConvMcParams {
   float* y;          // [batch][L][cout] fp32
   int64_t batch, N, L, cin, cout, k;
   int64_t ntiles;    // set by launch_conv_mc
+  unsigned long long* sched;  // dynamic tile counter slot (null: static round robin)
 };
 bool encode_mc_map(CUtensorMap* m, const void* x, int64_t positions, int64_t cin);
 cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t stream, int sms);
