@@ -809,23 +809,37 @@ __global__ void __launch_bounds__(512) pool2d_backward_plane_kernel(const __grid
 template <bool kAvg, int KH, int KW, int SH, int SW>
 __global__ void __launch_bounds__(256, 2) pool2d_backward_fixed_kernel(const __grid_constant__ Pool2DBackwardParams p) {
   extern __shared__ __align__(16) float s_fx[];
-  constexpr int NR = (KH + SH - 1) / SH, NCW = (KW + SW - 1) / SW;  // candidate windows per dimension
   const int H = (int)p.H, W = (int)p.W, OH = (int)p.OH, OW = (int)p.OW;
-  float* g = s_fx;                          // dy plane [OH][OW]
-  float* aux = s_fx + OH * OW;              // avg: R [OH][W]; max: argmax table [OH][OW] (int)
-  int* tab = reinterpret_cast<int*>(aux);
+  // shared: dy plane [OH][OW] (g), then avg: row sums [OH][W]; max: x plane [H][W] and the
+  // window-relative first-argmax table [OH][OW] (uint8, a * KW + b)
+  const int gsz = (OH * OW + 3) & ~3;
+  float* g = s_fx;
+  float* aux = s_fx + gsz;
+  float* xs = aux;
+  uint8_t* tab = reinterpret_cast<uint8_t*>(aux + ((H * W + 3) & ~3));
+  // 16-B cp.async when the planes' starts are 16-B aligned, else 4-B
+  auto stage = [&](float* dst, const float* __restrict__ src, int n) {
+    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && (n & 3) == 0) {
+      for (int e = 4 * threadIdx.x; e < n; e += 4 * 256) cp_async16(smem_u32(dst + e), src + e, 16u);
+    } else {
+      for (int e = threadIdx.x; e < n; e += 256) cp_async4(smem_u32(dst + e), src + e, 4u);
+    }
+  };
   for (int64_t pl = blockIdx.x; pl < p.planes; pl += gridDim.x) {
     const float* __restrict__ gp = p.dy + pl * OH * OW;
     float* __restrict__ d = p.dx + pl * H * W;
+    __syncthreads();  // the previous plane's readers are done
+    stage(g, gp, OH * OW);
+    if constexpr (!kAvg) stage(xs, p.x + pl * H * W, H * W);
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
-    for (int e = threadIdx.x; e < OH * OW; e += 256) g[e] = __ldg(gp + e);
     if constexpr (!kAvg && SH == 1) {
-      // overlapping window rows: each thread walks one window column down a band
-      // of rows with a ring of the last KH row results (first max of the row's KW
-      // inputs, value + column); the window's first row-major maximum is the
+      // overlapping window rows: each task walks one window column down a band of
+      // rows with a ring of the last KH row results (first max of the row's KW
+      // inputs, value + offset); the window's first row-major maximum is the
       // first strictly greater row result in row order
-      const float* __restrict__ xp = p.x + pl * H * W;
-      const int bands = 256 / OW > 0 ? 256 / OW : 1;
+      const int bands = 512 / OW > 0 ? 512 / OW : 1;
       const int band_rows = (OH + bands - 1) / bands;
       for (int u = threadIdx.x; u < OW * bands; u += 256) {
         const int c = u % OW, band = u / OW;
@@ -833,73 +847,52 @@ __global__ void __launch_bounds__(256, 2) pool2d_backward_fixed_kernel(const __g
         if (ra >= rb) continue;
         float rv[KH];
         int rc[KH];
-        auto row_first_max = [&](int h, float& v, int& col) {
-          const float* xr = xp + h * W + c * SW;
-          v = __ldg(xr);
-          col = c * SW;
+        auto row_first_max = [&](int h, float& v, int& off) {
+          const float* xr = xs + h * W + c * SW;
+          v = xr[0];
+          off = 0;
 #pragma unroll
-          for (int b = 1; b < KW; ++b) {
-            const float t = __ldg(xr + b);
-            if (t > v) { v = t; col = c * SW + b; }
+          for (int b2 = 1; b2 < KW; ++b2) {
+            const float t = xr[b2];
+            if (t > v) { v = t; off = b2; }
           }
         };
 #pragma unroll
-        for (int a = 0; a < KH - 1; ++a) row_first_max(ra + a, rv[a + 1], rc[a + 1]);
+        for (int a2 = 0; a2 < KH - 1; ++a2) row_first_max(ra + a2, rv[a2 + 1], rc[a2 + 1]);
         for (int r = ra; r < rb; ++r) {
 #pragma unroll
-          for (int a = 0; a < KH - 1; ++a) { rv[a] = rv[a + 1]; rc[a] = rc[a + 1]; }
+          for (int a2 = 0; a2 < KH - 1; ++a2) { rv[a2] = rv[a2 + 1]; rc[a2] = rc[a2 + 1]; }
           row_first_max(r + KH - 1, rv[KH - 1], rc[KH - 1]);
           float m = rv[0];
-          int best = r * W + rc[0];
+          int best = rc[0];
 #pragma unroll
-          for (int a = 1; a < KH; ++a)
-            if (rv[a] > m) { m = rv[a]; best = (r + a) * W + rc[a]; }
-          tab[r * OW + c] = best;
+          for (int a2 = 1; a2 < KH; ++a2)
+            if (rv[a2] > m) { m = rv[a2]; best = a2 * KW + rc[a2]; }
+          tab[r * OW + c] = (uint8_t)best;
         }
       }
     } else if constexpr (!kAvg) {
-      const float* __restrict__ xp = p.x + pl * H * W;
       for (int e = threadIdx.x; e < OH * OW; e += 256) {
         const int r = e / OW, c = e - r * OW;
-        const float* xw = xp + r * SH * W + c * SW;
-        float m = __ldg(xw);
+        const float* xw = xs + r * SH * W + c * SW;
+        float m = xw[0];
         int best = 0;
 #pragma unroll
-        for (int a = 0; a < KH; ++a)
+        for (int a2 = 0; a2 < KH; ++a2)
 #pragma unroll
-          for (int b = 0; b < KW; ++b) {
-            const float v = __ldg(xw + a * W + b);
-            if (v > m) { m = v; best = a * W + b; }
+          for (int b2 = 0; b2 < KW; ++b2) {
+            const float v = xw[a2 * W + b2];
+            if (v > m) { m = v; best = a2 * KW + b2; }
           }
-        tab[e] = (r * SH) * W + c * SW + best;
+        tab[e] = (uint8_t)best;
       }
     }
     __syncthreads();
-    if constexpr (kAvg) {
-      for (int e = threadIdx.x; e < OH * W; e += 256) {  // row pass
-        const int r = e / W, c = e - r * W;
-        const int c0 = c - KW + 1 <= 0 ? 0 : (c - KW + SW) / SW;
-        float acc = 0.0f;
-#pragma unroll
-        for (int q = 0; q < NCW; ++q) {
-          const int cc = c0 + q;
-          if (cc * SW <= c && cc < OW) acc = __fadd_rn(acc, g[r * OW + cc]);
-        }
-        aux[e] = acc;
-      }
-      __syncthreads();
-      for (int e = threadIdx.x; e < H * W; e += 256) {  // column pass
-        const int h = e / W, c = e - h * W;
-        const int r0 = h - KH + 1 <= 0 ? 0 : (h - KH + SH) / SH;
-        float acc = 0.0f;
-#pragma unroll
-        for (int q = 0; q < NR; ++q) {
-          const int r = r0 + q;
-          if (r * SH <= h && r < OH) acc = __fadd_rn(acc, aux[r * W + c]);
-        }
-        d[e] = __fmul_rn(acc, p.inv_area);
-      }
-    } else {
+    // warps take rows, lanes columns: no index divisions, coalesced dx rows
+    const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    if constexpr (SH > 1) {
+      // strided shapes: flat position loop over the <= ceil(k/s)^2 candidate windows
+      constexpr int NR = (KH + SH - 1) / SH, NCW = (KW + SW - 1) / SW;
       for (int e = threadIdx.x; e < H * W; e += 256) {
         const int h = e / W, c = e - h * W;
         const int r0 = h - KH + 1 <= 0 ? 0 : (h - KH + SH) / SH;
@@ -910,10 +903,64 @@ __global__ void __launch_bounds__(256, 2) pool2d_backward_fixed_kernel(const __g
 #pragma unroll
           for (int qc = 0; qc < NCW; ++qc) {
             const int r = r0 + qr, cc = c0 + qc;
-            if (r * SH <= h && r < OH && cc * SW <= c && cc < OW && tab[r * OW + cc] == e)
-              acc = __fadd_rn(acc, g[r * OW + cc]);
+            if (r * SH <= h && r < OH && cc * SW <= c && cc < OW) {
+              const int q = r * OW + cc;
+              if constexpr (kAvg) {
+                acc = __fadd_rn(acc, g[q]);
+              } else {
+                const int t = tab[q];
+                if (r * SH + t / KW == h && cc * SW + t % KW == c) acc = __fadd_rn(acc, g[q]);
+              }
+            }
           }
-        d[e] = acc;
+        d[e] = kAvg ? __fmul_rn(acc, p.inv_area) : acc;
+      }
+    } else if constexpr (kAvg) {
+      for (int r = wid; r < OH; r += 8) {  // row pass: aux[r][c] = sum of the windows of row r covering c
+        for (int c = ln; c < W; c += 32) {
+          float acc = 0.0f;
+#pragma unroll
+          for (int b2 = KW - 1; b2 >= 0; --b2) {  // windows cc = (c - b2) / SW in increasing order
+            const int cw = c - b2;
+            if (cw >= 0 && cw % SW == 0 && cw / SW < OW) acc = __fadd_rn(acc, g[r * OW + cw / SW]);
+          }
+          aux[r * W + c] = acc;
+        }
+      }
+      __syncthreads();
+      for (int h = wid; h < H; h += 8) {  // column pass
+        for (int c = ln; c < W; c += 32) {
+          float acc = 0.0f;
+#pragma unroll
+          for (int a2 = KH - 1; a2 >= 0; --a2) {
+            const int rw = h - a2;
+            if (rw >= 0 && rw % SH == 0 && rw / SH < OH) acc = __fadd_rn(acc, aux[(rw / SH) * W + c]);
+          }
+          d[h * W + c] = __fmul_rn(acc, p.inv_area);
+        }
+      }
+    } else {
+      // window (r, cc) routes its dy to (r SH + a, cc SW + b) with a KW + b = its table
+      // entry, so position (h, c) takes window ((h - a) / SH, (c - b) / SW) iff that
+      // window's entry is a KW + b; windows visited in increasing row-major order
+      for (int h = wid; h < H; h += 8) {
+        for (int c = ln; c < W; c += 32) {
+          float acc = 0.0f;
+#pragma unroll
+          for (int a2 = KH - 1; a2 >= 0; --a2) {
+            const int rw = h - a2;
+            if (rw < 0 || rw % SH != 0 || rw / SH >= OH) continue;
+            const int r = rw / SH;
+#pragma unroll
+            for (int b2 = KW - 1; b2 >= 0; --b2) {
+              const int cw = c - b2;
+              if (cw < 0 || cw % SW != 0 || cw / SW >= OW) continue;
+              const int q = r * OW + cw / SW;
+              if (tab[q] == a2 * KW + b2) acc = __fadd_rn(acc, g[q]);
+            }
+          }
+          d[h * W + c] = acc;
+        }
       }
     }
   }
@@ -977,7 +1024,11 @@ cudaError_t launch_pool_max_backward(const BackwardParams& p, cudaStream_t strea
 
 template <int KH, int KW, int SH, int SW>
 static cudaError_t launch_pool2d_bwd_fixed(const Pool2DBackwardParams& p, cudaStream_t stream, int sms) {
-  const size_t smem = (size_t)(p.OH * p.OW + (p.mode == 1 ? p.OH * p.W : p.OH * p.OW)) * sizeof(float);
+  // dy plane + (avg) row sums or (max) x plane and a byte table, all 16-B padded
+  const size_t r4 = [](int64_t n) { return (size_t)((n + 3) & ~int64_t(3)); }(p.OH * p.OW);
+  const size_t smem = p.mode == 1 ? (r4 + (size_t)p.OH * p.W) * sizeof(float)
+                                  : (r4 + (size_t)((p.H * p.W + 3) & ~int64_t(3))) * sizeof(float) +
+                                        (size_t)p.OH * p.OW;
   if (smem > (size_t)kSmemBudget / 2 || p.H * p.W >= (int64_t(1) << 30)) return cudaErrorInvalidConfiguration;
   const int64_t g = p.planes < (int64_t)sms * 2 ? p.planes : (int64_t)sms * 2;
   auto kfn = p.mode == 1 ? pool2d_backward_fixed_kernel<true, KH, KW, SH, SW>
