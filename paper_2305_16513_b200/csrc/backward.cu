@@ -810,13 +810,12 @@ template <bool kAvg, int KH, int KW, int SH, int SW>
 __global__ void __launch_bounds__(256, 2) pool2d_backward_fixed_kernel(const __grid_constant__ Pool2DBackwardParams p) {
   extern __shared__ __align__(16) float s_fx[];
   const int H = (int)p.H, W = (int)p.W, OH = (int)p.OH, OW = (int)p.OW;
-  // shared: dy plane [OH][OW] (g), then avg: row sums [OH][W]; max: x plane [H][W] and the
-  // window-relative first-argmax table [OH][OW] (uint8, a * KW + b)
+  // shared: dy plane [OH][OW] (g); max: then the x plane [H][W] and the window-relative
+  // first-argmax table [OH][OW] (uint8, a * KW + b)
   const int gsz = (OH * OW + 3) & ~3;
   float* g = s_fx;
-  float* aux = s_fx + gsz;
-  float* xs = aux;
-  uint8_t* tab = reinterpret_cast<uint8_t*>(aux + ((H * W + 3) & ~3));
+  float* xs = s_fx + gsz;
+  uint8_t* tab = reinterpret_cast<uint8_t*>(xs + ((H * W + 3) & ~3));
   // 16-B cp.async when the planes' starts are 16-B aligned, else 4-B
   auto stage = [&](float* dst, const float* __restrict__ src, int n) {
     if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && (n & 3) == 0) {
@@ -888,8 +887,6 @@ __global__ void __launch_bounds__(256, 2) pool2d_backward_fixed_kernel(const __g
       }
     }
     __syncthreads();
-    // warps take rows, lanes columns: no index divisions, coalesced dx rows
-    const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31;
     if constexpr (SH > 1) {
       // strided shapes: flat position loop over the <= ceil(k/s)^2 candidate windows
       constexpr int NR = (KH + SH - 1) / SH, NCW = (KW + SW - 1) / SW;
@@ -916,49 +913,77 @@ __global__ void __launch_bounds__(256, 2) pool2d_backward_fixed_kernel(const __g
         d[e] = kAvg ? __fmul_rn(acc, p.inv_area) : acc;
       }
     } else if constexpr (kAvg) {
-      for (int r = wid; r < OH; r += 8) {  // row pass: aux[r][c] = sum of the windows of row r covering c
-        for (int c = ln; c < W; c += 32) {
+      // dx[h][c] = (sum over windows (h - a, c - b)) / (KH KW): tasks walk one column down a
+      // band of rows with a ring of the KH window-row sums R[r] = sum_b dy[r][c - b] (windows
+      // in increasing column order), summed in increasing row order -- the separable form
+      const int bands = 512 / W > 0 ? 512 / W : 1;
+      const int band_rows = (H + bands - 1) / bands;
+      for (int u = threadIdx.x; u < W * bands; u += 256) {
+        const int c = u % W, band = u / W;
+        const int ha = band * band_rows, hb = min(ha + band_rows, H);
+        if (ha >= hb) continue;
+        float R[KH];
+        auto row_sum = [&](int r) {
+          float acc = 0.0f;
+          if (r >= 0 && r < OH) {
+#pragma unroll
+            for (int b2 = KW - 1; b2 >= 0; --b2) {
+              const int cc = c - b2;
+              if (cc >= 0 && cc < OW) acc = __fadd_rn(acc, g[r * OW + cc]);
+            }
+          }
+          return acc;
+        };
+#pragma unroll
+        for (int a2 = 0; a2 < KH - 1; ++a2) R[a2] = row_sum(ha - 1 - a2);  // state at h = ha - 1
+        for (int h = ha; h < hb; ++h) {
+#pragma unroll
+          for (int a2 = KH - 1; a2 > 0; --a2) R[a2] = R[a2 - 1];
+          R[0] = row_sum(h);
           float acc = 0.0f;
 #pragma unroll
-          for (int b2 = KW - 1; b2 >= 0; --b2) {  // windows cc = (c - b2) / SW in increasing order
-            const int cw = c - b2;
-            if (cw >= 0 && cw % SW == 0 && cw / SW < OW) acc = __fadd_rn(acc, g[r * OW + cw / SW]);
-          }
-          aux[r * W + c] = acc;
-        }
-      }
-      __syncthreads();
-      for (int h = wid; h < H; h += 8) {  // column pass
-        for (int c = ln; c < W; c += 32) {
-          float acc = 0.0f;
-#pragma unroll
-          for (int a2 = KH - 1; a2 >= 0; --a2) {
-            const int rw = h - a2;
-            if (rw >= 0 && rw % SH == 0 && rw / SH < OH) acc = __fadd_rn(acc, aux[(rw / SH) * W + c]);
-          }
+          for (int a2 = KH - 1; a2 >= 0; --a2)
+            if (h - a2 >= 0 && h - a2 < OH) acc = __fadd_rn(acc, R[a2]);
           d[h * W + c] = __fmul_rn(acc, p.inv_area);
         }
       }
     } else {
-      // window (r, cc) routes its dy to (r SH + a, cc SW + b) with a KW + b = its table
-      // entry, so position (h, c) takes window ((h - a) / SH, (c - b) / SW) iff that
-      // window's entry is a KW + b; windows visited in increasing row-major order
-      for (int h = wid; h < H; h += 8) {
-        for (int c = ln; c < W; c += 32) {
+      // window (r, cc) routes its dy to (r + a, cc + b) with a KW + b = its table entry.
+      // Tasks walk one column c down a band of rows and keep the table entries and dy of
+      // the KH window rows r = h - a (columns cc = c - b) in a register ring: each step
+      // loads one new window row (KW entries) instead of all KH x KW candidates.
+      const int bands = 512 / W > 0 ? 512 / W : 1;
+      const int band_rows = (H + bands - 1) / bands;
+      for (int u = threadIdx.x; u < W * bands; u += 256) {
+        const int c = u % W, band = u / W;
+        const int ha = band * band_rows, hb = min(ha + band_rows, H);
+        if (ha >= hb) continue;
+        int T[KH][KW];
+        float G[KH][KW];
+        auto load_row = [&](int r, int (&t)[KW], float (&gv)[KW]) {
+#pragma unroll
+          for (int b2 = 0; b2 < KW; ++b2) {
+            const int cc = c - b2;
+            const bool ok = r >= 0 && r < OH && cc >= 0 && cc < OW;
+            t[b2] = ok ? (int)tab[r * OW + cc] : -1;
+            gv[b2] = ok ? g[r * OW + cc] : 0.0f;
+          }
+        };
+        // state before the first step (h = ha - 1): slot a2 holds window row ha - 1 - a2
+#pragma unroll
+        for (int a2 = 0; a2 < KH - 1; ++a2) load_row(ha - 1 - a2, T[a2], G[a2]);
+        for (int h = ha; h < hb; ++h) {
+#pragma unroll
+          for (int a2 = KH - 1; a2 > 0; --a2)
+#pragma unroll
+            for (int b2 = 0; b2 < KW; ++b2) { T[a2][b2] = T[a2 - 1][b2]; G[a2][b2] = G[a2 - 1][b2]; }
+          load_row(h, T[0], G[0]);
           float acc = 0.0f;
 #pragma unroll
-          for (int a2 = KH - 1; a2 >= 0; --a2) {
-            const int rw = h - a2;
-            if (rw < 0 || rw % SH != 0 || rw / SH >= OH) continue;
-            const int r = rw / SH;
+          for (int a2 = KH - 1; a2 >= 0; --a2)  // windows in increasing row-major order
 #pragma unroll
-            for (int b2 = KW - 1; b2 >= 0; --b2) {
-              const int cw = c - b2;
-              if (cw < 0 || cw % SW != 0 || cw / SW >= OW) continue;
-              const int q = r * OW + cw / SW;
-              if (tab[q] == a2 * KW + b2) acc = __fadd_rn(acc, g[q]);
-            }
-          }
+            for (int b2 = KW - 1; b2 >= 0; --b2)
+              if (T[a2][b2] == a2 * KW + b2) acc = __fadd_rn(acc, G[a2][b2]);
           d[h * W + c] = acc;
         }
       }
@@ -1026,15 +1051,19 @@ template <int KH, int KW, int SH, int SW>
 static cudaError_t launch_pool2d_bwd_fixed(const Pool2DBackwardParams& p, cudaStream_t stream, int sms) {
   // dy plane + (avg) row sums or (max) x plane and a byte table, all 16-B padded
   const size_t r4 = [](int64_t n) { return (size_t)((n + 3) & ~int64_t(3)); }(p.OH * p.OW);
-  const size_t smem = p.mode == 1 ? (r4 + (size_t)p.OH * p.W) * sizeof(float)
+  const size_t smem = p.mode == 1 ? r4 * sizeof(float)
                                   : (r4 + (size_t)((p.H * p.W + 3) & ~int64_t(3))) * sizeof(float) +
                                         (size_t)p.OH * p.OW;
   if (smem > (size_t)kSmemBudget / 2 || p.H * p.W >= (int64_t(1) << 30)) return cudaErrorInvalidConfiguration;
-  const int64_t g = p.planes < (int64_t)sms * 2 ? p.planes : (int64_t)sms * 2;
   auto kfn = p.mode == 1 ? pool2d_backward_fixed_kernel<true, KH, KW, SH, SW>
                          : pool2d_backward_fixed_kernel<false, KH, KW, SH, SW>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
   if (e != cudaSuccess) return e;
+  int per_sm = 0;  // resident CTAs: one wave of the plane loop
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 256, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t cap = (int64_t)sms * (per_sm < 1 ? 1 : per_sm);
+  const int64_t g = p.planes < cap ? p.planes : cap;
   kfn<<<(unsigned)g, 256, smem, stream>>>(p);
   note_launch();
   return cudaGetLastError();
