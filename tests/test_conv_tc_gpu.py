@@ -1,7 +1,8 @@
 """GPU parity of the tensor-core conv1d path (csrc/conv_tc.cu; SURVEY 8f NEXT #2,
 the Conclusion's "small matrix multiplication"): every
-33 <= k <= 64 at stride 1 runs a Toeplitz matrix product on tcgen05 (3xTF32,
-fp32 accumulation in TMEM).  Checked against the oracle within the BASELINE.json
+33 <= k <= 64 at stride 1 runs a Toeplitz matrix product on tcgen05 (TF32 xh*fh
+plus one bf16 correction MMA per K-step, fp32 accumulation in TMEM; 3xTF32 with
+SS_CONV_TC_MIXED=0).  Checked against the oracle within the BASELINE.json
 bound |y - y_ref| <= 1e-5 * sum|x f| + 1e-6, over batch rows, misaligned x / y,
 ragged tails (the last CTA's direct-FMA tail) and padded outputs; integer
 inputs (P8) stay bit-exact; a subprocess forces the path onto small k."""
