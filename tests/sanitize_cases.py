@@ -1,6 +1,6 @@
 """Small cases through every kernel family, checked against the oracle; meant to
 run under compute-sanitizer (one --tool per invocation):
-    compute-sanitizer --tool memcheck python tools/sanitize_cases.py
+    compute-sanitizer --tool memcheck python tests/sanitize_cases.py
 Exits non-zero on a parity failure."""
 import os
 import sys

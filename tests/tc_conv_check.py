@@ -2,7 +2,8 @@
 the oracle over shapes / alignments, forced onto the TC path with
 SS_CONV_TC_MIN_K=1, then per-NC timing of BASELINE config 3 (64 x 2^20,
 k in {31, 48, 63}) against the FFMA2 tile kernel.  Usage (GPU box):
-    SS_CONV_TC_MIN_K=1 SS_CONV_TC_NC=64 python tools/tc_conv_check.py [parity|time]"""
+    SS_CONV_TC_MIN_K=1 python tests/tc_conv_check.py [parity|time|trace]
+(test infrastructure: imports oracle/; tests/test_conv_tc_gpu.py runs the parity mode)"""
 import os
 import sys
 

@@ -117,11 +117,12 @@ def test_tc_conv_deterministic(ss):
     np.testing.assert_array_equal(a, b)
 
 
-def test_tc_conv_forced_small_k():
+@pytest.mark.parametrize("mixed", ["1", "0"])
+def test_tc_conv_forced_small_k(mixed):
     # SS_CONV_TC_MIN_K=1 routes every k <= 64 through the tensor cores (fresh process:
-    # the threshold is read once)
-    env = dict(os.environ, SS_CONV_TC_MIN_K="1")
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "tc_conv_check.py"), "parity"], env=env,
+    # the threshold is read once); SS_CONV_TC_MIXED=0 checks the 3xTF32 mode as well
+    env = dict(os.environ, SS_CONV_TC_MIN_K="1", SS_CONV_TC_MIXED=mixed)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "tc_conv_check.py"), "parity"], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "parity ok" in r.stdout
