@@ -16,7 +16,9 @@ __global__ void probe(float* out, int iters, long long* cyc) {
     for (int j = 0; j < 16; ++j)
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        if (MODE == 0) acc[i] = __ffma2_rn(a[(i + j) & 15], b[j], acc[i]);
+        if (MODE == 3) { acc[i].x = __fmaf_rn(a[(i + j) & 15].x, kc[j].x, acc[i].x); acc[i].y = __fmaf_rn(a[(i + j) & 15].y, kc[j].x, acc[i].y); }
+        else if (MODE == 4) { acc[i].x = __fmaf_rn(a[(i + j) & 15].x, b[j].x, acc[i].x); acc[i].y = __fmaf_rn(a[(i + j) & 15].y, b[j].y, acc[i].y); }
+        else if (MODE == 0) acc[i] = __ffma2_rn(a[(i + j) & 15], b[j], acc[i]);
         else if (MODE == 1) acc[i] = __ffma2_rn(a[(i + j) & 15], make_float2(s + j, s + j), acc[i]);
         else acc[i] = __ffma2_rn(a[(i + j) & 15], kc[j], acc[i]);
       }
@@ -31,16 +33,17 @@ int main() {
   float* out; long long* cyc; cudaMalloc(&out, 148 * 1024 * 4 * 4); cudaMalloc(&cyc, 8);
   float2 h[64]; for (int i = 0; i < 64; ++i) h[i] = make_float2(0.1f * i, 0.2f); cudaMemcpyToSymbol(kc, h, sizeof h);
   const int iters = 2000;
-  for (int mode = 0; mode < 3; ++mode)
-    for (int threads : {128, 256, 512, 1024}) {
-      auto k = mode == 0 ? probe<0> : mode == 1 ? probe<1> : probe<2>;
+  for (int mode = 0; mode < 5; ++mode)
+    for (int threads : {256, 512}) {
+      auto k = mode == 0 ? probe<0> : mode == 1 ? probe<1> : mode == 2 ? probe<2> : mode == 3 ? probe<3> : probe<4>;
       k<<<148, threads>>>(out, 10, cyc);
       cudaDeviceSynchronize();
       k<<<148, threads>>>(out, iters, cyc);
       cudaDeviceSynchronize();
       long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
       double fma = 2.0 * 256 * iters * threads;  // per SM (one CTA per SM)
-      printf("mode %d threads %4d: %.1f FMA/clk/SM\n", mode, threads, fma / c);
+      const char* names[] = {"FFMA2 3 reg pairs", "FFMA2 pair x scalar", "FFMA2 pair x c-bank pair", "FFMA scalar x c-bank", "FFMA 3 regs"};
+      printf("%-26s threads %4d: %.1f FMA/clk/SM\n", names[mode], threads, fma / c);
     }
   return 0;
 }
