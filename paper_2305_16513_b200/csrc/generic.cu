@@ -54,13 +54,28 @@ __global__ void __launch_bounds__(kGenThreads) pool_generic_kernel(const __grid_
 // an unchecked loop when all of their windows lie inside the row.  Skip mode
 // (skip_lo < skip_hi): only outputs outside [skip_lo, skip_hi) -- the edges
 // around an interior the tile kernel computed -- one per thread.
+// Window taps are loaded in unrolled groups of 8 before they are combined, so a
+// thread has 8 loads in flight instead of one (the edge launches are latency
+// bound: ~12 us per launch with a serial load -> combine chain); the combine
+// order (increasing j, skipped taps contribute nothing) is unchanged.
+constexpr int kTapGroup = 8;
+
 template <class Op>
 __device__ __forceinline__ typename Op::T window_checked(const typename Op::T* __restrict__ xr,
                                                          int64_t t0, const GenericParams& p) {
   typename Op::T acc = Op::identity();
-  for (int j = 0; j < (int)p.w; ++j) {
-    const int64_t t = t0 + (int64_t)j * p.dilation;
-    if (t >= 0 && t < p.N) acc = Op::combine(acc, __ldg(xr + t));
+  for (int j0 = 0; j0 < (int)p.w; j0 += kTapGroup) {
+    typename Op::T v[kTapGroup];
+    bool ok[kTapGroup];
+#pragma unroll
+    for (int u = 0; u < kTapGroup; ++u) {
+      const int64_t t = t0 + (int64_t)(j0 + u) * p.dilation;
+      ok[u] = j0 + u < (int)p.w && t >= 0 && t < p.N;
+      v[u] = ok[u] ? __ldg(xr + t) : Op::identity();
+    }
+#pragma unroll
+    for (int u = 0; u < kTapGroup; ++u)
+      if (ok[u]) acc = Op::combine(acc, v[u]);
   }
   return acc;
 }
@@ -150,13 +165,21 @@ __global__ void __launch_bounds__(kGenThreads) conv_generic_kernel(const __grid_
 __device__ __forceinline__ float conv_checked(const float* __restrict__ xr, int64_t t0,
                                               const GenericParams& p) {
   float s0 = 0.0f, s1 = 0.0f;  // same association as conv_generic_kernel / ConvKind
-  for (int j = 0; j < (int)p.w; j += 2) {
-    const int64_t t = t0 + (int64_t)j * p.dilation;
-    if (t >= 0 && t < p.N) s0 = __fmaf_rn(p.taps[j], __ldg(xr + t), s0);
-  }
-  for (int j = 1; j < (int)p.w; j += 2) {
-    const int64_t t = t0 + (int64_t)j * p.dilation;
-    if (t >= 0 && t < p.N) s1 = __fmaf_rn(p.taps[j], __ldg(xr + t), s1);
+  for (int j0 = 0; j0 < (int)p.w; j0 += kTapGroup) {
+    float v[kTapGroup];
+    bool ok[kTapGroup];
+#pragma unroll
+    for (int u = 0; u < kTapGroup; ++u) {
+      const int64_t t = t0 + (int64_t)(j0 + u) * p.dilation;
+      ok[u] = j0 + u < (int)p.w && t >= 0 && t < p.N;
+      v[u] = ok[u] ? __ldg(xr + t) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < kTapGroup; u += 2)  // even taps (j0 is even)
+      if (ok[u]) s0 = __fmaf_rn(p.taps[j0 + u], v[u], s0);
+#pragma unroll
+    for (int u = 1; u < kTapGroup; u += 2)
+      if (ok[u]) s1 = __fmaf_rn(p.taps[j0 + u], v[u], s1);
   }
   return __fadd_rn(s0, s1);
 }
@@ -244,6 +267,14 @@ static dim3 grid_1d(const GenericParams& p, int sms) {
   return dim3((unsigned)(gx < 1 ? 1 : gx), (unsigned)gy, 1);
 }
 
+// skip mode (edges around a computed interior): one thread per edge output of a row
+static dim3 edge_grid(const GenericParams& p) {
+  const int64_t n_work = p.skip_lo + (p.L - p.skip_hi);
+  const int64_t gx = (n_work + kGenThreads - 1) / kGenThreads;
+  const int64_t gy = p.batch < 65535 ? p.batch : 65535;
+  return dim3((unsigned)(gx < 1 ? 1 : (gx > 4096 ? 4096 : gx)), (unsigned)(gy < 1 ? 1 : gy), 1);
+}
+
 static bool is_ex(const GenericParams& p) {
   return p.dilation != 1 || p.pad_left != 0 || p.skip_lo < p.skip_hi ||
          (p.L - 1) * p.stride + p.w > p.N;  // right padding
@@ -253,7 +284,7 @@ cudaError_t launch_pool_generic(const GenericParams& p, int op, int dtype, cudaS
                                 int grid) {
   const dim3 g = grid_1d(p, grid / 8 > 0 ? grid / 8 : 148);
   if (is_ex(p)) {
-    const dim3 ge = p.skip_lo < p.skip_hi ? dim3(g.x * kGenOuts, g.y, 1) : g;
+    const dim3 ge = p.skip_lo < p.skip_hi ? edge_grid(p) : g;
     if (op == kOpSum && dtype == 1) pool_generic_ex_kernel<OpSumI32><<<ge, kGenThreads, 0, stream>>>(p);
     else if (op == kOpSum && dtype == 0) pool_generic_ex_kernel<OpSumF32><<<ge, kGenThreads, 0, stream>>>(p);
     else if (op == kOpMax && dtype == 1) pool_generic_ex_kernel<OpMaxI32><<<ge, kGenThreads, 0, stream>>>(p);
@@ -273,7 +304,7 @@ cudaError_t launch_pool_generic(const GenericParams& p, int op, int dtype, cudaS
 cudaError_t launch_conv_generic(const GenericParams& p, cudaStream_t stream, int grid) {
   const dim3 g = grid_1d(p, grid / 8 > 0 ? grid / 8 : 148);
   if (is_ex(p))
-    conv_generic_ex_kernel<<<p.skip_lo < p.skip_hi ? dim3(g.x * kGenOuts, g.y, 1) : g, kGenThreads, 0, stream>>>(p);
+    conv_generic_ex_kernel<<<p.skip_lo < p.skip_hi ? edge_grid(p) : g, kGenThreads, 0, stream>>>(p);
   else conv_generic_kernel<<<g, kGenThreads, 0, stream>>>(p);
   note_launch();
   return cudaGetLastError();
