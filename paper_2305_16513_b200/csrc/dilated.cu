@@ -65,18 +65,28 @@ __global__ void __launch_bounds__(kDilThreads) dilated_tile_kernel(const __grid_
   const int d = (int)p.d;
   const int tbc = kDilThreads / d;                 // threads (run blocks) per phase
   const int64_t T = (int64_t)kDilR * d * tbc;      // outputs per tile
-  const int span = (int)(T + (p.w - 1) * d);       // inputs per tile
+  const int span = (int)(T + (KB - 1) * d);        // inputs staged per tile (every register read valid)
   const int64_t tiles_per_row = (p.L_int + T - 1) / T;
   const int64_t ntiles = p.batch * tiles_per_row;
   const float* __restrict__ x = static_cast<const float*>(p.x);
   float* __restrict__ y = static_cast<float*>(p.y);
   const int rho = threadIdx.x % d, tb = threadIdx.x / d;
   const bool active = tb < tbc;
+  // (row, tile-in-row) cursors advanced by gridDim.x without divisions: ic one tile ahead (issue), cc (compute)
+  const int64_t step_b = gridDim.x / tiles_per_row, step_t = gridDim.x - step_b * tiles_per_row;
+  int64_t ib = blockIdx.x / tiles_per_row, it = blockIdx.x - ib * tiles_per_row;
+  int64_t cb = ib, ct = it;
+  auto advance = [&](int64_t& b, int64_t& t) {
+    b += step_b;
+    t += step_t;
+    if (t >= tiles_per_row) { t -= tiles_per_row; ++b; }
+  };
   // two stages: tile it+1 streams in while tile it computes
   auto issue = [&](int64_t tile, int st) {
     if (tile < ntiles) {
-      const int64_t b = tile / tiles_per_row;
-      const int64_t i0 = (tile - b * tiles_per_row) * T;
+      const int64_t b = ib;
+      const int64_t i0 = it * T;
+      advance(ib, it);
       const float* __restrict__ xr = x + b * p.N + i0;
       const int64_t lim = p.N - i0;
       float* s = dil_smem + st * p.stage_floats;
@@ -101,18 +111,19 @@ __global__ void __launch_bounds__(kDilThreads) dilated_tile_kernel(const __grid_
     cp_async_wait<1>();
     __syncthreads();
     float* os = dil_smem + 2 * p.stage_floats;  // output tile staging (coalesced stores)
-    const int64_t bq = tile / tiles_per_row;
-    const int64_t iq0 = (tile - bq * tiles_per_row) * T;
+    const int64_t bq = cb;
+    const int64_t iq0 = ct * T;
+    advance(cb, ct);
     const int64_t nout = p.L_int - iq0 < T ? p.L_int - iq0 : T;
     if (active) {
       const float* s = dil_smem + st * p.stage_floats;
       const int base = rho + d * kDilR * tb;  // first input of this thread's run
       float xr[kDilR + KB - 1];
+      // reads stay below T + (KB - 1) d = span: staged x (or zero past the row end); taps
+      // past w are zero (conv) or not combined (sum / max)
+      const float* sb = s + base;
 #pragma unroll
-      for (int q = 0; q < kDilR + KB - 1; ++q) {
-        const int e = base + q * d;
-        xr[q] = e < span ? s[e] : 0.0f;
-      }
+      for (int q = 0; q < kDilR + KB - 1; ++q) xr[q] = sb[q * d];
       float out[kDilR];
       eval_run<Op, KB>(xr, p, out);
 #pragma unroll
@@ -121,7 +132,12 @@ __global__ void __launch_bounds__(kDilThreads) dilated_tile_kernel(const __grid_
     __syncthreads();  // stage st is refilled by the next iteration's issue; os complete
     {
       float* __restrict__ yr = y + bq * p.y_pitch + p.y_off + iq0;
-      for (int o = threadIdx.x; o < nout; o += kDilThreads) yr[o] = os[o];
+      if ((reinterpret_cast<uintptr_t>(yr) & 15) == 0 && nout == T && (T & 3) == 0) {
+        for (int o = 4 * threadIdx.x; o < nout; o += 4 * kDilThreads)
+          *reinterpret_cast<float4*>(yr + o) = *reinterpret_cast<const float4*>(os + o);
+      } else {
+        for (int o = threadIdx.x; o < nout; o += kDilThreads) yr[o] = os[o];
+      }
     }
     st ^= 1;
   }
@@ -133,7 +149,7 @@ static cudaError_t launch_op(DilatedParams& p, cudaStream_t stream, int sms) {
   const int kb = p.w <= 8 ? 8 : (p.w <= 16 ? 16 : 32);
   const int tbc = kDilThreads / (int)p.d;
   const int64_t T = (int64_t)kDilR * p.d * tbc;
-  p.stage_floats = (int)((T + (p.w - 1) * p.d + 3) & ~int64_t(3));
+  p.stage_floats = (int)((T + (kb - 1) * p.d + 3) & ~int64_t(3));
   const size_t smem = (2 * (size_t)p.stage_floats + (size_t)T) * sizeof(float);
   if (smem > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
   const int64_t tiles = p.batch * ((p.L_int + T - 1) / T);
