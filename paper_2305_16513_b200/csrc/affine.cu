@@ -157,63 +157,23 @@ __device__ __forceinline__ void affine_small_body(const Gp* g, Gp* y) {
   }
 }
 
-// Warp-cooperative inclusive prefix and suffix scans of the segment
-// B[s0, s0+len) into pre[] / suf[], in (+) order.  Lanes own contiguous chunks;
-// chunk totals are combined with an order-preserving shuffle scan.
-__device__ __forceinline__ Gp shfl_gp_up(Gp a, int d) {
-  return Gp{__shfl_up_sync(0xffffffffu, a.u, d), __shfl_up_sync(0xffffffffu, a.v, d)};
-}
-__device__ __forceinline__ Gp shfl_gp_down(Gp a, int d) {
-  return Gp{__shfl_down_sync(0xffffffffu, a.u, d), __shfl_down_sync(0xffffffffu, a.v, d)};
-}
-
-__device__ void warp_segment_scans(const Gp* B, Gp* pre, Gp* suf, int s0, int len, int lane) {
-  const int chunk = (len + 31) / 32;
-  const int c0 = s0 + min(lane * chunk, len), c1 = s0 + min((lane + 1) * chunk, len);
-  // prefix: local inclusive scan, then the exclusive carry from lower lanes
-  Gp acc = gid();
-  for (int k = c0; k < c1; ++k) {
-    acc = gcomb(acc, B[k]);
-    pre[k] = acc;
-  }
-  Gp inc = acc;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const Gp o = shfl_gp_up(inc, d);
-    if (lane >= d) inc = gcomb(o, inc);
-  }
-  Gp carry = shfl_gp_up(inc, 1);
-  if (lane > 0)
-    for (int k = c0; k < c1; ++k) pre[k] = gcomb(carry, pre[k]);
-  // suffix: local scan from the right, then the carry from higher lanes
-  acc = gid();
-  for (int k = c1 - 1; k >= c0; --k) {
-    acc = gcomb(B[k], acc);
-    suf[k] = acc;
-  }
-  inc = acc;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const Gp o = shfl_gp_down(inc, d);
-    if (lane + d < 32) inc = gcomb(inc, o);
-  }
-  carry = shfl_gp_down(inc, 1);
-  if (lane < 31)
-    for (int k = c0; k < c1; ++k) suf[k] = gcomb(suf[k], carry);
-}
-
 // w >= 9, stride 1; RHO = (w-1) % 8.  Computes the 8 outputs of thread t of
 // the tile into y (all threads take part in the block-total scans).
 template <int RHO, class Src>
 __device__ __forceinline__ void affine_pivot_body(const AffineParams& p, const Src& src, Gp* Bt, Gp* y) {
   Gp* Pre = Bt + p.nB;
   Gp* Suf = Pre + p.nB;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int t = threadIdx.x;
   const int q = p.q, m = p.q - 1;
 
   // (1) own block + totals of blocks 1 .. nB (tile-local block index)
   Gp own[8];
   src.load8(8 * t, own);
+  // M_t = blocks t+1 .. t+m = Bt[t] (+) ... (+) Bt[t+m-1], by doubling: level k holds the
+  // folds of 2^k consecutive block totals (built from level k-1 by all threads, ping-pong
+  // between Pre and Suf); the set bits of m, smallest first, select the pieces of M_t from
+  // left to right, so the (+) order is kept.  ~log2(m) barriers, no serial scans.
+  Gp M = gid();
   if (m > 0) {
     for (int k = t; k < p.nB; k += kAffThreads) {
       Gp g[8];
@@ -224,33 +184,21 @@ __device__ __forceinline__ void affine_pivot_body(const AffineParams& p, const S
       Bt[k] = a;
     }
     __syncthreads();
-    // (2) segmented prefix / suffix scans of the block totals, segments of m
-    const int nseg = (p.nB + m - 1) / m;
-    if (m <= 64) {
-      for (int sg = t; sg < nseg; sg += kAffThreads) {
-        const int s0 = sg * m, s1 = min(s0 + m, p.nB);
-        Gp a = gid();
-        for (int k = s0; k < s1; ++k) {
-          a = gcomb(a, Bt[k]);
-          Pre[k] = a;
-        }
-        a = gid();
-        for (int k = s1 - 1; k >= s0; --k) {
-          a = gcomb(Bt[k], a);
-          Suf[k] = a;
-        }
+    const Gp* cur = Bt;
+    int off = 0;
+    for (int span = 1, lvl = 0;; span <<= 1, ++lvl) {
+      if (m & span) {
+        M = gcomb(M, cur[t + off]);
+        off += span;
       }
-    } else {
-      for (int sg = warp; sg < nseg; sg += kAffThreads / 32) {
-        const int s0 = sg * m;
-        warp_segment_scans(Bt, Pre, Suf, s0, min(m, p.nB - s0), lane);
-      }
+      if (2 * span > m) break;
+      Gp* nxt = (lvl & 1) ? Suf : Pre;
+      const int nn = p.nB - 2 * span + 1;  // entries i with i + 2 span <= nB
+      for (int i = t; i < nn; i += kAffThreads) nxt[i] = gcomb(cur[i], cur[i + span]);
+      __syncthreads();
+      cur = nxt;
     }
-    __syncthreads();
   }
-  // M_t = blocks t+1 .. t+m = Bt[t .. t+m-1]  (second-level pivot)
-  Gp M = gid();
-  if (m > 0) M = (t % m == 0) ? Suf[t] : gcomb(Suf[t], Pre[t + m - 1]);
   // S_t[r]: suffixes of the own block
   Gp S[8];
   S[7] = own[7];
