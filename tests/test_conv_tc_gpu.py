@@ -75,6 +75,27 @@ def test_tc_conv_parity(ss, B, N, k, xoff, yoff):
     check(y, ref, mag, f"B={B} N={N} k={k}")
 
 
+def test_tc_conv_coherent_worst_case(ss):
+    # Inputs whose truncated-away TF32 bits are all ones (the largest xl, fl: ~2^-10 of the
+    # value) and all of one sign, so the bf16 rounding errors of the correction terms cannot
+    # cancel across the window: the per-product bound ~2^-18 |x f| (tensor-core
+    # conv) adds up coherently and must still stay inside 1e-5 sum|x f| + 1e-6.
+    rng = np.random.default_rng(7)
+    B, N, k = 2, 40000, 63
+    def worst(n, scale):
+        e = rng.integers(-3, 4, size=n)  # spread the exponents a little
+        mant = (1 << 23) | (0x1FFF + (rng.integers(0, 1 << 10, size=n) << 13))  # low 13 bits all ones
+        return (mant.astype(np.float64) * 2.0 ** (e - 23) * scale).astype(np.float32)
+    x = worst(B * N, 1.0).reshape(B, N)
+    f = worst(k, 0.1)
+    y, used = run(ss, x, f)
+    assert used == 1, "tensor-core path not taken"
+    ref, mag = oracle.conv1d(x, f)
+    ratio = check(y, ref, mag, "coherent worst case")
+    print(f"coherent worst case: max err/bound {ratio:.3f}")
+    assert ratio < 0.6, ratio  # measured margin; the analytical per-product bound gives ~0.38
+
+
 def test_tc_conv_padded(ss):
     x = synth.normal(5, 3 * 20000).reshape(3, 20000)
     f = synth.normal(4, 63, sigma=synth.cfg_sigma_filter(63))
