@@ -65,12 +65,14 @@ def lib() -> ctypes.CDLL:
             L.oracle_pool2d_f32.restype = ctypes.c_int
             L.oracle_out_len_ex.argtypes = [i64] * 6
             L.oracle_out_len_ex.restype = i64
-            for name in ("oracle_pool_sum_ex_i32", "oracle_pool_max_ex_i32", "oracle_pool_max_ex_f32"):
-                getattr(L, name).argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, vp]
+            ci = ctypes.c_int
+            for name in ("oracle_pool_sum_ex_i32", "oracle_pool_max_ex_i32", "oracle_pool_max_ex_f32",
+                         "oracle_pool_min_ex_i32", "oracle_pool_min_ex_f32"):
+                getattr(L, name).argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, ci, vp]
                 getattr(L, name).restype = ctypes.c_int
-            L.oracle_pool_sum_ex_f32.argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, vp, vp]
+            L.oracle_pool_sum_ex_f32.argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, ci, vp, vp]
             L.oracle_pool_sum_ex_f32.restype = ctypes.c_int
-            L.oracle_conv1d_ex_f32.argtypes = [vp, i64, i64, vp, i64, i64, i64, i64, i64, vp, vp]
+            L.oracle_conv1d_ex_f32.argtypes = [vp, i64, i64, vp, i64, i64, i64, i64, i64, ci, vp, vp]
             L.oracle_conv1d_ex_f32.restype = ctypes.c_int
             L.oracle_affine_window.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp, vp]
             L.oracle_affine_window.restype = ctypes.c_int
@@ -187,38 +189,59 @@ def _ex_len(N, w, s, d, pl, pr):
     return L
 
 
-def pool_sum_ex(x: np.ndarray, w: int, s: int = 1, d: int = 1, pl: int = 0, pr: int = 0):
-    """Zero-padded, dilated sliding sum (NEXT #1).  int32 -> int64; float32 -> (double, absmag)."""
+PAD_MODES = {"zeros": 0, "reflect": 1, "circular": 2, "replicate": 3}
+
+
+def _mode(mode) -> int:
+    return PAD_MODES[mode] if isinstance(mode, str) else int(mode)
+
+
+def pool_sum_ex(x: np.ndarray, w: int, s: int = 1, d: int = 1, pl: int = 0, pr: int = 0, mode="zeros"):
+    """Padded, dilated sliding sum (NEXT #1).  int32 -> int64; float32 -> (double, absmag)."""
     x, N, B = _rows(x)
     L = _ex_len(N, w, s, d, pl, pr)
     if x.dtype == np.int32:
         y = np.empty((B, L), np.int64)
-        _check(lib().oracle_pool_sum_ex_i32(_p(x), N, B, w, s, d, pl, pr, _p(y)))
+        _check(lib().oracle_pool_sum_ex_i32(_p(x), N, B, w, s, d, pl, pr, _mode(mode), _p(y)))
         return y if x.ndim == 2 else y[0]
     y = np.empty((B, L), np.float64)
     m = np.empty((B, L), np.float64)
-    _check(lib().oracle_pool_sum_ex_f32(_p(x), N, B, w, s, d, pl, pr, _p(y), _p(m)))
+    _check(lib().oracle_pool_sum_ex_f32(_p(x), N, B, w, s, d, pl, pr, _mode(mode), _p(y), _p(m)))
     return (y, m) if x.ndim == 2 else (y[0], m[0])
 
 
-def pool_max_ex(x: np.ndarray, w: int, s: int = 1, d: int = 1, pl: int = 0, pr: int = 0):
+def _extremum_ex(name, x, w, s, d, pl, pr, mode):
     x, N, B = _rows(x)
     L = _ex_len(N, w, s, d, pl, pr)
     y = np.empty((B, L), x.dtype)
-    fn = {np.dtype(np.int32): lib().oracle_pool_max_ex_i32,
-          np.dtype(np.float32): lib().oracle_pool_max_ex_f32}[x.dtype]
-    _check(fn(_p(x), N, B, w, s, d, pl, pr, _p(y)))
+    fn = {np.dtype(np.int32): getattr(lib(), f"oracle_pool_{name}_ex_i32"),
+          np.dtype(np.float32): getattr(lib(), f"oracle_pool_{name}_ex_f32")}[x.dtype]
+    _check(fn(_p(x), N, B, w, s, d, pl, pr, _mode(mode), _p(y)))
     return y if x.ndim == 2 else y[0]
 
 
-def conv1d_ex(x: np.ndarray, f: np.ndarray, s: int = 1, d: int = 1, pl: int = 0, pr: int = 0):
+def pool_max_ex(x: np.ndarray, w: int, s: int = 1, d: int = 1, pl: int = 0, pr: int = 0, mode="zeros"):
+    return _extremum_ex("max", x, w, s, d, pl, pr, mode)
+
+
+def pool_min_ex(x: np.ndarray, w: int, s: int = 1, d: int = 1, pl: int = 0, pr: int = 0, mode="zeros"):
+    """Sliding min (Sec. 2.3's other extremum), same dtype as x."""
+    return _extremum_ex("min", x, w, s, d, pl, pr, mode)
+
+
+def pool_min(x: np.ndarray, w: int, s: int = 1) -> np.ndarray:
+    """Valid-padding sliding min."""
+    return pool_min_ex(x, w, s)
+
+
+def conv1d_ex(x: np.ndarray, f: np.ndarray, s: int = 1, d: int = 1, pl: int = 0, pr: int = 0, mode="zeros"):
     x, N, B = _rows(x)
     f = np.ascontiguousarray(f, np.float32)
     k = f.shape[0]
     L = _ex_len(N, k, s, d, pl, pr)
     y = np.empty((B, L), np.float64)
     m = np.empty((B, L), np.float64)
-    _check(lib().oracle_conv1d_ex_f32(_p(x), N, B, _p(f), k, s, d, pl, pr, _p(y), _p(m)))
+    _check(lib().oracle_conv1d_ex_f32(_p(x), N, B, _p(f), k, s, d, pl, pr, _mode(mode), _p(y), _p(m)))
     return (y, m) if x.ndim == 2 else (y[0], m[0])
 
 

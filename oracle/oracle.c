@@ -156,7 +156,7 @@ int oracle_pool2d_f32(const float* x, int64_t planes, int64_t H, int64_t W,
   return 0;
 }
 
-/* ---- window spec with dilation d and zero padding (pl, pr): see oracle.h ---- */
+/* ---- window spec with dilation d and padding (pl, pr, mode): see oracle.h ---- */
 int64_t oracle_out_len_ex(int64_t N, int64_t w, int64_t s, int64_t d, int64_t pl, int64_t pr) {
   if (N < 1 || w < 1 || s < 1 || d < 1 || pl < 0 || pr < 0) return -1;
   int64_t E = (w - 1) * d + 1, Np = N + pl + pr;
@@ -164,21 +164,38 @@ int64_t oracle_out_len_ex(int64_t N, int64_t w, int64_t s, int64_t d, int64_t pl
   return (Np - E) / s + 1;
 }
 
+/* x index of padded position t - pl =: u (u may be outside [0, N)), or -1 for
+ * zero padding (the identity).  Modes: 0 zeros, 1 reflect (mirror about the end
+ * elements, which are not repeated), 2 circular (periodic), 3 replicate. */
+static int64_t pad_source(int64_t u, int64_t N, int mode) {
+  if (u >= 0 && u < N) return u;
+  switch (mode) {
+    case 1: return u < 0 ? -u : 2 * (N - 1) - u;
+    case 2: return ((u % N) + N) % N;
+    case 3: return u < 0 ? 0 : N - 1;
+    default: return -1;
+  }
+}
+
 static int bad_ex(const void* x, const void* y, int64_t N, int64_t batch, int64_t w, int64_t s,
-                  int64_t d, int64_t pl, int64_t pr) {
-  return x == NULL || y == NULL || batch < 1 || oracle_out_len_ex(N, w, s, d, pl, pr) < 0;
+                  int64_t d, int64_t pl, int64_t pr, int mode) {
+  if (x == NULL || y == NULL || batch < 1 || oracle_out_len_ex(N, w, s, d, pl, pr) < 0) return 1;
+  if (mode < 0 || mode > 3) return 1;
+  if (mode == 1 && (pl > N - 1 || pr > N - 1)) return 1; /* one reflection only */
+  if (mode == 2 && (pl > N || pr > N)) return 1;         /* one period only */
+  return 0;
 }
 
 int oracle_pool_sum_ex_i32(const int32_t* x, int64_t N, int64_t batch, int64_t w, int64_t s,
-                           int64_t d, int64_t pl, int64_t pr, int64_t* y) {
-  if (bad_ex(x, y, N, batch, w, s, d, pl, pr)) return -1;
+                           int64_t d, int64_t pl, int64_t pr, int mode, int64_t* y) {
+  if (bad_ex(x, y, N, batch, w, s, d, pl, pr, mode)) return -1;
   int64_t L = oracle_out_len_ex(N, w, s, d, pl, pr);
   for (int64_t b = 0; b < batch; ++b)
     for (int64_t i = 0; i < L; ++i) {
       int64_t acc = 0;
       for (int64_t j = 0; j < w; ++j) {
-        int64_t t = i * s + j * d - pl;
-        if (t >= 0 && t < N) acc += (int64_t)x[b * N + t];
+        int64_t t = pad_source(i * s + j * d - pl, N, mode);
+        if (t >= 0) acc += (int64_t)x[b * N + t];
       }
       y[b * L + i] = acc;
     }
@@ -186,15 +203,15 @@ int oracle_pool_sum_ex_i32(const int32_t* x, int64_t N, int64_t batch, int64_t w
 }
 
 int oracle_pool_sum_ex_f32(const float* x, int64_t N, int64_t batch, int64_t w, int64_t s,
-                           int64_t d, int64_t pl, int64_t pr, double* y, double* absmag) {
-  if (bad_ex(x, y, N, batch, w, s, d, pl, pr)) return -1;
+                           int64_t d, int64_t pl, int64_t pr, int mode, double* y, double* absmag) {
+  if (bad_ex(x, y, N, batch, w, s, d, pl, pr, mode)) return -1;
   int64_t L = oracle_out_len_ex(N, w, s, d, pl, pr);
   for (int64_t b = 0; b < batch; ++b)
     for (int64_t i = 0; i < L; ++i) {
       double acc = 0.0, mag = 0.0;
       for (int64_t j = 0; j < w; ++j) {
-        int64_t t = i * s + j * d - pl;
-        if (t >= 0 && t < N) {
+        int64_t t = pad_source(i * s + j * d - pl, N, mode);
+        if (t >= 0) {
           acc += (double)x[b * N + t];
           mag += fabs((double)x[b * N + t]);
         }
@@ -205,18 +222,20 @@ int oracle_pool_sum_ex_f32(const float* x, int64_t N, int64_t batch, int64_t w, 
   return 0;
 }
 
-int oracle_pool_max_ex_i32(const int32_t* x, int64_t N, int64_t batch, int64_t w, int64_t s,
-                           int64_t d, int64_t pl, int64_t pr, int32_t* y) {
-  if (bad_ex(x, y, N, batch, w, s, d, pl, pr)) return -1;
+/* max (sign = +1) or min (sign = -1) of each window; padding in zeros mode is
+ * skipped (the identity: -inf / INT32_MIN for max, +inf / INT32_MAX for min) */
+static int extremum_ex_i32(const int32_t* x, int64_t N, int64_t batch, int64_t w, int64_t s, int64_t d,
+                           int64_t pl, int64_t pr, int mode, int sign, int32_t* y) {
+  if (bad_ex(x, y, N, batch, w, s, d, pl, pr, mode)) return -1;
   int64_t L = oracle_out_len_ex(N, w, s, d, pl, pr);
   for (int64_t b = 0; b < batch; ++b)
     for (int64_t i = 0; i < L; ++i) {
-      int32_t m = INT32_MIN;
+      int32_t m = sign > 0 ? INT32_MIN : INT32_MAX;
       for (int64_t j = 0; j < w; ++j) {
-        int64_t t = i * s + j * d - pl;
-        if (t >= 0 && t < N) {
+        int64_t t = pad_source(i * s + j * d - pl, N, mode);
+        if (t >= 0) {
           int32_t v = x[b * N + t];
-          m = v > m ? v : m;
+          if (sign > 0 ? v > m : v < m) m = v;
         }
       }
       y[b * L + i] = m;
@@ -224,35 +243,52 @@ int oracle_pool_max_ex_i32(const int32_t* x, int64_t N, int64_t batch, int64_t w
   return 0;
 }
 
-int oracle_pool_max_ex_f32(const float* x, int64_t N, int64_t batch, int64_t w, int64_t s,
-                           int64_t d, int64_t pl, int64_t pr, float* y) {
-  if (bad_ex(x, y, N, batch, w, s, d, pl, pr)) return -1;
+static int extremum_ex_f32(const float* x, int64_t N, int64_t batch, int64_t w, int64_t s, int64_t d,
+                           int64_t pl, int64_t pr, int mode, int sign, float* y) {
+  if (bad_ex(x, y, N, batch, w, s, d, pl, pr, mode)) return -1;
   int64_t L = oracle_out_len_ex(N, w, s, d, pl, pr);
   for (int64_t b = 0; b < batch; ++b)
     for (int64_t i = 0; i < L; ++i) {
-      float m = -INFINITY;
+      float m = sign > 0 ? -INFINITY : INFINITY;
       for (int64_t j = 0; j < w; ++j) {
-        int64_t t = i * s + j * d - pl;
-        if (t >= 0 && t < N) {
+        int64_t t = pad_source(i * s + j * d - pl, N, mode);
+        if (t >= 0) {
           float v = x[b * N + t];
-          m = v > m ? v : m;
+          if (sign > 0 ? v > m : v < m) m = v;
         }
       }
       y[b * L + i] = m;
     }
   return 0;
+}
+
+int oracle_pool_max_ex_i32(const int32_t* x, int64_t N, int64_t batch, int64_t w, int64_t s,
+                           int64_t d, int64_t pl, int64_t pr, int mode, int32_t* y) {
+  return extremum_ex_i32(x, N, batch, w, s, d, pl, pr, mode, +1, y);
+}
+int oracle_pool_max_ex_f32(const float* x, int64_t N, int64_t batch, int64_t w, int64_t s,
+                           int64_t d, int64_t pl, int64_t pr, int mode, float* y) {
+  return extremum_ex_f32(x, N, batch, w, s, d, pl, pr, mode, +1, y);
+}
+int oracle_pool_min_ex_i32(const int32_t* x, int64_t N, int64_t batch, int64_t w, int64_t s,
+                           int64_t d, int64_t pl, int64_t pr, int mode, int32_t* y) {
+  return extremum_ex_i32(x, N, batch, w, s, d, pl, pr, mode, -1, y);
+}
+int oracle_pool_min_ex_f32(const float* x, int64_t N, int64_t batch, int64_t w, int64_t s,
+                           int64_t d, int64_t pl, int64_t pr, int mode, float* y) {
+  return extremum_ex_f32(x, N, batch, w, s, d, pl, pr, mode, -1, y);
 }
 
 int oracle_conv1d_ex_f32(const float* x, int64_t N, int64_t batch, const float* f, int64_t k,
-                         int64_t s, int64_t d, int64_t pl, int64_t pr, double* y, double* absmag) {
-  if (bad_ex(x, y, N, batch, k, s, d, pl, pr) || f == NULL) return -1;
+                         int64_t s, int64_t d, int64_t pl, int64_t pr, int mode, double* y, double* absmag) {
+  if (bad_ex(x, y, N, batch, k, s, d, pl, pr, mode) || f == NULL) return -1;
   int64_t L = oracle_out_len_ex(N, k, s, d, pl, pr);
   for (int64_t b = 0; b < batch; ++b)
     for (int64_t i = 0; i < L; ++i) {
       double acc = 0.0, mag = 0.0;
       for (int64_t j = 0; j < k; ++j) {
-        int64_t t = i * s + j * d - pl;
-        if (t >= 0 && t < N) {
+        int64_t t = pad_source(i * s + j * d - pl, N, mode);
+        if (t >= 0) {
           double p = (double)f[j] * (double)x[b * N + t];
           acc += p;
           mag += fabs(p);

@@ -66,24 +66,33 @@ int oracle_pool2d_f32(const float* x, int64_t planes, int64_t H, int64_t W,
                       int64_t kh, int64_t kw, int64_t sh, int64_t sw, int mode,
                       double* y, double* absmag);
 
-/* Window spec with dilation and zero padding (SPEC.md
- * l.263-268 WindowSpec, l.282 / l.332 pad semantics):
- *   xp[t] = x[t - pl] for 0 <= t - pl < N, else padding;
+/* Window spec with dilation and padding (SPEC.md l.263-268
+ * WindowSpec, l.282 / l.332 pad semantics; PAPER.md l.158 names "padding,
+ * mirroring, or periodicity" as the boundary conditions):
+ *   xp[t] = x[t - pl] for 0 <= t - pl < N, else padding by `mode`:
+ *     0 zeros (contributes 0 to sums and dot products, never wins a max or a
+ *       min: a window made only of padding gives the identity),
+ *     1 reflect (x[-u] = x[u], x[N-1+u] = x[N-1-u]; requires pl, pr <= N-1),
+ *     2 circular (x[u mod N]; requires pl, pr <= N),
+ *     3 replicate (the end element);
  *   output i covers xp[i*s + j*d], j < w;  extent E = (w-1)*d + 1;
  *   out_len = (N + pl + pr - E) / s + 1  (-1 if invalid or E > N + pl + pr).
- * Padding contributes 0 to sums and dot products and never wins a max (the
- * max of a window made only of padding is the identity: -inf / INT32_MIN). */
+ * Min is Sec. 2.3's other extremum ("min is associative"). */
 int64_t oracle_out_len_ex(int64_t N, int64_t w, int64_t s, int64_t d, int64_t pl, int64_t pr);
 int oracle_pool_sum_ex_i32(const int32_t* x, int64_t N, int64_t batch, int64_t w, int64_t s,
-                           int64_t d, int64_t pl, int64_t pr, int64_t* y);
+                           int64_t d, int64_t pl, int64_t pr, int mode, int64_t* y);
 int oracle_pool_sum_ex_f32(const float* x, int64_t N, int64_t batch, int64_t w, int64_t s,
-                           int64_t d, int64_t pl, int64_t pr, double* y, double* absmag);
+                           int64_t d, int64_t pl, int64_t pr, int mode, double* y, double* absmag);
 int oracle_pool_max_ex_i32(const int32_t* x, int64_t N, int64_t batch, int64_t w, int64_t s,
-                           int64_t d, int64_t pl, int64_t pr, int32_t* y);
+                           int64_t d, int64_t pl, int64_t pr, int mode, int32_t* y);
 int oracle_pool_max_ex_f32(const float* x, int64_t N, int64_t batch, int64_t w, int64_t s,
-                           int64_t d, int64_t pl, int64_t pr, float* y);
+                           int64_t d, int64_t pl, int64_t pr, int mode, float* y);
+int oracle_pool_min_ex_i32(const int32_t* x, int64_t N, int64_t batch, int64_t w, int64_t s,
+                           int64_t d, int64_t pl, int64_t pr, int mode, int32_t* y);
+int oracle_pool_min_ex_f32(const float* x, int64_t N, int64_t batch, int64_t w, int64_t s,
+                           int64_t d, int64_t pl, int64_t pr, int mode, float* y);
 int oracle_conv1d_ex_f32(const float* x, int64_t N, int64_t batch, const float* f, int64_t k,
-                         int64_t s, int64_t d, int64_t pl, int64_t pr, double* y, double* absmag);
+                         int64_t s, int64_t d, int64_t pl, int64_t pr, int mode, double* y, double* absmag);
 
 /* Sliding window of gamma pairs (Eq. 3 with the pair operator of Eq. 8; the
  * windowed linear recurrence s_t = u_t s_{t-1} + v_t):
