@@ -94,10 +94,10 @@ class Cell:
     """One kernel launch of the workload."""
 
     def __init__(self, cfg, name, op, *, w=None, f=None, kh=None, kw=None, sh=None, sw=None,
-                 mode=None, inp=None, inp2=None, stride=1, dilation=1, pads=(0, 0)):
+                 mode=None, inp=None, inp2=None, stride=1, dilation=1, pads=(0, 0), pad_mode="zeros"):
         self.cfg, self.name, self.op = cfg, name, op
         self.inp2 = inp2  # second input (affine: v), None otherwise
-        self.stride, self.dilation, self.pads = stride, dilation, pads
+        self.stride, self.dilation, self.pads, self.pad_mode = stride, dilation, pads, pad_mode
         self.w, self.f, self.kh, self.kw, self.sh, self.sw, self.mode = w, f, kh, kw, sh, sw, mode
         self.inp = inp  # key of the input tensor it reads
         self.n_out = 0
@@ -159,6 +159,11 @@ def cfg_cells(workload: str):
                               f=synth.normal(4, k, sigma=synth.cfg_sigma_filter(k)), inp="xw"))
         cells.append(Cell("winspec", "winspec_max_w3_p1", "max", w=3, pads=(1, 1), inp="xw"))
         cells.append(Cell("winspec", "winspec_sum_w8_d2", "sum", w=8, dilation=2, inp="xw"))
+        # padding modes ("mirroring, or periodicity") and the sliding min (l.136)
+        cells.append(Cell("winspec", "winspec_conv_k7_p3_reflect", "conv", w=7, pads=(3, 3), pad_mode="reflect",
+                          f=synth.normal(4, 7, sigma=synth.cfg_sigma_filter(7)), inp="xw"))
+        cells.append(Cell("winspec", "winspec_min_w16_p8_circular", "min", w=16, pads=(8, 7), pad_mode="circular",
+                          inp="xw"))
     if workload == "affine":  # sliding window of gamma pairs; not a BASELINE config
         inputs["xa_u"] = dict(rows=8, n=1 << 24, dtype="float32", dist="uab", seed=31,
                               kw=dict(lo=0.5, hi=1.0), shard="batch")
@@ -466,7 +471,7 @@ class Runner:
             N, B = x.shape[0], 1
         else:
             B, N = x.shape
-        win = (c.stride, c.dilation, c.pads[0], c.pads[1], code, s)
+        win = (c.stride, c.dilation, c.pads[0], c.pads[1], ss.PAD_MODES[c.pad_mode], code, s)
         if c.op == "affine":
             v = self.x[c.inp2]
             st = ss.ss_affine_window(x.data_ptr(), v.data_ptr(), y[0].data_ptr(), y[1].data_ptr(), N, B, c.w,
@@ -475,6 +480,8 @@ class Runner:
             st = ss.ss_conv1d_ex(x.data_ptr(), y.data_ptr(), N, B, c.f, c.w, *win)
         elif c.op == "sum":
             st = ss.ss_pool_sum_ex(x.data_ptr(), y.data_ptr(), N, B, c.w, *win)
+        elif c.op == "min":
+            st = ss.ss_pool_min_ex(x.data_ptr(), y.data_ptr(), N, B, c.w, *win)
         else:
             st = ss.ss_pool_max_ex(x.data_ptr(), y.data_ptr(), N, B, c.w, *win)
         ss.check(st)
@@ -891,6 +898,16 @@ def oracle_sample_plan(workload: str, frac: float):
             else:
                 fn = (lambda x=x, g=g, c=c: (oracle.pool_max_backward(x, g, c.w), x.size)[1])
             plan.append((c, fn))
+        elif c.cfg in ("stride", "winspec"):
+            rows, n = 1, max(4 * (c.w - 1) * c.dilation + 8, int(64 * (1 << 20) * frac))
+            x = synth.normal(3, rows * n).reshape(rows, n)
+            kw = dict(s=c.stride, d=c.dilation, pl=c.pads[0], pr=c.pads[1], mode=c.pad_mode)
+            L = oracle.out_len_ex(n, c.w, c.stride, c.dilation, c.pads[0], c.pads[1])
+            fn = {"sum": lambda x=x, c=c, kw=kw: oracle.pool_sum_ex(x, c.w, **kw),
+                  "max": lambda x=x, c=c, kw=kw: oracle.pool_max_ex(x, c.w, **kw),
+                  "min": lambda x=x, c=c, kw=kw: oracle.pool_min_ex(x, c.w, **kw),
+                  "conv": lambda x=x, c=c, kw=kw: oracle.conv1d_ex(x, c.f, **kw)}[c.op]
+            plan.append((c, lambda fn=fn, L=L: (fn(), L)[1]))
         elif c.cfg == "affine":
             n = max(c.w, int(8 * (1 << 24) * frac))
             u = synth.uab(31, n, 0.5, 1.0)

@@ -61,10 +61,16 @@
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 6
+#define SS_ABI_VERSION 7
 
 typedef enum { SS_F32 = 0, SS_I32 = 1 } ss_dtype_t;
 typedef enum { SS_POOL_MAX = 0, SS_POOL_AVG = 1 } ss_pool_mode_t;
+/* Boundary extension of the window spec ("padding, mirroring,
+ * or periodicity"): SS_PAD_ZEROS pads with the operator's identity (0 for sums
+ * and dot products; never wins a max / min), SS_PAD_REFLECT mirrors about the
+ * end elements without repeating them (x[-u] = x[u], x[N-1+u] = x[N-1-u]),
+ * SS_PAD_CIRCULAR wraps (x[u mod N]), SS_PAD_REPLICATE repeats the end element. */
+typedef enum { SS_PAD_ZEROS = 0, SS_PAD_REFLECT = 1, SS_PAD_CIRCULAR = 2, SS_PAD_REPLICATE = 3 } ss_pad_mode_t;
 
 typedef enum {
   SS_OK = 0,
@@ -100,6 +106,12 @@ ss_status_t ss_pool_sum(const void* x, void* y, int64_t N, int64_t batch,
 ss_status_t ss_pool_max(const void* x, void* y, int64_t N, int64_t batch,
                         int64_t w, int64_t stride, ss_dtype_t dtype, void* stream);
 
+/* Eq. 3 with (+) = min ("min is associative", the sliding min
+ * example).  y[b][i] = min_{j<w} x[b][i*stride + j].
+ * dtype SS_I32 or SS_F32; exact (bitwise), same kernels as ss_pool_max. */
+ss_status_t ss_pool_min(const void* x, void* y, int64_t N, int64_t batch,
+                        int64_t w, int64_t stride, ss_dtype_t dtype, void* stream);
+
 /* Sliding dot product = 1-D convolution with a length-k filter (PAPER.md
  * l.86-87, Sec. 2.5; Eq. 4 per window), cross-correlation orientation
  * (reading R2): y[b][i] = sum_{j<k} filter[j] * x[b][i*stride + j].
@@ -133,30 +145,39 @@ ss_status_t ss_pool2d(const void* x, void* y, int64_t planes, int64_t H, int64_t
                       int64_t kh, int64_t kw, int64_t sh, int64_t sw,
                       ss_pool_mode_t mode, ss_dtype_t dtype, void* stream);
 
-/* ---- window spec: stride, dilation, zero padding -------
- * The input is logically extended by pad_left / pad_right positions of
- * padding: xp[t] = x[t - pad_left] for 0 <= t - pad_left < N.  Output i of a
- * row covers xp[i*stride + j*dilation], j < w (or k), so
+/* ---- window spec: stride, dilation, padding -------------
+ * The input is logically extended by pad_left / pad_right positions:
+ * xp[t] = x[t - pad_left] for 0 <= t - pad_left < N, otherwise by pad_mode
+ * (ss_pad_mode_t above).  Output i of a row covers xp[i*stride + j*dilation],
+ * j < w (or k), so
  *   out_len = (N + pad_left + pad_right - ((w-1)*dilation + 1)) / stride + 1
- * (SPEC.md l.263-268 WindowSpec).  Padding adds 0 to sums and dot products and
- * never wins a max; a window made only of padding yields the
- * identity (0, -inf, INT32_MIN).  dilation >= 1, pads >= 0; everything else,
- * layout (y is [batch][out_len]), errors, streams and numerics as for the
- * valid-padding calls above (which equal these with dilation 1, pads 0).
- * Stride 1 without dilation runs the TMA tile kernel on the interior outputs
- * and a direct kernel on the pad_left + pad_right edge outputs of each row. */
+ * (SPEC.md l.263-268 WindowSpec).  SS_PAD_ZEROS: padding adds 0 to sums and dot
+ * products and never wins a max or a min; a window made only of
+ * padding yields the identity (0, -inf / INT32_MIN, +inf / INT32_MAX).
+ * SS_PAD_REFLECT needs pad_left, pad_right <= N-1 and SS_PAD_CIRCULAR <= N
+ * (one reflection / one period; else SS_ERR_BAD_SIZE); an unknown pad_mode is
+ * SS_ERR_UNSUPPORTED.  dilation >= 1, pads >= 0; everything else, layout (y is
+ * [batch][out_len]), errors, streams and numerics as for the valid-padding
+ * calls above (which equal these with dilation 1, pads 0).  Stride 1 runs the
+ * tile kernels (TMA tile kernel, dilated phase kernel or tensor cores) on the
+ * interior outputs -- whose windows never touch padding, so they are the same
+ * for every mode -- and a direct kernel on the pad_left + pad_right edge
+ * outputs of each row. */
 int64_t ss_out_len_ex(int64_t N, int64_t w, int64_t stride, int64_t dilation,
                       int64_t pad_left, int64_t pad_right);
 ss_status_t ss_pool_sum_ex(const void* x, void* y, int64_t N, int64_t batch, int64_t w,
                            int64_t stride, int64_t dilation, int64_t pad_left,
-                           int64_t pad_right, ss_dtype_t dtype, void* stream);
+                           int64_t pad_right, ss_pad_mode_t pad_mode, ss_dtype_t dtype, void* stream);
 ss_status_t ss_pool_max_ex(const void* x, void* y, int64_t N, int64_t batch, int64_t w,
                            int64_t stride, int64_t dilation, int64_t pad_left,
-                           int64_t pad_right, ss_dtype_t dtype, void* stream);
+                           int64_t pad_right, ss_pad_mode_t pad_mode, ss_dtype_t dtype, void* stream);
+ss_status_t ss_pool_min_ex(const void* x, void* y, int64_t N, int64_t batch, int64_t w,
+                           int64_t stride, int64_t dilation, int64_t pad_left,
+                           int64_t pad_right, ss_pad_mode_t pad_mode, ss_dtype_t dtype, void* stream);
 ss_status_t ss_conv1d_ex(const void* x, void* y, int64_t N, int64_t batch,
                          const float* filter_host, int64_t k, int64_t stride,
                          int64_t dilation, int64_t pad_left, int64_t pad_right,
-                         ss_dtype_t dtype, void* stream);
+                         ss_pad_mode_t pad_mode, ss_dtype_t dtype, void* stream);
 
 /* ---- sliding window of gamma pairs --------------------
  * The paper's pair operator (Eq. 8)

@@ -23,6 +23,12 @@ SS_F32 = 0
 SS_I32 = 1
 SS_POOL_MAX = 0
 SS_POOL_AVG = 1
+SS_PAD_ZEROS = 0
+SS_PAD_REFLECT = 1
+SS_PAD_CIRCULAR = 2
+SS_PAD_REPLICATE = 3
+PAD_MODES = {"zeros": SS_PAD_ZEROS, "reflect": SS_PAD_REFLECT, "circular": SS_PAD_CIRCULAR,
+             "replicate": SS_PAD_REPLICATE}
 SS_OK = 0
 SS_ERR_NULL = 1
 SS_ERR_BAD_SIZE = 2
@@ -33,9 +39,9 @@ SS_ERR_OVERLAP = 6
 SS_K_MAX = 1024
 SS_AFFINE_W_MAX = 65536
 
-EXPORTED = ("ss_abi_version", "ss_out_len", "ss_pool_sum", "ss_pool_max", "ss_conv1d",
+EXPORTED = ("ss_abi_version", "ss_out_len", "ss_pool_sum", "ss_pool_max", "ss_pool_min", "ss_conv1d",
             "ss_pool2d", "ss_status_string", "ss_last_error", "ss_launch_count",
-            "ss_out_len_ex", "ss_pool_sum_ex", "ss_pool_max_ex", "ss_conv1d_ex",
+            "ss_out_len_ex", "ss_pool_sum_ex", "ss_pool_max_ex", "ss_pool_min_ex", "ss_conv1d_ex",
             "ss_affine_window", "ss_pool_sum_backward", "ss_pool_max_backward",
             "ss_conv1d_backward_input", "ss_conv1d_backward_filter_workspace", "ss_conv1d_backward_filter",
             "ss_pool2d_backward", "ss_conv2d", "ss_conv1d_mc")
@@ -58,7 +64,7 @@ def _load() -> ctypes.CDLL:
     L.ss_abi_version.restype = i32
     L.ss_out_len.argtypes = [i64, i64, i64]
     L.ss_out_len.restype = i64
-    for n in ("ss_pool_sum", "ss_pool_max"):
+    for n in ("ss_pool_sum", "ss_pool_max", "ss_pool_min"):
         getattr(L, n).argtypes = [vp, vp, i64, i64, i64, i64, i32, vp]
         getattr(L, n).restype = i32
     L.ss_conv1d.argtypes = [vp, vp, i64, i64, ctypes.POINTER(ctypes.c_float), i64, i64, i32, vp]
@@ -67,11 +73,11 @@ def _load() -> ctypes.CDLL:
     L.ss_pool2d.restype = i32
     L.ss_out_len_ex.argtypes = [i64] * 6
     L.ss_out_len_ex.restype = i64
-    for n in ("ss_pool_sum_ex", "ss_pool_max_ex"):
-        getattr(L, n).argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, i32, vp]
+    for n in ("ss_pool_sum_ex", "ss_pool_max_ex", "ss_pool_min_ex"):
+        getattr(L, n).argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, i32, i32, vp]
         getattr(L, n).restype = i32
     L.ss_conv1d_ex.argtypes = [vp, vp, i64, i64, ctypes.POINTER(ctypes.c_float), i64, i64, i64, i64, i64,
-                               i32, vp]
+                               i32, i32, vp]
     L.ss_conv1d_ex.restype = i32
     L.ss_affine_window.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64, vp]
     L.ss_affine_window.restype = i32
@@ -135,6 +141,11 @@ def ss_pool_max(x_ptr: int, y_ptr: int, N: int, batch: int, w: int, stride: int,
     return _lib.ss_pool_max(x_ptr, y_ptr, N, batch, w, stride, dtype, stream)
 
 
+def ss_pool_min(x_ptr: int, y_ptr: int, N: int, batch: int, w: int, stride: int, dtype: int,
+                stream: int = 0) -> int:
+    return _lib.ss_pool_min(x_ptr, y_ptr, N, batch, w, stride, dtype, stream)
+
+
 def ss_conv1d(x_ptr: int, y_ptr: int, N: int, batch: int, filter_host, k: int, stride: int,
               dtype: int = SS_F32, stream: int = 0) -> int:
     if filter_host is None:
@@ -154,18 +165,29 @@ def ss_out_len_ex(N: int, w: int, stride: int = 1, dilation: int = 1, pad_left: 
     return int(_lib.ss_out_len_ex(N, w, stride, dilation, pad_left, pad_right))
 
 
-def ss_pool_sum_ex(x_ptr, y_ptr, N, batch, w, stride, dilation, pad_left, pad_right, dtype, stream=0) -> int:
-    return _lib.ss_pool_sum_ex(x_ptr, y_ptr, N, batch, w, stride, dilation, pad_left, pad_right, dtype, stream)
+def ss_pool_sum_ex(x_ptr, y_ptr, N, batch, w, stride, dilation, pad_left, pad_right, pad_mode, dtype,
+                   stream=0) -> int:
+    return _lib.ss_pool_sum_ex(x_ptr, y_ptr, N, batch, w, stride, dilation, pad_left, pad_right, pad_mode, dtype,
+                               stream)
 
 
-def ss_pool_max_ex(x_ptr, y_ptr, N, batch, w, stride, dilation, pad_left, pad_right, dtype, stream=0) -> int:
-    return _lib.ss_pool_max_ex(x_ptr, y_ptr, N, batch, w, stride, dilation, pad_left, pad_right, dtype, stream)
+def ss_pool_max_ex(x_ptr, y_ptr, N, batch, w, stride, dilation, pad_left, pad_right, pad_mode, dtype,
+                   stream=0) -> int:
+    return _lib.ss_pool_max_ex(x_ptr, y_ptr, N, batch, w, stride, dilation, pad_left, pad_right, pad_mode, dtype,
+                               stream)
 
 
-def ss_conv1d_ex(x_ptr, y_ptr, N, batch, filter_host, k, stride, dilation, pad_left, pad_right,
+def ss_pool_min_ex(x_ptr, y_ptr, N, batch, w, stride, dilation, pad_left, pad_right, pad_mode, dtype,
+                   stream=0) -> int:
+    return _lib.ss_pool_min_ex(x_ptr, y_ptr, N, batch, w, stride, dilation, pad_left, pad_right, pad_mode, dtype,
+                               stream)
+
+
+def ss_conv1d_ex(x_ptr, y_ptr, N, batch, filter_host, k, stride, dilation, pad_left, pad_right, pad_mode,
                  dtype=SS_F32, stream=0) -> int:
     fp = None if filter_host is None else (ctypes.c_float * len(filter_host))(*[float(v) for v in filter_host])
-    return _lib.ss_conv1d_ex(x_ptr, y_ptr, N, batch, fp, k, stride, dilation, pad_left, pad_right, dtype, stream)
+    return _lib.ss_conv1d_ex(x_ptr, y_ptr, N, batch, fp, k, stride, dilation, pad_left, pad_right, pad_mode, dtype,
+                             stream)
 
 
 def ss_affine_window(u_ptr, v_ptr, U_ptr, V_ptr, N, batch, w, stride=1, stream=0) -> int:
@@ -260,48 +282,59 @@ def _pads(padding):
     return int(padding), int(padding)
 
 
-def pool_sum(x, w: int, stride: int = 1, out=None, stream=None, dilation: int = 1, padding=0):
+def _pad_mode(pad_mode) -> int:
+    return PAD_MODES[pad_mode] if isinstance(pad_mode, str) else int(pad_mode)
+
+
+def _window(fn, x, w, stride, out, stream, dilation, padding, pad_mode):
+    N, B = _rows(x)
+    pl, pr = _pads(padding)
+    L = ss_out_len_ex(N, w, stride, dilation, pl, pr)
+    args = (N, B, w, stride, dilation, pl, pr, _pad_mode(pad_mode), _dtype_code(x), _stream(stream))
+    if L < 0:
+        check(fn(x.data_ptr(), 0, *args) or SS_ERR_BAD_SIZE)
+    y = _out(x, L, out)
+    check(fn(x.data_ptr(), y.data_ptr(), *args))
+    return y
+
+
+def pool_sum(x, w: int, stride: int = 1, out=None, stream=None, dilation: int = 1, padding=0,
+             pad_mode="zeros"):
     """Eq. 3 with + (raw window sums) over the last dim of a CUDA [N] / [B, N] tensor;
-    optional dilation and zero padding (int or (left, right))."""
-    N, B = _rows(x)
-    pl, pr = _pads(padding)
-    L = ss_out_len_ex(N, w, stride, dilation, pl, pr)
-    args = (N, B, w, stride, dilation, pl, pr, _dtype_code(x), _stream(stream))
-    if L < 0:
-        check(ss_pool_sum_ex(x.data_ptr(), 0, *args) or SS_ERR_BAD_SIZE)
-    y = _out(x, L, out)
-    check(ss_pool_sum_ex(x.data_ptr(), y.data_ptr(), *args))
-    return y
+    optional dilation and padding (int or (left, right); pad_mode zeros / reflect /
+    circular / replicate)."""
+    return _window(ss_pool_sum_ex, x, w, stride, out, stream, dilation, padding, pad_mode)
 
 
-def pool_max(x, w: int, stride: int = 1, out=None, stream=None, dilation: int = 1, padding=0):
+def pool_max(x, w: int, stride: int = 1, out=None, stream=None, dilation: int = 1, padding=0,
+             pad_mode="zeros"):
     """Eq. 3 with max over the last dim of a CUDA [N] / [B, N] tensor; optional
-    dilation and padding (padding never wins)."""
-    N, B = _rows(x)
-    pl, pr = _pads(padding)
-    L = ss_out_len_ex(N, w, stride, dilation, pl, pr)
-    args = (N, B, w, stride, dilation, pl, pr, _dtype_code(x), _stream(stream))
-    if L < 0:
-        check(ss_pool_max_ex(x.data_ptr(), 0, *args) or SS_ERR_BAD_SIZE)
-    y = _out(x, L, out)
-    check(ss_pool_max_ex(x.data_ptr(), y.data_ptr(), *args))
-    return y
+    dilation and padding (zeros padding never wins)."""
+    return _window(ss_pool_max_ex, x, w, stride, out, stream, dilation, padding, pad_mode)
 
 
-def conv1d(x, filt, stride: int = 1, out=None, stream=None, dilation: int = 1, padding=0):
+def pool_min(x, w: int, stride: int = 1, out=None, stream=None, dilation: int = 1, padding=0,
+             pad_mode="zeros"):
+    """Eq. 3 with min (the sliding min of PAPER.md l.136) over the last dim of a CUDA
+    [N] / [B, N] tensor; optional dilation and padding (zeros padding never wins)."""
+    return _window(ss_pool_min_ex, x, w, stride, out, stream, dilation, padding, pad_mode)
+
+
+def conv1d(x, filt, stride: int = 1, out=None, stream=None, dilation: int = 1, padding=0, pad_mode="zeros"):
     """Sliding dot product (cross-correlation) of a CUDA fp32 [N]/[B, N] tensor with
     a host filter (sequence of floats, numpy array or CPU tensor); optional
-    dilation and zero padding."""
+    dilation and padding."""
     N, B = _rows(x)
     f = [float(v) for v in (filt.tolist() if hasattr(filt, "tolist") else filt)]
     k = len(f)
     pl, pr = _pads(padding)
     L = ss_out_len_ex(N, k, stride, dilation, pl, pr)
+    pm = _pad_mode(pad_mode)
     if L < 0:
-        check(ss_conv1d_ex(x.data_ptr(), 0, N, B, f, k, stride, dilation, pl, pr, _dtype_code(x),
+        check(ss_conv1d_ex(x.data_ptr(), 0, N, B, f, k, stride, dilation, pl, pr, pm, _dtype_code(x),
                            _stream(stream)) or SS_ERR_BAD_SIZE)
     y = _out(x, L, out)
-    check(ss_conv1d_ex(x.data_ptr(), y.data_ptr(), N, B, f, k, stride, dilation, pl, pr, _dtype_code(x),
+    check(ss_conv1d_ex(x.data_ptr(), y.data_ptr(), N, B, f, k, stride, dilation, pl, pr, pm, _dtype_code(x),
                        _stream(stream)))
     return y
 

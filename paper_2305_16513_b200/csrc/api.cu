@@ -329,11 +329,16 @@ static int conv_bucket(int64_t k) {
 // generic launch fills the pl + pr edge outputs); everything else runs the
 // direct-window generic kernels.
 static ss_status_t window_impl(int op, const void* x, void* y, int64_t N, int64_t batch, int64_t w,
-                               int64_t stride, int64_t d, int64_t pl, int64_t pr, ss_dtype_t dtype,
-                               const float* taps, void* stream) {
+                               int64_t stride, int64_t d, int64_t pl, int64_t pr, int pad_mode,
+                               ss_dtype_t dtype, const float* taps, void* stream) {
   int64_t L = 0;
   ss_status_t st = validate_1d(x, y, N, batch, w, stride, d, pl, pr, op == kOpConv ? "k" : "w", &L);
   if (st != SS_OK) return st;
+  if (pad_mode < kPadZeros || pad_mode > kPadReplicate) return fail(SS_ERR_UNSUPPORTED, "pad_mode %d", pad_mode);
+  if (pad_mode == kPadReflect && (pl > N - 1 || pr > N - 1))
+    return fail(SS_ERR_BAD_SIZE, "reflect padding needs pad_left, pad_right <= N-1 (one reflection)");
+  if (pad_mode == kPadCircular && (pl > N || pr > N))
+    return fail(SS_ERR_BAD_SIZE, "circular padding needs pad_left, pad_right <= N (one period)");
   if (op == kOpConv) {
     if (dtype != SS_F32) return fail(SS_ERR_UNSUPPORTED, "conv1d supports SS_F32 only");
     if (w > SS_K_MAX) return fail(SS_ERR_UNSUPPORTED, "k=%lld > SS_K_MAX=%d", (long long)w, SS_K_MAX);
@@ -397,6 +402,7 @@ static ss_status_t window_impl(int op, const void* x, void* y, int64_t N, int64_
   }
   if (interior_done && pl == 0 && pr == 0) return SS_OK;
   GenericParams g = generic_params(x, y, N, L, batch, w, stride, d, pl);
+  g.pad_mode = pad_mode;
   if (interior_done) {
     g.skip_lo = pl;
     g.skip_hi = pl + L_int;
@@ -434,39 +440,51 @@ int64_t ss_out_len(int64_t N, int64_t w, int64_t stride) {
 
 ss_status_t ss_pool_sum(const void* x, void* y, int64_t N, int64_t batch, int64_t w,
                         int64_t stride, ss_dtype_t dtype, void* stream) {
-  return window_impl(kOpSum, x, y, N, batch, w, stride, 1, 0, 0, dtype, nullptr, stream);
+  return window_impl(kOpSum, x, y, N, batch, w, stride, 1, 0, 0, kPadZeros, dtype, nullptr, stream);
 }
 
 ss_status_t ss_pool_max(const void* x, void* y, int64_t N, int64_t batch, int64_t w,
                         int64_t stride, ss_dtype_t dtype, void* stream) {
-  return window_impl(kOpMax, x, y, N, batch, w, stride, 1, 0, 0, dtype, nullptr, stream);
+  return window_impl(kOpMax, x, y, N, batch, w, stride, 1, 0, 0, kPadZeros, dtype, nullptr, stream);
+}
+
+ss_status_t ss_pool_min(const void* x, void* y, int64_t N, int64_t batch, int64_t w,
+                        int64_t stride, ss_dtype_t dtype, void* stream) {
+  return window_impl(kOpMin, x, y, N, batch, w, stride, 1, 0, 0, kPadZeros, dtype, nullptr, stream);
 }
 
 ss_status_t ss_conv1d(const void* x, void* y, int64_t N, int64_t batch, const float* filter_host,
                       int64_t k, int64_t stride, ss_dtype_t dtype, void* stream) {
   if (!filter_host) return fail(SS_ERR_NULL, "filter_host must be non-NULL");
-  return window_impl(kOpConv, x, y, N, batch, k, stride, 1, 0, 0, dtype, filter_host, stream);
+  return window_impl(kOpConv, x, y, N, batch, k, stride, 1, 0, 0, kPadZeros, dtype, filter_host, stream);
 }
 
 ss_status_t ss_pool_sum_ex(const void* x, void* y, int64_t N, int64_t batch, int64_t w,
                            int64_t stride, int64_t dilation, int64_t pad_left, int64_t pad_right,
-                           ss_dtype_t dtype, void* stream) {
-  return window_impl(kOpSum, x, y, N, batch, w, stride, dilation, pad_left, pad_right, dtype, nullptr,
-                     stream);
+                           ss_pad_mode_t pad_mode, ss_dtype_t dtype, void* stream) {
+  return window_impl(kOpSum, x, y, N, batch, w, stride, dilation, pad_left, pad_right, (int)pad_mode, dtype,
+                     nullptr, stream);
 }
 
 ss_status_t ss_pool_max_ex(const void* x, void* y, int64_t N, int64_t batch, int64_t w,
                            int64_t stride, int64_t dilation, int64_t pad_left, int64_t pad_right,
-                           ss_dtype_t dtype, void* stream) {
-  return window_impl(kOpMax, x, y, N, batch, w, stride, dilation, pad_left, pad_right, dtype, nullptr,
-                     stream);
+                           ss_pad_mode_t pad_mode, ss_dtype_t dtype, void* stream) {
+  return window_impl(kOpMax, x, y, N, batch, w, stride, dilation, pad_left, pad_right, (int)pad_mode, dtype,
+                     nullptr, stream);
+}
+
+ss_status_t ss_pool_min_ex(const void* x, void* y, int64_t N, int64_t batch, int64_t w,
+                           int64_t stride, int64_t dilation, int64_t pad_left, int64_t pad_right,
+                           ss_pad_mode_t pad_mode, ss_dtype_t dtype, void* stream) {
+  return window_impl(kOpMin, x, y, N, batch, w, stride, dilation, pad_left, pad_right, (int)pad_mode, dtype,
+                     nullptr, stream);
 }
 
 ss_status_t ss_conv1d_ex(const void* x, void* y, int64_t N, int64_t batch, const float* filter_host,
                          int64_t k, int64_t stride, int64_t dilation, int64_t pad_left,
-                         int64_t pad_right, ss_dtype_t dtype, void* stream) {
+                         int64_t pad_right, ss_pad_mode_t pad_mode, ss_dtype_t dtype, void* stream) {
   if (!filter_host) return fail(SS_ERR_NULL, "filter_host must be non-NULL");
-  return window_impl(kOpConv, x, y, N, batch, k, stride, dilation, pad_left, pad_right, dtype,
+  return window_impl(kOpConv, x, y, N, batch, k, stride, dilation, pad_left, pad_right, (int)pad_mode, dtype,
                      filter_host, stream);
 }
 
@@ -492,7 +510,7 @@ static ss_status_t pool_sum_backward_impl(const void* dy, void* dx, int64_t N, i
   if (dtype != SS_F32 && dtype != SS_I32) return fail(SS_ERR_UNSUPPORTED, "dtype %d", (int)dtype);
   if (overlaps(dy, batch * L * 4, dx, batch * N * 4)) return fail(SS_ERR_OVERLAP, "dy and dx overlap");
   if (stride == 1)  // dx = sliding sum of dy zero-padded by w-1 on both sides (length L + w - 1 = N)
-    return window_impl(kOpSum, dy, dx, L, batch, w, 1, 1, w - 1, w - 1, dtype, nullptr, stream);
+    return window_impl(kOpSum, dy, dx, L, batch, w, 1, 1, w - 1, w - 1, kPadZeros, dtype, nullptr, stream);
   BackwardParams p;
   memset(&p, 0, sizeof p);
   p.dy = dy; p.dx = dx; p.N = N; p.L = L; p.batch = batch; p.w = w; p.stride = stride;
@@ -513,7 +531,7 @@ static ss_status_t conv1d_backward_input_impl(const void* dy, void* dx, int64_t 
   if (stride == 1) {  // dx = dy zero-padded by k-1 on both sides, correlated with the flipped filter
     float flipped[SS_K_MAX];
     for (int64_t j = 0; j < k; ++j) flipped[j] = f[k - 1 - j];
-    return window_impl(kOpConv, dy, dx, L, batch, k, 1, 1, k - 1, k - 1, SS_F32, flipped, stream);
+    return window_impl(kOpConv, dy, dx, L, batch, k, 1, 1, k - 1, k - 1, kPadZeros, SS_F32, flipped, stream);
   }
   BackwardParams p;
   memset(&p, 0, sizeof p);

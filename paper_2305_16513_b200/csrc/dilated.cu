@@ -171,6 +171,7 @@ cudaError_t launch_dilated(DilatedParams& p, int op, cudaStream_t stream, int sm
     return launch_op<ConvAcc>(p, stream, sms);
   }
   if (op == kOpSum) return launch_op<OpSumF32>(p, stream, sms);
+  if (op == kOpMin) return launch_op<OpMinF32>(p, stream, sms);
   return launch_op<OpMaxF32>(p, stream, sms);
 }
 

@@ -60,6 +60,17 @@ __global__ void __launch_bounds__(kGenThreads) pool_generic_kernel(const __grid_
 // order (increasing j, skipped taps contribute nothing) is unchanged.
 constexpr int kTapGroup = 8;
 
+// x index of padded position u (u = i*s + j*d - pad_left, possibly outside [0, N)), or -1
+// for zero padding (ss.h ss_pad_mode_t; the API bounds the pads so one reflection / one
+// period suffices)
+__device__ __forceinline__ int64_t pad_source(int64_t u, int64_t N, int mode) {
+  if (u >= 0 && u < N) return u;
+  if (mode == kPadReflect) return u < 0 ? -u : 2 * (N - 1) - u;
+  if (mode == kPadCircular) return u < 0 ? u + N : u - N;
+  if (mode == kPadReplicate) return u < 0 ? 0 : N - 1;
+  return -1;
+}
+
 template <class Op>
 __device__ __forceinline__ typename Op::T window_checked(const typename Op::T* __restrict__ xr,
                                                          int64_t t0, const GenericParams& p) {
@@ -69,8 +80,8 @@ __device__ __forceinline__ typename Op::T window_checked(const typename Op::T* _
     bool ok[kTapGroup];
 #pragma unroll
     for (int u = 0; u < kTapGroup; ++u) {
-      const int64_t t = t0 + (int64_t)(j0 + u) * p.dilation;
-      ok[u] = j0 + u < (int)p.w && t >= 0 && t < p.N;
+      const int64_t t = pad_source(t0 + (int64_t)(j0 + u) * p.dilation, p.N, p.pad_mode);
+      ok[u] = j0 + u < (int)p.w && t >= 0;
       v[u] = ok[u] ? __ldg(xr + t) : Op::identity();
     }
 #pragma unroll
@@ -170,8 +181,8 @@ __device__ __forceinline__ float conv_checked(const float* __restrict__ xr, int6
     bool ok[kTapGroup];
 #pragma unroll
     for (int u = 0; u < kTapGroup; ++u) {
-      const int64_t t = t0 + (int64_t)(j0 + u) * p.dilation;
-      ok[u] = j0 + u < (int)p.w && t >= 0 && t < p.N;
+      const int64_t t = pad_source(t0 + (int64_t)(j0 + u) * p.dilation, p.N, p.pad_mode);
+      ok[u] = j0 + u < (int)p.w && t >= 0;
       v[u] = ok[u] ? __ldg(xr + t) : 0.0f;
     }
 #pragma unroll
@@ -289,12 +300,16 @@ cudaError_t launch_pool_generic(const GenericParams& p, int op, int dtype, cudaS
     else if (op == kOpSum && dtype == 0) pool_generic_ex_kernel<OpSumF32><<<ge, kGenThreads, 0, stream>>>(p);
     else if (op == kOpMax && dtype == 1) pool_generic_ex_kernel<OpMaxI32><<<ge, kGenThreads, 0, stream>>>(p);
     else if (op == kOpMax && dtype == 0) pool_generic_ex_kernel<OpMaxF32><<<ge, kGenThreads, 0, stream>>>(p);
+    else if (op == kOpMin && dtype == 1) pool_generic_ex_kernel<OpMinI32><<<ge, kGenThreads, 0, stream>>>(p);
+    else if (op == kOpMin && dtype == 0) pool_generic_ex_kernel<OpMinF32><<<ge, kGenThreads, 0, stream>>>(p);
     else return cudaErrorInvalidValue;
   } else {
     if (op == kOpSum && dtype == 1) pool_generic_kernel<OpSumI32><<<g, kGenThreads, 0, stream>>>(p);
     else if (op == kOpSum && dtype == 0) pool_generic_kernel<OpSumF32><<<g, kGenThreads, 0, stream>>>(p);
     else if (op == kOpMax && dtype == 1) pool_generic_kernel<OpMaxI32><<<g, kGenThreads, 0, stream>>>(p);
     else if (op == kOpMax && dtype == 0) pool_generic_kernel<OpMaxF32><<<g, kGenThreads, 0, stream>>>(p);
+    else if (op == kOpMin && dtype == 1) pool_generic_kernel<OpMinI32><<<g, kGenThreads, 0, stream>>>(p);
+    else if (op == kOpMin && dtype == 0) pool_generic_kernel<OpMinF32><<<g, kGenThreads, 0, stream>>>(p);
     else return cudaErrorInvalidValue;
   }
   note_launch();

@@ -725,6 +725,8 @@ cudaError_t launch_pool_tma(Slide1DParams& p, int op, int dtype, int P, cudaStre
   if (op == kOpSum && dtype == 0) return launch_pool_op<OpSumF32>(p, P, stream, grid);
   if (op == kOpMax && dtype == 1) return launch_pool_op<OpMaxI32>(p, P, stream, grid);
   if (op == kOpMax && dtype == 0) return launch_pool_op<OpMaxF32>(p, P, stream, grid);
+  if (op == kOpMin && dtype == 1) return launch_pool_op<OpMinI32>(p, P, stream, grid);
+  if (op == kOpMin && dtype == 0) return launch_pool_op<OpMinF32>(p, P, stream, grid);
   return cudaErrorInvalidValue;
 }
 

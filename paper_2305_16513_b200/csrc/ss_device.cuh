@@ -38,6 +38,17 @@ struct OpMaxF32 {
   // the sign of a zero maximum unspecified)
   static __device__ __forceinline__ T combine(T a, T b) { return fmaxf(a, b); }
 };
+// Sliding min (Sec. 2.3's other extremum; "min is associative").
+struct OpMinI32 {
+  using T = int32_t;
+  static __device__ __forceinline__ T identity() { return INT32_MAX; }
+  static __device__ __forceinline__ T combine(T a, T b) { return a < b ? a : b; }
+};
+struct OpMinF32 {
+  using T = float;
+  static __device__ __forceinline__ T identity() { return INFINITY; }
+  static __device__ __forceinline__ T combine(T a, T b) { return fminf(a, b); }
+};
 
 // ---------------------------------------------------------------- smem / PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -10,6 +10,9 @@ namespace ss {
 constexpr int kOpSum = 0;
 constexpr int kOpMax = 1;
 constexpr int kOpConv = 2;
+constexpr int kOpMin = 3;
+// padding modes of the window spec (ss.h ss_pad_mode_t)
+constexpr int kPadZeros = 0, kPadReflect = 1, kPadCircular = 2, kPadReplicate = 3;
 constexpr int kSmemBudget = 227 * 1024;  // max dynamic smem per CTA on sm_100a
 // Dynamic tile scheduling of the persistent kernels: slot = {next, done}; tile
 // n >= gridDim.x of a launch is claimed with atomicAdd(next) + gridDim.x (the
@@ -54,6 +57,7 @@ struct GenericParams {
   int64_t N, L, batch, w, stride;
   int64_t dilation, pad_left;  // window spec (NEXT #1): x index of tap j of output i = i*s + j*d - pl
   int64_t skip_lo, skip_hi;    // if skip_lo < skip_hi: outputs in [skip_lo, skip_hi) are not computed
+  int pad_mode;                // kPadZeros / kPadReflect / kPadCircular / kPadReplicate
   float taps[1024];            // SS_K_MAX
 };
 

@@ -45,7 +45,7 @@ def test_library_is_sm100a(ss):
 
 
 def test_abi_version_and_out_len(ss):
-    assert ss.ss_abi_version() == 6
+    assert ss.ss_abi_version() == 7
     assert ss.ss_out_len(10, 3, 1) == 8
     assert ss.ss_out_len(10, 3, 4) == 2
     assert ss.ss_out_len(2 ** 32, 31, 1) == 2 ** 32 - 30
@@ -117,11 +117,18 @@ def test_window_spec_validation(ss):
     assert ss.ss_out_len_ex(3, 4, 1, 2, 1, 1) == -1
     assert ss.ss_out_len_ex(3, 4, 1, 1, 0, 0) == -1
     assert ss.ss_out_len_ex(10, 3, 1, 0, 0, 0) == -1
-    assert ss.ss_pool_sum_ex(FAKE_X, FAKE_Y, 10, 1, 3, 1, 0, 0, 0, ss.SS_F32) == ss.SS_ERR_BAD_SIZE
-    assert ss.ss_pool_max_ex(FAKE_X, FAKE_Y, 10, 1, 3, 1, 1, -2, 0, ss.SS_F32) == ss.SS_ERR_BAD_SIZE
-    assert ss.ss_pool_max_ex(FAKE_X, FAKE_Y, 3, 1, 3, 1, 2, 0, 0, ss.SS_F32) == ss.SS_ERR_WINDOW_EXCEEDS_INPUT
-    assert ss.ss_conv1d_ex(FAKE_X, FAKE_Y, 10, 1, None, 3, 1, 1, 0, 0, ss.SS_F32) == ss.SS_ERR_NULL
-    assert ss.ss_conv1d_ex(FAKE_X, FAKE_Y, 10, 1, [1.0] * 3, 3, 1, 1, 0, 0, ss.SS_I32) == ss.SS_ERR_UNSUPPORTED
+    Z = ss.SS_PAD_ZEROS
+    assert ss.ss_pool_sum_ex(FAKE_X, FAKE_Y, 10, 1, 3, 1, 0, 0, 0, Z, ss.SS_F32) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_pool_max_ex(FAKE_X, FAKE_Y, 10, 1, 3, 1, 1, -2, 0, Z, ss.SS_F32) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_pool_max_ex(FAKE_X, FAKE_Y, 3, 1, 3, 1, 2, 0, 0, Z, ss.SS_F32) == ss.SS_ERR_WINDOW_EXCEEDS_INPUT
+    assert ss.ss_conv1d_ex(FAKE_X, FAKE_Y, 10, 1, None, 3, 1, 1, 0, 0, Z, ss.SS_F32) == ss.SS_ERR_NULL
+    assert ss.ss_conv1d_ex(FAKE_X, FAKE_Y, 10, 1, [1.0] * 3, 3, 1, 1, 0, 0, Z, ss.SS_I32) == ss.SS_ERR_UNSUPPORTED
+    # padding modes: one reflection (pads <= N-1) / one period (<= N); unknown mode
+    assert ss.ss_pool_min_ex(FAKE_X, FAKE_Y, 10, 1, 3, 1, 1, 10, 0, ss.SS_PAD_REFLECT, ss.SS_F32) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_pool_sum_ex(FAKE_X, FAKE_Y, 10, 1, 3, 1, 1, 0, 11, ss.SS_PAD_CIRCULAR, ss.SS_F32) == ss.SS_ERR_BAD_SIZE
+    assert ss.ss_pool_sum_ex(FAKE_X, FAKE_Y, 10, 1, 3, 1, 1, 1, 1, 9, ss.SS_F32) == ss.SS_ERR_UNSUPPORTED
+    assert ss.ss_pool_min(0, FAKE_Y, 10, 1, 3, 1, ss.SS_F32) == ss.SS_ERR_NULL
+    assert ss.ss_pool_min(FAKE_X, FAKE_Y, 10, 1, 11, 1, ss.SS_F32) == ss.SS_ERR_WINDOW_EXCEEDS_INPUT
 
 
 def test_affine_window_validation(ss):
