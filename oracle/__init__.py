@@ -92,6 +92,10 @@ def lib() -> ctypes.CDLL:
             L.oracle_conv1d_mc_bf16.restype = ctypes.c_int
             L.oracle_conv2d_f32.argtypes = [vp, i64, i64, i64, vp, i64, i64, i64, i64, vp, vp]
             L.oracle_conv2d_f32.restype = ctypes.c_int
+            L.oracle_conv2d_backward_input_f32.argtypes = [vp, i64, i64, i64, vp, i64, i64, i64, i64, vp, vp]
+            L.oracle_conv2d_backward_input_f32.restype = ctypes.c_int
+            L.oracle_conv2d_backward_filter_f32.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, vp]
+            L.oracle_conv2d_backward_filter_f32.restype = ctypes.c_int
             for n in ("oracle_pool_sum_backward_f32", "oracle_pool_max_backward_f32",
                       "oracle_conv1d_backward_input_f32", "oracle_conv1d_backward_filter_f32",
                       "oracle_pool2d_backward_f32"):
@@ -374,6 +378,31 @@ def conv2d(x: np.ndarray, f: np.ndarray, sh: int = 1, sw: int = 1):
     m = np.empty((P, OH, OW), np.float64)
     _check(lib().oracle_conv2d_f32(_p(x), P, H, W, _p(f), kh, kw, sh, sw, _p(y), _p(m)))
     return y, m
+
+
+def conv2d_backward_input(dy: np.ndarray, f: np.ndarray, H: int, W: int, sh: int = 1, sw: int = 1):
+    """dx of the 2-D sliding dot product (reading R21): [planes, H, W]; (dx, absmag)."""
+    dy = np.ascontiguousarray(dy, np.float32)
+    f = np.ascontiguousarray(f, np.float32)
+    P = dy.shape[0]
+    kh, kw = f.shape
+    assert dy.shape[1:] == (out_len(H, kh, sh), out_len(W, kw, sw))
+    dx = np.empty((P, H, W), np.float64)
+    m = np.empty((P, H, W), np.float64)
+    _check(lib().oracle_conv2d_backward_input_f32(_p(dy), P, H, W, _p(f), kh, kw, sh, sw, _p(dx), _p(m)))
+    return dx, m
+
+
+def conv2d_backward_filter(x: np.ndarray, dy: np.ndarray, kh: int, kw: int, sh: int = 1, sw: int = 1):
+    """df [kh, kw] of the 2-D sliding dot product (reading R21); (df, absmag)."""
+    x = np.ascontiguousarray(x, np.float32)
+    dy = np.ascontiguousarray(dy, np.float32)
+    P, H, W = x.shape
+    assert dy.shape == (P, out_len(H, kh, sh), out_len(W, kw, sw))
+    df = np.empty((kh, kw), np.float64)
+    m = np.empty((kh, kw), np.float64)
+    _check(lib().oracle_conv2d_backward_filter_f32(_p(x), _p(dy), P, H, W, kh, kw, sh, sw, _p(df), _p(m)))
+    return df, m
 
 
 def to_bf16_bits(a: np.ndarray) -> np.ndarray:

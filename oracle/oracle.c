@@ -546,6 +546,53 @@ int oracle_conv2d_f32(const float* x, int64_t planes, int64_t H, int64_t W, cons
   return 0;
 }
 
+/* Backward passes of the 2-D sliding dot product (SURVEY 8f NEXT #4 "2-D
+ * convolution and backward passes"; reading R21), the vector-Jacobian
+ * products of y[p][r][c] = sum_a sum_b f[a][b] x[p][r*sh+a][c*sw+b]:
+ *   dx[p][r*sh+a][c*sw+b] += f[a][b] dy[p][r][c]   (scatter form, every (r, c, a, b))
+ *   df[a][b] = sum_p sum_r sum_c dy[p][r][c] x[p][r*sh+a][c*sw+b]
+ * accumulated in double; absmag = per-element sum of term magnitudes. */
+int oracle_conv2d_backward_input_f32(const float* dy, int64_t planes, int64_t H, int64_t W, const float* f,
+                                     int64_t kh, int64_t kw, int64_t sh, int64_t sw, double* dx, double* absmag) {
+  int64_t OH = oracle_out_len(H, kh, sh), OW = oracle_out_len(W, kw, sw);
+  if (dy == NULL || f == NULL || dx == NULL || planes < 1 || OH < 0 || OW < 0) return -1;
+  for (int64_t t = 0; t < planes * H * W; ++t) {
+    dx[t] = 0.0;
+    if (absmag) absmag[t] = 0.0;
+  }
+  for (int64_t p = 0; p < planes; ++p)
+    for (int64_t r = 0; r < OH; ++r)
+      for (int64_t c = 0; c < OW; ++c)
+        for (int64_t a = 0; a < kh; ++a)
+          for (int64_t b = 0; b < kw; ++b) {
+            double t = (double)f[a * kw + b] * (double)dy[(p * OH + r) * OW + c];
+            int64_t e = (p * H + r * sh + a) * W + c * sw + b;
+            dx[e] += t;
+            if (absmag) absmag[e] += fabs(t);
+          }
+  return 0;
+}
+
+int oracle_conv2d_backward_filter_f32(const float* x, const float* dy, int64_t planes, int64_t H, int64_t W,
+                                      int64_t kh, int64_t kw, int64_t sh, int64_t sw, double* df, double* absmag) {
+  int64_t OH = oracle_out_len(H, kh, sh), OW = oracle_out_len(W, kw, sw);
+  if (x == NULL || dy == NULL || df == NULL || planes < 1 || OH < 0 || OW < 0) return -1;
+  for (int64_t a = 0; a < kh; ++a)
+    for (int64_t b = 0; b < kw; ++b) {
+      double acc = 0.0, mag = 0.0;
+      for (int64_t p = 0; p < planes; ++p)
+        for (int64_t r = 0; r < OH; ++r)
+          for (int64_t c = 0; c < OW; ++c) {
+            double t = (double)dy[(p * OH + r) * OW + c] * (double)x[(p * H + r * sh + a) * W + c * sw + b];
+            acc += t;
+            mag += fabs(t);
+          }
+      df[a * kw + b] = acc;
+      if (absmag) absmag[a * kw + b] = mag;
+    }
+  return 0;
+}
+
 /* Multi-channel 1-D convolution ("with C_in > 1 it becomes a
  * real contraction"): the sliding dot product of Sec. 2.5 summed over input
  * channels, channels-last layout, inputs given as bfloat16 bit patterns

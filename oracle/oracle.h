@@ -135,6 +135,14 @@ int oracle_pool2d_backward_f32(const float* x, const float* dy, int64_t planes, 
 int oracle_conv2d_f32(const float* x, int64_t planes, int64_t H, int64_t W, const float* f,
                       int64_t kh, int64_t kw, int64_t sh, int64_t sw, double* y, double* absmag);
 
+/* Gradients of oracle_conv2d_f32 (reading R21): dx [planes][H][W] (scatter of
+ * f[a][b] dy[p][r][c] to x[p][r*sh+a][c*sw+b]; elements no window covers get 0)
+ * and df [kh][kw] = sum over planes and outputs of dy * x, both in double. */
+int oracle_conv2d_backward_input_f32(const float* dy, int64_t planes, int64_t H, int64_t W, const float* f,
+                                     int64_t kh, int64_t kw, int64_t sh, int64_t sw, double* dx, double* absmag);
+int oracle_conv2d_backward_filter_f32(const float* x, const float* dy, int64_t planes, int64_t H, int64_t W,
+                                      int64_t kh, int64_t kw, int64_t sh, int64_t sw, double* df, double* absmag);
+
 /* Multi-channel 1-D convolution, channels-last, bfloat16 inputs (bit patterns),
  * double result: y[b][i][co] = sum_j sum_ci w[co][ci][j] x[b][i+j][ci]. */
 int oracle_conv1d_mc_bf16(const uint16_t* x, const uint16_t* w, int64_t batch, int64_t N, int64_t cin,
