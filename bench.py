@@ -68,7 +68,7 @@ TC_CONV_K = (33, 64)
 TC_FLOP_PER_OUT = 3 * 192 * 2 if os.environ.get("SS_CONV_TC_MIXED", "1") == "0" else 2 * 192 * 2
 
 
-BWD_OPS = ("conv_bwd_in", "conv_bwd_f", "sum_bwd", "max_bwd", "pool2d_bwd")
+BWD_OPS = ("conv_bwd_in", "conv_bwd_f", "sum_bwd", "max_bwd", "pool2d_bwd", "conv2d_bwd_in", "conv2d_bwd_f")
 
 
 def conv_on_tensor_cores(c) -> bool:
@@ -99,6 +99,7 @@ class Cell:
         self.inp2 = inp2  # second input (affine: v), None otherwise
         self.stride, self.dilation, self.pads, self.pad_mode = stride, dilation, pads, pad_mode
         self.w, self.f, self.kh, self.kw, self.sh, self.sw, self.mode = w, f, kh, kw, sh, sw, mode
+        self.f_flat = None if f is None else [float(v) for v in f.reshape(-1)]  # host taps for 2-D calls
         self.inp = inp  # key of the input tensor it reads
         self.n_out = 0
         self.bytes = 0
@@ -204,6 +205,16 @@ def cfg_cells(workload: str):
             for mode in ("max", "avg"):
                 cells.append(Cell("backward", f"bwd_pool2d_{mode}_{kk}x{kk}_s{st}", "pool2d_bwd", kh=kk, kw=kk, sh=st,
                                   sw=st, mode=mode, inp="x4b", inp2=f"g4_{kk}"))
+        for kk in (3, 7):  # 2-D conv gradients (reading R21) on the config-4 planes
+            oh = 112 - kk + 1
+            if f"g4_{kk}" not in inputs:
+                inputs[f"g4_{kk}"] = dict(images=32, C=64, H=oh, W=oh, dtype="float32", dist="normal", seed=34,
+                                          kw={}, shard="image")
+            f = synth.normal(70 + kk, kk * kk, sigma=1.0 / kk).reshape(kk, kk)
+            cells.append(Cell("backward", f"bwd_conv2d_input_{kk}x{kk}", "conv2d_bwd_in", kh=kk, kw=kk, sh=1, sw=1,
+                              f=f, inp=f"g4_{kk}", inp2="x4b"))
+            cells.append(Cell("backward", f"bwd_conv2d_filter_{kk}x{kk}", "conv2d_bwd_f", kh=kk, kw=kk, sh=1, sw=1,
+                              f=f, inp="x4b", inp2=f"g4_{kk}"))
     if not cells:
         raise SystemExit(f"unknown workload {workload}")
     return inputs, cells
@@ -413,6 +424,23 @@ class Runner:
             c.n_out = x.numel()
             c.bytes = 4 * (x.numel() * (2 if c.mode == "max" else 1) + g.numel())
             return
+        if c.op == "conv2d_bwd_in":  # inp = dy [B, C, OH, OW], inp2 = x (shape only)
+            g, xs = x, self.x[c.inp2]
+            self.y[c.name] = torch.empty_like(xs)
+            c.n_out = xs.numel()
+            c.bytes = 4 * (g.numel() + xs.numel())
+            c.flops = 2 * c.kh * c.kw * g.numel()
+            return
+        if c.op == "conv2d_bwd_f":  # inp = x [B, C, H, W], inp2 = dy
+            g = self.x[c.inp2]
+            self.y[c.name] = torch.empty((c.kh, c.kw), dtype=torch.float32, device=self.device)
+            self.ws = getattr(self, "ws", {})
+            self.ws[c.name] = torch.empty(self.ss.ss_conv2d_backward_filter_workspace(c.kh, c.kw), dtype=torch.uint8,
+                                          device=self.device)
+            c.n_out = g.numel()
+            c.bytes = 4 * (x.numel() + g.numel())
+            c.flops = 2 * c.kh * c.kw * g.numel()
+            return
         if c.op in ("conv_bwd_in", "sum_bwd"):  # inp = dy [rows, L]
             rows, L = x.shape
             N = L + c.w - 1
@@ -445,6 +473,15 @@ class Runner:
             ss.check(ss.ss_pool2d_backward(x.data_ptr(), g.data_ptr(), y.data_ptr(), B * C, H, W, c.kh, c.kw, c.sh,
                                            c.sw, ss.SS_POOL_MAX if c.mode == "max" else ss.SS_POOL_AVG,
                                            ss.SS_F32, st))
+        elif c.op == "conv2d_bwd_in":
+            B, C, H, W = y.shape
+            ss.check(ss.ss_conv2d_backward_input(x.data_ptr(), y.data_ptr(), B * C, H, W, c.f_flat, c.kh, c.kw, 1, 1,
+                                                 ss.SS_F32, st))
+        elif c.op == "conv2d_bwd_f":
+            B, C, H, W = x.shape
+            ws = self.ws[c.name]
+            ss.check(ss.ss_conv2d_backward_filter(x.data_ptr(), self.x[c.inp2].data_ptr(), y.data_ptr(), B * C, H, W,
+                                                  c.kh, c.kw, 1, 1, ws.data_ptr(), ws.numel(), st))
         elif c.op == "conv_bwd_in":
             rows, L = x.shape
             ss.check(ss.ss_conv1d_backward_input(x.data_ptr(), y.data_ptr(), L + c.w - 1, rows, c.f, c.w, 1,
@@ -733,7 +770,7 @@ def run_ours(args):
             d["tc_frac"] = round(c.flops / (avg_ms * 1e-3) / 1e12 / (2 * tf32_peak_tflops()), 4)  # bf16 peak
         elif conv_on_tensor_cores(c):
             d["tc_frac"] = round(c.n_out * TC_FLOP_PER_OUT / (avg_ms * 1e-3) / 1e12 / tf32_peak_tflops(), 4)
-        elif c.op in ("conv", "conv_bwd_in", "conv_bwd_f", "conv2d"):
+        elif c.op in ("conv", "conv_bwd_in", "conv_bwd_f", "conv2d", "conv2d_bwd_in", "conv2d_bwd_f"):
             fma_s = c.flops / 2 / (avg_ms * 1e-3)
             d["fma_frac"] = round(fma_s / FP32_FMA_PEAK, 4)
         cells.append(d)
@@ -742,7 +779,7 @@ def run_ours(args):
         d["share"] = round(d["avg_ms"] / tot_k, 4)
     dom = max(cells, key=lambda d: d["avg_ms"])
     dom_cell = next(c for c in R.cells if c.name == dom["cell"])
-    if dom_cell.op in ("conv", "conv_bwd_in", "conv_bwd_f", "conv2d") and dom.get("fma_frac", 0) > dom["frac_hbm"]:
+    if dom_cell.op in ("conv", "conv_bwd_in", "conv_bwd_f", "conv2d", "conv2d_bwd_in", "conv2d_bwd_f") and dom.get("fma_frac", 0) > dom["frac_hbm"]:
         achieved = dom_cell.flops / (dom["avg_ms"] * 1e-3) / 1e12
         roofline = {"bound": "alu", "kernel": dom["cell"], "achieved": round(achieved, 2),
                     "peak": round(2 * FP32_FMA_PEAK / 1e12, 2), "unit": "TFLOP/s",
@@ -880,6 +917,16 @@ def oracle_sample_plan(workload: str, frac: float):
             m = oracle.POOL2D_MAX if c.mode == "max" else oracle.POOL2D_AVG
             plan.append((c, lambda x=x, g=g, c=c, m=m: (oracle.pool2d_backward(x, g, 112, 112, c.kh, c.kw, c.sh,
                                                                                c.sw, m), x.size)[1]))
+        elif c.cfg == "backward" and c.op in ("conv2d_bwd_in", "conv2d_bwd_f"):
+            planes = max(1, int(round(32 * 64 * frac)))
+            oh = 112 - c.kh + 1
+            x = synth.uniform01(5, planes * 112 * 112).reshape(planes, 112, 112)
+            g = synth.normal(34, planes * oh * oh).reshape(planes, oh, oh)
+            if c.op == "conv2d_bwd_in":
+                fn = (lambda g=g, c=c: (oracle.conv2d_backward_input(g, c.f, 112, 112), planes * 112 * 112)[1])
+            else:
+                fn = (lambda x=x, g=g, c=c: (oracle.conv2d_backward_filter(x, g, c.kh, c.kw), g.size)[1])
+            plan.append((c, fn))
         elif c.cfg == "backward":
             rows = max(1, int(round(64 * frac)))
             n = 1 << 20

@@ -61,7 +61,7 @@
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 7
+#define SS_ABI_VERSION 8
 
 typedef enum { SS_F32 = 0, SS_I32 = 1 } ss_dtype_t;
 typedef enum { SS_POOL_MAX = 0, SS_POOL_AVG = 1 } ss_pool_mode_t;
@@ -215,6 +215,32 @@ ss_status_t ss_affine_window(const float* u, const float* v, float* U, float* V,
 ss_status_t ss_conv2d(const void* x, void* y, int64_t planes, int64_t H, int64_t W,
                       const float* filter_host, int64_t kh, int64_t kw, int64_t sh, int64_t sw,
                       ss_dtype_t dtype, void* stream);
+
+/* Gradients of ss_conv2d (SURVEY 8f NEXT #4 "2-D convolution and backward
+ * passes"; the vector-Jacobian products, reading R21).  Shapes as
+ * ss_conv2d: x / dx [planes][H][W], dy [planes][OH][OW], all DEVICE fp32
+ * (SS_F32 only), 4-byte aligned, dx / df must not overlap an input.
+ *   ss_conv2d_backward_input   dx[p][h][w] = sum over windows (r, c) and taps
+ *                              (a, b) with r*sh + a = h, c*sw + b = w of
+ *                              filter[a*kw + b] * dy[p][r][c]; elements no
+ *                              window covers are written 0.  filter_host: HOST,
+ *                              kh*kw <= SS_K_MAX floats, read before return.
+ *   ss_conv2d_backward_filter  df[a*kw + b] = sum_p sum_r sum_c dy[p][r][c] *
+ *                              x[p][r*sh + a][c*sw + b]  (df: DEVICE, kh*kw
+ *                              floats; fp32 products summed in fp32 runs of one
+ *                              tile, then fp64, deterministic).  `workspace`
+ *                              (DEVICE, caller-owned, >= ss_conv2d_backward_
+ *                              filter_workspace(kh, kw) bytes on the current
+ *                              device) holds per-CTA fp64 partials.
+ * Accuracy: |g - g_exact| <= 1e-5 * sum of |term| + 1e-6 per element (BJ bound).
+ * Statuses as ss_conv2d; a short workspace -> SS_ERR_BAD_SIZE. */
+ss_status_t ss_conv2d_backward_input(const void* dy, void* dx, int64_t planes, int64_t H, int64_t W,
+                                     const float* filter_host, int64_t kh, int64_t kw, int64_t sh,
+                                     int64_t sw, ss_dtype_t dtype, void* stream);
+size_t ss_conv2d_backward_filter_workspace(int64_t kh, int64_t kw);
+ss_status_t ss_conv2d_backward_filter(const void* x, const void* dy, float* df, int64_t planes, int64_t H,
+                                      int64_t W, int64_t kh, int64_t kw, int64_t sh, int64_t sw,
+                                      void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- multi-channel convolution (a real contraction) -------
  * y[b][i][co] = sum_{j<k} sum_{ci<cin} w[co][ci][j] * x[b][i+j][ci],  i < N-k+1

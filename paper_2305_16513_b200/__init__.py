@@ -44,7 +44,8 @@ EXPORTED = ("ss_abi_version", "ss_out_len", "ss_pool_sum", "ss_pool_max", "ss_po
             "ss_out_len_ex", "ss_pool_sum_ex", "ss_pool_max_ex", "ss_pool_min_ex", "ss_conv1d_ex",
             "ss_affine_window", "ss_pool_sum_backward", "ss_pool_max_backward",
             "ss_conv1d_backward_input", "ss_conv1d_backward_filter_workspace", "ss_conv1d_backward_filter",
-            "ss_pool2d_backward", "ss_conv2d", "ss_conv1d_mc")
+            "ss_pool2d_backward", "ss_conv2d", "ss_conv2d_backward_input", "ss_conv2d_backward_filter_workspace",
+            "ss_conv2d_backward_filter", "ss_conv1d_mc")
 
 
 class SSError(RuntimeError):
@@ -97,6 +98,13 @@ def _load() -> ctypes.CDLL:
     L.ss_conv1d_mc.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, vp]
     L.ss_conv1d_mc.restype = i32
     L.ss_conv2d.restype = i32
+    L.ss_conv2d_backward_input.argtypes = [vp, vp, i64, i64, i64, ctypes.POINTER(ctypes.c_float), i64, i64, i64, i64,
+                                           i32, vp]
+    L.ss_conv2d_backward_input.restype = i32
+    L.ss_conv2d_backward_filter_workspace.argtypes = [i64, i64]
+    L.ss_conv2d_backward_filter_workspace.restype = ctypes.c_size_t
+    L.ss_conv2d_backward_filter.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, ctypes.c_size_t, vp]
+    L.ss_conv2d_backward_filter.restype = i32
     L.ss_status_string.argtypes = [i32]
     L.ss_status_string.restype = ctypes.c_char_p
     L.ss_last_error.argtypes = []
@@ -222,6 +230,21 @@ def ss_pool2d_backward(x_ptr, dy_ptr, dx_ptr, planes, H, W, kh, kw, sh, sw, mode
 def ss_conv2d(x_ptr, y_ptr, planes, H, W, filter_host, kh, kw, sh=1, sw=1, dtype=SS_F32, stream=0) -> int:
     fp = None if filter_host is None else (ctypes.c_float * len(filter_host))(*[float(v) for v in filter_host])
     return _lib.ss_conv2d(x_ptr, y_ptr, planes, H, W, fp, kh, kw, sh, sw, dtype, stream)
+
+
+def ss_conv2d_backward_input(dy_ptr, dx_ptr, planes, H, W, filter_host, kh, kw, sh=1, sw=1, dtype=SS_F32,
+                             stream=0) -> int:
+    fp = None if filter_host is None else (ctypes.c_float * len(filter_host))(*[float(v) for v in filter_host])
+    return _lib.ss_conv2d_backward_input(dy_ptr, dx_ptr, planes, H, W, fp, kh, kw, sh, sw, dtype, stream)
+
+
+def ss_conv2d_backward_filter_workspace(kh: int, kw: int) -> int:
+    return int(_lib.ss_conv2d_backward_filter_workspace(kh, kw))
+
+
+def ss_conv2d_backward_filter(x_ptr, dy_ptr, df_ptr, planes, H, W, kh, kw, sh, sw, ws_ptr, ws_bytes, stream=0) -> int:
+    return _lib.ss_conv2d_backward_filter(x_ptr, dy_ptr, df_ptr, planes, H, W, kh, kw, sh, sw, ws_ptr, ws_bytes,
+                                          stream)
 
 
 def ss_conv1d_mc(x_ptr, w_ptr, y_ptr, batch, N, cin, cout, k, stream=0) -> int:
@@ -449,6 +472,36 @@ def conv1d_backward_filter(x, dy, k: int, stride: int = 1, out=None, workspace=N
     if workspace is None or workspace.numel() * workspace.element_size() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
     check(ss_conv1d_backward_filter(x.data_ptr(), dy.data_ptr(), df.data_ptr(), N, B, k, stride,
+                                    workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+                                    _stream(stream)))
+    return df
+
+
+def conv2d_backward_input(dy, filt, H: int, W: int, stride=(1, 1), out=None, stream=None):
+    """dx of conv2d for a CUDA fp32 dy [..., OH, OW] and a host filter [kh, kw]: [..., H, W]."""
+    torch = _torch()
+    f = filt.tolist() if hasattr(filt, "tolist") else [list(r) for r in filt]
+    kh, kw = len(f), len(f[0])
+    sh, sw = stride
+    planes = dy.numel() // (dy.shape[-2] * dy.shape[-1])
+    dx = torch.empty(tuple(dy.shape[:-2]) + (H, W), dtype=torch.float32, device=dy.device) if out is None else out
+    check(ss_conv2d_backward_input(dy.data_ptr(), dx.data_ptr(), planes, H, W, [float(v) for r in f for v in r],
+                                   kh, kw, sh, sw, _dtype_code(dy), _stream(stream)))
+    return dx
+
+
+def conv2d_backward_filter(x, dy, kernel, stride=(1, 1), out=None, workspace=None, stream=None):
+    """df [kh, kw] of conv2d: sum over planes and outputs of dy * the shifted x (device tensor)."""
+    torch = _torch()
+    kh, kw = kernel
+    sh, sw = stride
+    H, W = x.shape[-2], x.shape[-1]
+    planes = x.numel() // (H * W)
+    df = torch.empty((kh, kw), dtype=torch.float32, device=x.device) if out is None else out
+    need = ss_conv2d_backward_filter_workspace(kh, kw)
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.empty(max(need, 8), dtype=torch.uint8, device=x.device)
+    check(ss_conv2d_backward_filter(x.data_ptr(), dy.data_ptr(), df.data_ptr(), planes, H, W, kh, kw, sh, sw,
                                     workspace.data_ptr(), workspace.numel() * workspace.element_size(),
                                     _stream(stream)))
     return df

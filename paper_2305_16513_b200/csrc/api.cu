@@ -605,6 +605,68 @@ static ss_status_t pool2d_backward_impl(const void* x, const void* dy, void* dx,
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "pool2d_backward launch");
 }
 
+static ss_status_t conv2d_bwd_check(int64_t planes, int64_t H, int64_t W, int64_t kh, int64_t kw, int64_t sh,
+                                     int64_t sw) {
+  if (planes < 1 || H < 1 || W < 1 || kh < 1 || kw < 1 || sh < 1 || sw < 1)
+    return fail(SS_ERR_BAD_SIZE, "planes/H/W/kh/kw/sh/sw must be >= 1");
+  if (H > INT64_MAX / 8 / W || H * W > INT64_MAX / 8 / planes) return fail(SS_ERR_BAD_SIZE, "sizes overflow int64");
+  if (kh > H || kw > W) return fail(SS_ERR_WINDOW_EXCEEDS_INPUT, "window exceeds input: %lldx%lld > %lldx%lld",
+                                    (long long)kh, (long long)kw, (long long)H, (long long)W);
+  if (kh * kw > SS_K_MAX) return fail(SS_ERR_UNSUPPORTED, "kh*kw=%lld > SS_K_MAX=%d", (long long)(kh * kw), SS_K_MAX);
+  return SS_OK;
+}
+
+ss_status_t ss_conv2d_backward_input(const void* dy, void* dx, int64_t planes, int64_t H, int64_t W,
+                                     const float* filter_host, int64_t kh, int64_t kw, int64_t sh, int64_t sw,
+                                     ss_dtype_t dtype, void* stream) {
+  if (!dy || !dx || !filter_host) return fail(SS_ERR_NULL, "dy, dx and filter_host must be non-NULL");
+  ss_status_t st = conv2d_bwd_check(planes, H, W, kh, kw, sh, sw);
+  if (st != SS_OK) return st;
+  if (dtype != SS_F32) return fail(SS_ERR_UNSUPPORTED, "conv2d backward supports SS_F32 only");
+  if ((reinterpret_cast<uintptr_t>(dy) & 3) || (reinterpret_cast<uintptr_t>(dx) & 3))
+    return fail(SS_ERR_BAD_SIZE, "dy and dx must be 4-byte aligned");
+  Conv2DBwdParams p;
+  memset(&p, 0, sizeof p);
+  p.dy = static_cast<const float*>(dy); p.dx = static_cast<float*>(dx);
+  p.planes = planes; p.H = H; p.W = W; p.kh = kh; p.kw = kw; p.sh = sh; p.sw = sw;
+  p.OH = (H - kh) / sh + 1; p.OW = (W - kw) / sw + 1;
+  if (overlaps(dy, planes * p.OH * p.OW * 4, dx, planes * H * W * 4)) return fail(SS_ERR_OVERLAP, "dx overlaps dy");
+  for (int64_t t = 0; t < kh * kw; ++t) p.taps[t] = filter_host[t];
+  cudaError_t e = launch_conv2d_backward_input(p, static_cast<cudaStream_t>(stream), current_sms());
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv2d_backward_input launch");
+}
+
+size_t ss_conv2d_backward_filter_workspace(int64_t kh, int64_t kw) {
+  if (kh < 1 || kw < 1 || kh * kw > SS_K_MAX) return 0;
+  return conv2d_backward_filter_workspace(kh * kw, conv2d_backward_filter_ctas(current_sms()));
+}
+
+ss_status_t ss_conv2d_backward_filter(const void* x, const void* dy, float* df, int64_t planes, int64_t H, int64_t W,
+                                      int64_t kh, int64_t kw, int64_t sh, int64_t sw, void* workspace,
+                                      size_t workspace_bytes, void* stream) {
+  if (!x || !dy || !df || !workspace) return fail(SS_ERR_NULL, "x, dy, df and workspace must be non-NULL");
+  ss_status_t st = conv2d_bwd_check(planes, H, W, kh, kw, sh, sw);
+  if (st != SS_OK) return st;
+  if ((reinterpret_cast<uintptr_t>(x) & 3) || (reinterpret_cast<uintptr_t>(dy) & 3) ||
+      (reinterpret_cast<uintptr_t>(df) & 3) || (reinterpret_cast<uintptr_t>(workspace) & 7))
+    return fail(SS_ERR_BAD_SIZE, "x, dy, df must be 4-byte and workspace 8-byte aligned");
+  const int ctas = conv2d_backward_filter_ctas(current_sms());
+  const size_t need = conv2d_backward_filter_workspace(kh * kw, ctas);
+  if (workspace_bytes < need)
+    return fail(SS_ERR_BAD_SIZE, "workspace of %zu bytes needed (ss_conv2d_backward_filter_workspace)", need);
+  Conv2DBwdParams p;
+  memset(&p, 0, sizeof p);
+  p.x = static_cast<const float*>(x); p.dy = static_cast<const float*>(dy);
+  p.planes = planes; p.H = H; p.W = W; p.kh = kh; p.kw = kw; p.sh = sh; p.sw = sw;
+  p.OH = (H - kh) / sh + 1; p.OW = (W - kw) / sw + 1;
+  const int64_t nx = planes * H * W * 4, ny = planes * p.OH * p.OW * 4, nw = (int64_t)need, nf = kh * kw * 4;
+  if (overlaps(workspace, nw, x, nx) || overlaps(workspace, nw, dy, ny) || overlaps(workspace, nw, df, nf) ||
+      overlaps(df, nf, x, nx) || overlaps(df, nf, dy, ny))
+    return fail(SS_ERR_OVERLAP, "df / workspace overlap an input");
+  cudaError_t e = launch_conv2d_backward_filter(p, df, workspace, ctas, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv2d_backward_filter launch");
+}
+
 ss_status_t ss_conv1d_mc(const void* x, const void* w, float* y, int64_t batch, int64_t N, int64_t cin,
                          int64_t cout, int64_t k, void* stream) {
   if (!x || !w || !y) return fail(SS_ERR_NULL, "x, w and y must be non-NULL device pointers");

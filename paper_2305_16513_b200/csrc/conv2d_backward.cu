@@ -1,0 +1,349 @@
+// conv2d_backward.cu -- gradients of the 2-D sliding dot product (SURVEY 8f
+// NEXT #4 "2-D convolution and backward passes"; reading R21), the
+// vector-Jacobian products of y[p][r][c] = sum_a sum_b f[a][b] x[p][r sh+a][c sw+b]:
+//
+//   dx[p][h][w] = sum over (r, c, a, b) with r sh + a = h, c sw + b = w of f[a][b] dy[p][r][c]
+//   df[a][b]    = sum_p sum_r sum_c dy[p][r][c] x[p][r sh+a][c sw+b]
+//
+// Input gradient (gather form, no atomics): a CTA owns an 8 x 128 dx tile; the
+// dy region every window over that tile reads is staged in shared memory with
+// zeros outside [0, OH) x [0, OW) (so uncovered dx elements come out 0 and the
+// inner loops carry no bounds checks), lane t owns columns t, t+32, t+64, t+96
+// (conflict-free LDS), taps in shared memory (warp-broadcast).
+//
+// Filter gradient: a CTA walks (plane, 16-row, 128-column) dy tiles; it stages
+// the dy tile and the x region under it.  kh, kw <= 4: every thread keeps all
+// taps' sums for its columns in registers (one LDS of x per FMA, dy read once
+// per tap set), fp32 runs of one tile flushed into fp64 registers; larger
+// filters: a warp per tap (fp32 run per tile, fp64 accumulator in shared
+// memory).  Per-CTA fp64 partials go to the caller's workspace and a finishing
+// kernel sums them in CTA order (deterministic).  Regions too large for
+// shared memory take direct kernels reading global memory.
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "ss_device.cuh"
+#include "ss_internal.h"
+
+namespace ss {
+
+namespace {
+
+constexpr int kC2bThreads = 256;
+constexpr int kDxTileH = 8, kDxTileW = 128;
+constexpr int kDfTileR = 16, kDfTileC = 128;
+constexpr size_t kC2bSmemMax = 96 * 1024;
+
+__device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+__device__ __forceinline__ int64_t ceildiv(int64_t a, int64_t b) { return -floordiv(-a, b); }
+
+// ------------------------------------------------------------ input gradient
+template <bool kS1>
+__global__ void __launch_bounds__(kC2bThreads) conv2d_bwd_input_tile_kernel(const __grid_constant__ Conv2DBwdParams p) {
+  extern __shared__ __align__(16) float c2b_smem[];
+  const int nt = (int)(p.kh * p.kw);
+  float* fs = c2b_smem;
+  float* ds = c2b_smem + ((nt + 3) & ~3);
+  for (int t = threadIdx.x; t < nt; t += kC2bThreads) fs[t] = p.taps[t];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tiles_h = (p.H + kDxTileH - 1) / kDxTileH, tiles_w = (p.W + kDxTileW - 1) / kDxTileW;
+  const int64_t ntiles = p.planes * tiles_h * tiles_w;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t tw = tile % tiles_w, rest = tile / tiles_w, th = rest % tiles_h, pl = rest / tiles_h;
+    const int64_t h0 = th * kDxTileH, w0 = tw * kDxTileW;
+    const int64_t r_lo = ceildiv(h0 - p.kh + 1, p.sh), r_hi = floordiv(h0 + kDxTileH - 1, p.sh);
+    const int64_t c_lo = ceildiv(w0 - p.kw + 1, p.sw), c_hi = floordiv(w0 + kDxTileW - 1, p.sw);
+    const int R = (int)(r_hi - r_lo + 1), C = (int)(c_hi - c_lo + 1);
+    const float* __restrict__ g = p.dy + pl * p.OH * p.OW;
+    __syncthreads();  // the previous tile's readers are done with ds
+    for (int i = threadIdx.x; i < R * C; i += kC2bThreads) {
+      const int rr = i / C, cc = i - rr * C;
+      const int64_t r = r_lo + rr, c = c_lo + cc;
+      ds[i] = (r >= 0 && r < p.OH && c >= 0 && c < p.OW) ? __ldg(g + r * p.OW + c) : 0.0f;
+    }
+    __syncthreads();
+    const int64_t h = h0 + warp;
+    if (h >= p.H) continue;
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    if (kS1) {
+      // r = h - a, c = w - b; smem column of output q, tap b: (lane + 32 q) + kw - 1 - b
+      for (int a = 0; a < (int)p.kh; ++a) {
+        const float* row = ds + (int)(h - a - r_lo) * C + lane + (int)p.kw - 1;
+        const float* fa = fs + a * (int)p.kw;
+        for (int b = 0; b < (int)p.kw; ++b) {
+          const float fv = fa[b];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] = __fmaf_rn(fv, row[32 * q - b], acc[q]);
+        }
+      }
+    } else {
+      const int64_t rmin = ceildiv(h - p.kh + 1, p.sh), rmax = floordiv(h, p.sh);
+      for (int64_t r = rmin; r <= rmax; ++r) {
+        const int a = (int)(h - r * p.sh);
+        const float* row = ds + (int)(r - r_lo) * C;
+        const float* fa = fs + a * (int)p.kw;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t w = w0 + lane + 32 * q;
+          const int64_t cmin = ceildiv(w - p.kw + 1, p.sw), cmax = floordiv(w, p.sw);
+          float s = acc[q];
+          for (int64_t c = cmin; c <= cmax; ++c) s = __fmaf_rn(fa[w - c * p.sw], row[c - c_lo], s);
+          acc[q] = s;
+        }
+      }
+    }
+    float* __restrict__ out = p.dx + (pl * p.H + h) * p.W;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t w = w0 + lane + 32 * q;
+      if (w < p.W) out[w] = acc[q];
+    }
+  }
+}
+
+// Direct gather (any size): one dx element per thread, dy through the read-only path.
+__global__ void __launch_bounds__(kC2bThreads) conv2d_bwd_input_direct_kernel(const __grid_constant__ Conv2DBwdParams p) {
+  const int64_t total = p.planes * p.H * p.W;
+  for (int64_t e = blockIdx.x * (int64_t)kC2bThreads + threadIdx.x; e < total; e += (int64_t)gridDim.x * kC2bThreads) {
+    const int64_t w = e % p.W, rest = e / p.W, h = rest % p.H, pl = rest / p.H;
+    const float* __restrict__ g = p.dy + pl * p.OH * p.OW;
+    int64_t rmin = ceildiv(h - p.kh + 1, p.sh), rmax = floordiv(h, p.sh);
+    int64_t cmin = ceildiv(w - p.kw + 1, p.sw), cmax = floordiv(w, p.sw);
+    if (rmin < 0) rmin = 0;
+    if (cmin < 0) cmin = 0;
+    if (rmax > p.OH - 1) rmax = p.OH - 1;
+    if (cmax > p.OW - 1) cmax = p.OW - 1;
+    float s = 0.0f;
+    for (int64_t r = rmin; r <= rmax; ++r) {
+      const int64_t a = h - r * p.sh;
+      for (int64_t c = cmin; c <= cmax; ++c) s = __fmaf_rn(p.taps[a * p.kw + (w - c * p.sw)], __ldg(g + r * p.OW + c), s);
+    }
+    p.dx[e] = s;
+  }
+}
+
+// ----------------------------------------------------------- filter gradient
+struct DfTile {
+  int64_t pl, r0, c0;
+  int nr, nc;
+};
+
+__device__ __forceinline__ DfTile df_tile(const Conv2DBwdParams& p, int64_t tile) {
+  const int64_t tiles_r = (p.OH + kDfTileR - 1) / kDfTileR, tiles_c = (p.OW + kDfTileC - 1) / kDfTileC;
+  DfTile t;
+  const int64_t tc = tile % tiles_c, rest = tile / tiles_c, tr = rest % tiles_r;
+  t.pl = rest / tiles_r;
+  t.r0 = tr * kDfTileR;
+  t.c0 = tc * kDfTileC;
+  t.nr = (int)min((int64_t)kDfTileR, p.OH - t.r0);
+  t.nc = (int)min((int64_t)kDfTileC, p.OW - t.c0);
+  return t;
+}
+
+// Stage dy[tile] into dys[kDfTileR][kDfTileC] and the x region under it into xs[XR][XC]
+// (zeros outside the tile, so padded lanes contribute 0 * 0).
+__device__ __forceinline__ void df_stage(const Conv2DBwdParams& p, const DfTile& t, float* dys, float* xs) {
+  const float* __restrict__ g = p.dy + (t.pl * p.OH + t.r0) * p.OW + t.c0;
+  for (int i = threadIdx.x; i < kDfTileR * kDfTileC; i += kC2bThreads) {
+    const int rr = i / kDfTileC, cc = i - rr * kDfTileC;
+    dys[i] = (rr < t.nr && cc < t.nc) ? __ldg(g + rr * p.OW + cc) : 0.0f;
+  }
+  const int xr = (t.nr - 1) * (int)p.sh + (int)p.kh, xc = (t.nc - 1) * (int)p.sw + (int)p.kw;
+  const float* __restrict__ xg = p.x + (t.pl * p.H + t.r0 * p.sh) * p.W + t.c0 * p.sw;
+  for (int i = threadIdx.x; i < p.df_xr * p.df_xc; i += kC2bThreads) {
+    const int rr = i / p.df_xc, cc = i - rr * p.df_xc;
+    xs[i] = (rr < xr && cc < xc) ? __ldg(xg + rr * p.W + cc) : 0.0f;
+  }
+}
+
+// kh <= KHM, kw <= KWM: all taps of a thread's columns in registers.
+template <int KHM, int KWM>
+__global__ void __launch_bounds__(kC2bThreads) conv2d_bwd_filter_reg_kernel(const __grid_constant__ Conv2DBwdParams p,
+                                                                            double* __restrict__ part) {
+  extern __shared__ __align__(16) float c2b_smem[];
+  float* dys = c2b_smem;
+  float* xs = dys + kDfTileR * kDfTileC;
+  __shared__ double red[kC2bThreads / 32][KHM * KWM];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kh = (int)p.kh, kw = (int)p.kw, sh = (int)p.sh, sw = (int)p.sw, XC = p.df_xc;
+  double d[KHM * KWM];
+#pragma unroll
+  for (int t = 0; t < KHM * KWM; ++t) d[t] = 0.0;
+  const int64_t ntiles = p.planes * ((p.OH + kDfTileR - 1) / kDfTileR) * ((p.OW + kDfTileC - 1) / kDfTileC);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const DfTile t = df_tile(p, tile);
+    __syncthreads();
+    df_stage(p, t, dys, xs);
+    __syncthreads();
+    float s[KHM * KWM];
+#pragma unroll
+    for (int i = 0; i < KHM * KWM; ++i) s[i] = 0.0f;
+    for (int rr = warp; rr < t.nr; rr += kC2bThreads / 32) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = lane + 32 * q;
+        const float dyv = dys[rr * kDfTileC + c];
+        const float* xb = xs + rr * sh * XC + c * sw;
+#pragma unroll
+        for (int a = 0; a < KHM; ++a) {
+          if (a < kh) {
+#pragma unroll
+            for (int b = 0; b < KWM; ++b)
+              if (b < kw) s[a * KWM + b] = __fmaf_rn(dyv, xb[a * XC + b], s[a * KWM + b]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < KHM * KWM; ++i) d[i] += (double)s[i];
+  }
+#pragma unroll
+  for (int i = 0; i < KHM * KWM; ++i) {
+    double v = d[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < KHM * KWM) {
+    const int a = threadIdx.x / KWM, b = threadIdx.x - a * KWM;
+    if (a < kh && b < kw) {
+      double v = 0.0;
+      for (int w = 0; w < kC2bThreads / 32; ++w) v += red[w][threadIdx.x];
+      part[(int64_t)(a * kw + b) * gridDim.x + blockIdx.x] = v;
+    }
+  }
+}
+
+// Any filter whose tile region fits: a warp per tap, fp64 accumulator per tap in shared memory.
+__global__ void __launch_bounds__(kC2bThreads) conv2d_bwd_filter_tap_kernel(const __grid_constant__ Conv2DBwdParams p,
+                                                                            double* __restrict__ part) {
+  extern __shared__ __align__(16) float c2b_smem[];
+  const int nt = (int)(p.kh * p.kw);
+  double* acc = reinterpret_cast<double*>(c2b_smem);
+  float* dys = c2b_smem + 2 * ((nt + 3) & ~3);
+  float* xs = dys + kDfTileR * kDfTileC;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kw = (int)p.kw, sh = (int)p.sh, sw = (int)p.sw, XC = p.df_xc;
+  for (int t = threadIdx.x; t < nt; t += kC2bThreads) acc[t] = 0.0;
+  const int64_t ntiles = p.planes * ((p.OH + kDfTileR - 1) / kDfTileR) * ((p.OW + kDfTileC - 1) / kDfTileC);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const DfTile t = df_tile(p, tile);
+    __syncthreads();
+    df_stage(p, t, dys, xs);
+    __syncthreads();
+    for (int tap = warp; tap < nt; tap += kC2bThreads / 32) {
+      const int a = tap / kw, b = tap - a * kw;
+      float s = 0.0f;
+      for (int rr = 0; rr < t.nr; ++rr) {
+        const float* xb = xs + (rr * sh + a) * XC + b;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = lane + 32 * q;
+          s = __fmaf_rn(dys[rr * kDfTileC + c], xb[c * sw], s);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) acc[tap] += (double)s;  // this warp alone owns tap
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nt; t += kC2bThreads) part[(int64_t)t * gridDim.x + blockIdx.x] = acc[t];
+}
+
+// Direct (any size): blockIdx.y = tap, grid-stride over dy elements, fp32 runs of 16 into fp64.
+__global__ void __launch_bounds__(kC2bThreads) conv2d_bwd_filter_direct_kernel(const __grid_constant__ Conv2DBwdParams p,
+                                                                               double* __restrict__ part) {
+  __shared__ double red[kC2bThreads];
+  const int64_t tap = blockIdx.y, a = tap / p.kw, b = tap - a * p.kw;
+  const int64_t total = p.planes * p.OH * p.OW, step = (int64_t)gridDim.x * kC2bThreads;
+  double acc64 = 0.0;
+  int64_t e = blockIdx.x * (int64_t)kC2bThreads + threadIdx.x;
+  while (e < total) {
+    float s = 0.0f;
+    for (int n = 0; n < 16 && e < total; ++n, e += step) {
+      const int64_t c = e % p.OW, rest = e / p.OW, r = rest % p.OH, pl = rest / p.OH;
+      s = __fmaf_rn(__ldg(p.dy + e), __ldg(p.x + (pl * p.H + r * p.sh + a) * p.W + c * p.sw + b), s);
+    }
+    acc64 += (double)s;
+  }
+  red[threadIdx.x] = acc64;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int t = 0; t < kC2bThreads; ++t) v += red[t];
+    part[tap * gridDim.x + blockIdx.x] = v;
+  }
+}
+
+__global__ void conv2d_bwd_filter_finish(const double* __restrict__ part, int ctas, int64_t nt, float* __restrict__ df) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  double v = 0.0;
+  for (int c = 0; c < ctas; ++c) v += part[t * ctas + c];
+  df[t] = (float)v;
+}
+
+size_t dx_smem(const Conv2DBwdParams& p) {
+  const int64_t R = (kDxTileH - 1 + p.kh - 1) / p.sh + 2, C = (kDxTileW - 1 + p.kw - 1) / p.sw + 2;
+  return (size_t)(((p.kh * p.kw + 3) & ~3) + R * C) * sizeof(float);
+}
+
+}  // namespace
+
+int conv2d_backward_filter_ctas(int sms) { return 2 * sms; }
+
+size_t conv2d_backward_filter_workspace(int64_t taps, int ctas) { return (size_t)taps * ctas * sizeof(double); }
+
+cudaError_t launch_conv2d_backward_input(Conv2DBwdParams& p, cudaStream_t stream, int sms) {
+  const size_t smem = dx_smem(p);
+  const int64_t ntiles = p.planes * ((p.H + kDxTileH - 1) / kDxTileH) * ((p.W + kDxTileW - 1) / kDxTileW);
+  if (smem <= kC2bSmemMax) {
+    auto kfn = (p.sh == 1 && p.sw == 1) ? conv2d_bwd_input_tile_kernel<true> : conv2d_bwd_input_tile_kernel<false>;
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kC2bThreads, smem);
+    if (e != cudaSuccess) return e;
+    const int64_t grid = min(ntiles, (int64_t)sms * (per_sm > 0 ? per_sm : 1));
+    kfn<<<(unsigned)grid, kC2bThreads, smem, stream>>>(p);
+  } else {
+    const int64_t total = p.planes * p.H * p.W;
+    const int64_t grid = min((total + kC2bThreads - 1) / kC2bThreads, (int64_t)sms * 8);
+    conv2d_bwd_input_direct_kernel<<<(unsigned)grid, kC2bThreads, 0, stream>>>(p);
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv2d_backward_filter(Conv2DBwdParams& p, float* df, void* workspace, int ctas,
+                                          cudaStream_t stream) {
+  double* part = static_cast<double*>(workspace);
+  const int64_t nt = p.kh * p.kw;
+  p.df_xr = (int)((kDfTileR - 1) * p.sh + p.kh);
+  p.df_xc = (int)((kDfTileC - 1) * p.sw + p.kw);
+  const size_t tile_bytes = ((size_t)kDfTileR * kDfTileC + (size_t)p.df_xr * p.df_xc) * sizeof(float);
+  const int64_t ntiles = p.planes * ((p.OH + kDfTileR - 1) / kDfTileR) * ((p.OW + kDfTileC - 1) / kDfTileC);
+  const int grid = (int)min((int64_t)ctas, ntiles);
+  cudaError_t e = cudaSuccess;
+  if (p.kh <= 4 && p.kw <= 4 && tile_bytes <= kC2bSmemMax) {
+    auto kfn = (p.kh == 3 && p.kw == 3) ? conv2d_bwd_filter_reg_kernel<3, 3> : conv2d_bwd_filter_reg_kernel<4, 4>;
+    e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
+    if (e == cudaSuccess) kfn<<<(unsigned)grid, kC2bThreads, tile_bytes, stream>>>(p, part);
+  } else if (tile_bytes + (size_t)((nt + 3) & ~3) * sizeof(double) <= kC2bSmemMax) {
+    const size_t smem = tile_bytes + (size_t)((nt + 3) & ~3) * sizeof(double);
+    e = ensure_smem_attr(reinterpret_cast<const void*>(conv2d_bwd_filter_tap_kernel));
+    if (e == cudaSuccess) conv2d_bwd_filter_tap_kernel<<<(unsigned)grid, kC2bThreads, smem, stream>>>(p, part);
+  } else {
+    conv2d_bwd_filter_direct_kernel<<<dim3((unsigned)grid, (unsigned)nt), kC2bThreads, 0, stream>>>(p, part);
+  }
+  if (e != cudaSuccess) return e;
+  note_launch();
+  conv2d_bwd_filter_finish<<<(unsigned)((nt + 127) / 128), 128, 0, stream>>>(part, grid, nt, df);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace ss

@@ -179,6 +179,21 @@ struct Conv2DParams {
 };
 cudaError_t launch_conv2d(Conv2DParams& p, cudaStream_t stream, int grid);
 
+// Gradients of the 2-D conv (conv2d_backward.cu, reading R21).
+struct Conv2DBwdParams {
+  const float* x;   // filter gradient
+  const float* dy;
+  float* dx;        // input gradient
+  int64_t planes, H, W, OH, OW, kh, kw, sh, sw;
+  int df_xr, df_xc;  // filter-gradient x region pitch (set by the launcher)
+  float taps[1024];  // input gradient: row-major [kh][kw]
+};
+cudaError_t launch_conv2d_backward_input(Conv2DBwdParams& p, cudaStream_t stream, int sms);
+int conv2d_backward_filter_ctas(int sms);
+size_t conv2d_backward_filter_workspace(int64_t taps, int ctas);
+cudaError_t launch_conv2d_backward_filter(Conv2DBwdParams& p, float* df, void* workspace, int ctas,
+                                          cudaStream_t stream);
+
 // Multi-channel conv1d, channels-last bf16 (conv_mc.cu).
 struct alignas(64) ConvMcParams {
   CUtensorMap tm_x;  // 3-D {64, batch*N, cin/64}, strides {cin*2 B, 128 B}, box {64, 136, cin/64}, SW128, bf16
