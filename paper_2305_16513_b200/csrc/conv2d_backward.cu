@@ -31,7 +31,7 @@ namespace ss {
 namespace {
 
 constexpr int kC2bThreads = 256;
-constexpr int kDxTileH = 8, kDxTileW = 128;
+constexpr int kDxTileH = 32, kDxTileW = 128;
 constexpr int kDfTileR = 16, kDfTileC = 128;
 constexpr size_t kC2bSmemMax = 96 * 1024;
 
@@ -39,7 +39,8 @@ __device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) { return a >= 
 __device__ __forceinline__ int64_t ceildiv(int64_t a, int64_t b) { return -floordiv(-a, b); }
 
 // ------------------------------------------------------------ input gradient
-template <bool kS1>
+// kS1: stride 1 (KH, KW > 0: that exact filter size, loops unrolled; 0: runtime).
+template <bool kS1, int KH, int KW>
 __global__ void __launch_bounds__(kC2bThreads) conv2d_bwd_input_tile_kernel(const __grid_constant__ Conv2DBwdParams p) {
   extern __shared__ __align__(16) float c2b_smem[];
   const int nt = (int)(p.kh * p.kw);
@@ -47,58 +48,87 @@ __global__ void __launch_bounds__(kC2bThreads) conv2d_bwd_input_tile_kernel(cons
   float* ds = c2b_smem + ((nt + 3) & ~3);
   for (int t = threadIdx.x; t < nt; t += kC2bThreads) fs[t] = p.taps[t];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kh = KH > 0 ? KH : (int)p.kh, kw = KW > 0 ? KW : (int)p.kw;
   const int64_t tiles_h = (p.H + kDxTileH - 1) / kDxTileH, tiles_w = (p.W + kDxTileW - 1) / kDxTileW;
   const int64_t ntiles = p.planes * tiles_h * tiles_w;
+  const int C = p.dx_c, buf_elems = p.dx_r * p.dx_c;
+  // stage tile `tl`'s dy region into buffer `bf` with cp.async (zero-filled outside dy)
+  auto stage = [&](int64_t tl, int bf) {
+    const int64_t tw = tl % tiles_w, rest = tl / tiles_w, th = rest % tiles_h, pl = rest / tiles_h;
+    const int64_t h0 = th * kDxTileH, w0 = tw * kDxTileW;
+    const int64_t r_lo = ceildiv(h0 - kh + 1, p.sh), r_hi = floordiv(h0 + kDxTileH - 1, p.sh);
+    const int64_t c_lo = ceildiv(w0 - kw + 1, p.sw), c_hi = floordiv(w0 + kDxTileW - 1, p.sw);
+    const int R = (int)(r_hi - r_lo + 1), Cn = (int)(c_hi - c_lo + 1);
+    const float* __restrict__ g = p.dy + pl * p.OH * p.OW;
+    const uint32_t sb = smem_u32(ds + bf * buf_elems);
+    for (int rr = warp; rr < R; rr += kC2bThreads / 32) {
+      const int64_t r = r_lo + rr;
+      const bool row_ok = r >= 0 && r < p.OH;
+      for (int cc = lane; cc < Cn; cc += 32) {
+        const int64_t c = c_lo + cc;
+        const bool ok = row_ok && c >= 0 && c < p.OW;
+        cp_async4(sb + 4u * (uint32_t)(rr * C + cc), ok ? (const void*)(g + r * p.OW + c) : (const void*)g, ok ? 4u : 0u);
+      }
+    }
+  };
+  if ((int64_t)blockIdx.x < ntiles) stage(blockIdx.x, 0);
+  cp_async_commit();
+  int buf = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (tile + gridDim.x < ntiles) stage(tile + gridDim.x, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();  // tile's region (and, first time, the taps) visible to every warp
     const int64_t tw = tile % tiles_w, rest = tile / tiles_w, th = rest % tiles_h, pl = rest / tiles_h;
     const int64_t h0 = th * kDxTileH, w0 = tw * kDxTileW;
-    const int64_t r_lo = ceildiv(h0 - p.kh + 1, p.sh), r_hi = floordiv(h0 + kDxTileH - 1, p.sh);
-    const int64_t c_lo = ceildiv(w0 - p.kw + 1, p.sw), c_hi = floordiv(w0 + kDxTileW - 1, p.sw);
-    const int R = (int)(r_hi - r_lo + 1), C = (int)(c_hi - c_lo + 1);
-    const float* __restrict__ g = p.dy + pl * p.OH * p.OW;
-    __syncthreads();  // the previous tile's readers are done with ds
-    for (int i = threadIdx.x; i < R * C; i += kC2bThreads) {
-      const int rr = i / C, cc = i - rr * C;
-      const int64_t r = r_lo + rr, c = c_lo + cc;
-      ds[i] = (r >= 0 && r < p.OH && c >= 0 && c < p.OW) ? __ldg(g + r * p.OW + c) : 0.0f;
-    }
-    __syncthreads();
-    const int64_t h = h0 + warp;
-    if (h >= p.H) continue;
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    if (kS1) {
-      // r = h - a, c = w - b; smem column of output q, tap b: (lane + 32 q) + kw - 1 - b
-      for (int a = 0; a < (int)p.kh; ++a) {
-        const float* row = ds + (int)(h - a - r_lo) * C + lane + (int)p.kw - 1;
-        const float* fa = fs + a * (int)p.kw;
-        for (int b = 0; b < (int)p.kw; ++b) {
-          const float fv = fa[b];
+    const int64_t r_lo = ceildiv(h0 - kh + 1, p.sh), c_lo = ceildiv(w0 - kw + 1, p.sw);
+    const float* dsb = ds + buf * buf_elems;
+    for (int hh = warp; hh < kDxTileH; hh += kC2bThreads / 32) {
+      const int64_t h = h0 + hh;
+      if (h >= p.H) break;
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      if (kS1) {
+        // r = h - a, c = w - b; smem column of output q, tap b: (lane + 32 q) + kw - 1 - b
 #pragma unroll
-          for (int q = 0; q < 4; ++q) acc[q] = __fmaf_rn(fv, row[32 * q - b], acc[q]);
+        for (int a = 0; a < (KH > 0 ? KH : 1); ++a) {
+          for (int a2 = (KH > 0 ? a : 0); a2 < (KH > 0 ? a + 1 : kh); ++a2) {
+            const float* row = dsb + (hh + kh - 1 - a2) * C + lane + kw - 1;
+            const float* fa = fs + a2 * kw;
+#pragma unroll
+            for (int b = 0; b < (KW > 0 ? KW : 1); ++b) {
+              for (int b2 = (KW > 0 ? b : 0); b2 < (KW > 0 ? b + 1 : kw); ++b2) {
+                const float fv = fa[b2];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] = __fmaf_rn(fv, row[32 * q - b2], acc[q]);
+              }
+            }
+          }
+        }
+      } else {
+        const int64_t rmin = ceildiv(h - kh + 1, p.sh), rmax = floordiv(h, p.sh);
+        for (int64_t r = rmin; r <= rmax; ++r) {
+          const int a = (int)(h - r * p.sh);
+          const float* row = dsb + (int)(r - r_lo) * C;
+          const float* fa = fs + a * kw;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int64_t w = w0 + lane + 32 * q;
+            const int64_t cmin = ceildiv(w - kw + 1, p.sw), cmax = floordiv(w, p.sw);
+            float s = acc[q];
+            for (int64_t c = cmin; c <= cmax; ++c) s = __fmaf_rn(fa[w - c * p.sw], row[c - c_lo], s);
+            acc[q] = s;
+          }
         }
       }
-    } else {
-      const int64_t rmin = ceildiv(h - p.kh + 1, p.sh), rmax = floordiv(h, p.sh);
-      for (int64_t r = rmin; r <= rmax; ++r) {
-        const int a = (int)(h - r * p.sh);
-        const float* row = ds + (int)(r - r_lo) * C;
-        const float* fa = fs + a * (int)p.kw;
+      float* __restrict__ out = p.dx + (pl * p.H + h) * p.W;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int64_t w = w0 + lane + 32 * q;
-          const int64_t cmin = ceildiv(w - p.kw + 1, p.sw), cmax = floordiv(w, p.sw);
-          float s = acc[q];
-          for (int64_t c = cmin; c <= cmax; ++c) s = __fmaf_rn(fa[w - c * p.sw], row[c - c_lo], s);
-          acc[q] = s;
-        }
+      for (int q = 0; q < 4; ++q) {
+        const int64_t w = w0 + lane + 32 * q;
+        if (w < p.W) out[w] = acc[q];
       }
     }
-    float* __restrict__ out = p.dx + (pl * p.H + h) * p.W;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t w = w0 + lane + 32 * q;
-      if (w < p.W) out[w] = acc[q];
-    }
+    __syncthreads();  // every warp is done with buf before it is restaged
+    buf ^= 1;
   }
 }
 
@@ -144,73 +174,104 @@ __device__ __forceinline__ DfTile df_tile(const Conv2DBwdParams& p, int64_t tile
 // Stage dy[tile] into dys[kDfTileR][kDfTileC] and the x region under it into xs[XR][XC]
 // (zeros outside the tile, so padded lanes contribute 0 * 0).
 __device__ __forceinline__ void df_stage(const Conv2DBwdParams& p, const DfTile& t, float* dys, float* xs) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* __restrict__ g = p.dy + (t.pl * p.OH + t.r0) * p.OW + t.c0;
-  for (int i = threadIdx.x; i < kDfTileR * kDfTileC; i += kC2bThreads) {
-    const int rr = i / kDfTileC, cc = i - rr * kDfTileC;
-    dys[i] = (rr < t.nr && cc < t.nc) ? __ldg(g + rr * p.OW + cc) : 0.0f;
-  }
+  const uint32_t sd = smem_u32(dys), sx = smem_u32(xs);
+  for (int rr = warp; rr < kDfTileR; rr += kC2bThreads / 32)
+#pragma unroll
+    for (int q = 0; q < kDfTileC / 32; ++q) {
+      const int cc = lane + 32 * q;
+      const bool ok = rr < t.nr && cc < t.nc;
+      cp_async4(sd + 4u * (uint32_t)(rr * kDfTileC + cc), ok ? (const void*)(g + rr * p.OW + cc) : (const void*)g,
+                ok ? 4u : 0u);
+    }
   const int xr = (t.nr - 1) * (int)p.sh + (int)p.kh, xc = (t.nc - 1) * (int)p.sw + (int)p.kw;
   const float* __restrict__ xg = p.x + (t.pl * p.H + t.r0 * p.sh) * p.W + t.c0 * p.sw;
-  for (int i = threadIdx.x; i < p.df_xr * p.df_xc; i += kC2bThreads) {
-    const int rr = i / p.df_xc, cc = i - rr * p.df_xc;
-    xs[i] = (rr < xr && cc < xc) ? __ldg(xg + rr * p.W + cc) : 0.0f;
+  for (int rr = warp; rr < p.df_xr; rr += kC2bThreads / 32) {
+    const bool row_ok = rr < xr;
+    for (int cc = lane; cc < p.df_xc; cc += 32) {
+      const bool ok = row_ok && cc < xc;
+      cp_async4(sx + 4u * (uint32_t)(rr * p.df_xc + cc), ok ? (const void*)(xg + rr * p.W + cc) : (const void*)xg,
+                ok ? 4u : 0u);
+    }
   }
 }
 
-// kh <= KHM, kw <= KWM: all taps of a thread's columns in registers.
-template <int KHM, int KWM>
+// kh == KH, kw == KW (3x3, 5x5, 7x7) or kh, kw <= 4 (KH = KW = 4, guarded): every
+// thread keeps all taps' sums for its columns in fp32 registers over a run of
+// kDfRun tiles (<= 8 kDfRun products per tap per thread), then the warp reduces
+// them (fp32 butterfly) into its own fp64 accumulators in shared memory.
+constexpr int kDfRun = 16;
+
+template <int KH, int KW, bool kExact>
 __global__ void __launch_bounds__(kC2bThreads) conv2d_bwd_filter_reg_kernel(const __grid_constant__ Conv2DBwdParams p,
                                                                             double* __restrict__ part) {
+  constexpr int T = KH * KW;
   extern __shared__ __align__(16) float c2b_smem[];
-  float* dys = c2b_smem;
+  double(*accw)[T] = reinterpret_cast<double(*)[T]>(c2b_smem);  // [warp][tap], warp-owned
+  float* dys = c2b_smem + 2 * (kC2bThreads / 32) * T;
   float* xs = dys + kDfTileR * kDfTileC;
-  __shared__ double red[kC2bThreads / 32][KHM * KWM];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kh = (int)p.kh, kw = (int)p.kw, sh = (int)p.sh, sw = (int)p.sw, XC = p.df_xc;
-  double d[KHM * KWM];
+  const int kh = kExact ? KH : (int)p.kh, kw = kExact ? KW : (int)p.kw;
+  const int sh = (int)p.sh, sw = (int)p.sw, XC = p.df_xc;
+  for (int i = threadIdx.x; i < (kC2bThreads / 32) * T; i += kC2bThreads) (&accw[0][0])[i] = 0.0;
+  float d[T];
 #pragma unroll
-  for (int t = 0; t < KHM * KWM; ++t) d[t] = 0.0;
+  for (int i = 0; i < T; ++i) d[i] = 0.0f;
+  auto flush = [&]() {
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+      float v = d[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) accw[warp][i] += (double)v;
+      d[i] = 0.0f;
+    }
+  };
   const int64_t ntiles = p.planes * ((p.OH + kDfTileR - 1) / kDfTileR) * ((p.OW + kDfTileC - 1) / kDfTileC);
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  int run = 0;
+  const int buf_elems = kDfTileR * kDfTileC + p.df_xr * p.df_xc;
+  if ((int64_t)blockIdx.x < ntiles) df_stage(p, df_tile(p, blockIdx.x), dys, xs);
+  cp_async_commit();
+  int buf = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
     const DfTile t = df_tile(p, tile);
+    if (tile + gridDim.x < ntiles)
+      df_stage(p, df_tile(p, tile + gridDim.x), dys + (buf ^ 1) * buf_elems, xs + (buf ^ 1) * buf_elems);
+    cp_async_commit();
+    cp_async_wait<1>();
     __syncthreads();
-    df_stage(p, t, dys, xs);
-    __syncthreads();
-    float s[KHM * KWM];
-#pragma unroll
-    for (int i = 0; i < KHM * KWM; ++i) s[i] = 0.0f;
+    const float* dyb = dys + buf * buf_elems;
+    const float* xsb = xs + buf * buf_elems;
     for (int rr = warp; rr < t.nr; rr += kC2bThreads / 32) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int c = lane + 32 * q;
-        const float dyv = dys[rr * kDfTileC + c];
-        const float* xb = xs + rr * sh * XC + c * sw;
+        const float dyv = dyb[rr * kDfTileC + c];
+        const float* xb = xsb + rr * sh * XC + c * sw;
 #pragma unroll
-        for (int a = 0; a < KHM; ++a) {
-          if (a < kh) {
+        for (int a = 0; a < KH; ++a) {
+          if (kExact || a < kh) {
 #pragma unroll
-            for (int b = 0; b < KWM; ++b)
-              if (b < kw) s[a * KWM + b] = __fmaf_rn(dyv, xb[a * XC + b], s[a * KWM + b]);
+            for (int b = 0; b < KW; ++b)
+              if (kExact || b < kw) d[a * KW + b] = __fmaf_rn(dyv, xb[a * XC + b], d[a * KW + b]);
           }
         }
       }
     }
-#pragma unroll
-    for (int i = 0; i < KHM * KWM; ++i) d[i] += (double)s[i];
+    if (++run == kDfRun) {
+      flush();
+      run = 0;
+    }
+    __syncthreads();  // every warp is done with buf before it is restaged
   }
-#pragma unroll
-  for (int i = 0; i < KHM * KWM; ++i) {
-    double v = d[i];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) red[warp][i] = v;
-  }
+  flush();
   __syncthreads();
-  if (threadIdx.x < KHM * KWM) {
-    const int a = threadIdx.x / KWM, b = threadIdx.x - a * KWM;
+  for (int i = threadIdx.x; i < T; i += kC2bThreads) {
+    const int a = i / KW, b = i - a * KW;
     if (a < kh && b < kw) {
       double v = 0.0;
-      for (int w = 0; w < kC2bThreads / 32; ++w) v += red[w][threadIdx.x];
+      for (int w = 0; w < kC2bThreads / 32; ++w) v += accw[w][i];
       part[(int64_t)(a * kw + b) * gridDim.x + blockIdx.x] = v;
     }
   }
@@ -228,26 +289,35 @@ __global__ void __launch_bounds__(kC2bThreads) conv2d_bwd_filter_tap_kernel(cons
   const int kw = (int)p.kw, sh = (int)p.sh, sw = (int)p.sw, XC = p.df_xc;
   for (int t = threadIdx.x; t < nt; t += kC2bThreads) acc[t] = 0.0;
   const int64_t ntiles = p.planes * ((p.OH + kDfTileR - 1) / kDfTileR) * ((p.OW + kDfTileC - 1) / kDfTileC);
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const int buf_elems = kDfTileR * kDfTileC + p.df_xr * p.df_xc;
+  if ((int64_t)blockIdx.x < ntiles) df_stage(p, df_tile(p, blockIdx.x), dys, xs);
+  cp_async_commit();
+  int buf = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
     const DfTile t = df_tile(p, tile);
+    if (tile + gridDim.x < ntiles)
+      df_stage(p, df_tile(p, tile + gridDim.x), dys + (buf ^ 1) * buf_elems, xs + (buf ^ 1) * buf_elems);
+    cp_async_commit();
+    cp_async_wait<1>();
     __syncthreads();
-    df_stage(p, t, dys, xs);
-    __syncthreads();
+    const float* dyb = dys + buf * buf_elems;
+    const float* xsb = xs + buf * buf_elems;
     for (int tap = warp; tap < nt; tap += kC2bThreads / 32) {
       const int a = tap / kw, b = tap - a * kw;
       float s = 0.0f;
       for (int rr = 0; rr < t.nr; ++rr) {
-        const float* xb = xs + (rr * sh + a) * XC + b;
+        const float* xb = xsb + (rr * sh + a) * XC + b;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int c = lane + 32 * q;
-          s = __fmaf_rn(dys[rr * kDfTileC + c], xb[c * sw], s);
+          s = __fmaf_rn(dyb[rr * kDfTileC + c], xb[c * sw], s);
         }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (lane == 0) acc[tap] += (double)s;  // this warp alone owns tap
     }
+    __syncthreads();  // every warp is done with buf before it is restaged
   }
   __syncthreads();
   for (int t = threadIdx.x; t < nt; t += kC2bThreads) part[(int64_t)t * gridDim.x + blockIdx.x] = acc[t];
@@ -286,14 +356,15 @@ __global__ void conv2d_bwd_filter_finish(const double* __restrict__ part, int ct
   df[t] = (float)v;
 }
 
-size_t dx_smem(const Conv2DBwdParams& p) {
-  const int64_t R = (kDxTileH - 1 + p.kh - 1) / p.sh + 2, C = (kDxTileW - 1 + p.kw - 1) / p.sw + 2;
-  return (size_t)(((p.kh * p.kw + 3) & ~3) + R * C) * sizeof(float);
+size_t dx_smem(Conv2DBwdParams& p) {
+  p.dx_r = (int)((kDxTileH - 1 + p.kh - 1) / p.sh + 2);
+  p.dx_c = (int)((kDxTileW - 1 + p.kw - 1) / p.sw + 2);
+  return (size_t)(((p.kh * p.kw + 3) & ~3) + 2 * (int64_t)p.dx_r * p.dx_c) * sizeof(float);
 }
 
 }  // namespace
 
-int conv2d_backward_filter_ctas(int sms) { return 2 * sms; }
+int conv2d_backward_filter_ctas(int sms) { return 4 * sms; }
 
 size_t conv2d_backward_filter_workspace(int64_t taps, int ctas) { return (size_t)taps * ctas * sizeof(double); }
 
@@ -301,7 +372,12 @@ cudaError_t launch_conv2d_backward_input(Conv2DBwdParams& p, cudaStream_t stream
   const size_t smem = dx_smem(p);
   const int64_t ntiles = p.planes * ((p.H + kDxTileH - 1) / kDxTileH) * ((p.W + kDxTileW - 1) / kDxTileW);
   if (smem <= kC2bSmemMax) {
-    auto kfn = (p.sh == 1 && p.sw == 1) ? conv2d_bwd_input_tile_kernel<true> : conv2d_bwd_input_tile_kernel<false>;
+    const bool s1 = p.sh == 1 && p.sw == 1;
+    auto kfn = !s1                         ? conv2d_bwd_input_tile_kernel<false, 0, 0>
+               : (p.kh == 3 && p.kw == 3) ? conv2d_bwd_input_tile_kernel<true, 3, 3>
+               : (p.kh == 5 && p.kw == 5) ? conv2d_bwd_input_tile_kernel<true, 5, 5>
+               : (p.kh == 7 && p.kw == 7) ? conv2d_bwd_input_tile_kernel<true, 7, 7>
+                                          : conv2d_bwd_input_tile_kernel<true, 0, 0>;
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -324,14 +400,25 @@ cudaError_t launch_conv2d_backward_filter(Conv2DBwdParams& p, float* df, void* w
   const int64_t nt = p.kh * p.kw;
   p.df_xr = (int)((kDfTileR - 1) * p.sh + p.kh);
   p.df_xc = (int)((kDfTileC - 1) * p.sw + p.kw);
-  const size_t tile_bytes = ((size_t)kDfTileR * kDfTileC + (size_t)p.df_xr * p.df_xc) * sizeof(float);
+  const size_t tile_bytes = 2 * ((size_t)kDfTileR * kDfTileC + (size_t)p.df_xr * p.df_xc) * sizeof(float);
   const int64_t ntiles = p.planes * ((p.OH + kDfTileR - 1) / kDfTileR) * ((p.OW + kDfTileC - 1) / kDfTileC);
   const int grid = (int)min((int64_t)ctas, ntiles);
   cudaError_t e = cudaSuccess;
-  if (p.kh <= 4 && p.kw <= 4 && tile_bytes <= kC2bSmemMax) {
-    auto kfn = (p.kh == 3 && p.kw == 3) ? conv2d_bwd_filter_reg_kernel<3, 3> : conv2d_bwd_filter_reg_kernel<4, 4>;
-    e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
-    if (e == cudaSuccess) kfn<<<(unsigned)grid, kC2bThreads, tile_bytes, stream>>>(p, part);
+  auto reg = [&](auto kfn, int T) {
+    const size_t smem = tile_bytes + (size_t)(kC2bThreads / 32) * T * sizeof(double);
+    cudaError_t err = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
+    if (err == cudaSuccess) kfn<<<(unsigned)grid, kC2bThreads, smem, stream>>>(p, part);
+    return err;
+  };
+  const bool fits = tile_bytes + 8 * 64 * sizeof(double) <= kC2bSmemMax;
+  if (fits && p.kh == 3 && p.kw == 3) {
+    e = reg(conv2d_bwd_filter_reg_kernel<3, 3, true>, 9);
+  } else if (fits && p.kh == 5 && p.kw == 5) {
+    e = reg(conv2d_bwd_filter_reg_kernel<5, 5, true>, 25);
+  } else if (fits && p.kh == 7 && p.kw == 7) {
+    e = reg(conv2d_bwd_filter_reg_kernel<7, 7, true>, 49);
+  } else if (fits && p.kh <= 4 && p.kw <= 4) {
+    e = reg(conv2d_bwd_filter_reg_kernel<4, 4, false>, 16);
   } else if (tile_bytes + (size_t)((nt + 3) & ~3) * sizeof(double) <= kC2bSmemMax) {
     const size_t smem = tile_bytes + (size_t)((nt + 3) & ~3) * sizeof(double);
     e = ensure_smem_attr(reinterpret_cast<const void*>(conv2d_bwd_filter_tap_kernel));

@@ -186,6 +186,7 @@ struct Conv2DBwdParams {
   float* dx;        // input gradient
   int64_t planes, H, W, OH, OW, kh, kw, sh, sw;
   int df_xr, df_xc;  // filter-gradient x region pitch (set by the launcher)
+  int dx_r, dx_c;    // input-gradient dy region rows / pitch per buffer (set by the launcher)
   float taps[1024];  // input gradient: row-major [kh][kw]
 };
 cudaError_t launch_conv2d_backward_input(Conv2DBwdParams& p, cudaStream_t stream, int sms);
