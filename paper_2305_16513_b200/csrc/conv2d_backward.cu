@@ -61,13 +61,16 @@ __global__ void __launch_bounds__(kC2bThreads) conv2d_bwd_input_tile_kernel(cons
     const int R = (int)(r_hi - r_lo + 1), Cn = (int)(c_hi - c_lo + 1);
     const float* __restrict__ g = p.dy + pl * p.OH * p.OW;
     const uint32_t sb = smem_u32(ds + bf * buf_elems);
+    const int c0 = (int)c_lo, ow = (int)p.OW;
     for (int rr = warp; rr < R; rr += kC2bThreads / 32) {
       const int64_t r = r_lo + rr;
       const bool row_ok = r >= 0 && r < p.OH;
+      const float* __restrict__ gr = g + (row_ok ? r : 0) * p.OW;
+      const uint32_t srow = sb + 4u * (uint32_t)(rr * C);
       for (int cc = lane; cc < Cn; cc += 32) {
-        const int64_t c = c_lo + cc;
-        const bool ok = row_ok && c >= 0 && c < p.OW;
-        cp_async4(sb + 4u * (uint32_t)(rr * C + cc), ok ? (const void*)(g + r * p.OW + c) : (const void*)g, ok ? 4u : 0u);
+        const int c = c0 + cc;
+        const bool ok = row_ok && (unsigned)c < (unsigned)ow;
+        cp_async4(srow + 4u * (uint32_t)cc, ok ? (const void*)(gr + c) : (const void*)g, ok ? 4u : 0u);
       }
     }
   };
@@ -189,10 +192,11 @@ __device__ __forceinline__ void df_stage(const Conv2DBwdParams& p, const DfTile&
   const float* __restrict__ xg = p.x + (t.pl * p.H + t.r0 * p.sh) * p.W + t.c0 * p.sw;
   for (int rr = warp; rr < p.df_xr; rr += kC2bThreads / 32) {
     const bool row_ok = rr < xr;
+    const float* __restrict__ xr_g = xg + (row_ok ? rr : 0) * p.W;
+    const uint32_t srow = sx + 4u * (uint32_t)(rr * p.df_xc);
     for (int cc = lane; cc < p.df_xc; cc += 32) {
       const bool ok = row_ok && cc < xc;
-      cp_async4(sx + 4u * (uint32_t)(rr * p.df_xc + cc), ok ? (const void*)(xg + rr * p.W + cc) : (const void*)xg,
-                ok ? 4u : 0u);
+      cp_async4(srow + 4u * (uint32_t)cc, ok ? (const void*)(xr_g + cc) : (const void*)xg, ok ? 4u : 0u);
     }
   }
 }
@@ -348,12 +352,16 @@ __global__ void __launch_bounds__(kC2bThreads) conv2d_bwd_filter_direct_kernel(c
   }
 }
 
+// One warp per tap, lane-strided partial sums then a fixed butterfly (deterministic).
 __global__ void conv2d_bwd_filter_finish(const double* __restrict__ part, int ctas, int64_t nt, float* __restrict__ df) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (t >= nt) return;
   double v = 0.0;
-  for (int c = 0; c < ctas; ++c) v += part[t * ctas + c];
-  df[t] = (float)v;
+  for (int c = lane; c < ctas; c += 32) v += part[t * ctas + c];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) df[t] = (float)v;
 }
 
 size_t dx_smem(Conv2DBwdParams& p) {
@@ -428,7 +436,7 @@ cudaError_t launch_conv2d_backward_filter(Conv2DBwdParams& p, float* df, void* w
   }
   if (e != cudaSuccess) return e;
   note_launch();
-  conv2d_bwd_filter_finish<<<(unsigned)((nt + 127) / 128), 128, 0, stream>>>(part, grid, nt, df);
+  conv2d_bwd_filter_finish<<<(unsigned)((nt + 3) / 4), 128, 0, stream>>>(part, grid, nt, df);
   note_launch();
   return cudaGetLastError();
 }
