@@ -89,6 +89,37 @@ __global__ void __launch_bounds__(kC2bThreads) conv2d_bwd_input_tile_kernel(cons
     for (int hh = warp; hh < kDxTileH; hh += kC2bThreads / 32) {
       const int64_t h = h0 + hh;
       if (h >= p.H) break;
+      if (kS1 && KH > 0 && KW > 0) {
+        // exact size, stride 1: lane owns 4 consecutive columns w0 + 4 lane + q; per filter row
+        // the ceil((KW + 3) / 4) LDS.128 it needs cover all KW taps of its 4 outputs (register
+        // reuse across taps); taps are constant-bank operands
+        constexpr int NV = (KW + 3 + 3) / 4;
+        float acc4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int a = 0; a < (KH > 0 ? KH : 1); ++a) {
+          const float4* row4 = reinterpret_cast<const float4*>(dsb + (hh + KH - 1 - a) * C) + lane;
+          float v[4 * NV];
+#pragma unroll
+          for (int u = 0; u < NV; ++u) {
+            const float4 t4 = row4[u];
+            v[4 * u] = t4.x; v[4 * u + 1] = t4.y; v[4 * u + 2] = t4.z; v[4 * u + 3] = t4.w;
+          }
+#pragma unroll
+          for (int b = 0; b < (KW > 0 ? KW : 1); ++b)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc4[q] = __fmaf_rn(p.taps[a * KW + b], v[q + KW - 1 - b], acc4[q]);
+        }
+        float* __restrict__ out = p.dx + (pl * p.H + h) * p.W;
+        const int64_t w = w0 + 4 * lane;
+        if (w + 3 < p.W && (reinterpret_cast<uintptr_t>(out + w) & 15) == 0) {
+          *reinterpret_cast<float4*>(out + w) = make_float4(acc4[0], acc4[1], acc4[2], acc4[3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (w + q < p.W) out[w + q] = acc4[q];
+        }
+        continue;
+      }
       float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
       if (kS1) {
         // r = h - a, c = w - b; smem column of output q, tap b: (lane + 32 q) + kw - 1 - b
@@ -247,6 +278,33 @@ __global__ void __launch_bounds__(kC2bThreads) conv2d_bwd_filter_reg_kernel(cons
     __syncthreads();
     const float* dyb = dys + buf * buf_elems;
     const float* xsb = xs + buf * buf_elems;
+    if (sw == 1) {
+      // lane owns 4 consecutive dy columns 4 lane + q: one LDS.128 of dy and ceil((KW + 3) / 4)
+      // LDS.128 of x per filter row cover all KW taps (register reuse across taps)
+      constexpr int NV = (KW + 3 + 3) / 4;
+      for (int rr = warp; rr < t.nr; rr += kC2bThreads / 32) {
+        const float4 d4 = reinterpret_cast<const float4*>(dyb + rr * kDfTileC)[lane];
+        const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+        for (int a = 0; a < KH; ++a) {
+          if (kExact || a < kh) {
+            const float4* x4 = reinterpret_cast<const float4*>(xsb + (rr * sh + a) * XC) + lane;
+            float v[4 * NV];
+#pragma unroll
+            for (int u = 0; u < NV; ++u) {
+              const float4 t4 = x4[u];
+              v[4 * u] = t4.x; v[4 * u + 1] = t4.y; v[4 * u + 2] = t4.z; v[4 * u + 3] = t4.w;
+            }
+#pragma unroll
+            for (int b = 0; b < KW; ++b)
+              if (kExact || b < kw) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) d[a * KW + b] = __fmaf_rn(dv[q], v[q + b], d[a * KW + b]);
+              }
+          }
+        }
+      }
+    } else
     for (int rr = warp; rr < t.nr; rr += kC2bThreads / 32) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -366,7 +424,7 @@ __global__ void conv2d_bwd_filter_finish(const double* __restrict__ part, int ct
 
 size_t dx_smem(Conv2DBwdParams& p) {
   p.dx_r = (int)((kDxTileH - 1 + p.kh - 1) / p.sh + 2);
-  p.dx_c = (int)((kDxTileW - 1 + p.kw - 1) / p.sw + 2);
+  p.dx_c = (int)((((kDxTileW - 1 + p.kw - 1) / p.sw + 2) + 3) / 4 * 4 + 4);  // LDS.128 rows + over-read
   return (size_t)(((p.kh * p.kw + 3) & ~3) + 2 * (int64_t)p.dx_r * p.dx_c) * sizeof(float);
 }
 
@@ -407,7 +465,7 @@ cudaError_t launch_conv2d_backward_filter(Conv2DBwdParams& p, float* df, void* w
   double* part = static_cast<double*>(workspace);
   const int64_t nt = p.kh * p.kw;
   p.df_xr = (int)((kDfTileR - 1) * p.sh + p.kh);
-  p.df_xc = (int)((kDfTileC - 1) * p.sw + p.kw);
+  p.df_xc = (int)(((kDfTileC - 1) * p.sw + p.kw + 3) / 4 * 4 + 4);  // LDS.128 rows + over-read
   const size_t tile_bytes = 2 * ((size_t)kDfTileR * kDfTileC + (size_t)p.df_xr * p.df_xc) * sizeof(float);
   const int64_t ntiles = p.planes * ((p.OH + kDfTileR - 1) / kDfTileR) * ((p.OW + kDfTileC - 1) / kDfTileC);
   const int grid = (int)min((int64_t)ctas, ntiles);
