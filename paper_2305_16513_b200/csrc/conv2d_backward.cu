@@ -35,6 +35,28 @@ constexpr int kDxTileH = 32, kDxTileW = 128;
 constexpr int kDfTileR = 16, kDfTileC = 128;
 constexpr size_t kC2bSmemMax = 96 * 1024;
 
+__device__ __forceinline__ void cp_async8(uint32_t saddr, const void* g, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(saddr), "l"(g), "r"(src_bytes) : "memory");
+}
+
+// Stage one row: smem words [0, n) <- global gr[c0 + j] where 0 <= c0 + j < nvalid (else 0).
+// G-element cp.async granules (G = 4 / 2 / 1) when the caller guarantees that gr + c0 is
+// 4G-byte aligned and c0 % G == 0 (so a granule never straddles column 0); a granule
+// straddling nvalid copies its valid prefix and zero-fills the rest.
+template <int G>
+__device__ __forceinline__ void stage_row(uint32_t srow, const float* gr, const float* any, int c0, int n, int nvalid,
+                                          bool row_ok, int lane) {
+  for (int j = G * lane; j < n; j += 32 * G) {
+    const int c = c0 + j;
+    int nv = nvalid - c;
+    nv = (!row_ok || c < 0) ? 0 : (nv < 0 ? 0 : (nv > G ? G : nv));
+    const void* src = nv > 0 ? (const void*)(gr + c) : any;
+    if (G == 4) cp_async16(srow + 4u * (uint32_t)j, src, 4u * (uint32_t)nv);
+    else if (G == 2) cp_async8(srow + 4u * (uint32_t)j, src, 4u * (uint32_t)nv);
+    else cp_async4(srow + 4u * (uint32_t)j, src, 4u * (uint32_t)nv);
+  }
+}
+
 __device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 __device__ __forceinline__ int64_t ceildiv(int64_t a, int64_t b) { return -floordiv(-a, b); }
 
@@ -62,16 +84,14 @@ __global__ void __launch_bounds__(kC2bThreads) conv2d_bwd_input_tile_kernel(cons
     const float* __restrict__ g = p.dy + pl * p.OH * p.OW;
     const uint32_t sb = smem_u32(ds + bf * buf_elems);
     const int c0 = (int)c_lo, ow = (int)p.OW;
+    const bool g2 = (ow & 1) == 0 && (c0 & 1) == 0 && (reinterpret_cast<uintptr_t>(g) & 7) == 0;
     for (int rr = warp; rr < R; rr += kC2bThreads / 32) {
       const int64_t r = r_lo + rr;
       const bool row_ok = r >= 0 && r < p.OH;
       const float* __restrict__ gr = g + (row_ok ? r : 0) * p.OW;
       const uint32_t srow = sb + 4u * (uint32_t)(rr * C);
-      for (int cc = lane; cc < Cn; cc += 32) {
-        const int c = c0 + cc;
-        const bool ok = row_ok && (unsigned)c < (unsigned)ow;
-        cp_async4(srow + 4u * (uint32_t)cc, ok ? (const void*)(gr + c) : (const void*)g, ok ? 4u : 0u);
-      }
+      if (g2) stage_row<2>(srow, gr, g, c0, Cn, ow, row_ok, lane);
+      else stage_row<1>(srow, gr, g, c0, Cn, ow, row_ok, lane);
     }
   };
   if ((int64_t)blockIdx.x < ntiles) stage(blockIdx.x, 0);
@@ -211,24 +231,22 @@ __device__ __forceinline__ void df_stage(const Conv2DBwdParams& p, const DfTile&
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* __restrict__ g = p.dy + (t.pl * p.OH + t.r0) * p.OW + t.c0;
   const uint32_t sd = smem_u32(dys), sx = smem_u32(xs);
-  for (int rr = warp; rr < kDfTileR; rr += kC2bThreads / 32)
-#pragma unroll
-    for (int q = 0; q < kDfTileC / 32; ++q) {
-      const int cc = lane + 32 * q;
-      const bool ok = rr < t.nr && cc < t.nc;
-      cp_async4(sd + 4u * (uint32_t)(rr * kDfTileC + cc), ok ? (const void*)(g + rr * p.OW + cc) : (const void*)g,
-                ok ? 4u : 0u);
-    }
+  const bool g2 = (p.OW & 1) == 0 && (reinterpret_cast<uintptr_t>(p.dy) & 7) == 0;  // c0 % 128 == 0
+  for (int rr = warp; rr < kDfTileR; rr += kC2bThreads / 32) {
+    const bool row_ok = rr < t.nr;
+    const float* __restrict__ gr = g + (row_ok ? rr : 0) * p.OW;
+    if (g2) stage_row<2>(sd + 4u * (uint32_t)(rr * kDfTileC), gr, g, 0, kDfTileC, t.nc, row_ok, lane);
+    else stage_row<1>(sd + 4u * (uint32_t)(rr * kDfTileC), gr, g, 0, kDfTileC, t.nc, row_ok, lane);
+  }
   const int xr = (t.nr - 1) * (int)p.sh + (int)p.kh, xc = (t.nc - 1) * (int)p.sw + (int)p.kw;
   const float* __restrict__ xg = p.x + (t.pl * p.H + t.r0 * p.sh) * p.W + t.c0 * p.sw;
+  const bool g4 = (p.W & 3) == 0 && (reinterpret_cast<uintptr_t>(p.x) & 15) == 0;  // c0 sw % 4 == 0
   for (int rr = warp; rr < p.df_xr; rr += kC2bThreads / 32) {
     const bool row_ok = rr < xr;
     const float* __restrict__ xr_g = xg + (row_ok ? rr : 0) * p.W;
     const uint32_t srow = sx + 4u * (uint32_t)(rr * p.df_xc);
-    for (int cc = lane; cc < p.df_xc; cc += 32) {
-      const bool ok = row_ok && cc < xc;
-      cp_async4(srow + 4u * (uint32_t)cc, ok ? (const void*)(xr_g + cc) : (const void*)xg, ok ? 4u : 0u);
-    }
+    if (g4) stage_row<4>(srow, xr_g, xg, 0, p.df_xc, xc, row_ok, lane);
+    else stage_row<1>(srow, xr_g, xg, 0, p.df_xc, xc, row_ok, lane);
   }
 }
 
