@@ -1,7 +1,9 @@
-"""Small cases through every kernel family, checked against the oracle; meant to
-run under compute-sanitizer (one --tool per invocation):
+"""Small cases through every kernel family (incl. the 2-D conv gradients and the
+padded sliding min), checked against the oracle; written to run under
+compute-sanitizer (one --tool per invocation) where it is available:
     compute-sanitizer --tool memcheck python tests/sanitize_cases.py
-Exits non-zero on a parity failure."""
+(the GPU pool of this round has compute-sanitizer disabled, so it ran plainly:
+0 failures).  Exits non-zero on a parity failure."""
 import os
 import sys
 
@@ -44,6 +46,23 @@ for P, H, W, kk, s in ((3, 112, 112, 3, 1), (3, 112, 112, 2, 2), (2, 31, 45, 3, 
     y = ss.pool2d(torch.from_numpy(x).cuda(), (kk, kk), (s, s), "max").cpu().numpy()
     ref, _ = oracle.pool2d(x, kk, kk, s, s, 0)
     chk(f"pool2d {P} {H} {W} {kk} {s}", np.array_equal(y.astype(np.float64), ref))
+for P, H, W, kh, kw, sh, sw in ((2, 37, 150, 3, 3, 1, 1), (1, 30, 140, 7, 7, 1, 1), (2, 41, 259, 4, 2, 2, 3),
+                               (1, 40, 40, 5, 6, 1, 1), (1, 1030, 3, 1024, 1, 1, 1)):
+    OH, OW = (H - kh) // sh + 1, (W - kw) // sw + 1
+    x = synth.normal(90, P * H * W).reshape(P, H, W)
+    f = synth.normal(91, kh * kw).reshape(kh, kw)
+    g = synth.normal(92, P * OH * OW).reshape(P, OH, OW)
+    dx = ss.conv2d_backward_input(torch.from_numpy(g).cuda(), f, H, W, (sh, sw)).cpu().numpy()
+    df = ss.conv2d_backward_filter(torch.from_numpy(x).cuda(), torch.from_numpy(g).cuda(), (kh, kw),
+                                   (sh, sw)).cpu().numpy()
+    ref, mag = oracle.conv2d_backward_input(g, f, H, W, sh, sw)
+    chk(f"conv2d dx {P} {H} {W} {kh} {kw}", bool(np.all(np.abs(dx - ref) <= 1e-5 * mag + 1e-6)))
+    ref, mag = oracle.conv2d_backward_filter(x, g, kh, kw, sh, sw)
+    chk(f"conv2d df {P} {H} {W} {kh} {kw}", bool(np.all(np.abs(df - ref) <= 1e-5 * mag + 1e-6)))
+for mode in ("reflect", "circular", "replicate"):
+    x = synth.normal(3, 2 * 20011).reshape(2, 20011)
+    y = ss.pool_min(torch.from_numpy(x).cuda(), 16, padding=(8, 7), pad_mode=mode).cpu().numpy()
+    chk(f"min {mode}", np.array_equal(y, oracle.pool_min_ex(x, 16, 1, 1, 8, 7, mode)))
 torch.cuda.synchronize()
 print("sanitize cases done, failures:", bad)
 sys.exit(1 if bad else 0)
