@@ -39,7 +39,16 @@
  *             surface at the caller's next synchronisation.  The library
  *             never aborts, throws or prints.
  *  Memory     The library allocates no device memory and keeps no per-call
- *             state; it caches per-device attributes (SM count) only.
+ *             or cross-call device state; it caches per-device attributes
+ *             (SM count, kernel smem attributes) only.  The persistent
+ *             kernels distribute their tiles dynamically by cluster launch
+ *             control (the grid has one CTA per tile; running CTAs cancel
+ *             pending CTAs and take their tiles), so the claim state lives
+ *             in the hardware scheduler of each launch: concurrent calls,
+ *             CUDA-graph captures (including a first call made inside a
+ *             capture) and concurrent graph replays are independent.  Calls
+ *             that need scratch (the filter gradients) take a caller-owned
+ *             workspace.
  *  Numerics   int32 + wraps modulo 2^32.  fp32 uses IEEE round-to-nearest
  *             FMA/adds (no fast-math, no flush-to-zero), except the
  *             tensor-core conv1d path (see ss_conv1d).  max equals

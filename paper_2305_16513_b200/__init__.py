@@ -278,25 +278,55 @@ def _stream(stream) -> int:
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
-def _rows(x):
-    if not x.is_cuda:
-        raise ValueError("x must be a CUDA tensor (there is no CPU path)")
-    if not x.is_contiguous():
-        raise ValueError("x must be contiguous")
+def _dev(t, name, dtype=None, shape=None, device=None):
+    """Argument check of a device tensor: CUDA, contiguous, and (if given) dtype,
+    shape and device.  The kernels trust the sizes they are given, so a wrong
+    tensor here would read or write out of bounds."""
+    if not getattr(t, "is_cuda", False):
+        raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} must be on {device}, got {t.device}")
+    return t
+
+
+def _alloc(out, shape, dtype, device, name="out"):
+    """A fresh output, or the caller's `out` after checking it matches."""
+    if out is None:
+        return _torch().empty(tuple(shape), dtype=dtype, device=device)
+    return _dev(out, name, dtype, shape, device)
+
+
+def _rows(x, name="x"):
+    _dev(x, name)
     if x.dim() == 1:
         return x.shape[0], 1
     if x.dim() == 2:
         return x.shape[1], x.shape[0]
-    raise ValueError("x must be [N] or [batch, N]")
+    raise ValueError(f"{name} must be [N] or [batch, N]")
 
 
 def _out(x, L, out):
-    torch = _torch()
     shape = (L,) if x.dim() == 1 else (x.shape[0], L)
-    if out is None:
-        return torch.empty(shape, dtype=x.dtype, device=x.device)
-    assert tuple(out.shape) == shape and out.dtype == x.dtype and out.is_contiguous()
-    return out
+    return _alloc(out, shape, x.dtype, x.device)
+
+
+# a non-NULL stand-in for an output pointer in validation-only calls (the size
+# checks fail before any pointer is used), so the C ABI reports the real status
+_VALIDATE_ONLY = 16
+
+
+def _plane_geom(x, name="x"):
+    _dev(x, name)
+    if x.dim() < 2:
+        raise ValueError(f"{name} must be [..., H, W]")
+    H, W = x.shape[-2], x.shape[-1]
+    return H, W, (x.numel() // (H * W) if H * W else 0)
 
 
 def _pads(padding):
@@ -315,7 +345,7 @@ def _window(fn, x, w, stride, out, stream, dilation, padding, pad_mode):
     L = ss_out_len_ex(N, w, stride, dilation, pl, pr)
     args = (N, B, w, stride, dilation, pl, pr, _pad_mode(pad_mode), _dtype_code(x), _stream(stream))
     if L < 0:
-        check(fn(x.data_ptr(), 0, *args) or SS_ERR_BAD_SIZE)
+        check(fn(x.data_ptr(), _VALIDATE_ONLY, *args) or SS_ERR_BAD_SIZE)
     y = _out(x, L, out)
     check(fn(x.data_ptr(), y.data_ptr(), *args))
     return y
@@ -354,7 +384,7 @@ def conv1d(x, filt, stride: int = 1, out=None, stream=None, dilation: int = 1, p
     L = ss_out_len_ex(N, k, stride, dilation, pl, pr)
     pm = _pad_mode(pad_mode)
     if L < 0:
-        check(ss_conv1d_ex(x.data_ptr(), 0, N, B, f, k, stride, dilation, pl, pr, pm, _dtype_code(x),
+        check(ss_conv1d_ex(x.data_ptr(), _VALIDATE_ONLY, N, B, f, k, stride, dilation, pl, pr, pm, _dtype_code(x),
                            _stream(stream)) or SS_ERR_BAD_SIZE)
     y = _out(x, L, out)
     check(ss_conv1d_ex(x.data_ptr(), y.data_ptr(), N, B, f, k, stride, dilation, pl, pr, pm, _dtype_code(x),
@@ -364,40 +394,38 @@ def conv1d(x, filt, stride: int = 1, out=None, stream=None, dilation: int = 1, p
 
 def pool2d(x, kernel, stride, mode: str = "max", out=None, stream=None):
     """Separable 2-D max/avg pooling of a CUDA fp32 tensor [..., H, W] (e.g. NCHW)."""
-    torch = _torch()
-    if not x.is_cuda or not x.is_contiguous():
-        raise ValueError("x must be a contiguous CUDA tensor")
+    H, W, planes = _plane_geom(x)
     kh, kw = kernel
     sh, sw = stride
-    H, W = x.shape[-2], x.shape[-1]
-    planes = x.numel() // (H * W)
     OH, OW = ss_out_len(H, kh, sh), ss_out_len(W, kw, sw)
     m = SS_POOL_MAX if mode == "max" else SS_POOL_AVG
     if OH < 0 or OW < 0:
-        check(ss_pool2d(x.data_ptr(), 0, planes, H, W, kh, kw, sh, sw, m, _dtype_code(x), _stream(stream)) or SS_ERR_BAD_SIZE)
-    shape = tuple(x.shape[:-2]) + (OH, OW)
-    y = torch.empty(shape, dtype=x.dtype, device=x.device) if out is None else out
+        check(ss_pool2d(x.data_ptr(), _VALIDATE_ONLY, planes, H, W, kh, kw, sh, sw, m, _dtype_code(x),
+                        _stream(stream)) or SS_ERR_BAD_SIZE)
+    y = _alloc(out, tuple(x.shape[:-2]) + (OH, OW), x.dtype, x.device)
     check(ss_pool2d(x.data_ptr(), y.data_ptr(), planes, H, W, kh, kw, sh, sw, m, _dtype_code(x), _stream(stream)))
     return y
+
+
+def _filter2d(filt):
+    f = filt.tolist() if hasattr(filt, "tolist") else [list(r) for r in filt]
+    kh, kw = len(f), len(f[0])
+    if any(len(r) != kw for r in f):
+        raise ValueError("filter rows must have equal length")
+    return kh, kw, [float(v) for row in f for v in row]
 
 
 def conv2d(x, filt, stride=(1, 1), out=None, stream=None):
     """2-D single-channel sliding dot product of a CUDA fp32 [..., H, W] tensor with a host
     filter [kh, kw] (nested sequence, numpy array or CPU tensor); valid padding."""
-    torch = _torch()
-    if not x.is_cuda or not x.is_contiguous():
-        raise ValueError("x must be a contiguous CUDA tensor")
-    f = filt.tolist() if hasattr(filt, "tolist") else [list(r) for r in filt]
-    kh, kw = len(f), len(f[0])
-    flat = [float(v) for row in f for v in row]
+    H, W, planes = _plane_geom(x)
+    kh, kw, flat = _filter2d(filt)
     sh, sw = stride
-    H, W = x.shape[-2], x.shape[-1]
-    planes = x.numel() // (H * W)
     OH, OW = ss_out_len(H, kh, sh), ss_out_len(W, kw, sw)
     if OH < 0 or OW < 0:
-        check(ss_conv2d(x.data_ptr(), 0, planes, H, W, flat, kh, kw, sh, sw, _dtype_code(x), _stream(stream))
-              or SS_ERR_BAD_SIZE)
-    y = torch.empty(tuple(x.shape[:-2]) + (OH, OW), dtype=x.dtype, device=x.device) if out is None else out
+        check(ss_conv2d(x.data_ptr(), _VALIDATE_ONLY, planes, H, W, flat, kh, kw, sh, sw, _dtype_code(x),
+                        _stream(stream)) or SS_ERR_BAD_SIZE)
+    y = _alloc(out, tuple(x.shape[:-2]) + (OH, OW), x.dtype, x.device)
     check(ss_conv2d(x.data_ptr(), y.data_ptr(), planes, H, W, flat, kh, kw, sh, sw, _dtype_code(x), _stream(stream)))
     return y
 
@@ -406,14 +434,13 @@ def affine_window(u, v, w: int, stride: int = 1, want_U: bool = True, out=None, 
     """Sliding window of gamma pairs (Eq. 8 operator, ss.h ss_affine_window) over the
     last dim of CUDA fp32 [N] / [B, N] tensors u, v.  Returns (U, V); U is None
     when want_U is False.  `out` = (U, V) preallocated (U may be None)."""
-    N, B = _rows(u)
-    if v.shape != u.shape or not v.is_cuda or not v.is_contiguous() or v.dtype != u.dtype:
-        raise ValueError("v must be a contiguous CUDA tensor shaped like u")
+    N, B = _rows(u, "u")
+    _dev(v, "v", u.dtype, u.shape, u.device)
     if _dtype_code(u) != SS_F32:
         raise TypeError("affine_window takes fp32 tensors")
     L = ss_out_len(N, w, stride)
     if L < 0:
-        check(ss_affine_window(u.data_ptr(), v.data_ptr(), 0, 0, N, B, w, stride) or SS_ERR_BAD_SIZE)
+        check(ss_affine_window(u.data_ptr(), v.data_ptr(), 0, _VALIDATE_ONLY, N, B, w, stride) or SS_ERR_BAD_SIZE)
     if out is None:
         V = _out(u, L, None)
         U = _out(u, L, None) if want_U else None
@@ -428,17 +455,24 @@ def affine_window(u, v, w: int, stride: int = 1, want_U: bool = True, out=None, 
 
 # ------------------------------------------------------------ backward passes
 def _grad_out(dy, N, out):
-    torch = _torch()
     shape = (N,) if dy.dim() == 1 else (dy.shape[0], N)
-    if out is None:
-        return torch.empty(shape, dtype=dy.dtype, device=dy.device)
-    assert tuple(out.shape) == shape and out.dtype == dy.dtype and out.is_contiguous()
-    return out
+    return _alloc(out, shape, dy.dtype, dy.device)
+
+
+def _check_dy_1d(dy, N, w, stride):
+    """dy must hold exactly the forward's out_len = (N - w) / stride + 1 outputs per row."""
+    L = ss_out_len(N, w, stride)
+    if L < 0:
+        raise SSError(SS_ERR_WINDOW_EXCEEDS_INPUT if N >= 1 and w > N else SS_ERR_BAD_SIZE,
+                      f"invalid window: N={N} w={w} stride={stride}")
+    if dy.shape[-1] != L:
+        raise ValueError(f"dy must have {L} outputs per row (N={N}, w={w}, stride={stride}), got {dy.shape[-1]}")
 
 
 def pool_sum_backward(dy, N: int, w: int, stride: int = 1, out=None, stream=None):
     """dx of pool_sum (valid padding): dx_t = sum of dy over the windows containing t."""
-    L, B = _rows(dy)
+    L, B = _rows(dy, "dy")
+    _check_dy_1d(dy, N, w, stride)
     dx = _grad_out(dy, N, out)
     check(ss_pool_sum_backward(dy.data_ptr(), dx.data_ptr(), N, B, w, stride, _dtype_code(dy), _stream(stream)))
     return dx
@@ -447,6 +481,10 @@ def pool_sum_backward(dy, N: int, w: int, stride: int = 1, out=None, stream=None
 def pool_max_backward(x, dy, w: int, stride: int = 1, out=None, stream=None):
     """dx of pool_max: each window's dy goes to its first maximum in x."""
     N, B = _rows(x)
+    _rows(dy, "dy")
+    if dy.dim() != x.dim() or (x.dim() == 2 and dy.shape[0] != B) or dy.dtype != x.dtype or dy.device != x.device:
+        raise ValueError("dy must match x's batch, dtype and device")
+    _check_dy_1d(dy, N, w, stride)
     dx = _grad_out(dy, N, out)
     check(ss_pool_max_backward(x.data_ptr(), dy.data_ptr(), dx.data_ptr(), N, B, w, stride, _dtype_code(x),
                                _stream(stream)))
@@ -455,38 +493,61 @@ def pool_max_backward(x, dy, w: int, stride: int = 1, out=None, stream=None):
 
 def conv1d_backward_input(dy, filt, N: int, stride: int = 1, out=None, stream=None):
     """dx of conv1d (valid padding, cross-correlation) for a host filter."""
-    L, B = _rows(dy)
+    L, B = _rows(dy, "dy")
     f = [float(v) for v in (filt.tolist() if hasattr(filt, "tolist") else filt)]
+    _check_dy_1d(dy, N, len(f), stride)
     dx = _grad_out(dy, N, out)
     check(ss_conv1d_backward_input(dy.data_ptr(), dx.data_ptr(), N, B, f, len(f), stride, _dtype_code(dy),
                                    _stream(stream)))
     return dx
 
 
+def _workspace(workspace, need, device):
+    torch = _torch()
+    if workspace is not None:
+        _dev(workspace, "workspace", device=device)
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.empty(max(need, 8), dtype=torch.uint8, device=device)
+    return workspace
+
+
 def conv1d_backward_filter(x, dy, k: int, stride: int = 1, out=None, workspace=None, stream=None):
     """df of conv1d: df_j = sum over rows and outputs of dy_i x_{i*stride+j} (device tensor of k floats)."""
     torch = _torch()
     N, B = _rows(x)
-    df = torch.empty(k, dtype=torch.float32, device=x.device) if out is None else out
-    need = ss_conv1d_backward_filter_workspace(k)
-    if workspace is None or workspace.numel() * workspace.element_size() < need:
-        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+    _rows(dy, "dy")
+    if dy.dim() != x.dim() or (x.dim() == 2 and dy.shape[0] != B) or dy.dtype != torch.float32 or \
+            x.dtype != torch.float32 or dy.device != x.device:
+        raise ValueError("x and dy must be fp32 on one device with the same batch")
+    _check_dy_1d(dy, N, k, stride)
+    df = _alloc(out, (k,), torch.float32, x.device)
+    workspace = _workspace(workspace, ss_conv1d_backward_filter_workspace(k), x.device)
     check(ss_conv1d_backward_filter(x.data_ptr(), dy.data_ptr(), df.data_ptr(), N, B, k, stride,
                                     workspace.data_ptr(), workspace.numel() * workspace.element_size(),
                                     _stream(stream)))
     return df
 
 
+def _check_dy_2d(dy, H, W, kh, kw, sh, sw):
+    OH, OW = ss_out_len(H, kh, sh), ss_out_len(W, kw, sw)
+    if OH < 0 or OW < 0:
+        raise SSError(SS_ERR_WINDOW_EXCEEDS_INPUT, f"window {kh}x{kw} exceeds input {H}x{W}")
+    if dy.dim() < 2 or tuple(dy.shape[-2:]) != (OH, OW):
+        raise ValueError(f"dy must be [..., {OH}, {OW}] (H={H}, W={W}, window {kh}x{kw}, stride {sh}x{sw}), "
+                         f"got {tuple(dy.shape)}")
+
+
 def conv2d_backward_input(dy, filt, H: int, W: int, stride=(1, 1), out=None, stream=None):
     """dx of conv2d for a CUDA fp32 dy [..., OH, OW] and a host filter [kh, kw]: [..., H, W]."""
     torch = _torch()
-    f = filt.tolist() if hasattr(filt, "tolist") else [list(r) for r in filt]
-    kh, kw = len(f), len(f[0])
+    _dev(dy, "dy", torch.float32)
+    kh, kw, flat = _filter2d(filt)
     sh, sw = stride
+    _check_dy_2d(dy, H, W, kh, kw, sh, sw)
     planes = dy.numel() // (dy.shape[-2] * dy.shape[-1])
-    dx = torch.empty(tuple(dy.shape[:-2]) + (H, W), dtype=torch.float32, device=dy.device) if out is None else out
-    check(ss_conv2d_backward_input(dy.data_ptr(), dx.data_ptr(), planes, H, W, [float(v) for r in f for v in r],
-                                   kh, kw, sh, sw, _dtype_code(dy), _stream(stream)))
+    dx = _alloc(out, tuple(dy.shape[:-2]) + (H, W), torch.float32, dy.device)
+    check(ss_conv2d_backward_input(dy.data_ptr(), dx.data_ptr(), planes, H, W, flat, kh, kw, sh, sw,
+                                   _dtype_code(dy), _stream(stream)))
     return dx
 
 
@@ -495,12 +556,14 @@ def conv2d_backward_filter(x, dy, kernel, stride=(1, 1), out=None, workspace=Non
     torch = _torch()
     kh, kw = kernel
     sh, sw = stride
-    H, W = x.shape[-2], x.shape[-1]
-    planes = x.numel() // (H * W)
-    df = torch.empty((kh, kw), dtype=torch.float32, device=x.device) if out is None else out
-    need = ss_conv2d_backward_filter_workspace(kh, kw)
-    if workspace is None or workspace.numel() * workspace.element_size() < need:
-        workspace = torch.empty(max(need, 8), dtype=torch.uint8, device=x.device)
+    H, W, planes = _plane_geom(x)
+    _dev(x, "x", torch.float32)
+    _dev(dy, "dy", torch.float32, device=x.device)
+    _check_dy_2d(dy, H, W, kh, kw, sh, sw)
+    if dy.numel() // (dy.shape[-2] * dy.shape[-1]) != planes:
+        raise ValueError("dy must have as many planes as x")
+    df = _alloc(out, (kh, kw), torch.float32, x.device)
+    workspace = _workspace(workspace, ss_conv2d_backward_filter_workspace(kh, kw), x.device)
     check(ss_conv2d_backward_filter(x.data_ptr(), dy.data_ptr(), df.data_ptr(), planes, H, W, kh, kw, sh, sw,
                                     workspace.data_ptr(), workspace.numel() * workspace.element_size(),
                                     _stream(stream)))
@@ -508,15 +571,17 @@ def conv2d_backward_filter(x, dy, kernel, stride=(1, 1), out=None, workspace=Non
 
 
 def pool2d_backward(x, dy, kernel, stride, mode: str = "max", out=None, stream=None):
-    """dx of pool2d for [..., H, W] tensors (x may be None for avg)."""
-    torch = _torch()
+    """dx of pool2d for [..., H, W] tensors (for avg, x only sizes dx and is not read)."""
+    if x is None:
+        raise ValueError("pass x (or a tensor of its shape) to size dx")
     kh, kw = kernel
     sh, sw = stride
-    H, W = (x.shape[-2], x.shape[-1]) if x is not None else (None, None)
-    if H is None:
-        raise ValueError("pass x (or a tensor of its shape) to size dx")
-    planes = x.numel() // (H * W)
-    dx = torch.empty_like(x) if out is None else out
+    H, W, planes = _plane_geom(x)
+    _dev(dy, "dy", x.dtype, device=x.device)
+    _check_dy_2d(dy, H, W, kh, kw, sh, sw)
+    if dy.numel() // (dy.shape[-2] * dy.shape[-1]) != planes:
+        raise ValueError("dy must have as many planes as x")
+    dx = _alloc(out, x.shape, x.dtype, x.device)
     m = SS_POOL_MAX if mode == "max" else SS_POOL_AVG
     check(ss_pool2d_backward(x.data_ptr() if mode == "max" else 0, dy.data_ptr(), dx.data_ptr(), planes, H, W,
                              kh, kw, sh, sw, m, _dtype_code(dy), _stream(stream)))
@@ -527,14 +592,16 @@ def conv1d_mc(x, w, out=None, stream=None):
     """Multi-channel conv1d, channels-last: x [B, N, Cin] bfloat16 (CUDA), w [Cout, Cin, k]
     bfloat16 (CUDA, torch conv1d weight order) -> y [B, N-k+1, Cout] float32."""
     torch = _torch()
-    if x.dtype != torch.bfloat16 or w.dtype != torch.bfloat16:
-        raise TypeError("conv1d_mc takes bfloat16 x and w")
-    if not (x.is_cuda and w.is_cuda and x.is_contiguous() and w.is_contiguous()):
-        raise ValueError("x and w must be contiguous CUDA tensors")
+    _dev(x, "x", torch.bfloat16)
+    _dev(w, "w", torch.bfloat16, device=x.device)
+    if x.dim() != 3 or w.dim() != 3:
+        raise ValueError("x must be [B, N, Cin] and w [Cout, Cin, k]")
     B, N, cin = x.shape
     cout, cin2, k = w.shape
     if cin2 != cin:
         raise ValueError("w's Cin does not match x")
-    y = torch.empty((B, N - k + 1, cout), dtype=torch.float32, device=x.device) if out is None else out
+    if k > N:
+        raise SSError(SS_ERR_WINDOW_EXCEEDS_INPUT, f"window exceeds input: k={k} > N={N}")
+    y = _alloc(out, (B, N - k + 1, cout), torch.float32, x.device)
     check(ss_conv1d_mc(x.data_ptr(), w.data_ptr(), y.data_ptr(), B, N, cin, cout, k, _stream(stream)))
     return y

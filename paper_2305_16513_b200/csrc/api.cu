@@ -73,34 +73,9 @@ static int current_sms() {
 
 static int env_int(const char* name, int dflt);
 
-// Dynamic tile scheduler slots (ss_internal.h): a per-device pool of zeroed
-// {next, done} counter pairs; each persistent-kernel launch takes the next slot
-// and the kernel's last CTA zeroes it again on exit.  Launches on one stream
-// reuse slots in order; a slot is only shared by two RUNNING launches if
-// kSchedSlots launches were enqueued while one of them was still running.
-// nullptr (static round-robin tiles) when the pool cannot be made, e.g. on
-// first use inside a stream capture.
-static unsigned long long* sched_slot(cudaStream_t stream) {
-  static std::mutex mu;
-  static unsigned long long* pool[128] = {nullptr};
-  static std::atomic<uint64_t> next{0};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 128) return nullptr;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    if (!pool[dev]) {
-      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-      if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
-      void* ptr = nullptr;
-      const size_t bytes = (size_t)kSchedSlots * 2 * sizeof(unsigned long long);
-      if (cudaMalloc(&ptr, bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
-      if (cudaMemset(ptr, 0, bytes) != cudaSuccess) { cudaGetLastError(); cudaFree(ptr); return nullptr; }
-      pool[dev] = static_cast<unsigned long long*>(ptr);
-    }
-  }
+int dynamic_tiles() {
   static int on = env_int("SS_DYNAMIC_TILES", 1);
-  if (!on) return nullptr;
-  return pool[dev] + 2 * (next.fetch_add(1, std::memory_order_relaxed) % kSchedSlots);
+  return on != 0;
 }
 
 // cuTensorMapEncodeTiled from the driver, without linking libcuda.
@@ -183,20 +158,11 @@ static int tc_min_k() {
   static int v = env_int("SS_CONV_TC_MIN_K", 33);
   return v;
 }
-// SS_CONV_TC_TRACE=1: a 64 x 8 device buffer of CTA-0 role timestamps
-// (debugging only; read back through ss_debug_conv_tc_trace).
-static unsigned long long* g_tc_trace = nullptr;
+// Debug trace of the tensor-core conv: a CALLER-OWNED device buffer of 1024
+// uint64 (64 x 8 CTA-0 role timestamps), set through ss_debug_conv_tc_set_trace
+// (not in ss.h); null (the default) disables it.  The library allocates nothing.
+static std::atomic<unsigned long long*> g_tc_trace{nullptr};
 static std::atomic<uint64_t> g_tc_launches{0};
-static unsigned long long* tc_trace_buf() {
-  static int on = env_int("SS_CONV_TC_TRACE", 0);
-  if (!on) return nullptr;
-  if (!g_tc_trace && cudaMalloc(&g_tc_trace, 1024 * sizeof(unsigned long long)) != cudaSuccess) g_tc_trace = nullptr;
-  return g_tc_trace;
-}
-static int tc_nc() {
-  static int v = env_int("SS_CONV_TC_NC", 64);
-  return v;
-}
 
 // Try the tensor-core conv for the interior outputs of every row (y_int =
 // first interior output of row 0, rows y_pitch apart).  false: not applicable.
@@ -226,15 +192,14 @@ static bool try_conv_tc(const void* x, float* y_int, int64_t N, int64_t batch, i
   // outputs need chunk m + 1's atoms 0 and 1, so chunks [0, m_map - 1) run on the tensor cores
   const int64_t m_map = (p.total_view - 128) / 128 + 1;
   p.m_ext = m_map - 1;
-  const int nc = tc_nc();
+  constexpr int nc = 64;  // chunks of 128 outputs per tile
   if (!encode_chunk_map(&p.tm_b, p.x_view, m_map, p.atoms, nc)) return false;
   for (int j = 0; j < (int)k; ++j) p.taps[j] = taps[j];
-  p.trace = tc_trace_buf();
-  static int lo_slots = env_int("SS_CONV_TC_LO", 0);
-  p.lo_bufs = lo_slots;
+  p.trace = g_tc_trace.load(std::memory_order_relaxed);
+  p.lo_bufs = 2;
   static int mixed = env_int("SS_CONV_TC_MIXED", 1);
   p.mixed = mixed;
-  p.sched = sched_slot(s);
+  p.clc = dynamic_tiles();
   *err = launch_conv_tc(p, nc, s, grid);
   if (*err == cudaErrorInvalidConfiguration) { *err = cudaSuccess; return false; }
   g_tc_launches.fetch_add(1, std::memory_order_relaxed);
@@ -387,7 +352,7 @@ static ss_status_t window_impl(int op, const void* x, void* y, int64_t N, int64_
       char* y_int = static_cast<char*>(y) + 4 * pl;
       if (make_slide_params(p, x, y_int, N, batch, L_int, L, 0)) {
         p.w = w;
-        p.sched = sched_slot(s);
+        p.clc = dynamic_tiles();
         cudaError_t e;
         if (op == kOpConv) {
           for (int j = 0; j < KT; ++j) p.taps[j] = j < w ? taps[j] : 0.0f;
@@ -426,11 +391,11 @@ int ss_abi_version(void) { return SS_ABI_VERSION; }
  * kernel (tests use it to check which path ran). */
 uint64_t ss_debug_conv_tc_launches(void) { return g_tc_launches.load(std::memory_order_relaxed); }
 
-/* Debug hook (not in ss.h): copies the tensor-core conv trace (64 x 8 clock64
- * values) to host memory; returns 0 if tracing is off. */
-int ss_debug_conv_tc_trace(unsigned long long* host) {
-  if (!g_tc_trace) return 0;
-  return cudaMemcpy(host, g_tc_trace, 1024 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) == cudaSuccess;
+/* Debug hook (not in ss.h): later tensor-core conv launches write CTA 0's role
+ * timestamps (64 x 8 clock64 values) into the caller's device buffer of 1024
+ * uint64; null disables. */
+void ss_debug_conv_tc_set_trace(void* device_buf) {
+  g_tc_trace.store(static_cast<unsigned long long*>(device_buf), std::memory_order_relaxed);
 }
 
 int64_t ss_out_len(int64_t N, int64_t w, int64_t stride) {
@@ -688,7 +653,7 @@ ss_status_t ss_conv1d_mc(const void* x, const void* w, float* y, int64_t batch, 
   const bool tc = (cin == 64 || cin == 128) && (cout == 64 || cout == 128) && k <= 9 &&
                   (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
                   encode_mc_map(&p.tm_x, x, batch * N, cin);
-  p.sched = sched_slot(static_cast<cudaStream_t>(stream));
+  p.clc = dynamic_tiles();
   cudaError_t e = launch_conv_mc(p, tc, static_cast<cudaStream_t>(stream), current_sms());
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv1d_mc launch");
 }
@@ -712,7 +677,7 @@ ss_status_t ss_conv2d(const void* x, void* y, int64_t planes, int64_t H, int64_t
   p.OH = (H - kh) / sh + 1; p.OW = (W - kw) / sw + 1;
   if (overlaps(x, planes * H * W * 4, y, planes * p.OH * p.OW * 4)) return fail(SS_ERR_OVERLAP, "x and y overlap");
   for (int64_t t = 0; t < kh * kw; ++t) p.taps[t] = filter_host[t];
-  p.sched = sched_slot(static_cast<cudaStream_t>(stream));
+  p.clc = dynamic_tiles();
   cudaError_t e = launch_conv2d(p, static_cast<cudaStream_t>(stream), current_sms());
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv2d launch");
 }
@@ -783,7 +748,7 @@ ss_status_t ss_pool2d(const void* x, void* y, int64_t planes, int64_t H, int64_t
   p.inv_area = (float)(1.0 / (double)(kh * kw));
   p.bulk = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (W % 4 == 0);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  p.sched = sched_slot(s);
+  p.clc = dynamic_tiles();
   cudaError_t e = launch_pool2d(p, s, current_sms());
   if (e == cudaErrorInvalidConfiguration) e = launch_pool2d_direct(p, s, current_sms() * 8);
   if (e == cudaSuccess) return SS_OK;

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
   constexpr uint32_t kWTap = AT * COUT * 128u;        // one tap of the weights
   constexpr int NH = COUT / 2;                        // epilogue columns per warp
   constexpr uint32_t kTmemCols = 2 * COUT <= 128 ? 128 : 256;
-  extern __shared__ __align__(1024) uint8_t mc_raw[];
+  extern __shared__ __align__(16) uint8_t mc_raw[];  // aligned to 1024 by hand (slack in conv_mc_smem_bytes)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(mc_raw) + 1023) & ~uintptr_t(1023));
   const int k = (int)p.k;
   uint8_t* xs = smem;                                  // [kMcStages][AT][kMcRows][128 B]
@@ -127,11 +127,13 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
   int64_t* tring = reinterpret_cast<int64_t*>(tempty + kMcRing);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tring + kMcRing);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ ClcSmem clc;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kMcStages; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(dfull + i, 1); mbar_init(dempty + i, kMcEpiWarps); }
     for (int i = 0; i < kMcRing; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, kMcEpiWarps); }
+    clc_init(&clc);
     fence_mbar_init();
     prefetch_tmap(&p.tm_x);
   }
@@ -159,10 +161,11 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
   const int64_t ntiles = p.ntiles;
 
   if (warp == 0) {
-    if (lane == 0) {  // producer: tile b, then dynamic claims (or + gridDim.x)
+    if (lane == 0) {  // producer: tile b, then claims by cluster launch control (or + gridDim.x)
       int s = 0;
-      uint32_t ph = 0;
+      uint32_t ph = 0, cph = 0;
       int64_t t = blockIdx.x;
+      if (p.clc && t < ntiles) clc_request(&clc);
       for (int it = 0;; ++it) {
         const int ts = it % kMcRing;
         mbar_wait(tempty + ts, ((uint32_t)(it / kMcRing) & 1u) ^ 1u);
@@ -173,15 +176,16 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
           mbar_arrive(full + s);
           break;
         }
-        const int64_t tnext = p.sched ? (int64_t)atomicAdd(p.sched, 1ull) + gridDim.x : t + gridDim.x;
         mbar_arrive_expect_tx(full + s, kStage);
         tma_load_3d_mc(xs + (size_t)s * kStage, &p.tm_x, 0, (int32_t)(t * 128), 0, full + s);
         if (++s == kMcStages) { s = 0; ph ^= 1; }
-        t = tnext;
-      }
-      if (p.sched && atomicAdd(p.sched + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
-        p.sched[0] = 0;
-        p.sched[1] = 0;
+        if (p.clc) {
+          t = clc_wait(&clc, cph);  // requested one tile ahead
+          if (t < 0) t = ntiles;
+          else clc_request(&clc);
+        } else {
+          t += gridDim.x;
+        }
       }
     }
   } else if (warp == kMcWarpMma) {
@@ -298,8 +302,10 @@ static cudaError_t launch_mc(ConvMcParams& p, cudaStream_t stream, int sms) {
   auto kfn = conv_mc_kernel<CIN, COUT>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
   if (e != cudaSuccess) return e;
-  const int64_t g = p.ntiles < sms ? p.ntiles : sms;
-  kfn<<<(unsigned)(g < 1 ? 1 : g), kMcThreads, smem, stream>>>(p);
+  // one CTA per SM (each allocates TMEM): pad the request past half the budget
+  const size_t smem_req = smem > (size_t)kSmemBudget / 2 ? smem : (size_t)kSmemBudget / 2 + 1024;
+  const int64_t g = launch_grid(p.ntiles, sms, p.clc);
+  kfn<<<(unsigned)g, kMcThreads, smem_req, stream>>>(p);
   note_launch();
   return cudaGetLastError();
 }

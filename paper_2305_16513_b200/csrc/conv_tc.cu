@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
   constexpr int kK = 32 * KA;
   static_assert(NC % 32 == 0 && NC <= 128, "NC/2 columns per epilogue warp, loaded 16 at a time");
   constexpr int kBlockRows = TcShape<NC>::kBlockRows, ND = TcShape<NC>::kDBufs;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  extern __shared__ __align__(16) uint8_t smem_raw[];  // aligned to 1024 by hand (slack in conv_tc_smem_bytes)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Rings of tile stages: 4 K-atom blocks of kBlockRows chunks x 128 B.  K-atoms 4 and 5 of
@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tring + kTcTileRing);
   float* fsm = reinterpret_cast<float*>(tslot + 4);  // [2][kConvTcMaxK + 256] zero-padded hi/lo taps
 
+  __shared__ ClcSmem clc;
   // ---- setup: barriers, TMEM, taps -----------------------------------------
   tc_trace_stamp(p.trace, 0);
   if (threadIdx.x == 0) {
@@ -247,6 +248,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
     for (int i = 0; i < SL; ++i) { mbar_init(lofull + i, kTcSplitWarps); mbar_init(loempty + i, 1); }
     for (int i = 0; i < ND; ++i) { mbar_init(dfull + i, 1); mbar_init(dempty + i, kTcEpiWarps); }
     for (int i = 0; i < kTcTileRing; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, kTcTileReaders); }
+    clc_init(&clc);
     fence_mbar_init();
     prefetch_tmap(&p.tm_b);
   }
@@ -273,15 +275,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
   if (warp == kTcWarpProducer) {
     tc_trace_stamp(p.trace, 1);
     if (lane == 0) {
-      // tiles: CTA b starts with tile b, then claims tiles from the launch's
-      // counter slot (dynamic: SMs that run faster take more tiles) or, without
-      // a slot, strides by gridDim.x
+      // tiles: CTA b starts with tile b, then claims tiles by cluster launch
+      // control (dynamic: SMs that run faster take more tiles) or strides by gridDim.x
       int s = 0;
-      uint32_t ph = 0;
+      uint32_t ph = 0, cph = 0;
       int64_t t = blockIdx.x;
+      if (p.clc && t < p.ntiles) clc_request(&clc);
       for (int it = 0;; ++it) {
         const int ts = it % kTcTileRing;
         bar_wait(tempty + ts, ((uint32_t)(it / kTcTileRing) & 1u) ^ 1u);
+        if (t < 0) t = p.ntiles;
         tring[ts] = t < p.ntiles ? t : -1;
         mbar_arrive(tfull + ts);
         if (t >= p.ntiles) {
@@ -291,13 +294,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
           mbar_arrive(full + s);
           break;
         }
-        const int64_t tnext = p.sched ? (int64_t)atomicAdd(p.sched, 1ull) + gridDim.x : t + gridDim.x;
         bar_wait(empty + s, ph ^ 1);
         mbar_arrive_expect_tx(full + s, kSlot);
         tma_load_3d(hi + (size_t)s * kSlot, &p.tm_b, 0, (int32_t)(t * NC), 0, full + s);
         if (++s == SH) { s = 0; ph ^= 1; }
         TC_TRACE(it, 0);
-        t = tnext;
+        if (p.clc) {
+          t = clc_wait(&clc, cph);  // requested one tile ahead
+          if (t >= 0) clc_request(&clc);
+        } else {
+          t += gridDim.x;
+        }
       }
     }
     __syncwarp();
@@ -478,9 +485,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
     int d = 0;
     uint32_t dph = 0;
     int it = 0;
+    bool did_last = false;  // this CTA computed the last tile: it also does the array tail
     for (;; ++it) {
       const int64_t t = next_tile(it);
       if (t < 0) break;
+      did_last |= t == p.ntiles - 1;
       bar_wait(dfull + d, dph);
       if (warp == kTcWarpEpi0 && lane == 0) TC_TRACE(it, 7);
       tc_fence_after();
@@ -522,7 +531,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
     // view positions beyond the tensor map (array tail, < 320): direct FMA windows on all
     // 256 epilogue threads, the window's loads issued together (a serial load->FMA chain
     // here cost ~8 us at the end of the kernel)
-    if (blockIdx.x == gridDim.x - 1) {
+    if (did_last) {  // (with CLC the grid's last CTA may never run: it can be canceled)
       const float* __restrict__ xv = p.x_view;
       const int e = 32 * (warp - kTcWarpEpi0) + lane;
       for (int64_t pos = 128 * p.m_ext + e; pos < p.total_view; pos += 32 * kTcEpiWarps) {
@@ -544,13 +553,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
   tc_fence_before();
   __syncthreads();
   tc_trace_stamp(p.trace, 2);
-  if (p.sched && threadIdx.x == 32 * kTcWarpMma) {
-    // every producer of this CTA has stopped claiming; the last CTA out re-zeroes the slot
-    if (atomicAdd(p.sched + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
-      p.sched[0] = 0;
-      p.sched[1] = 0;
-    }
-  }
   if (warp == kTcWarpMma) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
@@ -573,8 +575,7 @@ static cudaError_t launch_nc(ConvTCParams& p, cudaStream_t stream, int grid) {
   auto kfn = conv_tc_kernel<NC, kMixed, KA>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
   if (e != cudaSuccess) return e;
-  int64_t g = p.ntiles < grid ? p.ntiles : grid;
-  if (g < 1) g = 1;
+  const int64_t g = launch_grid(p.ntiles, grid, p.clc);
   kfn<<<(unsigned)g, kTcThreads, conv_tc_smem_bytes(SH, p.lo_bufs, NC), stream>>>(p);
   note_launch();
   return cudaGetLastError();
@@ -584,11 +585,10 @@ cudaError_t launch_conv_tc(ConvTCParams& p, int nc, cudaStream_t stream, int gri
   // K = 32 KA >= 127 + k: 160 covers k <= 33, 192 covers k <= 65
   const int ka = 127 + p.k <= 160 ? 5 : 6;
   const bool mixed = p.mixed != 0;
-  if (nc != 64 && nc != 128) return cudaErrorInvalidValue;
+  if (nc != 64) return cudaErrorInvalidValue;
 #define SS_TC_LAUNCH(NC_, M_, KA_) \
   if (nc == NC_ && mixed == M_ && ka == KA_) return launch_nc<NC_, M_, KA_>(p, stream, grid);
   SS_TC_LAUNCH(64, true, 5) SS_TC_LAUNCH(64, true, 6) SS_TC_LAUNCH(64, false, 5) SS_TC_LAUNCH(64, false, 6)
-  SS_TC_LAUNCH(128, true, 5) SS_TC_LAUNCH(128, true, 6) SS_TC_LAUNCH(128, false, 5) SS_TC_LAUNCH(128, false, 6)
 #undef SS_TC_LAUNCH
   return cudaErrorInvalidValue;
 }

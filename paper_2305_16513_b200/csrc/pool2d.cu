@@ -173,12 +173,14 @@ pool2d_vec_kernel(const __grid_constant__ Pool2DParams p) {
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
   uint64_t* empty = full + S;
   int64_t* pid = reinterpret_cast<int64_t*>(empty + S);  // plane of each stage (-1: no more)
+  __shared__ ClcSmem clc;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kP2VWarps);
     }
+    clc_init(&clc);
     fence_mbar_init();
   }
   __syncthreads();
@@ -186,7 +188,7 @@ pool2d_vec_kernel(const __grid_constant__ Pool2DParams p) {
   const uint32_t plane_bytes = (uint32_t)(plane_elems * 4);
 
   if (warp == kP2VWarps) {  // producer
-    if (lane == 0) plane_producer(p.planes, p.sched, S, full, empty, pid, [&](int64_t pl, int s) {
+    if (lane == 0) plane_producer(p.planes, p.clc, &clc, S, full, empty, pid, [&](int64_t pl, int s) {
       mbar_arrive_expect_tx(&full[s], plane_bytes);
       bulk_load_1d(smem + (size_t)s * p.stage_bytes, p.x + pl * plane_elems, plane_bytes, &full[s]);
     });
@@ -300,8 +302,8 @@ static cudaError_t launch_vec(Pool2DParams& p, cudaStream_t stream, int grid) {
   auto kfn = pool2d_vec_kernel<Op, KH, KW, SH, SW>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
   if (e != cudaSuccess) return e;
-  int64_t g = p.planes < grid ? p.planes : grid;
-  kfn<<<(unsigned)(g < 1 ? 1 : g), kP2VThreads, smem, stream>>>(p);
+  const int64_t g = launch_grid(p.planes, grid, p.clc);
+  kfn<<<(unsigned)g, kP2VThreads, smem, stream>>>(p);
   note_launch();
   return cudaGetLastError();
 }

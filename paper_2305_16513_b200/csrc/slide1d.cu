@@ -483,12 +483,14 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
   TileHdr* hdr = reinterpret_cast<TileHdr*>(empty + S);
   const uint32_t smem_s = smem_u32(smem);
 
+  __shared__ ClcSmem clc;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kWarps);
     }
+    clc_init(&clc);
     fence_mbar_init();
   }
   if (warp == kWarps && lane == 0) {
@@ -501,17 +503,17 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
   if (warp == kWarps) {
     // ---------------- producer: one lane walks the tiles, publishes headers, issues TMA
     if (lane == 0) {
-      // CTA b starts with tile b, then claims tiles from the launch's counter slot
+      // CTA b starts with tile b, then claims tiles by cluster launch control
       // (dynamic: SMs that stream faster take more tiles) or strides by gridDim.x
       const int64_t tpr = p.tiles_per_row;
       int it = 0;
+      uint32_t cph = 0;
       TileCursor tc;
       tc.init(blockIdx.x, tpr);
-      for (int64_t tau = blockIdx.x; tau < p.ntiles;) {
+      if (p.clc && (int64_t)blockIdx.x < p.ntiles) clc_request(&clc);
+      for (int64_t tau = blockIdx.x; tau >= 0 && tau < p.ntiles;) {
         const TileGeom g = tile_geom<kTileRows>(p, tc);
         const int64_t b_cur = tc.b;
-        // claim the next tile now: the atomic's round trip overlaps the slot wait and the TMA issue
-        const int64_t tau_next = p.sched ? (int64_t)atomicAdd(p.sched, 1ull) + gridDim.x : tau + gridDim.x;
         if (!g.empty) {
           const int s = it % S;
           mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
@@ -538,22 +540,22 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
           }
           ++it;
         }
-        if (p.sched) {
-          tc.init(tau_next, tpr);
+        if (p.clc) {
+          // the claim was requested one tile ahead: its round trip overlapped the slot wait and the TMA issue
+          tau = clc_wait(&clc, cph);
+          if (tau >= 0) {
+            clc_request(&clc);
+            tc.init(tau, tpr);
+          }
         } else {
           tc.advance(gridDim.x, tpr);
+          tau += gridDim.x;
         }
-        tau = tau_next;
       }
       const int s = it % S;  // end marker
       mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
       hdr[s].flags = 2;
       mbar_arrive(&full[s]);
-      // this CTA has stopped claiming; the last one to stop re-zeroes the slot
-      if (p.sched && atomicAdd(p.sched + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
-        p.sched[0] = 0;
-        p.sched[1] = 0;
-      }
     }
     return;
   }
@@ -677,8 +679,7 @@ static cudaError_t launch_kind(Slide1DParams& p, cudaStream_t stream, int grid) 
   auto kfn = slide1d_tma_kernel<Kind>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
   if (e != cudaSuccess) return e;
-  int64_t g = p.ntiles < grid ? p.ntiles : grid;
-  if (g < 1) g = 1;
+  const int64_t g = launch_grid(p.ntiles, grid, p.clc);
   kfn<<<(unsigned)g, kThreads, smem, stream>>>(p);
   note_launch();
   return cudaGetLastError();

@@ -190,32 +190,83 @@ __device__ __forceinline__ To bitcast(From v) {
 }
 
 
-// Producer side of a plane (or tile) ring with dynamic claims: CTA b starts with
-// unit b, then claims units from the launch's counter slot sched = {next, done}
-// (null: strides by gridDim.x).  For each unit it waits for the stage, publishes
-// the unit id in pid[stage] and calls load(unit, stage), which must arm full[stage]
-// (release: consumers read pid after their full wait); the end marker is
-// pid = -1 with a plain arrive.  The last CTA to stop claiming re-zeroes the slot.
+// ---------------------------------------------------------------- work claims
+// Dynamic work distribution by cluster launch control (sm_100 CLC): the grid
+// has one CTA per work unit (tile / plane); a running CTA cancels the launch of
+// a CTA that has not started yet and processes that CTA's unit itself, so the
+// SMs that stream faster take more units and the kernel ends on its slowest
+// unit, not its slowest SM.  The claim lives in the hardware scheduler: no
+// global memory, nothing shared between launches or graph replays (ss.h
+// ownership contract).  With clc == 0 the kernels stride statically by
+// gridDim.x over a persistent grid instead (SS_DYNAMIC_TILES=0, A/B only).
+struct alignas(16) ClcSmem {
+  uint4 resp;    // 16-B try_cancel response
+  uint64_t bar;  // its mbarrier (arrival count 1, tx 16 B)
+};
+
+__device__ __forceinline__ void clc_init(ClcSmem* c) { mbar_init(&c->bar, 1); }
+
+// One thread: request the cancellation of a not-yet-launched CTA.  At most one
+// request may be outstanding; none may follow a failed response.
+__device__ __forceinline__ void clc_request(ClcSmem* c) {
+  fence_proxy_async_smem();  // the previous response was read by the generic proxy
+  mbar_arrive_expect_tx(&c->bar, 16);
+  asm volatile(
+      "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];" ::"r"(
+          smem_u32(&c->resp)),
+      "r"(smem_u32(&c->bar))
+      : "memory");
+}
+
+// Wait for the outstanding request (phase bit `ph`, flipped here); returns the
+// x index of the canceled CTA -- the claimed unit -- or -1 if none was left.
+__device__ __forceinline__ int64_t clc_wait(ClcSmem* c, uint32_t& ph) {
+  mbar_wait(&c->bar, ph);
+  ph ^= 1u;
+  uint32_t ok, id;
+  uint64_t lo, hi;
+  asm volatile(
+      "{\n\t.reg .b128 r;\n\t.reg .pred p;\n\t"
+      "ld.shared.v2.b64 {%2, %3}, [%4];\n\t"
+      "mov.b128 r, {%2, %3};\n\t"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, r;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t"
+      "mov.u32 %1, 0;\n\t"
+      "@p clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, r;\n\t"
+      "}"
+      : "=r"(ok), "=r"(id), "=l"(lo), "=l"(hi)
+      : "r"(smem_u32(&c->resp))
+      : "memory");
+  return ok ? (int64_t)id : -1;
+}
+
+// Producer side of a plane (or tile) ring: CTA b starts with unit b, then claims
+// units by CLC (clc != 0) or strides by gridDim.x.  For each unit it waits for
+// the stage, publishes the unit id in pid[stage] and calls load(unit, stage),
+// which must arm full[stage] (release: consumers read pid after their full
+// wait); the end marker is pid = -1 with a plain arrive.
 template <class Load>
-__device__ __forceinline__ void plane_producer(int64_t units, unsigned long long* sched, int S, uint64_t* full,
+__device__ __forceinline__ void plane_producer(int64_t units, int clc, ClcSmem* cs, int S, uint64_t* full,
                                                uint64_t* empty, int64_t* pid, Load load) {
   int64_t u = blockIdx.x;
+  uint32_t cph = 0;
+  if (clc && u < units) clc_request(cs);
   for (int it = 0;; ++it) {
     const int s = it % S;
     mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
-    if (u >= units) {
+    if (u < 0 || u >= units) {
       pid[s] = -1;
       mbar_arrive(&full[s]);
       break;
     }
-    const int64_t next = sched ? (int64_t)atomicAdd(sched, 1ull) + gridDim.x : u + gridDim.x;
     pid[s] = u;
     load(u, s);
-    u = next;
-  }
-  if (sched && atomicAdd(sched + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
-    sched[0] = 0;
-    sched[1] = 0;
+    if (clc) {
+      u = clc_wait(cs, cph);  // the claim's round trip overlapped the stage wait and the load issue
+      if (u >= 0) clc_request(cs);
+    } else {
+      u += gridDim.x;
+    }
   }
 }
 

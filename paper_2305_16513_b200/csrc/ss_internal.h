@@ -13,11 +13,9 @@ constexpr int kOpConv = 2;
 constexpr int kOpMin = 3;
 // padding modes of the window spec (ss.h ss_pad_mode_t)
 constexpr int kPadZeros = 0, kPadReflect = 1, kPadCircular = 2, kPadReplicate = 3;
-constexpr int kSmemBudget = 227 * 1024;  // max dynamic smem per CTA on sm_100a
-// Dynamic tile scheduling of the persistent kernels: slot = {next, done}; tile
-// n >= gridDim.x of a launch is claimed with atomicAdd(next) + gridDim.x (the
-// first tile of CTA b is b), and the last CTA to finish zeroes the slot.
-constexpr int kSchedSlots = 4096;
+// max dynamic smem per CTA on sm_100a (227 KB) less room for the static
+// ClcSmem work-claim block (ss_device.cuh)
+constexpr int kSmemBudget = 227 * 1024 - 128;
 constexpr int kConvTmaMaxK = 64;          // largest k served by the TMA conv kernel
 constexpr int kPoolTmaMaxW = 1024;        // largest w served by the TMA pool kernel
 constexpr int kSlideWarps = 15;           // consumer warps of the 1-D tile kernel
@@ -46,7 +44,7 @@ struct alignas(64) Slide1DParams {
   int stages;
   int span;
   int has_y_map;
-  unsigned long long* sched;  // dynamic tile counter slot {next, done} (null: static round robin)
+  int clc;  // 1: one CTA per work unit, units claimed by cluster launch control (ss_device.cuh); 0: static stride
   float taps[kConvTmaMaxK];  // conv taps, zero-padded to the kernel's KT
 };
 
@@ -73,10 +71,22 @@ struct Pool2DParams {
   int bulk;             // 1: rows are 16-B aligned -> cp.async.bulk staging
   int mode;             // 0 max, 1 avg
   float inv_area;       // 1 / (kh * kw) for avg
-  unsigned long long* sched;  // dynamic plane counter slot (vector kernel; null: static round robin)
+  int clc;  // 1: one CTA per work unit, units claimed by cluster launch control (ss_device.cuh); 0: static stride
 };
 
 void note_launch();
+// Grid of a work-claiming kernel (ss_device.cuh ClcSmem): one CTA per unit
+// when units are claimed by cluster launch control, else a persistent grid of
+// `persistent` CTAs striding statically (clc is cleared if the unit count does
+// not fit gridDim.x).
+inline int64_t launch_grid(int64_t units, int64_t persistent, int& clc) {
+  if (units < 1) units = 1;
+  if (clc && units <= 0x7fffffffLL) return units;
+  clc = 0;
+  return units < persistent ? units : persistent;
+}
+// SS_DYNAMIC_TILES (read once, default 1): 0 selects the static stride (A/B only).
+int dynamic_tiles();
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize = kSmemBudget) once per kernel
 // per device (thread-safe); returns the first call's status afterwards.
 cudaError_t ensure_smem_attr(const void* kfn);
@@ -124,7 +134,7 @@ struct alignas(64) ConvTCParams {
   int k, K, atoms;         // filter length, MMA K (192), K-atoms (6)
   int hi_stages, lo_bufs;  // group slots (3 K-atoms) of the hi / lo rings (set by launch_conv_tc)
   int mixed;               // 1: TF32 xh*fh + one bf16 correction MMA; 0: 3xTF32
-  unsigned long long* sched;  // dynamic tile counter slot {next, done} (null: static round robin)
+  int clc;  // 1: one CTA per work unit, units claimed by cluster launch control (ss_device.cuh); 0: static stride
   unsigned long long* trace;  // debug: per-tile role timestamps of CTA 0 (null = off)
   float taps[kConvTcMaxK];
 };
@@ -174,7 +184,7 @@ struct Conv2DParams {
   int64_t planes, H, W, OH, OW, kh, kw, sh, sw;
   uint32_t stage_bytes;  // set by launch_conv2d
   int stages;
-  unsigned long long* sched;  // dynamic plane counter slot (vector kernel; null: static round robin)
+  int clc;  // 1: one CTA per work unit, units claimed by cluster launch control (ss_device.cuh); 0: static stride
   float taps[1024];      // row-major [kh][kw], kh * kw <= SS_K_MAX
 };
 cudaError_t launch_conv2d(Conv2DParams& p, cudaStream_t stream, int grid);
@@ -203,7 +213,7 @@ struct alignas(64) ConvMcParams {
   float* y;          // [batch][L][cout] fp32
   int64_t batch, N, L, cin, cout, k;
   int64_t ntiles;    // set by launch_conv_mc
-  unsigned long long* sched;  // dynamic tile counter slot (null: static round robin)
+  int clc;  // 1: one CTA per work unit, units claimed by cluster launch control (ss_device.cuh); 0: static stride
 };
 bool encode_mc_map(CUtensorMap* m, const void* x, int64_t positions, int64_t cin);
 cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t stream, int sms);

@@ -41,6 +41,15 @@ class SeqShard:
     rank: int
     w_max: int
 
+    def __post_init__(self):
+        # the halo of rank r is the first w_max-1 elements of rank r+1 ALONE: every
+        # shard must hold at least that many, or windows would need rank r+2's data
+        if self.world < 1 or not 0 <= self.rank < self.world or self.w_max < 1 or self.n_total < 1:
+            raise ValueError(f"bad shard geometry {self}")
+        if self.world > 1 and self.n_total // self.world < self.w_max - 1:
+            raise ValueError(f"sequence of {self.n_total} over {self.world} ranks: shards of "
+                             f"{self.n_total // self.world} < w_max-1 = {self.w_max - 1}; shard fewer ranks")
+
     @property
     def start(self) -> int:
         return even_split(self.n_total, self.world, self.rank)[0]

@@ -80,12 +80,13 @@ def trace():
     synth.fill_device(x, "normal", 3)
     f = synth.normal(4, k, sigma=synth.cfg_sigma_filter(k))
     y = torch.empty(B, N - k + 1, device="cuda")
+    tbuf = torch.zeros(1024, dtype=torch.int64, device="cuda")  # caller-owned trace buffer
+    ss.lib.ss_debug_conv_tc_set_trace(ctypes.c_void_p(tbuf.data_ptr()))
     for _ in range(int(os.environ.get("REPS", "3"))):
         ss.conv1d(x, f, out=y)
     torch.cuda.synchronize()
-    buf = (ctypes.c_ulonglong * 1024)()
-    assert ss.lib.ss_debug_conv_tc_trace(buf)
-    allv = np.array(buf, dtype=np.int64)
+    ss.lib.ss_debug_conv_tc_set_trace(ctypes.c_void_p(0))
+    allv = tbuf.cpu().numpy()
     t = allv[:512].reshape(64, 8)
 
     t0 = t[0, 0]

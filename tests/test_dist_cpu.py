@@ -99,3 +99,13 @@ def test_seq_shard_output_counts():
         for s in shards[:-1]:
             assert s.n_outputs(w) == s.size and s.halo == w - 1
         assert shards[-1].halo == 0
+
+
+def test_seq_shard_rejects_shards_shorter_than_halo():
+    # rank r's halo must come from rank r+1 alone: every shard needs >= w_max-1 elements
+    SeqShard(126, 2, 0, 64)  # 63 per shard = w_max-1: fine
+    with pytest.raises(ValueError):
+        SeqShard(125, 2, 0, 64)
+    with pytest.raises(ValueError):
+        SeqShard(100, 8, 3, 31)
+    SeqShard(10, 1, 0, 64 + 1)  # one rank: no halo, the window check is the kernel's

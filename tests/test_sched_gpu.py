@@ -1,11 +1,15 @@
-"""Dynamic tile claims of the persistent kernels (api.cu sched_slot, DESIGN.md
-"Dynamic tile claims"): which SM computes a tile must not change any output,
-a launch slot must come back zeroed so it can be reused (every call, every
-CUDA-graph replay), and launches running concurrently on two streams must not
-disturb each other.  Covers the 1-D TMA tile kernel (sum / max / conv k <= 32),
-the tensor-core conv (k = 63), the 2-D pooling and 2-D conv vector kernels and
-the multi-channel conv, against eager single-stream results (bit for bit) and
-against the static round-robin schedule (SS_DYNAMIC_TILES=0, subprocess)."""
+"""Dynamic work claims of the persistent kernels by cluster launch control
+(ss_device.cuh ClcSmem): the grid has one CTA
+per tile / plane and running CTAs cancel not-yet-launched CTAs to take their
+units, so the claim state lives in the hardware scheduler -- the library keeps
+no device memory and no state between launches (include/ss.h ownership).
+Which SM computes a unit must not change any output; calls on concurrent
+streams, graph replays (including two captured graphs replayed concurrently,
+and a capture that is the very first call of the process) must not disturb
+each other.  Covers the 1-D TMA tile kernel (sum / max / conv k <= 32), the
+tensor-core conv (k = 63), the 2-D pooling and 2-D conv vector kernels and the
+multi-channel conv, against eager single-stream results (bit for bit) and
+against the static schedule (SS_DYNAMIC_TILES=0, subprocess)."""
 import os
 import subprocess
 import sys
@@ -53,7 +57,6 @@ def test_repeated_calls_and_concurrent_streams_bitwise(ss):
     calls = workload(ss)
     ref = {n: fn().clone() for n, fn in calls}
     torch.cuda.synchronize()
-    # every call takes a fresh slot; slots come back zeroed (4096 > calls made here)
     for _ in range(3):
         for n, fn in calls:
             assert torch.equal(fn(), ref[n]), n
@@ -72,14 +75,14 @@ def test_repeated_calls_and_concurrent_streams_bitwise(ss):
 
 def test_graph_replays_bitwise(ss):
     calls = workload(ss, seed=1)
-    ref = {n: fn().clone() for n, fn in calls}  # eager first: the slot pool exists before capture
+    ref = {n: fn().clone() for n, fn in calls}
     torch.cuda.synchronize()
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
         outs = [(n, fn()) for n, fn in calls]
-    for _ in range(5):  # the same slots on every replay: each kernel re-zeroes its slot
+    for _ in range(5):
         g.replay()
         torch.cuda.synchronize()
         for n, y in outs:
@@ -105,3 +108,63 @@ def test_static_and_dynamic_schedules_agree(tmp_path):
         res[dyn] = np.load(out)
     for n in res["0"].files:
         np.testing.assert_array_equal(res["0"][n], res["1"][n], err_msg=n)
+
+
+def test_concurrent_graph_replays_and_eager_bitwise(ss):
+    """Two graphs of the same launches, replayed at the same time on two streams
+    while eager calls run on a third: no claim of one launch may leak into another."""
+    calls = workload(ss, seed=2)
+    ref = {n: fn().clone() for n, fn in calls}
+    torch.cuda.synchronize()
+    graphs = []
+    for _ in range(2):
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            outs = [(n, fn()) for n, fn in calls]
+        graphs.append((g, outs))
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    torch.cuda.synchronize()
+    for _ in range(4):
+        eager = []
+        for (g, _), st in zip(graphs, streams):
+            with torch.cuda.stream(st):
+                g.replay()
+        with torch.cuda.stream(streams[2]):
+            eager = [(n, fn()) for n, fn in calls]
+        torch.cuda.synchronize()
+        for _, outs in graphs:
+            for n, y in outs:
+                assert torch.equal(y, ref[n]), n
+        for n, y in eager:
+            assert torch.equal(y, ref[n]), n
+
+
+_CAPTURE_FIRST = r"""
+import sys, torch, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import paper_2305_16513_b200 as ss
+from test_sched_gpu import workload
+calls = workload(ss, seed=3)
+torch.cuda.synchronize()
+s = torch.cuda.Stream()
+s.wait_stream(torch.cuda.current_stream())
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=s):   # the first libss calls of this process
+    outs = [(n, fn()) for n, fn in calls]
+g.replay(); g.replay()
+torch.cuda.synchronize()
+cap = {{n: y.float().cpu().numpy() for n, y in outs}}
+ref = {{n: fn().float().cpu().numpy() for n, fn in calls}}
+for n in ref:
+    assert np.array_equal(cap[n], ref[n]), n
+print("capture-first ok")
+"""
+
+
+def test_first_call_inside_capture():
+    code = _CAPTURE_FIRST.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ), cwd=ROOT, timeout=600,
+                       capture_output=True, text=True)
+    assert r.returncode == 0 and "capture-first ok" in r.stdout, r.stdout + r.stderr
