@@ -2,47 +2,51 @@
 """Benchmark of the sliding-window-sum hot path (arXiv 2305.16513) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload suite|cfg1..cfg5|...]
-                    [--impl ours|reference] [--no-e2e] [--no-cpu-baseline] [--cells-out F]
-                    [--graph | --no-graph] [--cell-timing separate|inline]
+                    [--impl ours|reference] [--no-e2e] [--no-cpu-baseline] [--no-cfg5]
+                    [--verify] [--cells-out F] [--dist-backend nccl|gloo]
 
 One STEP = one pass of the whole hot path over one batch of the workload's
 synthetic inputs (BASELINE.json configs, seeded, generated on the device by
 synth/ -- the same counter-based stream the oracle side regenerates on the
-host).  Default workload "suite" = every BASELINE.json cell measured at one
-GPU except the oracle-sized config 1 and the 16 GiB config 5 (run those with
---workload cfg1 / cfg5):
+host).  Default workload "suite" = BASELINE.json configs 2-4 (config 1 is the
+oracle-sized case: --workload cfg1):
     cfg2: int32 N=2^26 sliding sum and max, w in {3,16,64,256}      (8 launches)
     cfg3: fp32 64 x 2^20 conv1d, k in {3,5,7,15,31,63}               (6 launches)
     cfg4: fp32 NCHW 32x64x112x112 max/avg pool 3x3 s1 and 2x2 s2     (4 launches)
+plus, as a sub-record ("cfg5" in the JSON line), config 5: one fp32 sequence
+of 2^32 elements, conv k=31 + max w=64, split over the N ranks (strong).
 Metric (BASELINE.json): output GElem/s (whole job, all ranks) plus achieved
 HBM GB/s = (input bytes + output bytes) / time.
 
 Timing: W untimed warm-up steps, then K steps bracketed by barrier +
 cuda.synchronize on both sides, timed with CUDA events on the launch stream,
-max over ranks.  On one GPU the step is captured once as a CUDA graph and
-replayed (--no-graph: eager launches; multi-GPU is always eager: the halo
-exchange is not captured).  Per-kernel durations (-> the dominant kernel's
-roofline) come from CUDA events around every launch on the same stream, in an
-eager pass of K more steps right after the timed ones (--cell-timing
-separate, default: an event pair between every two kernels costs ~7% of the
-step), or inside the timed eager steps (--cell-timing inline).  L2: every
-cell's input is larger than L2 (126 MB) or, for cfg4, each cell reads its own
-copy of the input, so no cell starts with its input L2-resident.
+max over ranks.  At every N the kernels of a step are two captured CUDA graphs:
+A = every interior (all of a batch-sharded cell), B = the sequence-shard tails;
+the NCCL halo is posted eagerly before A and waited before B.  Per-kernel
+durations (-> the dominant kernel's roofline) time each cell alone as a graph
+of --cell-reps launches alternating over two input/output buffer sets (no
+launch starts with its input in L2, every launch pays its own write-back);
+their sum is reported against the step time.  L2: every cell's input is larger
+than L2 (126 MB) or, for cfg4, each cell reads its own copy of the input.
 
-Multi-GPU (torchrun, one rank per GPU, NCCL): cfg2 / cfg5 are sequence-
-sharded with a (w_max-1)-element halo exchanged by NCCL send/recv and
-overlapped with the interior kernels; cfg3 / cfg4 are batch-sharded with no
-collective; cfg1 runs as replicas.  Default --scaling weak: the global problem
-is the BASELINE.json shape times N (N x the rows / images / sequence length),
-so every rank processes one config-sized share ("scaling":"weak");
---scaling strong keeps the BASELINE.json shape and splits it.
+Multi-GPU (one process per GPU, NCCL): `--gpus N` without WORLD_SIZE re-runs
+this command under torch.distributed.run with N ranks (rank 0 prints the
+line).  cfg2 / cfg5 are sequence-sharded with a (w_max-1)-element halo
+exchanged by NCCL send/recv and overlapped with the interior kernels; cfg3 /
+cfg4 are batch-sharded with no collective; cfg1 runs as replicas.  Default
+--scaling weak: the global problem is the BASELINE.json shape times N, so every
+rank processes one config-sized share ("scaling":"weak"); the cfg5 sub-record
+is always strong.  --verify compares every rank's outputs with one unsharded
+call on the regenerated global slice, bit for bit.
 
---impl reference: the CPU oracle (oracle/, plain C, 1 thread) timed on a
-bounded sample of the same workload (rank 0 only) -- the tier's reference arm.
+--impl reference: the CPU oracle (oracle/, plain C, as it stands) timed on a
+bounded sample of the same workload on every host core (rank 0 only) -- the
+tier's reference arm.
 """
 from __future__ import annotations
 
 import argparse
+import copy
 import json
 import os
 import statistics
@@ -110,7 +114,7 @@ class Cell:
         return [self.inp] + ([self.inp2] if self.inp2 else [])
 
 
-def cfg_cells(workload: str):
+def cfg_cells(workload: str, cfg5_log2n: int = 32):
     """(inputs spec, cells) for a workload; inputs spec: key -> dict(shape, dist, seed, kw, shard)."""
     import synth
     inputs, cells = {}, []
@@ -140,7 +144,7 @@ def cfg_cells(workload: str):
         cells.append(Cell("cfg1", "cfg1_max_w8", "max", w=8, inp="x1"))
         cells.append(Cell("cfg1", "cfg1_conv_k8", "conv", w=8, f=synth.uniform_pm1(1, 8), inp="x1"))
     if workload == "cfg5":
-        inputs["x5"] = dict(n=1 << 32, dtype="float32", dist="normal", seed=6, kw={}, shard="seq", w_max=64)
+        inputs["x5"] = dict(n=1 << cfg5_log2n, dtype="float32", dist="normal", seed=6, kw={}, shard="seq", w_max=64)
         cells.append(Cell("cfg5", "cfg5_conv_k31", "conv", w=31,
                           f=synth.normal(7, 31, sigma=synth.cfg_sigma_filter(31)), inp="x5"))
         cells.append(Cell("cfg5", "cfg5_max_w64", "max", w=64, inp="x5"))
@@ -317,7 +321,11 @@ def scale_inputs(inputs, factor: int):
 
 
 class Runner:
-    def __init__(self, workload, world, rank, device, weak=False):
+    """One rank's share of a workload: inputs (nsets independent copies of every
+    input and output, so a cell can be timed over distinct buffers), the launch
+    of every cell through the public C ABI, and the multi-GPU halo plumbing."""
+
+    def __init__(self, workload, world, rank, device, weak=False, nsets=1, cfg5_log2n=32):
         import torch
 
         import paper_2305_16513_b200 as ss
@@ -325,151 +333,167 @@ class Runner:
         from paper_2305_16513_b200 import dist as ssd
         self.torch, self.ss, self.synth, self.ssd = torch, ss, synth, ssd
         self.world, self.rank, self.device = world, rank, device
-        self.inputs_spec, self.cells = cfg_cells(workload)
+        self.inputs_spec, self.cells = cfg_cells(workload, cfg5_log2n)
         if weak and world > 1:
             scale_inputs(self.inputs_spec, world)
         self.stream = torch.cuda.current_stream()
-        self.x = {}      # device inputs (local shard, incl. halo slots)
         self.meta = {}   # per-input sharding geometry
-        self.y = {}      # device outputs per cell
-        self._alloc()
+        self.xs = []     # [set] -> {key: device input (local shard, incl. halo slots)}
+        self.ys = []     # [set] -> {cell name: device output}
+        self.ws = {}     # workspaces (shared by the sets: launches on one stream are ordered)
+        self.wmc = {}    # multi-channel conv weights
+        for _ in range(nsets):
+            self._alloc_set()
+
+    @property
+    def x(self):
+        return self.xs[0]
+
+    @property
+    def y(self):
+        return self.ys[0]
 
     # ---- inputs / outputs
-    def _alloc(self):
-        torch, synth, ssd = self.torch, self.synth, self.ssd
+    def _gen(self, sp, start, shape, dt):
+        t = self.torch.empty(shape, dtype=self.torch.float32 if sp["dtype"] == "bfloat16" else dt,
+                             device=self.device)
+        self.synth.fill_device(t, sp["dist"], sp["seed"], start=start, **sp["kw"])
+        if sp["dtype"] == "bfloat16":  # generated in fp32, rounded once (untimed)
+            t = t.to(self.torch.bfloat16)
+        return t
+
+    def _alloc_set(self):
+        torch, ssd = self.torch, self.ssd
+        xd, yd = {}, {}
         for key, sp in self.inputs_spec.items():
             dt = torch.int32 if sp["dtype"] == "int32" else torch.float32
             if sp["shard"] == "seq":
                 sh = ssd.SeqShard(sp["n"], self.world, self.rank, sp["w_max"])
                 t = torch.zeros(sh.size + sh.halo, dtype=dt, device=self.device)
-                synth.fill_device(t[:sh.size], sp["dist"], sp["seed"], start=sh.start, **sp["kw"])
+                self.synth.fill_device(t[:sh.size], sp["dist"], sp["seed"], start=sh.start, **sp["kw"])
                 self.meta[key] = ("seq", sh)
             elif sp["shard"] == "batch":
                 r0, r1 = ssd.even_split(sp["rows"], self.world, self.rank)
-                t = torch.empty((r1 - r0, sp["n"]), dtype=dt, device=self.device)
-                synth.fill_device(t, sp["dist"], sp["seed"], start=r0 * sp["n"], **sp["kw"])
-                if sp["dtype"] == "bfloat16":  # generated in fp32, rounded once (untimed)
-                    t = t.to(torch.bfloat16)
+                t = self._gen(sp, r0 * sp["n"], (r1 - r0, sp["n"]), dt)
                 self.meta[key] = ("batch", (r1 - r0, sp["n"]))
             elif sp["shard"] == "image":
                 i0, i1 = ssd.even_split(sp["images"], self.world, self.rank)
-                per = sp["C"] * sp["H"] * sp["W"]
-                t = torch.empty((i1 - i0, sp["C"], sp["H"], sp["W"]), dtype=dt, device=self.device)
-                synth.fill_device(t, sp["dist"], sp["seed"], start=i0 * per, **sp["kw"])
+                t = self._gen(sp, i0 * sp["C"] * sp["H"] * sp["W"], (i1 - i0, sp["C"], sp["H"], sp["W"]), dt)
                 self.meta[key] = ("image", (i1 - i0, sp["C"], sp["H"], sp["W"]))
             else:  # replica
-                t = torch.empty(sp["n"], dtype=dt, device=self.device)
-                synth.fill_device(t, sp["dist"], sp["seed"], start=0, **sp["kw"])
+                t = self._gen(sp, 0, (sp["n"],), dt)
                 self.meta[key] = ("replica", sp["n"])
-            self.x[key] = t
+            xd[key] = t
         for c in self.cells:
-            kind, geo = self.meta[c.inp]
-            x = self.x[c.inp]
-            es = x.element_size()
-            if c.op in BWD_OPS:
-                self._alloc_bwd(c)
-                continue
-            if c.op == "conv_mc":
-                rows, n = geo
-                cin, cout, k = c.kh, c.kw, c.w
-                N = n // cin
-                L = N - k + 1
-                self.y[c.name] = torch.empty((rows, L, cout), dtype=torch.float32, device=self.device)
-                self.wmc = getattr(self, "wmc", {})
-                self.wmc[c.name] = torch.from_numpy(c.f).to(self.device).to(torch.bfloat16).contiguous()
-                c.n_out = rows * L * cout
-                c.bytes = rows * N * cin * 2 + c.n_out * 4 + cout * cin * k * 2
-                c.flops = 2 * k * cin * c.n_out
-                continue
-            if c.op in ("pool2d", "conv2d"):
-                B, C, H, W = geo
-                OH, OW = (H - c.kh) // c.sh + 1, (W - c.kw) // c.sw + 1
-                self.y[c.name] = torch.empty((B, C, OH, OW), dtype=x.dtype, device=self.device)
-                c.n_out = B * C * OH * OW
-                c.bytes = (B * C * H * W + c.n_out) * es
-            elif kind == "seq":
-                sh = geo
-                c.n_out = sh.n_outputs(c.w)
-                self.y[c.name] = torch.empty(max(c.n_out, 1), dtype=x.dtype, device=self.device)
-                c.bytes = (sh.size + c.n_out) * es
-            elif kind == "batch" and c.op == "affine":  # y = [U; V]
-                rows, n = geo
-                L = (n - c.w) // c.stride + 1
-                self.y[c.name] = torch.empty((2, rows, L), dtype=x.dtype, device=self.device)
-                c.n_out = rows * L
-                c.bytes = 2 * (rows * n + c.n_out) * es
-            elif kind == "batch":
-                rows, n = geo
-                L = (n + sum(c.pads) - ((c.w - 1) * c.dilation + 1)) // c.stride + 1
-                self.y[c.name] = torch.empty((rows, L), dtype=x.dtype, device=self.device)
-                c.n_out = rows * L
-                c.bytes = (rows * n + c.n_out) * es
-            else:
-                n = geo
-                L = n - c.w + 1
-                self.y[c.name] = torch.empty(L, dtype=x.dtype, device=self.device)
-                c.n_out = L
-                c.bytes = (n + L) * es
-            c.flops = 2 * c.w * c.n_out if c.op == "conv" else (2 * c.kh * c.kw * c.n_out if c.op == "conv2d" else 0)
+            yd[c.name] = self._alloc_out(c, xd)
+        self.xs.append(xd)
+        self.ys.append(yd)
 
-    def _alloc_bwd(self, c):
+    def _alloc_out(self, c, xd):
+        """Output of cell c (and, on the first set, its unit counts / algorithmic bytes)."""
+        torch = self.torch
+        kind, geo = self.meta[c.inp]
+        x = xd[c.inp]
+        es = x.element_size()
+        if c.op in BWD_OPS:
+            return self._alloc_bwd(c, xd)
+        if c.op == "conv_mc":
+            rows, n = geo
+            cin, cout, k = c.kh, c.kw, c.w
+            N = n // cin
+            L = N - k + 1
+            if c.name not in self.wmc:
+                self.wmc[c.name] = torch.from_numpy(c.f).to(self.device).to(torch.bfloat16).contiguous()
+            c.n_out = rows * L * cout
+            c.bytes = rows * N * cin * 2 + c.n_out * 4 + cout * cin * k * 2
+            c.flops = 2 * k * cin * c.n_out
+            return torch.empty((rows, L, cout), dtype=torch.float32, device=self.device)
+        if c.op in ("pool2d", "conv2d"):
+            B, C, H, W = geo
+            OH, OW = (H - c.kh) // c.sh + 1, (W - c.kw) // c.sw + 1
+            y = torch.empty((B, C, OH, OW), dtype=x.dtype, device=self.device)
+            c.n_out = B * C * OH * OW
+            c.bytes = (B * C * H * W + c.n_out) * es
+        elif kind == "seq":
+            sh = geo
+            c.n_out = sh.n_outputs(c.w)
+            y = torch.empty(max(c.n_out, 1), dtype=x.dtype, device=self.device)
+            c.bytes = (sh.size + c.n_out) * es
+        elif kind == "batch" and c.op == "affine":  # y = [U; V]
+            rows, n = geo
+            L = (n - c.w) // c.stride + 1
+            y = torch.empty((2, rows, L), dtype=x.dtype, device=self.device)
+            c.n_out = rows * L
+            c.bytes = 2 * (rows * n + c.n_out) * es
+        elif kind == "batch":
+            rows, n = geo
+            L = (n + sum(c.pads) - ((c.w - 1) * c.dilation + 1)) // c.stride + 1
+            y = torch.empty((rows, L), dtype=x.dtype, device=self.device)
+            c.n_out = rows * L
+            c.bytes = (rows * n + c.n_out) * es
+        else:
+            n = geo
+            L = n - c.w + 1
+            y = torch.empty(L, dtype=x.dtype, device=self.device)
+            c.n_out = L
+            c.bytes = (n + L) * es
+        c.flops = 2 * c.w * c.n_out if c.op == "conv" else (2 * c.kh * c.kw * c.n_out if c.op == "conv2d" else 0)
+        return y
+
+    def _alloc_bwd(self, c, xd):
         """Backward cells: dx (or df + workspace) and the algorithmic bytes / unit counts.
         n_out = gradient elements written (dx), or for the filter gradient the
         rows x L products it reduces."""
         torch = self.torch
-        x = self.x[c.inp]
+        x = xd[c.inp]
         if c.op == "pool2d_bwd":
-            g = self.x[c.inp2]
-            self.y[c.name] = torch.empty_like(x)
+            g = xd[c.inp2]
             c.n_out = x.numel()
             c.bytes = 4 * (x.numel() * (2 if c.mode == "max" else 1) + g.numel())
-            return
+            return torch.empty_like(x)
         if c.op == "conv2d_bwd_in":  # inp = dy [B, C, OH, OW], inp2 = x (shape only)
-            g, xs = x, self.x[c.inp2]
-            self.y[c.name] = torch.empty_like(xs)
+            g, xs = x, xd[c.inp2]
             c.n_out = xs.numel()
             c.bytes = 4 * (g.numel() + xs.numel())
             c.flops = 2 * c.kh * c.kw * g.numel()
-            return
+            return torch.empty_like(xs)
         if c.op == "conv2d_bwd_f":  # inp = x [B, C, H, W], inp2 = dy
-            g = self.x[c.inp2]
-            self.y[c.name] = torch.empty((c.kh, c.kw), dtype=torch.float32, device=self.device)
-            self.ws = getattr(self, "ws", {})
-            self.ws[c.name] = torch.empty(self.ss.ss_conv2d_backward_filter_workspace(c.kh, c.kw), dtype=torch.uint8,
-                                          device=self.device)
+            g = xd[c.inp2]
+            if c.name not in self.ws:
+                self.ws[c.name] = torch.empty(max(8, self.ss.ss_conv2d_backward_filter_workspace(c.kh, c.kw)),
+                                              dtype=torch.uint8, device=self.device)
             c.n_out = g.numel()
             c.bytes = 4 * (x.numel() + g.numel())
             c.flops = 2 * c.kh * c.kw * g.numel()
-            return
+            return torch.empty((c.kh, c.kw), dtype=torch.float32, device=self.device)
         if c.op in ("conv_bwd_in", "sum_bwd"):  # inp = dy [rows, L]
             rows, L = x.shape
             N = L + c.w - 1
-            self.y[c.name] = torch.empty((rows, N), dtype=x.dtype, device=self.device)
             c.n_out = rows * N
             c.bytes = 4 * (rows * L + rows * N)
             c.flops = 2 * c.w * rows * L if c.op == "conv_bwd_in" else 0
-            return
+            return torch.empty((rows, N), dtype=x.dtype, device=self.device)
         rows, N = x.shape                          # inp = x [rows, N], inp2 = dy [rows, L]
-        L = self.x[c.inp2].shape[1]
+        L = xd[c.inp2].shape[1]
         if c.op == "max_bwd":
-            self.y[c.name] = torch.empty((rows, N), dtype=x.dtype, device=self.device)
             c.n_out = rows * N
             c.bytes = 4 * (2 * rows * N + rows * L)
-        else:  # conv_bwd_f
-            self.y[c.name] = torch.empty(c.w, dtype=torch.float32, device=self.device)
-            self.ws = getattr(self, "ws", {})
-            self.ws[c.name] = torch.empty(self.ss.ss_conv1d_backward_filter_workspace(c.w), dtype=torch.uint8,
-                                          device=self.device)
-            c.n_out = rows * L
-            c.bytes = 4 * (rows * N + rows * L + c.w)
-            c.flops = 2 * c.w * rows * L
+            return torch.empty((rows, N), dtype=x.dtype, device=self.device)
+        if c.name not in self.ws:  # conv_bwd_f
+            self.ws[c.name] = torch.empty(max(8, self.ss.ss_conv1d_backward_filter_workspace(c.w)),
+                                          dtype=torch.uint8, device=self.device)
+        c.n_out = rows * L
+        c.bytes = 4 * (rows * N + rows * L + c.w)
+        c.flops = 2 * c.w * rows * L
+        return torch.empty(c.w, dtype=torch.float32, device=self.device)
 
-    def _launch_bwd(self, c):
+    # ---- launches (every step of the path runs in libss through the C ABI)
+    def _launch_bwd(self, c, xd, y):
         ss, st = self.ss, self.stream.cuda_stream
-        x, y = self.x[c.inp], self.y[c.name]
+        x = xd[c.inp]
         if c.op == "pool2d_bwd":
             B, C, H, W = x.shape
-            g = self.x[c.inp2]
+            g = xd[c.inp2]
             ss.check(ss.ss_pool2d_backward(x.data_ptr(), g.data_ptr(), y.data_ptr(), B * C, H, W, c.kh, c.kw, c.sh,
                                            c.sw, ss.SS_POOL_MAX if c.mode == "max" else ss.SS_POOL_AVG,
                                            ss.SS_F32, st))
@@ -480,7 +504,7 @@ class Runner:
         elif c.op == "conv2d_bwd_f":
             B, C, H, W = x.shape
             ws = self.ws[c.name]
-            ss.check(ss.ss_conv2d_backward_filter(x.data_ptr(), self.x[c.inp2].data_ptr(), y.data_ptr(), B * C, H, W,
+            ss.check(ss.ss_conv2d_backward_filter(x.data_ptr(), xd[c.inp2].data_ptr(), y.data_ptr(), B * C, H, W,
                                                   c.kh, c.kw, 1, 1, ws.data_ptr(), ws.numel(), st))
         elif c.op == "conv_bwd_in":
             rows, L = x.shape
@@ -491,16 +515,15 @@ class Runner:
             ss.check(ss.ss_pool_sum_backward(x.data_ptr(), y.data_ptr(), L + c.w - 1, rows, c.w, 1, ss.SS_F32, st))
         elif c.op == "max_bwd":
             rows, N = x.shape
-            ss.check(ss.ss_pool_max_backward(x.data_ptr(), self.x[c.inp2].data_ptr(), y.data_ptr(), N, rows, c.w, 1,
+            ss.check(ss.ss_pool_max_backward(x.data_ptr(), xd[c.inp2].data_ptr(), y.data_ptr(), N, rows, c.w, 1,
                                              ss.SS_F32, st))
         else:
             rows, N = x.shape
             ws = self.ws[c.name]
-            ss.check(ss.ss_conv1d_backward_filter(x.data_ptr(), self.x[c.inp2].data_ptr(), y.data_ptr(), N, rows,
+            ss.check(ss.ss_conv1d_backward_filter(x.data_ptr(), xd[c.inp2].data_ptr(), y.data_ptr(), N, rows,
                                                   c.w, 1, ws.data_ptr(), ws.numel(), st))
 
-    # ---- one launch
-    def _launch_1d(self, c, x, y):
+    def launch_1d(self, c, x, y, v=None):
         ss = self.ss
         s = self.stream.cuda_stream
         code = ss.SS_I32 if x.dtype == self.torch.int32 else ss.SS_F32
@@ -510,7 +533,6 @@ class Runner:
             B, N = x.shape
         win = (c.stride, c.dilation, c.pads[0], c.pads[1], ss.PAD_MODES[c.pad_mode], code, s)
         if c.op == "affine":
-            v = self.x[c.inp2]
             st = ss.ss_affine_window(x.data_ptr(), v.data_ptr(), y[0].data_ptr(), y[1].data_ptr(), N, B, c.w,
                                      c.stride, s)
         elif c.op == "conv":
@@ -523,90 +545,196 @@ class Runner:
             st = ss.ss_pool_max_ex(x.data_ptr(), y.data_ptr(), N, B, c.w, *win)
         ss.check(st)
 
-    def _launch_cell(self, c, events=None):
+    def launch_cell(self, c, si=0, part="whole"):
+        """part: 'whole' (interior + tail), 'interior' (needs no halo) or 'tail'
+        (sequence-sharded cells only: the windows reaching into the halo)."""
+        ss = self.ss
         kind, geo = self.meta[c.inp]
-        x, y = self.x[c.inp], self.y[c.name]
+        xd, y = self.xs[si], self.ys[si][c.name]
+        x = xd[c.inp]
+        if kind == "seq":
+            fn = (lambda xv, yv, c=c: self.launch_1d(c, xv, yv))
+            if part in ("whole", "interior"):
+                self.ssd.run_interior(x, geo, c.w, fn, y)
+            if part in ("whole", "tail"):
+                self.ssd.run_tail(x, geo, c.w, fn, y)
+            return
+        if part == "tail":
+            return
         if c.op in BWD_OPS:
-            ev0 = self._ev(events)
-            self._launch_bwd(c)
-            self._ev_end(events, c, ev0)
+            self._launch_bwd(c, xd, y)
         elif c.op == "conv_mc":
             rows, n = geo
-            ev0 = self._ev(events)
-            self.ss.check(self.ss.ss_conv1d_mc(x.data_ptr(), self.wmc[c.name].data_ptr(), y.data_ptr(), rows,
-                                               n // c.kh, c.kh, c.kw, c.w, self.stream.cuda_stream))
-            self._ev_end(events, c, ev0)
+            ss.check(ss.ss_conv1d_mc(x.data_ptr(), self.wmc[c.name].data_ptr(), y.data_ptr(), rows,
+                                     n // c.kh, c.kh, c.kw, c.w, self.stream.cuda_stream))
         elif c.op == "conv2d":
             B, C, H, W = geo
-            ev0 = self._ev(events)
-            self.ss.check(self.ss.ss_conv2d(x.data_ptr(), y.data_ptr(), B * C, H, W, c.f.reshape(-1).tolist(), c.kh,
-                                            c.kw, c.sh, c.sw, self.ss.SS_F32, self.stream.cuda_stream))
-            self._ev_end(events, c, ev0)
+            ss.check(ss.ss_conv2d(x.data_ptr(), y.data_ptr(), B * C, H, W, c.f_flat, c.kh, c.kw, c.sh, c.sw,
+                                  ss.SS_F32, self.stream.cuda_stream))
         elif c.op == "pool2d":
             B, C, H, W = geo
-            ev0 = self._ev(events)
-            self.ss.check(self.ss.ss_pool2d(x.data_ptr(), y.data_ptr(), B * C, H, W, c.kh, c.kw, c.sh, c.sw,
-                                            self.ss.SS_POOL_MAX if c.mode == "max" else self.ss.SS_POOL_AVG,
-                                            self.ss.SS_F32, self.stream.cuda_stream))
-            self._ev_end(events, c, ev0)
-        elif kind == "seq":
-            ev0 = self._ev(events)
-            self.ssd.run_interior(x, geo, c.w, lambda xv, yv: self._launch_1d(c, xv, yv), y)
-            self._ev_end(events, c, ev0)
+            ss.check(ss.ss_pool2d(x.data_ptr(), y.data_ptr(), B * C, H, W, c.kh, c.kw, c.sh, c.sw,
+                                  ss.SS_POOL_MAX if c.mode == "max" else ss.SS_POOL_AVG, ss.SS_F32,
+                                  self.stream.cuda_stream))
         else:
-            ev0 = self._ev(events)
-            self._launch_1d(c, x, y)
-            self._ev_end(events, c, ev0)
+            self.launch_1d(c, x, y, xd.get(c.inp2) if c.inp2 else None)
 
-    def _ev(self, events):
-        if events is None:
-            return None
-        e = self.torch.cuda.Event(enable_timing=True)
-        e.record(self.stream)
-        return e
+    def seq_keys(self):
+        return [k for k, (kind, _) in self.meta.items() if kind == "seq"]
 
-    def _ev_end(self, events, c, ev0):
-        if events is None:
-            return
-        e = self.torch.cuda.Event(enable_timing=True)
-        e.record(self.stream)
-        events.append((c, ev0, e))
+    def post_halos(self, si=0):
+        """Post every sequence input's halo exchange (one NCCL send/recv pair per
+        neighbour); returns the work handles."""
+        works = []
+        if self.world > 1:
+            for key in self.seq_keys():
+                works += self.ssd.halo_start(self.xs[si][key], self.meta[key][1])
+        return works
 
-    def step(self, events=None, before=None, after=None):
-        """One pass of the hot path over the workload (this rank's share).
-        before(c)/after(c): optional hooks around each cell's launches (the
-        end-to-end loop uses them to chain copies on other streams)."""
-        works = {}
-        for key, (kind, geo) in self.meta.items():  # post halo exchanges first
-            if kind == "seq" and self.world > 1:
-                works[key] = self.ssd.halo_start(self.x[key], geo)
-        for c in self.cells:  # interiors / whole cells
-            if before:
-                before(c)
-            self._launch_cell(c, events)
-            if after and not (self.meta[c.inp][0] == "seq" and works):
-                after(c)
-        for key, wk in works.items():
-            self.ssd.wait_all(wk)
-        if works:
-            for c in self.cells:  # tails
-                kind, geo = self.meta[c.inp]
-                if kind == "seq":
-                    self.ssd.run_tail(self.x[c.inp], geo, c.w,
-                                      lambda xv, yv, c=c: self._launch_1d(c, xv, yv), self.y[c.name])
-                    if after:
-                        after(c)
+    def launch_interiors(self, si=0):
+        for c in self.cells:
+            self.launch_cell(c, si, "interior")
+
+    def launch_tails(self, si=0):
+        for c in self.cells:
+            if self.meta[c.inp][0] == "seq":
+                self.launch_cell(c, si, "tail")
+
+    def step_eager(self, si=0):
+        works = self.post_halos(si)
+        self.launch_interiors(si)
+        self.ssd.wait_all(works)
+        self.launch_tails(si)
+
+    # ---- CUDA graphs: the same launch mode at every N
+    def capture(self, si=0):
+        """Capture the step's kernels as two CUDA graphs: A = every cell's interior
+        (all of it for batch-sharded cells), B = the sequence-sharded tails (empty
+        at N = 1).  The NCCL halo is posted eagerly before A and waited before B.
+        Returns (graph A, graph B or None, libss launches per step)."""
+        torch, ss = self.torch, self.ss
+        n0 = ss.ss_launch_count()
+        ga = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(ga, stream=self.stream):
+            self.launch_interiors(si)
+        gb = None
+        if self.world > 1 and self.seq_keys():
+            gb = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gb, stream=self.stream):
+                self.launch_tails(si)
+        return ga, gb, ss.ss_launch_count() - n0
+
+    def step_graph(self, graphs, si=0):
+        ga, gb, _ = graphs
+        works = self.post_halos(si)
+        ga.replay()
+        self.ssd.wait_all(works)
+        if gb is not None:
+            gb.replay()
+
+    def cell_times(self, reps: int, replays: int):
+        """Per-cell kernel time: each cell captured alone as a graph of `reps`
+        launches alternating over the buffer sets (so no launch finds its input
+        in L2 and every launch pays its own output write-back), replayed
+        `replays` times after one warm replay; CUDA events on the launch stream.
+        Returns {cell name: ms per launch}."""
+        torch = self.torch
+        out = {}
+        nsets = len(self.xs)
+        for c in self.cells:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.stream):
+                for r in range(reps):
+                    self.launch_cell(c, r % nsets, "whole")
+            g.replay()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(self.stream)
+            for _ in range(replays):
+                g.replay()
+            e1.record(self.stream)
+            torch.cuda.synchronize()
+            out[c.name] = e0.elapsed_time(e1) / (reps * replays)
+            del g
+        return out
+
+    # ---- sharded == unsharded (the library against itself, on regenerated global slices)
+    def verify(self, seg: int = 8192):
+        """Recompute sampled outputs from the GLOBAL input regenerated locally
+        (synth is counter-based) with one unsharded call, and compare them with
+        this rank's outputs bit for bit: windows at both ends of every sequence
+        shard (the halo windows) and in its middle, the first and last local row
+        / image of batch-sharded inputs.  Returns (outputs compared, mismatch list)."""
+        torch, synth = self.torch, self.synth
+        n_cmp, bad = 0, []
+        for c in self.cells:
+            kind, geo = self.meta[c.inp]
+            sp = self.inputs_spec[c.inp]
+            y = self.y[c.name]
+            dt = self.x[c.inp].dtype
+            if kind == "seq":
+                sh = geo
+                n_out = sh.n_outputs(c.w)
+                if n_out == 0:
+                    continue
+                lo, hi = sh.start, sh.start + n_out
+                mid = (lo + hi) // 2
+                for o0, o1 in ((lo, lo + seg), (hi - seg, hi), (mid - seg // 2, mid + seg // 2)):
+                    o0, o1 = max(o0, lo), min(o1, hi)
+                    if o1 <= o0:
+                        continue
+                    xg = torch.empty(o1 - o0 + c.w - 1, dtype=dt, device=self.device)
+                    synth.fill_device(xg, sp["dist"], sp["seed"], start=o0, **sp["kw"])
+                    ref = torch.empty(o1 - o0, dtype=dt, device=self.device)
+                    self.launch_1d(c, xg, ref)
+                    torch.cuda.synchronize()
+                    n_cmp += o1 - o0
+                    if not torch.equal(ref, y[o0 - lo:o1 - lo]):
+                        bad.append(f"{c.name} outputs [{o0}, {o1})")
+            elif kind in ("batch", "image") and c.op in ("conv", "sum", "max", "min", "pool2d", "conv2d"):
+                rows = geo[0]
+                g0 = self.ssd.even_split(sp["rows"] if kind == "batch" else sp["images"], self.world, self.rank)[0]
+                per = geo[1] if kind == "batch" else geo[1] * geo[2] * geo[3]
+                for r in sorted({0, rows - 1}):
+                    shape = (1, geo[1]) if kind == "batch" else (1,) + tuple(geo[1:])
+                    xg = torch.empty(shape, dtype=dt, device=self.device)
+                    synth.fill_device(xg, sp["dist"], sp["seed"], start=(g0 + r) * per, **sp["kw"])
+                    ref = torch.empty((1,) + tuple(y.shape[1:]), dtype=y.dtype, device=self.device)
+                    if c.op == "pool2d":
+                        self.ss.pool2d(xg, (c.kh, c.kw), (c.sh, c.sw), c.mode, out=ref)
+                    elif c.op == "conv2d":
+                        self.ss.conv2d(xg, c.f, (c.sh, c.sw), out=ref)
+                    else:
+                        self.launch_1d(c, xg, ref)
+                    torch.cuda.synchronize()
+                    n_cmp += ref.numel()
+                    if conv_on_tensor_cores(c):
+                        # the tensor-core conv rounds by position in the staged view (a row's
+                        # array tail runs on the FFMA path): equal within twice the BJ bound,
+                        # the magnitudes sum|x||f| from the same library on |x|, |f|
+                        mag = torch.empty_like(ref)
+                        cabs = copy.copy(c)
+                        cabs.f = np.abs(c.f)
+                        self.launch_1d(cabs, xg.abs(), mag)
+                        torch.cuda.synchronize()
+                        ok = bool(((ref[0].double() - y[r].double()).abs() <=
+                                   2 * (1e-5 * mag[0].double() + 1e-6)).all())
+                    else:
+                        ok = torch.equal(ref[0], y[r])
+                    if not ok:
+                        bad.append(f"{c.name} local row {r} (global {g0 + r})")
+        return n_cmp, bad
 
     # ---- end to end: pinned host buffers -> device -> kernels -> host
     def setup_e2e(self):
-        """Pinned host buffers for every input and output, and the streams /
-        events of the overlapped end-to-end loop."""
+        """Pinned host buffers for every input (a sequence shard WITHOUT its halo
+        slots: those are filled by the exchange, never from the host) and every
+        output, and the streams / events of the overlapped end-to-end loop."""
         torch = self.torch
-        self.hx = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in self.x.items()}
+        self.own = {k: (self.meta[k][1].size if self.meta[k][0] == "seq" else v.numel()) for k, v in self.x.items()}
+        self.hx = {k: torch.empty(self.own[k], dtype=v.dtype, pin_memory=True) for k, v in self.x.items()}
         for k, v in self.x.items():
-            self.hx[k].copy_(v)
-        # cfg4 cells read distinct device copies in the kernel-only loop; end to end,
-        # every cell gets its own H2D copy too (same bytes).
+            self.hx[k].copy_(v.reshape(-1)[:self.own[k]])
         self.hy = {c.name: torch.empty(self.y[c.name].shape, dtype=self.y[c.name].dtype, pin_memory=True)
                    for c in self.cells}
         torch.cuda.synchronize()
@@ -628,18 +756,20 @@ class Runner:
         pinned memory (copy stream), the kernels (compute stream), D2H of every
         output to pinned memory (second copy stream).  Copies of one cell overlap
         kernels of the next; an input is overwritten only after its last reader
-        of the previous step, an output only after its previous D2H."""
+        of the previous step, an output only after its previous D2H.  Sequence
+        shards: the compute stream waits for the shard's H2D BEFORE the halo is
+        posted (NCCL orders against the compute stream), and the H2D never
+        touches the halo slots the exchange fills."""
         torch = self.torch
         for k in self.x:
             self.s_h2d.wait_event(self.ev_in_free[k])
             with torch.cuda.stream(self.s_h2d):
-                self.x[k].copy_(self.hx[k], non_blocking=True)
+                self.x[k].view(-1)[:self.own[k]].copy_(self.hx[k], non_blocking=True)
             self.ev_in_ready[k].record(self.s_h2d)
-
-        def before(c):
-            for k in c.inputs():
-                self.stream.wait_event(self.ev_in_ready[k])
-            self.stream.wait_event(self.ev_out_free[c.name])
+        for k in self.seq_keys():
+            self.stream.wait_event(self.ev_in_ready[k])
+        works = self.post_halos(0)
+        seq = {c.name for c in self.cells if self.meta[c.inp][0] == "seq"}
 
         def after(c):
             self.ev_out_ready[c.name].record(self.stream)
@@ -651,16 +781,99 @@ class Runner:
                 self.hy[c.name].copy_(self.y[c.name], non_blocking=True)
             self.ev_out_free[c.name].record(self.s_d2h)
 
-        self.step(before=before, after=after)
+        for c in self.cells:
+            for k in c.inputs():
+                self.stream.wait_event(self.ev_in_ready[k])
+            self.stream.wait_event(self.ev_out_free[c.name])
+            self.launch_cell(c, 0, "interior")
+            if c.name not in seq or self.world == 1:
+                after(c)
+        self.ssd.wait_all(works)
+        if self.world > 1:
+            for c in self.cells:
+                if c.name in seq:
+                    self.launch_cell(c, 0, "tail")
+                    after(c)
 
     def e2e_fence(self):
         """Make the compute stream wait for every outstanding copy."""
-        done = self.torch.cuda.Event()
-        done.record(self.s_d2h)
-        self.stream.wait_event(done)
-        done2 = self.torch.cuda.Event()
-        done2.record(self.s_h2d)
-        self.stream.wait_event(done2)
+        for s in (self.s_d2h, self.s_h2d):
+            done = self.torch.cuda.Event()
+            done.record(s)
+            self.stream.wait_event(done)
+
+
+def _dtype_label(cells):
+    """The arithmetic type(s) the timed path computes in, with the tensor-core conv's split precision."""
+    dts = []
+    if any(c.cfg == "cfg2" for c in cells):
+        dts.append("i32")
+    if any(c.cfg != "cfg2" for c in cells):
+        dts.append("f32")
+    lab = "/".join(dts)
+    tc = [c for c in cells if conv_on_tensor_cores(c)]
+    if tc:
+        mode = ("3xTF32" if os.environ.get("SS_CONV_TC_MIXED", "1") == "0"
+                else "TF32 hi*hi + one bf16 correction MMA")
+        lab += f" ({', '.join(c.name for c in tc)}: tensor cores, {mode}, fp32 accumulate)"
+    return lab
+
+
+def run_cfg5(args, world, rank, device, barrier, max_over_ranks, coll):
+    """BASELINE.json config 5 as a sub-record: one fp32 sequence of 2^32 elements
+    (16 GiB), conv k=31 + sliding max w=64, STRONG-scaled (the one sequence split
+    contiguously over the N ranks, (w_max-1)-element NCCL halo), timed like the
+    suite (graphs A / B around the eagerly posted halo, max over ranks)."""
+    import torch
+    R = Runner("cfg5", world, rank, device, weak=False, nsets=1, cfg5_log2n=args.cfg5_log2n)
+    R.step_eager()
+    graphs = R.capture()
+    torch.cuda.synchronize()
+    steps = max(3, min(args.steps, args.cfg5_steps))
+    for _ in range(3):
+        R.step_graph(graphs)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(R.stream)
+        for _ in range(steps):
+            R.step_graph(graphs)
+        t1.record(R.stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = max_over_ranks(t0.elapsed_time(t1))
+    cell_ms = R.cell_times(reps=2, replays=max(1, steps // 4))
+    tot = torch.tensor([float(sum(c.n_out for c in R.cells)), float(sum(c.bytes for c in R.cells))],
+                       dtype=torch.float64, device=coll)
+    if world > 1:
+        torch.distributed.all_reduce(tot)
+    n_out, nbytes = float(tot[0]), float(tot[1])
+    rec = {"workload": f"cfg5: fp32 N=2^{args.cfg5_log2n}, conv k=31 + max w=64, seq-sharded x{world} (strong)",
+           "value": round(n_out * steps / (ms * 1e-3) / 1e9, 3), "unit": "GElem/s",
+           "ms_per_step": round(ms / steps, 4), "steps": steps, "n_gpus": world, "scaling": "strong",
+           "hbm_gbs": round(nbytes * steps / (ms * 1e-3) / 1e9, 1),
+           "cells": {k: round(v, 4) for k, v in cell_ms.items()},
+           "gpu_launches_per_step": int(graphs[2]), "clocks": clk.summary(),
+           "parity": "tests/test_configs_gpu.py::test_cfg5_full_size_and_shard_emulation (oracle, sampled + shard "
+                     "boundaries); --verify: sharded == unsharded"}
+    if args.verify:
+        n_cmp, bad = R.verify()
+        t = torch.tensor([float(n_cmp), float(len(bad))], dtype=torch.float64, device=coll)
+        if world > 1:
+            torch.distributed.all_reduce(t)
+        rec["verify"] = {"compared": int(t[0]), "mismatches": int(t[1]), "first": bad[:4]}
+    del R, graphs
+    torch.cuda.empty_cache()
+    return rec
+
+
+_T0 = time.perf_counter()
+
+
+def _phase(name: str) -> None:
+    """Wall-clock progress of the bench phases on stderr (never part of the JSON line)."""
+    print(f"[bench {time.perf_counter() - _T0:7.1f} s] {name}", file=sys.stderr, flush=True)
 
 
 def run_ours(args):
@@ -671,22 +884,17 @@ def run_ours(args):
     if world > 1:
         torch.cuda.set_device(local % torch.cuda.device_count())
         if args.dist_backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            os.environ.setdefault("NCCL_DEBUG", "INFO")   # keep the communicator init lines in the log
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
         else:  # test mode: several ranks may share a GPU; host-staged halo
             dist.init_process_group("gloo")
     else:
         torch.cuda.set_device(0)
     device = torch.device("cuda", torch.cuda.current_device())
     import paper_2305_16513_b200 as ss
-    weak = args.scaling == "weak"
-    if args.graph is None:  # default: replay the step as a CUDA graph on one GPU (halo exchange is not captured)
-        args.graph = world == 1
-    if args.graph:  # graphs are captured on a non-default stream: run everything there
-        torch.cuda.set_stream(torch.cuda.Stream())
-    R = Runner(args.workload, world, rank, device, weak=weak)
-    torch.cuda.synchronize()
-
-    coll_dev = device if args.dist_backend == "nccl" else torch.device("cpu")
+    torch.cuda.set_stream(torch.cuda.Stream())  # graphs are captured on a non-default stream: run everything there
+    coll = device if args.dist_backend == "nccl" else torch.device("cpu")
 
     def barrier():
         torch.cuda.synchronize()
@@ -700,86 +908,71 @@ def run_ours(args):
     def max_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=coll_dev)
+        t = torch.tensor([v], dtype=torch.float64, device=coll)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    for _ in range(args.warmup):
-        R.step()
+    _phase("init")
+    R = Runner(args.workload, world, rank, device, weak=args.scaling == "weak", nsets=2,
+               cfg5_log2n=args.cfg5_log2n)
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):  # eager warm-up (kernel attributes, tensor maps)
+        R.step_eager()
     barrier()
-    events = []
-    graph = None
-    if args.graph:
-        # capture one step in a CUDA graph and replay it (no host launch gaps between kernels);
-        # per-kernel durations come from one eager pass with events (below)
-        if world > 1:
-            raise SystemExit("--graph is single-GPU only (the halo exchange is not captured)")
-        n_cap0 = ss.ss_launch_count()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=R.stream):
-            R.step()
-        launches_per_step = ss.ss_launch_count() - n_cap0
-        for _ in range(args.warmup):
-            graph.replay()
-        torch.cuda.synchronize()
-    n_launch0 = ss.ss_launch_count()
+    _phase("capture")
+    graphs = R.capture()
+    launches_per_step = graphs[2]
+    for _ in range(args.warmup):
+        R.step_graph(graphs)
+    barrier()
     with ClockSampler(torch.cuda.current_device()) as clk:
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         barrier()
         t0.record(R.stream)
         for _ in range(args.steps):
-            if graph is not None:
-                graph.replay()
-            else:
-                R.step(events if args.cell_timing == "inline" else None)
+            R.step_graph(graphs)
         t1.record(R.stream)
         torch.cuda.synchronize()
         barrier()
-    launches = ss.ss_launch_count() - n_launch0
-    if graph is not None:
-        launches = launches_per_step * args.steps
-    if graph is not None or args.cell_timing == "separate":
-        for _ in range(args.steps):  # instrumented eager pass: the per-kernel event durations
-            R.step(events)
-        torch.cuda.synchronize()
     ms_local = t0.elapsed_time(t1)
     ms = max_over_ranks(ms_local)
-    for c, a, b in events:
-        c.times.append(a.elapsed_time(b))
     out_local = sum(c.n_out for c in R.cells) * args.steps
     bytes_local = sum(c.bytes for c in R.cells) * args.steps
-    tot = torch.tensor([out_local, bytes_local], dtype=torch.float64, device=coll_dev)
+    tot = torch.tensor([out_local, bytes_local], dtype=torch.float64, device=coll)
     if world > 1:
         dist.all_reduce(tot)
     out_total, bytes_total = float(tot[0]), float(tot[1])
     value = out_total / (ms * 1e-3) / 1e9
     hbm_gbs = bytes_total / (ms * 1e-3) / 1e9
 
-    # per-kernel (cell) stats and the dominant kernel
+    _phase("cell timing")
+    # per-kernel (cell) times: each cell alone as a graph over 2 buffer sets
+    reps = 2 * max(2, args.cell_reps // 2)
+    cell_ms = R.cell_times(reps=reps, replays=max(1, args.steps // reps))
     peak_hbm, peak_src = measured_peaks()
     cells = []
     for c in R.cells:
-        avg_ms = sum(c.times) / len(c.times)
+        avg_ms = cell_ms[c.name]
         gbs = c.bytes / (avg_ms * 1e-3) / 1e9
         d = {"cell": c.name, "avg_ms": round(avg_ms, 5), "n_out": c.n_out, "bytes": c.bytes,
              "gelem_s": round(c.n_out / (avg_ms * 1e-3) / 1e9, 2), "gbs": round(gbs, 1),
-             "frac_hbm": round(gbs / peak_hbm, 4), "frac_8tbs": round(gbs / 8000.0, 4),
-             "share": 0.0}
+             "frac_hbm": round(gbs / peak_hbm, 4), "frac_8tbs": round(gbs / 8000.0, 4), "share": 0.0}
         if c.op == "conv_mc":
             d["tc_frac"] = round(c.flops / (avg_ms * 1e-3) / 1e12 / (2 * tf32_peak_tflops()), 4)  # bf16 peak
         elif conv_on_tensor_cores(c):
             d["tc_frac"] = round(c.n_out * TC_FLOP_PER_OUT / (avg_ms * 1e-3) / 1e12 / tf32_peak_tflops(), 4)
         elif c.op in ("conv", "conv_bwd_in", "conv_bwd_f", "conv2d", "conv2d_bwd_in", "conv2d_bwd_f"):
-            fma_s = c.flops / 2 / (avg_ms * 1e-3)
-            d["fma_frac"] = round(fma_s / FP32_FMA_PEAK, 4)
+            d["fma_frac"] = round(c.flops / 2 / (avg_ms * 1e-3) / FP32_FMA_PEAK, 4)
         cells.append(d)
+    step_ms = ms / args.steps
     tot_k = sum(d["avg_ms"] for d in cells)
     for d in cells:
         d["share"] = round(d["avg_ms"] / tot_k, 4)
     dom = max(cells, key=lambda d: d["avg_ms"])
     dom_cell = next(c for c in R.cells if c.name == dom["cell"])
-    if dom_cell.op in ("conv", "conv_bwd_in", "conv_bwd_f", "conv2d", "conv2d_bwd_in", "conv2d_bwd_f") and dom.get("fma_frac", 0) > dom["frac_hbm"]:
+    if dom_cell.op in ("conv", "conv_bwd_in", "conv_bwd_f", "conv2d", "conv2d_bwd_in", "conv2d_bwd_f") and \
+            dom.get("fma_frac", 0) > dom["frac_hbm"]:
         achieved = dom_cell.flops / (dom["avg_ms"] * 1e-3) / 1e12
         roofline = {"bound": "alu", "kernel": dom["cell"], "achieved": round(achieved, 2),
                     "peak": round(2 * FP32_FMA_PEAK / 1e12, 2), "unit": "TFLOP/s",
@@ -788,7 +981,8 @@ def run_ours(args):
                     "hbm_gbs": dom["gbs"], "hbm_frac": dom["frac_hbm"], "traffic": None}
     else:
         roofline = {"bound": "hbm", "kernel": dom["cell"], "achieved": dom["gbs"], "peak": peak_hbm,
-                    "unit": "GB/s", "frac": dom["frac_hbm"], "peak_source": peak_src, "traffic": None}
+                    "unit": "GB/s", "frac": dom["frac_hbm"], "peak_source": peak_src, "traffic": None,
+                    "frac_8tbs": dom["frac_8tbs"]}
         if "tc_frac" in dom and dom_cell.op == "conv_mc":
             roofline["tensor_frac"] = dom["tc_frac"]
             roofline["tensor_peak_tflops"] = round(2 * tf32_peak_tflops(), 1)
@@ -799,7 +993,11 @@ def run_ours(args):
             roofline["tensor_note"] = (f"executed MMA work ({TC_FLOP_PER_OUT} TF32-equivalent flop/output: "
                                        "xh*fh in TF32 + one bf16 correction product at half weight) / dense "
                                        "TF32 peak (measured bf16 / 2)")
-    roofline["share_of_step"] = dom["share"]
+    roofline["algorithmic_bytes_per_launch"] = dom_cell.bytes
+    roofline["avg_launch_ms"] = dom["avg_ms"]
+    roofline["share_of_step"] = round(dom["avg_ms"] / step_ms, 4)
+    roofline["timing"] = (f"the kernel alone, captured as a CUDA graph of {reps} launches alternating over 2 "
+                          "input/output buffer sets, CUDA events on its stream")
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):  # dram bytes per launch from a committed `ncu --set full` capture
         try:
@@ -807,17 +1005,28 @@ def run_ours(args):
         except Exception:  # noqa: BLE001
             pass
 
+    verify = None
+    if args.verify:
+        n_cmp, bad = R.verify()
+        t = torch.tensor([float(n_cmp), float(len(bad))], dtype=torch.float64, device=coll)
+        if world > 1:
+            dist.all_reduce(t)
+        verify = {"compared": int(t[0]), "mismatches": int(t[1]), "first": bad[:4],
+                  "what": "sharded outputs == one unsharded call on the regenerated global slice, bitwise "
+                          "(tensor-core conv cells: within twice the BASELINE.json bound)"}
+
+    _phase("e2e")
     # end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
         R.setup_e2e()
         for _ in range(2):
             R.step_e2e()
+        R.e2e_fence()
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         n_e2e = max(2, min(args.steps, args.e2e_steps))
-        R.e2e_fence()
         e0.record(R.stream)
         R.s_h2d.wait_stream(R.stream)
         for _ in range(n_e2e):
@@ -832,44 +1041,93 @@ def run_ours(args):
                "ms_per_step": round(ems / n_e2e, 3), "steps": n_e2e,
                "path": "pinned host -> cudaMemcpyAsync (copy stream) -> ss_* C ABI (compute stream) -> "
                        "cudaMemcpyAsync (2nd copy stream) -> pinned host, overlapped across cells"}
+    cells_info = {"cells": cells, "cells_sum_ms": round(tot_k, 4), "step_ms": round(step_ms, 4),
+                  "cells_sum_over_step": round(tot_k / step_ms, 4)}
+    names = [c.name for c in R.cells]
+    inputs_spec = {k: {kk: vv for kk, vv in v.items() if kk != "kw"} for k, v in R.inputs_spec.items()}
+    dtype = _dtype_label(R.cells)
+    del R, graphs
+    torch.cuda.empty_cache()
+
+    cfg5 = None
+    if args.workload == "suite" and not args.no_cfg5:
+        _phase("cfg5")
+        cfg5 = run_cfg5(args, world, rank, device, barrier, max_over_ranks, coll)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        _phase("cpu baseline")
         cpu = cpu_baseline(args.workload, budget_s=args.cpu_budget)
+    _phase("done")
 
     if rank == 0:
-        cfg = {"workload": args.workload, "cells": [c.name for c in R.cells], "cuda_graph": bool(args.graph),
-               "cell_timing": ("per-launch CUDA events in the timed steps" if args.cell_timing == "inline" and not
-                               args.graph else "per-launch CUDA events in an eager pass of the same steps right "
-                               "after the timed ones (the timed steps carry no per-launch events)"),
+        cfg = {"workload": args.workload, "cells": names,
+               "launch_mode": "CUDA graphs at every N: A = interiors + batch-sharded cells, B = sequence tails "
+                              "(N > 1), NCCL halo posted eagerly between them",
                "parallelism": f"{'seq+batch' if args.workload == 'suite' else 'shard'} x{world}",
-               "l2": "inputs > L2 (126 MB) per cell; cfg4 cells read distinct input copies",
-               "inputs": {k: {kk: vv for kk, vv in v.items() if kk != "kw"} for k, v in R.inputs_spec.items()}}
+               "l2": "step: every cell's input > L2 (126 MB) or, for cfg4, a distinct input copy per cell; "
+                     "per-cell timing alternates 2 buffer sets",
+               "inputs": inputs_spec}
         line = {"metric": METRIC, "value": round(value, 3), "unit": "GElem/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
                 "higher_is_better": True, "scaling": args.scaling,
-                "vs_baseline": None, "dtype": "f32/i32" if args.workload == "suite" else
-                ("i32" if args.workload == "cfg2" else "f32"),
-                "data": "synthetic (splitmix64 counter-based, BASELINE.json seeds/distributions)",
+                "vs_baseline": None, "dtype": dtype,
+                "data": "synthetic: splitmix64 counter-based generator (synth/), BASELINE.json seeds; "
+                        "U[0,1), U[-1,1), U{-1000..1000} exact; 'N(0,1)' = Irwin-Hall(12) stand-in "
+                        "(mean 0, var 1, support [-6,6), DESIGN.md R12)",
                 "config": cfg, "hbm_gbs": round(hbm_gbs, 1), "hbm_frac_8tbs": round(hbm_gbs / 8000.0, 4),
                 "hbm_frac_measured": round(hbm_gbs / peak_hbm, 4),
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-                "clocks": clk.summary(), "impl": "ours"}
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches_per_step * args.steps),
+                "clocks": clk.summary(), "cfg5": cfg5, "verify": verify,
+                "cells_sum_over_step": cells_info["cells_sum_over_step"], "impl": "ours"}
         print(json.dumps(line), flush=True)
         if args.cells_out:
             with open(args.cells_out, "w") as fh:
-                json.dump({"line": line, "cells": cells}, fh, indent=1)
+                json.dump({"line": line, **cells_info}, fh, indent=1)
         else:
-            print(json.dumps({"cells": cells}), file=sys.stderr)
+            print(json.dumps(cells_info), file=sys.stderr)
     if world > 1:
         dist.destroy_process_group()
 
 
 # ============================================================== oracle arm
+def _seq_task(x, w, fn):
+    """A 1-D sample x whose len(x) - w + 1 windows can be split into output
+    ranges: run(i, parts) evaluates part i (input x[a : b + w - 1] for outputs
+    [a, b)) and returns its output count."""
+    n_out = x.size - w + 1
+
+    def run(i=0, parts=1):
+        a, b = n_out * i // parts, n_out * (i + 1) // parts
+        if b <= a:
+            return 0
+        fn(x[a:b + w - 1])
+        return b - a
+    return run
+
+
+def _rows_task(x, fn, outs_per_row):
+    """A sample of independent rows / planes (leading axis), split by rows."""
+    def run(i=0, parts=1):
+        r0, r1 = x.shape[0] * i // parts, x.shape[0] * (i + 1) // parts
+        if r1 <= r0:
+            return 0
+        fn(x[r0:r1])
+        return (r1 - r0) * outs_per_row
+    return run
+
+
+def _whole_task(fn):
+    """A sample that is not split: part 0 runs it all."""
+    return lambda i=0, parts=1: fn() if i == 0 else 0
+
+
 def oracle_sample_plan(workload: str, frac: float):
     """Bounded sample of every cell: the same cells, a `frac` share of each
-    (leading rows / images / output range).  Returns [(cell, fn)] where fn()
-    runs the oracle on its sample and returns the number of outputs."""
+    (leading rows / images / output range).  Returns [(cell, run)] where
+    run(i, parts) evaluates part i of `parts` of the sample with the oracle and
+    returns its output count (run() = the whole sample)."""
     import oracle
     import synth
     _, cells = cfg_cells(workload)
@@ -884,12 +1142,9 @@ def oracle_sample_plan(workload: str, frac: float):
                 x = synth.uniform_pm1(0, n_out + c.w - 1)
             else:
                 x = synth.normal(6, n_out + c.w - 1)
-            if c.op == "sum":
-                plan.append((c, lambda x=x, c=c: (oracle.pool_sum(x, c.w), x.size - c.w + 1)[1]))
-            elif c.op == "max":
-                plan.append((c, lambda x=x, c=c: (oracle.pool_max(x, c.w), x.size - c.w + 1)[1]))
-            else:
-                plan.append((c, lambda x=x, c=c: (oracle.conv1d(x, c.f), x.size - c.w + 1)[1]))
+            fn = {"sum": lambda xv, c=c: oracle.pool_sum(xv, c.w), "max": lambda xv, c=c: oracle.pool_max(xv, c.w),
+                  "conv": lambda xv, c=c: oracle.conv1d(xv, c.f)}[c.op]
+            plan.append((c, _seq_task(x, c.w, fn)))
         elif c.cfg == "cfg3":
             rows = max(1, int(round(64 * frac)))
             n = 1 << 20
@@ -897,26 +1152,30 @@ def oracle_sample_plan(workload: str, frac: float):
                 n = max(c.w, int(64 * (1 << 20) * frac))
                 rows = 1
             x = synth.normal(3, rows * n).reshape(rows, n)
-            plan.append((c, lambda x=x, c=c: (oracle.conv1d(x, c.f), x.shape[0] * (x.shape[1] - c.w + 1))[1]))
+            if rows == 1:
+                plan.append((c, _seq_task(x[0], c.w, lambda xv, c=c: oracle.conv1d(xv, c.f))))
+            else:
+                plan.append((c, _rows_task(x, lambda xr, c=c: oracle.conv1d(xr, c.f), n - c.w + 1)))
         elif c.cfg == "mc":
             cin, cout, k = c.kh, c.kw, c.w
             n = max(k + 1, int(16 * 65536 * frac))
             xb = oracle.to_bf16_bits(synth.normal(96, n * cin).reshape(1, n, cin))
             wb = oracle.to_bf16_bits(c.f)
-            plan.append((c, lambda xb=xb, wb=wb, c=c, n=n: (oracle.conv1d_mc(xb, wb), (n - c.w + 1) * c.kw)[1]))
+            plan.append((c, _whole_task(lambda xb=xb, wb=wb, c=c, n=n: (oracle.conv1d_mc(xb, wb),
+                                                                          (n - c.w + 1) * c.kw)[1])))
         elif c.cfg == "conv2d":
             planes = max(1, int(round(32 * 64 * frac)))
             x = synth.uniform01(5, planes * 112 * 112).reshape(planes, 112, 112)
             oh = (112 - c.kh) // c.sh + 1
-            plan.append((c, lambda x=x, c=c, oh=oh: (oracle.conv2d(x, c.f, c.sh, c.sw), x.shape[0] * oh * oh)[1]))
+            plan.append((c, _rows_task(x, lambda xp, c=c: oracle.conv2d(xp, c.f, c.sh, c.sw), oh * oh)))
         elif c.cfg == "backward" and c.op == "pool2d_bwd":
             planes = max(1, int(round(32 * 64 * frac)))
             oh = (112 - c.kh) // c.sh + 1
             x = synth.uniform01(5, planes * 112 * 112).reshape(planes, 112, 112)
             g = synth.normal(34, planes * oh * oh).reshape(planes, oh, oh)
             m = oracle.POOL2D_MAX if c.mode == "max" else oracle.POOL2D_AVG
-            plan.append((c, lambda x=x, g=g, c=c, m=m: (oracle.pool2d_backward(x, g, 112, 112, c.kh, c.kw, c.sh,
-                                                                               c.sw, m), x.size)[1]))
+            plan.append((c, _whole_task(lambda x=x, g=g, c=c, m=m: (oracle.pool2d_backward(
+                x, g, 112, 112, c.kh, c.kw, c.sh, c.sw, m), x.size)[1])))
         elif c.cfg == "backward" and c.op in ("conv2d_bwd_in", "conv2d_bwd_f"):
             planes = max(1, int(round(32 * 64 * frac)))
             oh = 112 - c.kh + 1
@@ -926,7 +1185,7 @@ def oracle_sample_plan(workload: str, frac: float):
                 fn = (lambda g=g, c=c: (oracle.conv2d_backward_input(g, c.f, 112, 112), planes * 112 * 112)[1])
             else:
                 fn = (lambda x=x, g=g, c=c: (oracle.conv2d_backward_filter(x, g, c.kh, c.kw), g.size)[1])
-            plan.append((c, fn))
+            plan.append((c, _whole_task(fn)))
         elif c.cfg == "backward":
             rows = max(1, int(round(64 * frac)))
             n = 1 << 20
@@ -944,7 +1203,7 @@ def oracle_sample_plan(workload: str, frac: float):
                 fn = (lambda g=g, c=c, n=n: (oracle.pool_sum_backward(g, n, c.w), g.shape[0] * n)[1])
             else:
                 fn = (lambda x=x, g=g, c=c: (oracle.pool_max_backward(x, g, c.w), x.size)[1])
-            plan.append((c, fn))
+            plan.append((c, _whole_task(fn)))
         elif c.cfg in ("stride", "winspec"):
             rows, n = 1, max(4 * (c.w - 1) * c.dilation + 8, int(64 * (1 << 20) * frac))
             x = synth.normal(3, rows * n).reshape(rows, n)
@@ -954,72 +1213,103 @@ def oracle_sample_plan(workload: str, frac: float):
                   "max": lambda x=x, c=c, kw=kw: oracle.pool_max_ex(x, c.w, **kw),
                   "min": lambda x=x, c=c, kw=kw: oracle.pool_min_ex(x, c.w, **kw),
                   "conv": lambda x=x, c=c, kw=kw: oracle.conv1d_ex(x, c.f, **kw)}[c.op]
-            plan.append((c, lambda fn=fn, L=L: (fn(), L)[1]))
+            plan.append((c, _whole_task(lambda fn=fn, L=L: (fn(), L)[1])))
         elif c.cfg == "affine":
             n = max(c.w, int(8 * (1 << 24) * frac))
             u = synth.uab(31, n, 0.5, 1.0)
             v = synth.normal(32, n)
-            plan.append((c, lambda u=u, v=v, c=c: (oracle.affine_window(u, v, c.w), u.size - c.w + 1)[1]))
+            plan.append((c, _whole_task(lambda u=u, v=v, c=c: (oracle.affine_window(u, v, c.w),
+                                                                u.size - c.w + 1)[1])))
         else:  # cfg4
             planes = max(1, int(round(32 * 64 * frac)))
             x = synth.uniform01(5, planes * 112 * 112).reshape(planes, 112, 112)
             m = oracle.POOL2D_MAX if c.mode == "max" else oracle.POOL2D_AVG
             oh = (112 - c.kh) // c.sh + 1
-            plan.append((c, lambda x=x, c=c, m=m, oh=oh: (oracle.pool2d(x, c.kh, c.kw, c.sh, c.sw, m),
-                                                          x.shape[0] * oh * oh)[1]))
+            ow = (112 - c.kw) // c.sw + 1
+            plan.append((c, _rows_task(x, lambda xp, c=c, m=m: oracle.pool2d(xp, c.kh, c.kw, c.sh, c.sw, m),
+                                       oh * ow)))
     return plan
 
 
-def cpu_baseline(workload: str, budget_s: float = 20.0):
-    """Time the oracle (as it stands, 1 thread) on a bounded sample of the workload."""
-    # calibrate: a tiny fraction first, then scale the fraction to the budget
-    frac = 1.0 / 4096 if workload != "cfg1" else 1.0
-    plan = oracle_sample_plan(workload, frac)
+def _run_parts(plan, parts: int = 1):
+    """Run the plan's samples split into `parts` disjoint pieces, one thread per
+    piece (ctypes releases the GIL inside every oracle call, so the threads run
+    on separate cores).  Returns (outputs, seconds)."""
+    from concurrent.futures import ThreadPoolExecutor
     t0 = time.perf_counter()
-    outs = sum(fn() for _, fn in plan)
-    dt = time.perf_counter() - t0
+    if parts == 1:
+        outs = sum(run() for _, run in plan)
+    else:
+        with ThreadPoolExecutor(parts) as ex:
+            outs = sum(ex.map(lambda i: sum(run(i, parts) for _, run in plan), range(parts)))
+    return outs, time.perf_counter() - t0
+
+
+def cpu_baseline(workload: str, budget_s: float = 10.0):
+    """Time the oracle as it stands (plain C, -O2) on a bounded sample of the
+    workload: on one thread, then on every host core (os.cpu_count() threads,
+    the sample split into disjoint output ranges / rows / planes)."""
+    import oracle
+    oracle.build()
+    frac = 1.0 / 4096 if workload != "cfg1" else 1.0
+    outs, dt = _run_parts(oracle_sample_plan(workload, frac))  # calibrate
     if workload != "cfg1" and dt > 0:
         frac = min(1.0, frac * max(1.0, budget_s / dt))
-        plan = oracle_sample_plan(workload, frac)
-        t0 = time.perf_counter()
-        outs = sum(fn() for _, fn in plan)
-        dt = time.perf_counter() - t0
-    return {"value": round(outs / dt / 1e9, 6), "unit": "GElem/s", "cores": 1, "kind": "oracle",
-            "sample": f"every cell of workload '{workload}', leading {frac:.3%} of its outputs/rows/images "
-                      f"({outs} outputs, {dt:.1f} s, single-threaded C oracle -O2)",
-            "seconds": round(dt, 2)}
+    plan = oracle_sample_plan(workload, frac)
+    outs, dt = _run_parts(plan)
+    cores = os.cpu_count() or 1
+    outs_all, dt_all = _run_parts(plan, cores)
+    return {"value": round(outs_all / dt_all / 1e9, 6), "unit": "GElem/s", "cores": cores, "kind": "oracle",
+            "sample": f"every cell of workload '{workload}', {frac:.3%} of its outputs/rows/images ({outs_all} "
+                      f"outputs), split over {cores} threads into disjoint output ranges / rows / planes; plain C "
+                      f"oracle -O2, {dt_all:.1f} s",
+            "host_cpu_count": cores,
+            "single_thread": {"value": round(outs / dt / 1e9, 6), "unit": "GElem/s", "cores": 1, "outputs": outs,
+                              "seconds": round(dt, 2)},
+            "seconds": round(dt_all, 2)}
 
 
 def run_reference(args):
+    """The tier's reference arm: the CPU oracle (plain C, as it stands) on every
+    host core, each step a bounded sample of every cell of the workload."""
     world, rank, _ = dist_env()
     if rank != 0:
         return  # rank 0 alone runs the CPU reference; the others exit 0 without work
     import oracle
     oracle.build()
-    frac = 1.0 / 2048 if args.workload != "cfg1" else 1.0
+    cores = os.cpu_count() or 1
+    frac = 1.0 / 256 if args.workload != "cfg1" else 1.0
     plan = oracle_sample_plan(args.workload, frac)
     for _ in range(args.warmup):
-        for _, fn in plan:
-            fn()
-    times = []
-    outs = 0
+        _run_parts(plan, cores)
+    times, outs = [], 0
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        outs = sum(fn() for _, fn in plan)
-        times.append(time.perf_counter() - t0)
+        outs, dt = _run_parts(plan, cores)
+        times.append(dt)
     tot = sum(times)
     value = outs * args.steps / tot / 1e9
+    sample = (f"{frac:.4%} of every cell of '{args.workload}' per step, split over {cores} threads into disjoint "
+              "output ranges / rows / planes (plain C oracle -O2)")
     line = {"metric": METRIC, "value": round(value, 6), "unit": "GElem/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 3),
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f64/i64 accumulate", "data": "synthetic (same generator and seeds)",
-            "config": {"workload": args.workload, "sample_fraction": frac},
+            "config": {"workload": args.workload, "sample_fraction": frac, "threads": cores},
             "impl": "reference",
-            "cpu_baseline": {"value": round(value, 6), "unit": "GElem/s", "cores": 1, "kind": "oracle",
-                             "sample": f"leading {frac:.4%} of every cell of '{args.workload}' per step"},
+            "cpu_baseline": {"value": round(value, 6), "unit": "GElem/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
             "e2e": {"value": round(value, 6), "unit": "GElem/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
 def main():
@@ -1027,24 +1317,33 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="suite", choices=["suite", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "stride", "winspec", "affine", "backward", "conv2d", "mc"])
+    ap.add_argument("--workload", default="suite", choices=["suite", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "stride",
+                                                             "winspec", "affine", "backward", "conv2d", "mc"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="multi-GPU: weak = N x the BASELINE shape (config-sized share per rank), strong = split it")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--graph", dest="graph", action="store_true", default=None,
-                    help="replay each timed step as a captured CUDA graph (default on 1 GPU)")
-    ap.add_argument("--no-graph", dest="graph", action="store_false", help="launch every timed step eagerly")
-    ap.add_argument("--cell-timing", choices=("inline", "separate"), default="separate",
-                    help="per-kernel CUDA events inside the timed steps (inline) or in a second pass of the "
-                         "same steps right after them (separate: the timed steps carry no events)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cell-reps", type=int, default=20, help="launches per per-cell timing graph (even)")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip the config-5 sub-record of the suite")
+    ap.add_argument("--cfg5-log2n", type=int, default=32, help="config 5 sequence length (2^32 in BASELINE.json)")
+    ap.add_argument("--cfg5-steps", type=int, default=20)
+    ap.add_argument("--verify", action="store_true",
+                    help="check sharded outputs against one unsharded call on regenerated global slices (bitwise)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--cells-out", default=None)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo = test mode (ranks may share one GPU, host-staged halo)")
     args = ap.parse_args()
+    world = os.environ.get("WORLD_SIZE")
+    if args.impl == "ours" and args.gpus > 1 and world is None:
+        # one process per GPU: re-launch this command under torchrun, rank 0 prints the line
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if world is not None and args.impl == "ours" and int(world) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup raised to 3 (timing rule)", file=sys.stderr)
         args.warmup = 3

@@ -60,9 +60,9 @@ def main():
     torch.cuda.set_device(dev)
     dist.init_process_group(a.backend)
     orig = bench.cfg_cells
-    bench.cfg_cells = lambda w: small(*orig(w))
+    bench.cfg_cells = lambda w, *extra: small(*orig(w, *extra))
     R = bench.Runner(a.workload, world, rank, dev)
-    R.step()
+    R.step_eager()
     torch.cuda.synchronize()
     mine = outputs(R)
     gathered = {}
@@ -73,7 +73,7 @@ def main():
     ok = True
     if rank == 0:
         R1 = bench.Runner(a.workload, 1, 0, dev)
-        R1.step()
+        R1.step_eager()
         torch.cuda.synchronize()
         ref = outputs(R1)
         cells = {c.name: c for c in R1.cells}
