@@ -78,6 +78,13 @@ int dynamic_tiles() {
   return on != 0;
 }
 
+// SS_TILE_2D (read once, default 1): 0 routes stride-1 3x3 / 5x5 / 7x7 conv2d and its
+// input gradient to the previous kernels (A/B only).
+static int tile_2d_enabled() {
+  static int on = env_int("SS_TILE_2D", 1);
+  return on != 0;
+}
+
 // cuTensorMapEncodeTiled from the driver, without linking libcuda.
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -124,6 +131,25 @@ bool encode_chunk_map(CUtensorMap* m, const void* base, int64_t m_ext, int atoms
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Planes [planes][H][W] of fp32 for the 2-D tile kernel (conv2d_tile.cu): box
+// {box_w, box_h, 1} lands as box_h dense rows of box_w floats (SWIZZLE_NONE),
+// elements outside the plane (negative coordinates, columns >= W, rows >= H)
+// zero-filled -- the tile's padding and pitch in one copy.  W*4 must be a
+// multiple of 16 (TMA stride rule).
+bool encode_plane_map(CUtensorMap* m, const float* base, int64_t W, int64_t H, int64_t planes, int box_w,
+                      int box_h) {
+  auto enc = encode_fn();
+  if (!enc || (W * 4) % 16 || box_w > 256 || box_h > 256 || (box_w * 4) % 16) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)(W * 4), (cuuint64_t)(H * W * 4)};
+  cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -596,6 +622,20 @@ ss_status_t ss_conv2d_backward_input(const void* dy, void* dx, int64_t planes, i
   p.planes = planes; p.H = H; p.W = W; p.kh = kh; p.kw = kw; p.sh = sh; p.sw = sw;
   p.OH = (H - kh) / sh + 1; p.OW = (W - kw) / sw + 1;
   if (overlaps(dy, planes * p.OH * p.OW * 4, dx, planes * H * W * 4)) return fail(SS_ERR_OVERLAP, "dx overlaps dy");
+  if (sh == 1 && sw == 1 && tile_2d_enabled() && conv2d_tile_supported((int)kh, (int)kw, H, W)) {
+    // stride 1: dx = the full correlation of dy with the flipped filter = the tile kernel's
+    // valid correlation of dy bordered by kh-1 / kw-1 zeros (reading R21)
+    Conv2DTileParams t;
+    memset(&t, 0, sizeof t);
+    t.x = p.dy; t.y = p.dx; t.planes = planes;
+    t.IH = (int)p.OH; t.IW = (int)p.OW; t.OH = (int)H; t.OW = (int)W; t.KH = (int)kh; t.KW = (int)kw;
+    t.pad_t = (int)kh - 1; t.pad_l = (int)kw - 1;
+    for (int64_t i = 0; i < kh * kw; ++i) t.taps[i] = filter_host[kh * kw - 1 - i];
+    t.clc = dynamic_tiles();
+    cudaError_t e = launch_conv2d_tile(t, static_cast<cudaStream_t>(stream), current_sms());
+    if (e == cudaSuccess) return SS_OK;
+    if (e != cudaErrorInvalidConfiguration) return cuda_fail(e, "conv2d_backward_input tile launch");
+  }
   for (int64_t t = 0; t < kh * kw; ++t) p.taps[t] = filter_host[t];
   cudaError_t e = launch_conv2d_backward_input(p, static_cast<cudaStream_t>(stream), current_sms());
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv2d_backward_input launch");
@@ -676,6 +716,19 @@ ss_status_t ss_conv2d(const void* x, void* y, int64_t planes, int64_t H, int64_t
   p.planes = planes; p.H = H; p.W = W; p.kh = kh; p.kw = kw; p.sh = sh; p.sw = sw;
   p.OH = (H - kh) / sh + 1; p.OW = (W - kw) / sw + 1;
   if (overlaps(x, planes * H * W * 4, y, planes * p.OH * p.OW * 4)) return fail(SS_ERR_OVERLAP, "x and y overlap");
+  // stride-1 5x5 / 7x7: the FFMA2 tile kernel (FP32-pipe bound); 3x3 stays on the
+  // memory-bound vector kernel, measured faster there
+  if (sh == 1 && sw == 1 && kh * kw >= 25 && tile_2d_enabled() && conv2d_tile_supported((int)kh, (int)kw, p.OH, p.OW)) {
+    Conv2DTileParams t;
+    memset(&t, 0, sizeof t);
+    t.x = p.x; t.y = p.y; t.planes = planes;
+    t.IH = (int)H; t.IW = (int)W; t.OH = (int)p.OH; t.OW = (int)p.OW; t.KH = (int)kh; t.KW = (int)kw;
+    for (int64_t i = 0; i < kh * kw; ++i) t.taps[i] = filter_host[i];
+    t.clc = dynamic_tiles();
+    cudaError_t e = launch_conv2d_tile(t, static_cast<cudaStream_t>(stream), current_sms());
+    if (e == cudaSuccess) return SS_OK;
+    if (e != cudaErrorInvalidConfiguration) return cuda_fail(e, "conv2d tile launch");
+  }
   for (int64_t t = 0; t < kh * kw; ++t) p.taps[t] = filter_host[t];
   p.clc = dynamic_tiles();
   cudaError_t e = launch_conv2d(p, static_cast<cudaStream_t>(stream), current_sms());

@@ -90,6 +90,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// try_wait without a suspend hint (polling).  Needed where the phase is
+// completed by cp.async.mbarrier.arrive: ncu showed the hinted wait sleeping
+// out its NANOSLEEP there instead of waking on the arrival.
+__device__ __forceinline__ void mbar_wait_poll(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // TMA 2-D tile load global -> shared, completion on an mbarrier (tx bytes).
 __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map,
                                             int32_t c0, int32_t c1, uint64_t* bar) {
@@ -237,6 +250,8 @@ __device__ __forceinline__ int64_t clc_wait(ClcSmem* c, uint32_t& ph) {
       : "=r"(ok), "=r"(id), "=l"(lo), "=l"(hi)
       : "r"(smem_u32(&c->resp))
       : "memory");
+  (void)lo;
+  (void)hi;
   return ok ? (int64_t)id : -1;
 }
 

@@ -189,6 +189,30 @@ struct Conv2DParams {
 };
 cudaError_t launch_conv2d(Conv2DParams& p, cudaStream_t stream, int grid);
 
+// Stride-1 2-D correlation with virtual zero padding on FFMA2 (conv2d_tile.cu):
+// ss_conv2d (pad 0) and the input gradient ss_conv2d_backward_input (pad
+// KH-1 / KW-1, flipped filter) for 3x3, 5x5, 7x7 filters.
+struct alignas(64) Conv2DTileParams {
+  CUtensorMap tm_x;    // TMA mode: 3-D {IW, IH, planes}, box {P, TH, 1}, zero fill (encode_plane_map)
+  const float* x;      // input planes [planes][IH][IW]
+  float* y;            // output planes [planes][OH][OW], OH = IH + 2 pad_t - KH + 1
+  int64_t planes;
+  int IH, IW, OH, OW, KH, KW;
+  int pad_t, pad_l;    // zero rows / columns in front of (and behind) the input
+  int pad_c, shift;    // tile left padding pad_c = pad_l + shift, a multiple of 4 (set by the launcher)
+  int P;               // shared-tile row pitch in floats (set by the launcher)
+  int units, col_blocks;
+  int granule;         // relayout bytes per shared-memory copy: 16, 8 or 4
+  uint32_t tile_bytes, raw_bytes, tile_tx;
+  int tile_stages, raw_stages;
+  int tma;             // 1: each padded tile is one TMA tensor copy (16-B row pitch); 0: raw ring + relayout
+  int clc;  // 1: one CTA per plane, planes claimed by cluster launch control; 0: static stride
+  float taps[64];      // row-major [KH][KW]
+};
+bool conv2d_tile_supported(int kh, int kw, int64_t oh, int64_t ow);
+bool encode_plane_map(CUtensorMap* m, const float* base, int64_t W, int64_t H, int64_t planes, int box_w, int box_h);
+cudaError_t launch_conv2d_tile(Conv2DTileParams& p, cudaStream_t stream, int sms);
+
 // Gradients of the 2-D conv (conv2d_backward.cu, reading R21).
 struct Conv2DBwdParams {
   const float* x;   // filter gradient
