@@ -20,6 +20,7 @@
 // kernel sums them in CTA order (deterministic).  Regions too large for
 // shared memory take direct kernels reading global memory.
 #include <cstdint>
+#include <cstring>
 
 #include <cuda_runtime.h>
 
@@ -482,6 +483,22 @@ cudaError_t launch_conv2d_backward_filter(Conv2DBwdParams& p, float* df, void* w
                                           cudaStream_t stream) {
   double* part = static_cast<double*>(workspace);
   const int64_t nt = p.kh * p.kw;
+  if (p.sh == 1 && p.sw == 1 && conv2d_df_tile_supported((int)p.kh, (int)p.kw, p.H, p.W, p.OH, p.OW, p.x, p.dy)) {
+    // stride-1 3x3 / 5x5 / 7x7 with TMA-able x rows: the tile kernel (conv2d_tile.cu)
+    Conv2DTileParams t;
+    memset(&t, 0, sizeof t);
+    t.x = p.x; t.planes = p.planes;
+    t.IH = (int)p.H; t.IW = (int)p.W; t.OH = (int)p.OH; t.OW = (int)p.OW; t.KH = (int)p.kh; t.KW = (int)p.kw;
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    sms = num_sms(dev);
+    const int g = sms <= ctas ? launch_conv2d_df_tile(t, p.dy, part, sms, stream) : -1;
+    if (g > 0) {
+      conv2d_bwd_filter_finish<<<(unsigned)((nt + 3) / 4), 128, 0, stream>>>(part, g, nt, df);
+      note_launch();
+      return cudaGetLastError();
+    }
+  }
   p.df_xr = (int)((kDfTileR - 1) * p.sh + p.kh);
   p.df_xc = (int)(((kDfTileC - 1) * p.sw + p.kw + 3) / 4 * 4 + 4);  // LDS.128 rows + over-read
   const size_t tile_bytes = 2 * ((size_t)kDfTileR * kDfTileC + (size_t)p.df_xr * p.df_xc) * sizeof(float);

@@ -378,4 +378,189 @@ cudaError_t launch_conv2d_tile(Conv2DTileParams& p, cudaStream_t stream, int sms
   return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------
+// Filter gradient of the stride-1 2-D correlation (reading R21):
+//     df[a][b] = sum_p sum_r sum_c dy[p][r][c] * x[p][r + a][c + b]
+// Same staging and units as above: per plane the x tile arrives by one TMA
+// tensor copy (pitch P = 4 mod 8) and the dense dy plane by one bulk copy
+// (LDS.64 rows: the dy row pitch is 8 x an odd number of bytes for the
+// config-4 shapes, so 16 rows hit 16 distinct 8-B slots).  A lane (dy row r,
+// 16 columns) keeps all KH*KW tap sums in fp32 registers (scalar FFMA: the
+// FP32 pipe, not issue, bounds it) for 8 units at most (<= 128 products per
+// sum), then the warp sums each tap with a butterfly and one lane adds it to
+// the warp's fp64 accumulator in shared memory.  Planes are dealt statically
+// (CTA b: planes b, b + grid, ...) so the fp64 partials, the fixed-order CTA
+// reduction and the finishing kernel's fixed-order sum over CTAs make df
+// bitwise deterministic.
+namespace {
+constexpr int kDfFlush = 8;  // units per lane between fp32 -> fp64 flushes
+}
+
+template <int KH, int KW>
+__global__ void __launch_bounds__(kTWarps * 32 + 32, 1)
+conv2d_df_tile_kernel(const __grid_constant__ Conv2DTileParams p, const float* __restrict__ dy,
+                      double* __restrict__ part) {
+  constexpr int NT = KH * KW;
+  constexpr int NL = (kUnit + KW + 3) / 4;  // LDS.128 per x fragment
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  const int S = p.tile_stages;
+  const uint32_t stage = p.tile_bytes + p.raw_bytes;  // x tile, then the dense dy plane
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage);
+  uint64_t* empty = full + S;
+  int64_t* pid = reinterpret_cast<int64_t*>(empty + S);
+  double* wacc = reinterpret_cast<double*>(pid + S);  // [kTWarps][NT]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < kTWarps * NT; i += blockDim.x) wacc[i] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t smem_s = smem_u32(smem);
+  const int OH = p.OH, OW = p.OW, P = p.P;
+  const uint32_t dy_bytes = (uint32_t)((int64_t)OH * OW * 4);
+
+  if (warp == kTWarps) {  // producer lane: static plane schedule
+    if (lane == 0) {
+      prefetch_tmap(&p.tm_x);
+      int64_t u = blockIdx.x;
+      for (int it = 0;; ++it, u += gridDim.x) {
+        const int s = it % S;
+        mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
+        if (u >= p.planes) {
+          pid[s] = -1;
+          mbar_arrive(&full[s]);
+          break;
+        }
+        pid[s] = u;
+        mbar_arrive_expect_tx(&full[s], p.tile_tx + dy_bytes);
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_s + (uint32_t)s * stage),
+            "l"(reinterpret_cast<uint64_t>(&p.tm_x)), "r"(0), "r"(0), "r"((int32_t)u), "r"(smem_u32(&full[s]))
+            : "memory");
+        bulk_load_1d(smem + (size_t)s * stage + p.tile_bytes, dy + u * (int64_t)OH * OW, dy_bytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers
+  const int units = p.units, pairs = (units + 1) >> 1;
+  const int half = lane >> 4, row16 = lane & 15;
+  float acc[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) acc[t] = 0.0f;
+  auto flush = [&]() {
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      float v = acc[t];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (lane == (t & 31)) wacc[warp * NT + t] += (double)v;
+      acc[t] = 0.0f;
+    }
+  };
+  int cur = -1, since = 0;
+  bool done = false;
+  for (int64_t g = warp; !done; g += kTWarps) {
+    const int64_t it = g / pairs;
+    const int q = (int)(g - it * pairs);
+    while (cur < it) {
+      if (cur >= 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[cur % S]);
+      }
+      ++cur;
+      mbar_wait(&full[cur % S], (uint32_t)(cur / S) & 1u);
+      int64_t plane;
+      asm volatile("ld.shared.b64 %0, [%1];" : "=l"(plane) : "r"(smem_u32(pid + cur % S)) : "memory");
+      if (plane < 0) {
+        done = true;
+        break;
+      }
+    }
+    if (done) break;
+    const int un = 2 * q + half;
+    const int rg = un / p.col_blocks, cb = un - rg * p.col_blocks;
+    const int r = rg * kUnit + row16;
+    if (un < units && r < OH) {
+      const uint32_t xs = smem_s + (uint32_t)(cur % S) * stage + (uint32_t)(r * P + cb * kUnit) * 4u;
+      const uint32_t ds = smem_s + (uint32_t)(cur % S) * stage + p.tile_bytes + (uint32_t)(r * OW + cb * kUnit) * 4u;
+      const int nv = OW - cb * kUnit;  // valid dy columns of this block
+      float d[kUnit];
+#pragma unroll
+      for (int j = 0; j < kUnit; j += 2) {
+        float d0 = 0.f, d1 = 0.f;
+        if (j < nv) asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(d0), "=f"(d1) : "r"(ds + 4u * j));
+        d[j] = d0;
+        d[j + 1] = j + 1 < nv ? d1 : 0.f;
+      }
+#pragma unroll
+      for (int a = 0; a < KH; ++a) {
+        float xv[4 * NL];
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          const float4 v = lds128(xs + (uint32_t)(a * P) * 4u + 16u * l);
+          xv[4 * l] = v.x; xv[4 * l + 1] = v.y; xv[4 * l + 2] = v.z; xv[4 * l + 3] = v.w;
+        }
+#pragma unroll
+        for (int b = 0; b < KW; ++b)
+#pragma unroll
+          for (int j = 0; j < kUnit; ++j) acc[a * KW + b] = __fmaf_rn(d[j], xv[j + b], acc[a * KW + b]);
+      }
+    }
+    if (++since == kDfFlush) {
+      flush();
+      since = 0;
+    }
+  }
+  flush();
+  // fixed-order CTA reduction of the warps' fp64 sums -> this CTA's partial
+  asm volatile("bar.sync 1, %0;" ::"r"(kTWarps * 32) : "memory");
+  for (int t = threadIdx.x; t < NT; t += kTWarps * 32) {
+    double v = 0.0;
+    for (int w = 0; w < kTWarps; ++w) v += wacc[w * NT + t];
+    part[(int64_t)t * gridDim.x + blockIdx.x] = v;
+  }
+}
+
+bool conv2d_df_tile_supported(int kh, int kw, int64_t H, int64_t W, int64_t OH, int64_t OW, const void* x,
+                              const void* dy) {
+  if (!conv2d_tile_supported(kh, kw, OH, OW)) return false;
+  return (W * 4) % 16 == 0 && ((OH * OW * 4) % 16) == 0 && (OW % 2) == 0 &&
+         (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(dy) & 15) == 0 && H <= 256;
+}
+
+// Grid (CTAs whose fp64 partials the finishing kernel sums) or -1 if not applicable.
+int launch_conv2d_df_tile(Conv2DTileParams& p, const float* dy, double* part, int sms, cudaStream_t stream) {
+  p.col_blocks = (p.OW + kUnit - 1) / kUnit;
+  p.units = ((p.OH + kUnit - 1) / kUnit) * p.col_blocks;
+  const int need_cols = p.col_blocks * kUnit + (p.KW + 3) / 4 * 4;
+  p.P = tile_pitch(need_cols > p.IW ? need_cols : p.IW);
+  const int TH = p.IH;
+  if (p.P > 256 || TH > 256) return -1;
+  if (!encode_plane_map(&p.tm_x, p.x, p.IW, p.IH, p.planes, p.P, TH)) return -1;
+  p.tile_tx = (uint32_t)((size_t)TH * p.P * 4);
+  p.tile_bytes = (uint32_t)(((size_t)TH * p.P * 4 + 127) / 128 * 128);
+  p.raw_bytes = (uint32_t)(((size_t)p.OH * p.OW * 4 + 127) / 128 * 128);
+  const size_t fixed = 128 + 256 + (size_t)kTWarps * p.KH * p.KW * 8;
+  p.tile_stages = 2;
+  const size_t smem = (size_t)2 * (p.tile_bytes + p.raw_bytes) + fixed;
+  if (smem > (size_t)kSmemBudget) return -1;
+  auto kfn = p.KH == 3 ? conv2d_df_tile_kernel<3, 3>
+           : p.KH == 5 ? conv2d_df_tile_kernel<5, 5>
+                       : conv2d_df_tile_kernel<7, 7>;
+  if (ensure_smem_attr(reinterpret_cast<const void*>(kfn)) != cudaSuccess) return -1;
+  const int grid = (int)(p.planes < sms ? p.planes : sms);
+  kfn<<<(unsigned)grid, kTWarps * 32 + 32, smem, stream>>>(p, dy, part);
+  note_launch();
+  return grid;
+}
+
 }  // namespace ss

@@ -211,6 +211,11 @@ struct alignas(64) Conv2DTileParams {
 };
 bool conv2d_tile_supported(int kh, int kw, int64_t oh, int64_t ow);
 bool encode_plane_map(CUtensorMap* m, const float* base, int64_t W, int64_t H, int64_t planes, int box_w, int box_h);
+// Filter gradient on the same tiles (conv2d_tile.cu): x = p.x [planes][IH][IW], dy [planes][OH][OW];
+// writes part[tap * grid + cta] (fp64) and returns grid, or -1 if the shape does not fit.
+bool conv2d_df_tile_supported(int kh, int kw, int64_t H, int64_t W, int64_t OH, int64_t OW, const void* x,
+                              const void* dy);
+int launch_conv2d_df_tile(Conv2DTileParams& p, const float* dy, double* part, int sms, cudaStream_t stream);
 cudaError_t launch_conv2d_tile(Conv2DTileParams& p, cudaStream_t stream, int sms);
 
 // Gradients of the 2-D conv (conv2d_backward.cu, reading R21).
