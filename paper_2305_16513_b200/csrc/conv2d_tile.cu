@@ -9,23 +9,29 @@
 // valid correlation; pad = (KH-1, KW-1) with the flipped filter is the input
 // gradient dx of ss_conv2d_backward_input (the full correlation of dy).
 //
-// * Staging: a producer lane bulk-copies each dense plane (one
-//   cp.async.bulk, any row width) into a raw ring; a relayout warp copies it
-//   into a zero-bordered tile of row pitch P floats (P = 4 mod 8, so the 8
-//   lanes of an LDS.128 phase -- 8 consecutive rows -- hit 8 distinct bank
-//   groups).  Planes are claimed by cluster launch control.  (cp.async 16-B
-//   copies by one producer warp measured ~3x slower than the HBM needs.)
+// * Staging, TMA mode (16-B row pitch): one TMA tensor copy per plane lands a
+//   zero-bordered tile of row pitch P = 4 mod 8 floats (the 8 lanes of an
+//   LDS.128 phase -- 8 consecutive rows -- hit 8 distinct bank groups; the
+//   box's first column must be 16-B aligned, so the left padding is rounded
+//   up to 4 and the output shifts by the difference).  Dense mode (other even
+//   row widths, e.g. dy of 106 / 110 columns): one bulk copy of the dense
+//   plane; a lane then reads its rows with LDS.64 (row pitch = 8 x odd bytes:
+//   16 consecutive rows hit 16 distinct 8-B slots) and masks the padding
+//   itself.  (A relayout of dense planes into padded tiles by two warps, and
+//   per-row cp.async by one warp, were built and measured slower: staging
+//   latency, not bandwidth, bound them.)  Planes are claimed by cluster launch
+//   control.
 // * Work unit: 16 consecutive output rows x 16 consecutive columns; a half
 //   warp per unit, lane = output row.  Units are dealt round robin to the 15
 //   consumer warps across plane boundaries (two per warp at a time), so no
 //   warp idles at the end of a plane.
-// * Arithmetic: per filter row a the lane loads the 24 input columns it needs
-//   (<= 6 LDS.128 = 12 register pairs E) and applies every tap with FFMA2 on
-//   output pairs: even taps b act on pairs (2i, 2i+1) -> E[i + b/2], odd taps
-//   on pairs (2i-1, 2i) -> E[i + (b-1)/2]; both operands are aligned register
-//   pairs, no shuffles.  y = fl(S_even + S_odd): S_even sums the even-b taps,
-//   S_odd the odd-b taps, each in row-major tap order, so every output's
-//   association depends on (a, b) only (tiling independent, deterministic).
+// * Arithmetic: per filter row a the lane gets the 24 input columns it needs
+//   (12 register pairs E) and applies every tap with FFMA2 on output pairs:
+//   even taps b act on pairs (2i, 2i+1) -> E[i + b/2], odd taps on pairs
+//   (2i-1, 2i) -> E[i + (b-1)/2]; both operands are aligned register pairs.
+//   y = fl(S_even + S_odd): S_even sums the even-b taps, S_odd the odd-b taps,
+//   each in row-major tap order, so every output's association depends on
+//   (a, b) only (tiling independent, deterministic).
 // * Store: the lane's 16 outputs are one 64-B row segment (STG.128 where the
 //   row is 16-B aligned, else STG.64 + STG.128 x 3 + STG.64).
 #include <cstdint>
@@ -40,44 +46,34 @@ namespace ss {
 namespace {
 
 constexpr int kTWarps = 15;                    // consumer warps
-constexpr int kRWarps = 2;                     // relayout warps
-constexpr int kTThreads = (kTWarps + 1 + kRWarps) * 32;  // + the producer warp and the relayout warps
+constexpr int kTThreads = (kTWarps + 1) * 32;  // + the producer warp
 constexpr int kUnit = 16;                      // unit = 16 rows x 16 columns
+
+__device__ __forceinline__ float2 lds64(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
 
 }  // namespace
 
-template <int KH, int KW>
+template <int KH, int KW, bool TMA>
 __global__ void __launch_bounds__(kTThreads, 1) conv2d_tile_kernel(const __grid_constant__ Conv2DTileParams p) {
   static_assert(KW <= 8 && KH <= 8, "a lane's fragment is 24 columns");
   constexpr int NE = (kUnit + KW + 3) / 4 * 2;  // register pairs per fragment
-  constexpr int NL = NE / 2;                    // LDS.128 per fragment
+  constexpr int NL = NE / 2;                    // LDS.128 per fragment (TMA mode)
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-  const int ST = p.tile_stages, SR = p.raw_stages;
-  uint8_t* raw = smem + (size_t)ST * p.tile_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(raw + (size_t)SR * p.raw_bytes);  // [ST] relayout -> consumers
-  uint64_t* empty = full + ST;                                                   // [ST] consumers -> relayout
-  uint64_t* rfull = empty + ST;                                                  // [SR] bulk copy -> relayout
-  uint64_t* rempty = rfull + SR;                                                 // [SR] relayout -> producer
-  int64_t* pid = reinterpret_cast<int64_t*>(rempty + SR);                        // [ST] plane of each tile
-  int64_t* rpid = pid + ST;                                                      // [SR] plane of each raw buffer
+  const int ST = p.tile_stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)ST * p.tile_bytes);
+  uint64_t* empty = full + ST;
+  int64_t* pid = reinterpret_cast<int64_t*>(empty + ST);  // plane of each stage (-1: no more)
   __shared__ ClcSmem clc;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // zero the tiles once: their borders (padding) are never written again
-  {
-    float4* z = reinterpret_cast<float4*>(smem);
-    const int n4 = (int)((size_t)ST * p.tile_bytes / 16);
-    for (int i = threadIdx.x; i < n4; i += kTThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
-      // relayout: every relayout lane releases its own stores; direct: one expect_tx arrival
-      mbar_init(&full[s], p.tma ? 1 : 32 * kRWarps);
+      mbar_init(&full[s], 1);
       mbar_init(&empty[s], kTWarps);
-    }
-    for (int s = 0; s < SR; ++s) {
-      mbar_init(&rfull[s], 1);
-      mbar_init(&rempty[s], 32 * kRWarps);
     }
     clc_init(&clc);
     fence_mbar_init();
@@ -86,31 +82,36 @@ __global__ void __launch_bounds__(kTThreads, 1) conv2d_tile_kernel(const __grid_
   const uint32_t smem_s = smem_u32(smem);
   const int P = p.P;
 
-  if (warp == kTWarps && p.tma) {
-    // ---------------- producer lane, TMA mode: one tensor copy per plane lands the padded,
-    // pitched tile (box {P, TH} at (-pad_c, -pad_t); out-of-plane elements zero-filled; the
-    // box's first column must be 16-B aligned, hence pad_c = pad_l rounded up to 4)
+  if (warp == kTWarps) {
+    // ---------------- producer lane: one TMA tensor copy (padded tile) or one bulk copy
+    // (dense plane) per plane
     if (lane == 0) {
-      prefetch_tmap(&p.tm_x);
+      if (TMA) prefetch_tmap(&p.tm_x);
       int64_t u = blockIdx.x;
       uint32_t cph = 0;
       if (p.clc && u < p.planes) clc_request(&clc);
+      const uint32_t dense_bytes = (uint32_t)((int64_t)p.IH * p.IW * 4);
       for (int it = 0;; ++it) {
         const int st = it % ST;
-        mbar_wait(&empty[st], ((uint32_t)(it / ST) & 1u) ^ 1u);
+        mbar_wait_poll(&empty[st], ((uint32_t)(it / ST) & 1u) ^ 1u);
         if (u < 0 || u >= p.planes) {
           pid[st] = -1;
           mbar_arrive(&full[st]);
           break;
         }
         pid[st] = u;
-        mbar_arrive_expect_tx(&full[st], p.tile_tx);
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_s + (uint32_t)st * p.tile_bytes),
-            "l"(reinterpret_cast<uint64_t>(&p.tm_x)), "r"(-p.pad_c), "r"(-p.pad_t), "r"((int32_t)u),
-            "r"(smem_u32(&full[st]))
-            : "memory");
+        if (TMA) {
+          mbar_arrive_expect_tx(&full[st], p.tile_tx);
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_s + (uint32_t)st * p.tile_bytes),
+              "l"(reinterpret_cast<uint64_t>(&p.tm_x)), "r"(-p.pad_c), "r"(-p.pad_t), "r"((int32_t)u),
+              "r"(smem_u32(&full[st]))
+              : "memory");
+        } else {
+          mbar_arrive_expect_tx(&full[st], dense_bytes);
+          bulk_load_1d(smem + (size_t)st * p.tile_bytes, p.x + u * (int64_t)p.IH * p.IW, dense_bytes, &full[st]);
+        }
         if (p.clc) {
           u = clc_wait(&clc, cph);  // requested one plane ahead
           if (u >= 0) clc_request(&clc);
@@ -118,108 +119,16 @@ __global__ void __launch_bounds__(kTThreads, 1) conv2d_tile_kernel(const __grid_
           u += gridDim.x;
         }
       }
-    }
-    return;
-  }
-  if (warp > kTWarps && p.tma) return;
-  if (warp == kTWarps) {
-    // ---------------- producer lane: one bulk copy of each dense plane into the raw ring
-    if (lane == 0) {
-      int64_t u = blockIdx.x;
-      uint32_t cph = 0;
-      if (p.clc && u < p.planes) clc_request(&clc);
-      const uint32_t bytes = (uint32_t)((int64_t)p.IH * p.IW * 4);
-      for (int it = 0;; ++it) {
-        const int s = it % SR;
-        mbar_wait(&rempty[s], ((uint32_t)(it / SR) & 1u) ^ 1u);
-        if (u < 0 || u >= p.planes) {
-          rpid[s] = -1;
-          mbar_arrive(&rfull[s]);
-          break;
-        }
-        rpid[s] = u;
-        mbar_arrive_expect_tx(&rfull[s], bytes);
-        bulk_load_1d(raw + (size_t)s * p.raw_bytes, p.x + u * (int64_t)p.IH * p.IW, bytes, &rfull[s]);
-        if (p.clc) {
-          u = clc_wait(&clc, cph);  // requested one plane ahead
-          if (u >= 0) clc_request(&clc);
-        } else {
-          u += gridDim.x;
-        }
-      }
-    }
-    return;
-  }
-  if (warp > kTWarps) {
-    // ---------------- relayout warps: dense plane -> zero-bordered tile of pitch P.  Warp rw
-    // takes row blocks of 4 rows, rw, rw + kRWarps, ...; a lane issues its 4 loads before its
-    // 4 stores (the loop is latency-bound otherwise).
-    const int rw = warp - kTWarps - 1;
-    const int IH = p.IH, IW = p.IW, gel = p.granule / 4, gpr = IW / gel;
-    for (int it = 0;; ++it) {
-      const int sr = it % SR, st = it % ST;
-      mbar_wait(&rfull[sr], (uint32_t)(it / SR) & 1u);
-      int64_t u;
-      asm volatile("ld.shared.b64 %0, [%1];" : "=l"(u) : "r"(smem_u32(rpid + sr)) : "memory");
-      mbar_wait(&empty[st], ((uint32_t)(it / ST) & 1u) ^ 1u);
-      if (u < 0) {
-        if (rw == 0 && lane == 0) pid[st] = -1;
-        mbar_arrive(&full[st]);
-        break;
-      }
-      const uint32_t src = smem_u32(raw + (size_t)sr * p.raw_bytes);
-      const uint32_t dst = smem_s + (uint32_t)st * p.tile_bytes + (uint32_t)(p.pad_t * P + p.pad_c) * 4u;
-      for (int i0 = 4 * rw; i0 < IH; i0 += 4 * kRWarps) {
-        for (int g = lane; g < gpr; g += 32) {
-          if (gel == 4) {
-            float4 v[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (i0 + j < IH) v[j] = lds128(src + (uint32_t)((i0 + j) * IW + 4 * g) * 4u);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (i0 + j < IH) sts128(dst + (uint32_t)((i0 + j) * P + 4 * g) * 4u, v[j].x, v[j].y, v[j].z, v[j].w);
-          } else if (gel == 2) {
-            float v0[4], v1[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (i0 + j < IH)
-                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v0[j]), "=f"(v1[j])
-                             : "r"(src + (uint32_t)((i0 + j) * IW + 2 * g) * 4u));
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (i0 + j < IH)
-                asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(dst + (uint32_t)((i0 + j) * P + 2 * g) * 4u),
-                             "f"(v0[j]), "f"(v1[j])
-                             : "memory");
-          } else {
-            float v[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (i0 + j < IH)
-                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[j]) : "r"(src + (uint32_t)((i0 + j) * IW + g) * 4u));
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (i0 + j < IH)
-                asm volatile("st.shared.f32 [%0], %1;" ::"r"(dst + (uint32_t)((i0 + j) * P + g) * 4u), "f"(v[j])
-                             : "memory");
-          }
-        }
-      }
-      if (rw == 0 && lane == 0) pid[st] = u;
-      fence_proxy_async_smem();  // our reads of the raw buffer precede the next bulk copy into it
-      mbar_arrive(&rempty[sr]);
-      mbar_arrive(&full[st]);
     }
     return;
   }
 
   // ---------------- consumers
-  const int OH = p.OH, OW = p.OW;
+  const int OH = p.OH, OW = p.OW, IH = p.IH, IW = p.IW;
   const int units = p.units;            // per plane
   const int pairs = (units + 1) >> 1;   // warp units per plane
   const int half = lane >> 4, row16 = lane & 15;
-  int cur = -1;                         // plane iteration whose tile this warp holds
+  int cur = -1;                         // plane iteration whose stage this warp holds
   int64_t plane = 0;
   bool done = false;
   for (int64_t g = warp; !done; g += kTWarps) {
@@ -231,7 +140,7 @@ __global__ void __launch_bounds__(kTThreads, 1) conv2d_tile_kernel(const __grid_
         if (lane == 0) mbar_arrive(&empty[cur % ST]);
       }
       ++cur;
-      mbar_wait(&full[cur % ST], (uint32_t)(cur / ST) & 1u);
+      mbar_wait_poll(&full[cur % ST], (uint32_t)(cur / ST) & 1u);
       asm volatile("ld.shared.b64 %0, [%1];" : "=l"(plane) : "r"(smem_u32(pid + cur % ST)) : "memory");
       if (plane < 0) {
         done = true;
@@ -244,7 +153,10 @@ __global__ void __launch_bounds__(kTThreads, 1) conv2d_tile_kernel(const __grid_
     const int rg = un / p.col_blocks, cb = un - rg * p.col_blocks;
     const int r = rg * kUnit + row16;
     if (r >= OH) continue;
-    const uint32_t base = smem_s + (uint32_t)(cur % ST) * p.tile_bytes + (uint32_t)(r * P + cb * kUnit) * 4u;
+    const uint32_t stage_s = smem_s + (uint32_t)(cur % ST) * p.tile_bytes;
+    // dense mode: fragment columns = input columns c_in .. c_in + 2 NE; interior blocks skip the masks
+    const int c_in = cb * kUnit - p.pad_l;
+    const bool interior = c_in >= 0 && c_in + 2 * NE <= IW;
     float2 A0[kUnit / 2], A1[kUnit / 2 + 1];  // A0[i]: outputs (2i, 2i+1); A1[i]: (2i-1, 2i)
 #pragma unroll
     for (int i = 0; i < kUnit / 2; ++i) A0[i] = make_float2(0.f, 0.f);
@@ -253,11 +165,28 @@ __global__ void __launch_bounds__(kTThreads, 1) conv2d_tile_kernel(const __grid_
 #pragma unroll
     for (int a = 0; a < KH; ++a) {
       float2 E[NE];
+      if (TMA) {
+        const uint32_t base = stage_s + (uint32_t)((r + a) * P + cb * kUnit) * 4u;
 #pragma unroll
-      for (int l = 0; l < NL; ++l) {
-        const float4 v = lds128(base + (uint32_t)(a * P) * 4u + 16u * l);
-        E[2 * l] = make_float2(v.x, v.y);
-        E[2 * l + 1] = make_float2(v.z, v.w);
+        for (int l = 0; l < NL; ++l) {
+          const float4 v = lds128(base + 16u * l);
+          E[2 * l] = make_float2(v.x, v.y);
+          E[2 * l + 1] = make_float2(v.z, v.w);
+        }
+      } else {
+        const int i = r + a - p.pad_t;  // input row
+        const bool rv = (unsigned)i < (unsigned)IH;
+        const uint32_t base = stage_s + (uint32_t)(i * IW + c_in) * 4u;
+        if (interior) {
+#pragma unroll
+          for (int m = 0; m < NE; ++m) E[m] = rv ? lds64(base + 8u * m) : make_float2(0.f, 0.f);
+        } else {
+#pragma unroll
+          for (int m = 0; m < NE; ++m) {
+            const int c = c_in + 2 * m;  // pairs (c, c+1) lie wholly inside or outside the row (c, IW even)
+            E[m] = (rv && c >= 0 && c < IW) ? lds64(base + 8u * m) : make_float2(0.f, 0.f);
+          }
+        }
       }
 #pragma unroll
       for (int b = 0; b < KW; b += 2) {
@@ -279,18 +208,18 @@ __global__ void __launch_bounds__(kTThreads, 1) conv2d_tile_kernel(const __grid_
       const float so = (o & 1) ? A1[(o + 1) >> 1].x : A1[o >> 1].y;
       out[o] = __fadd_rn(se, so);
     }
-    // tile column t holds output column t - shift (the tile's left padding is pad_l + shift)
+    // tile column t holds output column t - shift (TMA mode's rounded-up left padding)
     const int c0 = cb * kUnit - p.shift;
     float* yrow = p.y + (plane * OH + r) * (int64_t)OW;
-    const int nvalid = OW - c0;
-    float* yr = yrow + c0;
-    const uintptr_t ya = reinterpret_cast<uintptr_t>(yrow) + 4 * (intptr_t)c0;
     if (c0 < 0) {
 #pragma unroll
       for (int o = 0; o < kUnit; ++o)
         if (c0 + o >= 0 && c0 + o < OW) yrow[c0 + o] = out[o];
       continue;
     }
+    const int nvalid = OW - c0;
+    float* yr = yrow + c0;
+    const uintptr_t ya = reinterpret_cast<uintptr_t>(yr);
     if (nvalid >= kUnit && (ya & 15) == 0) {
 #pragma unroll
       for (int o = 0; o < kUnit; o += 4)
@@ -330,46 +259,45 @@ bool conv2d_tile_supported(int kh, int kw, int64_t oh, int64_t ow) {
 
 cudaError_t launch_conv2d_tile(Conv2DTileParams& p, cudaStream_t stream, int sms) {
   if (!conv2d_tile_supported(p.KH, p.KW, p.OH, p.OW)) return cudaErrorInvalidConfiguration;
-  // TMA mode (16-B row pitch): the box's first column must be 16-B aligned, so the tile's left
-  // padding is rounded up to 4 columns and tile column t holds output column t - shift; the
-  // relayout mode places the rows at any column (shift 0)
-  const bool tma_ok = (p.IW * 4) % 16 == 0;
-  p.pad_c = tma_ok ? (p.pad_l + 3) / 4 * 4 : p.pad_l;
-  p.shift = p.pad_c - p.pad_l;
-  p.col_blocks = (p.OW + p.shift + kUnit - 1) / kUnit;
-  const int row_groups = (p.OH + kUnit - 1) / kUnit;
-  p.units = row_groups * p.col_blocks;
-  // staged columns: every lane of the last column block reads 16 + KW (+ pad to 4) columns
-  const int need_cols = p.col_blocks * kUnit + (p.KW + 3) / 4 * 4;
-  p.P = tile_pitch(need_cols > p.IW + p.pad_c ? need_cols : p.IW + p.pad_c);
-  const int TH = p.OH + p.KH - 1;  // staged rows (pad_t + IH + bottom zeros)
+  const int TH = p.OH + p.KH - 1;  // rows the outputs read (pad_t + IH + bottom zeros)
   if (TH < p.pad_t + p.IH) return cudaErrorInvalidConfiguration;
-  // the dense plane arrives by one bulk copy: 16-B aligned planes of a multiple of 16 bytes
-  const int64_t plane_bytes = (int64_t)p.IH * p.IW * 4;
-  if ((reinterpret_cast<uintptr_t>(p.x) & 15) || (plane_bytes & 15)) return cudaErrorInvalidConfiguration;
-  if (p.P > 256 || TH > 256) return cudaErrorInvalidConfiguration;  // one TMA box / tile rows
-  p.tile_bytes = (uint32_t)(((size_t)TH * p.P * 4 + 127) / 128 * 128);
-  p.raw_bytes = (uint32_t)((plane_bytes + 127) / 128 * 128);
-  if (p.IW % 4 == 0 && p.pad_c % 4 == 0) p.granule = 16;
-  else if (p.IW % 2 == 0 && p.pad_c % 2 == 0) p.granule = 8;
-  else p.granule = 4;
   const size_t fixed = 128 + 512;
-  // TMA mode: a 16-B row pitch lets one tensor copy per plane land the padded tile
   size_t smem = 0;
-  p.tma = tma_ok && encode_plane_map(&p.tm_x, p.x, p.IW, p.IH, p.planes, p.P, TH) ? 1 : 0;
-  if (p.tma) {
-    p.tile_tx = (uint32_t)((size_t)TH * p.P * 4);
-    p.raw_stages = 0;
-    p.tile_stages = 4;
-    while (p.tile_stages > 2 && (size_t)p.tile_stages * p.tile_bytes + fixed > (size_t)kSmemBudget) --p.tile_stages;
-    smem = (size_t)p.tile_stages * p.tile_bytes + fixed;
-  } else {
-    p.tile_stages = 2;
-    p.raw_stages = 2;
-    smem = (size_t)2 * p.tile_bytes + (size_t)2 * p.raw_bytes + fixed;
+  // TMA mode (16-B row pitch): the box's first column must be 16-B aligned, so the tile's left
+  // padding is rounded up to 4 columns and tile column t holds output column t - shift
+  if ((p.IW * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(p.x) & 15) == 0) {
+    p.pad_c = (p.pad_l + 3) / 4 * 4;
+    p.shift = p.pad_c - p.pad_l;
+    p.col_blocks = (p.OW + p.shift + kUnit - 1) / kUnit;
+    const int need_cols = p.col_blocks * kUnit + (p.KW + 3) / 4 * 4;  // last block reads 16 + KW (+ pad)
+    p.P = tile_pitch(need_cols > p.IW + p.pad_c ? need_cols : p.IW + p.pad_c);
+    if (p.P <= 256 && TH <= 256 && encode_plane_map(&p.tm_x, p.x, p.IW, p.IH, p.planes, p.P, TH)) {
+      p.tma = 1;
+      p.tile_tx = (uint32_t)((size_t)TH * p.P * 4);
+      p.tile_bytes = (uint32_t)(((size_t)TH * p.P * 4 + 127) / 128 * 128);
+    }
   }
+  if (!p.tma) {
+    // dense mode: the plane as it lies in memory (one bulk copy), padding masked by the lanes; needs
+    // 8-B aligned pairs (even row width and left padding) and a 16-B multiple plane
+    const int64_t plane_bytes = (int64_t)p.IH * p.IW * 4;
+    if (p.IW % 2 || p.pad_l % 2 || (plane_bytes & 15) || (reinterpret_cast<uintptr_t>(p.x) & 15))
+      return cudaErrorInvalidConfiguration;
+    p.pad_c = p.pad_l;
+    p.shift = 0;
+    p.col_blocks = (p.OW + kUnit - 1) / kUnit;
+    p.P = p.IW;
+    p.tile_bytes = (uint32_t)((plane_bytes + 127) / 128 * 128);
+  }
+  p.units = ((p.OH + kUnit - 1) / kUnit) * p.col_blocks;
+  p.tile_stages = 4;
+  while (p.tile_stages > 2 && (size_t)p.tile_stages * p.tile_bytes + fixed > (size_t)kSmemBudget) --p.tile_stages;
+  smem = (size_t)p.tile_stages * p.tile_bytes + fixed;
   if (smem > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
-  auto kfn = p.KH == 3 ? conv2d_tile_kernel<3, 3> : p.KH == 5 ? conv2d_tile_kernel<5, 5> : conv2d_tile_kernel<7, 7>;
+  auto kfn = p.tma ? (p.KH == 3 ? conv2d_tile_kernel<3, 3, true> : p.KH == 5 ? conv2d_tile_kernel<5, 5, true>
+                                                                      : conv2d_tile_kernel<7, 7, true>)
+                   : (p.KH == 3 ? conv2d_tile_kernel<3, 3, false> : p.KH == 5 ? conv2d_tile_kernel<5, 5, false>
+                                                                       : conv2d_tile_kernel<7, 7, false>);
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
   if (e != cudaSuccess) return e;
   const int64_t g = launch_grid(p.planes, sms, p.clc);
@@ -431,7 +359,7 @@ conv2d_df_tile_kernel(const __grid_constant__ Conv2DTileParams p, const float* _
       int64_t u = blockIdx.x;
       for (int it = 0;; ++it, u += gridDim.x) {
         const int s = it % S;
-        mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
+        mbar_wait_poll(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
         if (u >= p.planes) {
           pid[s] = -1;
           mbar_arrive(&full[s]);
@@ -477,7 +405,7 @@ conv2d_df_tile_kernel(const __grid_constant__ Conv2DTileParams p, const float* _
         if (lane == 0) mbar_arrive(&empty[cur % S]);
       }
       ++cur;
-      mbar_wait(&full[cur % S], (uint32_t)(cur / S) & 1u);
+      mbar_wait_poll(&full[cur % S], (uint32_t)(cur / S) & 1u);
       int64_t plane;
       asm volatile("ld.shared.b64 %0, [%1];" : "=l"(plane) : "r"(smem_u32(pid + cur % S)) : "memory");
       if (plane < 0) {

@@ -202,10 +202,9 @@ struct alignas(64) Conv2DTileParams {
   int pad_c, shift;    // tile left padding pad_c = pad_l + shift, a multiple of 4 (set by the launcher)
   int P;               // shared-tile row pitch in floats (set by the launcher)
   int units, col_blocks;
-  int granule;         // relayout bytes per shared-memory copy: 16, 8 or 4
   uint32_t tile_bytes, raw_bytes, tile_tx;
   int tile_stages, raw_stages;
-  int tma;             // 1: each padded tile is one TMA tensor copy (16-B row pitch); 0: raw ring + relayout
+  int tma;             // 1: each padded tile is one TMA tensor copy (16-B row pitch); 0: dense plane, lanes mask
   int clc;  // 1: one CTA per plane, planes claimed by cluster launch control; 0: static stride
   float taps[64];      // row-major [KH][KW]
 };
