@@ -90,6 +90,8 @@ def lib() -> ctypes.CDLL:
                                                      ctypes.c_int, vp, vp]
             L.oracle_conv1d_mc_bf16.argtypes = [vp, vp, i64, i64, i64, i64, i64, vp, vp]
             L.oracle_conv1d_mc_bf16.restype = ctypes.c_int
+            L.oracle_conv2d_mc_bf16.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, vp]
+            L.oracle_conv2d_mc_bf16.restype = ctypes.c_int
             L.oracle_conv2d_f32.argtypes = [vp, i64, i64, i64, vp, i64, i64, i64, i64, vp, vp]
             L.oracle_conv2d_f32.restype = ctypes.c_int
             L.oracle_conv2d_backward_input_f32.argtypes = [vp, i64, i64, i64, vp, i64, i64, i64, i64, vp, vp]
@@ -430,4 +432,21 @@ def conv1d_mc(x_bf16: np.ndarray, w_bf16: np.ndarray):
     y = np.empty((B, L, cout), np.float64)
     m = np.empty((B, L, cout), np.float64)
     _check(lib().oracle_conv1d_mc_bf16(_p(x), _p(w), B, N, cin, cout, k, _p(y), _p(m)))
+    return y, m
+
+
+def conv2d_mc(x_bf16: np.ndarray, w_bf16: np.ndarray):
+    """Multi-channel 2-D conv, NHWC: x [B, H, W, Cin] and w [Cout, Cin, kh, kw] as bf16 bit
+    patterns (uint16); valid padding, stride 1; returns (y double [B, OH, OW, Cout], absmag)."""
+    x = np.ascontiguousarray(x_bf16, np.uint16)
+    w = np.ascontiguousarray(w_bf16, np.uint16)
+    B, H, W, cin = x.shape
+    cout, cin2, kh, kw = w.shape
+    assert cin2 == cin
+    OH, OW = H - kh + 1, W - kw + 1
+    if OH < 1 or OW < 1:
+        raise ValueError("window exceeds input")
+    y = np.empty((B, OH, OW, cout), np.float64)
+    m = np.empty((B, OH, OW, cout), np.float64)
+    _check(lib().oracle_conv2d_mc_bf16(_p(x), _p(w), B, H, W, cin, cout, kh, kw, _p(y), _p(m)))
     return y, m

@@ -625,3 +625,37 @@ int oracle_conv1d_mc_bf16(const uint16_t* x, const uint16_t* w, int64_t batch, i
       }
   return 0;
 }
+
+/* Multi-channel 2-D convolution (the Conclusion's
+ * multi-dimensional extension, of the channel-summed sliding dot
+ * product of reading R18; reading R22): channels-last (NHWC) bf16
+ * activations, weights in torch conv2d order [cout][cin][kh][kw], valid padding,
+ * stride 1:
+ *   y[b][r][c][co] = sum_{a<kh} sum_{e<kw} sum_{ci<cin} w[co][ci][a][e] * x[b][r+a][c+e][ci]
+ * x [batch][H][W][cin], y [batch][H-kh+1][W-kw+1][cout]; accumulated in double
+ * (terms taken in a, e, ci order). */
+int oracle_conv2d_mc_bf16(const uint16_t* x, const uint16_t* w, int64_t batch, int64_t H, int64_t W, int64_t cin,
+                          int64_t cout, int64_t kh, int64_t kw, double* y, double* absmag) {
+  if (x == NULL || w == NULL || y == NULL || batch < 1 || cin < 1 || cout < 1 || kh < 1 || kw < 1 || kh > H ||
+      kw > W)
+    return -1;
+  int64_t OH = H - kh + 1, OW = W - kw + 1;
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t r = 0; r < OH; ++r)
+      for (int64_t c = 0; c < OW; ++c)
+        for (int64_t co = 0; co < cout; ++co) {
+          double acc = 0.0, mag = 0.0;
+          for (int64_t a = 0; a < kh; ++a)
+            for (int64_t e = 0; e < kw; ++e)
+              for (int64_t ci = 0; ci < cin; ++ci) {
+                double t = bf16_to_double(w[((co * cin + ci) * kh + a) * kw + e]) *
+                           bf16_to_double(x[((b * H + r + a) * W + c + e) * cin + ci]);
+                acc += t;
+                mag += fabs(t);
+              }
+          int64_t o = ((b * OH + r) * OW + c) * cout + co;
+          y[o] = acc;
+          if (absmag) absmag[o] = mag;
+        }
+  return 0;
+}

@@ -147,6 +147,10 @@ int oracle_conv2d_backward_filter_f32(const float* x, const float* dy, int64_t p
  * double result: y[b][i][co] = sum_j sum_ci w[co][ci][j] x[b][i+j][ci]. */
 int oracle_conv1d_mc_bf16(const uint16_t* x, const uint16_t* w, int64_t batch, int64_t N, int64_t cin,
                           int64_t cout, int64_t k, double* y, double* absmag);
+/* Multi-channel 2-D convolution, NHWC bf16 activations, [cout][cin][kh][kw] bf16
+ * weights, valid padding, stride 1 (reading R22); y [batch][H-kh+1][W-kw+1][cout]. */
+int oracle_conv2d_mc_bf16(const uint16_t* x, const uint16_t* w, int64_t batch, int64_t H, int64_t W, int64_t cin,
+                          int64_t cout, int64_t kh, int64_t kw, double* y, double* absmag);
 
 #ifdef __cplusplus
 }

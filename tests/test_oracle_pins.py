@@ -524,3 +524,40 @@ def test_conv1d_mc_vs_torch():
     wt = torch.tensor(oracle.bf16_bits_to_f32(wb), dtype=torch.float64)
     ref = torch.nn.functional.conv1d(xt, wt).permute(0, 2, 1).numpy()
     np.testing.assert_allclose(y, ref, rtol=1e-12, atol=1e-12)
+
+
+# ------------------------------------------------ multi-channel 2-D conv (reading R22)
+def test_conv2d_mc_sums_single_channel_2d_convs():
+    # integer-valued (exact in bf16 and in double): every (co, ci) pair is the single-channel
+    # 2-D correlation oracle.conv2d (pinned above against torch, separable filters, deltas)
+    B, H, W, cin, cout, kh, kw = 2, 9, 11, 3, 2, 3, 4
+    x = synth.randint(84, B * H * W * cin, -8, 8).astype(np.float32).reshape(B, H, W, cin)
+    w = synth.randint(85, cout * cin * kh * kw, -4, 4).astype(np.float32).reshape(cout, cin, kh, kw)
+    y, mag = oracle.conv2d_mc(oracle.to_bf16_bits(x), oracle.to_bf16_bits(w))
+    for co in range(cout):
+        ref = sum(oracle.conv2d(np.ascontiguousarray(x[..., ci]), w[co, ci])[0] for ci in range(cin))
+        np.testing.assert_array_equal(y[..., co], ref)
+        refm = sum(oracle.conv2d(np.abs(np.ascontiguousarray(x[..., ci])), np.abs(w[co, ci]))[0] for ci in range(cin))
+        np.testing.assert_array_equal(mag[..., co], refm)
+
+
+def test_conv2d_mc_vs_torch_and_reductions():
+    B, H, W, cin, cout = 2, 7, 10, 8, 5
+    xf = synth.normal(86, B * H * W * cin).reshape(B, H, W, cin)
+    for kh, kw in ((3, 3), (1, 1), (2, 5)):
+        wf = synth.normal(87, cout * cin * kh * kw).reshape(cout, cin, kh, kw)
+        xb, wb = oracle.to_bf16_bits(xf), oracle.to_bf16_bits(wf)
+        y, mag = oracle.conv2d_mc(xb, wb)
+        xt = torch.tensor(oracle.bf16_bits_to_f32(xb), dtype=torch.float64).permute(0, 3, 1, 2)  # NCHW
+        wt = torch.tensor(oracle.bf16_bits_to_f32(wb), dtype=torch.float64)
+        ref = torch.nn.functional.conv2d(xt, wt).permute(0, 2, 3, 1).numpy()
+        np.testing.assert_allclose(y, ref, rtol=1e-12, atol=1e-12)
+        refm = torch.nn.functional.conv2d(xt.abs(), wt.abs()).permute(0, 2, 3, 1).numpy()
+        np.testing.assert_allclose(mag, refm, rtol=1e-12, atol=1e-12)
+    # H = kh = 1: the multi-channel 1-D convolution, row by row
+    wb = oracle.to_bf16_bits(synth.normal(88, cout * cin * 3).reshape(cout, cin, 1, 3))
+    xb = oracle.to_bf16_bits(xf)
+    y, _ = oracle.conv2d_mc(xb, wb)
+    for r in range(H):
+        y1, _ = oracle.conv1d_mc(np.ascontiguousarray(xb[:, r]), np.ascontiguousarray(wb[:, :, 0, :]))
+        np.testing.assert_array_equal(y[:, r], y1)
