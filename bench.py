@@ -190,6 +190,14 @@ def cfg_cells(workload: str, cfg5_log2n: int = 32):
                                shard="batch")
             wf = synth.normal(97, cout * cin * k, sigma=(cin * k) ** -0.5).reshape(cout, cin, k)
             cells.append(Cell("mc", f"mc_c{cin}x{cout}_k{k}", "conv_mc", w=k, f=wf, inp=key, kh=cin, kw=cout))
+        # multi-channel 2-D convolution (reading R22), NHWC bf16, ResNet-like layers; the image
+        # shard's (C, H, W) slots hold (H, W, Cin) of the NHWC tensor
+        for hw, cin, cout in ((56, 64, 64), (56, 64, 128)):
+            key = f"x2mc{hw}"
+            inputs[key] = dict(images=128, C=hw, H=hw, W=cin, dtype="bfloat16", dist="normal", seed=102, kw={},
+                               shard="image")
+            wf = synth.normal(103, cout * cin * 9, sigma=(cin * 9) ** -0.5).reshape(cout, cin, 3, 3)
+            cells.append(Cell("mc", f"mc2d_{hw}x{hw}_c{cin}x{cout}_3x3", "conv2d_mc", kh=3, kw=3, f=wf, inp=key))
     if workload == "backward":  # backward passes on config-3 / config-4 shapes; not a BJ config
         inputs["xb"] = dict(rows=64, n=1 << 20, dtype="float32", dist="normal", seed=3, kw={}, shard="batch")
         for k in (7, 31, 63):
@@ -408,6 +416,16 @@ class Runner:
             c.bytes = rows * N * cin * 2 + c.n_out * 4 + cout * cin * k * 2
             c.flops = 2 * k * cin * c.n_out
             return torch.empty((rows, L, cout), dtype=torch.float32, device=self.device)
+        if c.op == "conv2d_mc":
+            B, H, W, cin = geo
+            cout = c.f.shape[0]
+            OH, OW = H - c.kh + 1, W - c.kw + 1
+            if c.name not in self.wmc:
+                self.wmc[c.name] = torch.from_numpy(c.f).to(self.device).to(torch.bfloat16).contiguous()
+            c.n_out = B * OH * OW * cout
+            c.bytes = B * H * W * cin * 2 + c.n_out * 4 + cout * cin * c.kh * c.kw * 2
+            c.flops = 2 * c.kh * c.kw * cin * c.n_out
+            return torch.empty((B, OH, OW, cout), dtype=torch.float32, device=self.device)
         if c.op in ("pool2d", "conv2d"):
             B, C, H, W = geo
             OH, OW = (H - c.kh) // c.sh + 1, (W - c.kw) // c.sw + 1
@@ -567,6 +585,10 @@ class Runner:
             rows, n = geo
             ss.check(ss.ss_conv1d_mc(x.data_ptr(), self.wmc[c.name].data_ptr(), y.data_ptr(), rows,
                                      n // c.kh, c.kh, c.kw, c.w, self.stream.cuda_stream))
+        elif c.op == "conv2d_mc":
+            B, H, W, cin = geo
+            ss.check(ss.ss_conv2d_mc(x.data_ptr(), self.wmc[c.name].data_ptr(), y.data_ptr(), B, H, W, cin,
+                                     c.f.shape[0], c.kh, c.kw, self.stream.cuda_stream))
         elif c.op == "conv2d":
             B, C, H, W = geo
             ss.check(ss.ss_conv2d(x.data_ptr(), y.data_ptr(), B * C, H, W, c.f_flat, c.kh, c.kw, c.sh, c.sw,
@@ -958,7 +980,7 @@ def run_ours(args):
         d = {"cell": c.name, "avg_ms": round(avg_ms, 5), "n_out": c.n_out, "bytes": c.bytes,
              "gelem_s": round(c.n_out / (avg_ms * 1e-3) / 1e9, 2), "gbs": round(gbs, 1),
              "frac_hbm": round(gbs / peak_hbm, 4), "frac_8tbs": round(gbs / 8000.0, 4), "share": 0.0}
-        if c.op == "conv_mc":
+        if c.op in ("conv_mc", "conv2d_mc"):
             d["tc_frac"] = round(c.flops / (avg_ms * 1e-3) / 1e12 / (2 * tf32_peak_tflops()), 4)  # bf16 peak
         elif conv_on_tensor_cores(c):
             d["tc_frac"] = round(c.n_out * TC_FLOP_PER_OUT / (avg_ms * 1e-3) / 1e12 / tf32_peak_tflops(), 4)
@@ -983,7 +1005,7 @@ def run_ours(args):
         roofline = {"bound": "hbm", "kernel": dom["cell"], "achieved": dom["gbs"], "peak": peak_hbm,
                     "unit": "GB/s", "frac": dom["frac_hbm"], "peak_source": peak_src, "traffic": None,
                     "frac_8tbs": dom["frac_8tbs"]}
-        if "tc_frac" in dom and dom_cell.op == "conv_mc":
+        if "tc_frac" in dom and dom_cell.op in ("conv_mc", "conv2d_mc"):
             roofline["tensor_frac"] = dom["tc_frac"]
             roofline["tensor_peak_tflops"] = round(2 * tf32_peak_tflops(), 1)
             roofline["tensor_note"] = "bf16 MMA work (2 k Cin flop/output) / measured dense bf16 peak"
@@ -1156,6 +1178,13 @@ def oracle_sample_plan(workload: str, frac: float):
                 plan.append((c, _seq_task(x[0], c.w, lambda xv, c=c: oracle.conv1d(xv, c.f))))
             else:
                 plan.append((c, _rows_task(x, lambda xr, c=c: oracle.conv1d(xr, c.f), n - c.w + 1)))
+        elif c.cfg == "mc" and c.op == "conv2d_mc":
+            hw, cin = int(c.name.split("_")[1].split("x")[0]), c.f.shape[1]
+            imgs = max(1, int(round(128 * frac)))
+            xb = oracle.to_bf16_bits(synth.normal(102, imgs * hw * hw * cin).reshape(imgs, hw, hw, cin))
+            wb = oracle.to_bf16_bits(c.f)
+            plan.append((c, _rows_task(xb, lambda xi, wb=wb: oracle.conv2d_mc(xi, wb),
+                                       (hw - 2) * (hw - 2) * c.f.shape[0])))
         elif c.cfg == "mc":
             cin, cout, k = c.kh, c.kw, c.w
             n = max(k + 1, int(16 * 65536 * frac))

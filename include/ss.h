@@ -70,7 +70,7 @@
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 8
+#define SS_ABI_VERSION 9
 
 typedef enum { SS_F32 = 0, SS_I32 = 1 } ss_dtype_t;
 typedef enum { SS_POOL_MAX = 0, SS_POOL_AVG = 1 } ss_pool_mode_t;
@@ -262,6 +262,21 @@ ss_status_t ss_conv2d_backward_filter(const void* x, const void* dy, float* df, 
  * shapes run a direct kernel (same definition).  Statuses as above. */
 ss_status_t ss_conv1d_mc(const void* x, const void* w, float* y, int64_t batch, int64_t N,
                          int64_t cin, int64_t cout, int64_t k, void* stream);
+
+/* Multi-channel 2-D convolution (the Conclusion's multi-dimensional extension,
+ * PAPER.md l.226, of the channel-summed dot product above; reading R22):
+ *   y[b][r][c][co] = sum_{a<kh} sum_{e<kw} sum_{ci<cin} w[co][ci][a][e] * x[b][r+a][c+e][ci]
+ * for r < H-kh+1, c < W-kw+1 (valid padding, stride 1).  NHWC: x is
+ * [batch][H][W][cin] bfloat16, w is [cout][cin][kh][kw] bfloat16 (torch conv2d
+ * weight order), y is [batch][H-kh+1][W-kw+1][cout] fp32, all DEVICE memory.
+ * bf16 products are exact; accumulation is fp32.  cin, cout in {64, 128},
+ * kh*kw <= 64, (kh-1)*W + kw - 1 <= 1024 and 16-B aligned x / y run on the
+ * tensor cores: positions are flat over the image rows, so tap (a, e) is the
+ * staged tile shifted by a*W + e positions (no im2col); other shapes run a
+ * direct kernel (same definition).  Statuses as above (kh > H or kw > W ->
+ * SS_ERR_WINDOW_EXCEEDS_INPUT). */
+ss_status_t ss_conv2d_mc(const void* x, const void* w, float* y, int64_t batch, int64_t H, int64_t W,
+                         int64_t cin, int64_t cout, int64_t kh, int64_t kw, void* stream);
 
 /* ---- backward passes (training) ----------
  * Vector-Jacobian products of the forward calls above (DESIGN.md reading

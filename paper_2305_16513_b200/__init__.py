@@ -45,7 +45,7 @@ EXPORTED = ("ss_abi_version", "ss_out_len", "ss_pool_sum", "ss_pool_max", "ss_po
             "ss_affine_window", "ss_pool_sum_backward", "ss_pool_max_backward",
             "ss_conv1d_backward_input", "ss_conv1d_backward_filter_workspace", "ss_conv1d_backward_filter",
             "ss_pool2d_backward", "ss_conv2d", "ss_conv2d_backward_input", "ss_conv2d_backward_filter_workspace",
-            "ss_conv2d_backward_filter", "ss_conv1d_mc")
+            "ss_conv2d_backward_filter", "ss_conv1d_mc", "ss_conv2d_mc")
 
 
 class SSError(RuntimeError):
@@ -97,6 +97,8 @@ def _load() -> ctypes.CDLL:
     L.ss_conv2d.argtypes = [vp, vp, i64, i64, i64, ctypes.POINTER(ctypes.c_float), i64, i64, i64, i64, i32, vp]
     L.ss_conv1d_mc.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, vp]
     L.ss_conv1d_mc.restype = i32
+    L.ss_conv2d_mc.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i64, vp]
+    L.ss_conv2d_mc.restype = i32
     L.ss_conv2d.restype = i32
     L.ss_conv2d_backward_input.argtypes = [vp, vp, i64, i64, i64, ctypes.POINTER(ctypes.c_float), i64, i64, i64, i64,
                                            i32, vp]
@@ -249,6 +251,10 @@ def ss_conv2d_backward_filter(x_ptr, dy_ptr, df_ptr, planes, H, W, kh, kw, sh, s
 
 def ss_conv1d_mc(x_ptr, w_ptr, y_ptr, batch, N, cin, cout, k, stream=0) -> int:
     return _lib.ss_conv1d_mc(x_ptr, w_ptr, y_ptr, batch, N, cin, cout, k, stream)
+
+
+def ss_conv2d_mc(x_ptr, w_ptr, y_ptr, batch, H, W, cin, cout, kh, kw, stream=0) -> int:
+    return _lib.ss_conv2d_mc(x_ptr, w_ptr, y_ptr, batch, H, W, cin, cout, kh, kw, stream)
 
 
 def check(status: int) -> None:
@@ -604,4 +610,23 @@ def conv1d_mc(x, w, out=None, stream=None):
         raise SSError(SS_ERR_WINDOW_EXCEEDS_INPUT, f"window exceeds input: k={k} > N={N}")
     y = _alloc(out, (B, N - k + 1, cout), torch.float32, x.device)
     check(ss_conv1d_mc(x.data_ptr(), w.data_ptr(), y.data_ptr(), B, N, cin, cout, k, _stream(stream)))
+    return y
+
+
+def conv2d_mc(x, w, out=None, stream=None):
+    """Multi-channel 2-D convolution, NHWC: x [B, H, W, Cin] bfloat16 (CUDA), w [Cout, Cin, kh, kw]
+    bfloat16 (CUDA, torch conv2d weight order) -> y [B, H-kh+1, W-kw+1, Cout] float32 (valid, stride 1)."""
+    torch = _torch()
+    _dev(x, "x", torch.bfloat16)
+    _dev(w, "w", torch.bfloat16, device=x.device)
+    if x.dim() != 4 or w.dim() != 4:
+        raise ValueError("x must be [B, H, W, Cin] and w [Cout, Cin, kh, kw]")
+    B, H, W, cin = x.shape
+    cout, cin2, kh, kw = w.shape
+    if cin2 != cin:
+        raise ValueError("w's Cin does not match x")
+    if kh > H or kw > W:
+        raise SSError(SS_ERR_WINDOW_EXCEEDS_INPUT, f"window {kh}x{kw} exceeds input {H}x{W}")
+    y = _alloc(out, (B, H - kh + 1, W - kw + 1, cout), torch.float32, x.device)
+    check(ss_conv2d_mc(x.data_ptr(), w.data_ptr(), y.data_ptr(), B, H, W, cin, cout, kh, kw, _stream(stream)))
     return y

@@ -155,15 +155,17 @@ bool encode_plane_map(CUtensorMap* m, const float* base, int64_t W, int64_t H, i
 }
 
 // Channels-last bf16 activations for the multi-channel conv (conv_mc.cu):
-// element (e, p, a) = x[p * cin + 64 a + e]; box {64, 136, cin/64} lands as
-// [atom][position][64] = the SWIZZLE_128B K-major operand, one position per row.
-bool encode_mc_map(CUtensorMap* m, const void* x, int64_t positions, int64_t cin) {
+// element (e, p, a) = x[p * cin + 64 a + e]; box {64, box_rows, 1} lands one
+// K-atom of box_rows positions as a SWIZZLE_128B K-major block, one position
+// per 128-B row (positions past the array zero-filled).
+bool encode_mc_map(CUtensorMap* m, const void* x, int64_t positions, int64_t cin, int box_rows) {
   auto enc = encode_fn();
-  if (!enc || positions < 1 || positions > (int64_t(1) << 32) || cin % 64) return false;
+  if (!enc || positions < 1 || positions > (int64_t(1) << 32) || cin % 64 || box_rows > 256 || box_rows < 8)
+    return false;
   const int64_t at = cin / 64;
   cuuint64_t dims[3] = {64, (cuuint64_t)positions, (cuuint64_t)at};
   cuuint64_t strides[2] = {(cuuint64_t)(cin * 2), at > 1 ? 128 : (cuuint64_t)(positions * cin * 2)};
-  cuuint32_t box[3] = {64, 136, (cuuint32_t)at};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(x), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -672,6 +674,15 @@ ss_status_t ss_conv2d_backward_filter(const void* x, const void* dy, float* df, 
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv2d_backward_filter launch");
 }
 
+// TMA boxes per staged atom: nbox boxes of box_rows (<= 256, a multiple of 8) cover p.rows.
+static bool mc_boxes(ConvMcParams& p) {
+  p.rows = (p.rows + 7) / 8 * 8;
+  p.nbox = (p.rows + 255) / 256;
+  p.box_rows = ((p.rows + p.nbox - 1) / p.nbox + 7) / 8 * 8;
+  p.rows = p.box_rows * p.nbox;
+  return p.rows <= 2048;
+}
+
 ss_status_t ss_conv1d_mc(const void* x, const void* w, float* y, int64_t batch, int64_t N, int64_t cin,
                          int64_t cout, int64_t k, void* stream) {
   if (!x || !w || !y) return fail(SS_ERR_NULL, "x, w and y must be non-NULL device pointers");
@@ -690,12 +701,52 @@ ss_status_t ss_conv1d_mc(const void* x, const void* w, float* y, int64_t batch, 
   ConvMcParams p;
   memset(&p, 0, sizeof p);
   p.x = x; p.w = w; p.y = y; p.batch = batch; p.N = N; p.L = L; p.cin = cin; p.cout = cout; p.k = k;
+  for (int64_t j = 0; j < k && j < kMcMaxTaps; ++j) p.tap_off[j] = (int)j;
+  p.rows = 136;  // 128 outputs + k - 1 <= 136 staged positions
   const bool tc = (cin == 64 || cin == 128) && (cout == 64 || cout == 128) && k <= 9 &&
                   (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
-                  encode_mc_map(&p.tm_x, x, batch * N, cin);
+                  mc_boxes(p) && encode_mc_map(&p.tm_x, x, batch * N, cin, p.box_rows);
   p.clc = dynamic_tiles();
   cudaError_t e = launch_conv_mc(p, tc, static_cast<cudaStream_t>(stream), current_sms());
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv1d_mc launch");
+}
+
+ss_status_t ss_conv2d_mc(const void* x, const void* w, float* y, int64_t batch, int64_t H, int64_t W, int64_t cin,
+                         int64_t cout, int64_t kh, int64_t kw, void* stream) {
+  if (!x || !w || !y) return fail(SS_ERR_NULL, "x, w and y must be non-NULL device pointers");
+  if (batch < 1 || H < 1 || W < 1 || cin < 1 || cout < 1 || kh < 1 || kw < 1)
+    return fail(SS_ERR_BAD_SIZE, "batch/H/W/cin/cout/kh/kw must all be >= 1");
+  if (H > INT64_MAX / 8 / W || H * W > INT64_MAX / 8 / batch || batch * H * W > INT64_MAX / 8 / cin ||
+      batch * H * W > INT64_MAX / 8 / cout || kh * kw > INT64_MAX / 8 / cin / cout)
+    return fail(SS_ERR_BAD_SIZE, "sizes overflow int64");
+  if (kh > H || kw > W)
+    return fail(SS_ERR_WINDOW_EXCEEDS_INPUT, "window %lldx%lld exceeds input %lldx%lld", (long long)kh, (long long)kw,
+                (long long)H, (long long)W);
+  if ((reinterpret_cast<uintptr_t>(x) & 1) || (reinterpret_cast<uintptr_t>(w) & 1) ||
+      (reinterpret_cast<uintptr_t>(y) & 3))
+    return fail(SS_ERR_BAD_SIZE, "x / w must be 2-byte and y 4-byte aligned");
+  const int64_t OH = H - kh + 1, OW = W - kw + 1;
+  const int64_t ybytes = batch * OH * OW * cout * 4;
+  if (overlaps(x, batch * H * W * cin * 2, y, ybytes) || overlaps(w, cout * cin * kh * kw * 2, y, ybytes))
+    return fail(SS_ERR_OVERLAP, "y overlaps an input");
+  ConvMcParams p;
+  memset(&p, 0, sizeof p);
+  p.x = x; p.w = w; p.y = y; p.batch = batch; p.N = H * W; p.cin = cin; p.cout = cout; p.k = kh * kw;
+  p.two_d = 1; p.H = H; p.W = W; p.OH = OH; p.OW = OW;
+  // flat positions over the image rows: tap (a, e) reads the staged tile shifted by a W + e
+  // positions; a tile of 128 flat output positions stages 128 + (kh-1) W + kw - 1 positions
+  bool tc = (cin == 64 || cin == 128) && (cout == 64 || cout == 128) && kh * kw <= kMcMaxTaps &&
+            (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
+            (kh - 1) * W + kw - 1 <= 1024;
+  if (tc) {
+    for (int64_t a = 0; a < kh; ++a)
+      for (int64_t e = 0; e < kw; ++e) p.tap_off[a * kw + e] = (int)(a * W + e);
+    p.rows = (int)(128 + (kh - 1) * W + kw - 1);
+    tc = mc_boxes(p) && encode_mc_map(&p.tm_x, x, batch * H * W, cin, p.box_rows);
+  }
+  p.clc = dynamic_tiles();
+  cudaError_t e = launch_conv_mc(p, tc, static_cast<cudaStream_t>(stream), current_sms());
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv2d_mc launch");
 }
 
 ss_status_t ss_conv2d(const void* x, void* y, int64_t planes, int64_t H, int64_t W, const float* filter_host,

@@ -36,7 +36,6 @@ constexpr int kMcThreads = 320;
 constexpr int kMcWarpMma = 1;
 constexpr int kMcWarpEpi0 = 2;
 constexpr int kMcEpiWarps = 8;
-constexpr int kMcRows = 136;  // staged positions per tile: 128 + k - 1 <= 136, a multiple of 8
 constexpr int kMcStages = 3;
 constexpr int kMcRing = 8;    // tile-id ring entries
 
@@ -105,19 +104,20 @@ __device__ __forceinline__ void tma_load_3d_mc(void* smem_dst, const CUtensorMap
 template <int CIN, int COUT>
 __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_constant__ ConvMcParams p) {
   constexpr int AT = CIN / 64;                        // K-atoms (64 bf16 = 128 B) per position
-  constexpr uint32_t kAtomBytes = kMcRows * 128u;     // one atom of a staged tile
-  constexpr uint32_t kStage = AT * kAtomBytes;
+  const uint32_t kAtomBytes = (uint32_t)p.rows * 128u;  // one atom of a staged tile
+  const uint32_t kStage = AT * kAtomBytes;
   constexpr uint32_t kWTap = AT * COUT * 128u;        // one tap of the weights
   constexpr int NH = COUT / 2;                        // epilogue columns per warp
   constexpr uint32_t kTmemCols = 2 * COUT <= 128 ? 128 : 256;
   extern __shared__ __align__(16) uint8_t mc_raw[];  // aligned to 1024 by hand (slack in conv_mc_smem_bytes)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(mc_raw) + 1023) & ~uintptr_t(1023));
   const int k = (int)p.k;
-  uint8_t* xs = smem;                                  // [kMcStages][AT][kMcRows][128 B]
+  const int kMcStages = p.stages;
+  uint8_t* xs = smem;                                  // [stages][AT][rows][128 B]
   uint8_t* ws = smem + kMcStages * kStage;             // [k][AT][COUT][128 B]
   uint64_t* bars = reinterpret_cast<uint64_t*>(ws + (size_t)k * kWTap);
-  uint64_t* full = bars;                               // [kMcStages]
-  uint64_t* empty = full + kMcStages;                  // [kMcStages]
+  uint64_t* full = bars;                               // [stages]
+  uint64_t* empty = full + kMcStages;                  // [stages]
   uint64_t* dfull = empty + kMcStages;                 // [2]
   uint64_t* dempty = dfull + 2;                        // [2]
   // tile ids, producer -> MMA (read after its `full` wait) and epilogue (own barrier pair);
@@ -177,7 +177,10 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
           break;
         }
         mbar_arrive_expect_tx(full + s, kStage);
-        tma_load_3d_mc(xs + (size_t)s * kStage, &p.tm_x, 0, (int32_t)(t * 128), 0, full + s);
+        for (int a = 0; a < AT; ++a)  // one SW128 block per K-atom, nbox boxes of box_rows positions
+          for (int bx = 0; bx < p.nbox; ++bx)
+            tma_load_3d_mc(xs + (size_t)s * kStage + (size_t)a * kAtomBytes + (size_t)bx * p.box_rows * 128, &p.tm_x,
+                           0, (int32_t)(t * 128 + bx * p.box_rows), a, full + s);
         if (++s == kMcStages) { s = 0; ph ^= 1; }
         if (p.clc) {
           t = clc_wait(&clc, cph);  // requested one tile ahead
@@ -209,7 +212,7 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
         for (int a = 0; a < AT; ++a)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {  // K-steps of 16 channels (32 B) inside the atom
-            const uint64_t da = dxs + (uint64_t)((a * kAtomBytes + (uint32_t)j * 128u + 32u * q) >> 4);
+            const uint64_t da = dxs + (uint64_t)((a * kAtomBytes + (uint32_t)p.tap_off[j] * 128u + 32u * q) >> 4);
             const uint64_t db = dw0 + (uint64_t)(((uint32_t)j * kWTap + a * (COUT * 128u) + 32u * q) >> 4);
             mma_bf16_ss(dcol, da, db, idesc, acc);
             acc = 1;
@@ -246,15 +249,24 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(dempty + d);
+      // flat input position of the tile's first row: one 64-bit division per tile
+      const int64_t b0 = (t * 128) / p.N, i0 = t * 128 - b0 * p.N;
 #pragma unroll
       for (int lh = 0; lh < 2; ++lh)
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {  // rows lane/4 and lane/4 + 8 of this 16-lane half
           const int m = 32 * q + 16 * lh + (lane >> 2) + 8 * rr;
-          const int64_t pos = t * 128 + m;  // flat input position = window start
-          const int64_t b = pos / p.N, i = pos - b * p.N;
-          if (b < p.batch && i < p.L) {
-            float* __restrict__ yr = p.y + (b * p.L + i) * COUT + h * NH + 2 * (lane & 3);
+          int64_t b = b0, i = i0 + m;       // flat input position = window start
+          while (i >= p.N) { i -= p.N; ++b; }
+          int64_t o = -1;                   // output row of this position (-1: its window leaves the row / image)
+          if (!p.two_d) {
+            if (b < p.batch && i < p.L) o = b * p.L + i;
+          } else {
+            const uint32_t r = (uint32_t)i / (uint32_t)p.W, c = (uint32_t)i - r * (uint32_t)p.W;
+            if (b < p.batch && r < p.OH && c < p.OW) o = (b * p.OH + r) * p.OW + c;
+          }
+          if (o >= 0) {
+            float* __restrict__ yr = p.y + o * COUT + h * NH + 2 * (lane & 3);
 #pragma unroll
             for (int cb = 0; cb < NH / 8; ++cb)
               *reinterpret_cast<float2*>(yr + 8 * cb) =
@@ -272,6 +284,26 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
 
 // Direct kernel (any shape / alignment): one (position, channel) per thread,
 // fp32 accumulation of the exact bf16 products in (j, ci) order.
+__global__ void __launch_bounds__(256) conv2d_mc_direct_kernel(const __grid_constant__ ConvMcParams p) {
+  const uint16_t* __restrict__ x = static_cast<const uint16_t*>(p.x);
+  const uint16_t* __restrict__ w = static_cast<const uint16_t*>(p.w);
+  const int64_t kw = p.k / (p.H - p.OH + 1);
+  const int64_t kh = p.k / kw;
+  const int64_t total = p.batch * p.OH * p.OW * p.cout;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t co = o % p.cout, pix = o / p.cout, c = pix % p.OW, rb = pix / p.OW, r = rb % p.OH, b = rb / p.OH;
+    float acc = 0.0f;
+    for (int64_t a = 0; a < kh; ++a)
+      for (int64_t e = 0; e < kw; ++e)
+        for (int64_t ci = 0; ci < p.cin; ++ci) {
+          const float xv = __uint_as_float((uint32_t)__ldg(x + ((b * p.H + r + a) * p.W + c + e) * p.cin + ci) << 16);
+          const float wv = __uint_as_float((uint32_t)__ldg(w + ((co * p.cin + ci) * kh + a) * kw + e) << 16);
+          acc = __fmaf_rn(wv, xv, acc);
+        }
+    p.y[o] = acc;
+  }
+}
+
 __global__ void __launch_bounds__(256) conv_mc_direct_kernel(const __grid_constant__ ConvMcParams p) {
   const uint16_t* __restrict__ x = static_cast<const uint16_t*>(p.x);
   const uint16_t* __restrict__ w = static_cast<const uint16_t*>(p.w);
@@ -289,15 +321,16 @@ __global__ void __launch_bounds__(256) conv_mc_direct_kernel(const __grid_consta
   }
 }
 
-size_t conv_mc_smem_bytes(int64_t cin, int64_t cout, int64_t k) {
-  const size_t stage = (size_t)(cin / 64) * kMcRows * 128;
-  return 1024 + kMcStages * stage + (size_t)k * (cin / 64) * cout * 128 + 8 * (2 * kMcStages + 4) +
-         24 * kMcRing + 16;
+size_t conv_mc_smem_bytes(int64_t cin, int64_t cout, int64_t k, int rows, int stages) {
+  const size_t stage = (size_t)(cin / 64) * rows * 128;
+  return 1024 + stages * stage + (size_t)k * (cin / 64) * cout * 128 + 8 * (2 * stages + 4) + 24 * kMcRing + 16;
 }
 
 template <int CIN, int COUT>
 static cudaError_t launch_mc(ConvMcParams& p, cudaStream_t stream, int sms) {
-  const size_t smem = conv_mc_smem_bytes(CIN, COUT, p.k);
+  p.stages = kMcStages;  // ring depth: 3, or 2 when the staged rows and the weights need the room
+  while (p.stages > 2 && conv_mc_smem_bytes(CIN, COUT, p.k, p.rows, p.stages) > (size_t)kSmemBudget) --p.stages;
+  const size_t smem = conv_mc_smem_bytes(CIN, COUT, p.k, p.rows, p.stages);
   if (smem > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
   auto kfn = conv_mc_kernel<CIN, COUT>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kfn));
@@ -320,10 +353,11 @@ cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t strea
     else if (p.cin == 128 && p.cout == 128) e = launch_mc<128, 128>(p, stream, sms);
     if (e != cudaErrorInvalidConfiguration) return e;
   }
-  const int64_t total = p.batch * p.L * p.cout;
+  const int64_t total = p.two_d ? p.batch * p.OH * p.OW * p.cout : p.batch * p.L * p.cout;
   int64_t g = (total + 255) / 256;
   if (g > (int64_t)sms * 16) g = (int64_t)sms * 16;
-  conv_mc_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
+  if (p.two_d) conv2d_mc_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
+  else conv_mc_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
   note_launch();
   return cudaGetLastError();
 }

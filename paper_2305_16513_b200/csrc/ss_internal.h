@@ -233,17 +233,24 @@ size_t conv2d_backward_filter_workspace(int64_t taps, int ctas);
 cudaError_t launch_conv2d_backward_filter(Conv2DBwdParams& p, float* df, void* workspace, int ctas,
                                           cudaStream_t stream);
 
-// Multi-channel conv1d, channels-last bf16 (conv_mc.cu).
+// Multi-channel conv1d / conv2d, channels-last bf16 (conv_mc.cu; SURVEY 8f NEXT #4,
+// readings R18, R22).  Positions are flat over batch x (H x) W; tap j reads the
+// staged tile shifted by tap_off[j] positions (1-D: j; 2-D: a W + e).
+constexpr int kMcMaxTaps = 64;
 struct alignas(64) ConvMcParams {
-  CUtensorMap tm_x;  // 3-D {64, batch*N, cin/64}, strides {cin*2 B, 128 B}, box {64, 136, cin/64}, SW128, bf16
-  const void* x;     // [batch][N][cin] bf16
-  const void* w;     // [cout][cin][k] bf16
-  float* y;          // [batch][L][cout] fp32
-  int64_t batch, N, L, cin, cout, k;
+  CUtensorMap tm_x;  // 3-D {64, positions, cin/64}, box {64, box_rows, 1}, SW128, bf16 (encode_mc_map)
+  const void* x;     // [batch][N][cin] or [batch][H][W][cin] bf16
+  const void* w;     // [cout][cin][k] or [cout][cin][kh][kw] bf16 (k = taps)
+  float* y;          // [batch][L][cout] or [batch][OH][OW][cout] fp32
+  int64_t batch, N, L, cin, cout, k;  // 1-D geometry (2-D: N = H * W, k = kh * kw)
+  int64_t H, W, OH, OW;               // 2-D geometry (two_d)
+  int two_d;
+  int rows, box_rows, nbox, stages;   // staged positions per tile (multiple of 8), TMA boxes per atom, ring depth
+  int tap_off[kMcMaxTaps];
   int64_t ntiles;    // set by launch_conv_mc
   int clc;  // 1: one CTA per work unit, units claimed by cluster launch control (ss_device.cuh); 0: static stride
 };
-bool encode_mc_map(CUtensorMap* m, const void* x, int64_t positions, int64_t cin);
+bool encode_mc_map(CUtensorMap* m, const void* x, int64_t positions, int64_t cin, int box_rows);
 cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t stream, int sms);
 
 }  // namespace ss
