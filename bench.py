@@ -1307,7 +1307,7 @@ def run_reference(args):
     import oracle
     oracle.build()
     cores = os.cpu_count() or 1
-    frac = 1.0 / 256 if args.workload != "cfg1" else 1.0
+    frac = 1.0 / 32 if args.workload != "cfg1" else 1.0
     plan = oracle_sample_plan(args.workload, frac)
     for _ in range(args.warmup):
         _run_parts(plan, cores)

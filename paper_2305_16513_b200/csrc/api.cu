@@ -594,6 +594,20 @@ static ss_status_t pool2d_backward_impl(const void* x, const void* dy, void* dx,
   p.inv_area = 1.0f / (float)(kh * kw);
   const int64_t nx = planes * H * W * 4, ny = planes * p.OH * p.OW * 4;
   if (overlaps(dy, ny, dx, nx) || (x && overlaps(x, nx, dx, nx))) return fail(SS_ERR_OVERLAP, "dx overlaps an input");
+  if (p.mode == 1 && sh == 1 && sw == 1 && tile_2d_enabled() && conv2d_tile_supported((int)kh, (int)kw, H, W)) {
+    // average pooling at stride 1: dx = the full correlation of dy with the box 1/(kh kw) -- the
+    // 2-D tile kernel's padded mode, as for the conv2d input gradient
+    Conv2DTileParams t;
+    memset(&t, 0, sizeof t);
+    t.x = p.dy; t.y = p.dx; t.planes = planes;
+    t.IH = (int)p.OH; t.IW = (int)p.OW; t.OH = (int)H; t.OW = (int)W; t.KH = (int)kh; t.KW = (int)kw;
+    t.pad_t = (int)kh - 1; t.pad_l = (int)kw - 1;
+    for (int64_t i = 0; i < kh * kw; ++i) t.taps[i] = p.inv_area;
+    t.clc = dynamic_tiles();
+    cudaError_t e = launch_conv2d_tile(t, static_cast<cudaStream_t>(stream), current_sms());
+    if (e == cudaSuccess) return SS_OK;
+    if (e != cudaErrorInvalidConfiguration) return cuda_fail(e, "pool2d_backward tile launch");
+  }
   cudaError_t e = launch_pool2d_backward(p, static_cast<cudaStream_t>(stream), current_sms());
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "pool2d_backward launch");
 }

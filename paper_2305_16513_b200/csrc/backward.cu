@@ -1075,7 +1075,58 @@ static cudaError_t launch_pool2d_bwd_fixed(const Pool2DBackwardParams& p, cudaSt
   return cudaGetLastError();
 }
 
+// 2x2 windows at stride 2 (disjoint, covering the plane; H even, W % 4 == 0):
+// a thread owns two neighbouring windows = a 2 x 4 block of dx.  avg spreads
+// dy / 4; max sends dy to the window's first maximum in row-major order (ties
+// to the earlier element, reading R16) and writes 0 elsewhere.  Every x / dx
+// access is one 16-B vector (rows are 16-B aligned), dy one 8-B vector: a pure
+// stream, read x (max) + dy, write dx.
+template <bool kAvg>
+__global__ void __launch_bounds__(256) pool2d_bwd_2x2s2_kernel(const __grid_constant__ Pool2DBackwardParams p) {
+  const int64_t qpr = p.W / 4;                 // window pairs per row of windows
+  const int64_t total = p.planes * p.OH * qpr;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e % qpr, rr = e / qpr;   // rr = plane * OH + r
+    const int64_t row0 = 2 * rr;                // first input row (plane-major flat: plane * H + 2 r)
+    const float2 g = *reinterpret_cast<const float2*>(p.dy + rr * p.OW + 2 * q);
+    float4* d0 = reinterpret_cast<float4*>(p.dx + row0 * p.W + 4 * q);
+    float4* d1 = reinterpret_cast<float4*>(p.dx + (row0 + 1) * p.W + 4 * q);
+    if (kAvg) {
+      const float a = g.x * p.inv_area, b = g.y * p.inv_area;
+      *d0 = make_float4(a, a, b, b);
+      *d1 = make_float4(a, a, b, b);
+    } else {
+      const float4 u = *reinterpret_cast<const float4*>(p.x + row0 * p.W + 4 * q);
+      const float4 v = *reinterpret_cast<const float4*>(p.x + (row0 + 1) * p.W + 4 * q);
+      // window 0: u.x u.y / v.x v.y ; window 1: u.z u.w / v.z v.w -- first maximum, row-major
+      int i0 = 0;
+      float m0 = u.x;
+      if (u.y > m0) { m0 = u.y; i0 = 1; }
+      if (v.x > m0) { m0 = v.x; i0 = 2; }
+      if (v.y > m0) { m0 = v.y; i0 = 3; }
+      int i1 = 0;
+      float m1 = u.z;
+      if (u.w > m1) { m1 = u.w; i1 = 1; }
+      if (v.z > m1) { m1 = v.z; i1 = 2; }
+      if (v.w > m1) { m1 = v.w; i1 = 3; }
+      *d0 = make_float4(i0 == 0 ? g.x : 0.f, i0 == 1 ? g.x : 0.f, i1 == 0 ? g.y : 0.f, i1 == 1 ? g.y : 0.f);
+      *d1 = make_float4(i0 == 2 ? g.x : 0.f, i0 == 3 ? g.x : 0.f, i1 == 2 ? g.y : 0.f, i1 == 3 ? g.y : 0.f);
+    }
+  }
+}
+
 cudaError_t launch_pool2d_backward(const Pool2DBackwardParams& p, cudaStream_t stream, int sms) {
+  if (p.kh == 2 && p.kw == 2 && p.sh == 2 && p.sw == 2 && p.H % 2 == 0 && p.W % 4 == 0 &&
+      ((reinterpret_cast<uintptr_t>(p.dx) | reinterpret_cast<uintptr_t>(p.x)) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(p.dy) & 7) == 0) {
+    const int64_t total = p.planes * p.OH * (p.W / 4);
+    int64_t g = (total + 255) / 256;
+    if (g > (int64_t)sms * 16) g = (int64_t)sms * 16;
+    if (p.mode == 1) pool2d_bwd_2x2s2_kernel<true><<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
+    else pool2d_bwd_2x2s2_kernel<false><<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
+    note_launch();
+    return cudaGetLastError();
+  }
   {
     cudaError_t e = cudaErrorInvalidConfiguration;
     if (p.kh == 3 && p.kw == 3 && p.sh == 1 && p.sw == 1) e = launch_pool2d_bwd_fixed<3, 3, 1, 1>(p, stream, sms);
