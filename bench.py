@@ -630,19 +630,20 @@ class Runner:
 
     # ---- CUDA graphs: the same launch mode at every N
     def capture(self, si=0):
-        """Capture the step's kernels as two CUDA graphs: A = every cell's interior
+        """Capture the step's kernels as two CUDA graphs (thread-local capture mode, so the NCCL
+        watchdog thread's event queries stay legal during capture): A = every cell's interior
         (all of it for batch-sharded cells), B = the sequence-sharded tails (empty
         at N = 1).  The NCCL halo is posted eagerly before A and waited before B.
         Returns (graph A, graph B or None, libss launches per step)."""
         torch, ss = self.torch, self.ss
         n0 = ss.ss_launch_count()
         ga = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(ga, stream=self.stream):
+        with torch.cuda.graph(ga, stream=self.stream, capture_error_mode="thread_local"):
             self.launch_interiors(si)
         gb = None
         if self.world > 1 and self.seq_keys():
             gb = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gb, stream=self.stream):
+            with torch.cuda.graph(gb, stream=self.stream, capture_error_mode="thread_local"):
                 self.launch_tails(si)
         return ga, gb, ss.ss_launch_count() - n0
 
@@ -665,7 +666,7 @@ class Runner:
         nsets = len(self.xs)
         for c in self.cells:
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=self.stream):
+            with torch.cuda.graph(g, stream=self.stream, capture_error_mode="thread_local"):
                 for r in range(reps):
                     self.launch_cell(c, r % nsets, "whole")
             g.replay()
