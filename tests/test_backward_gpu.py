@@ -212,3 +212,29 @@ def test_backward_matches_torch_autograd_cfg3_slice(ss):
     assert torch.all((dx.double() - xt.grad).abs() <= TOL_REL * mag_x + TOL_ABS)
     mag_f = (x.double().abs()[:, None, :].unfold(2, N - k + 1, 1)[:, 0] * dy.double().abs()[:, None, :]).sum((0, 2))
     assert torch.all((df.double() - ft.grad).abs() <= TOL_REL * mag_f + TOL_ABS)
+
+
+@pytest.mark.parametrize("P,H,W,kh,kw,sh,sw", [(3, 16, 16, 2, 2, 2, 2), (2, 112, 112, 2, 2, 2, 2), (2, 10, 36, 2, 2, 2, 2),
+                                                (2, 112, 112, 3, 3, 1, 1), (3, 37, 150, 3, 3, 1, 1),
+                                                (2, 30, 140, 5, 5, 1, 1), (1, 20, 21, 7, 7, 1, 1)])
+@pytest.mark.parametrize("mode", ["max", "avg"])
+@pytest.mark.parametrize("ties", [False, True])
+def test_pool2d_backward_fast_paths(ss, mode, ties, P, H, W, kh, kw, sh, sw):
+    """16-B aligned buffers take the round-2 kernels: the 2x2/2 stream kernel (first-max routing,
+    ties from integer-valued x) and, for avg at stride 1, the 2-D tile kernel (full correlation of
+    dy with the 1/(kh kw) box)."""
+    OH, OW = (H - kh) // sh + 1, (W - kw) // sw + 1
+    x = (synth.randint(33, P * H * W, 0, 3).astype(np.float32) if ties else
+         synth.uniform01(33, P * H * W)).reshape(P, H, W)
+    dy = synth.normal(34, P * OH * OW).reshape(P, OH, OW)
+    m = ss.SS_POOL_MAX if mode == "max" else ss.SS_POOL_AVG
+    xd = torch.from_numpy(x).cuda()
+    dyd = torch.from_numpy(dy).cuda()
+    dx = ss.pool2d_backward(xd, dyd, (kh, kw), (sh, sw), mode)
+    torch.cuda.synchronize()
+    ref, mag = oracle.pool2d_backward(x, dy, H, W, kh, kw, sh, sw, oracle.POOL2D_MAX if mode == "max" else
+                                      oracle.POOL2D_AVG)
+    got = dx.cpu().numpy()
+    within(got, ref, mag, f"pool2d bwd fast {mode} ties={ties} {(P, H, W, kh, kw, sh, sw)}")
+    if mode == "max":  # routing is exact: each dy lands whole on one element
+        np.testing.assert_array_equal(got.astype(np.float64) != 0, ref != 0)

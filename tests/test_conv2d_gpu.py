@@ -39,6 +39,10 @@ CASES = [  # (P, H, W, kh, kw, sh, sw)
     (3, 112, 112, 3, 3, 1, 1), (2, 112, 112, 5, 5, 1, 1), (2, 64, 96, 7, 7, 1, 1), (3, 40, 36, 1, 3, 1, 1),
     (2, 40, 36, 3, 1, 1, 1), (2, 112, 112, 3, 3, 1, 2), (2, 30, 44, 5, 5, 1, 2), (2, 112, 112, 3, 3, 2, 2),
     (3, 31, 29, 3, 3, 1, 1), (1, 17, 200, 4, 6, 3, 2), (2, 9, 9, 9, 9, 1, 1), (1, 5, 1000, 2, 33, 1, 1),
+    # the round-2 FFMA2 tile kernel (stride-1 5x5 / 7x7): TMA mode (16-B rows), dense mode (even
+    # rows of other widths), ragged units, a plane of one unit, an odd width (direct kernel)
+    (3, 112, 112, 7, 7, 1, 1), (2, 50, 114, 7, 7, 1, 1), (2, 23, 58, 5, 5, 1, 1), (1, 7, 7, 7, 7, 1, 1),
+    (2, 40, 113, 7, 7, 1, 1), (1, 250, 250, 5, 5, 1, 1), (3, 19, 36, 7, 7, 1, 1),
 ]
 
 
