@@ -21,7 +21,7 @@ __host__ __device__ constexpr uint32_t idesc(int fmt, int M, int N) {
   return (1u << 4) | ((uint32_t)fmt << 7) | ((uint32_t)fmt << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int KIND, bool A_TMEM, int N, int NACC, int M = 128>
+template <int KIND, bool A_TMEM, int N, int NACC, int M = 128, int AROW = 0>
 __global__ void probe(long long* out, int reps) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* s = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
@@ -45,7 +45,7 @@ __global__ void probe(long long* out, int reps) {
   if (warp == 0) {
     constexpr uint32_t id = idesc(KIND == 0 ? 2 : 1, M, N);
     const uint64_t bdesc = sw128_desc(smem_u32(s));
-    const uint64_t adesc = sw128_desc(smem_u32(s + 32768));
+    const uint64_t adesc = sw128_desc(smem_u32(s + 32768 + 128 * AROW));  // AROW: start AROW rows into a SW128 atom
     const uint32_t a_t = tmem, d0 = tmem + 256;
     long long t0 = clock64();
     for (int r = 0; r < reps; ++r) {
@@ -93,9 +93,9 @@ __global__ void probe(long long* out, int reps) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-template <int KIND, bool A_TMEM, int N, int NACC, int M = 128>
+template <int KIND, bool A_TMEM, int N, int NACC, int M = 128, int AROW = 0>
 void run(const char* name, long long* d) {
-  auto k = probe<KIND, A_TMEM, N, NACC, M>;
+  auto k = probe<KIND, A_TMEM, N, NACC, M, AROW>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   const int reps = 4096;
   k<<<148, 128, 80 * 1024>>>(d, 64);
@@ -126,5 +126,9 @@ int main() {
   run<1, true, 64, 1, 64>("M=64 bf16 K=16 A=TMEM N=64  1 acc", d);
   run<0, false, 64, 1, 64>("M=64 tf32 K=8  A=SMEM N=64  1 acc", d);
   run<0, true, 128, 1, 64>("M=64 tf32 K=8  A=TMEM N=128 1 acc", d);
+  run<1, false, 64, 1, 128, 1>("bf16 A=SMEM start +1 row (SW128) N=64", d);
+  run<1, false, 64, 1, 128, 3>("bf16 A=SMEM start +3 rows (SW128) N=64", d);
+  run<1, false, 64, 1, 128, 8>("bf16 A=SMEM start +8 rows (SW128) N=64", d);
+  run<1, false, 128, 1, 128, 1>("bf16 A=SMEM start +1 row (SW128) N=128", d);
   return 0;
 }
