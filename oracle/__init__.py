@@ -92,6 +92,8 @@ def lib() -> ctypes.CDLL:
             L.oracle_conv1d_mc_bf16.restype = ctypes.c_int
             L.oracle_conv2d_mc_bf16.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, vp]
             L.oracle_conv2d_mc_bf16.restype = ctypes.c_int
+            L.oracle_conv1d_mc_backward_input_bf16.argtypes = [vp, vp, i64, i64, i64, i64, i64, vp, vp]
+            L.oracle_conv1d_mc_backward_input_bf16.restype = ctypes.c_int
             L.oracle_conv2d_f32.argtypes = [vp, i64, i64, i64, vp, i64, i64, i64, i64, vp, vp]
             L.oracle_conv2d_f32.restype = ctypes.c_int
             L.oracle_conv2d_backward_input_f32.argtypes = [vp, i64, i64, i64, vp, i64, i64, i64, i64, vp, vp]
@@ -450,3 +452,17 @@ def conv2d_mc(x_bf16: np.ndarray, w_bf16: np.ndarray):
     m = np.empty((B, OH, OW, cout), np.float64)
     _check(lib().oracle_conv2d_mc_bf16(_p(x), _p(w), B, H, W, cin, cout, kh, kw, _p(y), _p(m)))
     return y, m
+
+
+def conv1d_mc_backward_input(dy_bf16: np.ndarray, w_bf16: np.ndarray, N: int):
+    """dx [B, N, Cin] (double) of the multi-channel conv1d for bf16 dy [B, N-k+1, Cout] and
+    w [Cout, Cin, k] (reading R23); returns (dx, absmag)."""
+    dy = np.ascontiguousarray(dy_bf16, np.uint16)
+    w = np.ascontiguousarray(w_bf16, np.uint16)
+    B, L, cout = dy.shape
+    cout2, cin, k = w.shape
+    assert cout2 == cout and L == N - k + 1
+    dx = np.empty((B, N, cin), np.float64)
+    m = np.empty((B, N, cin), np.float64)
+    _check(lib().oracle_conv1d_mc_backward_input_bf16(_p(dy), _p(w), B, N, cin, cout, k, _p(dx), _p(m)))
+    return dx, m

@@ -659,3 +659,31 @@ int oracle_conv2d_mc_bf16(const uint16_t* x, const uint16_t* w, int64_t batch, i
         }
   return 0;
 }
+
+/* Input gradient of the multi-channel 1-D convolution (reading R23: the
+ * vector-Jacobian product of reading R18), bf16 dy and weights:
+ *   y[b][i][co] = sum_j sum_ci w[co][ci][j] x[b][i+j][ci]
+ *   =>  dx[b][i+j][ci] += w[co][ci][j] * dy[b][i][co]   for every (b, i, j, co, ci)
+ * dy [batch][N-k+1][cout], w [cout][cin][k], dx [batch][N][cin] (elements no window
+ * covers get 0); the scatter is accumulated in double in (i, j, co) order. */
+int oracle_conv1d_mc_backward_input_bf16(const uint16_t* dy, const uint16_t* w, int64_t batch, int64_t N,
+                                         int64_t cin, int64_t cout, int64_t k, double* dx, double* absmag) {
+  if (dy == NULL || w == NULL || dx == NULL || batch < 1 || cin < 1 || cout < 1 || k < 1 || k > N) return -1;
+  int64_t L = N - k + 1;
+  for (int64_t t = 0; t < batch * N * cin; ++t) {
+    dx[t] = 0.0;
+    if (absmag) absmag[t] = 0.0;
+  }
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t i = 0; i < L; ++i)
+      for (int64_t j = 0; j < k; ++j)
+        for (int64_t co = 0; co < cout; ++co) {
+          double g = bf16_to_double(dy[(b * L + i) * cout + co]);
+          for (int64_t ci = 0; ci < cin; ++ci) {
+            double p = bf16_to_double(w[(co * cin + ci) * k + j]) * g;
+            dx[(b * N + i + j) * cin + ci] += p;
+            if (absmag) absmag[(b * N + i + j) * cin + ci] += fabs(p);
+          }
+        }
+  return 0;
+}

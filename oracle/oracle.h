@@ -151,6 +151,10 @@ int oracle_conv1d_mc_bf16(const uint16_t* x, const uint16_t* w, int64_t batch, i
  * weights, valid padding, stride 1 (reading R22); y [batch][H-kh+1][W-kw+1][cout]. */
 int oracle_conv2d_mc_bf16(const uint16_t* x, const uint16_t* w, int64_t batch, int64_t H, int64_t W, int64_t cin,
                           int64_t cout, int64_t kh, int64_t kw, double* y, double* absmag);
+/* Input gradient of the multi-channel 1-D convolution (reading R23): dy [batch][N-k+1][cout] and
+ * w [cout][cin][k] as bf16 bits; dx [batch][N][cin] = the scatter of w * dy, in double. */
+int oracle_conv1d_mc_backward_input_bf16(const uint16_t* dy, const uint16_t* w, int64_t batch, int64_t N,
+                                         int64_t cin, int64_t cout, int64_t k, double* dx, double* absmag);
 
 #ifdef __cplusplus
 }

@@ -561,3 +561,36 @@ def test_conv2d_mc_vs_torch_and_reductions():
     for r in range(H):
         y1, _ = oracle.conv1d_mc(np.ascontiguousarray(xb[:, r]), np.ascontiguousarray(wb[:, :, 0, :]))
         np.testing.assert_array_equal(y[:, r], y1)
+
+
+# ------------------------------------------------ multi-channel conv1d input gradient (reading R23)
+def test_conv1d_mc_backward_input_adjoint_and_torch():
+    B, N, cin, cout, k = 2, 30, 5, 4, 3
+    # adjoint identity on integers (exact in bf16 and double): <conv1d_mc(x), dy> = <x, dx>
+    x = synth.randint(104, B * N * cin, -5, 5).astype(np.float32).reshape(B, N, cin)
+    w = synth.randint(105, cout * cin * k, -3, 3).astype(np.float32).reshape(cout, cin, k)
+    dy = synth.randint(106, B * (N - k + 1) * cout, -4, 4).astype(np.float32).reshape(B, N - k + 1, cout)
+    xb, wb, gb = oracle.to_bf16_bits(x), oracle.to_bf16_bits(w), oracle.to_bf16_bits(dy)
+    y, _ = oracle.conv1d_mc(xb, wb)
+    dx, mag = oracle.conv1d_mc_backward_input(gb, wb, N)
+    assert float((y * dy).sum()) == float((x.astype(np.float64) * dx).sum())
+    # torch float64 autograd of conv1d (NCW), signed values; magnitude = the same VJP on |w|, |dy|
+    xf = synth.normal(107, B * N * cin).reshape(B, N, cin)
+    wf = synth.normal(108, cout * cin * k).reshape(cout, cin, k)
+    gf = synth.normal(109, B * (N - k + 1) * cout).reshape(B, N - k + 1, cout)
+    wb, gb = oracle.to_bf16_bits(wf), oracle.to_bf16_bits(gf)
+    dx, mag = oracle.conv1d_mc_backward_input(gb, wb, N)
+    wt = torch.tensor(oracle.bf16_bits_to_f32(wb), dtype=torch.float64)
+    gt = torch.tensor(oracle.bf16_bits_to_f32(gb), dtype=torch.float64).permute(0, 2, 1)
+    ref = torch.nn.grad.conv1d_input((B, cin, N), wt, gt).permute(0, 2, 1).numpy()
+    np.testing.assert_allclose(dx, ref, rtol=1e-12, atol=1e-12)
+    refm = torch.nn.grad.conv1d_input((B, cin, N), wt.abs(), gt.abs()).permute(0, 2, 1).numpy()
+    np.testing.assert_allclose(mag, refm, rtol=1e-12, atol=1e-12)
+    assert np.any(mag > np.abs(dx) + 1e-9)
+    # one channel each way: the single-channel input gradient oracle
+    g1 = synth.normal(110, B * (N - k + 1)).reshape(B, N - k + 1, 1)
+    w1 = synth.normal(111, k).reshape(1, 1, k)
+    g1b, w1b = oracle.to_bf16_bits(g1), oracle.to_bf16_bits(w1)
+    dx1, _ = oracle.conv1d_mc_backward_input(g1b, w1b, N)
+    ref1, _ = oracle.conv1d_backward_input(oracle.bf16_bits_to_f32(g1b)[..., 0], oracle.bf16_bits_to_f32(w1b)[0, 0], N)
+    np.testing.assert_allclose(dx1[..., 0], ref1, rtol=1e-12, atol=1e-12)
