@@ -190,6 +190,14 @@ def cfg_cells(workload: str, cfg5_log2n: int = 32):
                                shard="batch")
             wf = synth.normal(97, cout * cin * k, sigma=(cin * k) ** -0.5).reshape(cout, cin, k)
             cells.append(Cell("mc", f"mc_c{cin}x{cout}_k{k}", "conv_mc", w=k, f=wf, inp=key, kh=cin, kw=cout))
+        # its input gradient (reading R23): dy [16][65536-k+1][cout] bf16 -> dx [16][65536][cin] fp32
+        for cin, cout, k in ((64, 64, 3), (128, 128, 3)):
+            key = f"gmc{cout}_k{k}"
+            inputs[key] = dict(rows=16, n=(65536 - k + 1) * cout, dtype="bfloat16", dist="normal", seed=98, kw={},
+                               shard="batch")
+            wf = synth.normal(97, cout * cin * k, sigma=(cin * k) ** -0.5).reshape(cout, cin, k)
+            cells.append(Cell("mc", f"mc_dx_c{cin}x{cout}_k{k}", "conv_mc_bwd_in", w=k, f=wf, inp=key, kh=cin,
+                              kw=cout))
         # multi-channel 2-D convolution (reading R22), NHWC bf16, ResNet-like layers; the image
         # shard's (C, H, W) slots hold (H, W, Cin) of the NHWC tensor
         for hw, cin, cout in ((56, 64, 64), (56, 64, 128)):
@@ -416,6 +424,17 @@ class Runner:
             c.bytes = rows * N * cin * 2 + c.n_out * 4 + cout * cin * k * 2
             c.flops = 2 * k * cin * c.n_out
             return torch.empty((rows, L, cout), dtype=torch.float32, device=self.device)
+        if c.op == "conv_mc_bwd_in":
+            rows, n = geo
+            cin, cout, k = c.kh, c.kw, c.w
+            L = n // cout
+            N = L + k - 1
+            if c.name not in self.wmc:
+                self.wmc[c.name] = torch.from_numpy(c.f).to(self.device).to(torch.bfloat16).contiguous()
+            c.n_out = rows * N * cin
+            c.bytes = rows * L * cout * 2 + c.n_out * 4 + cout * cin * k * 2
+            c.flops = 2 * k * cout * c.n_out
+            return torch.empty((rows, N, cin), dtype=torch.float32, device=self.device)
         if c.op == "conv2d_mc":
             B, H, W, cin = geo
             cout = c.f.shape[0]
@@ -585,6 +604,11 @@ class Runner:
             rows, n = geo
             ss.check(ss.ss_conv1d_mc(x.data_ptr(), self.wmc[c.name].data_ptr(), y.data_ptr(), rows,
                                      n // c.kh, c.kh, c.kw, c.w, self.stream.cuda_stream))
+        elif c.op == "conv_mc_bwd_in":
+            rows, n = geo
+            L = n // c.kw
+            ss.check(ss.ss_conv1d_mc_backward_input(x.data_ptr(), self.wmc[c.name].data_ptr(), y.data_ptr(), rows,
+                                                    L + c.w - 1, c.kh, c.kw, c.w, self.stream.cuda_stream))
         elif c.op == "conv2d_mc":
             B, H, W, cin = geo
             ss.check(ss.ss_conv2d_mc(x.data_ptr(), self.wmc[c.name].data_ptr(), y.data_ptr(), B, H, W, cin,
@@ -831,8 +855,10 @@ def _dtype_label(cells):
     dts = []
     if any(c.cfg == "cfg2" for c in cells):
         dts.append("i32")
-    if any(c.cfg != "cfg2" for c in cells):
+    if any(c.cfg not in ("cfg2", "mc") for c in cells):
         dts.append("f32")
+    if any(c.cfg == "mc" for c in cells):
+        dts.append("bf16 x bf16 -> f32 accumulate (tensor cores, kind::f16)")
     lab = "/".join(dts)
     tc = [c for c in cells if conv_on_tensor_cores(c)]
     if tc:
@@ -981,7 +1007,7 @@ def run_ours(args):
         d = {"cell": c.name, "avg_ms": round(avg_ms, 5), "n_out": c.n_out, "bytes": c.bytes,
              "gelem_s": round(c.n_out / (avg_ms * 1e-3) / 1e9, 2), "gbs": round(gbs, 1),
              "frac_hbm": round(gbs / peak_hbm, 4), "frac_8tbs": round(gbs / 8000.0, 4), "share": 0.0}
-        if c.op in ("conv_mc", "conv2d_mc"):
+        if c.op in ("conv_mc", "conv2d_mc", "conv_mc_bwd_in"):
             d["tc_frac"] = round(c.flops / (avg_ms * 1e-3) / 1e12 / (2 * tf32_peak_tflops()), 4)  # bf16 peak
         elif conv_on_tensor_cores(c):
             d["tc_frac"] = round(c.n_out * TC_FLOP_PER_OUT / (avg_ms * 1e-3) / 1e12 / tf32_peak_tflops(), 4)
@@ -1006,7 +1032,7 @@ def run_ours(args):
         roofline = {"bound": "hbm", "kernel": dom["cell"], "achieved": dom["gbs"], "peak": peak_hbm,
                     "unit": "GB/s", "frac": dom["frac_hbm"], "peak_source": peak_src, "traffic": None,
                     "frac_8tbs": dom["frac_8tbs"]}
-        if "tc_frac" in dom and dom_cell.op in ("conv_mc", "conv2d_mc"):
+        if "tc_frac" in dom and dom_cell.op in ("conv_mc", "conv2d_mc", "conv_mc_bwd_in"):
             roofline["tensor_frac"] = dom["tc_frac"]
             roofline["tensor_peak_tflops"] = round(2 * tf32_peak_tflops(), 1)
             roofline["tensor_note"] = "bf16 MMA work (2 k Cin flop/output) / measured dense bf16 peak"
@@ -1186,6 +1212,13 @@ def oracle_sample_plan(workload: str, frac: float):
             wb = oracle.to_bf16_bits(c.f)
             plan.append((c, _rows_task(xb, lambda xi, wb=wb: oracle.conv2d_mc(xi, wb),
                                        (hw - 2) * (hw - 2) * c.f.shape[0])))
+        elif c.cfg == "mc" and c.op == "conv_mc_bwd_in":
+            cin, cout, k = c.kh, c.kw, c.w
+            N = max(k + 1, int(16 * 65536 * frac))
+            gb = oracle.to_bf16_bits(synth.normal(98, (N - k + 1) * cout).reshape(1, N - k + 1, cout))
+            wb = oracle.to_bf16_bits(c.f)
+            plan.append((c, _whole_task(lambda gb=gb, wb=wb, N=N, cin=cin: (
+                oracle.conv1d_mc_backward_input(gb, wb, N), N * cin)[1])))
         elif c.cfg == "mc":
             cin, cout, k = c.kh, c.kw, c.w
             n = max(k + 1, int(16 * 65536 * frac))

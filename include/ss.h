@@ -70,7 +70,7 @@
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 9
+#define SS_ABI_VERSION 10
 
 typedef enum { SS_F32 = 0, SS_I32 = 1 } ss_dtype_t;
 typedef enum { SS_POOL_MAX = 0, SS_POOL_AVG = 1 } ss_pool_mode_t;
@@ -277,6 +277,22 @@ ss_status_t ss_conv1d_mc(const void* x, const void* w, float* y, int64_t batch, 
  * SS_ERR_WINDOW_EXCEEDS_INPUT). */
 ss_status_t ss_conv2d_mc(const void* x, const void* w, float* y, int64_t batch, int64_t H, int64_t W,
                          int64_t cin, int64_t cout, int64_t kh, int64_t kw, void* stream);
+
+/* Input gradient of ss_conv1d_mc (the vector-Jacobian product of the channel-summed
+ * sliding dot product; reading R23):
+ *   dx[b][t][ci] = sum_{j<k} sum_{co<cout} w[co][ci][j] * dy[b][t-j][co],  t < N,
+ * terms with t-j outside [0, N-k+1) absent.  dy is [batch][N-k+1][cout] bfloat16
+ * (the forward output's gradient, rounded to bf16 like the forward's operands),
+ * w is the forward's [cout][cin][k] bfloat16, dx is [batch][N][cin] fp32 and fully
+ * overwritten; all DEVICE memory, dx must not overlap dy or w.  It is the forward
+ * contraction on dy with the weights transposed and flipped, w'[ci][co][j] =
+ * w[co][ci][k-1-j], over each row padded by k-1 zeros on both sides: cin, cout in
+ * {64, 128}, k <= 9 and 16-B aligned dy / dx run on the tensor cores (the
+ * padding is the TMA's zero fill of a 4-D box per row, no padded copy); other
+ * shapes run a direct kernel.  bf16 products are exact, accumulation is fp32.
+ * Statuses as ss_conv1d_mc (k > N -> SS_ERR_WINDOW_EXCEEDS_INPUT). */
+ss_status_t ss_conv1d_mc_backward_input(const void* dy, const void* w, float* dx, int64_t batch, int64_t N,
+                                        int64_t cin, int64_t cout, int64_t k, void* stream);
 
 /* ---- backward passes (training) ----------
  * Vector-Jacobian products of the forward calls above (DESIGN.md reading

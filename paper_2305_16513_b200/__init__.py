@@ -45,7 +45,7 @@ EXPORTED = ("ss_abi_version", "ss_out_len", "ss_pool_sum", "ss_pool_max", "ss_po
             "ss_affine_window", "ss_pool_sum_backward", "ss_pool_max_backward",
             "ss_conv1d_backward_input", "ss_conv1d_backward_filter_workspace", "ss_conv1d_backward_filter",
             "ss_pool2d_backward", "ss_conv2d", "ss_conv2d_backward_input", "ss_conv2d_backward_filter_workspace",
-            "ss_conv2d_backward_filter", "ss_conv1d_mc", "ss_conv2d_mc")
+            "ss_conv2d_backward_filter", "ss_conv1d_mc", "ss_conv2d_mc", "ss_conv1d_mc_backward_input")
 
 
 class SSError(RuntimeError):
@@ -99,6 +99,8 @@ def _load() -> ctypes.CDLL:
     L.ss_conv1d_mc.restype = i32
     L.ss_conv2d_mc.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i64, vp]
     L.ss_conv2d_mc.restype = i32
+    L.ss_conv1d_mc_backward_input.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, vp]
+    L.ss_conv1d_mc_backward_input.restype = i32
     L.ss_conv2d.restype = i32
     L.ss_conv2d_backward_input.argtypes = [vp, vp, i64, i64, i64, ctypes.POINTER(ctypes.c_float), i64, i64, i64, i64,
                                            i32, vp]
@@ -255,6 +257,10 @@ def ss_conv1d_mc(x_ptr, w_ptr, y_ptr, batch, N, cin, cout, k, stream=0) -> int:
 
 def ss_conv2d_mc(x_ptr, w_ptr, y_ptr, batch, H, W, cin, cout, kh, kw, stream=0) -> int:
     return _lib.ss_conv2d_mc(x_ptr, w_ptr, y_ptr, batch, H, W, cin, cout, kh, kw, stream)
+
+
+def ss_conv1d_mc_backward_input(dy_ptr, w_ptr, dx_ptr, batch, N, cin, cout, k, stream=0) -> int:
+    return _lib.ss_conv1d_mc_backward_input(dy_ptr, w_ptr, dx_ptr, batch, N, cin, cout, k, stream)
 
 
 def check(status: int) -> None:
@@ -630,3 +636,25 @@ def conv2d_mc(x, w, out=None, stream=None):
     y = _alloc(out, (B, H - kh + 1, W - kw + 1, cout), torch.float32, x.device)
     check(ss_conv2d_mc(x.data_ptr(), w.data_ptr(), y.data_ptr(), B, H, W, cin, cout, kh, kw, _stream(stream)))
     return y
+
+
+def conv1d_mc_backward_input(dy, w, N, out=None, stream=None):
+    """Input gradient of conv1d_mc: dy [B, N-k+1, Cout] bfloat16 (CUDA), w [Cout, Cin, k] bfloat16
+    (CUDA, the forward's weights) -> dx [B, N, Cin] float32."""
+    torch = _torch()
+    _dev(dy, "dy", torch.bfloat16)
+    _dev(w, "w", torch.bfloat16, device=dy.device)
+    if dy.dim() != 3 or w.dim() != 3:
+        raise ValueError("dy must be [B, N-k+1, Cout] and w [Cout, Cin, k]")
+    B, L, cout = dy.shape
+    cout2, cin, k = w.shape
+    if cout2 != cout:
+        raise ValueError("w's Cout does not match dy")
+    if k > N:
+        raise SSError(SS_ERR_WINDOW_EXCEEDS_INPUT, f"window exceeds input: k={k} > N={N}")
+    if L != N - k + 1:
+        raise ValueError(f"dy has {L} positions, expected N-k+1 = {N - k + 1}")
+    dx = _alloc(out, (B, N, cin), torch.float32, dy.device)
+    check(ss_conv1d_mc_backward_input(dy.data_ptr(), w.data_ptr(), dx.data_ptr(), B, N, cin, cout, k,
+                                      _stream(stream)))
+    return dx

@@ -173,6 +173,26 @@ bool encode_mc_map(CUtensorMap* m, const void* x, int64_t positions, int64_t cin
   return r == CUDA_SUCCESS;
 }
 
+// Batched variant: 4-D {64, positions, cin/64, batch} (strides: position cin*2 B, atom 128 B, row
+// positions*cin*2 B); a box starting before a row or running past it is zero-filled (row padding).
+bool encode_mc_map_batched(CUtensorMap* m, const void* x, int64_t batch, int64_t positions, int64_t cin,
+                           int box_rows) {
+  auto enc = encode_fn();
+  if (!enc || positions < 1 || positions > (int64_t(1) << 31) || batch < 1 || cin % 64 || box_rows > 256 ||
+      box_rows < 8 || (positions * cin * 2) % 16)
+    return false;
+  const int64_t at = cin / 64;
+  cuuint64_t dims[4] = {64, (cuuint64_t)positions, (cuuint64_t)at, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {(cuuint64_t)(cin * 2), 128, (cuuint64_t)(positions * cin * 2)};
+  cuuint32_t box[4] = {64, (cuuint32_t)box_rows, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+
 // Tensor-core conv selection: k in [tc_min_k, kConvTcMaxK] at stride 1 without
 // dilation (default 33: measured faster than the FFMA2 tile kernel for every
 // k >= 33 on config 3).  SS_CONV_TC_MIN_K (read once) overrides the threshold, 0 disables
@@ -723,6 +743,37 @@ ss_status_t ss_conv1d_mc(const void* x, const void* w, float* y, int64_t batch, 
   p.clc = dynamic_tiles();
   cudaError_t e = launch_conv_mc(p, tc, static_cast<cudaStream_t>(stream), current_sms());
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv1d_mc launch");
+}
+
+ss_status_t ss_conv1d_mc_backward_input(const void* dy, const void* w, float* dx, int64_t batch, int64_t N,
+                                        int64_t cin, int64_t cout, int64_t k, void* stream) {
+  if (!dy || !w || !dx) return fail(SS_ERR_NULL, "dy, w and dx must be non-NULL device pointers");
+  if (batch < 1 || N < 1 || cin < 1 || cout < 1 || k < 1)
+    return fail(SS_ERR_BAD_SIZE, "batch/N/cin/cout/k must all be >= 1");
+  if (N > INT64_MAX / 8 / batch / cin || N > INT64_MAX / 8 / batch / cout || k > INT64_MAX / 8 / cin / cout)
+    return fail(SS_ERR_BAD_SIZE, "sizes overflow int64");
+  if (k > N) return fail(SS_ERR_WINDOW_EXCEEDS_INPUT, "window exceeds input: k=%lld > N=%lld", (long long)k,
+                         (long long)N);
+  if ((reinterpret_cast<uintptr_t>(dy) & 1) || (reinterpret_cast<uintptr_t>(w) & 1) ||
+      (reinterpret_cast<uintptr_t>(dx) & 3))
+    return fail(SS_ERR_BAD_SIZE, "dy / w must be 2-byte and dx 4-byte aligned");
+  const int64_t L = N - k + 1;
+  if (overlaps(dy, batch * L * cout * 2, dx, batch * N * cin * 4) || overlaps(w, cout * cin * k * 2, dx, batch * N * cin * 4))
+    return fail(SS_ERR_OVERLAP, "dx overlaps an input");
+  // dx[b][t][ci] = sum_j sum_co w[co][ci][k-1-j] dy[b][t - (k-1) + j][co]: the forward implicit GEMM on dy
+  // (channels cout -> cin) with the weights transposed and flipped, over rows padded by k-1 zeros
+  ConvMcParams p;
+  memset(&p, 0, sizeof p);
+  p.x = dy; p.w = w; p.y = dx; p.batch = batch; p.N = L; p.L = N; p.cin = cout; p.cout = cin; p.k = k;
+  p.bwd_in = 1; p.batched = 1; p.pad = (int)(k - 1); p.n_out = N;
+  for (int64_t j = 0; j < k && j < kMcMaxTaps; ++j) p.tap_off[j] = (int)j;
+  p.rows = 136;
+  const bool tc = (cin == 64 || cin == 128) && (cout == 64 || cout == 128) && k <= 9 &&
+                  (reinterpret_cast<uintptr_t>(dy) & 15) == 0 && (reinterpret_cast<uintptr_t>(dx) & 15) == 0 &&
+                  mc_boxes(p) && encode_mc_map_batched(&p.tm_x, dy, batch, L, cout, p.box_rows);
+  p.clc = dynamic_tiles();
+  cudaError_t e = launch_conv_mc(p, tc, static_cast<cudaStream_t>(stream), current_sms());
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv1d_mc_backward_input launch");
 }
 
 ss_status_t ss_conv2d_mc(const void* x, const void* w, float* y, int64_t batch, int64_t H, int64_t W, int64_t cin,

@@ -99,6 +99,15 @@ __device__ __forceinline__ void tma_load_3d_mc(void* smem_dst, const CUtensorMap
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d_mc(void* smem_dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                               int32_t c2, int32_t c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
 }  // namespace
 
 template <int CIN, int COUT>
@@ -137,15 +146,17 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
     fence_mbar_init();
     prefetch_tmap(&p.tm_x);
   }
-  // weights: w[co][ci][j] (bf16) -> tap j, atom ci/64, row co, 16-B chunk (ci%64)/8 ^ (co%8)
+  // weights: w[co][ci][j] (bf16) -> tap j, atom ci/64, row co, 16-B chunk (ci%64)/8 ^ (co%8);
+  // input gradient: the staged w'[co][ci][j] is w[ci][co][k-1-j] (transposed and flipped)
   {
     const uint16_t* __restrict__ w = static_cast<const uint16_t*>(p.w);
     const int total = COUT * CIN * k;
     for (int e = threadIdx.x; e < total; e += kMcThreads) {
       const int j = e % k, ci = (e / k) % CIN, co = e / (k * CIN);
+      const int src = p.bwd_in ? (ci * COUT + co) * k + (k - 1 - j) : e;
       const uint32_t off = (uint32_t)j * kWTap + (uint32_t)(ci >> 6) * (COUT * 128u) + (uint32_t)co * 128u +
                            ((((uint32_t)(ci & 63) >> 3) ^ ((uint32_t)co & 7u)) << 4) + 2u * (uint32_t)(ci & 7);
-      *reinterpret_cast<uint16_t*>(ws + off) = __ldg(w + e);
+      *reinterpret_cast<uint16_t*>(ws + off) = __ldg(w + src);
     }
   }
   fence_proxy_async_smem();  // generic-proxy weight writes -> tensor core reads
@@ -177,10 +188,19 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
           break;
         }
         mbar_arrive_expect_tx(full + s, kStage);
-        for (int a = 0; a < AT; ++a)  // one SW128 block per K-atom, nbox boxes of box_rows positions
-          for (int bx = 0; bx < p.nbox; ++bx)
-            tma_load_3d_mc(xs + (size_t)s * kStage + (size_t)a * kAtomBytes + (size_t)bx * p.box_rows * 128, &p.tm_x,
-                           0, (int32_t)(t * 128 + bx * p.box_rows), a, full + s);
+        if (p.batched) {  // tile = 128 positions of one row, staged from `pad` positions earlier
+          const int64_t b = t / p.tiles_per_row;
+          const int32_t t0 = (int32_t)((t - b * p.tiles_per_row) * 128) - p.pad;
+          for (int a = 0; a < AT; ++a)
+            for (int bx = 0; bx < p.nbox; ++bx)
+              tma_load_4d_mc(xs + (size_t)s * kStage + (size_t)a * kAtomBytes + (size_t)bx * p.box_rows * 128,
+                             &p.tm_x, 0, t0 + bx * p.box_rows, a, (int32_t)b, full + s);
+        } else {
+          for (int a = 0; a < AT; ++a)  // one SW128 block per K-atom, nbox boxes of box_rows positions
+            for (int bx = 0; bx < p.nbox; ++bx)
+              tma_load_3d_mc(xs + (size_t)s * kStage + (size_t)a * kAtomBytes + (size_t)bx * p.box_rows * 128,
+                             &p.tm_x, 0, (int32_t)(t * 128 + bx * p.box_rows), a, full + s);
+        }
         if (++s == kMcStages) { s = 0; ph ^= 1; }
         if (p.clc) {
           t = clc_wait(&clc, cph);  // requested one tile ahead
@@ -250,18 +270,23 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
       __syncwarp();
       if (lane == 0) mbar_arrive(dempty + d);
       // flat input position of the tile's first row: one 64-bit division per tile
-      const int64_t b0 = (t * 128) / p.N, i0 = t * 128 - b0 * p.N;
+      // (batched: row b0, output positions i0 + m of it)
+      const int64_t b0 = p.batched ? t / p.tiles_per_row : (t * 128) / p.N;
+      const int64_t i0 = p.batched ? (t - b0 * p.tiles_per_row) * 128 : t * 128 - b0 * p.N;
 #pragma unroll
       for (int lh = 0; lh < 2; ++lh)
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {  // rows lane/4 and lane/4 + 8 of this 16-lane half
           const int m = 32 * q + 16 * lh + (lane >> 2) + 8 * rr;
           int64_t b = b0, i = i0 + m;       // flat input position = window start
-          while (i >= p.N) { i -= p.N; ++b; }
           int64_t o = -1;                   // output row of this position (-1: its window leaves the row / image)
-          if (!p.two_d) {
+          if (p.batched) {
+            if (i < p.n_out) o = b * p.n_out + i;
+          } else if (!p.two_d) {
+            while (i >= p.N) { i -= p.N; ++b; }
             if (b < p.batch && i < p.L) o = b * p.L + i;
           } else {
+            while (i >= p.N) { i -= p.N; ++b; }
             const uint32_t r = (uint32_t)i / (uint32_t)p.W, c = (uint32_t)i - r * (uint32_t)p.W;
             if (b < p.batch && r < p.OH && c < p.OW) o = (b * p.OH + r) * p.OW + c;
           }
@@ -321,6 +346,28 @@ __global__ void __launch_bounds__(256) conv_mc_direct_kernel(const __grid_consta
   }
 }
 
+// Input gradient, direct: dx[b][t][ci] = sum_j sum_co w[co][ci][k-1-j] dy[b][t-(k-1)+j][co] (dy rows of
+// p.N = N-k+1 positions, p.cin = C_out dy channels, p.cout = C_in dx channels, p.n_out = N).
+__global__ void __launch_bounds__(256) conv_mc_bwd_direct_kernel(const __grid_constant__ ConvMcParams p) {
+  const uint16_t* __restrict__ dy = static_cast<const uint16_t*>(p.x);
+  const uint16_t* __restrict__ w = static_cast<const uint16_t*>(p.w);
+  const int64_t total = p.batch * p.n_out * p.cout;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ci = o % p.cout, r = o / p.cout, t = r % p.n_out, b = r / p.n_out;
+    float acc = 0.0f;
+    for (int64_t j = 0; j < p.k; ++j) {
+      const int64_t s = t - (p.k - 1) + j;
+      if (s < 0 || s >= p.N) continue;
+      for (int64_t co = 0; co < p.cin; ++co) {
+        const float gv = __uint_as_float((uint32_t)__ldg(dy + (b * p.N + s) * p.cin + co) << 16);
+        const float wv = __uint_as_float((uint32_t)__ldg(w + (co * p.cout + ci) * p.k + (p.k - 1 - j)) << 16);
+        acc = __fmaf_rn(wv, gv, acc);
+      }
+    }
+    p.y[o] = acc;
+  }
+}
+
 size_t conv_mc_smem_bytes(int64_t cin, int64_t cout, int64_t k, int rows, int stages) {
   const size_t stage = (size_t)(cin / 64) * rows * 128;
   return 1024 + stages * stage + (size_t)k * (cin / 64) * cout * 128 + 8 * (2 * stages + 4) + 24 * kMcRing + 16;
@@ -345,7 +392,8 @@ static cudaError_t launch_mc(ConvMcParams& p, cudaStream_t stream, int sms) {
 
 cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t stream, int sms) {
   if (tensor_path) {
-    p.ntiles = (p.batch * p.N + 127) / 128;
+    if (p.batched) p.tiles_per_row = (p.n_out + 127) / 128;
+    p.ntiles = p.batched ? p.batch * p.tiles_per_row : (p.batch * p.N + 127) / 128;
     cudaError_t e = cudaErrorInvalidConfiguration;
     if (p.cin == 64 && p.cout == 64) e = launch_mc<64, 64>(p, stream, sms);
     else if (p.cin == 64 && p.cout == 128) e = launch_mc<64, 128>(p, stream, sms);
@@ -353,10 +401,12 @@ cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t strea
     else if (p.cin == 128 && p.cout == 128) e = launch_mc<128, 128>(p, stream, sms);
     if (e != cudaErrorInvalidConfiguration) return e;
   }
-  const int64_t total = p.two_d ? p.batch * p.OH * p.OW * p.cout : p.batch * p.L * p.cout;
+  const int64_t total = p.two_d ? p.batch * p.OH * p.OW * p.cout
+                                : p.bwd_in ? p.batch * p.n_out * p.cout : p.batch * p.L * p.cout;
   int64_t g = (total + 255) / 256;
   if (g > (int64_t)sms * 16) g = (int64_t)sms * 16;
-  if (p.two_d) conv2d_mc_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
+  if (p.bwd_in) conv_mc_bwd_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
+  else if (p.two_d) conv2d_mc_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
   else conv_mc_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
   note_launch();
   return cudaGetLastError();

@@ -246,11 +246,18 @@ struct alignas(64) ConvMcParams {
   int64_t H, W, OH, OW;               // 2-D geometry (two_d)
   int two_d;
   int rows, box_rows, nbox, stages;   // staged positions per tile (multiple of 8), TMA boxes per atom, ring depth
+  int batched;        // 1: tiles never cross batch rows; tm_x is 4-D {64, positions, atoms, batch} and a
+                      //    tile's box starts `pad` positions early (zero-filled outside the row)
+  int pad;            // left zero padding of each row (batched mode)
+  int bwd_in;         // 1: weights staged transposed and flipped (input gradient: w'[ci][co][j] = w[co][ci][k-1-j])
+  int64_t n_out, tiles_per_row;       // batched mode: outputs per row, tiles per row
   int tap_off[kMcMaxTaps];
   int64_t ntiles;    // set by launch_conv_mc
   int clc;  // 1: one CTA per work unit, units claimed by cluster launch control (ss_device.cuh); 0: static stride
 };
 bool encode_mc_map(CUtensorMap* m, const void* x, int64_t positions, int64_t cin, int box_rows);
+bool encode_mc_map_batched(CUtensorMap* m, const void* x, int64_t batch, int64_t positions, int64_t cin,
+                           int box_rows);
 cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t stream, int sms);
 
 }  // namespace ss
