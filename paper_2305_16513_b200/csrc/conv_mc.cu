@@ -147,16 +147,49 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
     prefetch_tmap(&p.tm_x);
   }
   // weights: w[co][ci][j] (bf16) -> tap j, atom ci/64, row co, 16-B chunk (ci%64)/8 ^ (co%8);
-  // input gradient: the staged w'[co][ci][j] is w[ci][co][k-1-j] (transposed and flipped)
+  // input gradient: the staged w'[co][ci][j] is w[ci][co][k-1-j] (transposed and flipped).
+  // 16-B loads in batches of 8 per thread (one L2 round trip per batch: the element-wise
+  // loop was a chain of ~k*CIN*COUT/1024 dependent round trips, 20% of a 2-D launch).
   {
     const uint16_t* __restrict__ w = static_cast<const uint16_t*>(p.w);
     const int total = COUT * CIN * k;
-    for (int e = threadIdx.x; e < total; e += kMcThreads) {
-      const int j = e % k, ci = (e / k) % CIN, co = e / (k * CIN);
-      const int src = p.bwd_in ? (ci * COUT + co) * k + (k - 1 - j) : e;
+    const int D2 = p.bwd_in ? COUT : CIN;  // middle dimension of the source array
+    const uint32_t ws_s = smem_u32(ws);
+    auto put = [&](int c1, int c2, int jj, uint16_t val) {
+      const int co = p.bwd_in ? c2 : c1, ci = p.bwd_in ? c1 : c2, j = p.bwd_in ? k - 1 - jj : jj;
       const uint32_t off = (uint32_t)j * kWTap + (uint32_t)(ci >> 6) * (COUT * 128u) + (uint32_t)co * 128u +
                            ((((uint32_t)(ci & 63) >> 3) ^ ((uint32_t)co & 7u)) << 4) + 2u * (uint32_t)(ci & 7);
-      *reinterpret_cast<uint16_t*>(ws + off) = __ldg(w + src);
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(ws_s + off), "h"(val) : "memory");
+    };
+    if ((reinterpret_cast<uintptr_t>(w) & 15) == 0) {
+      const uint4* __restrict__ w4 = reinterpret_cast<const uint4*>(w);
+      const int n8 = total / 8;  // CIN, COUT are multiples of 64
+      for (int base = 0; base < n8; base += 8 * kMcThreads) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = base + u * kMcThreads + (int)threadIdx.x;
+          if (i < n8) v[u] = __ldg(w4 + i);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = base + u * kMcThreads + (int)threadIdx.x;
+          if (i >= n8) break;
+          const int g = i * 8, r = g / k;
+          int jj = g - r * k, c2 = r % D2, c1 = r / D2;
+          const uint32_t word[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            put(c1, c2, jj, (uint16_t)(word[t >> 1] >> (16 * (t & 1))));
+            if (++jj == k) { jj = 0; if (++c2 == D2) { c2 = 0; ++c1; } }
+          }
+        }
+      }
+    } else {
+      for (int e = threadIdx.x; e < total; e += kMcThreads) {
+        const int r = e / k;
+        put(r / D2, r % D2, e - r * k, __ldg(w + e));
+      }
     }
   }
   fence_proxy_async_smem();  // generic-proxy weight writes -> tensor core reads
