@@ -710,10 +710,7 @@ ss_status_t ss_conv2d_backward_filter(const void* x, const void* dy, float* df, 
 
 // TMA boxes per staged atom: nbox boxes of box_rows (<= 256, a multiple of 8) cover p.rows.
 static bool mc_boxes(ConvMcParams& p) {
-  p.rows = (p.rows + 7) / 8 * 8;
-  p.nbox = (p.rows + 255) / 256;
-  p.box_rows = ((p.rows + p.nbox - 1) / p.nbox + 7) / 8 * 8;
-  p.rows = p.box_rows * p.nbox;
+  p.rows = mc_round_rows(p.rows, &p.nbox, &p.box_rows);
   return p.rows <= 2048;
 }
 
@@ -736,7 +733,8 @@ ss_status_t ss_conv1d_mc(const void* x, const void* w, float* y, int64_t batch, 
   memset(&p, 0, sizeof p);
   p.x = x; p.w = w; p.y = y; p.batch = batch; p.N = N; p.L = L; p.cin = cin; p.cout = cout; p.k = k;
   for (int64_t j = 0; j < k && j < kMcMaxTaps; ++j) p.tap_off[j] = (int)j;
-  p.rows = 136;  // 128 outputs + k - 1 <= 136 staged positions
+  p.mblk = conv_mc_choose_mblk(cin, cout, k, 136);
+  p.rows = 128 * p.mblk + 8;  // 128 mblk outputs + k - 1 <= 8 halo positions
   const bool tc = (cin == 64 || cin == 128) && (cout == 64 || cout == 128) && k <= 9 &&
                   (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
                   mc_boxes(p) && encode_mc_map(&p.tm_x, x, batch * N, cin, p.box_rows);
@@ -767,7 +765,8 @@ ss_status_t ss_conv1d_mc_backward_input(const void* dy, const void* w, float* dx
   p.x = dy; p.w = w; p.y = dx; p.batch = batch; p.N = L; p.L = N; p.cin = cout; p.cout = cin; p.k = k;
   p.bwd_in = 1; p.batched = 1; p.pad = (int)(k - 1); p.n_out = N;
   for (int64_t j = 0; j < k && j < kMcMaxTaps; ++j) p.tap_off[j] = (int)j;
-  p.rows = 136;
+  p.mblk = conv_mc_choose_mblk(cout, cin, k, 136);
+  p.rows = 128 * p.mblk + 8;
   const bool tc = (cin == 64 || cin == 128) && (cout == 64 || cout == 128) && k <= 9 &&
                   (reinterpret_cast<uintptr_t>(dy) & 15) == 0 && (reinterpret_cast<uintptr_t>(dx) & 15) == 0 &&
                   mc_boxes(p) && encode_mc_map_batched(&p.tm_x, dy, batch, L, cout, p.box_rows);
@@ -806,7 +805,8 @@ ss_status_t ss_conv2d_mc(const void* x, const void* w, float* y, int64_t batch, 
   if (tc) {
     for (int64_t a = 0; a < kh; ++a)
       for (int64_t e = 0; e < kw; ++e) p.tap_off[a * kw + e] = (int)(a * W + e);
-    p.rows = (int)(128 + (kh - 1) * W + kw - 1);
+    p.mblk = conv_mc_choose_mblk(cin, cout, kh * kw, (int)(128 + (kh - 1) * W + kw - 1));
+    p.rows = (int)(128 * p.mblk + (kh - 1) * W + kw - 1);
     tc = mc_boxes(p) && encode_mc_map(&p.tm_x, x, batch * H * W, cin, p.box_rows);
   }
   p.clc = dynamic_tiles();

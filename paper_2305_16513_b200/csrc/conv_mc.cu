@@ -22,6 +22,7 @@
 // split over two warps per lane quarter; positions whose window leaves their
 // batch row are masked).  Two TMEM accumulators.
 #include <cstdint>
+#include <cstdlib>
 
 #include <cuda_runtime.h>
 
@@ -90,6 +91,20 @@ __device__ __forceinline__ void mc_tmem_ld_16x256(uint32_t taddr, uint32_t* v) {
                : "r"(taddr)
                : "memory");
 }
+// .x4 / .x8: the same pattern repeated over 4 / 8 consecutive 8-column blocks (registers 4 r .. 4 r + 3
+// hold block r) -- one instruction per 16 lanes instead of one per 8 columns.
+__device__ __forceinline__ void mc_tmem_ld_16x256_x4(uint32_t taddr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                 "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+               : "r"(taddr)
+               : "memory");
+}
+template <int NB>
+__device__ __forceinline__ void mc_tmem_ld_row_blocks(uint32_t taddr, uint32_t (*v)[4]) {
+#pragma unroll
+  for (int c = 0; c < NB; c += 4) mc_tmem_ld_16x256_x4(taddr + 8u * c, &v[c][0]);
+}
 __device__ __forceinline__ void tma_load_3d_mc(void* smem_dst, const CUtensorMap* map, int32_t c0, int32_t c1,
                                                int32_t c2, uint64_t* bar) {
   asm volatile(
@@ -117,7 +132,8 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
   const uint32_t kStage = AT * kAtomBytes;
   constexpr uint32_t kWTap = AT * COUT * 128u;        // one tap of the weights
   constexpr int NH = COUT / 2;                        // epilogue columns per warp
-  constexpr uint32_t kTmemCols = 2 * COUT <= 128 ? 128 : 256;
+  constexpr int kAccMax = 4;                          // TMEM accumulators: p.nacc <= 4, nacc * mblk * COUT <= 512
+  const int kAcc = p.nacc, MB = p.mblk, TP = 128 * p.mblk;  // tile positions
   extern __shared__ __align__(16) uint8_t mc_raw[];  // aligned to 1024 by hand (slack in conv_mc_smem_bytes)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(mc_raw) + 1023) & ~uintptr_t(1023));
   const int k = (int)p.k;
@@ -127,20 +143,20 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
   uint64_t* bars = reinterpret_cast<uint64_t*>(ws + (size_t)k * kWTap);
   uint64_t* full = bars;                               // [stages]
   uint64_t* empty = full + kMcStages;                  // [stages]
-  uint64_t* dfull = empty + kMcStages;                 // [2]
-  uint64_t* dempty = dfull + 2;                        // [2]
+  uint64_t* dfull = empty + kMcStages;                 // [kAcc]
+  uint64_t* dempty = dfull + kAccMax;                  // [kAcc]
   // tile ids, producer -> MMA (read after its `full` wait) and epilogue (own barrier pair);
-  // the producer is at most kMcStages + 2 tiles ahead of the epilogue
-  uint64_t* tfull = dempty + 2;                        // [kMcRing]
+  // the producer is at most kMcStages + kAcc tiles ahead of the epilogue
+  uint64_t* tfull = dempty + kAccMax;                  // [kMcRing]
   uint64_t* tempty = tfull + kMcRing;                  // [kMcRing]
-  int64_t* tring = reinterpret_cast<int64_t*>(tempty + kMcRing);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tring + kMcRing);
+  int64_t* tring = reinterpret_cast<int64_t*>(tempty + kMcRing);  // [kMcRing][3]: tile, b0, i0
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tring + 3 * kMcRing);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ ClcSmem clc;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kMcStages; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(dfull + i, 1); mbar_init(dempty + i, kMcEpiWarps); }
+    for (int i = 0; i < kAcc; ++i) { mbar_init(dfull + i, 1); mbar_init(dempty + i, kMcEpiWarps); }
     for (int i = 0; i < kMcRing; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, kMcEpiWarps); }
     clc_init(&clc);
     fence_mbar_init();
@@ -148,54 +164,97 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
   }
   // weights: w[co][ci][j] (bf16) -> tap j, atom ci/64, row co, 16-B chunk (ci%64)/8 ^ (co%8);
   // input gradient: the staged w'[co][ci][j] is w[ci][co][k-1-j] (transposed and flipped).
-  // 16-B loads in batches of 8 per thread (one L2 round trip per batch: the element-wise
-  // loop was a chain of ~k*CIN*COUT/1024 dependent round trips, 20% of a 2-D launch).
+  // The source is read in chunks of R1 outer rows with coalesced 16-B loads into the (still
+  // unused) x ring, then each thread assembles whole 16-B destination units from 8 shared
+  // loads: per-element index math with 8 warps cost ~6 us per CTA.
   {
     const uint16_t* __restrict__ w = static_cast<const uint16_t*>(p.w);
-    const int total = COUT * CIN * k;
-    const int D2 = p.bwd_in ? COUT : CIN;  // middle dimension of the source array
-    const uint32_t ws_s = smem_u32(ws);
-    auto put = [&](int c1, int c2, int jj, uint16_t val) {
-      const int co = p.bwd_in ? c2 : c1, ci = p.bwd_in ? c1 : c2, j = p.bwd_in ? k - 1 - jj : jj;
-      const uint32_t off = (uint32_t)j * kWTap + (uint32_t)(ci >> 6) * (COUT * 128u) + (uint32_t)co * 128u +
-                           ((((uint32_t)(ci & 63) >> 3) ^ ((uint32_t)co & 7u)) << 4) + 2u * (uint32_t)(ci & 7);
-      asm volatile("st.shared.u16 [%0], %1;" ::"r"(ws_s + off), "h"(val) : "memory");
-    };
-    if ((reinterpret_cast<uintptr_t>(w) & 15) == 0) {
-      const uint4* __restrict__ w4 = reinterpret_cast<const uint4*>(w);
-      const int n8 = total / 8;  // CIN, COUT are multiples of 64
-      for (int base = 0; base < n8; base += 8 * kMcThreads) {
-        uint4 v[8];
+    const int D1 = p.bwd_in ? CIN : COUT, D2 = p.bwd_in ? COUT : CIN;  // outer / middle source dims
+    const int row_elems = D2 * k;                                       // one outer row
+    const int RS = row_elems * 2 + 4;  // padded scratch row (bytes): odd word stride, conflict-free gathers
+    int R1 = D1;
+    while (R1 > 8 && (size_t)R1 * RS > (size_t)kMcStages * kStage) R1 >>= 1;
+    const bool chunked = (reinterpret_cast<uintptr_t>(w) & 15) == 0 && (size_t)R1 * RS <= (size_t)kMcStages * kStage;
+    const uint32_t ws_s = smem_u32(ws), sc_s = smem_u32(xs);
+    if (chunked) {
+      const int q16 = row_elems / 8;  // 16-B pieces per source row
+      for (int c0 = 0; c0 < D1; c0 += R1) {
+        const uint4* __restrict__ src = reinterpret_cast<const uint4*>(w + (size_t)c0 * row_elems);
+        const int n16 = R1 * q16;
+        for (int base = 0; base < n16; base += 16 * kMcThreads) {
+          uint4 v[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int i = base + u * kMcThreads + (int)threadIdx.x;
-          if (i < n8) v[u] = __ldg(w4 + i);
-        }
+          for (int u = 0; u < 16; ++u) {
+            const int i = base + u * kMcThreads + (int)threadIdx.x;
+            if (i < n16) v[u] = __ldg(src + i);
+          }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int i = base + u * kMcThreads + (int)threadIdx.x;
-          if (i >= n8) break;
-          const int g = i * 8, r = g / k;
-          int jj = g - r * k, c2 = r % D2, c1 = r / D2;
-          const uint32_t word[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            put(c1, c2, jj, (uint16_t)(word[t >> 1] >> (16 * (t & 1))));
-            if (++jj == k) { jj = 0; if (++c2 == D2) { c2 = 0; ++c1; } }
+          for (int u = 0; u < 16; ++u) {
+            const int i = base + u * kMcThreads + (int)threadIdx.x;
+            if (i < n16) {
+              const int row = i / q16;
+              const uint32_t a0 = sc_s + (uint32_t)(row * RS) + 16u * (uint32_t)(i - row * q16);
+              asm volatile("st.shared.b32 [%0], %1;\n\tst.shared.b32 [%0+4], %2;\n\t"
+                           "st.shared.b32 [%0+8], %3;\n\tst.shared.b32 [%0+12], %4;" ::"r"(a0),
+                           "r"(v[u].x), "r"(v[u].y), "r"(v[u].z), "r"(v[u].w)
+                           : "memory");
+            }
           }
         }
+        __syncthreads();
+        // destination units of this chunk, tap by tap: (co, 8 consecutive ci); fwd: ci-group fastest,
+        // bwd: co fastest (both power-of-two extents: shifts only)
+        const int gi = p.bwd_in ? R1 / 8 : CIN / 8;  // ci groups
+        const int nco = p.bwd_in ? COUT : R1;        // co rows
+        const int lg_fast = 31 - __clz(p.bwd_in ? nco : gi);
+        const int lg_tap = 31 - __clz(nco * gi);
+        const int units = k << lg_tap;
+        {
+#pragma unroll 4
+          for (int e0 = threadIdx.x; e0 < units; e0 += kMcThreads) {
+            const int j = e0 >> lg_tap, e = e0 & ((1 << lg_tap) - 1);
+            const int fast = e & ((1 << lg_fast) - 1), slow = e >> lg_fast;
+            int co, ci0;
+            uint32_t s0, step;  // scratch address of element t = 0, stride between t
+            if (p.bwd_in) {     // source (ci = c0 + 8 g + t, co, k-1-j)
+              co = fast; ci0 = c0 + 8 * slow;
+              s0 = sc_s + (uint32_t)(8 * slow * RS) + 2u * (uint32_t)(co * k + (k - 1 - j));
+              step = (uint32_t)RS;
+            } else {            // source (co = c0 + col, ci = 8 g + t, j)
+              co = c0 + slow; ci0 = 8 * fast;
+              s0 = sc_s + (uint32_t)(slow * RS) + 2u * (uint32_t)(ci0 * k + j);
+              step = 2u * (uint32_t)k;
+            }
+            uint32_t h[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              uint16_t q;
+              asm volatile("ld.shared.u16 %0, [%1];" : "=h"(q) : "r"(s0 + step * t) : "memory");
+              h[t] = q;
+            }
+            const uint32_t off = (uint32_t)j * kWTap + (uint32_t)(ci0 >> 6) * (COUT * 128u) + (uint32_t)co * 128u +
+                                 ((((uint32_t)(ci0 & 63) >> 3) ^ ((uint32_t)co & 7u)) << 4);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ws_s + off), "r"(h[0] | (h[1] << 16)),
+                         "r"(h[2] | (h[3] << 16)), "r"(h[4] | (h[5] << 16)), "r"(h[6] | (h[7] << 16))
+                         : "memory");
+          }
+        }
+        __syncthreads();  // scratch reused by the next chunk / the x ring
       }
-    } else {
+    } else {  // unaligned weights: element by element
+      const int total = COUT * CIN * k;
       for (int e = threadIdx.x; e < total; e += kMcThreads) {
-        const int r = e / k;
-        put(r / D2, r % D2, e - r * k, __ldg(w + e));
+        const int r = e / k, c1 = r / D2, c2 = r % D2, jj = e - r * k;
+        const int co = p.bwd_in ? c2 : c1, ci = p.bwd_in ? c1 : c2, j = p.bwd_in ? k - 1 - jj : jj;
+        const uint32_t off = (uint32_t)j * kWTap + (uint32_t)(ci >> 6) * (COUT * 128u) + (uint32_t)co * 128u +
+                             ((((uint32_t)(ci & 63) >> 3) ^ ((uint32_t)co & 7u)) << 4) + 2u * (uint32_t)(ci & 7);
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(ws_s + off), "h"(__ldg(w + e)) : "memory");
       }
     }
   }
   fence_proxy_async_smem();  // generic-proxy weight writes -> tensor core reads
   if (warp == kMcWarpMma) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
-                 "n"(kTmemCols));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -213,7 +272,12 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
       for (int it = 0;; ++it) {
         const int ts = it % kMcRing;
         mbar_wait(tempty + ts, ((uint32_t)(it / kMcRing) & 1u) ^ 1u);
-        tring[ts] = t < ntiles ? t : -1;
+        tring[3 * ts] = t < ntiles ? t : -1;
+        if (t < ntiles) {  // the tile's first position (row b0, position i0 in it): divisions here, off the epilogue
+          const int64_t b0 = p.batched ? t / p.tiles_per_row : (t * TP) / p.N;
+          tring[3 * ts + 1] = b0;
+          tring[3 * ts + 2] = p.batched ? (t - b0 * p.tiles_per_row) * TP : t * TP - b0 * p.N;
+        }
         mbar_arrive(tfull + ts);
         mbar_wait(empty + s, ph ^ 1);
         if (t >= ntiles) {  // end marker for the MMA warp: the next `full` phase without data
@@ -223,7 +287,7 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
         mbar_arrive_expect_tx(full + s, kStage);
         if (p.batched) {  // tile = 128 positions of one row, staged from `pad` positions earlier
           const int64_t b = t / p.tiles_per_row;
-          const int32_t t0 = (int32_t)((t - b * p.tiles_per_row) * 128) - p.pad;
+          const int32_t t0 = (int32_t)((t - b * p.tiles_per_row) * TP) - p.pad;
           for (int a = 0; a < AT; ++a)
             for (int bx = 0; bx < p.nbox; ++bx)
               tma_load_4d_mc(xs + (size_t)s * kStage + (size_t)a * kAtomBytes + (size_t)bx * p.box_rows * 128,
@@ -232,7 +296,7 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
           for (int a = 0; a < AT; ++a)  // one SW128 block per K-atom, nbox boxes of box_rows positions
             for (int bx = 0; bx < p.nbox; ++bx)
               tma_load_3d_mc(xs + (size_t)s * kStage + (size_t)a * kAtomBytes + (size_t)bx * p.box_rows * 128,
-                             &p.tm_x, 0, (int32_t)(t * 128 + bx * p.box_rows), a, full + s);
+                             &p.tm_x, 0, (int32_t)(t * TP + bx * p.box_rows), a, full + s);
         }
         if (++s == kMcStages) { s = 0; ph ^= 1; }
         if (p.clc) {
@@ -253,28 +317,30 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
     uint32_t ph = 0, dph = 0;
     for (int it = 0;; ++it) {
       mc_wait(full + s, ph);
-      if (*reinterpret_cast<volatile int64_t*>(tring + it % kMcRing) < 0) break;
+      if (*reinterpret_cast<volatile int64_t*>(tring + 3 * (it % kMcRing)) < 0) break;
       mc_wait(dempty + d, dph ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t dcol = dc0 + (uint32_t)(d * COUT);
-      const uint64_t dxs = dx0 + (uint64_t)((s * kStage) >> 4);
-      uint32_t acc = 0;
+      for (int mb = 0; mb < MB; ++mb) {  // M-block mb: positions 128 mb .. 128 mb + 127 of the tile
+        const uint32_t dcol = dc0 + (uint32_t)((d * MB + mb) * COUT);
+        const uint64_t dxs = dx0 + (uint64_t)((s * kStage + (uint32_t)mb * 128u * 128u) >> 4);
+        uint32_t acc = 0;
 #pragma unroll 1
-      for (int j = 0; j < k; ++j) {
+        for (int j = 0; j < k; ++j) {
 #pragma unroll
-        for (int a = 0; a < AT; ++a)
+          for (int a = 0; a < AT; ++a)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {  // K-steps of 16 channels (32 B) inside the atom
-            const uint64_t da = dxs + (uint64_t)((a * kAtomBytes + (uint32_t)p.tap_off[j] * 128u + 32u * q) >> 4);
-            const uint64_t db = dw0 + (uint64_t)(((uint32_t)j * kWTap + a * (COUT * 128u) + 32u * q) >> 4);
-            mma_bf16_ss(dcol, da, db, idesc, acc);
-            acc = 1;
-          }
+            for (int q = 0; q < 4; ++q) {  // K-steps of 16 channels (32 B) inside the atom
+              const uint64_t da = dxs + (uint64_t)((a * kAtomBytes + (uint32_t)p.tap_off[j] * 128u + 32u * q) >> 4);
+              const uint64_t db = dw0 + (uint64_t)(((uint32_t)j * kWTap + a * (COUT * 128u) + 32u * q) >> 4);
+              mma_bf16_ss(dcol, da, db, idesc, acc);
+              acc = 1;
+            }
+        }
       }
       mc_commit(empty + s);
       mc_commit(dfull + d);
       if (++s == kMcStages) { s = 0; ph ^= 1; }
-      if (++d == 2) { d = 0; dph ^= 1; }
+      if (++d == kAcc) { d = 0; dph ^= 1; }
     }
   } else {
     // epilogue: quarter q's lanes (positions p0 + 32 q + [0, 32)) are read as two
@@ -285,59 +351,72 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
     for (int it = 0;; ++it) {
       const int ts = it % kMcRing;
       mc_wait(tfull + ts, (uint32_t)(it / kMcRing) & 1u);
-      const int64_t t = *reinterpret_cast<volatile int64_t*>(tring + ts);
+      const int64_t t = *reinterpret_cast<volatile int64_t*>(tring + 3 * ts);
+      const int64_t b0 = *reinterpret_cast<volatile int64_t*>(tring + 3 * ts + 1);
+      const int64_t i0 = *reinterpret_cast<volatile int64_t*>(tring + 3 * ts + 2);
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + ts);
       if (t < 0) break;
       mc_wait(dfull + d, dph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      uint32_t v[2][NH / 8][4];
+      for (int mb = 0; mb < MB; ++mb) {  // M-block by M-block (registers); the accumulator is freed after the last
+        uint32_t v[2][NH / 8][4];          // [16-lane half][8-column block][4]
 #pragma unroll
-      for (int lh = 0; lh < 2; ++lh)
-#pragma unroll
-        for (int cb = 0; cb < NH / 8; ++cb)
-          mc_tmem_ld_16x256(tmem + ((uint32_t)(32 * q + 16 * lh) << 16) + (uint32_t)(d * COUT + h * NH + 8 * cb),
-                            v[lh][cb]);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dempty + d);
-      // flat input position of the tile's first row: one 64-bit division per tile
-      // (batched: row b0, output positions i0 + m of it)
-      const int64_t b0 = p.batched ? t / p.tiles_per_row : (t * 128) / p.N;
-      const int64_t i0 = p.batched ? (t - b0 * p.tiles_per_row) * 128 : t * 128 - b0 * p.N;
-#pragma unroll
-      for (int lh = 0; lh < 2; ++lh)
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {  // rows lane/4 and lane/4 + 8 of this 16-lane half
-          const int m = 32 * q + 16 * lh + (lane >> 2) + 8 * rr;
-          int64_t b = b0, i = i0 + m;       // flat input position = window start
-          int64_t o = -1;                   // output row of this position (-1: its window leaves the row / image)
-          if (p.batched) {
-            if (i < p.n_out) o = b * p.n_out + i;
-          } else if (!p.two_d) {
-            while (i >= p.N) { i -= p.N; ++b; }
-            if (b < p.batch && i < p.L) o = b * p.L + i;
-          } else {
-            while (i >= p.N) { i -= p.N; ++b; }
-            const uint32_t r = (uint32_t)i / (uint32_t)p.W, c = (uint32_t)i - r * (uint32_t)p.W;
-            if (b < p.batch && r < p.OH && c < p.OW) o = (b * p.OH + r) * p.OW + c;
-          }
-          if (o >= 0) {
-            float* __restrict__ yr = p.y + o * COUT + h * NH + 2 * (lane & 3);
-#pragma unroll
-            for (int cb = 0; cb < NH / 8; ++cb)
-              *reinterpret_cast<float2*>(yr + 8 * cb) =
-                  make_float2(__uint_as_float(v[lh][cb][2 * rr]), __uint_as_float(v[lh][cb][2 * rr + 1]));
-          }
+        for (int lh = 0; lh < 2; ++lh)
+          mc_tmem_ld_row_blocks<NH / 8>(
+              tmem + ((uint32_t)(32 * q + 16 * lh) << 16) + (uint32_t)((d * MB + mb) * COUT + h * NH), v[lh]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (mb == MB - 1) {
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dempty + d);
         }
-      if (++d == 2) { d = 0; dph ^= 1; }
+        // rows of this thread: output index of flat position i0 + m of row / image b0 (-1: not an output);
+        // all four first, then the stores (independent chains, no per-row division)
+        int64_t orow[2][2];
+#pragma unroll
+        for (int lh = 0; lh < 2; ++lh)
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr) {
+            const int m = 128 * mb + 32 * q + 16 * lh + (lane >> 2) + 8 * rr;
+            int64_t b = b0, i = i0 + m;
+            int64_t o = -1;
+            if (p.batched) {
+              if (i < p.n_out) o = b * p.n_out + i;
+            } else {
+              while (i >= p.N) { i -= p.N; ++b; }
+              if (!p.two_d) {
+                if (b < p.batch && i < p.L) o = b * p.L + i;
+              } else {
+                const uint32_t iu = (uint32_t)i;
+                const uint32_t r = (uint32_t)(((uint64_t)__umulhi(iu, p.w_magic) + iu) >> p.w_shift);
+                const uint32_t c = iu - r * (uint32_t)p.W;
+                if (b < p.batch && r < (uint32_t)p.OH && c < (uint32_t)p.OW) o = (b * p.OH + r) * p.OW + c;
+              }
+            }
+            orow[lh][rr] = o;
+          }
+#pragma unroll
+        for (int lh = 0; lh < 2; ++lh)
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr) {  // rows lane/4 and lane/4 + 8 of this 16-lane half
+            const int64_t o = orow[lh][rr];
+            if (o >= 0) {
+              float* __restrict__ yr = p.y + o * COUT + h * NH + 2 * (lane & 3);
+#pragma unroll
+              for (int cb = 0; cb < NH / 8; ++cb)
+                *reinterpret_cast<float2*>(yr + 8 * cb) =
+                    make_float2(__uint_as_float(v[lh][cb][2 * rr]), __uint_as_float(v[lh][cb][2 * rr + 1]));
+            }
+          }
+      }
+      if (++d == kAcc) { d = 0; dph ^= 1; }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == kMcWarpMma)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 // Direct kernel (any shape / alignment): one (position, channel) per thread,
@@ -403,11 +482,21 @@ __global__ void __launch_bounds__(256) conv_mc_bwd_direct_kernel(const __grid_co
 
 size_t conv_mc_smem_bytes(int64_t cin, int64_t cout, int64_t k, int rows, int stages) {
   const size_t stage = (size_t)(cin / 64) * rows * 128;
-  return 1024 + stages * stage + (size_t)k * (cin / 64) * cout * 128 + 8 * (2 * stages + 4) + 24 * kMcRing + 16;
+  return 1024 + stages * stage + (size_t)k * (cin / 64) * cout * 128 + 8 * (2 * stages + 8) + 40 * kMcRing + 16;
+}
+
+int conv_mc_choose_mblk(int64_t cin, int64_t cout, int64_t k, int rows1) {
+  static const int forced = [] {
+    const char* e = getenv("SS_MC_MBLK");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 1 || forced == 2) return forced;
+  return conv_mc_smem_bytes(cin, cout, k, mc_round_rows(rows1 + 128), kMcStages) <= (size_t)kSmemBudget ? 2 : 1;
 }
 
 template <int CIN, int COUT>
 static cudaError_t launch_mc(ConvMcParams& p, cudaStream_t stream, int sms) {
+  p.nacc = 512 / (p.mblk * COUT) < 4 ? 512 / (p.mblk * COUT) : 4;
   p.stages = kMcStages;  // ring depth: 3, or 2 when the staged rows and the weights need the room
   while (p.stages > 2 && conv_mc_smem_bytes(CIN, COUT, p.k, p.rows, p.stages) > (size_t)kSmemBudget) --p.stages;
   const size_t smem = conv_mc_smem_bytes(CIN, COUT, p.k, p.rows, p.stages);
@@ -424,9 +513,22 @@ static cudaError_t launch_mc(ConvMcParams& p, cudaStream_t stream, int sms) {
 }
 
 cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t stream, int sms) {
+  if (p.two_d) {  // exact unsigned division by W for 31-bit numerators (round-up multiplier)
+    int sft = 0;
+    while ((1ll << sft) < p.W) ++sft;
+    p.w_shift = sft;
+    p.w_magic = (uint32_t)(((1ull << 32) * ((1ull << sft) - (uint64_t)p.W)) / (uint64_t)p.W + 1);
+  }
+  static unsigned long long* tbuf = nullptr;
+  if (getenv("SS_MC_TRACE")) {
+    if (!tbuf) cudaMalloc(&tbuf, 2048 * 8);
+    cudaMemsetAsync(tbuf, 0, 2048 * 8, stream);
+  }
   if (tensor_path) {
-    if (p.batched) p.tiles_per_row = (p.n_out + 127) / 128;
-    p.ntiles = p.batched ? p.batch * p.tiles_per_row : (p.batch * p.N + 127) / 128;
+    if (p.mblk < 1) p.mblk = 1;
+    const int64_t tp = 128 * p.mblk;
+    if (p.batched) p.tiles_per_row = (p.n_out + tp - 1) / tp;
+    p.ntiles = p.batched ? p.batch * p.tiles_per_row : (p.batch * p.N + tp - 1) / tp;
     cudaError_t e = cudaErrorInvalidConfiguration;
     if (p.cin == 64 && p.cout == 64) e = launch_mc<64, 64>(p, stream, sms);
     else if (p.cin == 64 && p.cout == 128) e = launch_mc<64, 128>(p, stream, sms);

@@ -251,6 +251,8 @@ struct alignas(64) ConvMcParams {
   int pad;            // left zero padding of each row (batched mode)
   int bwd_in;         // 1: weights staged transposed and flipped (input gradient: w'[ci][co][j] = w[co][ci][k-1-j])
   int64_t n_out, tiles_per_row;       // batched mode: outputs per row, tiles per row
+  int mblk, nacc;  // 128-position M-blocks per tile (1, 2), TMEM accumulators (tiles in flight)
+  uint32_t w_magic; int w_shift;     // 2-D: r = (umulhi(i, w_magic) + i) >> w_shift == i / W for i < 2^31
   int tap_off[kMcMaxTaps];
   int64_t ntiles;    // set by launch_conv_mc
   int clc;  // 1: one CTA per work unit, units claimed by cluster launch control (ss_device.cuh); 0: static stride
@@ -259,5 +261,16 @@ bool encode_mc_map(CUtensorMap* m, const void* x, int64_t positions, int64_t cin
 bool encode_mc_map_batched(CUtensorMap* m, const void* x, int64_t batch, int64_t positions, int64_t cin,
                            int box_rows);
 cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t stream, int sms);
+// Staged rows as the TMA boxes round them: multiple of 8, split into <= 256-row boxes of equal size
+inline int mc_round_rows(int rows, int* nbox = nullptr, int* box_rows = nullptr) {
+  rows = (rows + 7) / 8 * 8;
+  const int nb = (rows + 255) / 256, br = ((rows + nb - 1) / nb + 7) / 8 * 8;
+  if (nbox) *nbox = nb;
+  if (box_rows) *box_rows = br;
+  return br * nb;
+}
+// M-blocks per multi-channel tile: 2 (256 positions per tile, half the per-tile barrier round trips
+// and a smaller halo share) when a 3-stage ring of rows1 + 128 staged positions fits next to the weights
+int conv_mc_choose_mblk(int64_t cin, int64_t cout, int64_t k, int rows1);
 
 }  // namespace ss
