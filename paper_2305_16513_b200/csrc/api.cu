@@ -173,6 +173,20 @@ bool encode_mc_map(CUtensorMap* m, const void* x, int64_t positions, int64_t cin
   return r == CUDA_SUCCESS;
 }
 
+// 1-D fp32 view of n elements (16-B aligned base), boxes of 256, OOB zero fill.
+bool encode_flat_f32_map(CUtensorMap* m, const void* base, int64_t n) {
+  auto enc = encode_fn();
+  if (!enc || n < 1 || n >= (int64_t(1) << 31) || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+  cuuint64_t dims[1] = {(cuuint64_t)n};
+  cuuint64_t strides[1] = {4};
+  cuuint32_t box[1] = {256};
+  cuuint32_t estr[1] = {1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 1, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // Batched variant: 4-D {64, positions, cin/64, batch} (strides: position cin*2 B, atom 128 B, row
 // positions*cin*2 B); a box starting before a row or running past it is zero-filled (row padding).
 bool encode_mc_map_batched(CUtensorMap* m, const void* x, int64_t batch, int64_t positions, int64_t cin,
@@ -565,6 +579,15 @@ static ss_status_t pool_max_backward_impl(const void* x, const void* dy, void* d
   BackwardParams p;
   memset(&p, 0, sizeof p);
   p.x = x; p.dy = dy; p.dx = dx; p.N = N; p.L = L; p.batch = batch; p.w = w; p.stride = stride;
+  if (stride == 1 && pool_max_backward_s1_supported(w) && batch * N + 8192 < (int64_t(1) << 31)) {
+    MaxBwdS1Params q;
+    memset(&q, 0, sizeof q);
+    q.dx = static_cast<float*>(dx); q.N = N; q.L = L; q.batch = batch; q.w = w;
+    if (encode_flat_f32_map(&q.tm_x, x, batch * N) && encode_flat_f32_map(&q.tm_dy, dy, batch * L)) {
+      cudaError_t e = launch_pool_max_backward_s1(q, static_cast<cudaStream_t>(stream), current_sms());
+      return e == cudaSuccess ? SS_OK : cuda_fail(e, "pool_max_backward launch");
+    }
+  }
   cudaError_t e = launch_pool_max_backward(p, static_cast<cudaStream_t>(stream), current_sms());
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "pool_max_backward launch");
 }

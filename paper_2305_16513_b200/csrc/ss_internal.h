@@ -160,6 +160,18 @@ struct Pool2DBackwardParams {
 };
 cudaError_t launch_transpose_window(const BackwardParams& p, int op, int dtype, cudaStream_t stream, int sms);
 cudaError_t launch_pool_max_backward(const BackwardParams& p, cudaStream_t stream, int sms);
+// Stride-1 max-pool gradient, TMA-staged tile kernel (maxbwd.cu) for the window lengths it is
+// instantiated for (pool_max_backward_s1_supported); maps are 1-D over the flat x / dy arrays.
+struct alignas(64) MaxBwdS1Params {
+  CUtensorMap tm_x, tm_dy;  // fp32 [batch N] and [batch L], boxes of 256, OOB zero fill
+  float* dx;
+  int64_t N, L, batch, w;
+  int64_t tiles_per_row, ntiles;  // set by the launcher
+  int T;                          // stored positions per tile (2048 - w - 2)
+};
+bool pool_max_backward_s1_supported(int64_t w);
+cudaError_t launch_pool_max_backward_s1(MaxBwdS1Params& p, cudaStream_t stream, int sms);
+bool encode_flat_f32_map(CUtensorMap* m, const void* base, int64_t n);
 int conv_filter_grad_ctas(int sms);
 size_t conv_filter_grad_workspace(int64_t k, int ctas);
 cudaError_t launch_conv_filter_grad(const BackwardParams& p, float* df, void* workspace, int ctas,

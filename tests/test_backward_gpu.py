@@ -98,6 +98,32 @@ def test_pool_max_backward(ss, B, N, w, s, ties):
         np.testing.assert_array_equal(dx.cpu().numpy().reshape(B, N).astype(np.float64), ref)
 
 
+# stride-1 TMA tile kernel (csrc/maxbwd.cu, w in {2,3,4,5,7,8,9,16,17,32,33,64}, 16-B aligned x / dy):
+# T = 4094 - w stored positions per tile; rows of odd length (flat row starts at every
+# alignment), N around T and 2T, N < w + 3, integer ties
+S1_CASES = [  # (B, N, w)
+    (3, 4092, 2), (2, 4091, 3), (5, 4090, 4), (1, 8179, 5), (3, 4087, 7), (2, 8173, 8), (4, 4085, 9),
+    (3, 8157, 16), (2, 4077, 17), (2, 4061, 32), (2, 9000, 33), (3, 4030, 64), (2, 8061, 64), (7, 19, 16),
+    (5, 10, 9), (1, 2, 2), (3, 1 << 16, 16), (2, 5000, 5),
+]
+
+
+@pytest.mark.parametrize("B,N,w", S1_CASES)
+@pytest.mark.parametrize("ties", [False, True])
+def test_pool_max_backward_s1_tile(ss, B, N, w, ties):
+    L = N - w + 1
+    x = (synth.randint(27, B * N, -3, 3).astype(np.float32) if ties else synth.normal(27, B * N)).reshape(B, N)
+    dy = synth.normal(28, B * L).reshape(B, L)
+    buf, dx = out_buf(B * N, off=4)
+    xd, dyd = dev(x), dev(dy)
+    ss.check(ss.ss_pool_max_backward(xd.data_ptr(), dyd.data_ptr(), dx.data_ptr(), N, B, w, 1))
+    torch.cuda.synchronize()
+    assert canary_ok(buf, 4, B * N)
+    ref = oracle.pool_max_backward(x, dy, w, 1)
+    mag = oracle.pool_max_backward(x, np.abs(dy), w, 1)
+    within(dx.cpu().numpy().reshape(B, N), ref, mag, f"max bwd s1 tile B={B} N={N} w={w} ties={ties}")
+
+
 @pytest.mark.parametrize("w", [3, 8, 9, 40, 64, 100, 128])
 @pytest.mark.parametrize("pattern", ["spikes", "rising", "falling", "flat"])
 def test_pool_max_backward_runs(ss, w, pattern):
