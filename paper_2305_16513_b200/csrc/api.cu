@@ -73,6 +73,15 @@ static int current_sms() {
 
 static int env_int(const char* name, int dflt);
 
+// SS_FGRAD_TC=0: the FFMA filter-gradient kernels instead of the tensor-core one (A/B measurement)
+bool tc_filter_grad_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SS_FGRAD_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int dynamic_tiles() {
   static int on = env_int("SS_DYNAMIC_TILES", 1);
   return on != 0;
@@ -609,6 +618,15 @@ static ss_status_t conv1d_backward_filter_impl(const void* x, const void* dy, fl
   BackwardParams p;
   memset(&p, 0, sizeof p);
   p.x = x; p.dy = dy; p.N = N; p.L = L; p.batch = batch; p.w = k; p.stride = stride;
+  if (conv_filter_grad_tc_supported(N, k, stride, x)) {
+    FgradTcParams q;
+    memset(&q, 0, sizeof q);
+    q.x = static_cast<const float*>(x); q.dy = static_cast<const float*>(dy); q.part = static_cast<double*>(workspace);
+    q.N = N; q.L = L; q.batch = batch; q.k = k;
+    { const char* e = getenv("SS_FT_DBG"); q.dbg = e ? atoi(e) : 0; }
+    cudaError_t e = launch_conv_filter_grad_tc(q, df, ctas, current_sms(), static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv1d_backward_filter launch");
+  }
   cudaError_t e = launch_conv_filter_grad(p, df, workspace, ctas, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv1d_backward_filter launch");
 }

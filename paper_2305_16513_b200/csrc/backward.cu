@@ -679,6 +679,12 @@ __global__ void conv_filter_grad_finish(const double* __restrict__ partials, int
   if (lane == 0) df[j] = (float)s;
 }
 
+cudaError_t launch_conv_filter_grad_finish(const double* part, int ctas, int64_t k, float* df, cudaStream_t stream) {
+  conv_filter_grad_finish<<<(unsigned)((k + 3) / 4), 128, 0, stream>>>(part, ctas, k, 0, df);
+  note_launch();
+  return cudaGetLastError();
+}
+
 int conv_filter_grad_ctas(int sms) { return 2 * sms; }
 
 size_t conv_filter_grad_workspace(int64_t k, int ctas) {

@@ -177,6 +177,21 @@ size_t conv_filter_grad_workspace(int64_t k, int ctas);
 cudaError_t launch_conv_filter_grad(const BackwardParams& p, float* df, void* workspace, int ctas,
                                     cudaStream_t stream);
 cudaError_t launch_pool2d_backward(const Pool2DBackwardParams& p, cudaStream_t stream, int sms);
+cudaError_t launch_conv_filter_grad_finish(const double* part, int ctas, int64_t k, float* df, cudaStream_t stream);
+// Tensor-core filter gradient (fgrad_tc.cu): stride 1, k <= 64, N % 4 == 0, 16-B aligned x.
+struct FgradTcParams {
+  const float* x;
+  const float* dy;
+  double* part;                  // caller's workspace: per-CTA fp64 partials, [ctas][64]
+  int64_t N, L, batch, k;
+  int64_t U, units_per_row, nunits;  // set by the launcher
+  int64_t ctas;
+  int dbg;
+  unsigned long long* trace;
+};
+bool tc_filter_grad_enabled();
+bool conv_filter_grad_tc_supported(int64_t N, int64_t k, int64_t stride, const void* x);
+cudaError_t launch_conv_filter_grad_tc(FgradTcParams& p, float* df, int ctas, int sms, cudaStream_t stream);
 
 // Dilated stride-1 windows (dilated.cu): interior outputs
 // i < L_int = N - (w-1) d of each row go to y[b * y_pitch + y_off + i].

@@ -190,6 +190,36 @@ def test_conv_backward_filter(ss, B, N, k, s):
     within(df, ref, mag, f"conv bwd filter B={B} N={N} k={k} s={s}")
 
 
+# tensor-core filter gradient (csrc/fgrad_tc.cu): stride 1, k <= 64, N % 4 == 0, 16-B aligned x --
+# chunks of 128 dy positions, units of 64 chunks, row tails (L % 128), rows shorter than a chunk, one
+# unit per row and many, more units than CTAs
+FT_CASES = [  # (B, N, k)
+    (1, 4, 1), (2, 8, 3), (3, 100, 7), (2, 128, 64), (1, 132, 5), (4, 1000, 31), (2, 8192, 63), (3, 8196, 33),
+    (1, 70000, 64), (5, 20004, 2), (64, 16384, 63), (2, 1 << 18, 17),
+]
+
+
+@pytest.mark.parametrize("B,N,k", FT_CASES)
+def test_conv_backward_filter_tc(ss, B, N, k):
+    L = N - k + 1
+    x = synth.normal(33, B * N).reshape(B, N)
+    dy = synth.normal(34, B * L).reshape(B, L)
+    df = ss.conv1d_backward_filter(dev(x).view(B, N), dev(dy).view(B, L), k, 1).cpu().numpy()
+    ref, mag = oracle.conv1d_backward_filter(x, dy, k, 1)
+    within(df, ref, mag, f"conv bwd filter (tensor cores) B={B} N={N} k={k}")
+
+
+def test_conv_backward_filter_tc_integers_exact(ss):
+    # small integers: the TF32 split is exact (lo = 0), every product and partial sum is an exact integer
+    B, N, k = 3, 40000, 63
+    L = N - k + 1
+    x = synth.randint(35, B * N, -4, 4).astype(np.float32).reshape(B, N)
+    dy = synth.randint(36, B * L, -4, 4).astype(np.float32).reshape(B, L)
+    df = ss.conv1d_backward_filter(dev(x).view(B, N), dev(dy).view(B, L), k, 1).cpu().numpy()
+    ref, _ = oracle.conv1d_backward_filter(x, dy, k, 1)
+    np.testing.assert_array_equal(df.astype(np.float64), ref)
+
+
 def test_conv_backward_filter_deterministic(ss):
     x = torch.from_numpy(synth.normal(29, 8 * 100000).reshape(8, -1)).cuda()
     dy = torch.from_numpy(synth.normal(30, 8 * (100000 - 62)).reshape(8, -1)).cuda()
