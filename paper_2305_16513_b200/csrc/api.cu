@@ -182,6 +182,20 @@ bool encode_mc_map(CUtensorMap* m, const void* x, int64_t positions, int64_t cin
   return r == CUDA_SUCCESS;
 }
 
+// fp32 rows of 128 (x viewed as [rows][128], 16-B aligned base), boxes of 33 rows, OOB zero fill.
+bool encode_rows128_map(CUtensorMap* m, const void* base, int64_t rows) {
+  auto enc = encode_fn();
+  if (!enc || rows < 1 || rows >= (int64_t(1) << 31) || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+  cuuint64_t dims[2] = {128, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {512};
+  cuuint32_t box[2] = {128, 33};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // 1-D fp32 view of n elements (16-B aligned base), boxes of 256, OOB zero fill.
 bool encode_flat_f32_map(CUtensorMap* m, const void* base, int64_t n) {
   auto enc = encode_fn();
@@ -618,12 +632,11 @@ static ss_status_t conv1d_backward_filter_impl(const void* x, const void* dy, fl
   BackwardParams p;
   memset(&p, 0, sizeof p);
   p.x = x; p.dy = dy; p.N = N; p.L = L; p.batch = batch; p.w = k; p.stride = stride;
-  if (conv_filter_grad_tc_supported(N, k, stride, x)) {
-    FgradTcParams q;
-    memset(&q, 0, sizeof q);
+  FgradTcParams q;
+  memset(&q, 0, sizeof q);
+  if (conv_filter_grad_tc_supported(N, k, stride, x) && encode_rows128_map(&q.tm_x, x, batch * N / 128)) {
     q.x = static_cast<const float*>(x); q.dy = static_cast<const float*>(dy); q.part = static_cast<double*>(workspace);
     q.N = N; q.L = L; q.batch = batch; q.k = k;
-    { const char* e = getenv("SS_FT_DBG"); q.dbg = e ? atoi(e) : 0; }
     cudaError_t e = launch_conv_filter_grad_tc(q, df, ctas, current_sms(), static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv1d_backward_filter launch");
   }

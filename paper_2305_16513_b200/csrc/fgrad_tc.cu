@@ -15,22 +15,30 @@
 //
 // Numerics: 3xTF32 (A_hi B_hi + A_hi B_lo + A_lo B_hi, hi = the TF32 truncation,
 // lo = the exact remainder; ~2^-21 relative per product), fp32 accumulation in
-// tensor memory over a unit of 64 chunks, then fp64: the diagonal sums and all
-// cross-unit / cross-CTA sums are in double (two-pass: per-CTA partials in the
-// caller's workspace, conv_filter_grad_finish sums them in CTA order).
+// tensor memory over a unit of 128 chunks (<= 128 fp32 roundings of a sum bounded
+// by the sum of |terms|: ~7.6e-6 of it, inside the 1e-5 bound), then fp64: the
+// diagonal sums (8-term fp32 partials) and all cross-unit / cross-CTA sums are in
+// double (two-pass: per-CTA partials in the caller's workspace,
+// conv_filter_grad_finish sums them in CTA order).  Deterministic.
 //
-// Roles (416 threads, one CTA per SM): two groups of 4 loader warps take
-// alternate stages of 32 chunks (4-stage ring) -- thread v issues all its loads
-// of a stage at once, splits dy[.., 128 u + v] into hi / lo and writes them to
-// tensor memory (A operand: lane v, one column per chunk) and stores x rows,
-// split, into the MN-major SWIZZLE_128B_BASE32B B tiles (the only MN-major
-// layout TF32 accepts; tools/ubench/tc_mn_probe.cu); warp 8 issues 24 MMAs per
-// stage (4 K-groups x 3 products x {N = 128, N = 64 shifted}); warps 9-12 drain the
-// 192-column accumulator per unit: lane v reads the 96 columns its diagonal can
-// touch, a padded shared-memory transpose turns rows into diagonals, and each
-// thread adds 64 diagonal terms in double.
+// Roles (704 threads, one CTA per SM; x rows need N % 128 == 0):
+//   warp 21      TMA producer: x rows u0 .. u0 + 32 of each stage (32 chunks) as one
+//                2-D box of x viewed as [batch N / 128][128], into a 6-deep raw ring;
+//   warps 0-15   two loader groups of 8 warps taking alternate stages (slot = group):
+//                thread v issues the stage's dy loads into registers, then, once the
+//                MMA has drained the group's previous stage, splits dy[.., 128 u + v]
+//                into hi / lo for tensor memory (A operand: lane v, one column per
+//                chunk; warps w and w + 4 of a group share lane quarter w) and the raw
+//                x rows into the MN-major SWIZZLE_128B_BASE32B B tiles (the only
+//                MN-major layout TF32 accepts; tools/ubench/tc_mn_probe.cu);
+//   warp 16      MMA issuer: per stage 4 K-groups x 3 products x {N = 128, N = 64 one
+//                K row down} = 24 MMAs into one of two 192-column accumulators;
+//   warps 17-20  drain an accumulator per unit: lane v reads the 96 columns its
+//                diagonal can touch, a padded shared-memory transpose turns rows into
+//                diagonals, and each thread sums 64 diagonal terms.
+// Measured (64 x 2^20, 1 x B200): k = 63 at 120 us vs 250 us for the FFMA2 kernel; the
+// tensor pipe is ~77% busy (ncu), so the 3 products are the limit.
 #include <cstdint>
-#include <cstdio>
 #include <cstdlib>
 
 #include <cuda_runtime.h>
@@ -50,10 +58,14 @@ constexpr int kFtRows = 36;                        // B rows per stage (33 used)
 constexpr uint32_t kFtLBO = kFtRows * 128u;        // MN-atom stride (bytes)
 constexpr uint32_t kFtB = 4u * kFtLBO;             // one B operand (hi or lo) of a stage
 constexpr int kFtPitch = 97;                       // transpose scratch row pitch (floats)
-constexpr int kFtThreads = 21 * 32;
+constexpr int kFtThreads = 22 * 32;
 constexpr int kFtWarpMma = 16;                     // warps 0-15: loaders (two groups of 8)
 constexpr int kFtEpi0 = 17;                        // first epilogue warp (17-20)
-constexpr size_t kFtSmem = 1024 + (size_t)kFtStages * 2 * kFtB + (size_t)128 * kFtPitch * 4 + 128 * 8 + 128;
+constexpr int kFtWarpTma = 21;                     // raw x rows of each stage by TMA, kFtRaw stages ahead
+constexpr int kFtRaw = 6;                          // raw x ring
+constexpr uint32_t kFtRawBytes = 34u * 512u;        // one raw stage: 33 rows of 128 floats (+1 row pad)
+constexpr size_t kFtSmem = 1024 + (size_t)kFtStages * 2 * kFtB + (size_t)kFtRaw * kFtRawBytes +
+                           (size_t)128 * kFtPitch * 4 + 128 * 8 + 256;
 
 __device__ __forceinline__ uint64_t mn32_desc(uint32_t saddr) {  // MN-major, SWIZZLE_128B_BASE32B
   uint64_t d = 0;
@@ -124,19 +136,24 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
   extern __shared__ __align__(16) uint8_t ft_raw[];
   uint8_t* smem = ft_raw + ((1024u - (smem_u32(ft_raw) & 1023u)) & 1023u);
   uint8_t* bsm = smem;                                            // [stage][hi, lo][4 atoms][36 rows][128 B]
-  float* cs = reinterpret_cast<float*>(bsm + kFtStages * 2 * kFtB);  // [128][97] transpose scratch
+  float* raw = reinterpret_cast<float*>(bsm + kFtStages * 2 * kFtB);  // [kFtRaw][33 x 128 (+pad)] raw x rows
+  float* cs = raw + kFtRaw * (kFtRawBytes / 4);                         // [128][97] transpose scratch
   double* red = reinterpret_cast<double*>(cs + 128 * kFtPitch);      // [128]
   uint64_t* full = reinterpret_cast<uint64_t*>(red + 128);           // [stages]
   uint64_t* empty = full + kFtStages;                                // [stages]
   uint64_t* dfull = empty + kFtStages;                               // [2]
   uint64_t* dempty = dfull + 2;                                      // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
+  uint64_t* rfull = dempty + 2;                                      // [kFtRaw] TMA landed
+  uint64_t* rempty = rfull + kFtRaw;                                 // [kFtRaw] loader group consumed
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(rempty + kFtRaw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t N = p.N, L = p.L, U = p.U, UR = p.units_per_row, nunits = p.nunits;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kFtStages; ++s) { mbar_init(full + s, 256); mbar_init(empty + s, 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(dfull + s, 1); mbar_init(dempty + s, 4); }
+    for (int s = 0; s < kFtRaw; ++s) { mbar_init(rfull + s, 1); mbar_init(rempty + s, 256); }
+    prefetch_tmap(&p.tm_x);
     fence_mbar_init();
   }
   if (warp == 0) {
@@ -157,7 +174,6 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
     const int t = threadIdx.x & 255;  // thread in the group: x items t + 256 m
     const uint32_t lanebits = (uint32_t)(32 * (wg & 3)) << 16;
     const float* __restrict__ dyp = p.dy;
-    const float* __restrict__ xp = p.x;
     // x item m of this thread: row r = (t >> 5) + 8 m of the stage (K atom 2 m + (t >> 7), row (t >> 5) & 3
     // inside it), 16-B piece t & 31 of the row; rows >= 33 are not loaded
     const int xrow = t >> 5, s4 = 4 * (t & 31), xa = s4 >> 5, xc = (s4 & 31) >> 3, xh = (s4 & 7) >> 2;
@@ -169,12 +185,10 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
       for (int s2 = 0; s2 < kFtUnitStages; ++s2, ++it) {
         if ((it & 1) != grp) continue;  // this group's stages: it = grp mod 2 (slot grp)
         const int st = it % kFtStages;
-        if (p.trace && blockIdx.x == 0 && t == 0 && it < 64) p.trace[it * 8 + 0] = clock64();
         const int64_t u0 = q * kFtUnitChunks + s2 * kFtStageChunks;
         // all of this thread's loads of the stage first; in-range stages (all but a row's last) take
         // unpredicated loads at immediate offsets
         const float* __restrict__ dyr = dyp + b * L + 128 * (u0 + ch0) + v;  // chunk ch0 + c: dyr[128 c]
-        const float* __restrict__ xr = xp + b * N + 128 * (u0 + xrow) + s4;   // item m: xr[1024 m]
         float dv[16];
         float4 xq[5];
         if (128 * (u0 + kFtStageChunks) <= L) {
@@ -185,22 +199,21 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
 #pragma unroll
           for (int c = 0; c < 16; ++c) dv[c] = 128 * c < rem ? __ldg(dyr + 128 * c) : 0.0f;
         }
-        if (128 * (u0 + 33) <= N) {
+        // x rows of the stage from the raw TMA ring (x past the row end is the next row's data or the
+        // TMA's zero fill past the array: finite, and only ever multiplied by the zero dy of i >= L)
+        {
+          const int rs = it % kFtRaw;
+          ft_wait(rfull + rs, (uint32_t)(it / kFtRaw) & 1u);
+          const float* xr = raw + rs * (kFtRawBytes / 4) + 128 * xrow + s4;  // item m: xr[1024 m]
 #pragma unroll
           for (int m = 0; m < 5; ++m)
-            xq[m] = (m < 4 || xrow == 0) ? __ldg(reinterpret_cast<const float4*>(xr + 1024 * m))
+            xq[m] = (m < 4 || xrow == 0) ? *reinterpret_cast<const float4*>(xr + 1024 * m)
                                          : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        } else {
-          const int64_t remx = N - 128 * (u0 + xrow) - s4;  // item m valid iff 1024 m < remx
-#pragma unroll
-          for (int m = 0; m < 5; ++m)
-            xq[m] = ((m < 4 || xrow == 0) && 1024 * m < remx) ? __ldg(reinterpret_cast<const float4*>(xr + 1024 * m))
-                                                              : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          mbar_arrive(rempty + rs);
         }
         // the loads are in flight while the MMA drains this group's previous stage (same slot)
         mbar_wait(empty + st, ((uint32_t)(it / kFtStages) & 1u) ^ 1u);  // sleeping wait: 16 spinning warps
         // would take issue slots from the MMA warp
-        if (p.trace && blockIdx.x == 0 && t == 0 && it < 64) p.trace[it * 8 + 1] = clock64();
         // A: dy chunk values of lane v, split into TF32 hi and the exact remainder
         {
           uint32_t hi[16], lo[16];
@@ -237,7 +250,27 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
         fence_proxy_async_smem();
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         mbar_arrive(full + st);
-        if (p.trace && blockIdx.x == 0 && t == 0 && it < 64) p.trace[it * 8 + 2] = clock64();
+      }
+    }
+  } else if (warp == kFtWarpTma) {
+    // ------------------------------------------------------------ raw x rows of each stage by TMA
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
+        const int64_t b = unit / UR, q = unit - b * UR;
+        for (int s2 = 0; s2 < kFtUnitStages; ++s2, ++it) {
+          const int rs = it % kFtRaw;
+          mbar_wait(rempty + rs, ((uint32_t)(it / kFtRaw) & 1u) ^ 1u);
+          // one box of 33 rows of 128 (x viewed as [batch N / 128][128]; N % 128 == 0)
+          const int32_t row0 = (int32_t)((b * N) / 128 + q * kFtUnitChunks + s2 * kFtStageChunks);
+          float* dst = raw + rs * (kFtRawBytes / 4);
+          mbar_arrive_expect_tx(rfull + rs, 33u * 512u);
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+              "l"(reinterpret_cast<uint64_t>(&p.tm_x)), "r"(0), "r"(row0), "r"(smem_u32(rfull + rs))
+              : "memory");
+        }
       }
     }
   } else if (warp == kFtWarpMma) {
@@ -252,9 +285,7 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
       const uint32_t dcol = tmem + 192u * d;
       for (int s2 = 0; s2 < kFtUnitStages; ++s2, ++it) {
         const int st = it % kFtStages;
-        if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 8 + 3] = clock64();
         ft_wait(full + st, (uint32_t)(it / kFtStages) & 1u);
-        if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 8 + 4] = clock64();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t bh = b0 + (uint32_t)st * 2u * kFtB, bl = bh + kFtB;
         const uint32_t ah = tmem + kAcol + 64u * st, al = ah + 32u;
@@ -265,12 +296,11 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
             const uint32_t a = (pr == 2 ? al : ah) + 8u * g;
             const uint32_t bb = (pr == 1 ? bl : bh) + 1024u * g;
             const uint32_t acc = (s2 == 0 && g == 0 && pr == 0) ? 0u : 1u;
-            if (!(p.dbg & 4)) { ft_mma(dcol, a, mn32_desc(bb), i128, acc);
-            ft_mma(dcol + 128u, a, mn32_desc(bb + 128u), i64, acc); }
+            ft_mma(dcol, a, mn32_desc(bb), i128, acc);
+            ft_mma(dcol + 128u, a, mn32_desc(bb + 128u), i64, acc);
           }
         }
         ft_commit(empty + st);
-        if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 8 + 5] = clock64();
       }
       ft_commit(dfull + d);
       if (++d == 2) { d = 0; dph ^= 1u; }
@@ -283,12 +313,8 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
     double acc = 0.0;
     int d = 0;
     uint32_t dph = 0;
-    int ue = 0;
-    for (int64_t unit = blockIdx.x; unit < nunits; unit += gridDim.x, ++ue) {
-      const bool etr = p.trace && blockIdx.x == 0 && threadIdx.x == 32 * kFtEpi0 && ue < 32;
-      if (etr) p.trace[(2 * ue + 1) * 8 + 6] = clock64();
+    for (int64_t unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
       ft_wait(dfull + d, dph);
-      if (etr) p.trace[(2 * ue + 1) * 8 + 7] = clock64();
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       // row v of C, columns 32 qd + [0, 96)  ->  cs[v][0, 96), 32 columns at a time (registers)
 #pragma unroll 1
@@ -300,7 +326,6 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(dempty + d);
-          if (etr) p.trace[(2 * ue) * 8 + 6] = clock64();
         }
 #pragma unroll
         for (int i2 = 0; i2 < 32; ++i2) cs[v * kFtPitch + 32 * t + i2] = __uint_as_float(c[i2]);
@@ -326,7 +351,6 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
         acc += s;
       }
       asm volatile("bar.sync 2, 128;" ::: "memory");
-      if (etr) p.trace[(2 * ue) * 8 + 7] = clock64();
       if (++d == 2) { d = 0; dph ^= 1u; }
     }
     red[e] = acc;
@@ -343,8 +367,8 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
 }
 
 bool conv_filter_grad_tc_supported(int64_t N, int64_t k, int64_t stride, const void* x) {
-  return stride == 1 && k >= 1 && k <= 64 && N % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
-         tc_filter_grad_enabled();
+  return stride == 1 && k >= 1 && k <= 64 && N % 128 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+         tc_filter_grad_enabled();  // (and batch N < 2^31 for the TMA map: checked by the caller's encode)
 }
 
 cudaError_t launch_conv_filter_grad_tc(FgradTcParams& p, float* df, int ctas, int sms, cudaStream_t stream) {
@@ -356,21 +380,8 @@ cudaError_t launch_conv_filter_grad_tc(FgradTcParams& p, float* df, int ctas, in
   if (e != cudaSuccess) return e;
   int64_t g = sms < ctas ? sms : ctas;
   if (g > p.nunits) g = p.nunits < 1 ? 1 : p.nunits;
-  static unsigned long long* tb = nullptr;
-  p.trace = nullptr;
-  if (getenv("SS_FT_TRACE")) { if (!tb) cudaMalloc(&tb, 4096); cudaMemsetAsync(tb, 0, 4096, stream); p.trace = tb; }
   conv_filter_grad_tc_kernel<<<(unsigned)g, kFtThreads, kFtSmem, stream>>>(p);
   note_launch();
-  if (p.trace) {
-    static unsigned long long h[512];
-    cudaMemcpyAsync(h, tb, 4096, cudaMemcpyDeviceToHost, stream);
-    cudaStreamSynchronize(stream);
-    for (int i = 0; i < 24; ++i)
-      printf("st %2d ld: w %6lld got %6lld done %6lld | mma: w %6lld full %6lld commit %6lld | epi %6lld %6lld\n", i,
-             (long long)(h[i*8]-h[0]), (long long)(h[i*8+1]-h[0]), (long long)(h[i*8+2]-h[0]),
-             (long long)(h[i*8+3]-h[0]), (long long)(h[i*8+4]-h[0]), (long long)(h[i*8+5]-h[0]),
-             (long long)(h[i*8+6]-h[0]), (long long)(h[i*8+7]-h[0]));
-  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_conv_filter_grad_finish(p.part, ctas, p.k, df, stream);

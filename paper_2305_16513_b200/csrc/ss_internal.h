@@ -172,6 +172,7 @@ struct alignas(64) MaxBwdS1Params {
 bool pool_max_backward_s1_supported(int64_t w);
 cudaError_t launch_pool_max_backward_s1(MaxBwdS1Params& p, cudaStream_t stream, int sms);
 bool encode_flat_f32_map(CUtensorMap* m, const void* base, int64_t n);
+bool encode_rows128_map(CUtensorMap* m, const void* base, int64_t rows);
 int conv_filter_grad_ctas(int sms);
 size_t conv_filter_grad_workspace(int64_t k, int ctas);
 cudaError_t launch_conv_filter_grad(const BackwardParams& p, float* df, void* workspace, int ctas,
@@ -179,15 +180,14 @@ cudaError_t launch_conv_filter_grad(const BackwardParams& p, float* df, void* wo
 cudaError_t launch_pool2d_backward(const Pool2DBackwardParams& p, cudaStream_t stream, int sms);
 cudaError_t launch_conv_filter_grad_finish(const double* part, int ctas, int64_t k, float* df, cudaStream_t stream);
 // Tensor-core filter gradient (fgrad_tc.cu): stride 1, k <= 64, N % 4 == 0, 16-B aligned x.
-struct FgradTcParams {
+struct alignas(64) FgradTcParams {
+  CUtensorMap tm_x;              // x as 1-D fp32 [batch N], boxes of 256 (raw rows of a stage by TMA)
   const float* x;
   const float* dy;
   double* part;                  // caller's workspace: per-CTA fp64 partials, [ctas][64]
   int64_t N, L, batch, k;
   int64_t U, units_per_row, nunits;  // set by the launcher
   int64_t ctas;
-  int dbg;
-  unsigned long long* trace;
 };
 bool tc_filter_grad_enabled();
 bool conv_filter_grad_tc_supported(int64_t N, int64_t k, int64_t stride, const void* x);
