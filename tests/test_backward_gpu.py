@@ -190,12 +190,13 @@ def test_conv_backward_filter(ss, B, N, k, s):
     within(df, ref, mag, f"conv bwd filter B={B} N={N} k={k} s={s}")
 
 
-# tensor-core filter gradient (csrc/fgrad_tc.cu): stride 1, k <= 64, N % 4 == 0, 16-B aligned x --
-# chunks of 128 dy positions, units of 64 chunks, row tails (L % 128), rows shorter than a chunk, one
-# unit per row and many, more units than CTAs
+# tensor-core filter gradient (csrc/fgrad_tc.cu): stride 1, k <= 64, N % 128 == 0, 16-B aligned x --
+# chunks of 128 dy positions, units of 128 chunks, row tails (L % 128), one chunk per row, one unit per
+# row and many, more units than CTAs; N % 128 != 0 cases take the FFMA kernels
 FT_CASES = [  # (B, N, k)
-    (1, 4, 1), (2, 8, 3), (3, 100, 7), (2, 128, 64), (1, 132, 5), (4, 1000, 31), (2, 8192, 63), (3, 8196, 33),
-    (1, 70000, 64), (5, 20004, 2), (64, 16384, 63), (2, 1 << 18, 17),
+    (1, 128, 1), (2, 128, 64), (3, 256, 3), (2, 384, 64), (5, 1280, 7), (4, 16384 + 128, 31), (2, 8192, 63),
+    (3, 32768, 33), (64, 16384, 63), (2, 1 << 18, 17), (1, 70016, 64), (7, 20096, 2),
+    (1, 4, 1), (3, 100, 7), (1, 132, 5), (3, 8196, 33),
 ]
 
 
@@ -211,7 +212,7 @@ def test_conv_backward_filter_tc(ss, B, N, k):
 
 def test_conv_backward_filter_tc_integers_exact(ss):
     # small integers: the TF32 split is exact (lo = 0), every product and partial sum is an exact integer
-    B, N, k = 3, 40000, 63
+    B, N, k = 3, 40064, 63
     L = N - k + 1
     x = synth.randint(35, B * N, -4, 4).astype(np.float32).reshape(B, N)
     dy = synth.randint(36, B * L, -4, 4).astype(np.float32).reshape(B, L)
