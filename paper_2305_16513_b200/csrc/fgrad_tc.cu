@@ -41,6 +41,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "ss_device.cuh"
@@ -51,12 +52,21 @@ namespace ss {
 namespace {
 
 constexpr int kFtStageChunks = 32;                 // K rows per stage (4 K-groups of 8)
-constexpr int kFtUnitStages = 4;                   // stages per accumulation unit (128 chunks)
+// Mixed precision (the forward tensor-core conv's scheme): D += A_hi B_hi in kind::tf32 plus ONE
+// kind::f16 MMA of K = 16 for both cross terms, [bf16(A_hi) | bf16(A_lo)] . [bf16(B_lo) ; bf16(B_hi)]
+// (K pairs packed per TMEM column against interleaved B rows) -- two MMA-times per K-group
+// instead of three.  Per-product error ~2^-18, so units shrink to 64 chunks to keep the fp32
+// accumulation inside the bound.
+constexpr bool kFtMixed = false;  // measured: 123.6 us (tensor pipe 45% busy) vs 120 us for 3xTF32 -- the
+                                   // MMAs are not the limit once the loaders run two stages ahead
+constexpr int kFtUnitStages = kFtMixed ? 2 : 4;    // stages per accumulation unit (64 / 128 chunks)
 constexpr int kFtUnitChunks = kFtStageChunks * kFtUnitStages;
 constexpr int kFtStages = 2;                       // slots: loader group g owns slot g (stages it = g mod 2)
 constexpr int kFtRows = 36;                        // B rows per stage (33 used), 9 BASE32B atoms of 4
 constexpr uint32_t kFtLBO = kFtRows * 128u;        // MN-atom stride (bytes)
 constexpr uint32_t kFtB = 4u * kFtLBO;             // one B operand (hi or lo) of a stage
+constexpr uint32_t kFtLBO16 = 9u * 1024u;          // mixed: bf16 pair tile, MN atom (64 bf16) stride, 72 rows
+static_assert(2 * kFtLBO16 <= kFtB, "the bf16 pair tile reuses the lo tile's space");
 constexpr int kFtPitch = 97;                       // transpose scratch row pitch (floats)
 constexpr int kFtThreads = 22 * 32;
 constexpr int kFtWarpMma = 16;                     // warps 0-15: loaders (two groups of 8)
@@ -75,6 +85,22 @@ __device__ __forceinline__ uint64_t mn32_desc(uint32_t saddr) {  // MN-major, SW
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)1 << 61;
   return d;
+}
+__device__ __forceinline__ uint64_t mn16_desc(uint32_t saddr) {  // MN-major bf16, SWIZZLE_128B
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((kFtLBO16 >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((1024u >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+__host__ __device__ constexpr uint32_t idesc_bf16_bmn(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ uint32_t bf16_pack(float lo, float hi) {  // low half = lo (round to nearest)
+  return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(lo)) |
+         ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(hi)) << 16);
 }
 __host__ __device__ constexpr uint32_t idesc_tf32_bmn(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -179,6 +205,14 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
     const int xrow = t >> 5, s4 = 4 * (t & 31), xa = s4 >> 5, xc = (s4 & 31) >> 3, xh = (s4 & 7) >> 2;
     const uint32_t xoff0 = (uint32_t)xa * kFtLBO + (uint32_t)(xrow >> 2) * 512u + (uint32_t)(xrow & 3) * 128u +
                            ((uint32_t)(xc ^ (xrow & 3)) << 5) + (uint32_t)xh * 16u;
+    // mixed: bf16 pair tile rows kr = 2 r + e (e = 0 lo, 1 hi); row r = xrow + 8 m -> K atom (2 xrow + e) / 8
+    // + 2 m, row (2 xrow + e) % 8; 64-bf16 MN atom s4 / 64, 16-B chunk (s4 % 64) / 8, byte (s4 % 8) * 2
+    auto poff = [&](int e2) {
+      const int kr = 2 * xrow + e2, a16 = s4 >> 6, c16 = (s4 & 63) >> 3, rr16 = kr & 7;
+      return (uint32_t)a16 * kFtLBO16 + (uint32_t)(kr >> 3) * 1024u + (uint32_t)rr16 * 128u +
+             ((uint32_t)(c16 ^ rr16) << 4) + (uint32_t)(s4 & 7) * 2u;
+    };
+    const uint32_t xoffp0 = poff(0), xoffp1 = poff(1);
     int it = 0;
     for (int64_t unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
       const int64_t b = unit / UR, q = unit - b * UR;
@@ -221,7 +255,8 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
           for (int c = 0; c < 16; ++c) {
             const uint32_t h = tf32_hi(__float_as_uint(dv[c]));
             hi[c] = h;
-            lo[c] = __float_as_uint(dv[c] - __uint_as_float(h));
+            const float l = dv[c] - __uint_as_float(h);
+            lo[c] = kFtMixed ? bf16_pack(__uint_as_float(h), l) : __float_as_uint(l);  // mixed: (hi, lo) K pair
           }
           tmem_st16(tmem + lanebits + kAcol + 64u * st + (uint32_t)ch0, hi);
           tmem_st16(tmem + lanebits + kAcol + 64u * st + 32u + (uint32_t)ch0, lo);
@@ -229,6 +264,8 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
         // B: x rows u0 .. u0 + 32 (row r = x[b][128 (u0 + r) + s]), hi and lo, MN-major BASE32B swizzle
         {
           const uint32_t bh = smem_u32(bsm + (size_t)st * 2 * kFtB) + xoff0, bl = bh + kFtB;
+          const uint32_t bp = smem_u32(bsm + (size_t)st * 2 * kFtB + kFtB);
+          const uint32_t bp0 = bp + xoffp0, bp1 = bp + xoffp1;
 #pragma unroll
           for (int m = 0; m < 5; ++m) {
             if (m < 4 || xrow == 0) {
@@ -240,9 +277,19 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
               asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(bh + 1024u * m), "r"(h0), "r"(h1), "r"(h2),
                            "r"(h3)
                            : "memory");
-              asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(bl + 1024u * m), "f"(l0), "f"(l1), "f"(l2),
-                           "f"(l3)
-                           : "memory");
+              if (kFtMixed) {  // rows 2 r (lo) and 2 r + 1 (hi) of the bf16 pair tile
+                asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(bp0 + 2048u * m), "r"(bf16_pack(l0, l1)),
+                             "r"(bf16_pack(l2, l3))
+                             : "memory");
+                asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(bp1 + 2048u * m),
+                             "r"(bf16_pack(__uint_as_float(h0), __uint_as_float(h1))),
+                             "r"(bf16_pack(__uint_as_float(h2), __uint_as_float(h3)))
+                             : "memory");
+              } else {
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(bl + 1024u * m), "f"(l0), "f"(l1), "f"(l2),
+                             "f"(l3)
+                             : "memory");
+              }
             }
           }
         }
@@ -276,6 +323,7 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
   } else if (warp == kFtWarpMma) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t i128 = idesc_tf32_bmn(128, 128), i64 = idesc_tf32_bmn(128, 64);
+    constexpr uint32_t j128 = idesc_bf16_bmn(128, 128), j64 = idesc_bf16_bmn(128, 64);
     const uint32_t b0 = __shfl_sync(0xffffffffu, smem_u32(bsm), 0);
     int it = 0, d = 0;
     uint32_t dph = 0;
@@ -291,13 +339,21 @@ __global__ void __launch_bounds__(kFtThreads, 1) conv_filter_grad_tc_kernel(cons
         const uint32_t ah = tmem + kAcol + 64u * st, al = ah + 32u;
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
+          if (kFtMixed) {
+            const uint32_t acc = (s2 == 0 && g == 0) ? 0u : 1u;
+            ft_mma(dcol, ah + 8u * g, mn32_desc(bh + 1024u * g), i128, acc);          // hi * hi, TF32
+            ft_mma(dcol + 128u, ah + 8u * g, mn32_desc(bh + 1024u * g + 128u), i64, acc);
+            ft_mma(dcol, al + 8u * g, mn16_desc(bl + 2048u * g), j128, 1u);           // both cross terms, bf16
+            ft_mma(dcol + 128u, al + 8u * g, mn16_desc(bl + 2048u * g + 256u), j64, 1u);
+          } else {
 #pragma unroll
-          for (int pr = 0; pr < 3; ++pr) {  // hi*hi, hi*lo, lo*hi
-            const uint32_t a = (pr == 2 ? al : ah) + 8u * g;
-            const uint32_t bb = (pr == 1 ? bl : bh) + 1024u * g;
-            const uint32_t acc = (s2 == 0 && g == 0 && pr == 0) ? 0u : 1u;
-            ft_mma(dcol, a, mn32_desc(bb), i128, acc);
-            ft_mma(dcol + 128u, a, mn32_desc(bb + 128u), i64, acc);
+            for (int pr = 0; pr < 3; ++pr) {  // hi*hi, hi*lo, lo*hi
+              const uint32_t a = (pr == 2 ? al : ah) + 8u * g;
+              const uint32_t bb = (pr == 1 ? bl : bh) + 1024u * g;
+              const uint32_t acc = (s2 == 0 && g == 0 && pr == 0) ? 0u : 1u;
+              ft_mma(dcol, a, mn32_desc(bb), i128, acc);
+              ft_mma(dcol + 128u, a, mn32_desc(bb + 128u), i64, acc);
+            }
           }
         }
         ft_commit(empty + st);
