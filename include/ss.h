@@ -312,7 +312,11 @@ ss_status_t ss_conv1d_mc_backward_input(const void* dy, const void* w, float* dx
  *   ss_conv1d_backward_input   dx_t = sum_{(i,j): i*s+j = t} f_j dy_i.  SS_F32.
  *   ss_conv1d_backward_filter  df_j = sum_b sum_i dy[b][i] x[b][i*s+j]  (df: DEVICE,
  *                          k floats; fp32 products summed in fp32 runs of 64, then
- *                          fp64).  `workspace` (DEVICE, caller-owned,
+ *                          fp64.  Stride 1, k <= 64, N % 128 == 0 and 16-B aligned x
+ *                          run on the tensor cores (reading R24): the same
+ *                          products regrouped by chunks of 128 dy positions, 3xTF32
+ *                          (~2^-21 relative each), fp32 over <= 128 chunks, then fp64;
+ *                          also deterministic, within the same bound).  `workspace` (DEVICE, caller-owned,
  *                          >= ss_conv1d_backward_filter_workspace(k) bytes on the
  *                          current device) holds per-CTA fp64 partials.
  *   ss_pool2d_backward     [planes][H][W] gradient of ss_pool2d: avg spreads
