@@ -94,6 +94,8 @@ def lib() -> ctypes.CDLL:
             L.oracle_conv2d_mc_bf16.restype = ctypes.c_int
             L.oracle_conv1d_mc_backward_input_bf16.argtypes = [vp, vp, i64, i64, i64, i64, i64, vp, vp]
             L.oracle_conv1d_mc_backward_input_bf16.restype = ctypes.c_int
+            L.oracle_conv1d_mc_backward_filter_bf16.argtypes = [vp, vp, i64, i64, i64, i64, i64, vp, vp]
+            L.oracle_conv1d_mc_backward_filter_bf16.restype = ctypes.c_int
             L.oracle_conv2d_f32.argtypes = [vp, i64, i64, i64, vp, i64, i64, i64, i64, vp, vp]
             L.oracle_conv2d_f32.restype = ctypes.c_int
             L.oracle_conv2d_backward_input_f32.argtypes = [vp, i64, i64, i64, vp, i64, i64, i64, i64, vp, vp]
@@ -466,3 +468,17 @@ def conv1d_mc_backward_input(dy_bf16: np.ndarray, w_bf16: np.ndarray, N: int):
     m = np.empty((B, N, cin), np.float64)
     _check(lib().oracle_conv1d_mc_backward_input_bf16(_p(dy), _p(w), B, N, cin, cout, k, _p(dx), _p(m)))
     return dx, m
+
+
+def conv1d_mc_backward_filter(dy_bf16: np.ndarray, x_bf16: np.ndarray, k: int):
+    """dw [Cout, Cin, k] (double) of the multi-channel conv1d for bf16 dy [B, N-k+1, Cout] and
+    x [B, N, Cin] (reading R25); returns (dw, absmag)."""
+    dy = np.ascontiguousarray(dy_bf16, np.uint16)
+    x = np.ascontiguousarray(x_bf16, np.uint16)
+    B, L, cout = dy.shape
+    B2, N, cin = x.shape
+    assert B2 == B and L == N - k + 1
+    dw = np.empty((cout, cin, k), np.float64)
+    m = np.empty((cout, cin, k), np.float64)
+    _check(lib().oracle_conv1d_mc_backward_filter_bf16(_p(dy), _p(x), B, N, cin, cout, k, _p(dw), _p(m)))
+    return dw, m

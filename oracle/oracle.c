@@ -687,3 +687,29 @@ int oracle_conv1d_mc_backward_input_bf16(const uint16_t* dy, const uint16_t* w, 
         }
   return 0;
 }
+
+/* Filter gradient of the multi-channel 1-D convolution (reading R25: the
+ * vector-Jacobian product of reading R18 with respect to the weights), bf16 dy and x:
+ *   y[b][i][co] = sum_j sum_ci w[co][ci][j] x[b][i+j][ci]
+ *   =>  dw[co][ci][j] = sum_b sum_{i < N-k+1} dy[b][i][co] * x[b][i+j][ci]
+ * dy [batch][N-k+1][cout], x [batch][N][cin], dw [cout][cin][k]; accumulated in
+ * double in (b, i) order. */
+int oracle_conv1d_mc_backward_filter_bf16(const uint16_t* dy, const uint16_t* x, int64_t batch, int64_t N,
+                                          int64_t cin, int64_t cout, int64_t k, double* dw, double* absmag) {
+  if (dy == NULL || x == NULL || dw == NULL || batch < 1 || cin < 1 || cout < 1 || k < 1 || k > N) return -1;
+  int64_t L = N - k + 1;
+  for (int64_t co = 0; co < cout; ++co)
+    for (int64_t ci = 0; ci < cin; ++ci)
+      for (int64_t j = 0; j < k; ++j) {
+        double acc = 0.0, mag = 0.0;
+        for (int64_t b = 0; b < batch; ++b)
+          for (int64_t i = 0; i < L; ++i) {
+            double t = bf16_to_double(dy[(b * L + i) * cout + co]) * bf16_to_double(x[(b * N + i + j) * cin + ci]);
+            acc += t;
+            mag += fabs(t);
+          }
+        dw[(co * cin + ci) * k + j] = acc;
+        if (absmag) absmag[(co * cin + ci) * k + j] = mag;
+      }
+  return 0;
+}

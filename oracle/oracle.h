@@ -155,6 +155,8 @@ int oracle_conv2d_mc_bf16(const uint16_t* x, const uint16_t* w, int64_t batch, i
  * w [cout][cin][k] as bf16 bits; dx [batch][N][cin] = the scatter of w * dy, in double. */
 int oracle_conv1d_mc_backward_input_bf16(const uint16_t* dy, const uint16_t* w, int64_t batch, int64_t N,
                                          int64_t cin, int64_t cout, int64_t k, double* dx, double* absmag);
+int oracle_conv1d_mc_backward_filter_bf16(const uint16_t* dy, const uint16_t* x, int64_t batch, int64_t N,
+                                          int64_t cin, int64_t cout, int64_t k, double* dw, double* absmag);
 
 #ifdef __cplusplus
 }

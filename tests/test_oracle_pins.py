@@ -594,3 +594,36 @@ def test_conv1d_mc_backward_input_adjoint_and_torch():
     dx1, _ = oracle.conv1d_mc_backward_input(g1b, w1b, N)
     ref1, _ = oracle.conv1d_backward_input(oracle.bf16_bits_to_f32(g1b)[..., 0], oracle.bf16_bits_to_f32(w1b)[0, 0], N)
     np.testing.assert_allclose(dx1[..., 0], ref1, rtol=1e-12, atol=1e-12)
+
+
+def test_conv1d_mc_backward_filter_adjoint_torch_and_single_channel():
+    # reading R25: dw[co][ci][j] = sum_b sum_i dy[b][i][co] x[b][i+j][ci]
+    B, N, cin, cout, k = 2, 30, 5, 4, 3
+    L = N - k + 1
+    # adjoint identity on integers (exact in bf16 and double): <conv1d_mc(x, w), dy> = <w, dw>
+    x = synth.randint(112, B * N * cin, -5, 5).astype(np.float32).reshape(B, N, cin)
+    w = synth.randint(113, cout * cin * k, -3, 3).astype(np.float32).reshape(cout, cin, k)
+    dy = synth.randint(114, B * L * cout, -4, 4).astype(np.float32).reshape(B, L, cout)
+    xb, wb, gb = oracle.to_bf16_bits(x), oracle.to_bf16_bits(w), oracle.to_bf16_bits(dy)
+    y, _ = oracle.conv1d_mc(xb, wb)
+    dw, _ = oracle.conv1d_mc_backward_filter(gb, xb, k)
+    assert float((y * dy).sum()) == float((w.astype(np.float64) * dw).sum())
+    # torch float64 autograd (NCW), signed values; magnitude = the same VJP on |x|, |dy|
+    xf = synth.normal(115, B * N * cin).reshape(B, N, cin)
+    gf = synth.normal(116, B * L * cout).reshape(B, L, cout)
+    xb, gb = oracle.to_bf16_bits(xf), oracle.to_bf16_bits(gf)
+    dw, mag = oracle.conv1d_mc_backward_filter(gb, xb, k)
+    xt = torch.tensor(oracle.bf16_bits_to_f32(xb), dtype=torch.float64).permute(0, 2, 1)
+    gt = torch.tensor(oracle.bf16_bits_to_f32(gb), dtype=torch.float64).permute(0, 2, 1)
+    ref = torch.nn.grad.conv1d_weight(xt, (cout, cin, k), gt).numpy()
+    np.testing.assert_allclose(dw, ref, rtol=1e-12, atol=1e-12)
+    refm = torch.nn.grad.conv1d_weight(xt.abs(), (cout, cin, k), gt.abs()).numpy()
+    np.testing.assert_allclose(mag, refm, rtol=1e-12, atol=1e-12)
+    assert np.any(mag > np.abs(dw) + 1e-9)
+    # one channel each way: the single-channel filter gradient oracle
+    g1 = synth.normal(117, B * L).reshape(B, L, 1)
+    x1 = synth.normal(118, B * N).reshape(B, N, 1)
+    g1b, x1b = oracle.to_bf16_bits(g1), oracle.to_bf16_bits(x1)
+    dw1, _ = oracle.conv1d_mc_backward_filter(g1b, x1b, k)
+    ref1, _ = oracle.conv1d_backward_filter(oracle.bf16_bits_to_f32(x1b)[..., 0], oracle.bf16_bits_to_f32(g1b)[..., 0], k)
+    np.testing.assert_allclose(dw1[0, 0], ref1, rtol=1e-12, atol=1e-12)
