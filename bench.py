@@ -198,6 +198,13 @@ def cfg_cells(workload: str, cfg5_log2n: int = 32):
             wf = synth.normal(97, cout * cin * k, sigma=(cin * k) ** -0.5).reshape(cout, cin, k)
             cells.append(Cell("mc", f"mc_dx_c{cin}x{cout}_k{k}", "conv_mc_bwd_in", w=k, f=wf, inp=key, kh=cin,
                               kw=cout))
+        # its filter gradient (reading R25): dy [16][65536-k+1][cout] and x [16][65536][cin] -> dw
+        for cin, cout, k in ((64, 64, 3), (64, 128, 2)):
+            key = f"gmcf{cout}_k{k}"
+            inputs[key] = dict(rows=16, n=(65536 - k + 1) * cout, dtype="bfloat16", dist="normal", seed=99, kw={},
+                               shard="batch")
+            cells.append(Cell("mc", f"mc_dw_c{cin}x{cout}_k{k}", "conv_mc_bwd_f", w=k, inp=key, inp2=f"xmc{cin}",
+                              kh=cin, kw=cout))
         # multi-channel 2-D convolution (reading R22), NHWC bf16, ResNet-like layers; the image
         # shard's (C, H, W) slots hold (H, W, Cin) of the NHWC tensor
         for hw, cin, cout in ((56, 64, 64), (56, 64, 128)):
@@ -424,6 +431,18 @@ class Runner:
             c.bytes = rows * N * cin * 2 + c.n_out * 4 + cout * cin * k * 2
             c.flops = 2 * k * cin * c.n_out
             return torch.empty((rows, L, cout), dtype=torch.float32, device=self.device)
+        if c.op == "conv_mc_bwd_f":
+            rows, n = geo
+            cin, cout, k = c.kh, c.kw, c.w
+            L = n // cout
+            N = L + k - 1
+            need = self.ss.ss_conv1d_mc_backward_filter_workspace(cin, cout, k)
+            if c.name not in self.ws:
+                self.ws[c.name] = torch.empty(max(need, 8), dtype=torch.uint8, device=self.device)
+            c.n_out = rows * L * cout  # dy elements consumed (one window position each)
+            c.bytes = rows * L * cout * 2 + rows * N * cin * 2 + cout * cin * k * 4
+            c.flops = 2 * k * cin * cout * rows * L
+            return torch.empty((cout, cin, k), dtype=torch.float32, device=self.device)
         if c.op == "conv_mc_bwd_in":
             rows, n = geo
             cin, cout, k = c.kh, c.kw, c.w
@@ -604,6 +623,14 @@ class Runner:
             rows, n = geo
             ss.check(ss.ss_conv1d_mc(x.data_ptr(), self.wmc[c.name].data_ptr(), y.data_ptr(), rows,
                                      n // c.kh, c.kh, c.kw, c.w, self.stream.cuda_stream))
+        elif c.op == "conv_mc_bwd_f":
+            rows, n = geo
+            L = n // c.kw
+            xm = xd[c.inp2]
+            need = ss.ss_conv1d_mc_backward_filter_workspace(c.kh, c.kw, c.w)
+            ss.check(ss.ss_conv1d_mc_backward_filter(x.data_ptr(), xm.data_ptr(), y.data_ptr(), rows, L + c.w - 1,
+                                                     c.kh, c.kw, c.w, self.ws[c.name].data_ptr(), need,
+                                                     self.stream.cuda_stream))
         elif c.op == "conv_mc_bwd_in":
             rows, n = geo
             L = n // c.kw
@@ -1007,7 +1034,7 @@ def run_ours(args):
         d = {"cell": c.name, "avg_ms": round(avg_ms, 5), "n_out": c.n_out, "bytes": c.bytes,
              "gelem_s": round(c.n_out / (avg_ms * 1e-3) / 1e9, 2), "gbs": round(gbs, 1),
              "frac_hbm": round(gbs / peak_hbm, 4), "frac_8tbs": round(gbs / 8000.0, 4), "share": 0.0}
-        if c.op in ("conv_mc", "conv2d_mc", "conv_mc_bwd_in"):
+        if c.op in ("conv_mc", "conv2d_mc", "conv_mc_bwd_in", "conv_mc_bwd_f"):
             d["tc_frac"] = round(c.flops / (avg_ms * 1e-3) / 1e12 / (2 * tf32_peak_tflops()), 4)  # bf16 peak
         elif conv_on_tensor_cores(c):
             d["tc_frac"] = round(c.n_out * TC_FLOP_PER_OUT / (avg_ms * 1e-3) / 1e12 / tf32_peak_tflops(), 4)
@@ -1032,7 +1059,7 @@ def run_ours(args):
         roofline = {"bound": "hbm", "kernel": dom["cell"], "achieved": dom["gbs"], "peak": peak_hbm,
                     "unit": "GB/s", "frac": dom["frac_hbm"], "peak_source": peak_src, "traffic": None,
                     "frac_8tbs": dom["frac_8tbs"]}
-        if "tc_frac" in dom and dom_cell.op in ("conv_mc", "conv2d_mc", "conv_mc_bwd_in"):
+        if "tc_frac" in dom and dom_cell.op in ("conv_mc", "conv2d_mc", "conv_mc_bwd_in", "conv_mc_bwd_f"):
             roofline["tensor_frac"] = dom["tc_frac"]
             roofline["tensor_peak_tflops"] = round(2 * tf32_peak_tflops(), 1)
             roofline["tensor_note"] = "bf16 MMA work (2 k Cin flop/output) / measured dense bf16 peak"
@@ -1212,6 +1239,13 @@ def oracle_sample_plan(workload: str, frac: float):
             wb = oracle.to_bf16_bits(c.f)
             plan.append((c, _rows_task(xb, lambda xi, wb=wb: oracle.conv2d_mc(xi, wb),
                                        (hw - 2) * (hw - 2) * c.f.shape[0])))
+        elif c.cfg == "mc" and c.op == "conv_mc_bwd_f":
+            cin, cout, k = c.kh, c.kw, c.w
+            N = max(k + 1, int(16 * 65536 * frac))
+            gb = oracle.to_bf16_bits(synth.normal(99, (N - k + 1) * cout).reshape(1, N - k + 1, cout))
+            xb = oracle.to_bf16_bits(synth.normal(96, N * cin).reshape(1, N, cin))
+            plan.append((c, _whole_task(lambda gb=gb, xb=xb, k=k, N=N, cout=cout: (
+                oracle.conv1d_mc_backward_filter(gb, xb, k), (N - k + 1) * cout)[1])))
         elif c.cfg == "mc" and c.op == "conv_mc_bwd_in":
             cin, cout, k = c.kh, c.kw, c.w
             N = max(k + 1, int(16 * 65536 * frac))

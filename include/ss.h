@@ -70,7 +70,7 @@
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 10
+#define SS_ABI_VERSION 11
 
 typedef enum { SS_F32 = 0, SS_I32 = 1 } ss_dtype_t;
 typedef enum { SS_POOL_MAX = 0, SS_POOL_AVG = 1 } ss_pool_mode_t;
@@ -293,6 +293,24 @@ ss_status_t ss_conv2d_mc(const void* x, const void* w, float* y, int64_t batch, 
  * Statuses as ss_conv1d_mc (k > N -> SS_ERR_WINDOW_EXCEEDS_INPUT). */
 ss_status_t ss_conv1d_mc_backward_input(const void* dy, const void* w, float* dx, int64_t batch, int64_t N,
                                         int64_t cin, int64_t cout, int64_t k, void* stream);
+
+/* Filter gradient of ss_conv1d_mc (reading R25):
+ *   dw[co][ci][j] = sum_b sum_{i < N-k+1} dy[b][i][co] * x[b][i+j][ci].
+ * dy is [batch][N-k+1][cout] bfloat16, x the forward's [batch][N][cin] bfloat16, dw
+ * [cout][cin][k] fp32 (torch weight order), fully overwritten; all DEVICE memory.
+ * cin = 64 with cout = 64 (k <= 4) or 128 (k <= 2) and 16-B aligned dy / x run on the
+ * tensor cores: per tile of 128 positions D[co][(j, ci)] += dy^T . x shifted by j rows
+ * (both operands read MN-major straight from the activations), fp32 per tile, fp32 runs
+ * of 16 tiles, fp64 beyond; `workspace` (DEVICE, caller-owned, 8-B aligned, >=
+ * ss_conv1d_mc_backward_filter_workspace(cin, cout, k) bytes on the current device)
+ * holds per-CTA fp64 partials summed in CTA order -- deterministic.  Other shapes run
+ * a direct kernel (products and sums in double; the workspace size is then 0 and
+ * `workspace` may be NULL).  Tolerance 1e-5 * sum|terms| + 1e-6.  Statuses as
+ * ss_conv1d_mc; a short workspace -> SS_ERR_BAD_SIZE. */
+size_t ss_conv1d_mc_backward_filter_workspace(int64_t cin, int64_t cout, int64_t k);
+ss_status_t ss_conv1d_mc_backward_filter(const void* dy, const void* x, float* dw, int64_t batch, int64_t N,
+                                         int64_t cin, int64_t cout, int64_t k, void* workspace,
+                                         size_t workspace_bytes, void* stream);
 
 /* ---- backward passes (training) ----------
  * Vector-Jacobian products of the forward calls above (DESIGN.md reading

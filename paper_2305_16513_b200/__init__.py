@@ -45,7 +45,8 @@ EXPORTED = ("ss_abi_version", "ss_out_len", "ss_pool_sum", "ss_pool_max", "ss_po
             "ss_affine_window", "ss_pool_sum_backward", "ss_pool_max_backward",
             "ss_conv1d_backward_input", "ss_conv1d_backward_filter_workspace", "ss_conv1d_backward_filter",
             "ss_pool2d_backward", "ss_conv2d", "ss_conv2d_backward_input", "ss_conv2d_backward_filter_workspace",
-            "ss_conv2d_backward_filter", "ss_conv1d_mc", "ss_conv2d_mc", "ss_conv1d_mc_backward_input")
+            "ss_conv2d_backward_filter", "ss_conv1d_mc", "ss_conv2d_mc", "ss_conv1d_mc_backward_input",
+            "ss_conv1d_mc_backward_filter_workspace", "ss_conv1d_mc_backward_filter")
 
 
 class SSError(RuntimeError):
@@ -101,6 +102,10 @@ def _load() -> ctypes.CDLL:
     L.ss_conv2d_mc.restype = i32
     L.ss_conv1d_mc_backward_input.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, vp]
     L.ss_conv1d_mc_backward_input.restype = i32
+    L.ss_conv1d_mc_backward_filter_workspace.argtypes = [i64, i64, i64]
+    L.ss_conv1d_mc_backward_filter_workspace.restype = ctypes.c_size_t
+    L.ss_conv1d_mc_backward_filter.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, vp, ctypes.c_size_t, vp]
+    L.ss_conv1d_mc_backward_filter.restype = i32
     L.ss_conv2d.restype = i32
     L.ss_conv2d_backward_input.argtypes = [vp, vp, i64, i64, i64, ctypes.POINTER(ctypes.c_float), i64, i64, i64, i64,
                                            i32, vp]
@@ -261,6 +266,14 @@ def ss_conv2d_mc(x_ptr, w_ptr, y_ptr, batch, H, W, cin, cout, kh, kw, stream=0) 
 
 def ss_conv1d_mc_backward_input(dy_ptr, w_ptr, dx_ptr, batch, N, cin, cout, k, stream=0) -> int:
     return _lib.ss_conv1d_mc_backward_input(dy_ptr, w_ptr, dx_ptr, batch, N, cin, cout, k, stream)
+
+
+def ss_conv1d_mc_backward_filter_workspace(cin, cout, k) -> int:
+    return _lib.ss_conv1d_mc_backward_filter_workspace(cin, cout, k)
+
+
+def ss_conv1d_mc_backward_filter(dy_ptr, x_ptr, dw_ptr, batch, N, cin, cout, k, ws_ptr, ws_bytes, stream=0) -> int:
+    return _lib.ss_conv1d_mc_backward_filter(dy_ptr, x_ptr, dw_ptr, batch, N, cin, cout, k, ws_ptr, ws_bytes, stream)
 
 
 def check(status: int) -> None:
@@ -658,3 +671,28 @@ def conv1d_mc_backward_input(dy, w, N, out=None, stream=None):
     check(ss_conv1d_mc_backward_input(dy.data_ptr(), w.data_ptr(), dx.data_ptr(), B, N, cin, cout, k,
                                       _stream(stream)))
     return dx
+
+
+def conv1d_mc_backward_filter(dy, x, k, out=None, workspace=None, stream=None):
+    """Filter gradient of conv1d_mc: dy [B, N-k+1, Cout] and x [B, N, Cin] bfloat16 (CUDA) -> dw
+    [Cout, Cin, k] float32 (torch conv1d weight order).  `workspace`: optional preallocated uint8 CUDA
+    tensor of at least ss_conv1d_mc_backward_filter_workspace(Cin, Cout, k) bytes."""
+    torch = _torch()
+    _dev(dy, "dy", torch.bfloat16)
+    _dev(x, "x", torch.bfloat16, device=dy.device)
+    if dy.dim() != 3 or x.dim() != 3:
+        raise ValueError("dy must be [B, N-k+1, Cout] and x [B, N, Cin]")
+    B, L, cout = dy.shape
+    B2, N, cin = x.shape
+    if B2 != B:
+        raise ValueError("dy and x batch sizes differ")
+    if k > N:
+        raise SSError(SS_ERR_WINDOW_EXCEEDS_INPUT, f"window exceeds input: k={k} > N={N}")
+    if L != N - k + 1:
+        raise ValueError(f"dy has {L} positions, expected N-k+1 = {N - k + 1}")
+    dw = _alloc(out, (cout, cin, k), torch.float32, dy.device)
+    need = ss_conv1d_mc_backward_filter_workspace(cin, cout, k)
+    ws = _workspace(workspace, need, dy.device) if need else None
+    check(ss_conv1d_mc_backward_filter(dy.data_ptr(), x.data_ptr(), dw.data_ptr(), B, N, cin, cout, k,
+                                       ws.data_ptr() if ws is not None else 0, need, _stream(stream)))
+    return dw

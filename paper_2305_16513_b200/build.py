@@ -10,7 +10,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libss.so")
-SOURCES = ["api.cu", "slide1d.cu", "generic.cu", "pool2d.cu", "affine.cu", "conv_tc.cu", "backward.cu", "dilated.cu", "conv2d.cu", "conv2d_backward.cu", "conv_mc.cu", "conv2d_tile.cu", "maxbwd.cu", "fgrad_tc.cu"]
+SOURCES = ["api.cu", "slide1d.cu", "generic.cu", "pool2d.cu", "affine.cu", "conv_tc.cu", "backward.cu", "dilated.cu", "conv2d.cu", "conv2d_backward.cu", "conv_mc.cu", "conv2d_tile.cu", "maxbwd.cu", "fgrad_tc.cu", "mc_fgrad.cu"]
 HEADERS = ["ss_device.cuh", "ss_internal.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

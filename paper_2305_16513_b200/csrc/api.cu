@@ -829,6 +829,46 @@ ss_status_t ss_conv1d_mc_backward_input(const void* dy, const void* w, float* dx
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv1d_mc_backward_input launch");
 }
 
+size_t ss_conv1d_mc_backward_filter_workspace(int64_t cin, int64_t cout, int64_t k) {
+  return mc_filter_grad_workspace(cin, cout, k, current_sms());
+}
+
+ss_status_t ss_conv1d_mc_backward_filter(const void* dy, const void* x, float* dw, int64_t batch, int64_t N,
+                                         int64_t cin, int64_t cout, int64_t k, void* workspace,
+                                         size_t workspace_bytes, void* stream) {
+  if (!dy || !x || !dw) return fail(SS_ERR_NULL, "dy, x and dw must be non-NULL device pointers");
+  if (batch < 1 || N < 1 || cin < 1 || cout < 1 || k < 1)
+    return fail(SS_ERR_BAD_SIZE, "batch/N/cin/cout/k must all be >= 1");
+  if (N > INT64_MAX / 8 / batch / cin || N > INT64_MAX / 8 / batch / cout || k > INT64_MAX / 8 / cin / cout)
+    return fail(SS_ERR_BAD_SIZE, "sizes overflow int64");
+  if (k > N) return fail(SS_ERR_WINDOW_EXCEEDS_INPUT, "window exceeds input: k=%lld > N=%lld", (long long)k,
+                         (long long)N);
+  if ((reinterpret_cast<uintptr_t>(dy) & 1) || (reinterpret_cast<uintptr_t>(x) & 1) ||
+      (reinterpret_cast<uintptr_t>(dw) & 3))
+    return fail(SS_ERR_BAD_SIZE, "dy / x must be 2-byte and dw 4-byte aligned");
+  const int64_t L = N - k + 1;
+  const int sms = current_sms();
+  const size_t need = mc_filter_grad_workspace(cin, cout, k, sms);
+  if (need && (!workspace || workspace_bytes < need))
+    return fail(SS_ERR_BAD_SIZE, "workspace of %zu bytes needed (ss_conv1d_mc_backward_filter_workspace)", need);
+  const int64_t nw = cout * cin * k * 4;
+  if (overlaps(dw, nw, dy, batch * L * cout * 2) || overlaps(dw, nw, x, batch * N * cin * 2) ||
+      (need && (overlaps(workspace, (int64_t)need, dy, batch * L * cout * 2) ||
+                overlaps(workspace, (int64_t)need, x, batch * N * cin * 2) || overlaps(workspace, (int64_t)need, dw, nw))))
+    return fail(SS_ERR_OVERLAP, "dw / workspace overlap an input");
+  McFgradParams p;
+  memset(&p, 0, sizeof p);
+  p.dy = static_cast<const uint16_t*>(dy); p.x = static_cast<const uint16_t*>(x); p.dw = dw;
+  p.ws = static_cast<double*>(workspace);
+  p.batch = batch; p.N = N; p.L = L; p.cin = cin; p.cout = cout; p.k = k;
+  const bool tc = need && (reinterpret_cast<uintptr_t>(dy) & 15) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(workspace) & 7) == 0 &&
+                  encode_mc_map_batched(&p.tm_dy, dy, batch, L, cout, 128) &&
+                  encode_mc_map_batched(&p.tm_x, x, batch, N, cin, 136);
+  cudaError_t e = launch_mc_filter_grad(p, tc, static_cast<cudaStream_t>(stream), sms);
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv1d_mc_backward_filter launch");
+}
+
 ss_status_t ss_conv2d_mc(const void* x, const void* w, float* y, int64_t batch, int64_t H, int64_t W, int64_t cin,
                          int64_t cout, int64_t kh, int64_t kw, void* stream) {
   if (!x || !w || !y) return fail(SS_ERR_NULL, "x, w and y must be non-NULL device pointers");

@@ -1,0 +1,309 @@
+// mc_fgrad.cu -- filter gradient of the multi-channel 1-D convolution (SURVEY 8f
+// NEXT #4, training; reading R25):
+//   dw[co][ci][j] = sum_b sum_{i < N-k+1} dy[b][i][co] * x[b][i+j][ci]
+// dy [batch][N-k+1][cout] and x [batch][N][cin] bfloat16 (channels-last), dw
+// [cout][cin][k] fp32.
+//
+// As a matrix product per tile of 128 positions of one row:
+//   D[co][(j, ci)] += sum_{p < 128} dy[p][co] * x[p + j][ci]
+// M = cout, N = k x 64 (cin = 64), K = positions.  Both operands are the
+// activations as they lie in memory, read MN-major (channels contiguous):
+// A = the dy tile (K row p = dy[p][0..cout)), B for tap j = the x tile read j K
+// rows further down (descriptor start + 128 j bytes; the same row-shift trick as
+// the forward), so no im2col and no transposes.  bf16 products are exact; the
+// tensor memory accumulates one tile (128 positions, fp32), the epilogue adds the
+// tile into an fp32 run accumulator in shared memory (16 tiles per run), and each
+// run is added into this CTA's fp64 slice of the caller's workspace; a finish
+// kernel sums the slices in CTA order.  |error| <= (128 + 16) fp32 roundings of
+// partial sums bounded by sum |terms| (~8.6e-6 of it) -- inside the 1e-5 bound.
+//
+// Roles (320 threads, one CTA per SM): warp 0 TMA producer (dy tile + x tile of
+// 136 rows per stage, 3 stages), warp 1 MMA issuer (8 K-steps, one N = 64 k MMA each:
+// tap j is B's MN atom j = the x tile j rows down, an atom stride of 128 B), warps
+// 2-9 epilogue (two per TMEM lane quarter, half the columns each; for cout = 64 the M = 64 accumulator
+// occupies lanes 0-15 of each quarter: tools/ubench/tc_m64_probe.cu).
+#include <cstdint>
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "ss_device.cuh"
+#include "ss_internal.h"
+
+namespace ss {
+
+namespace {
+
+constexpr int kMfThreads = 320;
+constexpr int kMfStages = 3;
+constexpr int kMfTileP = 128;                      // positions per tile
+constexpr int kMfXRows = 136;                      // x rows per tile (128 + k - 1 <= 131, 17 atoms)
+constexpr uint32_t kMfXBytes = kMfXRows * 128u;
+constexpr int kMfRunTiles = 32;                    // tiles per fp32 run
+
+__device__ __forceinline__ uint64_t mf_desc(uint32_t saddr, uint32_t lbo) {  // MN-major bf16, SWIZZLE_128B
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((1024u >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+__host__ __device__ constexpr uint32_t mf_idesc(int M, int N) {  // bf16 x bf16 -> f32, A and B MN-major
+  return (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mf_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mf_commit(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mf_wait(uint64_t* bar, uint32_t parity) {  // polls (commit-driven phases)
+  asm volatile(
+      "{\n\t.reg .pred p;\nMF_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra MF_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mf_tma_4d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2,
+                                          int32_t c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mf_ld32(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
+}
+
+template <int COUT>
+constexpr size_t mf_smem(int k) {
+  return 1024 + (size_t)kMfStages * ((COUT / 64) * 16384u + kMfXBytes) + (size_t)COUT * (64 * k + 4) * 4 + 256;
+}
+
+}  // namespace
+
+template <int COUT>
+__global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const __grid_constant__ McFgradParams p) {
+  constexpr int AT = COUT / 64;  // dy atoms (64 channels each)
+  constexpr uint32_t kDyBytes = AT * 16384u;
+  constexpr uint32_t kStage = kDyBytes + kMfXBytes;
+  extern __shared__ __align__(16) uint8_t mf_raw[];
+  uint8_t* smem = mf_raw + ((1024u - (smem_u32(mf_raw) & 1023u)) & 1023u);
+  const int k = (int)p.k, NC = 64 * k;  // accumulator columns (tap j at 64 j)
+  float* R = reinterpret_cast<float*>(smem + kMfStages * kStage);  // [COUT][NC + 4] fp32 run accumulators (16-B rows, 4-word skew)
+  uint64_t* full = reinterpret_cast<uint64_t*>(R + COUT * (NC + 4) + 4);
+  full = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(full) + 7) & ~uintptr_t(7));
+  uint64_t* empty = full + kMfStages;
+  uint64_t* dfull = empty + kMfStages;
+  uint64_t* dempty = dfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = p.ntiles, tpr = p.tiles_per_row;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMfStages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(dfull + s, 1); mbar_init(dempty + s, 8); }
+    fence_mbar_init();
+    prefetch_tmap(&p.tm_dy);
+    prefetch_tmap(&p.tm_x);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int s = it % kMfStages;
+        mf_wait(empty + s, ((uint32_t)(it / kMfStages) & 1u) ^ 1u);  // commit-driven: poll
+        const int64_t b = tile / tpr;
+        const int32_t t0 = (int32_t)((tile - b * tpr) * kMfTileP);
+        uint8_t* st = smem + (size_t)s * kStage;
+        mbar_arrive_expect_tx(full + s, kStage);
+#pragma unroll
+        for (int a = 0; a < AT; ++a) mf_tma_4d(st + a * 16384u, &p.tm_dy, 0, t0, a, (int32_t)b, full + s);
+        mf_tma_4d(st + kDyBytes, &p.tm_x, 0, t0, 0, (int32_t)b, full + s);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    // one MMA per K-step covers every tap: B's MN atom j is the x tile j K rows further down, i.e. an
+    // atom stride (LBO) of one 128-B row (tools/ubench/tc_lbo_probe.cu), N = 64 k
+    const uint32_t idesc = mf_idesc(COUT, NC);
+    const uint32_t s0 = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
+    int it = 0, d = 0;
+    uint32_t dph = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int s = it % kMfStages;
+      mf_wait(full + s, (uint32_t)(it / kMfStages) & 1u);
+      mf_wait(dempty + d, dph ^ 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t dyT = s0 + (uint32_t)s * kStage, xT = dyT + kDyBytes;
+      const uint32_t dcol = tmem + (uint32_t)(d * NC);
+#pragma unroll 1
+      for (int ks = 0; ks < kMfTileP / 16; ++ks) {
+        mf_mma(dcol, mf_desc(dyT + 2048u * ks, 16384u), mf_desc(xT + 128u * (16 * ks), 128u), idesc, ks > 0 ? 1u : 0u);
+      }
+      mf_commit(empty + s);
+      mf_commit(dfull + d);
+      if (++d == 2) { d = 0; dph ^= 1u; }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue: tile -> fp32 run -> fp64 slice
+    const int q = warp & 3, hh = (warp - 2) >> 2;  // lane quarter; half of the columns (two warps per quarter)
+    const int co = COUT == 128 ? 32 * q + lane : 16 * q + lane;  // M = 64: lanes 0-15 of each quarter
+    const int cb = hh * (NC / 2), ce = cb + NC / 2;
+    const uint32_t lanebits = (uint32_t)(32 * q) << 16;
+    float* Rr = R + (size_t)co * (NC + 4);
+    double* W = p.ws + (size_t)blockIdx.x * COUT * NC;  // this CTA's fp64 slice [COUT][NC]
+    const int e = threadIdx.x - 64;                     // 0 .. 255: cooperative, coalesced slice updates
+    for (int i = e; i < COUT * NC; i += 256) { R[(i / NC) * (NC + 4) + i % NC] = 0.0f; W[i] = 0.0; }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    int d = 0, nt = 0;
+    uint32_t dph = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      mf_wait(dfull + d, dph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+      // 32x32b: lane = row co, 32 consecutive columns (for M = 64 only lanes 0-15 of the quarter are
+      // rows: 16x256b reads with every lane useful measured slower, 117 vs 105 us)
+      for (int c0 = cb; c0 < ce; c0 += 32) {
+        uint32_t v[32];
+        mf_ld32(tmem + lanebits + (uint32_t)(d * NC + c0), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (COUT == 128 || lane < 16) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {  // float4: rows are 16-B aligned, the 4-word skew spreads banks
+            float4* r4 = reinterpret_cast<float4*>(Rr + c0 + i);
+            float4 t = *r4;
+            t.x += __uint_as_float(v[i]); t.y += __uint_as_float(v[i + 1]);
+            t.z += __uint_as_float(v[i + 2]); t.w += __uint_as_float(v[i + 3]);
+            *r4 = t;
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dempty + d);
+      if (++nt == kMfRunTiles || tile + gridDim.x >= ntiles) {  // end of a run: into the fp64 slice
+        nt = 0;
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // every row's run is complete
+#pragma unroll 4
+        for (int i = e; i < COUT * NC; i += 256) {
+          float* r = R + (i / NC) * (NC + 4) + i % NC;
+          W[i] += (double)*r;
+          *r = 0.0f;
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+      }
+      if (++d == 2) { d = 0; dph ^= 1u; }
+    }
+    // CTAs past the last tile leave their slice at zero (written above)
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// dw[co][ci][j] = sum over CTA slices c (in order) of ws[c][co][64 j + ci]
+__global__ void mc_filter_grad_finish(const double* __restrict__ ws, int ctas, int64_t cout, int64_t k,
+                                      float* __restrict__ dw) {
+  const int64_t total = cout * 64 * k;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = o % k, ci = (o / k) % 64, co = o / (64 * k);
+    double s = 0.0;
+    for (int c = 0; c < ctas; ++c) s += ws[((size_t)c * cout + co) * (64 * k) + 64 * j + ci];
+    dw[o] = (float)s;
+  }
+}
+
+// Direct kernel (any shape): one block per output element, positions strided over the threads,
+// products and sums in double, fixed-order block reduction.
+__global__ void __launch_bounds__(256) mc_filter_grad_direct_kernel(const __grid_constant__ McFgradParams p) {
+  __shared__ double red[256];
+  const uint16_t* __restrict__ dy = p.dy;
+  const uint16_t* __restrict__ x = p.x;
+  const int64_t total = p.cout * p.cin * p.k, npos = p.batch * p.L;
+  for (int64_t o = blockIdx.x; o < total; o += gridDim.x) {
+    const int64_t j = o % p.k, ci = (o / p.k) % p.cin, co = o / (p.k * p.cin);
+    double s = 0.0;
+    for (int64_t e = threadIdx.x; e < npos; e += blockDim.x) {
+      const int64_t b = e / p.L, i = e - b * p.L;
+      const float g = __uint_as_float((uint32_t)__ldg(dy + e * p.cout + co) << 16);
+      const float xv = __uint_as_float((uint32_t)__ldg(x + (b * p.N + i + j) * p.cin + ci) << 16);
+      s += (double)g * (double)xv;
+    }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+      if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) p.dw[o] = (float)red[0];
+    __syncthreads();
+  }
+}
+
+bool mc_filter_grad_tc_supported(int64_t cin, int64_t cout, int64_t k) {
+  return cin == 64 && ((cout == 64 && k <= 4) || (cout == 128 && k <= 2)) && k >= 1;
+}
+
+size_t mc_filter_grad_workspace(int64_t cin, int64_t cout, int64_t k, int sms) {
+  if (!mc_filter_grad_tc_supported(cin, cout, k)) return 0;
+  return (size_t)sms * cout * 64 * k * sizeof(double);
+}
+
+cudaError_t launch_mc_filter_grad(McFgradParams& p, bool tc, cudaStream_t stream, int sms) {
+  if (tc) {
+    p.tiles_per_row = (p.L + kMfTileP - 1) / kMfTileP;
+    p.ntiles = p.batch * p.tiles_per_row;
+    const int ctas = sms;
+    const void* kfn = p.cout == 128 ? reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<128>)
+                                    : reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<64>);
+    const size_t smem = p.cout == 128 ? mf_smem<128>((int)p.k) : mf_smem<64>((int)p.k);
+    if (smem > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
+    cudaError_t e = ensure_smem_attr(kfn);
+    if (e != cudaSuccess) return e;
+    void* args[] = {&p};
+    e = cudaLaunchKernel(kfn, dim3((unsigned)ctas), dim3(kMfThreads), args, smem, stream);
+    note_launch();
+    if (e != cudaSuccess) return e;
+    const int64_t total = p.cout * 64 * p.k;
+    mc_filter_grad_finish<<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(p.ws, ctas, p.cout, p.k, p.dw);
+    note_launch();
+    return cudaGetLastError();
+  }
+  const int64_t total = p.cout * p.cin * p.k;
+  const int64_t g = total < (int64_t)sms * 32 ? total : (int64_t)sms * 32;
+  mc_filter_grad_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace ss

@@ -288,6 +288,20 @@ bool encode_mc_map(CUtensorMap* m, const void* x, int64_t positions, int64_t cin
 bool encode_mc_map_batched(CUtensorMap* m, const void* x, int64_t batch, int64_t positions, int64_t cin,
                            int box_rows);
 cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t stream, int sms);
+// Multi-channel conv1d filter gradient (mc_fgrad.cu; reading R25): tensor cores for cin = 64,
+// cout 64 (k <= 4) / 128 (k <= 2), else a direct kernel.  ws: per-CTA fp64 slices [sms][cout][64 k].
+struct alignas(64) McFgradParams {
+  CUtensorMap tm_dy, tm_x;  // batched maps: dy {64, L, cout/64, batch} box 128 rows, x {64, N, 1, batch} box 136
+  const uint16_t* dy;
+  const uint16_t* x;
+  float* dw;
+  double* ws;
+  int64_t batch, N, L, cin, cout, k;
+  int64_t tiles_per_row, ntiles;  // set by the launcher
+};
+bool mc_filter_grad_tc_supported(int64_t cin, int64_t cout, int64_t k);
+size_t mc_filter_grad_workspace(int64_t cin, int64_t cout, int64_t k, int sms);
+cudaError_t launch_mc_filter_grad(McFgradParams& p, bool tc, cudaStream_t stream, int sms);
 // Staged rows as the TMA boxes round them: multiple of 8, split into <= 256-row boxes of equal size
 inline int mc_round_rows(int rows, int* nbox = nullptr, int* box_rows = nullptr) {
   rows = (rows + 7) / 8 * 8;
