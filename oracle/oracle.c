@@ -713,3 +713,38 @@ int oracle_conv1d_mc_backward_filter_bf16(const uint16_t* dy, const uint16_t* x,
       }
   return 0;
 }
+
+/* Input gradient of the multi-channel 2-D convolution (reading R26: the
+ * vector-Jacobian product of reading R22), bf16 dy and weights, NHWC:
+ *   y[b][r][c][co] = sum_{a,e,ci} w[co][ci][a][e] x[b][r+a][c+e][ci]
+ *   =>  dx[b][r+a][c+e][ci] += w[co][ci][a][e] * dy[b][r][c][co]
+ * dy [batch][H-kh+1][W-kw+1][cout], w [cout][cin][kh][kw], dx [batch][H][W][cin]
+ * (elements no window covers get 0); the scatter is accumulated in double in
+ * (r, c, a, e, co) order. */
+int oracle_conv2d_mc_backward_input_bf16(const uint16_t* dy, const uint16_t* w, int64_t batch, int64_t H, int64_t W,
+                                         int64_t cin, int64_t cout, int64_t kh, int64_t kw, double* dx,
+                                         double* absmag) {
+  if (dy == NULL || w == NULL || dx == NULL || batch < 1 || cin < 1 || cout < 1 || kh < 1 || kw < 1 || kh > H ||
+      kw > W)
+    return -1;
+  int64_t OH = H - kh + 1, OW = W - kw + 1;
+  for (int64_t t = 0; t < batch * H * W * cin; ++t) {
+    dx[t] = 0.0;
+    if (absmag) absmag[t] = 0.0;
+  }
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t r = 0; r < OH; ++r)
+      for (int64_t c = 0; c < OW; ++c)
+        for (int64_t a = 0; a < kh; ++a)
+          for (int64_t e = 0; e < kw; ++e)
+            for (int64_t co = 0; co < cout; ++co) {
+              double g = bf16_to_double(dy[((b * OH + r) * OW + c) * cout + co]);
+              for (int64_t ci = 0; ci < cin; ++ci) {
+                double p = bf16_to_double(w[((co * cin + ci) * kh + a) * kw + e]) * g;
+                int64_t o = ((b * H + r + a) * W + c + e) * cin + ci;
+                dx[o] += p;
+                if (absmag) absmag[o] += fabs(p);
+              }
+            }
+  return 0;
+}

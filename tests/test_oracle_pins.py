@@ -627,3 +627,32 @@ def test_conv1d_mc_backward_filter_adjoint_torch_and_single_channel():
     dw1, _ = oracle.conv1d_mc_backward_filter(g1b, x1b, k)
     ref1, _ = oracle.conv1d_backward_filter(oracle.bf16_bits_to_f32(x1b)[..., 0], oracle.bf16_bits_to_f32(g1b)[..., 0], k)
     np.testing.assert_allclose(dw1[0, 0], ref1, rtol=1e-12, atol=1e-12)
+
+
+def test_conv2d_mc_backward_input_adjoint_torch_and_1d_reduction():
+    # reading R26: dx[b][r+a][c+e][ci] += w[co][ci][a][e] dy[b][r][c][co]
+    B, H, W, cin, cout, kh, kw = 2, 7, 9, 3, 4, 3, 2
+    OH, OW = H - kh + 1, W - kw + 1
+    x = synth.randint(130, B * H * W * cin, -4, 4).astype(np.float32).reshape(B, H, W, cin)
+    w = synth.randint(131, cout * cin * kh * kw, -3, 3).astype(np.float32).reshape(cout, cin, kh, kw)
+    dy = synth.randint(132, B * OH * OW * cout, -4, 4).astype(np.float32).reshape(B, OH, OW, cout)
+    xb, wb, gb = oracle.to_bf16_bits(x), oracle.to_bf16_bits(w), oracle.to_bf16_bits(dy)
+    y, _ = oracle.conv2d_mc(xb, wb)
+    dx, _ = oracle.conv2d_mc_backward_input(gb, wb, H, W)
+    assert float((y * dy).sum()) == float((x.astype(np.float64) * dx).sum())  # adjoint, exact on integers
+    wf = synth.normal(133, cout * cin * kh * kw).reshape(cout, cin, kh, kw)
+    gf = synth.normal(134, B * OH * OW * cout).reshape(B, OH, OW, cout)
+    wb, gb = oracle.to_bf16_bits(wf), oracle.to_bf16_bits(gf)
+    dx, mag = oracle.conv2d_mc_backward_input(gb, wb, H, W)
+    wt = torch.tensor(oracle.bf16_bits_to_f32(wb), dtype=torch.float64)
+    gt = torch.tensor(oracle.bf16_bits_to_f32(gb), dtype=torch.float64).permute(0, 3, 1, 2)
+    ref = torch.nn.grad.conv2d_input((B, cin, H, W), wt, gt).permute(0, 2, 3, 1).numpy()
+    np.testing.assert_allclose(dx, ref, rtol=1e-12, atol=1e-12)
+    refm = torch.nn.grad.conv2d_input((B, cin, H, W), wt.abs(), gt.abs()).permute(0, 2, 3, 1).numpy()
+    np.testing.assert_allclose(mag, refm, rtol=1e-12, atol=1e-12)
+    # one image row (H = kh = 1): the 1-D multi-channel input gradient
+    g1 = oracle.to_bf16_bits(synth.normal(135, B * 1 * (W - 2) * cout).reshape(B, 1, W - 2, cout))
+    w1 = oracle.to_bf16_bits(synth.normal(136, cout * cin * 3).reshape(cout, cin, 1, 3))
+    dx2, _ = oracle.conv2d_mc_backward_input(g1, w1, 1, W)
+    dx1, _ = oracle.conv1d_mc_backward_input(g1[:, 0], w1[:, :, 0], W)
+    np.testing.assert_array_equal(dx2[:, 0], dx1)
