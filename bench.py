@@ -213,6 +213,11 @@ def cfg_cells(workload: str, cfg5_log2n: int = 32):
                                shard="image")
             wf = synth.normal(103, cout * cin * 9, sigma=(cin * 9) ** -0.5).reshape(cout, cin, 3, 3)
             cells.append(Cell("mc", f"mc2d_{hw}x{hw}_c{cin}x{cout}_3x3", "conv2d_mc", kh=3, kw=3, f=wf, inp=key))
+        # its input gradient (reading R26): dy [128][54][54][64] bf16 -> dx [128][56][56][64] fp32
+        inputs["g2mc56"] = dict(images=128, C=54, H=54, W=64, dtype="bfloat16", dist="normal", seed=104, kw={},
+                                shard="image")
+        wf = synth.normal(103, 64 * 64 * 9, sigma=(64 * 9) ** -0.5).reshape(64, 64, 3, 3)
+        cells.append(Cell("mc", "mc2d_dx_56x56_c64x64_3x3", "conv2d_mc_bwd_in", kh=3, kw=3, f=wf, inp="g2mc56"))
     if workload == "backward":  # backward passes on config-3 / config-4 shapes; not a BJ config
         inputs["xb"] = dict(rows=64, n=1 << 20, dtype="float32", dist="normal", seed=3, kw={}, shard="batch")
         for k in (7, 31, 63):
@@ -454,6 +459,16 @@ class Runner:
             c.bytes = rows * L * cout * 2 + c.n_out * 4 + cout * cin * k * 2
             c.flops = 2 * k * cout * c.n_out
             return torch.empty((rows, N, cin), dtype=torch.float32, device=self.device)
+        if c.op == "conv2d_mc_bwd_in":
+            B, OH, OW, cout = geo
+            cin = c.f.shape[1]
+            H, W = OH + c.kh - 1, OW + c.kw - 1
+            if c.name not in self.wmc:
+                self.wmc[c.name] = torch.from_numpy(c.f).to(self.device).to(torch.bfloat16).contiguous()
+            c.n_out = B * H * W * cin
+            c.bytes = B * OH * OW * cout * 2 + c.n_out * 4 + cout * cin * c.kh * c.kw * 2
+            c.flops = 2 * c.kh * c.kw * cout * c.n_out
+            return torch.empty((B, H, W, cin), dtype=torch.float32, device=self.device)
         if c.op == "conv2d_mc":
             B, H, W, cin = geo
             cout = c.f.shape[0]
@@ -636,6 +651,11 @@ class Runner:
             L = n // c.kw
             ss.check(ss.ss_conv1d_mc_backward_input(x.data_ptr(), self.wmc[c.name].data_ptr(), y.data_ptr(), rows,
                                                     L + c.w - 1, c.kh, c.kw, c.w, self.stream.cuda_stream))
+        elif c.op == "conv2d_mc_bwd_in":
+            B, OH, OW, cout = geo
+            ss.check(ss.ss_conv2d_mc_backward_input(x.data_ptr(), self.wmc[c.name].data_ptr(), y.data_ptr(), B,
+                                                    OH + c.kh - 1, OW + c.kw - 1, c.f.shape[1], cout, c.kh, c.kw,
+                                                    self.stream.cuda_stream))
         elif c.op == "conv2d_mc":
             B, H, W, cin = geo
             ss.check(ss.ss_conv2d_mc(x.data_ptr(), self.wmc[c.name].data_ptr(), y.data_ptr(), B, H, W, cin,
@@ -1034,7 +1054,7 @@ def run_ours(args):
         d = {"cell": c.name, "avg_ms": round(avg_ms, 5), "n_out": c.n_out, "bytes": c.bytes,
              "gelem_s": round(c.n_out / (avg_ms * 1e-3) / 1e9, 2), "gbs": round(gbs, 1),
              "frac_hbm": round(gbs / peak_hbm, 4), "frac_8tbs": round(gbs / 8000.0, 4), "share": 0.0}
-        if c.op in ("conv_mc", "conv2d_mc", "conv_mc_bwd_in", "conv_mc_bwd_f"):
+        if c.op in ("conv_mc", "conv2d_mc", "conv_mc_bwd_in", "conv_mc_bwd_f", "conv2d_mc_bwd_in"):
             d["tc_frac"] = round(c.flops / (avg_ms * 1e-3) / 1e12 / (2 * tf32_peak_tflops()), 4)  # bf16 peak
         elif conv_on_tensor_cores(c):
             d["tc_frac"] = round(c.n_out * TC_FLOP_PER_OUT / (avg_ms * 1e-3) / 1e12 / tf32_peak_tflops(), 4)
@@ -1059,7 +1079,8 @@ def run_ours(args):
         roofline = {"bound": "hbm", "kernel": dom["cell"], "achieved": dom["gbs"], "peak": peak_hbm,
                     "unit": "GB/s", "frac": dom["frac_hbm"], "peak_source": peak_src, "traffic": None,
                     "frac_8tbs": dom["frac_8tbs"]}
-        if "tc_frac" in dom and dom_cell.op in ("conv_mc", "conv2d_mc", "conv_mc_bwd_in", "conv_mc_bwd_f"):
+        if "tc_frac" in dom and dom_cell.op in ("conv_mc", "conv2d_mc", "conv_mc_bwd_in", "conv_mc_bwd_f",
+                                                "conv2d_mc_bwd_in"):
             roofline["tensor_frac"] = dom["tc_frac"]
             roofline["tensor_peak_tflops"] = round(2 * tf32_peak_tflops(), 1)
             roofline["tensor_note"] = "bf16 MMA work (2 k Cin flop/output) / measured dense bf16 peak"
@@ -1239,6 +1260,12 @@ def oracle_sample_plan(workload: str, frac: float):
             wb = oracle.to_bf16_bits(c.f)
             plan.append((c, _rows_task(xb, lambda xi, wb=wb: oracle.conv2d_mc(xi, wb),
                                        (hw - 2) * (hw - 2) * c.f.shape[0])))
+        elif c.cfg == "mc" and c.op == "conv2d_mc_bwd_in":
+            imgs = max(1, int(round(128 * frac)))
+            gb = oracle.to_bf16_bits(synth.normal(104, imgs * 54 * 54 * 64).reshape(imgs, 54, 54, 64))
+            wb = oracle.to_bf16_bits(c.f)
+            plan.append((c, _rows_task(gb, lambda gi, wb=wb: oracle.conv2d_mc_backward_input(gi, wb, 56, 56),
+                                       56 * 56 * 64)))
         elif c.cfg == "mc" and c.op == "conv_mc_bwd_f":
             cin, cout, k = c.kh, c.kw, c.w
             N = max(k + 1, int(16 * 65536 * frac))

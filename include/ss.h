@@ -70,7 +70,7 @@
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 11
+#define SS_ABI_VERSION 12
 
 typedef enum { SS_F32 = 0, SS_I32 = 1 } ss_dtype_t;
 typedef enum { SS_POOL_MAX = 0, SS_POOL_AVG = 1 } ss_pool_mode_t;
@@ -277,6 +277,22 @@ ss_status_t ss_conv1d_mc(const void* x, const void* w, float* y, int64_t batch, 
  * SS_ERR_WINDOW_EXCEEDS_INPUT). */
 ss_status_t ss_conv2d_mc(const void* x, const void* w, float* y, int64_t batch, int64_t H, int64_t W,
                          int64_t cin, int64_t cout, int64_t kh, int64_t kw, void* stream);
+
+/* Input gradient of ss_conv2d_mc (reading R26):
+ *   dx[b][r][c][ci] = sum_{a<kh} sum_{e<kw} sum_{co<cout} w[co][ci][a][e] * dy[b][r-a][c-e][co]
+ * for r < H, c < W, terms with (r-a, c-e) outside the H-kh+1 x W-kw+1 output
+ * absent.  dy is [batch][H-kh+1][W-kw+1][cout] bfloat16, w the forward's
+ * [cout][cin][kh][kw] bfloat16, dx [batch][H][W][cin] fp32, fully overwritten;
+ * all DEVICE memory, dx must not overlap dy or w.  It is the forward contraction
+ * on dy zero-padded by kh-1 rows and kw-1 columns on each side with the weights
+ * transposed and flipped: cin, cout in {64, 128}, kh*kw <= 64 and 16-B aligned
+ * dy / dx run on the tensor cores (tiles of R dx rows x Cw columns, staged as one
+ * 5-D TMA box per 64 channels whose zero fill is the padding, no padded copy);
+ * other shapes (or tilings that do not fit shared memory) run a direct kernel.
+ * bf16 products are exact, accumulation is fp32.  Statuses as ss_conv2d_mc
+ * (kh > H or kw > W -> SS_ERR_WINDOW_EXCEEDS_INPUT). */
+ss_status_t ss_conv2d_mc_backward_input(const void* dy, const void* w, float* dx, int64_t batch, int64_t H,
+                                        int64_t W, int64_t cin, int64_t cout, int64_t kh, int64_t kw, void* stream);
 
 /* Input gradient of ss_conv1d_mc (the vector-Jacobian product of the channel-summed
  * sliding dot product; reading R23):

@@ -46,7 +46,8 @@ EXPORTED = ("ss_abi_version", "ss_out_len", "ss_pool_sum", "ss_pool_max", "ss_po
             "ss_conv1d_backward_input", "ss_conv1d_backward_filter_workspace", "ss_conv1d_backward_filter",
             "ss_pool2d_backward", "ss_conv2d", "ss_conv2d_backward_input", "ss_conv2d_backward_filter_workspace",
             "ss_conv2d_backward_filter", "ss_conv1d_mc", "ss_conv2d_mc", "ss_conv1d_mc_backward_input",
-            "ss_conv1d_mc_backward_filter_workspace", "ss_conv1d_mc_backward_filter")
+            "ss_conv1d_mc_backward_filter_workspace", "ss_conv1d_mc_backward_filter",
+            "ss_conv2d_mc_backward_input")
 
 
 class SSError(RuntimeError):
@@ -102,6 +103,8 @@ def _load() -> ctypes.CDLL:
     L.ss_conv2d_mc.restype = i32
     L.ss_conv1d_mc_backward_input.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, vp]
     L.ss_conv1d_mc_backward_input.restype = i32
+    L.ss_conv2d_mc_backward_input.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i64, vp]
+    L.ss_conv2d_mc_backward_input.restype = i32
     L.ss_conv1d_mc_backward_filter_workspace.argtypes = [i64, i64, i64]
     L.ss_conv1d_mc_backward_filter_workspace.restype = ctypes.c_size_t
     L.ss_conv1d_mc_backward_filter.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, vp, ctypes.c_size_t, vp]
@@ -266,6 +269,10 @@ def ss_conv2d_mc(x_ptr, w_ptr, y_ptr, batch, H, W, cin, cout, kh, kw, stream=0) 
 
 def ss_conv1d_mc_backward_input(dy_ptr, w_ptr, dx_ptr, batch, N, cin, cout, k, stream=0) -> int:
     return _lib.ss_conv1d_mc_backward_input(dy_ptr, w_ptr, dx_ptr, batch, N, cin, cout, k, stream)
+
+
+def ss_conv2d_mc_backward_input(dy_ptr, w_ptr, dx_ptr, batch, H, W, cin, cout, kh, kw, stream=0) -> int:
+    return _lib.ss_conv2d_mc_backward_input(dy_ptr, w_ptr, dx_ptr, batch, H, W, cin, cout, kh, kw, stream)
 
 
 def ss_conv1d_mc_backward_filter_workspace(cin, cout, k) -> int:
@@ -669,6 +676,28 @@ def conv1d_mc_backward_input(dy, w, N, out=None, stream=None):
         raise ValueError(f"dy has {L} positions, expected N-k+1 = {N - k + 1}")
     dx = _alloc(out, (B, N, cin), torch.float32, dy.device)
     check(ss_conv1d_mc_backward_input(dy.data_ptr(), w.data_ptr(), dx.data_ptr(), B, N, cin, cout, k,
+                                      _stream(stream)))
+    return dx
+
+
+def conv2d_mc_backward_input(dy, w, H, W, out=None, stream=None):
+    """Input gradient of conv2d_mc: dy [B, H-kh+1, W-kw+1, Cout] bfloat16 (CUDA), w [Cout, Cin, kh, kw]
+    bfloat16 (CUDA, the forward's weights) -> dx [B, H, W, Cin] float32."""
+    torch = _torch()
+    _dev(dy, "dy", torch.bfloat16)
+    _dev(w, "w", torch.bfloat16, device=dy.device)
+    if dy.dim() != 4 or w.dim() != 4:
+        raise ValueError("dy must be [B, H-kh+1, W-kw+1, Cout] and w [Cout, Cin, kh, kw]")
+    B, OH, OW, cout = dy.shape
+    cout2, cin, kh, kw = w.shape
+    if cout2 != cout:
+        raise ValueError("w's Cout does not match dy")
+    if kh > H or kw > W:
+        raise SSError(SS_ERR_WINDOW_EXCEEDS_INPUT, f"window {kh}x{kw} exceeds input {H}x{W}")
+    if OH != H - kh + 1 or OW != W - kw + 1:
+        raise ValueError(f"dy is {OH}x{OW}, expected {H - kh + 1}x{W - kw + 1}")
+    dx = _alloc(out, (B, H, W, cin), torch.float32, dy.device)
+    check(ss_conv2d_mc_backward_input(dy.data_ptr(), w.data_ptr(), dx.data_ptr(), B, H, W, cin, cout, kh, kw,
                                       _stream(stream)))
     return dx
 

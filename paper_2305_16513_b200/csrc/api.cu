@@ -229,6 +229,24 @@ bool encode_mc_map_batched(CUtensorMap* m, const void* x, int64_t batch, int64_t
   return r == CUDA_SUCCESS;
 }
 
+// 5-D view of an NHWC bf16 image batch: {64 channels, OW, OH, c/64 atoms, batch}, box {64, box_w, box_h, 1, 1}
+// (pad2d staging: boxes start up to kh-1 rows / kw-1 columns outside the image, zero-filled).
+bool encode_mc_map_2d(CUtensorMap* m, const void* x, int64_t batch, int64_t OH, int64_t OW, int64_t c, int box_w,
+                      int box_h) {
+  auto enc = encode_fn();
+  if (!enc || batch < 1 || OH < 1 || OW < 1 || c % 64 || box_w < 1 || box_w > 256 || box_h < 1 || box_h > 256 ||
+      OH > (int64_t(1) << 31) || OW > (int64_t(1) << 31) || batch > (int64_t(1) << 31))
+    return false;
+  const int64_t at = c / 64;
+  cuuint64_t dims[5] = {64, (cuuint64_t)OW, (cuuint64_t)OH, (cuuint64_t)at, (cuuint64_t)batch};
+  cuuint64_t strides[4] = {(cuuint64_t)(c * 2), (cuuint64_t)(OW * c * 2), 128, (cuuint64_t)(OH * OW * c * 2)};
+  cuuint32_t box[5] = {64, (cuuint32_t)box_w, (cuuint32_t)box_h, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(x), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
 
 // Tensor-core conv selection: k in [tc_min_k, kConvTcMaxK] at stride 1 without
 // dilation (default 33: measured faster than the FFMA2 tile kernel for every
@@ -906,6 +924,40 @@ ss_status_t ss_conv2d_mc(const void* x, const void* w, float* y, int64_t batch, 
   p.clc = dynamic_tiles();
   cudaError_t e = launch_conv_mc(p, tc, static_cast<cudaStream_t>(stream), current_sms());
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv2d_mc launch");
+}
+
+ss_status_t ss_conv2d_mc_backward_input(const void* dy, const void* w, float* dx, int64_t batch, int64_t H,
+                                        int64_t W, int64_t cin, int64_t cout, int64_t kh, int64_t kw, void* stream) {
+  if (!dy || !w || !dx) return fail(SS_ERR_NULL, "dy, w and dx must be non-NULL device pointers");
+  if (batch < 1 || H < 1 || W < 1 || cin < 1 || cout < 1 || kh < 1 || kw < 1)
+    return fail(SS_ERR_BAD_SIZE, "batch/H/W/cin/cout/kh/kw must all be >= 1");
+  if (H > INT64_MAX / 8 / W || H * W > INT64_MAX / 8 / batch || batch * H * W > INT64_MAX / 8 / cin ||
+      batch * H * W > INT64_MAX / 8 / cout || kh * kw > INT64_MAX / 8 / cin / cout)
+    return fail(SS_ERR_BAD_SIZE, "sizes overflow int64");
+  if (kh > H || kw > W)
+    return fail(SS_ERR_WINDOW_EXCEEDS_INPUT, "window %lldx%lld exceeds input %lldx%lld", (long long)kh, (long long)kw,
+                (long long)H, (long long)W);
+  if ((reinterpret_cast<uintptr_t>(dy) & 1) || (reinterpret_cast<uintptr_t>(w) & 1) ||
+      (reinterpret_cast<uintptr_t>(dx) & 3))
+    return fail(SS_ERR_BAD_SIZE, "dy / w must be 2-byte and dx 4-byte aligned");
+  const int64_t OH = H - kh + 1, OW = W - kw + 1;
+  const int64_t dxbytes = batch * H * W * cin * 4;
+  if (overlaps(dy, batch * OH * OW * cout * 2, dx, dxbytes) || overlaps(w, cout * cin * kh * kw * 2, dx, dxbytes))
+    return fail(SS_ERR_OVERLAP, "dx overlaps an input");
+  // dx = the forward on dy zero-padded by (kh-1, kw-1) with the weights transposed and flipped (reading R26):
+  // tiles of R dx rows x Cw columns, each staged as one TMA box per atom that starts outside dy
+  ConvMcParams p;
+  memset(&p, 0, sizeof p);
+  p.x = dy; p.w = w; p.y = dx; p.batch = batch; p.cin = cout; p.cout = cin; p.k = kh * kw;
+  p.H = H; p.W = W; p.OH = OH; p.OW = OW; p.N = OH * OW; p.L = H * W;
+  p.pad2d = 1; p.bwd_in = 1; p.pd_kh = (int)(kh < 1024 ? kh : 1024); p.pd_kw = (int)(kw < 1024 ? kw : 1024);  // tc: kh kw <= 64
+  const bool tc = (cin == 64 || cin == 128) && (cout == 64 || cout == 128) && kh * kw <= kMcMaxTaps &&
+                  (reinterpret_cast<uintptr_t>(dy) & 15) == 0 && (reinterpret_cast<uintptr_t>(dx) & 15) == 0 &&
+                  H < (int64_t(1) << 31) && W < (int64_t(1) << 31) && conv_mc_plan_pad2d(p) &&
+                  encode_mc_map_2d(&p.tm_x, dy, batch, OH, OW, cout, p.pd_P, p.pd_R + (int)kh - 1);
+  p.clc = dynamic_tiles();
+  cudaError_t e = launch_conv_mc(p, tc, static_cast<cudaStream_t>(stream), current_sms());
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv2d_mc_backward_input launch");
 }
 
 ss_status_t ss_conv2d(const void* x, void* y, int64_t planes, int64_t H, int64_t W, const float* filter_host,

@@ -123,6 +123,15 @@ __device__ __forceinline__ void tma_load_4d_mc(void* smem_dst, const CUtensorMap
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_5d_mc(void* smem_dst, const CUtensorMap* map, int32_t c1, int32_t c2,
+                                               int32_t c3, int32_t c4, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+      : "memory");
+}
+
 }  // namespace
 
 template <int CIN, int COUT>
@@ -273,7 +282,13 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
         const int ts = it % kMcRing;
         mbar_wait(tempty + ts, ((uint32_t)(it / kMcRing) & 1u) ^ 1u);
         tring[3 * ts] = t < ntiles ? t : -1;
-        if (t < ntiles) {  // the tile's first position (row b0, position i0 in it): divisions here, off the epilogue
+        if (t < ntiles && p.pad2d) {  // dx rows r0.., columns c0..: global row b H + r0, packed c0 / valid extents
+          const int64_t per = p.pd_nrt * p.pd_nct, b = t / per, rem = t - b * per, rt = rem / p.pd_nct;
+          const int64_t r0 = rt * p.pd_R, c0 = (rem - rt * p.pd_nct) * p.pd_Cw;
+          const int64_t nr = p.H - r0 < p.pd_R ? p.H - r0 : p.pd_R, nc = p.W - c0 < p.pd_Cw ? p.W - c0 : p.pd_Cw;
+          tring[3 * ts + 1] = b * p.H + r0;
+          tring[3 * ts + 2] = (c0 << 18) | (nr << 9) | nc;
+        } else if (t < ntiles) {  // the tile's first position (row b0, position i0 in it): divisions here, off the epilogue
           const int64_t b0 = p.batched ? t / p.tiles_per_row : (t * TP) / p.N;
           tring[3 * ts + 1] = b0;
           tring[3 * ts + 2] = p.batched ? (t - b0 * p.tiles_per_row) * TP : t * TP - b0 * p.N;
@@ -284,8 +299,14 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
           mbar_arrive(full + s);
           break;
         }
-        mbar_arrive_expect_tx(full + s, kStage);
-        if (p.batched) {  // tile = 128 positions of one row, staged from `pad` positions earlier
+        mbar_arrive_expect_tx(full + s, p.pad2d ? (uint32_t)p.pd_tx : kStage);
+        if (p.pad2d) {  // one box per atom: (R + kh - 1) dy rows x P positions, kh-1 rows / kw-1 columns early
+          const int64_t per = p.pd_nrt * p.pd_nct, b = t / per, rem = t - b * per, rt = rem / p.pd_nct;
+          const int32_t r0 = (int32_t)(rt * p.pd_R), c0 = (int32_t)((rem - rt * p.pd_nct) * p.pd_Cw);
+          for (int a = 0; a < AT; ++a)
+            tma_load_5d_mc(xs + (size_t)s * kStage + (size_t)a * kAtomBytes, &p.tm_x, c0 - (p.pd_kw - 1),
+                           r0 - (p.pd_kh - 1), a, (int32_t)b, full + s);
+        } else if (p.batched) {  // tile = 128 positions of one row, staged from `pad` positions earlier
           const int64_t b = t / p.tiles_per_row;
           const int32_t t0 = (int32_t)((t - b * p.tiles_per_row) * TP) - p.pad;
           for (int a = 0; a < AT; ++a)
@@ -381,7 +402,12 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
             const int m = 128 * mb + 32 * q + 16 * lh + (lane >> 2) + 8 * rr;
             int64_t b = b0, i = i0 + m;
             int64_t o = -1;
-            if (p.batched) {
+            if (p.pad2d) {  // m = row P + col of the tile's staged grid
+              const uint32_t mu = (uint32_t)m;
+              const uint32_t r = (uint32_t)(((uint64_t)__umulhi(mu, p.w_magic) + mu) >> p.w_shift);
+              const uint32_t c = mu - r * (uint32_t)p.pd_P;
+              if (r < (uint32_t)((i0 >> 9) & 511) && c < (uint32_t)(i0 & 511)) o = (b0 + r) * p.W + (i0 >> 18) + c;
+            } else if (p.batched) {
               if (i < p.n_out) o = b * p.n_out + i;
             } else {
               while (i >= p.N) { i -= p.N; ++b; }
@@ -480,6 +506,33 @@ __global__ void __launch_bounds__(256) conv_mc_bwd_direct_kernel(const __grid_co
   }
 }
 
+// 2-D input gradient, direct: dx[b][r][c][ci] = sum_{a,e,co} w[co][ci][a][e] dy[b][r-a][c-e][co] (p.cin = C_out
+// dy channels, p.cout = C_in dx channels; H x W = dx, OH x OW = dy), fp32 accumulation in (a, e, co) order.
+__global__ void __launch_bounds__(256) conv2d_mc_bwd_direct_kernel(const __grid_constant__ ConvMcParams p) {
+  const uint16_t* __restrict__ dy = static_cast<const uint16_t*>(p.x);
+  const uint16_t* __restrict__ w = static_cast<const uint16_t*>(p.w);
+  const int64_t kh = p.H - p.OH + 1, kw = p.W - p.OW + 1;
+  const int64_t total = p.batch * p.H * p.W * p.cout;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ci = o % p.cout, pix = o / p.cout, c = pix % p.W, rb = pix / p.W, r = rb % p.H, b = rb / p.H;
+    float acc = 0.0f;
+    for (int64_t a = 0; a < kh; ++a) {
+      const int64_t rr = r - a;
+      if (rr < 0 || rr >= p.OH) continue;
+      for (int64_t e = 0; e < kw; ++e) {
+        const int64_t cc = c - e;
+        if (cc < 0 || cc >= p.OW) continue;
+        for (int64_t co = 0; co < p.cin; ++co) {
+          const float gv = __uint_as_float((uint32_t)__ldg(dy + ((b * p.OH + rr) * p.OW + cc) * p.cin + co) << 16);
+          const float wv = __uint_as_float((uint32_t)__ldg(w + ((co * p.cout + ci) * kh + a) * kw + e) << 16);
+          acc = __fmaf_rn(wv, gv, acc);
+        }
+      }
+    }
+    p.y[o] = acc;
+  }
+}
+
 size_t conv_mc_smem_bytes(int64_t cin, int64_t cout, int64_t k, int rows, int stages) {
   const size_t stage = (size_t)(cin / 64) * rows * 128;
   return 1024 + stages * stage + (size_t)k * (cin / 64) * cout * 128 + 8 * (2 * stages + 8) + 40 * kMcRing + 16;
@@ -492,6 +545,50 @@ int conv_mc_choose_mblk(int64_t cin, int64_t cout, int64_t k, int rows1) {
   }();
   if (forced == 1 || forced == 2) return forced;
   return conv_mc_smem_bytes(cin, cout, k, mc_round_rows(rows1 + 128), kMcStages) <= (size_t)kSmemBudget ? 2 : 1;
+}
+
+// pad2d tiling: over pitches P = Cw + kw - 1 <= 256 and M-blocks (2 preferred when it fits three
+// stages, as conv_mc_choose_mblk), R = min(128 mblk / P, H, 257 - kh) dx rows per tile; fewest tiles
+// wins (the MMA work), then the fewest staged rows.  Staged rows cover the box and every row a tap of
+// a masked output reads (positions past the box are never stored).
+bool conv_mc_plan_pad2d(ConvMcParams& p) {
+  static const int forced = [] {
+    const char* e = getenv("SS_MC_MBLK");
+    return e ? atoi(e) : 0;
+  }();
+  const int64_t kh = p.pd_kh, kw = p.pd_kw;
+  if (kh * kw > kMcMaxTaps || kh > 256) return false;
+  for (int mb = 2; mb >= 1; --mb) {
+    if (forced && forced != mb) continue;
+    const int64_t TP = 128 * mb;
+    int64_t best = -1, best_rows = 0;
+    int bP = 0, bR = 0, bC = 0;
+    for (int64_t Cw = 1; Cw <= p.W && Cw + kw - 1 <= 256; ++Cw) {
+      const int64_t P = Cw + kw - 1;
+      int64_t R = TP / P;
+      if (R > p.H) R = p.H;
+      if (R > 257 - kh) R = 257 - kh;
+      if (R < 1) continue;
+      const int64_t box = (R + kh - 1) * P, reach = TP + (kh - 1) * P + kw - 1;
+      const int64_t rows = ((box > reach ? box : reach) + 7) / 8 * 8;
+      if (rows > 2048) continue;
+      const int64_t nt = ((p.H + R - 1) / R) * ((p.W + Cw - 1) / Cw);
+      if (best < 0 || nt < best || (nt == best && rows < best_rows)) {
+        best = nt; best_rows = rows; bP = (int)P; bR = (int)R; bC = (int)Cw;
+      }
+    }
+    if (best < 0) continue;
+    const int stages_needed = mb == 2 && !forced ? kMcStages : 2;
+    if (conv_mc_smem_bytes(p.cin, p.cout, kh * kw, (int)best_rows, stages_needed) > (size_t)kSmemBudget) continue;
+    p.mblk = mb; p.rows = (int)best_rows; p.nbox = 1; p.box_rows = 0;
+    p.pd_P = bP; p.pd_R = bR; p.pd_Cw = bC;
+    p.pd_nrt = (p.H + bR - 1) / bR; p.pd_nct = (p.W + bC - 1) / bC;
+    p.pd_tx = (int)((p.cin / 64) * (bR + kh - 1) * bP * 128);
+    for (int64_t a = 0; a < kh; ++a)
+      for (int64_t e = 0; e < kw; ++e) p.tap_off[a * kw + e] = (int)(a * bP + e);
+    return true;
+  }
+  return false;
 }
 
 template <int CIN, int COUT>
@@ -513,11 +610,12 @@ static cudaError_t launch_mc(ConvMcParams& p, cudaStream_t stream, int sms) {
 }
 
 cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t stream, int sms) {
-  if (p.two_d) {  // exact unsigned division by W for 31-bit numerators (round-up multiplier)
+  if (p.two_d || (p.pad2d && tensor_path)) {  // exact unsigned division by W (pad2d: P) for 31-bit numerators
+    const uint64_t dv = p.pad2d ? (uint64_t)p.pd_P : (uint64_t)p.W;
     int sft = 0;
-    while ((1ll << sft) < p.W) ++sft;
+    while ((1ull << sft) < dv) ++sft;
     p.w_shift = sft;
-    p.w_magic = (uint32_t)(((1ull << 32) * ((1ull << sft) - (uint64_t)p.W)) / (uint64_t)p.W + 1);
+    p.w_magic = (uint32_t)(((1ull << 32) * ((1ull << sft) - dv)) / dv + 1);
   }
   static unsigned long long* tbuf = nullptr;
   if (getenv("SS_MC_TRACE")) {
@@ -528,7 +626,8 @@ cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t strea
     if (p.mblk < 1) p.mblk = 1;
     const int64_t tp = 128 * p.mblk;
     if (p.batched) p.tiles_per_row = (p.n_out + tp - 1) / tp;
-    p.ntiles = p.batched ? p.batch * p.tiles_per_row : (p.batch * p.N + tp - 1) / tp;
+    p.ntiles = p.pad2d ? p.batch * p.pd_nrt * p.pd_nct
+                       : p.batched ? p.batch * p.tiles_per_row : (p.batch * p.N + tp - 1) / tp;
     cudaError_t e = cudaErrorInvalidConfiguration;
     if (p.cin == 64 && p.cout == 64) e = launch_mc<64, 64>(p, stream, sms);
     else if (p.cin == 64 && p.cout == 128) e = launch_mc<64, 128>(p, stream, sms);
@@ -536,11 +635,13 @@ cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t strea
     else if (p.cin == 128 && p.cout == 128) e = launch_mc<128, 128>(p, stream, sms);
     if (e != cudaErrorInvalidConfiguration) return e;
   }
-  const int64_t total = p.two_d ? p.batch * p.OH * p.OW * p.cout
+  const int64_t total = p.pad2d  ? p.batch * p.H * p.W * p.cout
+                      : p.two_d ? p.batch * p.OH * p.OW * p.cout
                                 : p.bwd_in ? p.batch * p.n_out * p.cout : p.batch * p.L * p.cout;
   int64_t g = (total + 255) / 256;
   if (g > (int64_t)sms * 16) g = (int64_t)sms * 16;
-  if (p.bwd_in) conv_mc_bwd_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
+  if (p.pad2d) conv2d_mc_bwd_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
+  else if (p.bwd_in) conv_mc_bwd_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
   else if (p.two_d) conv2d_mc_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
   else conv_mc_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
   note_launch();

@@ -281,6 +281,12 @@ struct alignas(64) ConvMcParams {
   int mblk, nacc;  // 128-position M-blocks per tile (1, 2), TMEM accumulators (tiles in flight)
   uint32_t w_magic; int w_shift;     // 2-D: r = (umulhi(i, w_magic) + i) >> w_shift == i / W for i < 2^31
   int tap_off[kMcMaxTaps];
+  // pad2d (2-D input gradient, reading R26): a tile is pd_R rows x pd_Cw columns of dx, staged as one
+  // 5-D TMA box per atom of (pd_R + kh - 1) x pd_P dy positions (pitch pd_P = pd_Cw + kw - 1) starting
+  // kh-1 rows / kw-1 columns early (zero-filled outside dy); tm_x is {64, OW, OH, atoms, batch}.
+  // x = dy, y = dx, cin = dy channels, cout = dx channels, H x W = dx, OH x OW = dy.
+  int pad2d, pd_kh, pd_kw, pd_P, pd_R, pd_Cw, pd_tx;
+  int64_t pd_nrt, pd_nct;  // row / column tiles per image
   int64_t ntiles;    // set by launch_conv_mc
   int clc;  // 1: one CTA per work unit, units claimed by cluster launch control (ss_device.cuh); 0: static stride
 };
@@ -288,6 +294,10 @@ bool encode_mc_map(CUtensorMap* m, const void* x, int64_t positions, int64_t cin
 bool encode_mc_map_batched(CUtensorMap* m, const void* x, int64_t batch, int64_t positions, int64_t cin,
                            int box_rows);
 cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t stream, int sms);
+// pad2d tiling (sets pd_*, mblk, rows, tap_off); false: no tensor-core plan fits
+bool conv_mc_plan_pad2d(ConvMcParams& p);
+bool encode_mc_map_2d(CUtensorMap* m, const void* x, int64_t batch, int64_t OH, int64_t OW, int64_t c, int box_w,
+                      int box_h);
 // Multi-channel conv1d filter gradient (mc_fgrad.cu; reading R25): tensor cores for cin = 64,
 // cout 64 (k <= 4) / 128 (k <= 2), else a direct kernel.  ws: per-CTA fp64 slices [sms][cout][64 k].
 struct alignas(64) McFgradParams {
