@@ -12,10 +12,11 @@
 // rows further down (descriptor start + 128 j bytes; the same row-shift trick as
 // the forward), so no im2col and no transposes.  bf16 products are exact; the
 // tensor memory accumulates one tile (128 positions, fp32), the epilogue adds the
-// tile into an fp32 run accumulator in shared memory (16 tiles per run), and each
-// run is added into this CTA's fp64 slice of the caller's workspace; a finish
-// kernel sums the slices in CTA order.  |error| <= (128 + 16) fp32 roundings of
-// partial sums bounded by sum |terms| (~8.6e-6 of it) -- inside the 1e-5 bound.
+// tile into an fp32 run accumulator in registers (32 tiles per run), and each run
+// goes through shared memory into this CTA's fp64 slice of the caller's workspace,
+// coalesced; a finish kernel sums the slices in a fixed order.  |error| <= (128 + 32)
+// fp32 roundings of partial sums bounded by sum |terms| (~9.5e-6 of it) -- inside
+// the 1e-5 bound.
 //
 // Roles (320 threads, one CTA per SM): warp 0 TMA producer (dy tile + x tile of
 // 136 rows per stage, 3 stages), warp 1 MMA issuer (8 K-steps, one N = 64 k MMA each:
@@ -101,14 +102,14 @@ constexpr size_t mf_smem(int k) {
 
 }  // namespace
 
-template <int COUT>
+template <int COUT, int KT>
 __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const __grid_constant__ McFgradParams p) {
   constexpr int AT = COUT / 64;  // dy atoms (64 channels each)
   constexpr uint32_t kDyBytes = AT * 16384u;
   constexpr uint32_t kStage = kDyBytes + kMfXBytes;
   extern __shared__ __align__(16) uint8_t mf_raw[];
   uint8_t* smem = mf_raw + ((1024u - (smem_u32(mf_raw) & 1023u)) & 1023u);
-  const int k = (int)p.k, NC = 64 * k;  // accumulator columns (tap j at 64 j)
+  constexpr int NC = 64 * KT, NH = NC / 2;  // accumulator columns (tap j at 64 j); per epilogue warp
   float* R = reinterpret_cast<float*>(smem + kMfStages * kStage);  // [COUT][NC + 4] fp32 run accumulators (16-B rows, 4-word skew)
   uint64_t* full = reinterpret_cast<uint64_t*>(R + COUT * (NC + 4) + 4);
   full = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(full) + 7) & ~uintptr_t(7));
@@ -178,48 +179,45 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
     // ------------------------------------------------------------ epilogue: tile -> fp32 run -> fp64 slice
     const int q = warp & 3, hh = (warp - 2) >> 2;  // lane quarter; half of the columns (two warps per quarter)
     const int co = COUT == 128 ? 32 * q + lane : 16 * q + lane;  // M = 64: lanes 0-15 of each quarter
-    const int cb = hh * (NC / 2), ce = cb + NC / 2;
+    const int cb = hh * NH;
     const uint32_t lanebits = (uint32_t)(32 * q) << 16;
     float* Rr = R + (size_t)co * (NC + 4);
     double* W = p.ws + (size_t)blockIdx.x * COUT * NC;  // this CTA's fp64 slice [COUT][NC]
     const int e = threadIdx.x - 64;                     // 0 .. 255: cooperative, coalesced slice updates
-    for (int i = e; i < COUT * NC; i += 256) { R[(i / NC) * (NC + 4) + i % NC] = 0.0f; W[i] = 0.0; }
-    asm volatile("bar.sync 1, 256;" ::: "memory");
+    for (int i = e; i < COUT * NC; i += 256) W[i] = 0.0;
+    // the fp32 run lives in registers: row co, columns [cb, cb + NH) (tcgen05.ld 32x32b: lane = row);
+    // at the end of a run it goes through shared memory into the slice, coalesced
+    float acc[NH];
+#pragma unroll
+    for (int i = 0; i < NH; ++i) acc[i] = 0.0f;
     int d = 0, nt = 0;
     uint32_t dph = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       mf_wait(dfull + d, dph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll 1
-      // 32x32b: lane = row co, 32 consecutive columns (for M = 64 only lanes 0-15 of the quarter are
-      // rows: 16x256b reads with every lane useful measured slower, 117 vs 105 us)
-      for (int c0 = cb; c0 < ce; c0 += 32) {
-        uint32_t v[32];
-        mf_ld32(tmem + lanebits + (uint32_t)(d * NC + c0), v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (COUT == 128 || lane < 16) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {  // float4: rows are 16-B aligned, the 4-word skew spreads banks
-            float4* r4 = reinterpret_cast<float4*>(Rr + c0 + i);
-            float4 t = *r4;
-            t.x += __uint_as_float(v[i]); t.y += __uint_as_float(v[i + 1]);
-            t.z += __uint_as_float(v[i + 2]); t.w += __uint_as_float(v[i + 3]);
-            *r4 = t;
-          }
-        }
+      for (int c0 = 0; c0 < NH; c0 += 32) {
+        uint32_t v[32];
+        mf_ld32(tmem + lanebits + (uint32_t)(d * NC + cb + c0), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[c0 + i] += __uint_as_float(v[i]);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(dempty + d);
       if (++nt == kMfRunTiles || tile + gridDim.x >= ntiles) {  // end of a run: into the fp64 slice
         nt = 0;
-        asm volatile("bar.sync 1, 256;" ::: "memory");  // every row's run is complete
-#pragma unroll 4
-        for (int i = e; i < COUT * NC; i += 256) {
-          float* r = R + (i / NC) * (NC + 4) + i % NC;
-          W[i] += (double)*r;
-          *r = 0.0f;
+        if (COUT == 128 || lane < 16) {  // M = 64: lanes 0-15 of each quarter are the rows
+#pragma unroll
+          for (int i = 0; i < NH; i += 4) {
+            *reinterpret_cast<float4*>(Rr + cb + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+            acc[i] = acc[i + 1] = acc[i + 2] = acc[i + 3] = 0.0f;
+          }
         }
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // every row's run is in shared memory
+#pragma unroll 4
+        for (int i = e; i < COUT * NC; i += 256) W[i] += (double)R[(i / NC) * (NC + 4) + i % NC];
         asm volatile("bar.sync 1, 256;" ::: "memory");
       }
       if (++d == 2) { d = 0; dph ^= 1u; }
@@ -231,16 +229,23 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-// dw[co][ci][j] = sum over CTA slices c (in order) of ws[c][co][64 j + ci]
-__global__ void mc_filter_grad_finish(const double* __restrict__ ws, int ctas, int64_t cout, int64_t k,
-                                      float* __restrict__ dw) {
-  const int64_t total = cout * 64 * k;
-  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = o % k, ci = (o / k) % 64, co = o / (64 * k);
-    double s = 0.0;
-    for (int c = 0; c < ctas; ++c) s += ws[((size_t)c * cout + co) * (64 * k) + 64 * j + ci];
-    dw[o] = (float)s;
-  }
+// dw[co][ci][a][e] = sum over the CTA slices c = a, a + kh, ... of ws[c][co][64 e + ci] (1-D: kh = 1,
+// e = j).  Block (co, a, e), thread (ci, g): slices c = a + kh (g + 4 i) in increasing i (64 threads read
+// 512 contiguous bytes per slice), then the four partial sums in g order: a fixed order, deterministic.
+__global__ void __launch_bounds__(256) mc_filter_grad_finish(const double* __restrict__ ws, int ctas, int64_t cout,
+                                                             int kh, int kw, float* __restrict__ dw) {
+  __shared__ double part[4][64];
+  const int ci = threadIdx.x & 63, g = threadIdx.x >> 6;
+  const int64_t blk = blockIdx.x, e = blk % kw, a = (blk / kw) % kh, co = blk / ((int64_t)kw * kh);
+  const int per = ctas / kh;  // slices of tap row a
+  const double* __restrict__ src = ws + (size_t)co * 64 * kw + 64 * e + ci;
+  const size_t cstride = (size_t)cout * 64 * kw;
+  double s = 0.0;
+#pragma unroll 8
+  for (int m = g; m < per; m += 4) s += src[(size_t)(a + (int64_t)kh * m) * cstride];
+  part[g][ci] = s;
+  __syncthreads();
+  if (g == 0) dw[((co * 64 + ci) * kh + a) * kw + e] = (float)(((part[0][ci] + part[1][ci]) + part[2][ci]) + part[3][ci]);
 }
 
 // Direct kernel (any shape): one block per output element, positions strided over the threads,
@@ -284,9 +289,15 @@ cudaError_t launch_mc_filter_grad(McFgradParams& p, bool tc, cudaStream_t stream
     p.tiles_per_row = (p.L + kMfTileP - 1) / kMfTileP;
     p.ntiles = p.batch * p.tiles_per_row;
     const int ctas = sms;
-    const void* kfn = p.cout == 128 ? reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<128>)
-                                    : reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<64>);
-    const size_t smem = p.cout == 128 ? mf_smem<128>((int)p.k) : mf_smem<64>((int)p.k);
+    const void* kfn = nullptr;
+    const int k = (int)p.k;
+    if (p.cout == 128) kfn = k == 1 ? reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<128, 1>)
+                                    : reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<128, 2>);
+    else kfn = k == 1   ? reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<64, 1>)
+               : k == 2 ? reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<64, 2>)
+               : k == 3 ? reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<64, 3>)
+                        : reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<64, 4>);
+    const size_t smem = p.cout == 128 ? mf_smem<128>(k) : mf_smem<64>(k);
     if (smem > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
     cudaError_t e = ensure_smem_attr(kfn);
     if (e != cudaSuccess) return e;
@@ -294,8 +305,7 @@ cudaError_t launch_mc_filter_grad(McFgradParams& p, bool tc, cudaStream_t stream
     e = cudaLaunchKernel(kfn, dim3((unsigned)ctas), dim3(kMfThreads), args, smem, stream);
     note_launch();
     if (e != cudaSuccess) return e;
-    const int64_t total = p.cout * 64 * p.k;
-    mc_filter_grad_finish<<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(p.ws, ctas, p.cout, p.k, p.dw);
+    mc_filter_grad_finish<<<(unsigned)(p.cout * p.k), 256, 0, stream>>>(p.ws, ctas, p.cout, 1, (int)p.k, p.dw);
     note_launch();
     return cudaGetLastError();
   }

@@ -1,5 +1,5 @@
 """Launch the multi-channel conv kernels on their bench shapes (for ncu captures):
-    python tools/mc_prof.py [2d|1d9|dx] [reps]"""
+    python tools/mc_prof.py [2d|1d9|dx|dw|dx2d|dw2d] [reps]"""
 import os
 import sys
 
@@ -19,6 +19,14 @@ elif which == "1d9":
     x = torch.randn(16, 65536, 64, device="cuda").to(torch.bfloat16)
     w = (torch.randn(64, 64, 9, device="cuda") / 24).to(torch.bfloat16)
     f = lambda: ss.conv1d_mc(x, w)  # noqa: E731
+elif which == "dw":
+    g = torch.randn(16, 65534, 64, device="cuda").to(torch.bfloat16)
+    x = torch.randn(16, 65536, 64, device="cuda").to(torch.bfloat16)
+    f = lambda: ss.conv1d_mc_backward_filter(g, x, 3)  # noqa: E731
+elif which == "dx2d":
+    g = torch.randn(128, 54, 54, 64, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(64, 64, 3, 3, device="cuda") / 24).to(torch.bfloat16)
+    f = lambda: ss.conv2d_mc_backward_input(g, w, 56, 56)  # noqa: E731
 else:
     g = torch.randn(16, 65534, 64, device="cuda").to(torch.bfloat16)
     w = (torch.randn(64, 64, 3, device="cuda") / 24).to(torch.bfloat16)
