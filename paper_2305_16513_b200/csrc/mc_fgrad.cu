@@ -13,13 +13,15 @@
 // the forward), so no im2col and no transposes.  bf16 products are exact; the
 // tensor memory accumulates one tile (128 positions, fp32), the epilogue adds the
 // tile into an fp32 run accumulator in registers (32 tiles per run), and each run
-// goes through shared memory into this CTA's fp64 slice of the caller's workspace,
-// coalesced; a finish kernel sums the slices in a fixed order.  |error| <= (128 + 32)
+// goes straight from registers into this CTA's fp64 slice of the caller's workspace
+// (slice [64 k][cout]: a warp's rows are contiguous; the first run is stored, later
+// ones are added by fire-and-forget reductions, in program order per slot); a
+// finish kernel sums the slices in a fixed order.  |error| <= (128 + 32)
 // fp32 roundings of partial sums bounded by sum |terms| (~9.5e-6 of it) -- inside
 // the 1e-5 bound.
 //
 // Roles (320 threads, one CTA per SM): warp 0 TMA producer (dy tile + x tile of
-// 136 rows per stage, 3 stages), warp 1 MMA issuer (8 K-steps, one N = 64 k MMA each:
+// 136 rows per stage, as many stages as shared memory holds: 6 at cout = 64), warp 1 MMA issuer (8 K-steps, one N = 64 k MMA each:
 // tap j is B's MN atom j = the x tile j rows down, an atom stride of 128 B), warps
 // 2-9 epilogue (two per TMEM lane quarter, half the columns each; for cout = 64 the M = 64 accumulator
 // occupies lanes 0-15 of each quarter: tools/ubench/tc_m64_probe.cu).
@@ -36,7 +38,7 @@ namespace ss {
 namespace {
 
 constexpr int kMfThreads = 320;
-constexpr int kMfStages = 3;
+constexpr int kMfMaxStages = 8;                   // ring depth: as many one-tile stages as shared memory holds
 constexpr int kMfTileP = 128;                      // positions per tile
 constexpr int kMfXRows = 136;                      // x rows per tile (128 + k - 1 <= 131, 17 atoms)
 constexpr uint32_t kMfXBytes = kMfXRows * 128u;
@@ -95,10 +97,8 @@ __device__ __forceinline__ void mf_ld32(uint32_t taddr, uint32_t* v) {
       : "memory");
 }
 
-template <int COUT>
-constexpr size_t mf_smem(int k) {
-  return 1024 + (size_t)kMfStages * ((COUT / 64) * 16384u + kMfXBytes) + (size_t)COUT * (64 * k + 4) * 4 + 256;
-}
+constexpr size_t mf_stage_bytes(int64_t cout) { return (size_t)(cout / 64) * 16384u + kMfXBytes; }
+constexpr size_t mf_smem(size_t stage, int stages) { return 1024 + (size_t)stages * stage + 256; }
 
 }  // namespace
 
@@ -110,11 +110,10 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
   extern __shared__ __align__(16) uint8_t mf_raw[];
   uint8_t* smem = mf_raw + ((1024u - (smem_u32(mf_raw) & 1023u)) & 1023u);
   constexpr int NC = 64 * KT, NH = NC / 2;  // accumulator columns (tap j at 64 j); per epilogue warp
-  float* R = reinterpret_cast<float*>(smem + kMfStages * kStage);  // [COUT][NC + 4] fp32 run accumulators (16-B rows, 4-word skew)
-  uint64_t* full = reinterpret_cast<uint64_t*>(R + COUT * (NC + 4) + 4);
-  full = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(full) + 7) & ~uintptr_t(7));
-  uint64_t* empty = full + kMfStages;
-  uint64_t* dfull = empty + kMfStages;
+  const int kMfStages = p.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kMfStages * kStage);
+  uint64_t* empty = full + kMfMaxStages;
+  uint64_t* dfull = empty + kMfMaxStages;
   uint64_t* dempty = dfull + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -181,12 +180,14 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
     const int co = COUT == 128 ? 32 * q + lane : 16 * q + lane;  // M = 64: lanes 0-15 of each quarter
     const int cb = hh * NH;
     const uint32_t lanebits = (uint32_t)(32 * q) << 16;
-    float* Rr = R + (size_t)co * (NC + 4);
-    double* W = p.ws + (size_t)blockIdx.x * COUT * NC;  // this CTA's fp64 slice [COUT][NC]
-    const int e = threadIdx.x - 64;                     // 0 .. 255: cooperative, coalesced slice updates
-    for (int i = e; i < COUT * NC; i += 256) W[i] = 0.0;
-    // the fp32 run lives in registers: row co, columns [cb, cb + NH) (tcgen05.ld 32x32b: lane = row);
-    // at the end of a run it goes through shared memory into the slice, coalesced
+    // this CTA's fp64 slice [NC][COUT] (row co fastest: a warp's 16 / 32 rows are contiguous, so a run
+    // flushes straight from registers, coalesced); each thread owns (co, [cb, cb + NH))
+    double* W = p.ws + (size_t)blockIdx.x * COUT * NC + (size_t)cb * COUT + co;
+    const bool owner = COUT == 128 || lane < 16;  // M = 64: lanes 0-15 of each quarter are the rows
+    if (owner && (int64_t)blockIdx.x >= ntiles)  // no tiles: the slice is zero
+      for (int i = 0; i < NH; ++i) W[(size_t)i * COUT] = 0.0;
+    bool first = true;  // the first run is stored, later runs are added (fire-and-forget reductions)
+    // the fp32 run lives in registers: row co, columns [cb, cb + NH) (tcgen05.ld 32x32b: lane = row)
     float acc[NH];
 #pragma unroll
     for (int i = 0; i < NH; ++i) acc[i] = 0.0f;
@@ -208,17 +209,20 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
       if (lane == 0) mbar_arrive(dempty + d);
       if (++nt == kMfRunTiles || tile + gridDim.x >= ntiles) {  // end of a run: into the fp64 slice
         nt = 0;
-        if (COUT == 128 || lane < 16) {  // M = 64: lanes 0-15 of each quarter are the rows
+        if (owner) {
+          // one thread owns each slot and issues its writes in program order, so the additions land in
+          // a fixed order (per-location coherence): deterministic; a reduction needs no round trip
+          if (first) {
 #pragma unroll
-          for (int i = 0; i < NH; i += 4) {
-            *reinterpret_cast<float4*>(Rr + cb + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
-            acc[i] = acc[i + 1] = acc[i + 2] = acc[i + 3] = 0.0f;
+            for (int i = 0; i < NH; ++i) W[(size_t)i * COUT] = (double)acc[i];
+          } else {
+#pragma unroll
+            for (int i = 0; i < NH; ++i) atomicAdd(W + (size_t)i * COUT, (double)acc[i]);
           }
+#pragma unroll
+          for (int i = 0; i < NH; ++i) acc[i] = 0.0f;
         }
-        asm volatile("bar.sync 1, 256;" ::: "memory");  // every row's run is in shared memory
-#pragma unroll 4
-        for (int i = e; i < COUT * NC; i += 256) W[i] += (double)R[(i / NC) * (NC + 4) + i % NC];
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+        first = false;
       }
       if (++d == 2) { d = 0; dph ^= 1u; }
     }
@@ -229,23 +233,28 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-// dw[co][ci][a][e] = sum over the CTA slices c = a, a + kh, ... of ws[c][co][64 e + ci] (1-D: kh = 1,
-// e = j).  Block (co, a, e), thread (ci, g): slices c = a + kh (g + 4 i) in increasing i (64 threads read
-// 512 contiguous bytes per slice), then the four partial sums in g order: a fixed order, deterministic.
-__global__ void __launch_bounds__(256) mc_filter_grad_finish(const double* __restrict__ ws, int ctas, int64_t cout,
-                                                             int kh, int kw, float* __restrict__ dw) {
-  __shared__ double part[4][64];
-  const int ci = threadIdx.x & 63, g = threadIdx.x >> 6;
-  const int64_t blk = blockIdx.x, e = blk % kw, a = (blk / kw) % kh, co = blk / ((int64_t)kw * kh);
+// dw[co][ci][a][e] = sum over the CTA slices c = a, a + kh, ... of ws[c][64 e + ci][co] (1-D: kh = 1,
+// e = j).  Block (column 64 e + ci, a), thread (co, g): slices c = a + kh (g + G i) in increasing i (the
+// block's COUT threads read COUT contiguous doubles per slice), then the G partial sums in g order: a
+// fixed order, deterministic.
+__global__ void __launch_bounds__(1024) mc_filter_grad_finish(const double* __restrict__ ws, int ctas, int cout,
+                                                              int kh, int kw, float* __restrict__ dw) {
+  __shared__ double part[1024];
+  const int G = 1024 / cout, co = threadIdx.x % cout, g = threadIdx.x / cout;
+  const int nc = 64 * kw, col = blockIdx.x % nc, a = blockIdx.x / nc;
   const int per = ctas / kh;  // slices of tap row a
-  const double* __restrict__ src = ws + (size_t)co * 64 * kw + 64 * e + ci;
-  const size_t cstride = (size_t)cout * 64 * kw;
+  const double* __restrict__ src = ws + (size_t)col * cout + co;
+  const size_t cstride = (size_t)nc * cout;
   double s = 0.0;
-#pragma unroll 8
-  for (int m = g; m < per; m += 4) s += src[(size_t)(a + (int64_t)kh * m) * cstride];
-  part[g][ci] = s;
+#pragma unroll 4
+  for (int m = g; m < per; m += G) s += src[(size_t)(a + kh * m) * cstride];
+  part[threadIdx.x] = s;
   __syncthreads();
-  if (g == 0) dw[((co * 64 + ci) * kh + a) * kw + e] = (float)(((part[0][ci] + part[1][ci]) + part[2][ci]) + part[3][ci]);
+  if (g == 0) {
+    for (int h = 1; h < G; ++h) s += part[h * cout + co];
+    const int e = col / 64, ci = col % 64;
+    dw[(((int64_t)co * 64 + ci) * kh + a) * kw + e] = (float)s;
+  }
 }
 
 // Direct kernel (any shape): one block per output element, positions strided over the threads,
@@ -297,7 +306,11 @@ cudaError_t launch_mc_filter_grad(McFgradParams& p, bool tc, cudaStream_t stream
                : k == 2 ? reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<64, 2>)
                : k == 3 ? reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<64, 3>)
                         : reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<64, 4>);
-    const size_t smem = p.cout == 128 ? mf_smem<128>(k) : mf_smem<64>(k);
+    const size_t stage = mf_stage_bytes(p.cout);
+    p.stages = (int)((kSmemBudget - 1024 - 256) / stage);
+    if (p.stages > kMfMaxStages) p.stages = kMfMaxStages;
+    if (p.stages < 2) return cudaErrorInvalidConfiguration;
+    const size_t smem = mf_smem(stage, p.stages);
     if (smem > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
     cudaError_t e = ensure_smem_attr(kfn);
     if (e != cudaSuccess) return e;
@@ -305,7 +318,7 @@ cudaError_t launch_mc_filter_grad(McFgradParams& p, bool tc, cudaStream_t stream
     e = cudaLaunchKernel(kfn, dim3((unsigned)ctas), dim3(kMfThreads), args, smem, stream);
     note_launch();
     if (e != cudaSuccess) return e;
-    mc_filter_grad_finish<<<(unsigned)(p.cout * p.k), 256, 0, stream>>>(p.ws, ctas, p.cout, 1, (int)p.k, p.dw);
+    mc_filter_grad_finish<<<(unsigned)(64 * p.k), 1024, 0, stream>>>(p.ws, ctas, (int)p.cout, 1, (int)p.k, p.dw);
     note_launch();
     return cudaGetLastError();
   }

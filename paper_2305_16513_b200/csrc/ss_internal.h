@@ -299,7 +299,7 @@ bool conv_mc_plan_pad2d(ConvMcParams& p);
 bool encode_mc_map_2d(CUtensorMap* m, const void* x, int64_t batch, int64_t OH, int64_t OW, int64_t c, int box_w,
                       int box_h);
 // Multi-channel conv1d filter gradient (mc_fgrad.cu; reading R25): tensor cores for cin = 64,
-// cout 64 (k <= 4) / 128 (k <= 2), else a direct kernel.  ws: per-CTA fp64 slices [sms][cout][64 k].
+// cout 64 (k <= 4) / 128 (k <= 2), else a direct kernel.  ws: per-CTA fp64 slices [sms][64 k][cout].
 struct alignas(64) McFgradParams {
   CUtensorMap tm_dy, tm_x;  // batched maps: dy {64, L, cout/64, batch} box 128 rows, x {64, N, 1, batch} box 136
   const uint16_t* dy;
@@ -308,6 +308,7 @@ struct alignas(64) McFgradParams {
   double* ws;
   int64_t batch, N, L, cin, cout, k;
   int64_t tiles_per_row, ntiles;  // set by the launcher
+  int stages;                     // set by the launcher
 };
 bool mc_filter_grad_tc_supported(int64_t cin, int64_t cout, int64_t k);
 size_t mc_filter_grad_workspace(int64_t cin, int64_t cout, int64_t k, int sms);
