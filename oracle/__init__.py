@@ -98,6 +98,8 @@ def lib() -> ctypes.CDLL:
             L.oracle_conv1d_mc_backward_filter_bf16.restype = ctypes.c_int
             L.oracle_conv2d_mc_backward_input_bf16.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, vp]
             L.oracle_conv2d_mc_backward_input_bf16.restype = ctypes.c_int
+            L.oracle_conv2d_mc_backward_filter_bf16.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, vp]
+            L.oracle_conv2d_mc_backward_filter_bf16.restype = ctypes.c_int
             L.oracle_conv2d_f32.argtypes = [vp, i64, i64, i64, vp, i64, i64, i64, i64, vp, vp]
             L.oracle_conv2d_f32.restype = ctypes.c_int
             L.oracle_conv2d_backward_input_f32.argtypes = [vp, i64, i64, i64, vp, i64, i64, i64, i64, vp, vp]
@@ -498,3 +500,17 @@ def conv2d_mc_backward_input(dy_bf16: np.ndarray, w_bf16: np.ndarray, H: int, W:
     m = np.empty((B, H, W, cin), np.float64)
     _check(lib().oracle_conv2d_mc_backward_input_bf16(_p(dy), _p(w), B, H, W, cin, cout, kh, kw, _p(dx), _p(m)))
     return dx, m
+
+
+def conv2d_mc_backward_filter(dy_bf16: np.ndarray, x_bf16: np.ndarray, kh: int, kw: int):
+    """dw [Cout, Cin, kh, kw] (double) of the multi-channel 2-D conv for bf16 dy [B, H-kh+1, W-kw+1, Cout]
+    and x [B, H, W, Cin] (reading R27); returns (dw, absmag)."""
+    dy = np.ascontiguousarray(dy_bf16, np.uint16)
+    x = np.ascontiguousarray(x_bf16, np.uint16)
+    B, OH, OW, cout = dy.shape
+    B2, H, W, cin = x.shape
+    assert B2 == B and OH == H - kh + 1 and OW == W - kw + 1
+    dw = np.empty((cout, cin, kh, kw), np.float64)
+    m = np.empty((cout, cin, kh, kw), np.float64)
+    _check(lib().oracle_conv2d_mc_backward_filter_bf16(_p(dy), _p(x), B, H, W, cin, cout, kh, kw, _p(dw), _p(m)))
+    return dw, m

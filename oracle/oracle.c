@@ -748,3 +748,35 @@ int oracle_conv2d_mc_backward_input_bf16(const uint16_t* dy, const uint16_t* w, 
             }
   return 0;
 }
+
+/* Filter gradient of the multi-channel 2-D convolution (reading R27: the weight
+ * vector-Jacobian product of reading R22), bf16 dy and x, NHWC:
+ *   dw[co][ci][a][e] = sum_b sum_{r < H-kh+1} sum_{c < W-kw+1} dy[b][r][c][co] x[b][r+a][c+e][ci]
+ * dy [batch][H-kh+1][W-kw+1][cout], x [batch][H][W][cin], dw [cout][cin][kh][kw];
+ * each sum in double in (b, r, c) order. */
+int oracle_conv2d_mc_backward_filter_bf16(const uint16_t* dy, const uint16_t* x, int64_t batch, int64_t H, int64_t W,
+                                          int64_t cin, int64_t cout, int64_t kh, int64_t kw, double* dw,
+                                          double* absmag) {
+  if (dy == NULL || x == NULL || dw == NULL || batch < 1 || cin < 1 || cout < 1 || kh < 1 || kw < 1 || kh > H ||
+      kw > W)
+    return -1;
+  int64_t OH = H - kh + 1, OW = W - kw + 1;
+  for (int64_t co = 0; co < cout; ++co)
+    for (int64_t ci = 0; ci < cin; ++ci)
+      for (int64_t a = 0; a < kh; ++a)
+        for (int64_t e = 0; e < kw; ++e) {
+          double acc = 0.0, mag = 0.0;
+          for (int64_t b = 0; b < batch; ++b)
+            for (int64_t r = 0; r < OH; ++r)
+              for (int64_t c = 0; c < OW; ++c) {
+                double t = bf16_to_double(dy[((b * OH + r) * OW + c) * cout + co]) *
+                           bf16_to_double(x[((b * H + r + a) * W + c + e) * cin + ci]);
+                acc += t;
+                mag += fabs(t);
+              }
+          int64_t o = ((co * cin + ci) * kh + a) * kw + e;
+          dw[o] = acc;
+          if (absmag) absmag[o] = mag;
+        }
+  return 0;
+}

@@ -160,6 +160,9 @@ int oracle_conv1d_mc_backward_filter_bf16(const uint16_t* dy, const uint16_t* x,
 int oracle_conv2d_mc_backward_input_bf16(const uint16_t* dy, const uint16_t* w, int64_t batch, int64_t H, int64_t W,
                                          int64_t cin, int64_t cout, int64_t kh, int64_t kw, double* dx,
                                          double* absmag);
+int oracle_conv2d_mc_backward_filter_bf16(const uint16_t* dy, const uint16_t* x, int64_t batch, int64_t H, int64_t W,
+                                          int64_t cin, int64_t cout, int64_t kh, int64_t kw, double* dw,
+                                          double* absmag);
 
 #ifdef __cplusplus
 }

@@ -656,3 +656,33 @@ def test_conv2d_mc_backward_input_adjoint_torch_and_1d_reduction():
     dx2, _ = oracle.conv2d_mc_backward_input(g1, w1, 1, W)
     dx1, _ = oracle.conv1d_mc_backward_input(g1[:, 0], w1[:, :, 0], W)
     np.testing.assert_array_equal(dx2[:, 0], dx1)
+
+
+def test_conv2d_mc_backward_filter_adjoint_torch_and_1d_reduction():
+    # reading R27: dw[co][ci][a][e] = sum_{b,r,c} dy[b][r][c][co] x[b][r+a][c+e][ci]
+    B, H, W, cin, cout, kh, kw = 2, 7, 9, 3, 4, 3, 2
+    OH, OW = H - kh + 1, W - kw + 1
+    x = synth.randint(150, B * H * W * cin, -4, 4).astype(np.float32).reshape(B, H, W, cin)
+    w = synth.randint(151, cout * cin * kh * kw, -3, 3).astype(np.float32).reshape(cout, cin, kh, kw)
+    dy = synth.randint(152, B * OH * OW * cout, -4, 4).astype(np.float32).reshape(B, OH, OW, cout)
+    xb, wb, gb = oracle.to_bf16_bits(x), oracle.to_bf16_bits(w), oracle.to_bf16_bits(dy)
+    y, _ = oracle.conv2d_mc(xb, wb)
+    dw, _ = oracle.conv2d_mc_backward_filter(gb, xb, kh, kw)
+    assert float((y * dy).sum()) == float((w.astype(np.float64) * dw).sum())  # <y(w), dy> = <w, dw>, exact
+    xf = synth.normal(153, B * H * W * cin).reshape(B, H, W, cin)
+    gf = synth.normal(154, B * OH * OW * cout).reshape(B, OH, OW, cout)
+    xb, gb = oracle.to_bf16_bits(xf), oracle.to_bf16_bits(gf)
+    dw, mag = oracle.conv2d_mc_backward_filter(gb, xb, kh, kw)
+    xt = torch.tensor(oracle.bf16_bits_to_f32(xb), dtype=torch.float64).permute(0, 3, 1, 2)
+    gt = torch.tensor(oracle.bf16_bits_to_f32(gb), dtype=torch.float64).permute(0, 3, 1, 2)
+    ref = torch.nn.grad.conv2d_weight(xt, (cout, cin, kh, kw), gt).numpy()
+    np.testing.assert_allclose(dw, ref, rtol=1e-12, atol=1e-12)
+    refm = torch.nn.grad.conv2d_weight(xt.abs(), (cout, cin, kh, kw), gt.abs()).numpy()
+    np.testing.assert_allclose(mag, refm, rtol=1e-12, atol=1e-12)
+    # one image row (H = kh = 1): the 1-D multi-channel filter gradient
+    x1 = oracle.to_bf16_bits(synth.normal(155, B * 1 * W * cin).reshape(B, 1, W, cin))
+    g1 = oracle.to_bf16_bits(synth.normal(156, B * 1 * (W - 2) * cout).reshape(B, 1, W - 2, cout))
+    dw2, m2 = oracle.conv2d_mc_backward_filter(g1, x1, 1, 3)
+    dw1, m1 = oracle.conv1d_mc_backward_filter(g1[:, 0], x1[:, 0], 3)
+    np.testing.assert_array_equal(dw2[:, :, 0], dw1)
+    np.testing.assert_array_equal(m2[:, :, 0], m1)
