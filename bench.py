@@ -218,6 +218,9 @@ def cfg_cells(workload: str, cfg5_log2n: int = 32):
                                 shard="image")
         wf = synth.normal(103, 64 * 64 * 9, sigma=(64 * 9) ** -0.5).reshape(64, 64, 3, 3)
         cells.append(Cell("mc", "mc2d_dx_56x56_c64x64_3x3", "conv2d_mc_bwd_in", kh=3, kw=3, f=wf, inp="g2mc56"))
+        # and its filter gradient (reading R27): dy [128][54][54][64] and x [128][56][56][64] -> dw [64][64][3][3]
+        cells.append(Cell("mc", "mc2d_dw_56x56_c64x64_3x3", "conv2d_mc_bwd_f", kh=3, kw=3, inp="g2mc56",
+                          inp2="x2mc56"))
     if workload == "backward":  # backward passes on config-3 / config-4 shapes; not a BJ config
         inputs["xb"] = dict(rows=64, n=1 << 20, dtype="float32", dist="normal", seed=3, kw={}, shard="batch")
         for k in (7, 31, 63):
@@ -459,6 +462,17 @@ class Runner:
             c.bytes = rows * L * cout * 2 + c.n_out * 4 + cout * cin * k * 2
             c.flops = 2 * k * cout * c.n_out
             return torch.empty((rows, N, cin), dtype=torch.float32, device=self.device)
+        if c.op == "conv2d_mc_bwd_f":
+            B, OH, OW, cout = geo
+            H, W = OH + c.kh - 1, OW + c.kw - 1
+            cin = 64
+            need = self.ss.ss_conv2d_mc_backward_filter_workspace(cin, cout, c.kh, c.kw)
+            if c.name not in self.ws:
+                self.ws[c.name] = torch.empty(max(need, 8), dtype=torch.uint8, device=self.device)
+            c.n_out = B * OH * OW * cout  # dy elements consumed
+            c.bytes = B * OH * OW * cout * 2 + B * H * W * cin * 2 + cout * cin * c.kh * c.kw * 4
+            c.flops = 2 * c.kh * c.kw * cin * cout * B * OH * OW
+            return torch.empty((cout, cin, c.kh, c.kw), dtype=torch.float32, device=self.device)
         if c.op == "conv2d_mc_bwd_in":
             B, OH, OW, cout = geo
             cin = c.f.shape[1]
@@ -651,6 +665,13 @@ class Runner:
             L = n // c.kw
             ss.check(ss.ss_conv1d_mc_backward_input(x.data_ptr(), self.wmc[c.name].data_ptr(), y.data_ptr(), rows,
                                                     L + c.w - 1, c.kh, c.kw, c.w, self.stream.cuda_stream))
+        elif c.op == "conv2d_mc_bwd_f":
+            B, OH, OW, cout = geo
+            xm = xd[c.inp2]
+            need = ss.ss_conv2d_mc_backward_filter_workspace(64, cout, c.kh, c.kw)
+            ss.check(ss.ss_conv2d_mc_backward_filter(x.data_ptr(), xm.data_ptr(), y.data_ptr(), B, OH + c.kh - 1,
+                                                     OW + c.kw - 1, 64, cout, c.kh, c.kw,
+                                                     self.ws[c.name].data_ptr(), need, self.stream.cuda_stream))
         elif c.op == "conv2d_mc_bwd_in":
             B, OH, OW, cout = geo
             ss.check(ss.ss_conv2d_mc_backward_input(x.data_ptr(), self.wmc[c.name].data_ptr(), y.data_ptr(), B,
@@ -1054,7 +1075,8 @@ def run_ours(args):
         d = {"cell": c.name, "avg_ms": round(avg_ms, 5), "n_out": c.n_out, "bytes": c.bytes,
              "gelem_s": round(c.n_out / (avg_ms * 1e-3) / 1e9, 2), "gbs": round(gbs, 1),
              "frac_hbm": round(gbs / peak_hbm, 4), "frac_8tbs": round(gbs / 8000.0, 4), "share": 0.0}
-        if c.op in ("conv_mc", "conv2d_mc", "conv_mc_bwd_in", "conv_mc_bwd_f", "conv2d_mc_bwd_in"):
+        if c.op in ("conv_mc", "conv2d_mc", "conv_mc_bwd_in", "conv_mc_bwd_f", "conv2d_mc_bwd_in",
+                    "conv2d_mc_bwd_f"):
             d["tc_frac"] = round(c.flops / (avg_ms * 1e-3) / 1e12 / (2 * tf32_peak_tflops()), 4)  # bf16 peak
         elif conv_on_tensor_cores(c):
             d["tc_frac"] = round(c.n_out * TC_FLOP_PER_OUT / (avg_ms * 1e-3) / 1e12 / tf32_peak_tflops(), 4)
@@ -1080,7 +1102,7 @@ def run_ours(args):
                     "unit": "GB/s", "frac": dom["frac_hbm"], "peak_source": peak_src, "traffic": None,
                     "frac_8tbs": dom["frac_8tbs"]}
         if "tc_frac" in dom and dom_cell.op in ("conv_mc", "conv2d_mc", "conv_mc_bwd_in", "conv_mc_bwd_f",
-                                                "conv2d_mc_bwd_in"):
+                                                "conv2d_mc_bwd_in", "conv2d_mc_bwd_f"):
             roofline["tensor_frac"] = dom["tc_frac"]
             roofline["tensor_peak_tflops"] = round(2 * tf32_peak_tflops(), 1)
             roofline["tensor_note"] = "bf16 MMA work (2 k Cin flop/output) / measured dense bf16 peak"
@@ -1260,6 +1282,12 @@ def oracle_sample_plan(workload: str, frac: float):
             wb = oracle.to_bf16_bits(c.f)
             plan.append((c, _rows_task(xb, lambda xi, wb=wb: oracle.conv2d_mc(xi, wb),
                                        (hw - 2) * (hw - 2) * c.f.shape[0])))
+        elif c.cfg == "mc" and c.op == "conv2d_mc_bwd_f":
+            imgs = max(1, int(round(128 * frac)))
+            gb = oracle.to_bf16_bits(synth.normal(104, imgs * 54 * 54 * 64).reshape(imgs, 54, 54, 64))
+            xb = oracle.to_bf16_bits(synth.normal(102, imgs * 56 * 56 * 64).reshape(imgs, 56, 56, 64))
+            plan.append((c, _whole_task(lambda gb=gb, xb=xb, imgs=imgs: (
+                oracle.conv2d_mc_backward_filter(gb, xb, 3, 3), imgs * 54 * 54 * 64)[1])))
         elif c.cfg == "mc" and c.op == "conv2d_mc_bwd_in":
             imgs = max(1, int(round(128 * frac)))
             gb = oracle.to_bf16_bits(synth.normal(104, imgs * 54 * 54 * 64).reshape(imgs, 54, 54, 64))

@@ -70,7 +70,7 @@
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 12
+#define SS_ABI_VERSION 13
 
 typedef enum { SS_F32 = 0, SS_I32 = 1 } ss_dtype_t;
 typedef enum { SS_POOL_MAX = 0, SS_POOL_AVG = 1 } ss_pool_mode_t;
@@ -293,6 +293,26 @@ ss_status_t ss_conv2d_mc(const void* x, const void* w, float* y, int64_t batch, 
  * (kh > H or kw > W -> SS_ERR_WINDOW_EXCEEDS_INPUT). */
 ss_status_t ss_conv2d_mc_backward_input(const void* dy, const void* w, float* dx, int64_t batch, int64_t H,
                                         int64_t W, int64_t cin, int64_t cout, int64_t kh, int64_t kw, void* stream);
+
+/* Filter gradient of ss_conv2d_mc (reading R27):
+ *   dw[co][ci][a][e] = sum_b sum_{r < H-kh+1} sum_{c < W-kw+1} dy[b][r][c][co] * x[b][r+a][c+e][ci].
+ * dy is [batch][H-kh+1][W-kw+1][cout] bfloat16, x the forward's [batch][H][W][cin]
+ * bfloat16, dw [cout][cin][kh][kw] fp32 (torch weight order), fully overwritten; all
+ * DEVICE memory.  workspace: caller-owned device memory of at least
+ * ss_conv2d_mc_backward_filter_workspace(cin, cout, kh, kw) bytes (8-byte aligned;
+ * may be NULL when that is 0), not overlapping dy, x or dw; its contents are
+ * scratch.  cin = 64 with cout = 64 (kw <= 4) or 128 (kw <= 2), kh <= 64, W <= 128
+ * and 16-B aligned dy / x run on the tensor cores: a tile is R = floor(128 / W) dy
+ * rows staged with pitch W (the 5-D TMA box runs past the row's W-kw+1 outputs and
+ * zero-fills) against the x rows the tap row reads, as the 1-D filter gradient
+ * below, with the CTAs split over the kh tap rows; numerics as that function
+ * (fp32 per 128-position tile and 32-tile run, fp64 across runs and CTAs, a
+ * fixed order: deterministic).  Other shapes run a direct kernel (double).
+ * Statuses as ss_conv2d_mc; workspace too small -> SS_ERR_BAD_SIZE. */
+size_t ss_conv2d_mc_backward_filter_workspace(int64_t cin, int64_t cout, int64_t kh, int64_t kw);
+ss_status_t ss_conv2d_mc_backward_filter(const void* dy, const void* x, float* dw, int64_t batch, int64_t H,
+                                         int64_t W, int64_t cin, int64_t cout, int64_t kh, int64_t kw,
+                                         void* workspace, size_t workspace_bytes, void* stream);
 
 /* Input gradient of ss_conv1d_mc (the vector-Jacobian product of the channel-summed
  * sliding dot product; reading R23):

@@ -47,7 +47,7 @@ EXPORTED = ("ss_abi_version", "ss_out_len", "ss_pool_sum", "ss_pool_max", "ss_po
             "ss_pool2d_backward", "ss_conv2d", "ss_conv2d_backward_input", "ss_conv2d_backward_filter_workspace",
             "ss_conv2d_backward_filter", "ss_conv1d_mc", "ss_conv2d_mc", "ss_conv1d_mc_backward_input",
             "ss_conv1d_mc_backward_filter_workspace", "ss_conv1d_mc_backward_filter",
-            "ss_conv2d_mc_backward_input")
+            "ss_conv2d_mc_backward_input", "ss_conv2d_mc_backward_filter_workspace", "ss_conv2d_mc_backward_filter")
 
 
 class SSError(RuntimeError):
@@ -105,6 +105,10 @@ def _load() -> ctypes.CDLL:
     L.ss_conv1d_mc_backward_input.restype = i32
     L.ss_conv2d_mc_backward_input.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i64, vp]
     L.ss_conv2d_mc_backward_input.restype = i32
+    L.ss_conv2d_mc_backward_filter_workspace.argtypes = [i64, i64, i64, i64]
+    L.ss_conv2d_mc_backward_filter_workspace.restype = ctypes.c_size_t
+    L.ss_conv2d_mc_backward_filter.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, ctypes.c_size_t, vp]
+    L.ss_conv2d_mc_backward_filter.restype = i32
     L.ss_conv1d_mc_backward_filter_workspace.argtypes = [i64, i64, i64]
     L.ss_conv1d_mc_backward_filter_workspace.restype = ctypes.c_size_t
     L.ss_conv1d_mc_backward_filter.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, vp, ctypes.c_size_t, vp]
@@ -273,6 +277,16 @@ def ss_conv1d_mc_backward_input(dy_ptr, w_ptr, dx_ptr, batch, N, cin, cout, k, s
 
 def ss_conv2d_mc_backward_input(dy_ptr, w_ptr, dx_ptr, batch, H, W, cin, cout, kh, kw, stream=0) -> int:
     return _lib.ss_conv2d_mc_backward_input(dy_ptr, w_ptr, dx_ptr, batch, H, W, cin, cout, kh, kw, stream)
+
+
+def ss_conv2d_mc_backward_filter_workspace(cin, cout, kh, kw) -> int:
+    return _lib.ss_conv2d_mc_backward_filter_workspace(cin, cout, kh, kw)
+
+
+def ss_conv2d_mc_backward_filter(dy_ptr, x_ptr, dw_ptr, batch, H, W, cin, cout, kh, kw, ws_ptr, ws_bytes,
+                                 stream=0) -> int:
+    return _lib.ss_conv2d_mc_backward_filter(dy_ptr, x_ptr, dw_ptr, batch, H, W, cin, cout, kh, kw, ws_ptr, ws_bytes,
+                                             stream)
 
 
 def ss_conv1d_mc_backward_filter_workspace(cin, cout, k) -> int:
@@ -723,5 +737,30 @@ def conv1d_mc_backward_filter(dy, x, k, out=None, workspace=None, stream=None):
     need = ss_conv1d_mc_backward_filter_workspace(cin, cout, k)
     ws = _workspace(workspace, need, dy.device) if need else None
     check(ss_conv1d_mc_backward_filter(dy.data_ptr(), x.data_ptr(), dw.data_ptr(), B, N, cin, cout, k,
+                                       ws.data_ptr() if ws is not None else 0, need, _stream(stream)))
+    return dw
+
+
+def conv2d_mc_backward_filter(dy, x, kh, kw, out=None, workspace=None, stream=None):
+    """Filter gradient of conv2d_mc: dy [B, H-kh+1, W-kw+1, Cout] and x [B, H, W, Cin] bfloat16 (CUDA) -> dw
+    [Cout, Cin, kh, kw] float32 (torch conv2d weight order).  `workspace`: optional preallocated uint8 CUDA
+    tensor of at least ss_conv2d_mc_backward_filter_workspace(Cin, Cout, kh, kw) bytes."""
+    torch = _torch()
+    _dev(dy, "dy", torch.bfloat16)
+    _dev(x, "x", torch.bfloat16, device=dy.device)
+    if dy.dim() != 4 or x.dim() != 4:
+        raise ValueError("dy must be [B, H-kh+1, W-kw+1, Cout] and x [B, H, W, Cin]")
+    B, OH, OW, cout = dy.shape
+    B2, H, W, cin = x.shape
+    if B2 != B:
+        raise ValueError("dy and x batch sizes differ")
+    if kh > H or kw > W:
+        raise SSError(SS_ERR_WINDOW_EXCEEDS_INPUT, f"window {kh}x{kw} exceeds input {H}x{W}")
+    if OH != H - kh + 1 or OW != W - kw + 1:
+        raise ValueError(f"dy is {OH}x{OW}, expected {H - kh + 1}x{W - kw + 1}")
+    dw = _alloc(out, (cout, cin, kh, kw), torch.float32, dy.device)
+    need = ss_conv2d_mc_backward_filter_workspace(cin, cout, kh, kw)
+    ws = _workspace(workspace, need, dy.device) if need else None
+    check(ss_conv2d_mc_backward_filter(dy.data_ptr(), x.data_ptr(), dw.data_ptr(), B, H, W, cin, cout, kh, kw,
                                        ws.data_ptr() if ws is not None else 0, need, _stream(stream)))
     return dw

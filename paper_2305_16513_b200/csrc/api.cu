@@ -960,6 +960,51 @@ ss_status_t ss_conv2d_mc_backward_input(const void* dy, const void* w, float* dx
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv2d_mc_backward_input launch");
 }
 
+size_t ss_conv2d_mc_backward_filter_workspace(int64_t cin, int64_t cout, int64_t kh, int64_t kw) {
+  if (kh < 1 || kh > 64) return 0;
+  return mc_filter_grad_workspace(cin, cout, kw, current_sms());
+}
+
+ss_status_t ss_conv2d_mc_backward_filter(const void* dy, const void* x, float* dw, int64_t batch, int64_t H,
+                                         int64_t W, int64_t cin, int64_t cout, int64_t kh, int64_t kw,
+                                         void* workspace, size_t workspace_bytes, void* stream) {
+  if (!dy || !x || !dw) return fail(SS_ERR_NULL, "dy, x and dw must be non-NULL device pointers");
+  if (batch < 1 || H < 1 || W < 1 || cin < 1 || cout < 1 || kh < 1 || kw < 1)
+    return fail(SS_ERR_BAD_SIZE, "batch/H/W/cin/cout/kh/kw must all be >= 1");
+  if (H > INT64_MAX / 8 / W || H * W > INT64_MAX / 8 / batch || batch * H * W > INT64_MAX / 8 / cin ||
+      batch * H * W > INT64_MAX / 8 / cout || kh * kw > INT64_MAX / 8 / cin / cout)
+    return fail(SS_ERR_BAD_SIZE, "sizes overflow int64");
+  if (kh > H || kw > W)
+    return fail(SS_ERR_WINDOW_EXCEEDS_INPUT, "window %lldx%lld exceeds input %lldx%lld", (long long)kh, (long long)kw,
+                (long long)H, (long long)W);
+  if ((reinterpret_cast<uintptr_t>(dy) & 1) || (reinterpret_cast<uintptr_t>(x) & 1) ||
+      (reinterpret_cast<uintptr_t>(dw) & 3))
+    return fail(SS_ERR_BAD_SIZE, "dy / x must be 2-byte and dw 4-byte aligned");
+  const int64_t OH = H - kh + 1, OW = W - kw + 1;
+  const int sms = current_sms();
+  const size_t need = ss_conv2d_mc_backward_filter_workspace(cin, cout, kh, kw);
+  if (need && (!workspace || workspace_bytes < need))
+    return fail(SS_ERR_BAD_SIZE, "workspace of %zu bytes needed (ss_conv2d_mc_backward_filter_workspace)", need);
+  const int64_t nw = cout * cin * kh * kw * 4, ndy = batch * OH * OW * cout * 2, nx = batch * H * W * cin * 2;
+  if (overlaps(dw, nw, dy, ndy) || overlaps(dw, nw, x, nx) ||
+      (need && (overlaps(workspace, (int64_t)need, dy, ndy) || overlaps(workspace, (int64_t)need, x, nx) ||
+                overlaps(workspace, (int64_t)need, dw, nw))))
+    return fail(SS_ERR_OVERLAP, "dw / workspace overlap an input");
+  McFgradParams p;
+  memset(&p, 0, sizeof p);
+  p.dy = static_cast<const uint16_t*>(dy); p.x = static_cast<const uint16_t*>(x); p.dw = dw;
+  p.ws = static_cast<double*>(workspace);
+  p.batch = batch; p.N = H * W; p.L = OH * OW; p.cin = cin; p.cout = cout; p.k = kw;
+  p.two_d = 1; p.kh = (int)(kh < 1024 ? kh : 1024); p.H = H; p.W = W; p.OH = OH; p.OW = OW;
+  // dy rows staged with pitch W (the box runs past OW: zero fill) against x rows shifted by the tap row
+  const bool tc = need && (reinterpret_cast<uintptr_t>(dy) & 15) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(workspace) & 7) == 0 && mc_filter_grad_2d_plan(p) &&
+                  encode_mc_map_2d(&p.tm_dy, dy, batch, OH, OW, cout, (int)W, p.R) &&
+                  encode_mc_map_2d(&p.tm_x, x, batch, H, W, cin, (int)W, p.R + 1);
+  cudaError_t e = launch_mc_filter_grad(p, tc, static_cast<cudaStream_t>(stream), sms);
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv2d_mc_backward_filter launch");
+}
+
 ss_status_t ss_conv2d(const void* x, void* y, int64_t planes, int64_t H, int64_t W, const float* filter_host,
                       int64_t kh, int64_t kw, int64_t sh, int64_t sw, ss_dtype_t dtype, void* stream) {
   if (!x || !y || !filter_host) return fail(SS_ERR_NULL, "x, y and filter_host must be non-NULL");

@@ -85,7 +85,23 @@ __device__ __forceinline__ void mf_tma_4d(void* dst, const CUtensorMap* map, int
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void mf_ld32(uint32_t taddr, uint32_t* v) {
+__device__ __forceinline__ void mf_tma_5d(void* dst, const CUtensorMap* map, int32_t c1, int32_t c2, int32_t c3,
+                                          int32_t c4, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mf_ld16(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ __attribute__((unused)) void mf_ld32(uint32_t taddr, uint32_t* v) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
       "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -97,7 +113,7 @@ __device__ __forceinline__ void mf_ld32(uint32_t taddr, uint32_t* v) {
       : "memory");
 }
 
-constexpr size_t mf_stage_bytes(int64_t cout) { return (size_t)(cout / 64) * 16384u + kMfXBytes; }
+constexpr size_t mf_stage_bytes(int64_t cout, int xrows) { return (size_t)(cout / 64) * 16384u + (size_t)xrows * 128u; }
 constexpr size_t mf_smem(size_t stage, int stages) { return 1024 + (size_t)stages * stage + 256; }
 
 }  // namespace
@@ -106,7 +122,7 @@ template <int COUT, int KT>
 __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const __grid_constant__ McFgradParams p) {
   constexpr int AT = COUT / 64;  // dy atoms (64 channels each)
   constexpr uint32_t kDyBytes = AT * 16384u;
-  constexpr uint32_t kStage = kDyBytes + kMfXBytes;
+  const uint32_t kStage = kDyBytes + (uint32_t)p.xrows * 128u;
   extern __shared__ __align__(16) uint8_t mf_raw[];
   uint8_t* smem = mf_raw + ((1024u - (smem_u32(mf_raw) & 1023u)) & 1023u);
   constexpr int NC = 64 * KT, NH = NC / 2;  // accumulator columns (tap j at 64 j); per epilogue warp
@@ -118,6 +134,10 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
   uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = p.ntiles, tpr = p.tiles_per_row;
+  // units: tiles t0, t0 + tstep, ...; 2-D: CTA c serves tap row ta = c % kh over every kh-th CTA's tiles
+  const int ta = p.two_d ? (int)(blockIdx.x % (unsigned)p.kh) : 0;
+  const int64_t t0 = p.two_d ? blockIdx.x / (unsigned)p.kh : blockIdx.x;
+  const int64_t tstep = p.two_d ? gridDim.x / (unsigned)p.kh : gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMfStages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
@@ -125,6 +145,19 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
     fence_mbar_init();
     prefetch_tmap(&p.tm_dy);
     prefetch_tmap(&p.tm_x);
+  }
+  // staged rows no box writes (2-D: dy rows past R W, x rows past (R + 1) W) meet zero dy or are never
+  // multiplied, but must be finite: zero them once
+  if (p.dy_rows < 128 || p.x_rows < p.xrows) {
+    for (int s = 0; s < kMfStages; ++s) {
+      uint8_t* st = smem + (size_t)s * kStage;
+      for (int a = 0; a < AT; ++a)
+        for (int i = p.dy_rows * 32 + (int)threadIdx.x; i < 128 * 32; i += kMfThreads)
+          reinterpret_cast<uint32_t*>(st + a * 16384u)[i] = 0u;
+      for (int i = p.x_rows * 32 + (int)threadIdx.x; i < p.xrows * 32; i += kMfThreads)
+        reinterpret_cast<uint32_t*>(st + kDyBytes)[i] = 0u;
+    }
+    fence_proxy_async_smem();
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
@@ -139,16 +172,24 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int it = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      for (int64_t tile = t0; tile < ntiles; tile += tstep, ++it) {
         const int s = it % kMfStages;
         mf_wait(empty + s, ((uint32_t)(it / kMfStages) & 1u) ^ 1u);  // commit-driven: poll
-        const int64_t b = tile / tpr;
-        const int32_t t0 = (int32_t)((tile - b * tpr) * kMfTileP);
         uint8_t* st = smem + (size_t)s * kStage;
-        mbar_arrive_expect_tx(full + s, kStage);
+        mbar_arrive_expect_tx(full + s, p.tx);
+        if (p.two_d) {  // dy rows r0 .. r0 + R - 1 (pitch W), x rows r0 + ta .. r0 + ta + R
+          const int64_t b = tile / p.nrt;
+          const int32_t r0 = (int32_t)((tile - b * p.nrt) * p.R);
 #pragma unroll
-        for (int a = 0; a < AT; ++a) mf_tma_4d(st + a * 16384u, &p.tm_dy, 0, t0, a, (int32_t)b, full + s);
-        mf_tma_4d(st + kDyBytes, &p.tm_x, 0, t0, 0, (int32_t)b, full + s);
+          for (int a = 0; a < AT; ++a) mf_tma_5d(st + a * 16384u, &p.tm_dy, 0, r0, a, (int32_t)b, full + s);
+          mf_tma_5d(st + kDyBytes, &p.tm_x, 0, r0 + ta, 0, (int32_t)b, full + s);
+        } else {
+          const int64_t b = tile / tpr;
+          const int32_t p0 = (int32_t)((tile - b * tpr) * kMfTileP);
+#pragma unroll
+          for (int a = 0; a < AT; ++a) mf_tma_4d(st + a * 16384u, &p.tm_dy, 0, p0, a, (int32_t)b, full + s);
+          mf_tma_4d(st + kDyBytes, &p.tm_x, 0, p0, 0, (int32_t)b, full + s);
+        }
       }
     }
   } else if (warp == 1) {
@@ -159,7 +200,7 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
     const uint32_t s0 = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
     int it = 0, d = 0;
     uint32_t dph = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    for (int64_t tile = t0; tile < ntiles; tile += tstep, ++it) {
       const int s = it % kMfStages;
       mf_wait(full + s, (uint32_t)(it / kMfStages) & 1u);
       mf_wait(dempty + d, dph ^ 1u);
@@ -184,7 +225,7 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
     // flushes straight from registers, coalesced); each thread owns (co, [cb, cb + NH))
     double* W = p.ws + (size_t)blockIdx.x * COUT * NC + (size_t)cb * COUT + co;
     const bool owner = COUT == 128 || lane < 16;  // M = 64: lanes 0-15 of each quarter are the rows
-    if (owner && (int64_t)blockIdx.x >= ntiles)  // no tiles: the slice is zero
+    if (owner && t0 >= ntiles)  // no tiles: the slice is zero
       for (int i = 0; i < NH; ++i) W[(size_t)i * COUT] = 0.0;
     bool first = true;  // the first run is stored, later runs are added (fire-and-forget reductions)
     // the fp32 run lives in registers: row co, columns [cb, cb + NH) (tcgen05.ld 32x32b: lane = row)
@@ -193,21 +234,21 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
     for (int i = 0; i < NH; ++i) acc[i] = 0.0f;
     int d = 0, nt = 0;
     uint32_t dph = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int64_t tile = t0; tile < ntiles; tile += tstep) {
       mf_wait(dfull + d, dph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-      for (int c0 = 0; c0 < NH; c0 += 32) {
-        uint32_t v[32];
-        mf_ld32(tmem + lanebits + (uint32_t)(d * NC + cb + c0), v);
+      for (int c0 = 0; c0 < NH; c0 += 16) {  // x16: acc + v stay under the 10-warp CTA's 168-register cap
+        uint32_t v[16];
+        mf_ld16(tmem + lanebits + (uint32_t)(d * NC + cb + c0), v);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int i = 0; i < 32; ++i) acc[c0 + i] += __uint_as_float(v[i]);
+        for (int i = 0; i < 16; ++i) acc[c0 + i] += __uint_as_float(v[i]);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(dempty + d);
-      if (++nt == kMfRunTiles || tile + gridDim.x >= ntiles) {  // end of a run: into the fp64 slice
+      if (++nt == kMfRunTiles || tile + tstep >= ntiles) {  // end of a run: into the fp64 slice
         nt = 0;
         if (owner) {
           // one thread owns each slot and issues its writes in program order, so the additions land in
@@ -284,6 +325,33 @@ __global__ void __launch_bounds__(256) mc_filter_grad_direct_kernel(const __grid
   }
 }
 
+// 2-D direct kernel: as above over the positions (b, r, c) of dy, tap (a, e).
+__global__ void __launch_bounds__(256) mc_filter_grad2d_direct_kernel(const __grid_constant__ McFgradParams p) {
+  __shared__ double red[256];
+  const uint16_t* __restrict__ dy = p.dy;
+  const uint16_t* __restrict__ x = p.x;
+  const int64_t kw = p.k, kh = p.H - p.OH + 1, taps = kh * kw;
+  const int64_t total = p.cout * p.cin * taps, npos = p.batch * p.OH * p.OW;
+  for (int64_t o = blockIdx.x; o < total; o += gridDim.x) {
+    const int64_t e = o % kw, a = (o / kw) % kh, ci = (o / taps) % p.cin, co = o / (taps * p.cin);
+    double s = 0.0;
+    for (int64_t q = threadIdx.x; q < npos; q += blockDim.x) {
+      const int64_t c = q % p.OW, rb = q / p.OW, r = rb % p.OH, b = rb / p.OH;
+      const float g = __uint_as_float((uint32_t)__ldg(dy + q * p.cout + co) << 16);
+      const float xv = __uint_as_float((uint32_t)__ldg(x + ((b * p.H + r + a) * p.W + c + e) * p.cin + ci) << 16);
+      s += (double)g * (double)xv;
+    }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+      if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) p.dw[o] = (float)red[0];
+    __syncthreads();
+  }
+}
+
 bool mc_filter_grad_tc_supported(int64_t cin, int64_t cout, int64_t k) {
   return cin == 64 && ((cout == 64 && k <= 4) || (cout == 128 && k <= 2)) && k >= 1;
 }
@@ -293,11 +361,32 @@ size_t mc_filter_grad_workspace(int64_t cin, int64_t cout, int64_t k, int sms) {
   return (size_t)sms * cout * 64 * k * sizeof(double);
 }
 
+// 2-D tiling: R = the most dy rows of pitch W that fit 128 positions, balanced over the image's rows
+bool mc_filter_grad_2d_plan(McFgradParams& p) {
+  if (!mc_filter_grad_tc_supported(p.cin, p.cout, p.k) || p.W > 128 || p.kh < 1 || p.kh > 64) return false;
+  const int64_t rmax = 128 / p.W, nt = (p.OH + rmax - 1) / rmax;
+  p.R = (int)((p.OH + nt - 1) / nt);
+  p.nrt = (p.OH + p.R - 1) / p.R;
+  p.dy_rows = (int)(p.R * p.W);
+  p.x_rows = (int)((p.R + 1) * p.W);
+  const int reach = 128 + (int)p.k - 1;
+  p.xrows = ((p.x_rows > reach ? p.x_rows : reach) + 7) / 8 * 8;
+  p.tx = (uint32_t)((p.cout / 64) * p.dy_rows * 128 + p.x_rows * 128);
+  return p.xrows <= 256;
+}
+
 cudaError_t launch_mc_filter_grad(McFgradParams& p, bool tc, cudaStream_t stream, int sms) {
   if (tc) {
-    p.tiles_per_row = (p.L + kMfTileP - 1) / kMfTileP;
-    p.ntiles = p.batch * p.tiles_per_row;
-    const int ctas = sms;
+    int ctas = sms;
+    if (p.two_d) {  // planned by mc_filter_grad_2d_plan; kh CTA groups
+      p.ntiles = p.batch * p.nrt;
+      ctas = sms / p.kh * p.kh;
+    } else {
+      p.tiles_per_row = (p.L + kMfTileP - 1) / kMfTileP;
+      p.ntiles = p.batch * p.tiles_per_row;
+      p.kh = 1; p.xrows = kMfXRows; p.dy_rows = 128; p.x_rows = kMfXRows;
+      p.tx = (uint32_t)mf_stage_bytes(p.cout, kMfXRows);
+    }
     const void* kfn = nullptr;
     const int k = (int)p.k;
     if (p.cout == 128) kfn = k == 1 ? reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<128, 1>)
@@ -306,25 +395,26 @@ cudaError_t launch_mc_filter_grad(McFgradParams& p, bool tc, cudaStream_t stream
                : k == 2 ? reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<64, 2>)
                : k == 3 ? reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<64, 3>)
                         : reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<64, 4>);
-    const size_t stage = mf_stage_bytes(p.cout);
+    const size_t stage = mf_stage_bytes(p.cout, p.xrows);
     p.stages = (int)((kSmemBudget - 1024 - 256) / stage);
     if (p.stages > kMfMaxStages) p.stages = kMfMaxStages;
-    if (p.stages < 2) return cudaErrorInvalidConfiguration;
     const size_t smem = mf_smem(stage, p.stages);
-    if (smem > (size_t)kSmemBudget) return cudaErrorInvalidConfiguration;
+    if (p.stages < 2 || smem > (size_t)kSmemBudget || ctas < p.kh) return cudaErrorInvalidConfiguration;
     cudaError_t e = ensure_smem_attr(kfn);
     if (e != cudaSuccess) return e;
     void* args[] = {&p};
     e = cudaLaunchKernel(kfn, dim3((unsigned)ctas), dim3(kMfThreads), args, smem, stream);
     note_launch();
     if (e != cudaSuccess) return e;
-    mc_filter_grad_finish<<<(unsigned)(64 * p.k), 1024, 0, stream>>>(p.ws, ctas, (int)p.cout, 1, (int)p.k, p.dw);
+    mc_filter_grad_finish<<<(unsigned)(64 * p.k * p.kh), 1024, 0, stream>>>(p.ws, ctas, (int)p.cout, p.kh, (int)p.k,
+                                                                         p.dw);
     note_launch();
     return cudaGetLastError();
   }
-  const int64_t total = p.cout * p.cin * p.k;
+  const int64_t total = p.cout * p.cin * p.k * (p.two_d ? p.H - p.OH + 1 : 1);
   const int64_t g = total < (int64_t)sms * 32 ? total : (int64_t)sms * 32;
-  mc_filter_grad_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
+  if (p.two_d) mc_filter_grad2d_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
+  else mc_filter_grad_direct_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, stream>>>(p);
   note_launch();
   return cudaGetLastError();
 }

@@ -309,8 +309,15 @@ struct alignas(64) McFgradParams {
   int64_t batch, N, L, cin, cout, k;
   int64_t tiles_per_row, ntiles;  // set by the launcher
   int stages;                     // set by the launcher
+  // 2-D (reading R27; k = kw, N = H * W): a tile is R dy rows staged with pitch W (dy box {64, W, R} of
+  // the 5-D map {64, OW, OH, atoms, batch}: columns >= OW zero-filled) against x rows r0 + a .. r0 + a + R
+  // (box {64, W, R + 1}); CTA c serves tap row a = c % kh.  Staged rows past the boxes are zeroed once.
+  int two_d, kh, R, xrows, dy_rows, x_rows;  // xrows: x rows per stage (1-D: 136); rows the boxes fill
+  uint32_t tx;                               // bytes per stage the boxes deliver
+  int64_t H, W, OH, OW, nrt;                 // 2-D geometry; row tiles per image
 };
 bool mc_filter_grad_tc_supported(int64_t cin, int64_t cout, int64_t k);
+bool mc_filter_grad_2d_plan(McFgradParams& p);  // 2-D tensor-core tiling (sets R, xrows, ...); false: direct
 size_t mc_filter_grad_workspace(int64_t cin, int64_t cout, int64_t k, int sms);
 cudaError_t launch_mc_filter_grad(McFgradParams& p, bool tc, cudaStream_t stream, int sms);
 // Staged rows as the TMA boxes round them: multiple of 8, split into <= 256-row boxes of equal size

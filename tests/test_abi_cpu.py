@@ -45,7 +45,7 @@ def test_library_is_sm100a(ss):
 
 
 def test_abi_version_and_out_len(ss):
-    assert ss.ss_abi_version() == 12
+    assert ss.ss_abi_version() == 13
     assert ss.ss_out_len(10, 3, 1) == 8
     assert ss.ss_out_len(10, 3, 4) == 2
     assert ss.ss_out_len(2 ** 32, 31, 1) == 2 ** 32 - 30

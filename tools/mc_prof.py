@@ -25,6 +25,12 @@ elif which == "dw":
     dw = torch.empty(64, 64, 3, device="cuda")
     wsb = torch.empty(ss.ss_conv1d_mc_backward_filter_workspace(64, 64, 3), dtype=torch.uint8, device="cuda")
     f = lambda: ss.conv1d_mc_backward_filter(g, x, 3, out=dw, workspace=wsb)  # noqa: E731
+elif which == "dw2d":
+    g = torch.randn(128, 54, 54, 64, device="cuda").to(torch.bfloat16)
+    x = torch.randn(128, 56, 56, 64, device="cuda").to(torch.bfloat16)
+    dw = torch.empty(64, 64, 3, 3, device="cuda")
+    wsb = torch.empty(ss.ss_conv2d_mc_backward_filter_workspace(64, 64, 3, 3), dtype=torch.uint8, device="cuda")
+    f = lambda: ss.conv2d_mc_backward_filter(g, x, 3, 3, out=dw, workspace=wsb)  # noqa: E731
 elif which == "dx2d":
     g = torch.randn(128, 54, 54, 64, device="cuda").to(torch.bfloat16)
     w = (torch.randn(64, 64, 3, 3, device="cuda") / 24).to(torch.bfloat16)
