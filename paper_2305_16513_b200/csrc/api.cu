@@ -962,7 +962,7 @@ ss_status_t ss_conv2d_mc_backward_input(const void* dy, const void* w, float* dx
 
 size_t ss_conv2d_mc_backward_filter_workspace(int64_t cin, int64_t cout, int64_t kh, int64_t kw) {
   if (kh < 1 || kh > 64) return 0;
-  return mc_filter_grad_workspace(cin, cout, kw, current_sms());
+  return mc_filter_grad_workspace(cin, cout, kw, current_sms(), true);
 }
 
 ss_status_t ss_conv2d_mc_backward_filter(const void* dy, const void* x, float* dw, int64_t batch, int64_t H,
@@ -999,7 +999,7 @@ ss_status_t ss_conv2d_mc_backward_filter(const void* dy, const void* x, float* d
   // dy rows staged with pitch W (the box runs past OW: zero fill) against x rows shifted by the tap row
   const bool tc = need && (reinterpret_cast<uintptr_t>(dy) & 15) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
                   (reinterpret_cast<uintptr_t>(workspace) & 7) == 0 && mc_filter_grad_2d_plan(p) &&
-                  encode_mc_map_2d(&p.tm_dy, dy, batch, OH, OW, cout, (int)W, p.R) &&
+                  encode_mc_map_2d(&p.tm_dy, dy, batch, OH, OW, cout, (int)W, p.dy_fill / (int)W) &&
                   encode_mc_map_2d(&p.tm_x, x, batch, H, W, cin, (int)W, p.R + 1);
   cudaError_t e = launch_mc_filter_grad(p, tc, static_cast<cudaStream_t>(stream), sms);
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "conv2d_mc_backward_filter launch");

@@ -113,7 +113,9 @@ __device__ __forceinline__ __attribute__((unused)) void mf_ld32(uint32_t taddr, 
       : "memory");
 }
 
-constexpr size_t mf_stage_bytes(int64_t cout, int xrows) { return (size_t)(cout / 64) * 16384u + (size_t)xrows * 128u; }
+constexpr size_t mf_stage_bytes(int dyreg, int dyrow_cap, int xrows) {
+  return (size_t)dyreg * dyrow_cap * 128u + (size_t)xrows * 128u;
+}
 constexpr size_t mf_smem(size_t stage, int stages) { return 1024 + (size_t)stages * stage + 256; }
 
 }  // namespace
@@ -121,7 +123,8 @@ constexpr size_t mf_smem(size_t stage, int stages) { return 1024 + (size_t)stage
 template <int COUT, int KT>
 __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const __grid_constant__ McFgradParams p) {
   constexpr int AT = COUT / 64;  // dy atoms (64 channels each)
-  constexpr uint32_t kDyBytes = AT * 16384u;
+  const uint32_t kRegBytes = (uint32_t)p.dyrow_cap * 128u;  // one dy region
+  const uint32_t kDyBytes = (uint32_t)p.dyreg * kRegBytes;
   const uint32_t kStage = kDyBytes + (uint32_t)p.xrows * 128u;
   extern __shared__ __align__(16) uint8_t mf_raw[];
   uint8_t* smem = mf_raw + ((1024u - (smem_u32(mf_raw) & 1023u)) & 1023u);
@@ -134,10 +137,15 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
   uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = p.ntiles, tpr = p.tiles_per_row;
-  // units: tiles t0, t0 + tstep, ...; 2-D: CTA c serves tap row ta = c % kh over every kh-th CTA's tiles
-  const int ta = p.two_d ? (int)(blockIdx.x % (unsigned)p.kh) : 0;
-  const int64_t t0 = p.two_d ? blockIdx.x / (unsigned)p.kh : blockIdx.x;
-  const int64_t tstep = p.two_d ? gridDim.x / (unsigned)p.kh : gridDim.x;
+  // units: tiles t0, t0 + tstep, ...; 2-D: CTA c is in group c % groups, which serves tap row ta (and,
+  // paired, ta - 1 through a second dy region one image row down: an M = 128 accumulator)
+  const int grp = p.two_d ? (int)(blockIdx.x % (unsigned)p.groups) : 0;
+  const bool paired = p.pair && 2 * grp + 1 <= p.kh - 1;
+  const int ta = p.pair ? (2 * grp + 1 < p.kh - 1 ? 2 * grp + 1 : p.kh - 1) : grp;
+  const int64_t t0 = p.two_d ? blockIdx.x / (unsigned)p.groups : blockIdx.x;
+  const int64_t tstep = p.two_d ? gridDim.x / (unsigned)p.groups : gridDim.x;
+  const bool m128 = COUT == 128 || paired;  // accumulator rows: all 128 lanes, else lanes 0-15 per quarter
+  const int nreg = paired ? p.dyreg : AT;   // dy regions this CTA loads
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMfStages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
@@ -148,12 +156,12 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
   }
   // staged rows no box writes (2-D: dy rows past R W, x rows past (R + 1) W) meet zero dy or are never
   // multiplied, but must be finite: zero them once
-  if (p.dy_rows < 128 || p.x_rows < p.xrows) {
+  if (p.dy_fill < p.dyrow_cap || p.x_rows < p.xrows) {
     for (int s = 0; s < kMfStages; ++s) {
       uint8_t* st = smem + (size_t)s * kStage;
-      for (int a = 0; a < AT; ++a)
-        for (int i = p.dy_rows * 32 + (int)threadIdx.x; i < 128 * 32; i += kMfThreads)
-          reinterpret_cast<uint32_t*>(st + a * 16384u)[i] = 0u;
+      for (int a = 0; a < p.dyreg; ++a)
+        for (int i = p.dy_fill * 32 + (int)threadIdx.x; i < p.dyrow_cap * 32; i += kMfThreads)
+          reinterpret_cast<uint32_t*>(st + a * kRegBytes)[i] = 0u;
       for (int i = p.x_rows * 32 + (int)threadIdx.x; i < p.xrows * 32; i += kMfThreads)
         reinterpret_cast<uint32_t*>(st + kDyBytes)[i] = 0u;
     }
@@ -176,12 +184,12 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
         const int s = it % kMfStages;
         mf_wait(empty + s, ((uint32_t)(it / kMfStages) & 1u) ^ 1u);  // commit-driven: poll
         uint8_t* st = smem + (size_t)s * kStage;
-        mbar_arrive_expect_tx(full + s, p.tx);
-        if (p.two_d) {  // dy rows r0 .. r0 + R - 1 (pitch W), x rows r0 + ta .. r0 + ta + R
+        mbar_arrive_expect_tx(full + s, (uint32_t)nreg * p.tx_dy + p.tx_x);
+        if (p.two_d) {  // dy rows r0 .. r0 + R - 1 (pitch W; paired: and r0 + 1 ..), x rows r0 + ta .. r0 + ta + R
           const int64_t b = tile / p.nrt;
-          const int32_t r0 = (int32_t)((tile - b * p.nrt) * p.R);
-#pragma unroll
-          for (int a = 0; a < AT; ++a) mf_tma_5d(st + a * 16384u, &p.tm_dy, 0, r0, a, (int32_t)b, full + s);
+          const int32_t r0 = (int32_t)((tile - b * p.nrt) * p.R) - p.shift;
+          for (int a = 0; a < nreg; ++a)
+            mf_tma_5d(st + a * kRegBytes, &p.tm_dy, 0, r0 + (paired ? a : 0), paired ? 0 : a, (int32_t)b, full + s);
           mf_tma_5d(st + kDyBytes, &p.tm_x, 0, r0 + ta, 0, (int32_t)b, full + s);
         } else {
           const int64_t b = tile / tpr;
@@ -196,7 +204,7 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
     // ------------------------------------------------------------ MMA issuer
     // one MMA per K-step covers every tap: B's MN atom j is the x tile j K rows further down, i.e. an
     // atom stride (LBO) of one 128-B row (tools/ubench/tc_lbo_probe.cu), N = 64 k
-    const uint32_t idesc = mf_idesc(COUT, NC);
+    const uint32_t idesc = mf_idesc(m128 ? 128 : 64, NC);
     const uint32_t s0 = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
     int it = 0, d = 0;
     uint32_t dph = 0;
@@ -208,8 +216,8 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
       const uint32_t dyT = s0 + (uint32_t)s * kStage, xT = dyT + kDyBytes;
       const uint32_t dcol = tmem + (uint32_t)(d * NC);
 #pragma unroll 1
-      for (int ks = 0; ks < kMfTileP / 16; ++ks) {
-        mf_mma(dcol, mf_desc(dyT + 2048u * ks, 16384u), mf_desc(xT + 128u * (16 * ks), 128u), idesc, ks > 0 ? 1u : 0u);
+      for (int ks = 0; ks < p.ks; ++ks) {
+        mf_mma(dcol, mf_desc(dyT + 2048u * ks, p.alo), mf_desc(xT + 128u * (16 * ks), 128u), idesc, ks > 0 ? 1u : 0u);
       }
       mf_commit(empty + s);
       mf_commit(dfull + d);
@@ -218,15 +226,16 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
   } else {
     // ------------------------------------------------------------ epilogue: tile -> fp32 run -> fp64 slice
     const int q = warp & 3, hh = (warp - 2) >> 2;  // lane quarter; half of the columns (two warps per quarter)
-    const int co = COUT == 128 ? 32 * q + lane : 16 * q + lane;  // M = 64: lanes 0-15 of each quarter
+    const int co = m128 ? 32 * q + lane : 16 * q + lane;  // accumulator row (M = 64: lanes 0-15 of a quarter)
     const int cb = hh * NH;
     const uint32_t lanebits = (uint32_t)(32 * q) << 16;
-    // this CTA's fp64 slice [NC][COUT] (row co fastest: a warp's 16 / 32 rows are contiguous, so a run
-    // flushes straight from registers, coalesced); each thread owns (co, [cb, cb + NH))
-    double* W = p.ws + (size_t)blockIdx.x * COUT * NC + (size_t)cb * COUT + co;
-    const bool owner = COUT == 128 || lane < 16;  // M = 64: lanes 0-15 of each quarter are the rows
+    // this CTA's fp64 slice [NC][mr] (row fastest: a warp's 16 / 32 rows are contiguous, so a run
+    // flushes straight from registers, coalesced); each thread owns (row co, [cb, cb + NH))
+    constexpr int MR = 128;  // slice rows (M = 64 accumulators fill rows 0-63)
+    double* W = p.ws + (size_t)blockIdx.x * MR * NC + (size_t)cb * MR + co;
+    const bool owner = m128 || lane < 16;
     if (owner && t0 >= ntiles)  // no tiles: the slice is zero
-      for (int i = 0; i < NH; ++i) W[(size_t)i * COUT] = 0.0;
+      for (int i = 0; i < NH; ++i) W[(size_t)i * MR] = 0.0;
     bool first = true;  // the first run is stored, later runs are added (fire-and-forget reductions)
     // the fp32 run lives in registers: row co, columns [cb, cb + NH) (tcgen05.ld 32x32b: lane = row)
     float acc[NH];
@@ -255,10 +264,10 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
           // a fixed order (per-location coherence): deterministic; a reduction needs no round trip
           if (first) {
 #pragma unroll
-            for (int i = 0; i < NH; ++i) W[(size_t)i * COUT] = (double)acc[i];
+            for (int i = 0; i < NH; ++i) W[(size_t)i * MR] = (double)acc[i];
           } else {
 #pragma unroll
-            for (int i = 0; i < NH; ++i) atomicAdd(W + (size_t)i * COUT, (double)acc[i]);
+            for (int i = 0; i < NH; ++i) atomicAdd(W + (size_t)i * MR, (double)acc[i]);
           }
 #pragma unroll
           for (int i = 0; i < NH; ++i) acc[i] = 0.0f;
@@ -274,21 +283,25 @@ __global__ void __launch_bounds__(kMfThreads, 1) mc_filter_grad_tc_kernel(const 
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-// dw[co][ci][a][e] = sum over the CTA slices c = a, a + kh, ... of ws[c][64 e + ci][co] (1-D: kh = 1,
-// e = j).  Block (column 64 e + ci, a), thread (co, g): slices c = a + kh (g + G i) in increasing i (the
-// block's COUT threads read COUT contiguous doubles per slice), then the G partial sums in g order: a
-// fixed order, deterministic.
+// dw[co][ci][a][e] = sum over the slices c of tap row a's group (c = grp, grp + groups, ...) of
+// ws[c][64 e + ci][m] (1-D: one group, kh = 1, e = j; m = co, or 64 + co for the upper half of a paired
+// group, which holds tap row a = 2 grp).  Block (column 64 e + ci, a), thread (co, g), G = 1024 / cout:
+// slices grp + groups (g + G i) in increasing i (cout threads read cout contiguous doubles per slice),
+// then the G partial sums in g order: a fixed order, deterministic.
 __global__ void __launch_bounds__(1024) mc_filter_grad_finish(const double* __restrict__ ws, int ctas, int cout,
-                                                              int kh, int kw, float* __restrict__ dw) {
+                                                              int kh, int kw, int groups, int pair, int mr,
+                                                              float* __restrict__ dw) {
   __shared__ double part[1024];
   const int G = 1024 / cout, co = threadIdx.x % cout, g = threadIdx.x / cout;
   const int nc = 64 * kw, col = blockIdx.x % nc, a = blockIdx.x / nc;
-  const int per = ctas / kh;  // slices of tap row a
-  const double* __restrict__ src = ws + (size_t)col * cout + co;
-  const size_t cstride = (size_t)nc * cout;
+  const int grp = pair ? a / 2 : a;
+  const int m = (pair && a % 2 == 0 && a + 1 <= kh - 1) ? 64 + co : co;
+  const int per = ctas / groups;  // slices of the group
+  const double* __restrict__ src = ws + (size_t)col * mr + m;
+  const size_t cstride = (size_t)nc * mr;
   double s = 0.0;
 #pragma unroll 4
-  for (int m = g; m < per; m += G) s += src[(size_t)(a + kh * m) * cstride];
+  for (int i = g; i < per; i += G) s += src[(size_t)(grp + groups * i) * cstride];
   part[threadIdx.x] = s;
   __syncthreads();
   if (g == 0) {
@@ -356,23 +369,48 @@ bool mc_filter_grad_tc_supported(int64_t cin, int64_t cout, int64_t k) {
   return cin == 64 && ((cout == 64 && k <= 4) || (cout == 128 && k <= 2)) && k >= 1;
 }
 
-size_t mc_filter_grad_workspace(int64_t cin, int64_t cout, int64_t k, int sms) {
+size_t mc_filter_grad_workspace(int64_t cin, int64_t cout, int64_t k, int sms, bool two_d) {
   if (!mc_filter_grad_tc_supported(cin, cout, k)) return 0;
-  return (size_t)sms * cout * 64 * k * sizeof(double);
+  (void)two_d;
+  return (size_t)sms * 128 * 64 * k * sizeof(double);  // slices [64 k][128]
 }
 
 // 2-D tiling: R = the most dy rows of pitch W that fit 128 positions, balanced over the image's rows
 bool mc_filter_grad_2d_plan(McFgradParams& p) {
   if (!mc_filter_grad_tc_supported(p.cin, p.cout, p.k) || p.W > 128 || p.kh < 1 || p.kh > 64) return false;
-  const int64_t rmax = 128 / p.W, nt = (p.OH + rmax - 1) / rmax;
-  p.R = (int)((p.OH + nt - 1) / nt);
-  p.nrt = (p.OH + p.R - 1) / p.R;
+  // cout = 64 pairs tap rows (a, a - 1) into M = 128 MMAs: ceil(kh / 2) groups; tiles start one row
+  // early so both halves see every dy row once (row -1 and rows past OH are the TMA's zero fill)
+  p.pair = p.cout == 64 && p.kh >= 2;
+  p.shift = p.pair ? 1 : 0;
+  p.groups = p.pair ? (p.kh + 1) / 2 : p.kh;
+  p.mr = 128;
+  p.dyreg = p.pair ? 2 : (int)(p.cout / 64);
+  const int64_t rows = p.OH + p.shift;  // dy rows the tiles cover (from -shift)
+  const int64_t rmax = 128 / p.W, nt = (rows + rmax - 1) / rmax;
+  p.R = (int)((rows + nt - 1) / nt);
+  bool shifted = false;  // paired, R W % 16 == 0: one region of R + 1 rows, the upper half W rows down
+  if (p.pair)
+    for (int64_t r = rmax; r >= 1 && !shifted; --r)
+      if ((r * p.W) % 16 == 0) { p.R = (int)r; shifted = true; }
+  p.nrt = (rows + p.R - 1) / p.R;
   p.dy_rows = (int)(p.R * p.W);
+  p.ks = (p.dy_rows + 15) / 16;  // K-steps: the tile's R W positions (zero rows past them)
+  if (shifted) {
+    p.dyreg = 1;
+    p.dy_fill = (int)((p.R + 1) * p.W);
+    p.dyrow_cap = (p.dy_fill + 7) / 8 * 8;
+    p.alo = (uint32_t)(p.W * 128);
+  } else {
+    p.dy_fill = p.dy_rows;
+    p.dyrow_cap = 128;
+    p.alo = 16384u;
+  }
   p.x_rows = (int)((p.R + 1) * p.W);
-  const int reach = 128 + (int)p.k - 1;
+  const int reach = 16 * p.ks + (int)p.k - 1;
   p.xrows = ((p.x_rows > reach ? p.x_rows : reach) + 7) / 8 * 8;
-  p.tx = (uint32_t)((p.cout / 64) * p.dy_rows * 128 + p.x_rows * 128);
-  return p.xrows <= 256;
+  p.tx_dy = (uint32_t)(p.dy_fill * 128);
+  p.tx_x = (uint32_t)(p.x_rows * 128);
+  return p.xrows <= 256 && p.dyrow_cap <= 256;
 }
 
 cudaError_t launch_mc_filter_grad(McFgradParams& p, bool tc, cudaStream_t stream, int sms) {
@@ -380,12 +418,14 @@ cudaError_t launch_mc_filter_grad(McFgradParams& p, bool tc, cudaStream_t stream
     int ctas = sms;
     if (p.two_d) {  // planned by mc_filter_grad_2d_plan; kh CTA groups
       p.ntiles = p.batch * p.nrt;
-      ctas = sms / p.kh * p.kh;
+      ctas = sms / p.groups * p.groups;
     } else {
       p.tiles_per_row = (p.L + kMfTileP - 1) / kMfTileP;
       p.ntiles = p.batch * p.tiles_per_row;
       p.kh = 1; p.xrows = kMfXRows; p.dy_rows = 128; p.x_rows = kMfXRows;
-      p.tx = (uint32_t)mf_stage_bytes(p.cout, kMfXRows);
+      p.groups = 1; p.pair = 0; p.shift = 0; p.mr = 128; p.dyreg = (int)(p.cout / 64);
+      p.dyrow_cap = 128; p.dy_fill = 128; p.ks = kMfTileP / 16; p.alo = 16384u;
+      p.tx_dy = 16384u; p.tx_x = kMfXRows * 128u;
     }
     const void* kfn = nullptr;
     const int k = (int)p.k;
@@ -395,11 +435,11 @@ cudaError_t launch_mc_filter_grad(McFgradParams& p, bool tc, cudaStream_t stream
                : k == 2 ? reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<64, 2>)
                : k == 3 ? reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<64, 3>)
                         : reinterpret_cast<const void*>(mc_filter_grad_tc_kernel<64, 4>);
-    const size_t stage = mf_stage_bytes(p.cout, p.xrows);
+    const size_t stage = mf_stage_bytes(p.dyreg, p.dyrow_cap, p.xrows);
     p.stages = (int)((kSmemBudget - 1024 - 256) / stage);
     if (p.stages > kMfMaxStages) p.stages = kMfMaxStages;
     const size_t smem = mf_smem(stage, p.stages);
-    if (p.stages < 2 || smem > (size_t)kSmemBudget || ctas < p.kh) return cudaErrorInvalidConfiguration;
+    if (p.stages < 2 || smem > (size_t)kSmemBudget || ctas < p.groups) return cudaErrorInvalidConfiguration;
     cudaError_t e = ensure_smem_attr(kfn);
     if (e != cudaSuccess) return e;
     void* args[] = {&p};
@@ -407,7 +447,7 @@ cudaError_t launch_mc_filter_grad(McFgradParams& p, bool tc, cudaStream_t stream
     note_launch();
     if (e != cudaSuccess) return e;
     mc_filter_grad_finish<<<(unsigned)(64 * p.k * p.kh), 1024, 0, stream>>>(p.ws, ctas, (int)p.cout, p.kh, (int)p.k,
-                                                                         p.dw);
+                                                                         p.groups, p.pair, p.mr, p.dw);
     note_launch();
     return cudaGetLastError();
   }

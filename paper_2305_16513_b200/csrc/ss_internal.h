@@ -299,7 +299,7 @@ bool conv_mc_plan_pad2d(ConvMcParams& p);
 bool encode_mc_map_2d(CUtensorMap* m, const void* x, int64_t batch, int64_t OH, int64_t OW, int64_t c, int box_w,
                       int box_h);
 // Multi-channel conv1d filter gradient (mc_fgrad.cu; reading R25): tensor cores for cin = 64,
-// cout 64 (k <= 4) / 128 (k <= 2), else a direct kernel.  ws: per-CTA fp64 slices [sms][64 k][cout].
+// cout 64 (k <= 4) / 128 (k <= 2), else a direct kernel.  ws: per-CTA fp64 slices [sms][64 k][128].
 struct alignas(64) McFgradParams {
   CUtensorMap tm_dy, tm_x;  // batched maps: dy {64, L, cout/64, batch} box 128 rows, x {64, N, 1, batch} box 136
   const uint16_t* dy;
@@ -313,12 +313,21 @@ struct alignas(64) McFgradParams {
   // the 5-D map {64, OW, OH, atoms, batch}: columns >= OW zero-filled) against x rows r0 + a .. r0 + a + R
   // (box {64, W, R + 1}); CTA c serves tap row a = c % kh.  Staged rows past the boxes are zeroed once.
   int two_d, kh, R, xrows, dy_rows, x_rows;  // xrows: x rows per stage (1-D: 136); rows the boxes fill
-  uint32_t tx;                               // bytes per stage the boxes deliver
+  uint32_t tx_dy, tx_x;                      // bytes one dy region / the x box deliver
   int64_t H, W, OH, OW, nrt;                 // 2-D geometry; row tiles per image
+  // CTA groups (2-D: one per tap row, or per tap-row pair): pair = 1 (cout = 64) runs M = 128 MMAs whose
+  // second dy region is the tile one image row down, accumulating tap rows a (rows 0-63) and a - 1
+  // (rows 64-127) together; tiles then start one row early (shift).  mr: slice rows; dyreg: dy regions
+  int groups, pair, shift, mr, dyreg;
+  // dy staging: regions of dyrow_cap rows (the box fills dy_fill); ks K-steps of 16 positions; alo = the A
+  // operand's M-atom stride (a region, or -- shifted mode, R W % 16 == 0 -- W rows: ONE region of R + 1
+  // dy rows serves both halves of a paired accumulator)
+  int dyrow_cap, dy_fill, ks;
+  uint32_t alo;
 };
 bool mc_filter_grad_tc_supported(int64_t cin, int64_t cout, int64_t k);
 bool mc_filter_grad_2d_plan(McFgradParams& p);  // 2-D tensor-core tiling (sets R, xrows, ...); false: direct
-size_t mc_filter_grad_workspace(int64_t cin, int64_t cout, int64_t k, int sms);
+size_t mc_filter_grad_workspace(int64_t cin, int64_t cout, int64_t k, int sms, bool two_d = false);
 cudaError_t launch_mc_filter_grad(McFgradParams& p, bool tc, cudaStream_t stream, int sms);
 // Staged rows as the TMA boxes round them: multiple of 8, split into <= 256-row boxes of equal size
 inline int mc_round_rows(int rows, int* nbox = nullptr, int* box_rows = nullptr) {
