@@ -271,6 +271,25 @@ def test_backward_matches_torch_autograd_cfg3_slice(ss):
     assert torch.all((df.double() - ft.grad).abs() <= TOL_REL * mag_f + TOL_ABS)
 
 
+STRIP_CASES = [(2, 3, 3), (1, 5, 31), (2, 40, 30), (1, 7, 61), (2, 200, 9), (3, 33, 59), (1, 130, 95), (4, 4, 32)]
+
+
+@pytest.mark.parametrize("P,H,W", STRIP_CASES)
+@pytest.mark.parametrize("ties", [False, True])
+def test_pool2d_max_backward_3x3_strips(ss, ties, P, H, W):
+    """3x3/1 max gradient (the plane kernel): widths around multiples of 30 and 32, narrow and short
+    planes, tall planes, ties (first row-major maximum)."""
+    OH, OW = H - 2, W - 2
+    x = (synth.randint(35, P * H * W, 0, 2).astype(np.float32) if ties else
+         synth.uniform01(35, P * H * W)).reshape(P, H, W)
+    dy = synth.normal(36, P * OH * OW).reshape(P, OH, OW)
+    dx = ss.pool2d_backward(torch.from_numpy(x).cuda(), torch.from_numpy(dy).cuda(), (3, 3), (1, 1), "max")
+    ref, mag = oracle.pool2d_backward(x, dy, H, W, 3, 3, 1, 1, oracle.POOL2D_MAX)
+    got = dx.cpu().numpy()
+    within(got, ref, mag, f"pool2d max bwd strips ties={ties} {(P, H, W)}")
+    np.testing.assert_array_equal(got.astype(np.float64) != 0, ref != 0)
+
+
 @pytest.mark.parametrize("P,H,W,kh,kw,sh,sw", [(3, 16, 16, 2, 2, 2, 2), (2, 112, 112, 2, 2, 2, 2), (2, 10, 36, 2, 2, 2, 2),
                                                 (2, 112, 112, 3, 3, 1, 1), (3, 37, 150, 3, 3, 1, 1),
                                                 (2, 30, 140, 5, 5, 1, 1), (1, 20, 21, 7, 7, 1, 1)])
