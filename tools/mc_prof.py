@@ -1,5 +1,5 @@
 """Launch the multi-channel conv kernels on their bench shapes (for ncu captures):
-    python tools/mc_prof.py [2d|1d9|dx|dw|dx2d|dw2d] [reps]"""
+    python tools/mc_prof.py [2d|1d9|dx|dw|dw128|dx2d|dw2d] [reps]"""
 import os
 import sys
 
@@ -25,6 +25,12 @@ elif which == "dw":
     dw = torch.empty(64, 64, 3, device="cuda")
     wsb = torch.empty(ss.ss_conv1d_mc_backward_filter_workspace(64, 64, 3), dtype=torch.uint8, device="cuda")
     f = lambda: ss.conv1d_mc_backward_filter(g, x, 3, out=dw, workspace=wsb)  # noqa: E731
+elif which == "dw128":
+    g = torch.randn(16, 65535, 128, device="cuda").to(torch.bfloat16)
+    x = torch.randn(16, 65536, 64, device="cuda").to(torch.bfloat16)
+    dw = torch.empty(128, 64, 2, device="cuda")
+    wsb = torch.empty(ss.ss_conv1d_mc_backward_filter_workspace(64, 128, 2), dtype=torch.uint8, device="cuda")
+    f = lambda: ss.conv1d_mc_backward_filter(g, x, 2, out=dw, workspace=wsb)  # noqa: E731
 elif which == "dw2d":
     g = torch.randn(128, 54, 54, 64, device="cuda").to(torch.bfloat16)
     x = torch.randn(128, 56, 56, 64, device="cuda").to(torch.bfloat16)
