@@ -617,11 +617,6 @@ cudaError_t launch_conv_mc(ConvMcParams& p, bool tensor_path, cudaStream_t strea
     p.w_shift = sft;
     p.w_magic = (uint32_t)(((1ull << 32) * ((1ull << sft) - dv)) / dv + 1);
   }
-  static unsigned long long* tbuf = nullptr;
-  if (getenv("SS_MC_TRACE")) {
-    if (!tbuf) cudaMalloc(&tbuf, 2048 * 8);
-    cudaMemsetAsync(tbuf, 0, 2048 * 8, stream);
-  }
   if (tensor_path) {
     if (p.mblk < 1) p.mblk = 1;
     const int64_t tp = 128 * p.mblk;
