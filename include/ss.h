@@ -305,7 +305,9 @@ ss_status_t ss_conv2d_mc_backward_input(const void* dy, const void* w, float* dx
  * and 16-B aligned dy / x run on the tensor cores: a tile is R = floor(128 / W) dy
  * rows staged with pitch W (the 5-D TMA box runs past the row's W-kw+1 outputs and
  * zero-fills) against the x rows the tap row reads, as the 1-D filter gradient
- * below, with the CTAs split over the kh tap rows; numerics as that function
+ * below, with the CTAs split over the kh tap rows (cout = 64: tap rows a, a-1
+ * share one M = 128 accumulator whose second dy atom is one image row down);
+ * numerics as that function
  * (fp32 per 128-position tile and 32-tile run, fp64 across runs and CTAs, a
  * fixed order: deterministic).  Other shapes run a direct kernel (double).
  * Statuses as ss_conv2d_mc; workspace too small -> SS_ERR_BAD_SIZE. */
