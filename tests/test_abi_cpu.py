@@ -98,7 +98,9 @@ def test_pool2d_validation(ss):
 def test_status_strings(ss):
     for code in range(7):
         assert ss.ss_status_string(code).startswith("SS_")
-    assert ss.ss_launch_count() == 0  # nothing was launched on this CPU box
+    import torch
+    if not torch.cuda.is_available():  # nothing was launched on a CPU box (a GPU session may have launched)
+        assert ss.ss_launch_count() == 0
 
 
 def test_product_package_never_imports_oracle():
