@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kMcThreads, 1) conv_mc_kernel(const __grid_con
   constexpr int kAccMax = 4;                          // TMEM accumulators: p.nacc <= 4, nacc * mblk * COUT <= 512
   const int kAcc = p.nacc, MB = p.mblk, TP = 128 * p.mblk;  // tile positions
   extern __shared__ __align__(16) uint8_t mc_raw[];  // aligned to 1024 by hand (slack in conv_mc_smem_bytes)
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(mc_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = mc_raw + ((1024u - (smem_u32(mc_raw) & 1023u)) & 1023u);  // shared-space pointer arithmetic
   const int k = (int)p.k;
   const int kMcStages = p.stages;
   uint8_t* xs = smem;                                  // [stages][AT][rows][128 B]

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
   static_assert(NC % 32 == 0 && NC <= 128, "NC/2 columns per epilogue warp, loaded 16 at a time");
   constexpr int kBlockRows = TcShape<NC>::kBlockRows, ND = TcShape<NC>::kDBufs;
   extern __shared__ __align__(16) uint8_t smem_raw[];  // aligned to 1024 by hand (slack in conv_tc_smem_bytes)
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // shared-space pointer arithmetic
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Rings of tile stages: 4 K-atom blocks of kBlockRows chunks x 128 B.  K-atoms 4 and 5 of
   // chunk m are atoms 0 and 1 of chunk m + 1, i.e. blocks 0 and 1 read one row further down

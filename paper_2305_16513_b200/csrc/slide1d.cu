@@ -472,8 +472,8 @@ slide1d_tma_kernel(const __grid_constant__ Slide1DParams p) {
   constexpr int kTileRows = kWarps * kWarpRows;       // 240 or 480
   constexpr int kStagingBytes = kWarpRows * 128;      // per warp buffer
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + kStageAlign - 1) & ~uintptr_t(kStageAlign - 1));
+  uint8_t* smem = smem_raw + ((kStageAlign - (smem_u32(smem_raw) & (kStageAlign - 1u))) &
+                              (kStageAlign - 1u));  // shared-space pointer arithmetic
   const int S = p.stages;
   const uint32_t stage_bytes = p.stage_bytes;
   uint8_t* staging = smem + (size_t)S * stage_bytes;  // kWarps * kStagingBufs * 2 KB
