@@ -332,7 +332,7 @@ conv2d_df_tile_kernel(const __grid_constant__ Conv2DTileParams p, const float* _
   constexpr int NT = KH * KW;
   constexpr int NL = (kUnit + KW + 3) / 4;  // LDS.128 per x fragment
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);  // shared-space pointer arithmetic
   const int S = p.tile_stages;
   const uint32_t stage = p.tile_bytes + p.raw_bytes;  // x tile, then the dense dy plane
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage);
