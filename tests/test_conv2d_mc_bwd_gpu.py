@@ -196,3 +196,21 @@ def test_conv2d_mc_backward_filter_helper_and_validation(ss):
                                            ws.data_ptr(), need) == ss.SS_ERR_WINDOW_EXCEEDS_INPUT
     assert ss.ss_conv2d_mc_backward_filter(g.data_ptr(), x.data_ptr(), x.data_ptr(), *args, ws.data_ptr(), need) == \
         ss.SS_ERR_OVERLAP
+
+
+def test_conv2d_mc_backward_filter_misaligned_dy_uses_the_direct_kernel(ss):
+    B, H, W, cin, cout, kh, kw = 2, 12, 20, 64, 64, 3, 3
+    OH, OW = H - kh + 1, W - kw + 1
+    gb = oracle.to_bf16_bits(synth.normal(164, B * OH * OW * cout).reshape(B, OH, OW, cout))
+    xb = oracle.to_bf16_bits(synth.normal(165, B * H * W * cin).reshape(B, H, W, cin))
+    n = gb.size
+    gbuf = torch.zeros(n + 8, dtype=torch.bfloat16, device="cuda")
+    gbuf[1:1 + n] = bf16_dev(gb).reshape(-1)  # dy 2-B aligned, not 16-B
+    xd = bf16_dev(xb)
+    need = ss.ss_conv2d_mc_backward_filter_workspace(cin, cout, kh, kw)
+    ws = torch.empty(max(need, 8), dtype=torch.uint8, device="cuda")
+    dw = torch.empty(cout * cin * kh * kw, device="cuda")
+    ss.check(ss.ss_conv2d_mc_backward_filter(gbuf[1:].data_ptr(), xd.data_ptr(), dw.data_ptr(), B, H, W, cin, cout,
+                                             kh, kw, ws.data_ptr(), need))
+    ref, mag = oracle.conv2d_mc_backward_filter(gb, xb, kh, kw)
+    check(dw.cpu().numpy().reshape(cout, cin, kh, kw), ref, mag, "filter grad, dy offset by one element")
