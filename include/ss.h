@@ -339,9 +339,9 @@ ss_status_t ss_conv1d_mc_backward_input(const void* dy, const void* w, float* dx
  * cin = 64 with cout = 64 (k <= 4) or 128 (k <= 2) and 16-B aligned dy / x run on the
  * tensor cores: per tile of 128 positions D[co][(j, ci)] += dy^T . x shifted by j rows
  * (both operands read MN-major straight from the activations), fp32 per tile, fp32 runs
- * of 16 tiles, fp64 beyond; `workspace` (DEVICE, caller-owned, 8-B aligned, >=
+ * of 32 tiles, fp64 beyond; `workspace` (DEVICE, caller-owned, 8-B aligned, >=
  * ss_conv1d_mc_backward_filter_workspace(cin, cout, k) bytes on the current device)
- * holds per-CTA fp64 partials summed in CTA order -- deterministic.  Other shapes run
+ * holds per-CTA fp64 partials summed in a fixed order -- deterministic.  Other shapes run
  * a direct kernel (products and sums in double; the workspace size is then 0 and
  * `workspace` may be NULL).  Tolerance 1e-5 * sum|terms| + 1e-6.  Statuses as
  * ss_conv1d_mc; a short workspace -> SS_ERR_BAD_SIZE. */
