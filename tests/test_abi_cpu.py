@@ -197,3 +197,15 @@ def test_conv1d_mc_validation(ss):
     assert ss.ss_conv1d_mc(X + 1, W, Y, 1, 100, 64, 64, 3) == ss.SS_ERR_BAD_SIZE
     assert ss.ss_conv1d_mc(X, W, X + 64, 1, 100, 64, 64, 3) == ss.SS_ERR_OVERLAP
     assert ss.ss_launch_count() == 0
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    # the product path has no CPU fallback: a package without libss.so refuses to import
+    import shutil
+    import sys
+    pkg = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2305_16513_b200")
+    dst = tmp_path / "paper_2305_16513_b200"
+    shutil.copytree(pkg, dst, ignore=shutil.ignore_patterns("*.so", "csrc", "__pycache__"))
+    r = subprocess.run([sys.executable, "-c", "import paper_2305_16513_b200"], cwd=tmp_path, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode != 0 and "ImportError" in r.stderr
