@@ -805,7 +805,7 @@ ss_status_t ss_conv1d_mc(const void* x, const void* w, float* y, int64_t batch, 
   memset(&p, 0, sizeof p);
   p.x = x; p.w = w; p.y = y; p.batch = batch; p.N = N; p.L = L; p.cin = cin; p.cout = cout; p.k = k;
   for (int64_t j = 0; j < k && j < kMcMaxTaps; ++j) p.tap_off[j] = (int)j;
-  p.mblk = conv_mc_choose_mblk(cin, cout, k, 136);
+  p.mblk = conv_mc_choose_mblk(cin, cout, k, 136, k <= 4);
   p.rows = 128 * p.mblk + 8;  // 128 mblk outputs + k - 1 <= 8 halo positions
   const bool tc = (cin == 64 || cin == 128) && (cout == 64 || cout == 128) && k <= 9 &&
                   (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
@@ -917,7 +917,7 @@ ss_status_t ss_conv2d_mc(const void* x, const void* w, float* y, int64_t batch, 
   if (tc) {
     for (int64_t a = 0; a < kh; ++a)
       for (int64_t e = 0; e < kw; ++e) p.tap_off[a * kw + e] = (int)(a * W + e);
-    p.mblk = conv_mc_choose_mblk(cin, cout, kh * kw, (int)(128 + (kh - 1) * W + kw - 1));
+    p.mblk = conv_mc_choose_mblk(cin, cout, kh * kw, (int)(128 + (kh - 1) * W + kw - 1), true);
     p.rows = (int)(128 * p.mblk + (kh - 1) * W + kw - 1);
     tc = mc_boxes(p) && encode_mc_map(&p.tm_x, x, batch * H * W, cin, p.box_rows);
   }

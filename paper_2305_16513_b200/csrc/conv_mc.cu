@@ -538,12 +538,13 @@ size_t conv_mc_smem_bytes(int64_t cin, int64_t cout, int64_t k, int rows, int st
   return 1024 + stages * stage + (size_t)k * (cin / 64) * cout * 128 + 8 * (2 * stages + 8) + 40 * kMcRing + 16;
 }
 
-int conv_mc_choose_mblk(int64_t cin, int64_t cout, int64_t k, int rows1) {
+int conv_mc_choose_mblk(int64_t cin, int64_t cout, int64_t k, int rows1, bool prefer_one) {
   static const int forced = [] {
     const char* e = getenv("SS_MC_MBLK");
     return e ? atoi(e) : 0;
   }();
   if (forced == 1 || forced == 2) return forced;
+  if (prefer_one) return 1;
   return conv_mc_smem_bytes(cin, cout, k, mc_round_rows(rows1 + 128), kMcStages) <= (size_t)kSmemBudget ? 2 : 1;
 }
 

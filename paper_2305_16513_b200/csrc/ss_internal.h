@@ -339,6 +339,8 @@ inline int mc_round_rows(int rows, int* nbox = nullptr, int* box_rows = nullptr)
 }
 // M-blocks per multi-channel tile: 2 (256 positions per tile, half the per-tile barrier round trips
 // and a smaller halo share) when a 3-stage ring of rows1 + 128 staged positions fits next to the weights
-int conv_mc_choose_mblk(int64_t cin, int64_t cout, int64_t k, int rows1);
+// and the shape does not prefer one M-block (forward passes with k <= 4 and the 2-D forward: measured
+// 2-3% faster with 128-position tiles, the 1-D k = 9 forward and the input gradients with 256)
+int conv_mc_choose_mblk(int64_t cin, int64_t cout, int64_t k, int rows1, bool prefer_one = false);
 
 }  // namespace ss
